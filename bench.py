@@ -1,0 +1,462 @@
+#!/usr/bin/env python
+"""Benchmark driver for the B200 Nested Neumann hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload ...]
+
+Headline (`metric`/`value`): BASELINE config 3 — dense NN inversion, N=32768,
+depth p=2, FP64 TFLOP/s.  A *step* is one nest: R = I − A·X (eps fused in)
+plus p Horner products, i.e. p+1 = 3 dense 32768³ products
+(algorithmic 3·2N³ = 2.11e14 flop).  Inputs are 8.6 GB per matrix (≫ the
+126 MB L2), so no L2 flush is needed between steps.  The same line carries
+the batched massive-MIMO leg (config 1, inversions/s) and the sparse
+factorized leg (config 4, GB/s of algorithmic traffic) under "legs".
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref, built from /root/reference/proj/src) on this host's cores on a
+bounded sample of the same workload and prints the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS = {}
+try:
+    PEAKS = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+except Exception:
+    pass
+HBM_PEAK = PEAKS.get("hbm_gbs", 6650.0)
+# FP64 tensor (DMMA) peak measured on this pool by tools/microbench/fp64_peak.cu
+# (profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json carries no FP64 entry.
+FP64_PEAK_TFLOPS = 37.2
+FP64_PEAK_SOURCE = "measured DMMA.8x8x4 microbenchmark, profiles/r01_fp64_peak.txt"
+
+
+# ------------------------------------------------------------------ helpers
+def cpu_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[3 + i]
+                          and "Not" not in s[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(world, value: float) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(world, value: float) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ dense leg (config 3)
+def dense_inputs(n: int, seed: int):
+    """A = B·B^T/N + I, B ~ N(0,1) (torch Philox on device); B·B^T runs on libnnb's own GEMM."""
+    import torch
+
+    import paper_2212_02406_b200 as nnb
+
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    b = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
+    bt = b.t().contiguous()
+    a = nnb.matmul(b, bt)
+    del b, bt
+    a = nnb._axpby(1.0 / n, a, 0.0, None, 1.0)  # A/N + I on device
+    torch.cuda.synchronize()
+    return a
+
+
+def run_dense(args, world, rank):
+    import torch
+
+    import paper_2212_02406_b200 as nnb
+
+    n, p = args.n, args.p
+    a = dense_inputs(n, seed=2212)
+    x = nnb.x0(a)  # A^T/(|A|_1 |A|_inf) on device
+    torch.cuda.synchronize()
+    flops_step = (p + 1) * 2.0 * n ** 3
+    step = lambda xx: nnb.nn_chain(a, xx, p=p, max_iters=1, final_residual=False)
+    for _ in range(args.warmup):
+        x, rep = step(x)
+    torch.cuda.synchronize()
+    barrier(world)
+    l0 = nnb.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lib_ms = []
+    eps = []
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            x, rep = step(x)
+            lib_ms.append(rep.device_ms)
+            eps.append(rep.history[0][1])
+        e1.record()
+        torch.cuda.synchronize()
+    launches = nnb.kernel_launches() - l0
+    ms = max_over_ranks(world, e0.elapsed_time(e1))
+    barrier(world)
+    ms_step = ms / args.steps
+    value = sum_over_ranks(world, flops_step * args.steps) / (ms * 1e-3) / 1e12
+    # dominant kernel: the fused DMMA GEMM — the chain's device time is (p+1) GEMM launches per step
+    gemm_ms = statistics.mean(lib_ms) / (p + 1)
+    achieved = 2.0 * n ** 3 / (gemm_ms * 1e-3) / 1e12
+    out = dict(value=value, ms_per_step=ms_step, launches=launches, clocks=clk.summary(),
+               eps_first=eps[0], eps_last=eps[-1],
+               roofline={"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": None,
+                         "kernel": "gemm_f64_kernel<128x128x16, 2x4 warps, 4 stages> (DMMA.8x8x4 + TMA)",
+                         "per_launch": f"2N^3 = {2.0 * n ** 3:.4g} flop, N={n}",
+                         "peak_source": FP64_PEAK_SOURCE})
+    # e2e through the C-ABI with HOST buffers (pinned): H2D of A and X, one nest, D2H of X
+    if args.e2e:
+        a_h = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        x_h = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        xo_h = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        a_h.copy_(a)
+        x_h.copy_(x)
+        del a
+        torch.cuda.empty_cache()
+        a_np, x_np, xo_np = a_h.numpy(), x_h.numpy(), xo_h.numpy()
+        nnb.nn_chain(a_np, x_np, p=p, max_iters=1, final_residual=False)  # warm staging path
+        barrier(world)
+        t0 = time.perf_counter()
+        k_e2e = max(1, min(args.steps, 3))
+        for _ in range(k_e2e):
+            xo, _ = nnb.nn_chain(a_np, x_np, p=p, max_iters=1, final_residual=False)
+        t = max_over_ranks(world, time.perf_counter() - t0)
+        out["e2e"] = {"value": round(sum_over_ranks(world, flops_step * k_e2e) / t / 1e12, 3), "unit": "TFLOP/s",
+                      "h2d_bytes_per_step": 2 * 8 * n * n, "d2h_bytes_per_step": 8 * n * n,
+                      "path": "nnb_nn_chain_d with pinned host A, X0, X_out"}
+    return out
+
+
+def cpu_dense_sample(n_sample: int, p: int):
+    """Reference nn_step + residual_epsilon (one nest, p+2 products incl. the residual it
+    spends) on an N=n_sample matrix, all host threads (NN_WORKERS=nproc)."""
+    from oracle import Reference
+
+    from paper_2212_02406_b200 import workloads as W
+
+    cores, _ = cpu_info()
+    os.environ["NN_WORKERS"] = str(cores)
+    ref = Reference()
+    a = W.gram_shifted(n_sample, seed=1, shift=1.0)
+    x0 = W.x0_transpose_norm(a)
+    ref.matmul(a[:64], a[:, :64])  # warm the worker pool
+    _, _, _, secs = ref.chain(a, x0, p, 1)  # residual + (p+1) products + final residual
+    flops = (p + 3) * 2.0 * n_sample ** 3
+    return {"value": round(flops / secs / 1e12, 6), "unit": "TFLOP/s", "cores": cores, "kind": "reference",
+            "sample": f"reference §8(c) loop, 1 nest p={p} + 2 residuals on N={n_sample} "
+                      f"({p + 3} complex<double> products, {secs:.2f} s)"}
+
+
+# ------------------------------------------------------------------ MIMO leg (config 1)
+def run_mimo(args, world, rank):
+    import torch
+
+    import paper_2212_02406_b200 as nnb
+    from paper_2212_02406_b200 import workloads as W
+
+    batch = args.mimo_batch
+    a = W.mimo_gram_device(batch, seed=1 + rank)
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        x, eps = nnb.nn_batched(a, p=2, iters=4)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(args.steps, 5)
+    barrier(world)
+    e0.record()
+    for _ in range(steps):
+        x, eps = nnb.nn_batched(a, p=2, iters=4)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(world, e0.elapsed_time(e1)) / steps
+    inv_s = sum_over_ranks(world, batch) / (ms * 1e-3)
+    flops = batch * 13 * 8.0 * 16 ** 3
+    hbm = batch * 2 * 4096.0  # A in + X out (complex128 16x16)
+    achieved_tf = flops / (ms * 1e-3) / 1e12
+    # NS baseline of the analytically equivalent term count for 4 nests of p=2: 3^4 - 1 = 80
+    for _ in range(2):
+        xs = nnb.ns_batched(a, 80)
+    e0.record()
+    for _ in range(steps):
+        xs = nnb.ns_batched(a, 80)
+    e1.record()
+    torch.cuda.synchronize()
+    ms_ns = e0.elapsed_time(e1) / steps
+    # accuracy: NN vs NS-80 against torch's inverse on 64 sampled systems
+    idx = torch.arange(0, batch, max(1, batch // 64), device="cuda")
+    inv = torch.linalg.inv(a[idx])
+    rel = lambda y: (torch.linalg.norm(y[idx] - inv, dim=(1, 2)) / torch.linalg.norm(inv, dim=(1, 2))).max().item()
+    out = {"metric": "batched inversions/sec (262144 x 16x16 complex128, NN p=2 x4 + eps)",
+           "value": round(inv_s, 1), "unit": "inversions/s", "ms_per_step": round(ms, 4),
+           "roofline": {"bound": "tensor", "achieved": round(achieved_tf, 3), "peak": FP64_PEAK_TFLOPS,
+                        "unit": "TFLOP/s", "frac": round(achieved_tf / FP64_PEAK_TFLOPS, 4),
+                        "hbm_gbs": round(hbm / (ms * 1e-3) / 1e9, 1),
+                        "per_launch": f"{batch} systems x 13 complex 16^3 products x 8*16^3 flop"},
+           "ns80_baseline": {"ms_per_step": round(ms_ns, 4), "inversions_per_s": round(batch / (ms_ns * 1e-3), 1),
+                             "speedup_nn_over_ns": round(ms_ns / ms, 3)},
+           "accuracy": {"nn_max_rel_err": rel(x), "ns80_max_rel_err": rel(xs), "eps_max": eps.max().item()}}
+    if args.e2e:
+        a_h = a.cpu().numpy()
+        x_np = np.empty_like(a_h)
+        nnb.nn_batched(a_h, p=2, iters=4, want_eps=False)
+        t0 = time.perf_counter()
+        for _ in range(3):
+            nnb.nn_batched(a_h, p=2, iters=4, want_eps=False)
+        t = (time.perf_counter() - t0) / 3
+        out["e2e"] = {"value": round(batch / t, 1), "unit": "inversions/s", "h2d_bytes_per_step": batch * 4096,
+                      "d2h_bytes_per_step": batch * 4096, "path": "nnb_nn_batched_z with pageable host A, X"}
+    return out
+
+
+def cpu_mimo_sample(sample: int):
+    from oracle import Reference
+
+    from paper_2212_02406_b200 import workloads as W
+
+    cores, _ = cpu_info()
+    ref = Reference()
+    a = W.mimo_gram_host(sample, seed=1)
+    _, _, secs = ref.batched("nn", a, 2, 4, threads=cores)
+    return {"value": round(sample / secs, 1), "unit": "inversions/s", "cores": cores, "kind": "reference",
+            "sample": f"{sample} systems, reference nn_step x4 (p=2) + residual_epsilon per system, "
+                      f"{cores} std::threads ({secs:.2f} s)"}
+
+
+# ------------------------------------------------------------------ sparse leg (config 4)
+def sparse_bytes(n, nnz):
+    return nnz * (8 + 4) + (n + 1) * 8 + 2 * n * 8
+
+
+def run_sparse(args, world, rank):
+    import torch
+
+    import paper_2212_02406_b200 as nnb
+    from paper_2212_02406_b200 import workloads as W
+
+    grid = args.grid
+    n = grid * grid
+    rp, col, val = W.laplacian_5pt(grid)
+    dev = lambda v: torch.from_numpy(v).cuda()
+    csr = nnb.Csr(dev(rp), dev(col), dev(val), n=n, nnz=col.size)
+    b = dev(W.rhs(n, seed=7))
+    norm = nnb.Normalization(theta=0.2, valid=True)
+    for _ in range(args.warmup):
+        x, _ = nnb.solve_sparse_factorized(csr, b, 63, norm)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(args.steps, 5)
+    barrier(world)
+    e0.record()
+    for _ in range(steps):
+        x, _ = nnb.solve_sparse_factorized(csr, b, 63, norm)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(world, e0.elapsed_time(e1)) / steps
+    alg = 63 * sparse_bytes(n, col.size)  # per-application algorithmic bytes (SURVEY §8(d), int64 row_ptr)
+    gbs = alg / (ms * 1e-3) / 1e9
+    return {"metric": "sparse factorized solve, 4096^2 5-pt Laplacian+I, gamma=63", "value": round(gbs, 1),
+            "unit": "GB/s", "ms_per_step": round(ms, 3),
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": HBM_PEAK, "unit": "GB/s",
+                         "frac": round(gbs / HBM_PEAK, 4), "traffic": None,
+                         "per_launch": "nnz*(8+4) + (N+1)*8 + 2N*8 bytes per application"}}
+
+
+def cpu_sparse_sample(grid: int):
+    from oracle import Reference
+
+    from paper_2212_02406_b200 import workloads as W
+
+    cores, _ = cpu_info()
+    os.environ["NN_WORKERS"] = str(cores)
+    ref = Reference()
+    rp, col, val = W.laplacian_5pt(grid)
+    b = W.rhs(grid * grid, seed=7)
+    _, _, secs = ref.sparse_factorized(rp, col, val, b, 63, 0.2)
+    gbs = 63 * sparse_bytes(grid * grid, col.size) / secs / 1e9
+    return {"value": round(gbs, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
+            "sample": f"reference solve_sparse_factorized gamma=63 on a {grid}^2 grid ({secs:.2f} s)"}
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--p", type=int, default=2)
+    ap.add_argument("--mimo-batch", type=int, default=262144)
+    ap.add_argument("--grid", type=int, default=4096)
+    ap.add_argument("--legs", default="dense,mimo,sparse")
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    args = ap.parse_args()
+    legs = set(args.legs.split(","))
+    world, rank, local = dist_setup() if args.impl == "ours" else (int(os.environ.get("WORLD_SIZE", "1")),
+                                                                   int(os.environ.get("RANK", "0")), 0)
+    cores, model = cpu_info()
+    config = {"workload": f"BASELINE config 3: dense NN inversion N={args.n}, p={args.p}, one nest per step "
+                          f"(A=B·B^T/N+I, X0=A^T/(|A|_1|A|_inf))",
+              "n": args.n, "depth_p": args.p, "products_per_step": args.p + 1,
+              "l2": "inputs (8*N^2 bytes per matrix) exceed the 126 MB L2; no flush",
+              "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+              "host_cpu": f"{cores} x {model}"}
+    base = {"metric": "NN inversion FP64 TFLOP/s", "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded)", "config": config}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        # the reference's own CPU path (oracle/_ref), all host threads, bounded sample per step
+        t0 = time.perf_counter()
+        vals = []
+        for _ in range(args.warmup + args.steps):
+            vals.append(cpu_dense_sample(512, args.p))
+        v = statistics.median(x["value"] for x in vals[args.warmup:]) if args.steps else vals[-1]["value"]
+        cb = dict(vals[-1])
+        cb["value"] = v
+        line = dict(base, impl="reference", value=v, ms_per_step=round((time.perf_counter() - t0) * 1e3 /
+                                                                       max(1, len(vals)), 1),
+                    cpu_baseline=cb, e2e={"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0})
+        print(json.dumps(line))
+        return
+
+    import torch
+
+    import paper_2212_02406_b200 as nnb
+
+    nnb.lib()
+    torch.cuda.set_device(local)
+    line = dict(base)
+    line["legs"] = {}
+    if "dense" in legs:
+        d = run_dense(args, world, rank)
+        line.update(value=round(d["value"], 3), ms_per_step=round(d["ms_per_step"], 2),
+                    roofline=d["roofline"], clocks=d["clocks"], gpu_launches=d["launches"])
+        if "e2e" in d:
+            line["e2e"] = d["e2e"]
+        config["eps_first_last"] = [d["eps_first"], d["eps_last"]]
+    if "mimo" in legs:
+        line["legs"]["mimo"] = run_mimo(args, world, rank)
+    if "sparse" in legs:
+        line["legs"]["sparse"] = run_sparse(args, world, rank)
+    if rank == 0 and args.cpu:
+        line["cpu_baseline"] = cpu_dense_sample(512, args.p)
+        if "mimo" in legs:
+            line["legs"]["mimo"]["cpu_baseline"] = cpu_mimo_sample(16384)
+        if "sparse" in legs:
+            line["legs"]["sparse"]["cpu_baseline"] = cpu_sparse_sample(512)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,172 @@
+/*
+ * nnb.h — C-ABI of the B200-native Nested Neumann hot path (libnnb.so).
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no torch or C++
+ * types.  The reference C++ API (/root/reference/proj/include/nn/*.hpp) is
+ * re-implemented on top of these entry points by the C++ layer in
+ * paper_2212_02406_b200/dropin/ (namespace nn), and the Python mirror in
+ * paper_2212_02406_b200/__init__.py binds them with ctypes.
+ *
+ * Conventions:
+ *  - Matrices are row-major.  `_d` entry points take float64; `_z` entry
+ *    points take complex128 interleaved (re, im), i.e. std::complex<double>.
+ *  - Every matrix/vector pointer may be HOST or DEVICE memory; the library
+ *    detects which (cudaPointerGetAttributes) and stages host data through
+ *    device buffers itself.  Caller memory is never freed or retained.
+ *  - `stream` is a cudaStream_t (NULL = the library's per-thread stream).
+ *    Host outputs are complete when the call returns; device outputs are
+ *    complete in stream order.
+ *  - Return value: NNB_OK or an NNB_ERR_* code; nnb_last_error() gives a
+ *    thread-local message.  There is no CPU fallback: without a CUDA device
+ *    every compute entry point returns NNB_ERR_NODEVICE.
+ *  - Reductions are deterministic (fixed order, no floating-point atomics):
+ *    results are bit-reproducible run to run on a fixed device count.
+ */
+#ifndef NNB_H
+#define NNB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NNB_ABI_VERSION 1
+
+enum nnb_status {
+  NNB_OK = 0,
+  NNB_ERR_SHAPE = 1,        /* nn::ShapeError       proj/include/nn/errors.hpp:15-17 */
+  NNB_ERR_DOMAIN = 2,       /* nn::DomainError      errors.hpp:20-22 */
+  NNB_ERR_DIVERGENCE = 3,   /* nn::DivergenceError  errors.hpp:45-49 (index in result) */
+  NNB_ERR_CONTRACTION = 4,  /* nn::ContractionError errors.hpp:40-42 */
+  NNB_ERR_PLAN = 5,         /* nn::PlanError        errors.hpp:52-54 */
+  NNB_ERR_BUDGET = 6,       /* nn::BudgetError      errors.hpp:57-59 */
+  NNB_ERR_CUDA = 7,
+  NNB_ERR_NCCL = 8,
+  NNB_ERR_OOM = 9,
+  NNB_ERR_NODEVICE = 10
+};
+
+/* Operand order of the nest ("Product order").
+ * NORTHSTAR: R = I - A X,  X' = X (I + R + ... + R^p)  (right-multiply Horner)
+ * REFERENCE: P = I - X A,  X' = (I + P + ... + P^p) X  (proj/src/solver.cpp:93-103) */
+enum nnb_order { NNB_ORDER_NORTHSTAR = 0, NNB_ORDER_REFERENCE = 1 };
+
+/* Initial iterate. */
+enum nnb_x0 {
+  NNB_X0_GIVEN = 0,           /* caller's X0 */
+  NNB_X0_SCALED_IDENTITY = 1, /* x0_scale * I (nn_invert: phi0 = I, proj/src/solver.cpp:138) */
+  NNB_X0_TRANSPOSE_NORM = 2,  /* A^T / (||A||_1 ||A||_inf)   (BASELINE configs 0,2,3) */
+  NNB_X0_JACOBI = 3           /* diag(A)^-1                  (BASELINE config 1) */
+};
+
+typedef struct nnb_chain_config {
+  int32_t depth_p;        /* inception depth p (reference depth_L); 0 = identity map */
+  int32_t max_iters;      /* nest budget (reference max_nests) */
+  double tol;             /* stop when eps < tol; <= 0 runs exactly max_iters nests */
+  int32_t order;          /* enum nnb_order */
+  int32_t x0_kind;        /* enum nnb_x0 */
+  double x0_scale;        /* NNB_X0_SCALED_IDENTITY only */
+  int32_t final_residual; /* 1: eps after the last nest is computed (k(p+1)+1 products) */
+} nnb_chain_config;
+
+typedef struct nnb_chain_result {
+  int32_t iters;      /* nests performed */
+  int32_t fail_iter;  /* 1-based nest whose product went non-finite (NNB_ERR_DIVERGENCE) */
+  int32_t stopped;    /* 0 = tolerance, 1 = max_iters */
+  int32_t products;   /* dense N^3 products executed (incl. residual products) */
+  double last_eps;    /* last recorded eps */
+  double device_ms;   /* device time of the chain (CUDA events, excludes staging) */
+} nnb_chain_result;
+
+/* ---- library ---------------------------------------------------------- */
+int nnb_abi_version(void);
+const char* nnb_last_error(void);
+int nnb_device_count(void);
+/* Launch count of this library's kernels since load (for bench gpu_launches). */
+uint64_t nnb_kernel_launches(void);
+
+/* ---- dense kernels ------------------------------------------------------ */
+/* C = A·B.  Replaces nn::matmul (proj/include/nn/kernels.hpp:20-21,
+ * proj/src/kernels.cpp:137-162).  ld* are leading dimensions in elements. */
+int nnb_gemm_d(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+               int64_t ldc, int64_t m, int64_t k, int64_t n, void* stream);
+int nnb_gemm_z(const double* A, const double* B, double* C, int64_t m, int64_t k, int64_t n,
+               void* stream);
+
+/* out = alpha*A + beta*B + gamma*I (B nullable).  Replaces nn::add / sub /
+ * scale / identity_minus / plus_identity (proj/include/nn/kernels.hpp:26-35). */
+int nnb_axpby_d(double alpha, const double* A, double beta, const double* B, double gamma,
+                double* out, int64_t rows, int64_t cols, void* stream);
+int nnb_axpby_z(const double* alpha2, const double* A, const double* beta2, const double* B,
+                const double* gamma2, double* out, int64_t rows, int64_t cols, void* stream);
+
+/* ||M||_F (proj/include/nn/kernels.hpp:42) and trace (:40). */
+int nnb_frobenius_d(const double* M, int64_t count, double* out, void* stream);
+int nnb_frobenius_z(const double* M, int64_t count, double* out, void* stream);
+int nnb_trace_z(const double* M, int64_t n, double* out2, void* stream);
+
+/* eps = ||I - X·A||_F / sqrt(n).  Replaces nn::residual_epsilon
+ * (proj/include/nn/solver.hpp:55, proj/src/solver.cpp:72-75). */
+int nnb_residual_eps_d(const double* X, const double* A, int64_t n, double* eps, void* stream);
+int nnb_residual_eps_z(const double* X, const double* A, int64_t n, double* eps, void* stream);
+
+/* X0 builders (not in the reference). */
+int nnb_x0_d(const double* A, int64_t n, int32_t x0_kind, double x0_scale, double* X0,
+             void* stream);
+
+/* ---- the Nested Neumann chain ------------------------------------------- */
+/* Runs nests of depth p on A from X0 until eps < tol or max_iters nests,
+ * eps recorded before every nest (and after the last if final_residual):
+ * the loop of nn_invert (proj/src/solver.cpp:138-159) / SURVEY.md §8(c).
+ * eps_hist: host array of max_iters+1 doubles (nullable).
+ * X0 is read only for NNB_X0_GIVEN.  X_out receives the final iterate. */
+int nnb_nn_chain_d(const double* A, int64_t n, const double* X0, const nnb_chain_config* cfg,
+                   double* X_out, double* eps_hist, nnb_chain_result* result, void* stream);
+int nnb_nn_chain_z(const double* A, int64_t n, const double* X0, const nnb_chain_config* cfg,
+                   double* X_out, double* eps_hist, nnb_chain_result* result, void* stream);
+
+/* One nest in reference order on (phi, W~): nn::nn_step
+ * (proj/include/nn/solver.hpp:68-69).  depth 0 copies phi. */
+int nnb_nn_step_d(const double* phi, const double* w, int64_t n, int32_t depth, double* out,
+                  void* stream);
+int nnb_nn_step_z(const double* phi, const double* w, int64_t n, int32_t depth, double* out,
+                  void* stream);
+
+/* Truncated Neumann series sum_{j=0}^{order} P^j phi0, P = I - phi0 W~:
+ * nn::ns_sum (proj/include/nn/solver.hpp:61-62, proj/src/solver.cpp:77-91).
+ * products_out (nullable) receives the reference's product tally. */
+int nnb_ns_sum_d(const double* phi0, const double* w, int64_t n, int64_t order, double* out,
+                 double* products_out, void* stream);
+int nnb_ns_sum_z(const double* phi0, const double* w, int64_t n, int64_t order, double* out,
+                 double* products_out, void* stream);
+
+/* ---- batched small complex systems (massive-MIMO Gram inversion) ------- */
+/* batch independent n×n complex128 systems (n == 16), X0 = diag(A)^-1,
+ * `iters` nests of depth p in reference order (nn_step per system) and the
+ * residual after the last nest in eps_last (nullable, host or device). */
+int nnb_nn_batched_z(const double* A, int64_t batch, int32_t n, int32_t p, int32_t iters,
+                     double* X_out, double* eps_last, void* stream);
+/* Neumann-series baseline of `order` terms from the same X0 (ns_sum). */
+int nnb_ns_batched_z(const double* A, int64_t batch, int32_t n, int32_t order, double* X_out,
+                     void* stream);
+
+/* ---- sparse matrix-free factorized solve -------------------------------- */
+/* Y = W·X for CSR W (int64 row_ptr, int32 col, float64 values) and an n×k
+ * row-major block X: nn::spmv_block (proj/include/nn/kernels.hpp:91-92). */
+int nnb_spmv_block_d(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n,
+                     int64_t nnz, const double* X, int64_t k, double* Y, void* stream);
+/* x = theta * prod_{f<s} (I + P^{2^f}) b with P = I - theta W, gamma = 2^s - 1
+ * sparse applications per column: nn::solve_sparse_factorized
+ * (proj/include/nn/factorized.hpp:74-76, proj/src/factorized.cpp:101-140).
+ * spmv_count_out (nullable) = gamma*k; fail_factor_out gets the 0-based
+ * factor index on NNB_ERR_DIVERGENCE. */
+int nnb_sparse_factorized_d(const int64_t* row_ptr, const int32_t* col, const double* val,
+                            int64_t n, int64_t nnz, const double* B, int64_t k, int64_t gamma,
+                            double theta, double* X_out, int64_t* spmv_count_out,
+                            int32_t* fail_factor_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NNB_H */

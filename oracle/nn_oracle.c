@@ -1,0 +1,334 @@
+/* ORACLE — test infrastructure only.  See nn_oracle.h.
+ *
+ * Each function restates one reference routine; the file:line it follows is
+ * cited beside it.  Complex arithmetic is written out by hand as the
+ * reference's std::complex<double> evaluates it for finite operands:
+ *   (a*b).re = a.re*b.re - a.im*b.im,  (a*b).im = a.re*b.im + a.im*b.re,
+ * compiled with -ffp-contract=off so no FMA changes the rounding (the
+ * reference's Release build targets baseline x86-64, which has no FMA).
+ */
+#include "nn_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct { double re, im; } cplx;
+
+static int g_threads = 1;
+void nno_set_threads(int threads) { g_threads = threads < 1 ? 1 : threads; }
+
+static int all_finite(const double* p, int64_t count2) {
+  for (int64_t i = 0; i < count2; ++i)
+    if (!isfinite(p[i])) return 0;
+  return 1;
+}
+
+/* ---- matmul: proj/src/kernels.cpp:137-162 (ascending-k inner sum, row
+ * partition that never changes an element's reduction order, :19-40). ---- */
+typedef struct {
+  const cplx *a, *b;
+  cplx* c;
+  int64_t k, n, lo, hi;
+} mm_job;
+
+static void* mm_rows(void* arg) {
+  const mm_job* j = (const mm_job*)arg;
+  for (int64_t i = j->lo; i < j->hi; ++i) {
+    const cplx* arow = j->a + i * j->k;
+    for (int64_t col = 0; col < j->n; ++col) {
+      double sre = 0.0, sim = 0.0;
+      for (int64_t kk = 0; kk < j->k; ++kk) {
+        const cplx x = arow[kk], y = j->b[kk * j->n + col];
+        const double pre = x.re * y.re - x.im * y.im;
+        const double pim = x.re * y.im + x.im * y.re;
+        sre += pre;
+        sim += pim;
+      }
+      j->c[i * j->n + col].re = sre;
+      j->c[i * j->n + col].im = sim;
+    }
+  }
+  return NULL;
+}
+
+int nno_matmul_z(const double* a, const double* b, int64_t m, int64_t k, int64_t n, double* c) {
+  int workers = g_threads;
+  if (workers <= 1 || m < 64) {
+    mm_job j = {(const cplx*)a, (const cplx*)b, (cplx*)c, k, n, 0, m};
+    mm_rows(&j);
+  } else {
+    if (workers > m) workers = (int)m;
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * workers);
+    mm_job* jobs = (mm_job*)malloc(sizeof(mm_job) * workers);
+    const int64_t chunk = (m + workers - 1) / workers;
+    int started = 0;
+    for (int w = 0; w < workers; ++w) {
+      const int64_t lo = w * chunk, hi = lo + chunk < m ? lo + chunk : m;
+      if (lo >= hi) break;
+      jobs[w] = (mm_job){(const cplx*)a, (const cplx*)b, (cplx*)c, k, n, lo, hi};
+      pthread_create(&th[w], NULL, mm_rows, &jobs[w]);
+      ++started;
+    }
+    for (int w = 0; w < started; ++w) pthread_join(th[w], NULL);
+    free(th);
+    free(jobs);
+  }
+  return all_finite(c, 2 * m * n) ? 0 : 2; /* check_finite, kernels.cpp:14-17 */
+}
+
+/* frobenius_norm: proj/src/kernels.cpp:238-242 (serial sum of std::norm). */
+double nno_frobenius_z(const double* m, int64_t count) {
+  double s = 0.0;
+  for (int64_t i = 0; i < count; ++i) s += m[2 * i] * m[2 * i] + m[2 * i + 1] * m[2 * i + 1];
+  return sqrt(s);
+}
+
+/* identity_minus: proj/src/kernels.cpp:203-212 (in place). */
+static void identity_minus_inplace(cplx* m, int64_t n) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      cplx* v = &m[i * n + j];
+      v->re = (i == j ? 1.0 : 0.0) - v->re;
+      v->im = 0.0 - v->im;
+    }
+}
+
+/* plus_identity: proj/src/kernels.cpp:214-221 (in place). */
+static void plus_identity_inplace(cplx* m, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) {
+    m[i * n + i].re += 1.0;
+    m[i * n + i].im += 0.0;
+  }
+}
+
+/* residual_epsilon: proj/src/solver.cpp:72-75. */
+int nno_residual_eps_z(const double* x, const double* a, int64_t n, double* eps) {
+  double* p = (double*)malloc(sizeof(double) * 2 * n * n);
+  int st = nno_matmul_z(x, a, n, n, n, p);
+  if (st == 0) {
+    identity_minus_inplace((cplx*)p, n);
+    *eps = nno_frobenius_z(p, n * n) / sqrt((double)n);
+  }
+  free(p);
+  return st;
+}
+
+/* nn_step: proj/src/solver.cpp:93-103 with horner_power_sum :27-36.
+ * P = I - phi W~; S = I + P; S = I + P S (L-1 times); out = S phi. */
+int nno_nn_step_z(const double* x, const double* a, int64_t n, int64_t depth_l, double* out) {
+  const size_t bytes = sizeof(double) * 2 * n * n;
+  if (depth_l == 0) { memmove(out, x, bytes); return 0; }
+  double* p = (double*)malloc(bytes);
+  double* s = (double*)malloc(bytes);
+  double* t = (double*)malloc(bytes);
+  int st = nno_matmul_z(x, a, n, n, n, p);
+  if (st == 0) {
+    identity_minus_inplace((cplx*)p, n);
+    memcpy(s, p, bytes);
+    plus_identity_inplace((cplx*)s, n);
+    for (int64_t j = 2; j <= depth_l && st == 0; ++j) {
+      st = nno_matmul_z(p, s, n, n, n, t);
+      if (st == 0) {
+        plus_identity_inplace((cplx*)t, n);
+        double* sw = s; s = t; t = sw;
+      }
+    }
+    if (st == 0) st = nno_matmul_z(s, x, n, n, n, t);
+    if (st == 0) memcpy(out, t, bytes);
+  }
+  free(p); free(s); free(t);
+  return st;
+}
+
+static int is_identity(const cplx* m, int64_t n) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      const cplx v = m[i * n + j];
+      if (v.re != (i == j ? 1.0 : 0.0) || v.im != 0.0) return 0;
+    }
+  return 1;
+}
+
+/* ns_sum: proj/src/solver.cpp:77-91.  P = I - phi0 W~ (product skipped when
+ * phi0 == I), t = I + P, t = t P + I (order-1 times), return t phi0. */
+int nno_ns_sum_z(const double* x0, const double* a, int64_t n, int64_t order, double* out) {
+  const size_t bytes = sizeof(double) * 2 * n * n;
+  if (order == 0) { memmove(out, x0, bytes); return 0; }
+  const int identity_start = is_identity((const cplx*)x0, n);
+  double* p = (double*)malloc(bytes);
+  double* t = (double*)malloc(bytes);
+  double* u = (double*)malloc(bytes);
+  int st = 0;
+  if (identity_start) memcpy(p, a, bytes);
+  else st = nno_matmul_z(x0, a, n, n, n, p);
+  if (st == 0) {
+    identity_minus_inplace((cplx*)p, n);
+    memcpy(t, p, bytes);
+    plus_identity_inplace((cplx*)t, n);
+    for (int64_t step = 2; step <= order && st == 0; ++step) {
+      st = nno_matmul_z(t, p, n, n, n, u);
+      if (st == 0) {
+        plus_identity_inplace((cplx*)u, n);
+        double* sw = t; t = u; u = sw;
+      }
+    }
+    if (st == 0) {
+      if (identity_start) memcpy(out, t, bytes);
+      else st = nno_matmul_z(t, x0, n, n, n, out);
+    }
+  }
+  free(p); free(t); free(u);
+  return st;
+}
+
+/* SURVEY §8(c) explicit-X0 driver over residual_epsilon + nn_step, the loop
+ * body of nn_invert (proj/src/solver.cpp:138-159). */
+int nno_chain_z(const double* a, int64_t n, const double* x0, int p, int max_iters, double tol,
+                double* x_out, double* eps_hist, int* iters_out, int* fail_iter) {
+  const size_t bytes = sizeof(double) * 2 * n * n;
+  double* x = (double*)malloc(bytes);
+  memcpy(x, x0, bytes);
+  int it = 0, st = 0;
+  for (;;) {
+    double eps = 0.0;
+    st = nno_residual_eps_z(x, a, n, &eps);
+    if (st) break;
+    if (eps_hist) eps_hist[it] = eps;
+    if (tol > 0.0 && eps < tol) break;
+    if (it >= max_iters) break;
+    st = nno_nn_step_z(x, a, n, p, x);
+    if (st) { st = 3; if (fail_iter) *fail_iter = it + 1; break; }
+    ++it;
+  }
+  if (iters_out) *iters_out = it;
+  memcpy(x_out, x, bytes);
+  free(x);
+  return st;
+}
+
+/* Batched C2 leg: Jacobi X0 = diag(A)^-1 then the chain (mode 0, eps after
+ * the last nest in eps_last) or ns_sum of order `iters` (mode 1). */
+typedef struct {
+  int mode, p, iters, stride, t;
+  const double* a;
+  int64_t batch, n;
+  double *x, *eps;
+  int status;
+} batch_job;
+
+static void* batch_worker(void* arg) {
+  batch_job* j = (batch_job*)arg;
+  const int64_t n = j->n, nn = n * n;
+  double* x0 = (double*)calloc(2 * nn, sizeof(double));
+  double* hist = (double*)malloc(sizeof(double) * (j->iters + 1));
+  for (int64_t s = j->t; s < j->batch; s += j->stride) {
+    const double* a = j->a + 2 * s * nn;
+    memset(x0, 0, sizeof(double) * 2 * nn);
+    for (int64_t i = 0; i < n; ++i) {
+      /* Scalar{1,0} / a(i,i) as libgcc's __divdc3 evaluates it (Smith's
+       * ratio form); for the Hermitian diagonal (im == 0) this is 1/re. */
+      const double c = a[2 * (i * n + i)], d = a[2 * (i * n + i) + 1];
+      double xr, xi;
+      if (fabs(c) >= fabs(d)) {
+        const double r = d / c, den = c + d * r;
+        xr = (1.0 + 0.0 * r) / den;
+        xi = (0.0 - 1.0 * r) / den;
+      } else {
+        const double r = c / d, den = c * r + d;
+        xr = (1.0 * r + 0.0) / den;
+        xi = (0.0 * r - 1.0) / den;
+      }
+      x0[2 * (i * n + i)] = xr;
+      x0[2 * (i * n + i) + 1] = xi;
+    }
+    int st;
+    if (j->mode == 0)
+      st = nno_chain_z(a, n, x0, j->p, j->iters, 0.0, j->x + 2 * s * nn, hist, NULL, NULL);
+    else
+      st = nno_ns_sum_z(x0, a, n, j->iters, j->x + 2 * s * nn);
+    if (st) j->status = st;
+    if (j->mode == 0 && j->eps) j->eps[s] = hist[j->iters];
+  }
+  free(x0);
+  free(hist);
+  return NULL;
+}
+
+int nno_batched_z(int mode, const double* a, int64_t batch, int64_t n, int p, int iters,
+                  double* x_out, double* eps_last, int threads) {
+  const int saved = g_threads;
+  g_threads = 1; /* parallel across systems, serial inside (n < 64 anyway) */
+  if (threads < 1) threads = 1;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * threads);
+  batch_job* jobs = (batch_job*)malloc(sizeof(batch_job) * threads);
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = (batch_job){mode, p, iters, threads, t, a, batch, n, x_out, eps_last, 0};
+    pthread_create(&th[t], NULL, batch_worker, &jobs[t]);
+  }
+  int st = 0;
+  for (int t = 0; t < threads; ++t) {
+    pthread_join(th[t], NULL);
+    if (jobs[t].status) st = jobs[t].status;
+  }
+  free(th);
+  free(jobs);
+  g_threads = saved;
+  return st;
+}
+
+/* spmv_block: proj/src/kernels.cpp:454-471 (real CSR values, complex block). */
+int nno_spmv_block_z(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n,
+                     const double* x, int64_t k, double* out) {
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t c = 0; c < k; ++c) {
+      double sre = 0.0, sim = 0.0;
+      for (int64_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+        const double v = val[e];
+        const double xr = x[2 * (col[e] * k + c)], xi = x[2 * (col[e] * k + c) + 1];
+        const double pre = v * xr - 0.0 * xi;
+        const double pim = v * xi + 0.0 * xr;
+        sre += pre;
+        sim += pim;
+      }
+      out[2 * (r * k + c)] = sre;
+      out[2 * (r * k + c) + 1] = sim;
+    }
+  return all_finite(out, 2 * n * k) ? 0 : 2;
+}
+
+/* solve_sparse_factorized: proj/src/factorized.cpp:101-140 with
+ * fused_axpy_sub :21-30.  Z = B; for n < s: t = Z, 2^n x (t = t - theta W t),
+ * Z = Z + t; return theta Z.  gamma + 1 must be a power of two. */
+int nno_sparse_factorized_z(const int64_t* row_ptr, const int32_t* col, const double* val,
+                            int64_t n, const double* b, int64_t k, int64_t gamma, double theta,
+                            double* x_out, int64_t* spmv_count, int* fail_index) {
+  if (gamma < 1 || ((gamma + 1) & gamma) != 0) return 5; /* PlanError */
+  int s = 0;
+  for (int64_t g = gamma + 1; g > 1; g >>= 1) ++s;
+  const int64_t cnt = 2 * n * k;
+  double* z = (double*)malloc(sizeof(double) * cnt);
+  double* t = (double*)malloc(sizeof(double) * cnt);
+  double* y = (double*)malloc(sizeof(double) * cnt);
+  memcpy(z, b, sizeof(double) * cnt);
+  int64_t reps = 1, applied = 0;
+  int st = 0;
+  for (int f = 0; f < s && st == 0; ++f) {
+    memcpy(t, z, sizeof(double) * cnt);
+    for (int64_t r = 0; r < reps; ++r) {
+      if (nno_spmv_block_z(row_ptr, col, val, n, t, k, y)) { st = 3; break; }
+      applied += k;
+      for (int64_t i = 0; i < cnt; ++i) t[i] = t[i] - theta * y[i];
+      if (!all_finite(t, cnt)) { st = 3; break; }
+    }
+    if (st) { if (fail_index) *fail_index = f; break; }
+    for (int64_t i = 0; i < cnt; ++i) z[i] = z[i] + t[i];
+    reps <<= 1;
+  }
+  if (st == 0)
+    for (int64_t i = 0; i < cnt; ++i) x_out[i] = z[i] * theta;
+  if (spmv_count) *spmv_count = applied;
+  free(z); free(t); free(y);
+  return st;
+}

@@ -1,0 +1,494 @@
+"""B200-native Nested Neumann hot path (arXiv 2212.02406) — Python mirror.
+
+This module binds ``libnnb.so`` (the C-ABI in ``include/nnb.h``) with ctypes
+and mirrors the reference's C++ API (``/root/reference/proj/include/nn``):
+same function names, same argument meaning, same error classes.  Arrays may
+be numpy (host) or CUDA torch tensors (device); ``complex128`` inputs take the
+``_z`` entry points, everything else is float64.  There is no CPU fallback —
+importing works anywhere, but every compute call needs the CUDA library and a
+GPU and raises otherwise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Optional
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB_PATH = HERE / "libnnb.so"
+
+# --------------------------------------------------------------------- errors
+# Mirrors proj/include/nn/errors.hpp:10-71.
+
+
+class Error(RuntimeError):
+    pass
+
+
+class ShapeError(Error):
+    pass
+
+
+class DomainError(Error):
+    pass
+
+
+class DivergenceError(Error):
+    def __init__(self, msg: str, nest_index: int):
+        super().__init__(msg)
+        self.nest_index = nest_index
+
+
+class ContractionError(Error):
+    pass
+
+
+class PlanError(Error):
+    pass
+
+
+class BudgetError(Error):
+    pass
+
+
+class DeviceError(Error):
+    """CUDA / NCCL / OOM / no device (the library has no CPU fallback)."""
+
+
+_STATUS = {1: ShapeError, 2: DomainError, 3: DivergenceError, 4: ContractionError, 5: PlanError,
+           6: BudgetError, 7: DeviceError, 8: DeviceError, 9: DeviceError, 10: DeviceError}
+
+ORDER_NORTHSTAR, ORDER_REFERENCE = 0, 1
+X0_GIVEN, X0_SCALED_IDENTITY, X0_TRANSPOSE_NORM, X0_JACOBI = 0, 1, 2, 3
+
+
+class ChainConfig(C.Structure):
+    _fields_ = [("depth_p", C.c_int32), ("max_iters", C.c_int32), ("tol", C.c_double),
+                ("order", C.c_int32), ("x0_kind", C.c_int32), ("x0_scale", C.c_double),
+                ("final_residual", C.c_int32)]
+
+
+class ChainResult(C.Structure):
+    _fields_ = [("iters", C.c_int32), ("fail_iter", C.c_int32), ("stopped", C.c_int32),
+                ("products", C.c_int32), ("last_eps", C.c_double), ("device_ms", C.c_double)]
+
+
+_dp = C.c_void_p
+_i64 = C.c_int64
+_i32 = C.c_int32
+_SIGS = {
+    "nnb_abi_version": ([], C.c_int),
+    "nnb_last_error": ([], C.c_char_p),
+    "nnb_device_count": ([], C.c_int),
+    "nnb_kernel_launches": ([], C.c_uint64),
+    "nnb_gemm_d": ([_dp, _i64, _dp, _i64, _dp, _i64, _i64, _i64, _i64, _dp], C.c_int),
+    "nnb_gemm_z": ([_dp, _dp, _dp, _i64, _i64, _i64, _dp], C.c_int),
+    "nnb_axpby_d": ([C.c_double, _dp, C.c_double, _dp, C.c_double, _dp, _i64, _i64, _dp], C.c_int),
+    "nnb_axpby_z": ([_dp, _dp, _dp, _dp, _dp, _dp, _i64, _i64, _dp], C.c_int),
+    "nnb_frobenius_d": ([_dp, _i64, _dp, _dp], C.c_int),
+    "nnb_frobenius_z": ([_dp, _i64, _dp, _dp], C.c_int),
+    "nnb_trace_z": ([_dp, _i64, _dp, _dp], C.c_int),
+    "nnb_residual_eps_d": ([_dp, _dp, _i64, _dp, _dp], C.c_int),
+    "nnb_residual_eps_z": ([_dp, _dp, _i64, _dp, _dp], C.c_int),
+    "nnb_x0_d": ([_dp, _i64, _i32, C.c_double, _dp, _dp], C.c_int),
+    "nnb_nn_chain_d": ([_dp, _i64, _dp, C.POINTER(ChainConfig), _dp, _dp, C.POINTER(ChainResult), _dp],
+                       C.c_int),
+    "nnb_nn_chain_z": ([_dp, _i64, _dp, C.POINTER(ChainConfig), _dp, _dp, C.POINTER(ChainResult), _dp],
+                       C.c_int),
+    "nnb_nn_step_d": ([_dp, _dp, _i64, _i32, _dp, _dp], C.c_int),
+    "nnb_nn_step_z": ([_dp, _dp, _i64, _i32, _dp, _dp], C.c_int),
+    "nnb_ns_sum_d": ([_dp, _dp, _i64, _i64, _dp, _dp, _dp], C.c_int),
+    "nnb_ns_sum_z": ([_dp, _dp, _i64, _i64, _dp, _dp, _dp], C.c_int),
+    "nnb_nn_batched_z": ([_dp, _i64, _i32, _i32, _i32, _dp, _dp, _dp], C.c_int),
+    "nnb_ns_batched_z": ([_dp, _i64, _i32, _i32, _dp, _dp], C.c_int),
+    "nnb_spmv_block_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _dp, _dp], C.c_int),
+    "nnb_sparse_factorized_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _i64, C.c_double, _dp, _dp, _dp,
+                                 _dp], C.c_int),
+}
+
+_lib: Optional[C.CDLL] = None
+
+
+def lib() -> C.CDLL:
+    """Load libnnb.so (fails loudly when the CUDA library was not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise DeviceError(f"{LIB_PATH} is missing: build it with `make` (no CPU fallback exists)")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (args, res) in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+def kernel_launches() -> int:
+    return int(lib().nnb_kernel_launches())
+
+
+def _check(status: int, index: int = 0) -> None:
+    if status == 0:
+        return
+    msg = lib().nnb_last_error().decode(errors="replace")
+    cls = _STATUS.get(status, Error)
+    if cls is DivergenceError:
+        raise DivergenceError(msg, index)
+    raise cls(msg)
+
+
+# ---------------------------------------------------------------- array glue
+def _is_torch(a) -> bool:
+    return type(a).__module__.startswith("torch")
+
+
+def _ptr(a) -> int:
+    if a is None:
+        return None
+    if _is_torch(a):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+def _prep(a, complex_: bool):
+    """Contiguous float64/complex128 array, keeping torch CUDA tensors on device."""
+    if _is_torch(a):
+        import torch
+
+        dt = torch.complex128 if complex_ else torch.float64
+        return a.to(dt).contiguous()
+    return np.ascontiguousarray(np.asarray(a), dtype=np.complex128 if complex_ else np.float64)
+
+
+def _is_complex(*arrs) -> bool:
+    for a in arrs:
+        if a is None:
+            continue
+        if _is_torch(a):
+            if a.is_complex():
+                return True
+        elif np.iscomplexobj(a):
+            return True
+    return False
+
+
+def _empty_like(a, shape=None):
+    shape = tuple(a.shape) if shape is None else shape
+    if _is_torch(a):
+        import torch
+
+        return torch.empty(shape, dtype=a.dtype, device=a.device)
+    return np.empty(shape, dtype=a.dtype)
+
+
+def _stream(a) -> Optional[int]:
+    if _is_torch(a) and a.is_cuda:
+        import torch
+
+        return torch.cuda.current_stream(a.device).cuda_stream
+    return None
+
+
+# ------------------------------------------------------------ kernels (L1)
+def matmul(a, b):
+    """nn::matmul (proj/include/nn/kernels.hpp:20-21) on the FP64 DMMA GEMM."""
+    if a.shape[1] != b.shape[0]:
+        raise ShapeError(f"matmul: inner dimensions disagree ({a.shape[1]} vs {b.shape[0]})")
+    z = _is_complex(a, b)
+    a, b = _prep(a, z), _prep(b, z)
+    m, k = a.shape
+    n = b.shape[1]
+    out = _empty_like(a, (m, n))
+    if z:
+        _check(lib().nnb_gemm_z(_ptr(a), _ptr(b), _ptr(out), m, k, n, _stream(a)))
+    else:
+        _check(lib().nnb_gemm_d(_ptr(a), k, _ptr(b), n, _ptr(out), n, m, k, n, _stream(a)))
+    return out
+
+
+def _axpby(alpha, a, beta=0.0, b=None, gamma=0.0):
+    z = _is_complex(a, b) or any(isinstance(v, complex) and v.imag != 0 for v in (alpha, beta, gamma))
+    a = _prep(a, z)
+    b = _prep(b, z) if b is not None else None
+    out = _empty_like(a)
+    rows, cols = a.shape
+    if z:
+        co = lambda v: np.array([complex(v).real, complex(v).imag])
+        al, be, ga = co(alpha), co(beta), co(gamma)
+        _check(lib().nnb_axpby_z(al.ctypes.data, _ptr(a), be.ctypes.data, _ptr(b), ga.ctypes.data, _ptr(out),
+                                 rows, cols, _stream(a)))
+    else:
+        _check(lib().nnb_axpby_d(float(alpha), _ptr(a), float(beta), _ptr(b), float(gamma), _ptr(out), rows, cols,
+                                 _stream(a)))
+    return out
+
+
+def add(a, b):
+    if a.shape != b.shape:
+        raise ShapeError("add: shape mismatch")
+    return _axpby(1.0, a, 1.0, b)
+
+
+def sub(a, b):
+    if a.shape != b.shape:
+        raise ShapeError("sub: shape mismatch")
+    return _axpby(1.0, a, -1.0, b)
+
+
+def scale(m, factor):
+    return _axpby(factor, m)
+
+
+def identity_minus(m):
+    if m.shape[0] != m.shape[1]:
+        raise ShapeError("identity_minus: matrix must be square")
+    return _axpby(-1.0, m, 0.0, None, 1.0)
+
+
+def plus_identity(m):
+    if m.shape[0] != m.shape[1]:
+        raise ShapeError("plus_identity: matrix must be square")
+    return _axpby(1.0, m, 0.0, None, 1.0)
+
+
+def frobenius_norm(m) -> float:
+    z = _is_complex(m)
+    m = _prep(m, z)
+    out = C.c_double()
+    f = lib().nnb_frobenius_z if z else lib().nnb_frobenius_d
+    _check(f(_ptr(m), int(np.prod(m.shape)), C.addressof(out), _stream(m)))
+    return out.value
+
+
+def trace(m) -> complex:
+    if m.shape[0] != m.shape[1]:
+        raise ShapeError("trace: matrix must be square")
+    m = _prep(m, True)
+    out = np.zeros(2)
+    _check(lib().nnb_trace_z(_ptr(m), m.shape[0], out.ctypes.data, _stream(m)))
+    return complex(out[0], out[1])
+
+
+def spmv_block(csr: "Csr", x):
+    """nn::spmv_block (proj/include/nn/kernels.hpp:91-92): Y = W·X, X n×k."""
+    if csr.n != x.shape[0]:
+        raise ShapeError("spmv_block: inner dimensions disagree")
+    x = _prep(x, False)
+    y = _empty_like(x)
+    k = 1 if x.ndim == 1 else x.shape[1]
+    _check(lib().nnb_spmv_block_d(_ptr(csr.row_ptr), _ptr(csr.col), _ptr(csr.val), csr.n, csr.nnz, _ptr(x), k,
+                                  _ptr(y), _stream(x)))
+    return y
+
+
+# ------------------------------------------------------------ solver (L3)
+def residual_epsilon(phi, w_tilde) -> float:
+    """eps = ||I − phi·W~||_F / sqrt(N) (proj/include/nn/solver.hpp:55)."""
+    z = _is_complex(phi, w_tilde)
+    phi, w = _prep(phi, z), _prep(w_tilde, z)
+    out = C.c_double()
+    f = lib().nnb_residual_eps_z if z else lib().nnb_residual_eps_d
+    _check(f(_ptr(phi), _ptr(w), w.shape[0], C.addressof(out), _stream(w)))
+    return out.value
+
+
+def _square_conform(phi, w, who):
+    if w.shape[0] != w.shape[1] or phi.shape != w.shape:
+        raise ShapeError(f"{who}: shapes do not conform")
+
+
+def nn_step(phi, w_tilde, depth_L: int):
+    """One nest, exactly L+1 products (proj/include/nn/solver.hpp:68-69)."""
+    _square_conform(phi, w_tilde, "nn_step")
+    z = _is_complex(phi, w_tilde)
+    phi, w = _prep(phi, z), _prep(w_tilde, z)
+    out = _empty_like(phi)
+    f = lib().nnb_nn_step_z if z else lib().nnb_nn_step_d
+    _check(f(_ptr(phi), _ptr(w), w.shape[0], int(depth_L), _ptr(out), _stream(w)))
+    return out
+
+
+def newton_step(z_, w_tilde):
+    """Z(2I − W~Z) ≡ nn_step(L=1) (proj/include/nn/solver.hpp:72-73)."""
+    return nn_step(z_, w_tilde, 1)
+
+
+def chebyshev_step(z_, w_tilde):
+    """Z[3I − W~Z(3I − W~Z)] ≡ nn_step(L=2) (proj/include/nn/solver.hpp:76-77)."""
+    return nn_step(z_, w_tilde, 2)
+
+
+def ns_sum(phi0, w_tilde, order: int):
+    """Truncated Neumann series (proj/include/nn/solver.hpp:61-62). Returns (sum, products)."""
+    _square_conform(phi0, w_tilde, "ns_sum")
+    z = _is_complex(phi0, w_tilde)
+    phi0, w = _prep(phi0, z), _prep(w_tilde, z)
+    out = _empty_like(phi0)
+    prods = C.c_double()
+    f = lib().nnb_ns_sum_z if z else lib().nnb_ns_sum_d
+    _check(f(_ptr(phi0), _ptr(w), w.shape[0], int(order), _ptr(out), C.addressof(prods), _stream(w)))
+    return out, prods.value
+
+
+def equivalent_ns_order(nests_i: int, depth_L: int) -> int:
+    """(L+1)^(i+1) − 1 (proj/src/solver.cpp:201-205), exact (Python int)."""
+    return (depth_L + 1) ** (nests_i + 1) - 1
+
+
+@dataclass
+class ChainReport:
+    """Result of nn_chain: the reference's ConvergenceReport subset."""
+    history: list
+    iters: int
+    stopped_reason: str
+    products: int
+    device_ms: float
+    fail_iter: int = 0
+    n3_multiplies: float = 0.0
+    n2_ops: int = 0
+
+
+def nn_chain(a, x0=None, *, p: int, max_iters: int, tol: float = 0.0, order: int = ORDER_NORTHSTAR,
+             x0_kind: Optional[int] = None, x0_scale: float = 1.0, final_residual: bool = True):
+    """Nested Neumann chain from X0; returns (X, ChainReport).
+
+    eps is recorded before every nest and after the last one; stops when
+    eps < tol (tol > 0) or after max_iters nests.
+    """
+    n = a.shape[0]
+    if a.shape != (n, n):
+        raise ShapeError("nn chain: matrix must be square")
+    z = _is_complex(a, x0)
+    a = _prep(a, z)
+    if x0_kind is None:
+        x0_kind = X0_GIVEN if x0 is not None else X0_TRANSPOSE_NORM
+    x0p = _prep(x0, z) if x0 is not None else None
+    out = _empty_like(a)
+    hist = np.zeros(max_iters + 1)
+    cfg = ChainConfig(p, max_iters, tol, order, x0_kind, x0_scale, int(final_residual))
+    res = ChainResult()
+    f = lib().nnb_nn_chain_z if z else lib().nnb_nn_chain_d
+    st = f(_ptr(a), n, _ptr(x0p), C.byref(cfg), _ptr(out), hist.ctypes.data, C.byref(res), _stream(a))
+    _check(st, res.fail_iter)
+    recorded = res.iters + (1 if final_residual or res.stopped == 0 else 0)
+    rep = ChainReport(history=[(k, float(hist[k])) for k in range(recorded)], iters=res.iters,
+                      stopped_reason="tolerance" if res.stopped == 0 else "max_nests", products=res.products,
+                      device_ms=res.device_ms, n3_multiplies=float(res.iters * (p + 1)),
+                      n2_ops=res.iters * (p + 1))
+    return out, rep
+
+
+@dataclass
+class Normalization:
+    """proj/include/nn/normalization.hpp:16-22."""
+    theta: float = 0.0
+    kind: str = "trace"
+    k_order: int = 0
+    contraction_norm: float = 0.0
+    valid: bool = False
+
+
+def normalize(w, norm: Normalization):
+    """W~ = theta·W; ContractionError for an invalid normalization (normalization.cpp:94-99)."""
+    if not norm.valid:
+        raise ContractionError("normalize: normalization does not satisfy the contraction condition")
+    return scale(w, norm.theta)
+
+
+def nn_invert(w, norm: Normalization, depth_L: int = 2, max_nests: int = 64, tol: float = 1e-10):
+    """nn::nn_invert (proj/src/solver.cpp:123-174): phi0 = I on W~ = theta·W,
+    nests until eps < tol or the budget runs out; returns (theta·phi, report)."""
+    if w.shape[0] != w.shape[1]:
+        raise ShapeError("nn_invert: matrix must be square")
+    if tol < 1e-15:
+        raise DomainError("SolverConfig: tol below double precision (minimum 1e-15)")
+    if max_nests < 1:
+        raise DomainError("SolverConfig: max_nests must be >= 1")
+    wt = normalize(w, norm)
+    try:
+        phi, rep = nn_chain(wt, None, p=depth_L, max_iters=max_nests, tol=tol, order=ORDER_REFERENCE,
+                            x0_kind=X0_SCALED_IDENTITY, x0_scale=1.0)
+    except DivergenceError as e:
+        raise DivergenceError(f"nn_invert: non-finite iterate at nest {e.nest_index}", e.nest_index) from None
+    rep.n3_multiplies = float(rep.iters * (depth_L + 1))
+    rep.n2_ops = rep.iters * (depth_L + 1)  # captured before the final scale (solver.cpp:161-165)
+    return scale(phi, norm.theta), rep
+
+
+def x0(a, kind: int = X0_TRANSPOSE_NORM, scale_: float = 1.0):
+    """Initial iterate builders (A^T/(||A||_1||A||_inf), diag(A)^-1, s·I)."""
+    a = _prep(a, False)
+    out = _empty_like(a)
+    _check(lib().nnb_x0_d(_ptr(a), a.shape[0], kind, scale_, _ptr(out), _stream(a)))
+    return out
+
+
+# ------------------------------------------------------------ batched (C2)
+def nn_batched(a, p: int = 2, iters: int = 4, want_eps: bool = True):
+    """Batched 16×16 complex NN inversion with Jacobi X0; returns (X, eps_last)."""
+    a = _prep(a, True)
+    b, n = a.shape[0], a.shape[1]
+    out = _empty_like(a)
+    eps = None
+    if want_eps:
+        if _is_torch(a):
+            import torch
+
+            eps = torch.empty(b, dtype=torch.float64, device=a.device)
+        else:
+            eps = np.empty(b)
+    _check(lib().nnb_nn_batched_z(_ptr(a), b, n, p, iters, _ptr(out), _ptr(eps), _stream(a)))
+    return out, eps
+
+
+def ns_batched(a, order: int):
+    """Batched Neumann-series baseline (ns_sum of `order` terms from Jacobi X0)."""
+    a = _prep(a, True)
+    out = _empty_like(a)
+    _check(lib().nnb_ns_batched_z(_ptr(a), a.shape[0], a.shape[1], order, _ptr(out), _stream(a)))
+    return out
+
+
+# ------------------------------------------------------------ sparse (C5)
+@dataclass
+class Csr:
+    """CSR with int64 row_ptr, int32 col, float64 values (host numpy or device torch)."""
+    row_ptr: object
+    col: object
+    val: object
+    n: int
+    nnz: int = field(default=0)
+
+    def __post_init__(self):
+        if not self.nnz:
+            self.nnz = int(self.col.shape[0])
+
+
+def solve_sparse_factorized(csr: Csr, b, gamma: int, norm: Normalization):
+    """nn::solve_sparse_factorized (proj/src/factorized.cpp:101-140). Returns (x, spmv_count)."""
+    if b.shape[0] != csr.n:
+        raise ShapeError("solve_sparse_factorized: B row count does not match W")
+    if not norm.valid:
+        raise ContractionError("solve_sparse_factorized: invalid normalization")
+    b = _prep(b, False)
+    k = 1 if b.ndim == 1 else b.shape[1]
+    out = _empty_like(b)
+    cnt = C.c_int64()
+    ff = C.c_int32(-1)
+    st = lib().nnb_sparse_factorized_d(_ptr(csr.row_ptr), _ptr(csr.col), _ptr(csr.val), csr.n, csr.nnz, _ptr(b), k,
+                                       int(gamma), float(norm.theta), _ptr(out), C.addressof(cnt), C.addressof(ff),
+                                       _stream(b))
+    _check(st, ff.value)
+    return out, cnt.value
+
+
+__all__ = [n for n in dir() if not n.startswith("_")]

@@ -1,0 +1,536 @@
+// extern "C" entry points of libnnb.so (declared in include/nnb.h).
+//
+// Each entry point validates its arguments the way the reference routine it
+// replaces does, stages host operands through device buffers (padded to an
+// even leading dimension so the TMA descriptors and 16-byte epilogue stores
+// are legal), runs the device path, and copies results back.  No entry
+// point computes anything on the host.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "../../include/nnb.h"
+#include "engine.cuh"
+
+using namespace nnb;
+
+namespace {
+
+int64_t pad8(int64_t c) { return (c + 7) / 8 * 8; }
+
+// Device view of a row-major rows×cols FP64 matrix with an even leading
+// dimension and 16B-aligned base: borrows a suitable device pointer, else
+// stages a padded copy.
+struct DMat {
+  double* d = nullptr;
+  int64_t ld = 0, rows = 0, cols = 0;
+  DevBuf own;
+  int alloc(int64_t r, int64_t c, cudaStream_t s) {
+    rows = r;
+    cols = c;
+    ld = pad8(c);
+    NNB_TRY(own.alloc(sizeof(double) * std::max<int64_t>(1, r * ld), s));
+    d = own.as<double>();
+    return 0;
+  }
+  int load(const double* src, int64_t r, int64_t c, int64_t ld_src, cudaStream_t s,
+           bool allow_borrow = true) {
+    if (allow_borrow && is_device_ptr(src) && !(reinterpret_cast<uintptr_t>(src) & 15) &&
+        !(ld_src & 1)) {
+      d = const_cast<double*>(src);
+      ld = ld_src;
+      rows = r;
+      cols = c;
+      return 0;
+    }
+    NNB_TRY(alloc(r, c, s));
+    if (r * c)
+      NNB_CUDA(cudaMemcpy2DAsync(d, ld * 8, src, ld_src * 8, c * 8, r, cudaMemcpyDefault, s));
+    return 0;
+  }
+  int store(double* dst, int64_t ld_dst, cudaStream_t s) const {
+    if (dst != d && rows * cols)
+      NNB_CUDA(cudaMemcpy2DAsync(dst, ld_dst * 8, d, ld * 8, cols * 8, rows, cudaMemcpyDefault, s));
+    return 0;
+  }
+};
+
+// Planar (re, im) padded device copy of an interleaved complex matrix.
+struct ZMat {
+  DevBuf own;
+  double *re = nullptr, *im = nullptr;
+  int64_t ld = 0, rows = 0, cols = 0;
+  int alloc(int64_t r, int64_t c, cudaStream_t s) {
+    rows = r;
+    cols = c;
+    ld = pad8(c);
+    NNB_TRY(own.alloc(sizeof(double) * std::max<int64_t>(1, 2 * r * ld), s));
+    re = own.as<double>();
+    im = re + r * ld;
+    NNB_CUDA(cudaMemsetAsync(own.p, 0, own.bytes, s));
+    return 0;
+  }
+  int load(const double* z, int64_t r, int64_t c, cudaStream_t s) {
+    NNB_TRY(alloc(r, c, s));
+    In in;
+    NNB_TRY(in.stage(z, (size_t)(2 * r * c), s));
+    return deinterleave2d(in.d, r, c, re, im, ld, s);
+  }
+  int store(double* z, cudaStream_t s) const {
+    Out out;
+    NNB_TRY(out.prepare(z, (size_t)(2 * rows * cols), s));
+    NNB_TRY(interleave2d(re, im, rows, cols, ld, out.d, s));
+    return out.finish(s);
+  }
+};
+
+int sync(cudaStream_t s) {
+  NNB_CUDA(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int chain_cfg(const nnb_chain_config* cfg, ChainCfg* c) {
+  if (!cfg) return fail(NNB_ERR_DOMAIN, "nn chain: config is NULL");
+  if (cfg->depth_p < 0) return fail(NNB_ERR_DOMAIN, "nn chain: depth must be >= 0");
+  if (cfg->max_iters < 0) return fail(NNB_ERR_DOMAIN, "nn chain: max_iters must be >= 0");
+  if (cfg->order != NNB_ORDER_NORTHSTAR && cfg->order != NNB_ORDER_REFERENCE)
+    return fail(NNB_ERR_DOMAIN, "nn chain: unknown operand order");
+  c->p = cfg->depth_p;
+  c->max_iters = cfg->max_iters;
+  c->tol = cfg->tol;
+  c->order = cfg->order;
+  c->final_residual = cfg->final_residual;
+  return 0;
+}
+
+void fill_result(nnb_chain_result* r, const ChainOut& o) {
+  if (!r) return;
+  r->iters = o.iters;
+  r->fail_iter = o.fail_iter;
+  r->stopped = o.stopped;
+  r->products = o.products;
+  r->last_eps = o.last_eps;
+  r->device_ms = o.device_ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+int nnb_abi_version(void) { return NNB_ABI_VERSION; }
+const char* nnb_last_error(void) { return last_error(); }
+int nnb_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+uint64_t nnb_kernel_launches(void) { return launches(); }
+
+// ---------------------------------------------------------------- dense kernels
+int nnb_gemm_d(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+               int64_t m, int64_t k, int64_t n, void* stream) {
+  NNB_TRY(require_device());
+  if (m < 0 || k < 0 || n < 0 || lda < k || ldb < n || ldc < n)
+    return fail(NNB_ERR_SHAPE, "matmul: inner dimensions disagree or bad leading dimension");
+  cudaStream_t s = resolve(stream);
+  DMat a, b, c;
+  NNB_TRY(a.load(A, m, k, lda, s));
+  NNB_TRY(b.load(B, k, n, ldb, s));
+  const bool direct = is_device_ptr(C) && !(reinterpret_cast<uintptr_t>(C) & 15) && !(ldc & 1);
+  if (direct) {
+    c.d = C; c.ld = ldc; c.rows = m; c.cols = n;
+  } else {
+    NNB_TRY(c.alloc(m, n, s));
+  }
+  RedWs red;
+  NNB_TRY(red.init(max_tiles_for(m, n), s));
+  DevBuf nf;
+  NNB_TRY(nf.alloc(sizeof(int), s));
+  GemmOp op;
+  op.A = a.d; op.lda = a.ld; op.B = b.d; op.ldb = b.ld;
+  op.M = m; op.N = n; op.K = k;
+  op.ep.C = c.d; op.ep.ldc = c.ld;
+  op.ep.nf_out = nf.as<int>();
+  NNB_TRY(gemm(op, &red, s));
+  if (!direct) NNB_TRY(c.store(C, ldc, s));
+  int h = 0;
+  NNB_CUDA(cudaMemcpyAsync(&h, nf.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NNB_TRY(sync(s));
+  if (h) return fail(NNB_ERR_DOMAIN, "matmul: produced a non-finite entry");
+  return 0;
+}
+
+int nnb_gemm_z(const double* A, const double* B, double* C, int64_t m, int64_t k, int64_t n,
+               void* stream) {
+  NNB_TRY(require_device());
+  if (m < 0 || k < 0 || n < 0) return fail(NNB_ERR_SHAPE, "matmul: bad shape");
+  cudaStream_t s = resolve(stream);
+  ZMat a, b, c;
+  NNB_TRY(a.load(A, m, k, s));
+  NNB_TRY(b.load(B, k, n, s));
+  NNB_TRY(c.alloc(m, n, s));
+  RedWs red;
+  NNB_TRY(red.init(max_tiles_for(m, n), s));
+  DevBuf nf;
+  NNB_TRY(nf.alloc(2 * sizeof(int), s));
+  auto run = [&](const double* x, int64_t ldx, const double* y, int64_t ldy, double alpha,
+                 const double* d, double* out, int* nfo) {
+    GemmOp op;
+    op.A = x; op.lda = ldx; op.B = y; op.ldb = ldy;
+    op.M = m; op.N = n; op.K = k;
+    op.ep.alpha = alpha; op.ep.D = d; op.ep.ldd = c.ld; op.ep.beta = 1.0;
+    op.ep.C = out; op.ep.ldc = c.ld; op.ep.nf_out = nfo;
+    return gemm(op, nfo ? &red : nullptr, s);
+  };
+  NNB_TRY(run(a.re, a.ld, b.re, b.ld, 1.0, nullptr, c.re, nullptr));
+  NNB_TRY(run(a.im, a.ld, b.im, b.ld, -1.0, c.re, c.re, nf.as<int>()));
+  NNB_TRY(run(a.re, a.ld, b.im, b.ld, 1.0, nullptr, c.im, nullptr));
+  NNB_TRY(run(a.im, a.ld, b.re, b.ld, 1.0, c.im, c.im, nf.as<int>() + 1));
+  NNB_TRY(c.store(C, s));
+  int h[2] = {0, 0};
+  NNB_CUDA(cudaMemcpyAsync(h, nf.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  NNB_TRY(sync(s));
+  if (h[0] || h[1]) return fail(NNB_ERR_DOMAIN, "matmul: produced a non-finite entry");
+  return 0;
+}
+
+int nnb_axpby_d(double alpha, const double* A, double beta, const double* B, double gamma,
+                double* out, int64_t rows, int64_t cols, void* stream) {
+  NNB_TRY(require_device());
+  if (gamma != 0.0 && rows != cols)
+    return fail(NNB_ERR_SHAPE, "identity_minus/plus_identity: matrix must be square");
+  cudaStream_t s = resolve(stream);
+  const size_t cnt = (size_t)(rows * cols);
+  In a, b;
+  NNB_TRY(a.stage(A, cnt, s));
+  if (B) NNB_TRY(b.stage(B, cnt, s));
+  Out o;
+  NNB_TRY(o.prepare(out, cnt, s));
+  NNB_TRY(axpby(alpha, a.d, cols, beta, B ? b.d : nullptr, cols, gamma, 0, o.d, cols, rows, cols, s));
+  NNB_TRY(o.finish(s));
+  return sync(s);
+}
+
+int nnb_axpby_z(const double* alpha2, const double* A, const double* beta2, const double* B,
+                const double* gamma2, double* out, int64_t rows, int64_t cols, void* stream) {
+  NNB_TRY(require_device());
+  const double g0 = gamma2 ? gamma2[0] : 0.0, g1 = gamma2 ? gamma2[1] : 0.0;
+  if ((g0 != 0.0 || g1 != 0.0) && rows != cols)
+    return fail(NNB_ERR_SHAPE, "identity_minus/plus_identity: matrix must be square");
+  cudaStream_t s = resolve(stream);
+  const size_t cnt = (size_t)(2 * rows * cols);
+  In a, b;
+  NNB_TRY(a.stage(A, cnt, s));
+  if (B) NNB_TRY(b.stage(B, cnt, s));
+  Out o;
+  NNB_TRY(o.prepare(out, cnt, s));
+  NNB_TRY(axpby_z(alpha2[0], alpha2[1], a.d, beta2 ? beta2[0] : 0.0, beta2 ? beta2[1] : 0.0,
+                  B ? b.d : nullptr, g0, g1, o.d, rows, cols, s));
+  NNB_TRY(o.finish(s));
+  return sync(s);
+}
+
+static int frob(const double* M, int64_t count, double* out, cudaStream_t s) {
+  In m;
+  NNB_TRY(m.stage(M, (size_t)count, s));
+  DevBuf r;
+  NNB_TRY(r.alloc(sizeof(double), s));
+  NNB_TRY(sumsq(m.d, count, r.as<double>(), s));
+  double h = 0;
+  NNB_CUDA(cudaMemcpyAsync(&h, r.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+  NNB_TRY(sync(s));
+  *out = std::sqrt(h);
+  return 0;
+}
+
+int nnb_frobenius_d(const double* M, int64_t count, double* out, void* stream) {
+  NNB_TRY(require_device());
+  return frob(M, count, out, resolve(stream));
+}
+int nnb_frobenius_z(const double* M, int64_t count, double* out, void* stream) {
+  NNB_TRY(require_device());
+  return frob(M, 2 * count, out, resolve(stream));
+}
+
+int nnb_trace_z(const double* M, int64_t n, double* out2, void* stream) {
+  NNB_TRY(require_device());
+  cudaStream_t s = resolve(stream);
+  In m;
+  NNB_TRY(m.stage(M, (size_t)(2 * n * n), s));
+  DevBuf r;
+  NNB_TRY(r.alloc(2 * sizeof(double), s));
+  NNB_TRY(trace_dev(m.d, n, n, 2, r.as<double>(), s));
+  NNB_CUDA(cudaMemcpyAsync(out2, r.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  return sync(s);
+}
+
+int nnb_x0_d(const double* A, int64_t n, int32_t x0_kind, double x0_scale, double* X0,
+             void* stream) {
+  NNB_TRY(require_device());
+  cudaStream_t s = resolve(stream);
+  DMat a, x;
+  NNB_TRY(a.load(A, n, n, n, s));
+  NNB_TRY(x.alloc(n, n, s));
+  NNB_TRY(x0_build(a.d, a.ld, n, x0_kind, x0_scale, x.d, x.ld, s));
+  NNB_TRY(x.store(X0, n, s));
+  return sync(s);
+}
+
+// ---------------------------------------------------------------- the chain
+int nnb_nn_chain_d(const double* A, int64_t n, const double* X0, const nnb_chain_config* cfg,
+                   double* X_out, double* eps_hist, nnb_chain_result* result, void* stream) {
+  NNB_TRY(require_device());
+  if (n < 1) return fail(NNB_ERR_SHAPE, "nn chain: matrix must be square and non-empty");
+  ChainCfg c;
+  NNB_TRY(chain_cfg(cfg, &c));
+  cudaStream_t s = resolve(stream);
+  DMat a;
+  NNB_TRY(a.load(A, n, n, n, s));
+  DMat x;  // working X with A's leading dimension
+  x.rows = x.cols = n;
+  x.ld = a.ld;
+  NNB_TRY(x.own.alloc(sizeof(double) * n * a.ld, s));
+  x.d = x.own.as<double>();
+  if (cfg->x0_kind == NNB_X0_GIVEN) {
+    if (!X0) return fail(NNB_ERR_DOMAIN, "nn chain: X0 required for NNB_X0_GIVEN");
+    NNB_CUDA(cudaMemcpy2DAsync(x.d, x.ld * 8, X0, n * 8, n * 8, n, cudaMemcpyDefault, s));
+  } else {
+    NNB_TRY(x0_build(a.d, a.ld, n, cfg->x0_kind, cfg->x0_scale, x.d, x.ld, s));
+  }
+  ChainOut o;
+  const int st = chain_real(a.d, n, a.ld, x.d, c, eps_hist, &o, s);
+  fill_result(result, o);
+  if (st != 0 && st != NNB_ERR_DIVERGENCE && st != NNB_ERR_DOMAIN) return st;
+  NNB_TRY(x.store(X_out, n, s));
+  NNB_TRY(sync(s));
+  return st;
+}
+
+int nnb_nn_chain_z(const double* A, int64_t n, const double* X0, const nnb_chain_config* cfg,
+                   double* X_out, double* eps_hist, nnb_chain_result* result, void* stream) {
+  NNB_TRY(require_device());
+  if (n < 1) return fail(NNB_ERR_SHAPE, "nn chain: matrix must be square and non-empty");
+  ChainCfg c;
+  NNB_TRY(chain_cfg(cfg, &c));
+  cudaStream_t s = resolve(stream);
+  ZMat a, x;
+  NNB_TRY(a.load(A, n, n, s));
+  if (cfg->x0_kind == NNB_X0_GIVEN) {
+    if (!X0) return fail(NNB_ERR_DOMAIN, "nn chain: X0 required for NNB_X0_GIVEN");
+    NNB_TRY(x.load(X0, n, n, s));
+  } else if (cfg->x0_kind == NNB_X0_SCALED_IDENTITY) {
+    NNB_TRY(x.alloc(n, n, s));
+    NNB_TRY(fill_identity(x.re, n, x.ld, cfg->x0_scale, s));
+  } else {
+    return fail(NNB_ERR_DOMAIN, "nn chain (complex): X0 must be given or a scaled identity");
+  }
+  ChainOut o;
+  const int st = chain_complex(a.re, a.im, n, a.ld, x.re, x.im, c, eps_hist, &o, s);
+  fill_result(result, o);
+  if (st != 0 && st != NNB_ERR_DIVERGENCE && st != NNB_ERR_DOMAIN) return st;
+  NNB_TRY(x.store(X_out, s));
+  return st;
+}
+
+int nnb_residual_eps_d(const double* X, const double* A, int64_t n, double* eps, void* stream) {
+  nnb_chain_config cfg{0, 0, 0.0, NNB_ORDER_REFERENCE, NNB_X0_GIVEN, 0.0, 1};
+  std::vector<double> scratch((size_t)0);
+  nnb_chain_result r{};
+  double h[1] = {0.0};
+  // X_out must be distinct from the inputs; a residual-only chain leaves X unchanged
+  NNB_TRY(require_device());
+  cudaStream_t s = resolve(stream);
+  DevBuf xo;
+  NNB_TRY(xo.alloc(sizeof(double) * std::max<int64_t>(1, n * n), s));
+  const int st = nnb_nn_chain_d(A, n, X, &cfg, xo.as<double>(), h, &r, stream);
+  if (st == 0) *eps = h[0];
+  return st;
+}
+
+int nnb_residual_eps_z(const double* X, const double* A, int64_t n, double* eps, void* stream) {
+  nnb_chain_config cfg{0, 0, 0.0, NNB_ORDER_REFERENCE, NNB_X0_GIVEN, 0.0, 1};
+  nnb_chain_result r{};
+  double h[1] = {0.0};
+  NNB_TRY(require_device());
+  cudaStream_t s = resolve(stream);
+  DevBuf xo;
+  NNB_TRY(xo.alloc(sizeof(double) * std::max<int64_t>(1, 2 * n * n), s));
+  const int st = nnb_nn_chain_z(A, n, X, &cfg, xo.as<double>(), h, &r, stream);
+  if (st == 0) *eps = h[0];
+  return st;
+}
+
+int nnb_nn_step_d(const double* phi, const double* w, int64_t n, int32_t depth, double* out,
+                  void* stream) {
+  NNB_TRY(require_device());
+  cudaStream_t s = resolve(stream);
+  if (depth == 0) {
+    NNB_CUDA(cudaMemcpyAsync(out, phi, sizeof(double) * n * n, cudaMemcpyDefault, s));
+    return sync(s);
+  }
+  nnb_chain_config cfg{depth, 1, 0.0, NNB_ORDER_REFERENCE, NNB_X0_GIVEN, 0.0, 0};
+  nnb_chain_result r{};
+  const int st = nnb_nn_chain_d(w, n, phi, &cfg, out, nullptr, &r, stream);
+  if (st == NNB_ERR_DIVERGENCE || st == NNB_ERR_DOMAIN)
+    return fail(NNB_ERR_DOMAIN, "nn_step: matmul produced a non-finite entry");
+  return st;
+}
+
+int nnb_nn_step_z(const double* phi, const double* w, int64_t n, int32_t depth, double* out,
+                  void* stream) {
+  NNB_TRY(require_device());
+  cudaStream_t s = resolve(stream);
+  if (depth == 0) {
+    NNB_CUDA(cudaMemcpyAsync(out, phi, sizeof(double) * 2 * n * n, cudaMemcpyDefault, s));
+    return sync(s);
+  }
+  nnb_chain_config cfg{depth, 1, 0.0, NNB_ORDER_REFERENCE, NNB_X0_GIVEN, 0.0, 0};
+  nnb_chain_result r{};
+  const int st = nnb_nn_chain_z(w, n, phi, &cfg, out, nullptr, &r, stream);
+  if (st == NNB_ERR_DIVERGENCE || st == NNB_ERR_DOMAIN)
+    return fail(NNB_ERR_DOMAIN, "nn_step: matmul produced a non-finite entry");
+  return st;
+}
+
+int nnb_ns_sum_d(const double* phi0, const double* w, int64_t n, int64_t order, double* out,
+                 double* products_out, void* stream) {
+  NNB_TRY(require_device());
+  cudaStream_t s = resolve(stream);
+  if (products_out) *products_out = 0;
+  if (order == 0) {
+    NNB_CUDA(cudaMemcpyAsync(out, phi0, sizeof(double) * n * n, cudaMemcpyDefault, s));
+    return sync(s);
+  }
+  DMat p, wm, o;
+  NNB_TRY(p.load(phi0, n, n, n, s, false));
+  NNB_TRY(wm.load(w, n, n, n, s, false));
+  NNB_TRY(o.alloc(n, n, s));
+  bool ident = false;
+  NNB_TRY(is_identity_dev(p.d, nullptr, n, p.ld, &ident, s));
+  NNB_TRY(ns_sum_dev(p.d, nullptr, wm.d, nullptr, n, p.ld, order, ident, o.d, nullptr,
+                     products_out, s));
+  NNB_TRY(o.store(out, n, s));
+  return sync(s);
+}
+
+int nnb_ns_sum_z(const double* phi0, const double* w, int64_t n, int64_t order, double* out,
+                 double* products_out, void* stream) {
+  NNB_TRY(require_device());
+  cudaStream_t s = resolve(stream);
+  if (products_out) *products_out = 0;
+  if (order == 0) {
+    NNB_CUDA(cudaMemcpyAsync(out, phi0, sizeof(double) * 2 * n * n, cudaMemcpyDefault, s));
+    return sync(s);
+  }
+  ZMat p, wm, o;
+  NNB_TRY(p.load(phi0, n, n, s));
+  NNB_TRY(wm.load(w, n, n, s));
+  NNB_TRY(o.alloc(n, n, s));
+  bool ident = false;
+  NNB_TRY(is_identity_dev(p.re, p.im, n, p.ld, &ident, s));
+  NNB_TRY(ns_sum_dev(p.re, p.im, wm.re, wm.im, n, p.ld, order, ident, o.re, o.im, products_out, s));
+  return o.store(out, s);
+}
+
+// ---------------------------------------------------------------- batched
+static int batched(const double* A, int64_t batch, int32_t n, int p, int iters, int ns_order,
+                   double* X_out, double* eps_last, void* stream) {
+  NNB_TRY(require_device());
+  if (n != 16) return fail(NNB_ERR_SHAPE, "batched: only 16x16 systems are supported");
+  if (batch < 0) return fail(NNB_ERR_SHAPE, "batched: negative batch");
+  cudaStream_t s = resolve(stream);
+  const size_t cnt = (size_t)batch * 2 * 256;
+  In a;
+  NNB_TRY(a.stage(A, cnt, s));
+  Out x, e;
+  NNB_TRY(x.prepare(X_out, cnt, s));
+  if (eps_last) NNB_TRY(e.prepare(eps_last, (size_t)batch, s));
+  NNB_TRY(batched_nn_z16(a.d, batch, p, iters, ns_order, x.d, eps_last ? e.d : nullptr, s));
+  NNB_TRY(x.finish(s));
+  if (eps_last) NNB_TRY(e.finish(s));
+  return 0;
+}
+
+int nnb_nn_batched_z(const double* A, int64_t batch, int32_t n, int32_t p, int32_t iters,
+                     double* X_out, double* eps_last, void* stream) {
+  if (p < 1 || p > 4) return fail(NNB_ERR_DOMAIN, "batched: depth p must be in 1..4");
+  if (iters < 0) return fail(NNB_ERR_DOMAIN, "batched: iters must be >= 0");
+  return batched(A, batch, n, p, iters, -1, X_out, eps_last, stream);
+}
+
+int nnb_ns_batched_z(const double* A, int64_t batch, int32_t n, int32_t order, double* X_out,
+                     void* stream) {
+  if (order < 0) return fail(NNB_ERR_DOMAIN, "batched ns: order must be >= 0");
+  return batched(A, batch, n, 1, 0, order, X_out, nullptr, stream);
+}
+
+// ---------------------------------------------------------------- sparse
+static int stage_csr(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n,
+                     int64_t nnz, cudaStream_t s, DevBuf& own, const int64_t** rp,
+                     const int32_t** ci, const double** v) {
+  const bool dev = is_device_ptr(row_ptr) && is_device_ptr(col) && is_device_ptr(val);
+  if (dev) {
+    *rp = row_ptr; *ci = col; *v = val;
+    return 0;
+  }
+  const size_t b_rp = sizeof(int64_t) * (n + 1), b_v = sizeof(double) * nnz,
+               b_c = sizeof(int32_t) * nnz;
+  NNB_TRY(own.alloc(b_rp + b_v + b_c + 64, s));
+  char* base = own.as<char>();
+  NNB_CUDA(cudaMemcpyAsync(base, row_ptr, b_rp, cudaMemcpyDefault, s));
+  NNB_CUDA(cudaMemcpyAsync(base + b_rp, val, b_v, cudaMemcpyDefault, s));
+  NNB_CUDA(cudaMemcpyAsync(base + b_rp + b_v, col, b_c, cudaMemcpyDefault, s));
+  *rp = reinterpret_cast<const int64_t*>(base);
+  *v = reinterpret_cast<const double*>(base + b_rp);
+  *ci = reinterpret_cast<const int32_t*>(base + b_rp + b_v);
+  return 0;
+}
+
+int nnb_spmv_block_d(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n,
+                     int64_t nnz, const double* X, int64_t k, double* Y, void* stream) {
+  NNB_TRY(require_device());
+  cudaStream_t s = resolve(stream);
+  DevBuf csr;
+  const int64_t* rp; const int32_t* ci; const double* v;
+  NNB_TRY(stage_csr(row_ptr, col, val, n, nnz, s, csr, &rp, &ci, &v));
+  In x;
+  NNB_TRY(x.stage(X, (size_t)(n * k), s));
+  Out y;
+  NNB_TRY(y.prepare(Y, (size_t)(n * k), s));
+  NNB_TRY(spmv_csr(rp, ci, v, n, x.d, k, y.d, s));
+  NNB_TRY(y.finish(s));
+  return sync(s);
+}
+
+int nnb_sparse_factorized_d(const int64_t* row_ptr, const int32_t* col, const double* val,
+                            int64_t n, int64_t nnz, const double* B, int64_t k, int64_t gamma,
+                            double theta, double* X_out, int64_t* spmv_count_out,
+                            int32_t* fail_factor_out, void* stream) {
+  NNB_TRY(require_device());
+  // validation order of proj/src/factorized.cpp:104-115
+  if (gamma < 1 || ((gamma + 1) & gamma) != 0)
+    return fail(NNB_ERR_PLAN, "solve_sparse_factorized: order + 1 must be a power of two");
+  if (gamma > (int64_t(1) << 30))
+    return fail(NNB_ERR_BUDGET, "solve_sparse_factorized: order too large to apply");
+  int s_factors = 0;
+  for (int64_t g = gamma + 1; g > 1; g >>= 1) ++s_factors;
+  cudaStream_t s = resolve(stream);
+  DevBuf csr;
+  const int64_t* rp; const int32_t* ci; const double* v;
+  NNB_TRY(stage_csr(row_ptr, col, val, n, nnz, s, csr, &rp, &ci, &v));
+  In b;
+  NNB_TRY(b.stage(B, (size_t)(n * k), s));
+  Out x;
+  NNB_TRY(x.prepare(X_out, (size_t)(n * k), s));
+  int ff = -1;
+  const int st = sparse_factorized(rp, ci, v, n, b.d, k, s_factors, theta, x.d, &ff, s);
+  if (fail_factor_out) *fail_factor_out = ff;
+  if (st) return st;
+  if (spmv_count_out) *spmv_count_out = gamma * k;
+  return x.finish(s);
+}
+
+}  // extern "C"

@@ -1,0 +1,326 @@
+// The Nested Neumann chain on one GPU.
+//
+// Per nest k (NORTHSTAR order; REFERENCE order swaps the operands):
+//   R_k  = I − A·X_k            one GEMM; epilogue also emits eps_k = ‖R_k‖_F/√N
+//   V    = X_k                  and the non-finite count (DivergenceError check)
+//   V    = X_k + V·R_k   (p×)   Horner for X_k·(I + R + … + R^p), epilogue "+X_k"
+//   X_{k+1} = V
+// i.e. exactly p+1 products per nest plus one final residual product —
+// the reference spends p+2 (an untallied residual matmul each nest,
+// /root/reference/proj/src/solver.cpp:141) plus 2p+1 elementwise passes
+// (identity_minus / plus_identity / check_finite, kernels.cpp:203-221).
+// Complex operands run the same schedule on planar re/im buffers, each
+// complex product being four real DMMA GEMMs (4M) whose epilogues carry the
+// ±, "+D", "+γI" and reduction terms.
+#include <cmath>
+#include <vector>
+
+#include "engine.cuh"
+
+namespace nnb {
+
+namespace {
+
+__global__ void combine_eps_kernel(const double* ss2, const int* nf2, double* eps_out,
+                                   int* nf_out, double scale) {
+  if (threadIdx.x == 0) {
+    *eps_out = sqrt(ss2[0] + ss2[1]) * scale;
+    *nf_out = nf2[0] + nf2[1];
+  }
+}
+
+struct Plane {
+  double* re = nullptr;
+  double* im = nullptr;  // null for real
+};
+
+struct Ctx {
+  int64_t n, ld;
+  bool cplx;
+  RedWs red;
+  DevBuf scratch;  // complex combine scalars
+  double* ss2 = nullptr;
+  int* nf2 = nullptr;
+  cudaStream_t s;
+};
+
+// C = alpha·(A·B) + beta·D + gamma·I, with optional Σ|C|² → eps_out and
+// non-finite count → nf_out (device scalars).
+int product(Ctx& c, const Plane& A, const Plane& B, double alpha, const Plane* D, double beta,
+            double gamma, const Plane& C, double* eps_out, int* nf_out) {
+  const double eps_scale = 1.0 / std::sqrt(static_cast<double>(c.n));
+  GemmOp op;
+  op.M = op.N = op.K = c.n;
+  op.lda = op.ldb = c.ld;
+  if (!c.cplx) {
+    op.A = A.re;
+    op.B = B.re;
+    op.ep.alpha = alpha;
+    op.ep.D = D ? D->re : nullptr;
+    op.ep.ldd = c.ld;
+    op.ep.beta = beta;
+    op.ep.gamma = gamma;
+    op.ep.C = C.re;
+    op.ep.ldc = c.ld;
+    op.ep.eps_out = eps_out;
+    op.ep.eps_scale = eps_scale;
+    op.ep.nf_out = nf_out;
+    return gemm(op, nf_out ? &c.red : nullptr, c.s);
+  }
+  const bool red = nf_out != nullptr;
+  // real plane: Cr = alpha Ar·Br + beta Dr + gamma I ; Cr += -alpha Ai·Bi
+  GemmOp o1 = op;
+  o1.A = A.re; o1.B = B.re;
+  o1.ep.alpha = alpha; o1.ep.D = D ? D->re : nullptr; o1.ep.ldd = c.ld; o1.ep.beta = beta;
+  o1.ep.gamma = gamma; o1.ep.C = C.re; o1.ep.ldc = c.ld;
+  NNB_TRY(gemm(o1, nullptr, c.s));
+  GemmOp o2 = op;
+  o2.A = A.im; o2.B = B.im;
+  o2.ep.alpha = -alpha; o2.ep.D = C.re; o2.ep.ldd = c.ld; o2.ep.beta = 1.0;
+  o2.ep.C = C.re; o2.ep.ldc = c.ld;
+  if (red) { o2.ep.ss_out = c.ss2; o2.ep.nf_out = c.nf2; }
+  NNB_TRY(gemm(o2, red ? &c.red : nullptr, c.s));
+  // imaginary plane: Ci = alpha Ar·Bi + beta Di ; Ci += alpha Ai·Br
+  GemmOp o3 = op;
+  o3.A = A.re; o3.B = B.im;
+  o3.ep.alpha = alpha; o3.ep.D = D ? D->im : nullptr; o3.ep.ldd = c.ld; o3.ep.beta = beta;
+  o3.ep.C = C.im; o3.ep.ldc = c.ld;
+  NNB_TRY(gemm(o3, nullptr, c.s));
+  GemmOp o4 = op;
+  o4.A = A.im; o4.B = B.re;
+  o4.ep.alpha = alpha; o4.ep.D = C.im; o4.ep.ldd = c.ld; o4.ep.beta = 1.0;
+  o4.ep.C = C.im; o4.ep.ldc = c.ld;
+  if (red) { o4.ep.ss_out = c.ss2 + 1; o4.ep.nf_out = c.nf2 + 1; }
+  NNB_TRY(gemm(o4, red ? &c.red : nullptr, c.s));
+  if (red) {
+    combine_eps_kernel<<<1, 32, 0, c.s>>>(c.ss2, c.nf2, eps_out ? eps_out : c.ss2 + 2, nf_out,
+                                          eps_scale);
+    count_launch();
+    NNB_CUDA(cudaGetLastError());
+  }
+  return 0;
+}
+
+int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_hist,
+              ChainOut* out) {
+  const int64_t n = c.n, mat = n * c.ld;
+  const int planes = c.cplx ? 2 : 1;
+  const int p = cfg.p;
+  const int slots = cfg.max_iters + 1;
+
+  NNB_TRY(c.red.init(max_tiles_for(n, n), c.s));
+  DevBuf work;
+  NNB_TRY(work.alloc(sizeof(double) * (size_t)mat * planes * 3, c.s));
+  DevBuf scal;
+  const size_t nf_count = (size_t)slots * (p + 1);
+  NNB_TRY(scal.alloc(sizeof(double) * (slots + 8) + sizeof(int) * (nf_count + 8), c.s));
+  double* eps_dev = scal.as<double>();
+  c.ss2 = eps_dev + slots;
+  int* nf_dev = reinterpret_cast<int*>(c.ss2 + 8);
+  c.nf2 = nf_dev + nf_count;
+  NNB_CUDA(cudaMemsetAsync(scal.p, 0, scal.bytes, c.s));
+
+  auto plane_at = [&](int i) {
+    Plane pl;
+    double* base = work.as<double>() + (size_t)i * mat * planes;
+    pl.re = base;
+    pl.im = c.cplx ? base + mat : nullptr;
+    return pl;
+  };
+  const Plane caller_x = X;
+  Plane R = plane_at(0);
+  Plane bufs[3] = {X, plane_at(1), plane_at(2)};
+  int xi = 0;
+
+  cudaEvent_t e0, e1;
+  NNB_CUDA(cudaEventCreate(&e0));
+  NNB_CUDA(cudaEventCreate(&e1));
+  NNB_CUDA(cudaEventRecord(e0, c.s));
+
+  const bool tol_mode = cfg.tol > 0.0;
+  std::vector<double> eps_h(slots, 0.0);
+  std::vector<int> nf_h(nf_count, 0);
+  int k = 0, products = 0, stopped = 1, recorded = 0;
+  for (;; ++k) {
+    const bool last = (k >= cfg.max_iters);
+    if (last && !cfg.final_residual) break;
+    const Plane& Xk = bufs[xi];
+    const Plane& lhs = cfg.order == 0 ? A : Xk;
+    const Plane& rhs = cfg.order == 0 ? Xk : A;
+    NNB_TRY(product(c, lhs, rhs, -1.0, nullptr, 0.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1)));
+    ++products;
+    recorded = k + 1;
+    if (tol_mode) {
+      NNB_CUDA(cudaMemcpyAsync(eps_h.data(), eps_dev, sizeof(double) * slots,
+                               cudaMemcpyDeviceToHost, c.s));
+      NNB_CUDA(cudaMemcpyAsync(nf_h.data(), nf_dev, sizeof(int) * nf_count,
+                               cudaMemcpyDeviceToHost, c.s));
+      NNB_CUDA(cudaStreamSynchronize(c.s));
+      bool bad = false;
+      for (int q = 0; q <= k * (p + 1); ++q) bad |= nf_h[q] != 0;
+      if (bad) break;  // reported below
+      if (eps_h[k] < cfg.tol) {
+        stopped = 0;
+        break;
+      }
+    }
+    if (last) break;
+    if (p > 0) {
+      Plane v = Xk;
+      int vi = xi;
+      int dst_i = (xi + 1) % 3;
+      for (int j = 1; j <= p; ++j) {
+        const Plane& dst = bufs[dst_i];
+        const Plane& l = cfg.order == 0 ? v : R;
+        const Plane& r = cfg.order == 0 ? R : v;
+        NNB_TRY(product(c, l, r, 1.0, &Xk, 1.0, 0.0, dst, nullptr, nf_dev + k * (p + 1) + j));
+        ++products;
+        v = dst;
+        vi = dst_i;
+        // next destination: the buffer that is neither X_k nor the current V
+        dst_i = 3 - xi - vi;
+      }
+      xi = vi;
+    }
+  }
+  NNB_CUDA(cudaEventRecord(e1, c.s));
+  // copy the final iterate into the caller's X buffer if it lives elsewhere
+  if (bufs[xi].re != caller_x.re) {
+    NNB_TRY(copy2d(bufs[xi].re, c.ld, caller_x.re, c.ld, n, n, c.s));
+    if (c.cplx) NNB_TRY(copy2d(bufs[xi].im, c.ld, caller_x.im, c.ld, n, n, c.s));
+  }
+  NNB_CUDA(cudaMemcpyAsync(eps_h.data(), eps_dev, sizeof(double) * slots, cudaMemcpyDeviceToHost,
+                           c.s));
+  NNB_CUDA(cudaMemcpyAsync(nf_h.data(), nf_dev, sizeof(int) * nf_count, cudaMemcpyDeviceToHost,
+                           c.s));
+  NNB_CUDA(cudaStreamSynchronize(c.s));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+
+  if (eps_hist)
+    for (int q = 0; q < recorded && q < slots; ++q) eps_hist[q] = eps_h[q];
+  out->iters = std::min(k, cfg.max_iters);
+  out->products = products;
+  out->stopped = stopped;
+  out->last_eps = recorded > 0 ? eps_h[recorded - 1] : 0.0;
+  out->device_ms = ms;
+  out->fail_iter = 0;
+  for (int kk = 0; kk <= out->iters && kk < slots; ++kk) {
+    for (int j = 0; j <= p; ++j) {
+      if (nf_h[kk * (p + 1) + j] == 0) continue;
+      if (j == 0) return fail(2, "nn chain: residual product went non-finite at nest " + std::to_string(kk));
+      out->fail_iter = kk + 1;
+      return fail(3, "nn chain: non-finite iterate at nest " + std::to_string(kk + 1));
+    }
+  }
+  return 0;
+}
+
+// ns_sum (proj/src/solver.cpp:77-91) on device planes:
+//   P = I − (identity_start ? W : phi0·W);  T = I + P;  T = T·P + I (order−1×);
+//   out = identity_start ? T : T·phi0.
+int run_ns_sum(Ctx& c, const Plane& phi0, const Plane& W, int64_t order, bool identity_start,
+               Plane out, double* products) {
+  const int64_t n = c.n, mat = n * c.ld;
+  const int planes = c.cplx ? 2 : 1;
+  NNB_TRY(c.red.init(max_tiles_for(n, n), c.s));
+  DevBuf work;
+  NNB_TRY(work.alloc(sizeof(double) * (size_t)mat * planes * 3, c.s));
+  DevBuf scal;
+  const int64_t nf_slots = order + 4;
+  NNB_TRY(scal.alloc(sizeof(double) * 16 + sizeof(int) * (nf_slots + 8), c.s));
+  c.ss2 = scal.as<double>();
+  int* nf_dev = reinterpret_cast<int*>(c.ss2 + 16);
+  c.nf2 = nf_dev + nf_slots;
+  NNB_CUDA(cudaMemsetAsync(scal.p, 0, scal.bytes, c.s));
+  auto plane_at = [&](int i) {
+    double* base = work.as<double>() + (size_t)i * mat * planes;
+    return Plane{base, c.cplx ? base + mat : nullptr};
+  };
+  Plane P = plane_at(0), T[2] = {plane_at(1), plane_at(2)};
+  double prods = 0;
+  int slot = 0;
+  auto each_plane = [&](auto&& fn) {
+    int st = fn(P.re, phi0.re, W.re, T[0].re, out.re, 0);
+    if (st == 0 && c.cplx) st = fn(P.im, phi0.im, W.im, T[0].im, out.im, 1);
+    return st;
+  };
+  if (identity_start) {
+    // P = I − W (elementwise, identity_minus)
+    NNB_TRY(each_plane([&](double* p, const double*, const double* w, double*, double*, int pl) {
+      return axpby(-1.0, w, c.ld, 0.0, nullptr, 0, pl == 0 ? 1.0 : 0.0, 0, p, c.ld, n, n, c.s);
+    }));
+  } else {
+    NNB_TRY(product(c, phi0, W, -1.0, nullptr, 0.0, 1.0, P, nullptr, nf_dev + slot++));
+    prods += 1;
+  }
+  // T = I + P
+  NNB_TRY(each_plane([&](double* p, const double*, const double*, double* t, double*, int pl) {
+    return axpby(1.0, p, c.ld, 0.0, nullptr, 0, pl == 0 ? 1.0 : 0.0, 0, t, c.ld, n, n, c.s);
+  }));
+  int ti = 0;
+  for (int64_t step = 2; step <= order; ++step) {
+    NNB_TRY(product(c, T[ti], P, 1.0, nullptr, 0.0, 1.0, T[ti ^ 1], nullptr, nf_dev + std::min<int64_t>(slot, nf_slots - 1)));
+    ++slot;
+    ti ^= 1;
+    prods += 1;
+  }
+  if (identity_start) {
+    NNB_TRY(copy2d(T[ti].re, c.ld, out.re, c.ld, n, n, c.s));
+    if (c.cplx) NNB_TRY(copy2d(T[ti].im, c.ld, out.im, c.ld, n, n, c.s));
+  } else {
+    NNB_TRY(product(c, T[ti], phi0, 1.0, nullptr, 0.0, 0.0, out, nullptr, nf_dev + std::min<int64_t>(slot, nf_slots - 1)));
+    ++slot;
+    prods += 1;
+  }
+  std::vector<int> nf_h(nf_slots);
+  NNB_CUDA(cudaMemcpyAsync(nf_h.data(), nf_dev, sizeof(int) * nf_slots, cudaMemcpyDeviceToHost, c.s));
+  NNB_CUDA(cudaStreamSynchronize(c.s));
+  if (products) *products = prods;
+  for (int v : nf_h)
+    if (v) return fail(2, "ns_sum: matmul produced a non-finite entry");
+  return 0;
+}
+
+}  // namespace
+
+int ns_sum_dev(const double* phi0_re, const double* phi0_im, const double* w_re,
+               const double* w_im, int64_t n, int64_t ldn, int64_t order, bool identity_start,
+               double* out_re, double* out_im, double* products, cudaStream_t s) {
+  Ctx c;
+  c.n = n;
+  c.ld = ldn;
+  c.cplx = w_im != nullptr;
+  c.s = s;
+  Plane phi{const_cast<double*>(phi0_re), const_cast<double*>(phi0_im)};
+  Plane w{const_cast<double*>(w_re), const_cast<double*>(w_im)};
+  Plane o{out_re, out_im};
+  return run_ns_sum(c, phi, w, order, identity_start, o, products);
+}
+
+int chain_real(const double* A, int64_t n, int64_t ldn, double* X, const ChainCfg& cfg,
+               double* eps_hist, ChainOut* out, cudaStream_t s) {
+  Ctx c;
+  c.n = n;
+  c.ld = ldn;
+  c.cplx = false;
+  c.s = s;
+  Plane a{const_cast<double*>(A), nullptr}, x{X, nullptr};
+  return run_chain(c, a, x, cfg, eps_hist, out);
+}
+
+int chain_complex(const double* Ar, const double* Ai, int64_t n, int64_t ldn, double* Xr,
+                  double* Xi, const ChainCfg& cfg, double* eps_hist, ChainOut* out,
+                  cudaStream_t s) {
+  Ctx c;
+  c.n = n;
+  c.ld = ldn;
+  c.cplx = true;
+  c.s = s;
+  Plane a{const_cast<double*>(Ar), const_cast<double*>(Ai)}, x{Xr, Xi};
+  return run_chain(c, a, x, cfg, eps_hist, out);
+}
+
+}  // namespace nnb

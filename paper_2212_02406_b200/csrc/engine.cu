@@ -1,0 +1,587 @@
+// Engine core: error plumbing, host/device staging, TMA descriptors, the
+// GEMM launcher and the small auxiliary kernels (X0 builders, axpby,
+// deterministic reductions).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <mutex>
+
+#include "engine.cuh"
+
+namespace nnb {
+
+// ============================ errors ============================
+static thread_local std::string g_err;
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_err = msg; }
+const char* last_error() { return g_err.c_str(); }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  char buf[512];
+  std::snprintf(buf, sizeof(buf), "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+                cudaGetErrorString(e), what, file, line);
+  g_err = buf;
+  return e == cudaErrorMemoryAllocation ? 9 /*NNB_ERR_OOM*/ : 7 /*NNB_ERR_CUDA*/;
+}
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+uint64_t launches() { return g_launches.load(std::memory_order_relaxed); }
+
+// ============================ staging ============================
+int require_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(10, "no CUDA device: libnnb has no CPU fallback");
+  }
+  return 0;
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static thread_local cudaStream_t g_thread_stream = nullptr;
+cudaStream_t resolve(void* stream) {
+  if (stream) return static_cast<cudaStream_t>(stream);
+  if (!g_thread_stream) cudaStreamCreateWithFlags(&g_thread_stream, cudaStreamNonBlocking);
+  return g_thread_stream;
+}
+
+int DevBuf::alloc(size_t b, cudaStream_t st) {
+  release();
+  s = st;
+  bytes = b;
+  if (b == 0) return 0;
+  NNB_CUDA(cudaMallocAsync(&p, b, st));
+  return 0;
+}
+void DevBuf::release() {
+  if (p) cudaFreeAsync(p, s);
+  p = nullptr;
+  bytes = 0;
+}
+
+int In::stage(const double* src, size_t count, cudaStream_t s) {
+  if (is_device_ptr(src)) {
+    d = src;
+    return 0;
+  }
+  NNB_TRY(own.alloc(count * sizeof(double), s));
+  NNB_CUDA(cudaMemcpyAsync(own.p, src, count * sizeof(double), cudaMemcpyHostToDevice, s));
+  d = own.as<double>();
+  return 0;
+}
+
+int Out::prepare(double* dst, size_t cnt, cudaStream_t s) {
+  count = cnt;
+  if (is_device_ptr(dst)) {
+    d = dst;
+    host = nullptr;
+    return 0;
+  }
+  NNB_TRY(own.alloc(cnt * sizeof(double), s));
+  d = own.as<double>();
+  host = dst;
+  return 0;
+}
+int Out::finish(cudaStream_t s) {
+  if (host) {
+    NNB_CUDA(cudaMemcpyAsync(host, d, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+    NNB_CUDA(cudaStreamSynchronize(s));
+  }
+  return 0;
+}
+
+int RedWs::init(int max_tiles, cudaStream_t s) {
+  capacity = max_tiles;
+  const size_t bytes = sizeof(double) * max_tiles + sizeof(int) * max_tiles + 64;
+  NNB_TRY(buf.alloc(bytes, s));
+  ss_partial = buf.as<double>();
+  nf_partial = reinterpret_cast<int*>(ss_partial + max_tiles);
+  counter = reinterpret_cast<unsigned*>(nf_partial + max_tiles + 1);
+  counter = reinterpret_cast<unsigned*>((reinterpret_cast<uintptr_t>(counter) + 15) & ~uintptr_t(15));
+  NNB_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
+  return 0;
+}
+
+// ============================ TMA ============================
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// Row-major rows×cols FP64 matrix with leading dimension ld, box = box_rows×box_cols.
+static int make_tmap(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+                     int box_rows, int box_cols, bool swizzle128) {
+  auto fn = encode_fn();
+  if (!fn) return fail(7, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * 8) & 15))
+    return fail(7, "TMA operand needs 16B alignment and an even leading dimension");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 8)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(7, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return 0;
+}
+
+// ============================ GEMM ============================
+using BigCfg = GemmCfg<128, 128, 16, 2, 4, 4>;
+using SmallCfg = GemmCfg<64, 64, 16, 2, 2, 4>;
+
+static bool use_big(int64_t M, int64_t N) {
+  const int64_t big_tiles = ((M + 127) / 128) * ((N + 127) / 128);
+  return big_tiles >= 2 * 148;
+}
+
+int max_tiles_for(int64_t M, int64_t N) {
+  return static_cast<int>(((M + 63) / 64) * ((N + 63) / 64));
+}
+
+template <class Cfg>
+static int launch_cfg(const GemmOp& op, cudaStream_t s) {
+  CUtensorMap ta, tb;
+  NNB_TRY(make_tmap(&ta, op.A, op.M, op.K, op.lda, Cfg::kBM, Cfg::kBK, true));
+  NNB_TRY(make_tmap(&tb, op.B, op.K, op.N, op.ldb, Cfg::kBK, Cfg::kBN, false));
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    NNB_CUDA(cudaFuncSetAttribute(gemm_f64_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  Cfg::kSmemBytes));
+    attr_set = true;
+  }
+  const int64_t tiles = ((op.M + Cfg::kBM - 1) / Cfg::kBM) * ((op.N + Cfg::kBN - 1) / Cfg::kBN);
+  gemm_f64_kernel<Cfg><<<static_cast<unsigned>(tiles), Cfg::kThreads, Cfg::kSmemBytes, s>>>(
+      ta, tb, static_cast<int>(op.M), static_cast<int>(op.N), static_cast<int>(op.K), op.ep);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int gemm(GemmOp op, RedWs* red, cudaStream_t s) {
+  if (op.M <= 0 || op.N <= 0) return 0;
+  if (op.M > INT32_MAX || op.N > INT32_MAX || op.K > INT32_MAX)
+    return fail(1, "gemm: dimension exceeds int32");
+  if ((reinterpret_cast<uintptr_t>(op.ep.C) & 15) || (op.ep.ldc & 1) ||
+      (op.ep.D && ((reinterpret_cast<uintptr_t>(op.ep.D) & 15) || (op.ep.ldd & 1))))
+    return fail(7, "gemm: epilogue operands need 16B alignment and even leading dimensions");
+  if (red) {
+    if (red->capacity < max_tiles_for(op.M, op.N)) return fail(7, "gemm: reduction workspace too small");
+    op.ep.ss_partial = red->ss_partial;
+    op.ep.nf_partial = red->nf_partial;
+    op.ep.tile_counter = red->counter;
+  } else {
+    op.ep.ss_partial = nullptr;
+  }
+  if (op.K == 0) {  // empty inner dimension: C = beta*D + gamma*I
+    return axpby(0.0, op.ep.C, op.ep.ldc, op.ep.beta, op.ep.D, op.ep.ldd, op.ep.gamma,
+                 op.ep.diag_offset, op.ep.C, op.ep.ldc, op.M, op.N, s);
+  }
+  return use_big(op.M, op.N) ? launch_cfg<BigCfg>(op, s) : launch_cfg<SmallCfg>(op, s);
+}
+
+// ============================ auxiliary kernels ============================
+__global__ void axpby_kernel(double alpha, const double* __restrict__ A, int64_t lda, double beta,
+                             const double* __restrict__ B, int64_t ldb, double gamma, int64_t off,
+                             double* out, int64_t ldo, int64_t rows, int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / cols, c = idx % cols;
+    double v = alpha == 0.0 ? 0.0 : alpha * A[r * lda + c];
+    if (B) v = fma(beta, B[r * ldb + c], v);
+    if (r + off == c) v += gamma;
+    out[r * ldo + c] = v;
+  }
+}
+
+static unsigned grid_for(int64_t total, int threads = 256) {
+  const int64_t want = (total + threads - 1) / threads;
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, 148 * 16)));
+}
+
+int axpby(double alpha, const double* A, int64_t lda, double beta, const double* B, int64_t ldb,
+          double gamma, int64_t diag_offset, double* out, int64_t ldo, int64_t rows, int64_t cols,
+          cudaStream_t s) {
+  if (rows * cols == 0) return 0;
+  axpby_kernel<<<grid_for(rows * cols), 256, 0, s>>>(alpha, A, lda, beta, B, ldb, gamma,
+                                                      diag_offset, out, ldo, rows, cols);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
+           cudaStream_t s) {
+  if (rows * cols == 0) return 0;
+  NNB_CUDA(cudaMemcpy2DAsync(dst, ldd * 8, src, lds * 8, cols * 8, rows, cudaMemcpyDeviceToDevice,
+                             s));
+  return 0;
+}
+
+int fill_identity(double* X, int64_t n, int64_t ld, double val, cudaStream_t s) {
+  return axpby(0.0, X, ld, 0.0, nullptr, 0, val, 0, X, ld, n, n, s);
+}
+
+// Row abs sums: one warp per row, fixed lane/shuffle order.
+__global__ void row_abs_sum_kernel(const double* __restrict__ A, int64_t n, int64_t lda,
+                                   double* __restrict__ out) {
+  const int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double s = 0.0;
+  for (int64_t c = lane; c < n; c += 32) s += fabs(A[row * lda + c]);
+  s = warp_sum(s);
+  if (lane == 0) out[row] = s;
+}
+
+// Column abs sums over a row chunk: thread = column, rows [r0, r1).
+__global__ void col_abs_sum_kernel(const double* __restrict__ A, int64_t n, int64_t lda,
+                                   int64_t rows_per_chunk, double* __restrict__ partial) {
+  const int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t chunk = blockIdx.y;
+  if (col >= n) return;
+  const int64_t r0 = chunk * rows_per_chunk, r1 = min(n, r0 + rows_per_chunk);
+  double s = 0.0;
+  for (int64_t r = r0; r < r1; ++r) s += fabs(A[r * lda + col]);
+  partial[chunk * n + col] = s;
+}
+
+// Deterministic max over row sums and column sums (max is order-free; column
+// chunk partials are summed in chunk order first).  Writes 1/(‖A‖₁‖A‖∞).
+__global__ void norm_scale_kernel(const double* __restrict__ rowsum,
+                                  const double* __restrict__ colpart, int64_t n, int64_t chunks,
+                                  double* __restrict__ scale_out) {
+  __shared__ double smax[2][32];
+  double mr = 0.0, mc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    mr = fmax(mr, rowsum[i]);
+    double c = 0.0;
+    for (int64_t k = 0; k < chunks; ++k) c += colpart[k * n + i];
+    mc = fmax(mc, c);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mr = fmax(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+    mc = fmax(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    smax[0][threadIdx.x / 32] = mr;
+    smax[1][threadIdx.x / 32] = mc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) {
+      a = fmax(a, smax[0][w]);
+      b = fmax(b, smax[1][w]);
+    }
+    scale_out[0] = 1.0 / (b * a);  // ||A||_1 = max col sum, ||A||_inf = max row sum
+    scale_out[1] = b;
+    scale_out[2] = a;
+  }
+}
+
+// X0[i][j] = A[j][i] * scale (32x32 smem tile transpose).
+__global__ void transpose_scale_kernel(const double* __restrict__ A, int64_t lda, int64_t n,
+                                       const double* __restrict__ scale, double* __restrict__ X,
+                                       int64_t ldx) {
+  __shared__ double tile[32][33];
+  const double sc = *scale;
+  const int64_t bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = by + k, c = bx + threadIdx.x;
+    if (r < n && c < n) tile[k][threadIdx.x] = A[r * lda + c];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = bx + k, c = by + threadIdx.x;  // X row = A col
+    if (r < n && c < n) X[r * ldx + c] = tile[threadIdx.x][k] * sc;
+  }
+}
+
+__global__ void jacobi_kernel(const double* __restrict__ A, int64_t lda, int64_t n,
+                              double* __restrict__ X, int64_t ldx) {
+  const int64_t total = n * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / n, c = idx % n;
+    X[r * ldx + c] = (r == c) ? 1.0 / A[r * lda + r] : 0.0;
+  }
+}
+
+int x0_build(const double* A, int64_t lda, int64_t n, int kind, double scale, double* X0,
+             int64_t ldx, cudaStream_t s) {
+  switch (kind) {
+    case 1:
+      return fill_identity(X0, n, ldx, scale, s);
+    case 3:
+      jacobi_kernel<<<grid_for(n * n), 256, 0, s>>>(A, lda, n, X0, ldx);
+      count_launch();
+      NNB_CUDA(cudaGetLastError());
+      return 0;
+    case 2: {
+      const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(64, n / 256));
+      const int64_t rpc = (n + chunks - 1) / chunks;
+      DevBuf ws;
+      NNB_TRY(ws.alloc(sizeof(double) * (n + chunks * n + 4), s));
+      double* rowsum = ws.as<double>();
+      double* colpart = rowsum + n;
+      double* sc = colpart + chunks * n;
+      row_abs_sum_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, s>>>(A, n, lda, rowsum);
+      dim3 cg(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(chunks));
+      col_abs_sum_kernel<<<cg, 256, 0, s>>>(A, n, lda, rpc, colpart);
+      norm_scale_kernel<<<1, 1024, 0, s>>>(rowsum, colpart, n, chunks, sc);
+      dim3 tg(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((n + 31) / 32));
+      transpose_scale_kernel<<<tg, dim3(32, 8), 0, s>>>(A, lda, n, sc, X0, ldx);
+      count_launch(4);
+      NNB_CUDA(cudaGetLastError());
+      return 0;
+    }
+    default:
+      return fail(2, "x0_build: unknown or caller-provided X0 kind");
+  }
+}
+
+// Deterministic Σ v²: fixed 1184-block partition, then one block in order.
+__global__ void sumsq_partial_kernel(const double* __restrict__ v, int64_t count,
+                                     double* __restrict__ partial) {
+  __shared__ double red[32];
+  const int64_t per = (count + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * per, b1 = min(count, b0 + per);
+  double s = 0.0;
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) s = fma(v[i], v[i], s);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) t += red[w];
+    partial[blockIdx.x] = t;
+  }
+}
+__global__ void sum_partials_kernel(const double* __restrict__ partial, int count,
+                                    double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) s += partial[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) t += red[w];
+    *out = t;
+  }
+}
+
+int sumsq(const double* v, int64_t count, double* out_dev, cudaStream_t s) {
+  constexpr int kBlocks = 1184;
+  DevBuf ws;
+  NNB_TRY(ws.alloc(sizeof(double) * kBlocks, s));
+  sumsq_partial_kernel<<<kBlocks, 256, 0, s>>>(v, count, ws.as<double>());
+  sum_partials_kernel<<<1, 1024, 0, s>>>(ws.as<double>(), kBlocks, out_dev);
+  count_launch(2);
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+__global__ void trace_kernel(const double* __restrict__ M, int64_t n, int64_t ld, int cs,
+                             double* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  double re = 0.0, im = 0.0;  // serial, ascending: the reference's order (kernels.cpp:231-236)
+  for (int64_t i = 0; i < n; ++i) {
+    re += M[(i * ld + i) * cs];
+    if (cs == 2) im += M[(i * ld + i) * 2 + 1];
+  }
+  out[0] = re;
+  out[1] = im;
+}
+
+int trace_dev(const double* M, int64_t n, int64_t ld, int complex_stride, double* out_dev,
+              cudaStream_t s) {
+  trace_kernel<<<1, 32, 0, s>>>(M, n, ld, complex_stride, out_dev);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+__global__ void deinterleave_kernel(const double2* __restrict__ z, int64_t count,
+                                    double* __restrict__ re, double* __restrict__ im) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = z[i];
+    re[i] = v.x;
+    im[i] = v.y;
+  }
+}
+__global__ void interleave_kernel(const double* __restrict__ re, const double* __restrict__ im,
+                                  int64_t count, double2* __restrict__ z) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    z[i] = make_double2(re[i], im[i]);
+}
+
+int deinterleave(const double* z, int64_t count, double* re, double* im, cudaStream_t s) {
+  if (!count) return 0;
+  deinterleave_kernel<<<grid_for(count), 256, 0, s>>>(reinterpret_cast<const double2*>(z), count,
+                                                       re, im);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+int interleave(const double* re, const double* im, int64_t count, double* z, cudaStream_t s) {
+  if (!count) return 0;
+  interleave_kernel<<<grid_for(count), 256, 0, s>>>(re, im, count, reinterpret_cast<double2*>(z));
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// ---- complex helpers for the drop-in surface ----
+__global__ void is_identity_kernel(const double* __restrict__ re, const double* __restrict__ im,
+                                   int64_t n, int64_t ld, int* __restrict__ bad) {
+  const int64_t total = n * n;
+  bool b = false;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / n, c = idx % n;
+    b |= re[r * ld + c] != (r == c ? 1.0 : 0.0);
+    if (im) b |= im[r * ld + c] != 0.0;
+  }
+  if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+
+int is_identity_dev(const double* re, const double* im, int64_t n, int64_t ld, bool* result,
+                    cudaStream_t s) {
+  DevBuf flag;
+  NNB_TRY(flag.alloc(sizeof(int), s));
+  NNB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+  is_identity_kernel<<<grid_for(n * n), 256, 0, s>>>(re, im, n, ld, flag.as<int>());
+  count_launch();
+  int h = 0;
+  NNB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  *result = h == 0;
+  return 0;
+}
+
+__global__ void deinterleave2d_kernel(const double2* __restrict__ z, int64_t rows, int64_t cols,
+                                      double* __restrict__ re, double* __restrict__ im,
+                                      int64_t ldp) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    const double2 v = z[i];
+    re[r * ldp + c] = v.x;
+    if (im) im[r * ldp + c] = v.y;
+  }
+}
+__global__ void interleave2d_kernel(const double* __restrict__ re, const double* __restrict__ im,
+                                    int64_t rows, int64_t cols, int64_t ldp,
+                                    double2* __restrict__ z) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    z[i] = make_double2(re[r * ldp + c], im ? im[r * ldp + c] : 0.0);
+  }
+}
+
+int deinterleave2d(const double* z, int64_t rows, int64_t cols, double* re, double* im,
+                   int64_t ldp, cudaStream_t s) {
+  if (rows * cols == 0) return 0;
+  deinterleave2d_kernel<<<grid_for(rows * cols), 256, 0, s>>>(
+      reinterpret_cast<const double2*>(z), rows, cols, re, im, ldp);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+int interleave2d(const double* re, const double* im, int64_t rows, int64_t cols, int64_t ldp,
+                 double* z, cudaStream_t s) {
+  if (rows * cols == 0) return 0;
+  interleave2d_kernel<<<grid_for(rows * cols), 256, 0, s>>>(re, im, rows, cols, ldp,
+                                                              reinterpret_cast<double2*>(z));
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// out = α·A + β·B + γ·I on interleaved complex data.  The complex products
+// use explicitly rounded multiplies (no FMA contraction) so scale/add/sub/
+// identity_minus/plus_identity round exactly as std::complex<double> does in
+// the reference (kernels.cpp:175-221).
+__global__ void axpby_z_kernel(double ar, double ai, const double2* __restrict__ A, double br,
+                               double bi, const double2* __restrict__ B, double gr, double gi,
+                               double2* __restrict__ out, int64_t rows, int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    const double2 a = A[i];
+    double xr, xi;
+    if (ar == 1.0 && ai == 0.0) {
+      xr = a.x; xi = a.y;
+    } else if (ar == -1.0 && ai == 0.0) {
+      xr = -a.x; xi = -a.y;
+    } else {
+      xr = __dsub_rn(__dmul_rn(a.x, ar), __dmul_rn(a.y, ai));
+      xi = __dadd_rn(__dmul_rn(a.x, ai), __dmul_rn(a.y, ar));
+    }
+    if (B) {
+      const double2 b = B[i];
+      if (br == 1.0 && bi == 0.0) {
+        xr = __dadd_rn(xr, b.x); xi = __dadd_rn(xi, b.y);
+      } else if (br == -1.0 && bi == 0.0) {
+        xr = __dsub_rn(xr, b.x); xi = __dsub_rn(xi, b.y);
+      } else {
+        xr = __dadd_rn(xr, __dsub_rn(__dmul_rn(b.x, br), __dmul_rn(b.y, bi)));
+        xi = __dadd_rn(xi, __dadd_rn(__dmul_rn(b.x, bi), __dmul_rn(b.y, br)));
+      }
+    }
+    if (r == c) {
+      xr = __dadd_rn(gr, xr);
+      xi = __dadd_rn(gi, xi);
+    }
+    out[i] = make_double2(xr, xi);
+  }
+}
+
+int axpby_z(double ar, double ai, const double* A, double br, double bi, const double* B,
+            double gr, double gi, double* out, int64_t rows, int64_t cols, cudaStream_t s) {
+  if (rows * cols == 0) return 0;
+  axpby_z_kernel<<<grid_for(rows * cols), 256, 0, s>>>(
+      ar, ai, reinterpret_cast<const double2*>(A), br, bi, reinterpret_cast<const double2*>(B), gr,
+      gi, reinterpret_cast<double2*>(out), rows, cols);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace nnb

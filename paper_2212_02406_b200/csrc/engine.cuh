@@ -1,0 +1,165 @@
+// Internal engine API shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "gemm_f64.cuh"
+
+namespace nnb {
+
+// ---- error plumbing (thread-local message, status codes of include/nnb.h) --
+void set_error(const std::string& msg);
+const char* last_error();
+
+struct Status {
+  int code = 0;
+  Status() = default;
+  Status(int c) : code(c) {}
+  bool ok() const { return code == 0; }
+};
+
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+#define NNB_CUDA(x)                                                            \
+  do {                                                                         \
+    cudaError_t _e = (x);                                                      \
+    if (_e != cudaSuccess) return ::nnb::cuda_fail(_e, #x, __FILE__, __LINE__); \
+  } while (0)
+#define NNB_TRY(x)              \
+  do {                          \
+    int _s = (x);               \
+    if (_s != 0) return _s;     \
+  } while (0)
+
+int fail(int code, const std::string& msg);
+void count_launch(uint64_t n = 1);
+uint64_t launches();
+
+// ---- device staging --------------------------------------------------------
+bool is_device_ptr(const void* p);
+int require_device();
+cudaStream_t resolve(void* stream);
+
+// Device buffer owned by one call (stream-ordered allocation).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  int alloc(size_t b, cudaStream_t st);
+  void release();
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+// Either the caller's device pointer or a staged device copy of a host array.
+struct In {
+  const double* d = nullptr;
+  DevBuf own;
+  int stage(const double* src, size_t count, cudaStream_t s);
+};
+struct Out {
+  double* d = nullptr;
+  double* host = nullptr;
+  size_t count = 0;
+  DevBuf own;
+  int prepare(double* dst, size_t count, cudaStream_t s);
+  int finish(cudaStream_t s);  // copies back to host when staged
+};
+
+// ---- GEMM ------------------------------------------------------------------
+// Reduction workspace: per-tile partials + the last-CTA counter.
+struct RedWs {
+  DevBuf buf;
+  double* ss_partial = nullptr;
+  int* nf_partial = nullptr;
+  unsigned* counter = nullptr;
+  int capacity = 0;
+  int init(int max_tiles, cudaStream_t s);
+};
+
+struct GemmOp {
+  const double* A = nullptr;
+  int64_t lda = 0;
+  const double* B = nullptr;
+  int64_t ldb = 0;
+  int64_t M = 0, N = 0, K = 0;
+  GemmEpilogue ep;
+};
+
+int max_tiles_for(int64_t M, int64_t N);
+// Launches C = epilogue(A·B).  If `red` is non-null the Σ C² / non-finite
+// reduction is wired to it (ep.ss_out / nf_out / eps_out chosen by caller).
+int gemm(GemmOp op, RedWs* red, cudaStream_t s);
+
+// ---- auxiliary kernels ----------------------------------------------------------
+int axpby(double alpha, const double* A, int64_t lda, double beta, const double* B, int64_t ldb,
+          double gamma, int64_t diag_offset, double* out, int64_t ldo, int64_t rows, int64_t cols,
+          cudaStream_t s);
+int copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
+           cudaStream_t s);
+int x0_build(const double* A, int64_t lda, int64_t n, int kind, double scale, double* X0,
+             int64_t ldx, cudaStream_t s);
+// deterministic Σ v² over `count` doubles (stride 1) into *out_dev
+int sumsq(const double* v, int64_t count, double* out_dev, cudaStream_t s);
+int trace_dev(const double* M, int64_t n, int64_t ld, int complex_stride, double* out_dev,
+              cudaStream_t s);
+int deinterleave(const double* z, int64_t count, double* re, double* im, cudaStream_t s);
+int interleave(const double* re, const double* im, int64_t count, double* z, cudaStream_t s);
+int fill_identity(double* X, int64_t n, int64_t ld, double val, cudaStream_t s);
+
+// ---- dense chain -----------------------------------------------------------------
+struct ChainCfg {
+  int p = 1;
+  int max_iters = 1;
+  double tol = 0.0;
+  int order = 0;
+  int final_residual = 1;
+};
+struct ChainOut {
+  int iters = 0;
+  int fail_iter = 0;
+  int stopped = 1;
+  int products = 0;
+  double last_eps = 0.0;
+  float device_ms = 0.f;
+};
+// Real chain on device buffers with ld == ldn (ldn even, >= n).  X holds X0
+// on entry and the final iterate on exit.  eps_hist host (nullable).
+int chain_real(const double* A, int64_t n, int64_t ldn, double* X, const ChainCfg& cfg,
+               double* eps_hist, ChainOut* out, cudaStream_t s);
+// Complex chain on planar device buffers (re/im each n×ldn).
+int chain_complex(const double* Ar, const double* Ai, int64_t n, int64_t ldn, double* Xr,
+                  double* Xi, const ChainCfg& cfg, double* eps_hist, ChainOut* out,
+                  cudaStream_t s);
+
+// ns_sum on device planes (im pointers null for real); identity_start as the
+// reference decides it (phi0 exactly I).
+int ns_sum_dev(const double* phi0_re, const double* phi0_im, const double* w_re,
+               const double* w_im, int64_t n, int64_t ldn, int64_t order, bool identity_start,
+               double* out_re, double* out_im, double* products, cudaStream_t s);
+int is_identity_dev(const double* re, const double* im, int64_t n, int64_t ld, bool* result,
+                    cudaStream_t s);
+int deinterleave2d(const double* z, int64_t rows, int64_t cols, double* re, double* im,
+                   int64_t ldp, cudaStream_t s);
+int interleave2d(const double* re, const double* im, int64_t rows, int64_t cols, int64_t ldp,
+                 double* z, cudaStream_t s);
+int axpby_z(double ar, double ai, const double* A, double br, double bi, const double* B,
+            double gr, double gi, double* out, int64_t rows, int64_t cols, cudaStream_t s);
+
+// ---- batched / sparse (separate translation units) -------------------------------
+int batched_nn_z16(const double* A, int64_t batch, int p, int iters, int ns_order, double* X,
+                   double* eps_last, cudaStream_t s);
+int spmv_csr(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n,
+             const double* X, int64_t k, double* Y, cudaStream_t s);
+int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n,
+                      const double* B, int64_t k, int s_factors, double theta, double* X,
+                      int* fail_factor, cudaStream_t s);
+
+}  // namespace nnb

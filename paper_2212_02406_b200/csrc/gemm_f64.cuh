@@ -1,0 +1,261 @@
+// FP64 DMMA GEMM with the Nested Neumann epilogues fused in.
+//
+//   C = alpha * (A·B) + beta * D + gamma * I_shifted        (row-major, FP64)
+//
+// plus, optionally, a deterministic Σ C² / non-finite count over the whole
+// output (per-tile partials, then the last CTA to finish sums them in fixed
+// tile order — no floating-point atomics, so eps is bit-reproducible run to
+// run).  One kernel therefore covers every dense product of the chain:
+//   R = I − A·X      alpha=-1, gamma=1, Σ‖R‖² → eps   (residual + first product)
+//   V = X + V·R      alpha= 1, beta=1, D=X           (Horner step of X·S(R))
+//   P = I − X·A, V = X + P·V                          (reference operand order)
+// replacing the reference's matmul + identity_minus + plus_identity +
+// frobenius_norm passes (/root/reference/proj/src/kernels.cpp:137-242,
+// /root/reference/proj/src/solver.cpp:27-36,72-75,93-103): no separate
+// elementwise or norm kernel touches HBM.
+//
+// Structure (sm_100a): one TMA producer warp streams BMxBK tiles of A
+// (128B-swizzled) and BKxBN tiles of B (linear) into a STAGES-deep shared
+// ring guarded by full/empty mbarriers; WM×WN consumer warps run
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4) out of shared memory with the
+// accumulators in registers; the epilogue runs from registers.
+#pragma once
+
+#include "common.cuh"
+
+namespace nnb {
+
+struct GemmEpilogue {
+  double alpha = 1.0;
+  double beta = 0.0;
+  const double* D = nullptr;  // may alias C (read-before-write per element)
+  int64_t ldd = 0;
+  double gamma = 0.0;         // added where (row + diag_offset) == col
+  int64_t diag_offset = 0;
+  double* C = nullptr;
+  int64_t ldc = 0;
+  // Σ C² / non-finite reduction (all nullable => skipped)
+  double* ss_partial = nullptr;  // [num_tiles]
+  int* nf_partial = nullptr;     // [num_tiles]
+  unsigned* tile_counter = nullptr;  // zero on entry, reset to zero by the last CTA
+  double* ss_out = nullptr;      // Σ C²
+  int* nf_out = nullptr;         // Σ non-finite
+  double* eps_out = nullptr;     // sqrt(Σ C²) * eps_scale
+  double eps_scale = 1.0;
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+struct GemmCfg {
+  static constexpr int kBM = BM, kBN = BN, kBK = BK, kWM = WM, kWN = WN, kStages = STAGES;
+  static constexpr int kConsumerWarps = WM * WN;
+  static constexpr int kThreads = (kConsumerWarps + 1) * 32;
+  static constexpr int kWarpM = BM / WM, kWarpN = BN / WN;
+  static constexpr int kMI = kWarpM / 8, kNI = kWarpN / 8;
+  static constexpr int kABytes = BM * BK * 8, kBBytes = BK * BN * 8;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(BK == 16, "A tile rows are one 128-byte swizzle row");
+  static_assert(kWarpM % 8 == 0 && kWarpN % 8 == 0, "warp tile must be a multiple of 8x8");
+  static_assert(kABytes % 1024 == 0 && kBBytes % 1024 == 0, "stages must stay 1024B aligned");
+};
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::kThreads, 1)
+    gemm_f64_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    int M, int N, int K, GemmEpilogue ep) {
+  constexpr int BM = Cfg::kBM, BN = Cfg::kBN, BK = Cfg::kBK, STAGES = Cfg::kStages;
+  constexpr int MI = Cfg::kMI, NI = Cfg::kNI, NCW = Cfg::kConsumerWarps;
+
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes);
+  uint64_t* empty = full + STAGES;
+  double* red = reinterpret_cast<double*>(empty + STAGES);  // [NCW]
+  int* redi = reinterpret_cast<int*>(red + NCW);            // [NCW]
+  int* last_flag = redi + NCW;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // grouped raster: GROUP_M tile-rows sweep the tile-columns together (L2 reuse)
+  constexpr int GROUP_M = 8;
+  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  const int pid = blockIdx.x;
+  const int group = pid / (GROUP_M * tiles_n);
+  const int first_m = group * GROUP_M;
+  const int gsz = min(tiles_m - first_m, GROUP_M);
+  const int tm = first_m + (pid % gsz);
+  const int tn = (pid % (GROUP_M * tiles_n)) / gsz;
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int KT = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == NCW) {
+    // ===== TMA producer (one elected lane) =====
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % STAGES;
+        const uint32_t ph = (kt / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * Cfg::kStageBytes;
+        uint8_t* sb = sa + Cfg::kABytes;
+        mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
+        tma_load_2d(sa, &tmA, &full[s], kt * BK, m0);
+        tma_load_2d(sb, &tmB, &full[s], n0, kt * BK);
+      }
+    }
+    return;
+  }
+
+  // ===== DMMA consumers =====
+  const int wm = warp / Cfg::kWN, wn = warp % Cfg::kWN;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[MI][NI][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // Per-thread fragment byte offsets inside a stage.
+  // A (128B swizzle): (r,k) -> r*128 + ((k>>1) ^ (r&7))*16 + (k&1)*8, r&7 == g.
+  // B (linear):       (k,n) -> (k*BN + n)*8.
+  const uint32_t a_row_off = (wm * Cfg::kWarpM + g) * 128;
+  const uint32_t b_col_off = (wn * Cfg::kWarpN + g) * 8 + t * BN * 8;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % STAGES;
+    const uint32_t ph = (kt / STAGES) & 1;
+    mbar_wait(&full[s], ph);
+    const uint8_t* sa = smem + s * Cfg::kStageBytes;
+    const uint8_t* sb = sa + Cfg::kABytes;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double af[MI], bf[NI];
+      const uint32_t a_chunk = (((kk * 2 + (t >> 1)) ^ g) << 4) | ((t & 1) << 3);
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+        af[i] = *reinterpret_cast<const double*>(sa + a_row_off + i * 8 * 128 + a_chunk);
+#pragma unroll
+      for (int j = 0; j < NI; ++j)
+        bf[j] = *reinterpret_cast<const double*>(sb + b_col_off + kk * 4 * BN * 8 + j * 64);
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ===== fused epilogue from registers =====
+  double ss = 0.0;
+  int nf = 0;
+  const bool want_red = ep.ss_partial != nullptr;
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const int r = m0 + wm * Cfg::kWarpM + i * 8 + g;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      const int c = n0 + wn * Cfg::kWarpN + j * 8 + 2 * t;
+      if (c >= N) continue;
+      const bool two = (c + 1) < N;
+      double v0 = ep.alpha * acc[i][j][0];
+      double v1 = ep.alpha * acc[i][j][1];
+      if (ep.D) {
+        const double* dp = ep.D + (int64_t)r * ep.ldd + c;
+        if (two) {
+          const double2 d = *reinterpret_cast<const double2*>(dp);
+          v0 = fma(ep.beta, d.x, v0);
+          v1 = fma(ep.beta, d.y, v1);
+        } else {
+          v0 = fma(ep.beta, dp[0], v0);
+        }
+      }
+      const int64_t dr = (int64_t)r + ep.diag_offset;
+      if (dr == c) v0 += ep.gamma;
+      if (dr == c + 1) v1 += ep.gamma;
+      double* cp = ep.C + (int64_t)r * ep.ldc + c;
+      if (two) {
+        *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
+      } else {
+        cp[0] = v0;
+      }
+      if (want_red) {
+        ss = fma(v0, v0, ss);
+        nf += !isfinite(v0);
+        if (two) {
+          ss = fma(v1, v1, ss);
+          nf += !isfinite(v1);
+        }
+      }
+    }
+  }
+  if (!want_red) return;
+
+  // deterministic tile reduction: fixed shuffle tree, fixed warp order
+  ss = warp_sum(ss);
+  nf = warp_sum_i(nf);
+  if (lane == 0) {
+    red[warp] = ss;
+    redi[warp] = nf;
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32));
+  const int ntiles = gridDim.x;
+  if (threadIdx.x == 0) {
+    double tss = 0.0;
+    int tnf = 0;
+    for (int w = 0; w < NCW; ++w) {
+      tss += red[w];
+      tnf += redi[w];
+    }
+    ep.ss_partial[pid] = tss;
+    ep.nf_partial[pid] = tnf;
+    __threadfence();
+    const unsigned done = atomicAdd(ep.tile_counter, 1u);
+    *last_flag = (done == (unsigned)(ntiles - 1));
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32));
+  if (!*last_flag) return;
+
+  // last CTA: sum all tile partials in a fixed order
+  __threadfence();
+  double s2 = 0.0;
+  int n2 = 0;
+  for (int k = threadIdx.x; k < ntiles; k += NCW * 32) {
+    s2 += __ldcg(ep.ss_partial + k);
+    n2 += __ldcg(ep.nf_partial + k);
+  }
+  s2 = warp_sum(s2);
+  n2 = warp_sum_i(n2);
+  asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32));
+  if (lane == 0) {
+    red[warp] = s2;
+    redi[warp] = n2;
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32));
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    int ntot = 0;
+    for (int w = 0; w < NCW; ++w) {
+      tot += red[w];
+      ntot += redi[w];
+    }
+    if (ep.ss_out) *ep.ss_out = tot;
+    if (ep.nf_out) *ep.nf_out = ntot;
+    if (ep.eps_out) *ep.eps_out = sqrt(tot) * ep.eps_scale;
+    *ep.tile_counter = 0u;
+  }
+}
+
+}  // namespace nnb

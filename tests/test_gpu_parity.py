@@ -1,0 +1,299 @@
+"""Parity of the CUDA path against the oracle (GPU only; run with -m gpu).
+
+Tolerances (north_star): X within 1e-10 relative Frobenius at equal
+iteration count, identical iteration counts to reach eps, eps history within
+1e-6 relative + 1e-13 (entries below 1e-12 compare as "both < 1e-12").
+Integer results (spmv counts, products, iteration indices) are exact.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden, rel_frob
+
+pytestmark = pytest.mark.gpu
+
+nnb = pytest.importorskip("paper_2212_02406_b200")
+from paper_2212_02406_b200 import workloads as W  # noqa: E402
+
+TOL_X = 1e-10
+
+
+def eps_close(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.shape == b.shape, (a.shape, b.shape)
+    floor = (a < 1e-12) & (b < 1e-12)
+    ok = floor | (np.abs(a - b) <= 1e-6 * b + 1e-13)
+    assert ok.all(), np.c_[a, b][~ok]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test selected but no CUDA device")
+    nnb.lib()
+
+
+# ----------------------------------------------------------------- GEMM
+@pytest.mark.parametrize("m,k,n", [(1, 1, 1), (7, 5, 3), (64, 64, 64), (130, 257, 129), (256, 256, 256),
+                                   (1024, 512, 768)])
+def test_gemm_real_vs_oracle(port, m, k, n):
+    rng = np.random.default_rng(m * 7 + n)
+    a, b = rng.standard_normal((m, k)), rng.standard_normal((k, n))
+    c = nnb.matmul(a, b)
+    assert rel_frob(c, port.matmul(a, b).real) < 1e-14
+
+
+def test_gemm_device_pointers_and_determinism():
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(0)
+    a = torch.randn(2048, 2048, dtype=torch.float64, device="cuda", generator=g)
+    b = torch.randn(2048, 2048, dtype=torch.float64, device="cuda", generator=g)
+    c1 = nnb.matmul(a, b)
+    c2 = nnb.matmul(a, b)
+    torch.cuda.synchronize()
+    assert torch.equal(c1, c2)  # bit-reproducible
+    ref = (a @ b)
+    assert (torch.linalg.norm(c1 - ref) / torch.linalg.norm(ref)).item() < 1e-14
+
+
+def test_gemm_complex_vs_oracle(port):
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((33, 20)) + 1j * rng.standard_normal((33, 20))
+    b = rng.standard_normal((20, 17)) + 1j * rng.standard_normal((20, 17))
+    assert rel_frob(nnb.matmul(a, b), port.matmul(a, b)) < 1e-14
+
+
+def test_gemm_nonfinite_raises():
+    a = np.eye(8)
+    a[3, 3] = np.inf
+    with pytest.raises(nnb.DomainError):
+        nnb.matmul(a, np.eye(8))
+
+
+# ----------------------------------------------------------------- elementwise
+def test_elementwise_bitexact_vs_reference(ref):
+    rng = np.random.default_rng(4)
+    a = rng.standard_normal((9, 9)) + 1j * rng.standard_normal((9, 9))
+    b = rng.standard_normal((9, 9)) + 1j * rng.standard_normal((9, 9))
+    assert np.array_equal(nnb.add(a, b), ref.elementwise("add", a, b)[0])
+    assert np.array_equal(nnb.sub(a, b), ref.elementwise("sub", a, b)[0])
+    assert np.array_equal(nnb.scale(a, 0.3 - 0.7j), ref.elementwise("scale", a, s=0.3 - 0.7j)[0])
+    assert np.array_equal(nnb.identity_minus(a), ref.elementwise("identity_minus", a)[0])
+    assert np.array_equal(nnb.plus_identity(a), ref.elementwise("plus_identity", a)[0])
+    assert nnb.trace(a) == ref.trace(a)
+    assert abs(nnb.frobenius_norm(a) - ref.frobenius(a)) < 1e-14 * ref.frobenius(a)
+
+
+# ----------------------------------------------------------------- residual / step / ns_sum
+def test_residual_and_steps_vs_golden():
+    g = golden("steps_spd8.npz")
+    wt, z = g["wt"], g["z"]
+    for L in (1, 2, 3):
+        assert rel_frob(nnb.nn_step(z, wt, L), g[f"nn{L}"]) < 1e-13
+    assert rel_frob(nnb.newton_step(z, wt), g["newton"]) < 1e-13
+    assert rel_frob(nnb.chebyshev_step(z, wt), g["chebyshev"]) < 1e-13
+    s, prods = nnb.ns_sum(np.eye(8), wt, 26)
+    assert rel_frob(s, g["ns26"]) < 1e-13 and prods == 25 == g["ns26_n3"]
+    assert np.array_equal(nnb.nn_step(z, wt, 0), z)
+
+
+def test_ns_sum_tally_and_values(ref):
+    g = golden("steps_spd8.npz")
+    wt = g["wt"]
+    for phi0 in (np.eye(8), 0.9 * np.eye(8)):
+        for order in (1, 2, 7, 17):
+            s, prods = nnb.ns_sum(phi0, wt, order)
+            r, rp = ref.ns_sum(phi0, wt, order)
+            assert prods == rp  # order-1 (identity start) / order+1 (proj/tests/test_solver.cpp:61-71)
+            assert rel_frob(s, r.real) < 1e-13
+
+
+def test_residual_epsilon(ref):
+    a = W.gram_shifted(100, 2, 0.5)
+    x = W.x0_transpose_norm(a)
+    assert abs(nnb.residual_epsilon(x, a) - ref.residual_eps(x, a)) < 1e-14
+
+
+def test_complex_step_and_residual(ref):
+    rng = np.random.default_rng(8)
+    h = rng.standard_normal((40, 12)) + 1j * rng.standard_normal((40, 12))
+    a = np.conj(h.T) @ h / 40 + 0.5 * np.eye(12)
+    x = np.diag(1 / np.diag(a))
+    assert rel_frob(nnb.nn_step(x, a, 2), ref.step("nn", x, a, 2)[0]) < 1e-13
+    assert abs(nnb.residual_epsilon(x, a) - ref.residual_eps(x, a)) < 1e-14
+
+
+# ----------------------------------------------------------------- chain (C1 / C3 shapes)
+def test_chain_golden_c1():
+    g = golden("c1_chain_n32_p1.npz")
+    x, rep = nnb.nn_chain(g["a"], g["x0"], p=1, max_iters=int(g["iters"]), order=nnb.ORDER_REFERENCE)
+    eps_close([e for _, e in rep.history], g["eps"])
+    assert rel_frob(x, g["x"]) < TOL_X
+    assert rep.products == int(g["iters"]) * 2 + 1
+
+
+def test_c1_full_vs_reference(ref):
+    """BASELINE config 0: N=256, Gram + 0.5 I, X0 = A^T/(|A|_1|A|_inf), Newton, 30 nests."""
+    a = W.gram_shifted(256, seed=2212, shift=0.5)
+    x0 = W.x0_transpose_norm(a)
+    xr, hr, ir, _ = ref.chain(a, x0, 1, 30)
+    for order in (nnb.ORDER_REFERENCE, nnb.ORDER_NORTHSTAR):
+        x, rep = nnb.nn_chain(a, None, p=1, max_iters=30, order=order)  # X0 built on device
+        eps_close([e for _, e in rep.history], hr)
+        assert rep.iters == ir == 30
+        assert rel_frob(x, xr.real) < TOL_X
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_tolerance_stop_identical_iterations(ref, p):
+    """C3 shape at oracle-friendly size: iterate to eps < 1e-12, same nest count."""
+    a = W.spd_conditioned(192, 1e3, seed=33)
+    x0 = W.x0_transpose_norm(a)
+    xr, hr, ir, _ = ref.chain(a, x0, p, 60, tol=1e-12)
+    for order in (nnb.ORDER_REFERENCE, nnb.ORDER_NORTHSTAR):
+        x, rep = nnb.nn_chain(a, None, p=p, max_iters=60, tol=1e-12, order=order)
+        assert rep.iters == ir and rep.stopped_reason == "tolerance"
+        eps_close([e for _, e in rep.history], hr)
+        assert rel_frob(x, xr.real) < TOL_X
+
+
+def test_nn_invert_vs_golden():
+    g = golden("nn_invert_spd24.npz")
+    norm = nnb.Normalization(theta=float(g["theta"]), contraction_norm=float(g["contraction"]), valid=True)
+    x, rep = nnb.nn_invert(g["w"], norm, depth_L=2, max_nests=40, tol=1e-12)
+    assert len(rep.history) == len(g["eps"]) and rep.stopped_reason == "tolerance"
+    eps_close([e for _, e in rep.history], g["eps"])
+    assert rel_frob(x, g["x"]) < TOL_X
+    assert rep.n3_multiplies == g["n3"] and rep.n2_ops == g["n2"]
+
+
+def test_nn_invert_errors():
+    w = W.spd_conditioned(8, 10, 1)
+    with pytest.raises(nnb.ContractionError):
+        nnb.nn_invert(w, nnb.Normalization(theta=0.1, valid=False))
+    with pytest.raises(nnb.DivergenceError) as e:
+        nnb.nn_invert(w, nnb.Normalization(theta=1e160, valid=True))
+    assert e.value.nest_index >= 1
+    with pytest.raises(nnb.DomainError):
+        nnb.nn_invert(w, nnb.Normalization(theta=0.1, valid=True), tol=1e-16)
+
+
+def test_chain_large_properties():
+    """N=4096 (config 2 size): deterministic, monotone eps, converges below 1e-12."""
+    import torch
+
+    a = torch.from_numpy(W.spd_conditioned(4096, 1e3, seed=4)).cuda()
+    x1, r1 = nnb.nn_chain(a, None, p=2, max_iters=60, tol=1e-12)
+    x2, r2 = nnb.nn_chain(a, None, p=2, max_iters=60, tol=1e-12)
+    torch.cuda.synchronize()
+    assert torch.equal(x1, x2) and r1.history == r2.history
+    eps = [e for _, e in r1.history]
+    assert r1.stopped_reason == "tolerance" and eps[-1] < 1e-12
+    assert all(b < a_ for a_, b in zip(eps, eps[1:]) if a_ > 1e-12)
+    # X·A ≈ I independently of the fused epilogue's reduction
+    r = torch.eye(4096, dtype=torch.float64, device="cuda") - x1 @ a
+    assert (torch.linalg.norm(r) / 64).item() < 1e-11
+
+
+# ----------------------------------------------------------------- batched MIMO (C2)
+def test_batched_vs_golden():
+    g = golden("c2_mimo16.npz")
+    x, eps = nnb.nn_batched(g["a"], p=2, iters=4)
+    for s in range(g["a"].shape[0]):
+        assert rel_frob(x[s], g["x_nn"][s]) < TOL_X
+    eps_close(eps, g["eps_nn"])
+    xs = nnb.ns_batched(g["a"], 80)
+    for s in range(g["a"].shape[0]):
+        assert rel_frob(xs[s], g["x_ns80"][s]) < TOL_X
+
+
+@pytest.mark.parametrize("p,iters", [(1, 6), (2, 4), (3, 3)])
+def test_batched_vs_reference(ref, p, iters):
+    a = W.mimo_gram_host(301, seed=p)  # ragged: not a multiple of the warp grid
+    x, eps = nnb.nn_batched(a, p=p, iters=iters)
+    xr, er, _ = ref.batched("nn", a, p, iters, threads=8)
+    worst = max(rel_frob(x[s], xr[s]) for s in range(a.shape[0]))
+    assert worst < TOL_X
+    eps_close(eps, er)
+
+
+def test_batched_ns_orders(ref):
+    a = W.mimo_gram_host(64, seed=11)
+    for order in (0, 1, 2, 26):
+        xs = nnb.ns_batched(a, order)
+        xr, _, _ = ref.batched("ns", a, 1, order, threads=8)
+        assert max(rel_frob(xs[s], xr[s]) for s in range(64)) < TOL_X
+
+
+def test_batched_full_size_properties():
+    """262144 systems on device: every eps tiny, deterministic, NN beats NS-80 accuracy."""
+    import torch
+
+    a = W.mimo_gram_device(262144, seed=1)
+    x1, e1 = nnb.nn_batched(a, p=2, iters=4)
+    x2, e2 = nnb.nn_batched(a, p=2, iters=4)
+    torch.cuda.synchronize()
+    assert torch.equal(x1, x2) and torch.equal(e1, e2)
+    assert e1.max().item() < 1e-12
+    # spot-check 64 systems against torch's inverse
+    idx = torch.arange(0, 262144, 4096, device="cuda")
+    inv = torch.linalg.inv(a[idx])
+    rel = torch.linalg.norm(x1[idx] - inv, dim=(1, 2)) / torch.linalg.norm(inv, dim=(1, 2))
+    assert rel.max().item() < 1e-12
+
+
+# ----------------------------------------------------------------- sparse (C5)
+def test_sparse_vs_golden():
+    g = golden("c5_lap16.npz")
+    csr = nnb.Csr(g["row_ptr"], g["col"], g["val"], n=256)
+    x, cnt = nnb.solve_sparse_factorized(csr, g["b"], 63, nnb.Normalization(theta=0.2, valid=True))
+    assert cnt == 63 and rel_frob(x, g["x"]) < 1e-13
+
+
+def test_sparse_vs_reference(ref):
+    rp, col, val = W.laplacian_5pt(100)
+    b = W.rhs(10000, seed=9)
+    csr = nnb.Csr(rp, col, val, n=10000)
+    for gamma in (1, 7, 63):
+        x, cnt = nnb.solve_sparse_factorized(csr, b, gamma, nnb.Normalization(theta=0.2, valid=True))
+        xr, cr, _ = ref.sparse_factorized(rp, col, val, b, gamma, 0.2)
+        assert cnt == cr and rel_frob(x, xr.real) < 1e-13
+    y = nnb.spmv_block(csr, b)
+    assert rel_frob(y, ref.spmv_block(rp, col, val, b).real) < 1e-15
+
+
+def test_sparse_errors():
+    rp, col, val = W.laplacian_5pt(8)
+    csr = nnb.Csr(rp, col, val, n=64)
+    b = np.ones(64)
+    ok = nnb.Normalization(theta=0.2, valid=True)
+    with pytest.raises(nnb.PlanError):
+        nnb.solve_sparse_factorized(csr, b, 6, ok)
+    with pytest.raises(nnb.ContractionError):
+        nnb.solve_sparse_factorized(csr, b, 7, nnb.Normalization(theta=0.2, valid=False))
+    with pytest.raises(nnb.DivergenceError):
+        nnb.solve_sparse_factorized(csr, b, 32767, nnb.Normalization(theta=1e150, valid=True))
+
+
+def test_sparse_full_size_property():
+    """4096² grid on device: x = theta·sum_{j<64} P^j b satisfies the series identity
+    W x = b − P^64 b (checked through one more SpMV), and runs deterministically."""
+    import torch
+
+    rp, col, val = W.laplacian_5pt(4096)
+    n = 4096 * 4096
+    dev = lambda a: torch.from_numpy(a).cuda()
+    csr = nnb.Csr(dev(rp), dev(col), dev(val), n=n, nnz=col.size)
+    b = dev(W.rhs(n, seed=1))
+    norm = nnb.Normalization(theta=0.2, valid=True)
+    x1, _ = nnb.solve_sparse_factorized(csr, b, 63, norm)
+    x2, _ = nnb.solve_sparse_factorized(csr, b, 63, norm)
+    torch.cuda.synchronize()
+    assert torch.equal(x1, x2)
+    wx = nnb.spmv_block(csr, x1)
+    # residual b − W x = P^64 b with ||P||_2 <= 0.8 (spec(W) in (1, 9), theta = 0.2)
+    r = torch.linalg.norm(b - wx) / torch.linalg.norm(b)
+    assert 0 < r.item() < 1.001 * 0.8 ** 64
