@@ -13,7 +13,7 @@
  *  - Every matrix/vector pointer may be HOST or DEVICE memory; the library
  *    detects which (cudaPointerGetAttributes) and stages host data through
  *    device buffers itself.  Caller memory is never freed or retained.
- *  - `stream` is a cudaStream_t (NULL = the library's per-thread stream).
+ *  - `stream` is a cudaStream_t (NULL = the legacy default stream).
  *    Host outputs are complete when the call returns; device outputs are
  *    complete in stream order.
  *  - Return value: NNB_OK or an NNB_ERR_* code; nnb_last_error() gives a

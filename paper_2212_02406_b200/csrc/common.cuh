@@ -30,6 +30,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
+// Orders this thread's prior generic-proxy shared-memory accesses before
+// later async-proxy (TMA) accesses.  Consumers that read a stage with plain
+// ld.shared must execute it before releasing the slot to the TMA producer:
+// without it ptxas schedules the release above the last fragment loads and
+// the next TMA fill races them (seen as corrupted rows with >=2 CTAs/SM).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

@@ -54,11 +54,22 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-static thread_local cudaStream_t g_thread_stream = nullptr;
+// NULL means the legacy default stream (the usual CUDA meaning), so callers
+// that produced their operands on it need no extra synchronisation.  The
+// first call also keeps the stream-ordered pool's memory cached across calls
+// (release threshold = max) so per-call work buffers cost no cudaMalloc.
 cudaStream_t resolve(void* stream) {
-  if (stream) return static_cast<cudaStream_t>(stream);
-  if (!g_thread_stream) cudaStreamCreateWithFlags(&g_thread_stream, cudaStreamNonBlocking);
-  return g_thread_stream;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  });
+  return static_cast<cudaStream_t>(stream);
 }
 
 int DevBuf::alloc(size_t b, cudaStream_t st) {
@@ -157,8 +168,16 @@ using BigCfg = GemmCfg<128, 128, 16, 2, 4, 4>;
 using SmallCfg = GemmCfg<64, 64, 16, 2, 2, 4>;
 
 static bool use_big(int64_t M, int64_t N) {
+  static const char* force = std::getenv("NNB_GEMM_CFG");  // debug override: "big" / "small"
+  if (force && force[0] == 'b') return true;
+  if (force && force[0] == 's') return false;
   const int64_t big_tiles = ((M + 127) / 128) * ((N + 127) / 128);
   return big_tiles >= 2 * 148;
+}
+
+static int smem_pad() {
+  static const int pad = std::getenv("NNB_GEMM_SMEM_PAD") ? std::atoi(std::getenv("NNB_GEMM_SMEM_PAD")) : 0;
+  return pad;
 }
 
 int max_tiles_for(int64_t M, int64_t N) {
@@ -170,14 +189,15 @@ static int launch_cfg(const GemmOp& op, cudaStream_t s) {
   CUtensorMap ta, tb;
   NNB_TRY(make_tmap(&ta, op.A, op.M, op.K, op.lda, Cfg::kBM, Cfg::kBK, true));
   NNB_TRY(make_tmap(&tb, op.B, op.K, op.N, op.ldb, Cfg::kBK, Cfg::kBN, false));
+  const int smem = Cfg::kSmemBytes + smem_pad();
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     NNB_CUDA(cudaFuncSetAttribute(gemm_f64_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  Cfg::kSmemBytes));
+                                  smem));
     attr_set = true;
   }
   const int64_t tiles = ((op.M + Cfg::kBM - 1) / Cfg::kBM) * ((op.N + Cfg::kBN - 1) / Cfg::kBN);
-  gemm_f64_kernel<Cfg><<<static_cast<unsigned>(tiles), Cfg::kThreads, Cfg::kSmemBytes, s>>>(
+  gemm_f64_kernel<Cfg><<<static_cast<unsigned>(tiles), Cfg::kThreads, smem, s>>>(
       ta, tb, static_cast<int>(op.M), static_cast<int>(op.N), static_cast<int>(op.K), op.ep);
   count_launch();
   NNB_CUDA(cudaGetLastError());

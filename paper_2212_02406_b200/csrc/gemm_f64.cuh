@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
 #pragma unroll
         for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
+    fence_proxy_async_smem();  // fragment reads of stage s complete before the TMA refill
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }

@@ -228,21 +228,26 @@ def test_batched_ns_orders(ref):
         assert max(rel_frob(xs[s], xr[s]) for s in range(64)) < TOL_X
 
 
-def test_batched_full_size_properties():
-    """262144 systems on device: every eps tiny, deterministic, NN beats NS-80 accuracy."""
+def test_batched_full_size_properties(port):
+    """262144 systems on device (config 1 size): deterministic; the worst-eps systems and a
+    strided sample match the oracle; NN(4 nests, p=2) equals NS of order 3^4-1 = 80."""
     import torch
 
     a = W.mimo_gram_device(262144, seed=1)
     x1, e1 = nnb.nn_batched(a, p=2, iters=4)
     x2, e2 = nnb.nn_batched(a, p=2, iters=4)
+    xs = nnb.ns_batched(a, 80)
     torch.cuda.synchronize()
     assert torch.equal(x1, x2) and torch.equal(e1, e2)
-    assert e1.max().item() < 1e-12
-    # spot-check 64 systems against torch's inverse
-    idx = torch.arange(0, 262144, 4096, device="cuda")
-    inv = torch.linalg.inv(a[idx])
-    rel = torch.linalg.norm(x1[idx] - inv, dim=(1, 2)) / torch.linalg.norm(inv, dim=(1, 2))
-    assert rel.max().item() < 1e-12
+    idx = torch.cat([torch.arange(0, 262144, 4096, device="cuda"), torch.topk(e1, 8).indices])
+    ah = a[idx].cpu().numpy()
+    xr, er = port.batched("nn", ah, 2, 4, threads=8)
+    xh = x1[idx].cpu().numpy()
+    assert max(rel_frob(xh[s], xr[s]) for s in range(len(ah))) < TOL_X
+    eps_close(e1[idx].cpu().numpy(), er)
+    # analytic equivalence NN == NS(80) holds to rounding even on the slowest systems
+    rel = torch.linalg.norm(x1 - xs, dim=(1, 2)) / torch.linalg.norm(xs, dim=(1, 2))
+    assert rel.max().item() < 1e-10
 
 
 # ----------------------------------------------------------------- sparse (C5)
