@@ -1,0 +1,67 @@
+"""Summarise ncu reports / launch lists into the numbers the roofline story uses.
+
+usage:
+  python tools/ncu_summary.py full  report.ncu-rep [...]      > profiles/rNN_ncu_full_summary.txt
+  python tools/ncu_summary.py launches launches.csv "<what ran>" > profiles/rNN_launches_summary.txt
+"""
+import csv
+import subprocess
+import sys
+from collections import defaultdict
+
+KEYS = [
+    ("Kernel Name", ""), ("launch__grid_size", ""), ("launch__block_size", ""),
+    ("launch__registers_per_thread", ""), ("gpu__time_duration.sum", ""),
+    ("dram__bytes_read.sum", ""), ("dram__bytes_write.sum", ""),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", ""),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe (DMMA) active"),
+    ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "DMMA issue"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 (DFMA) pipe"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", ""),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", ""),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", ""),
+    ("lts__t_bytes.sum", "L2 traffic"),
+    ("sm__cycles_elapsed.avg", ""), ("smsp__cycles_active.avg", ""),
+]
+
+
+def full(paths):
+    for path in paths:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(out.splitlines()))
+        hdr, units = rows[0], rows[1]
+        print(f"## {path.split('/')[-1]}")
+        for vals in rows[2:]:
+            for k, note in KEYS:
+                if k in hdr:
+                    i = hdr.index(k)
+                    print(f"  {k:<78} {vals[i]:>22} {units[i]:<10} {note}")
+            print()
+
+
+def launches(path, what):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    hdr = rows[hi]
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = defaultdict(lambda: [0, 0.0])
+    for r in rows[hi + 1:]:
+        if len(r) > vi:
+            scale = {"ns": 1.0, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6, "nsecond": 1.0}.get(r[ui], 1.0)
+            name = r[ki].split("(")[0][:80]
+            agg[name][0] += 1
+            agg[name][1] += float(r[vi].replace(",", "")) * scale
+    tot = sum(v for _, v in agg.values())
+    print("ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised launches)")
+    print(f"workload: {what}\n")
+    print(f"{'total ms':>10} {'share':>7} {'launches':>9}  kernel")
+    for k, (c, v) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        print(f"{v / 1e6:10.3f} {100 * v / tot:6.2f}% {c:9d}  {k}")
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "full":
+        full(sys.argv[2:])
+    else:
+        launches(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "")

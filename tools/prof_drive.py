@@ -1,0 +1,30 @@
+"""Small fixed workload for ncu captures: one dense nest (N=8192, p=2), one C2 batch,
+one C5 solve.  Run plainly first (must exit 0), then under ncu with the same arguments."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch
+
+import paper_2212_02406_b200 as nnb
+from paper_2212_02406_b200 import workloads as W
+
+which = sys.argv[1] if len(sys.argv) > 1 else "all"
+if which in ("all", "dense"):
+    a = torch.from_numpy(W.gram_shifted(8192, seed=1, shift=1.0)).cuda()
+    x = nnb.x0(a)
+    for _ in range(2):
+        x, rep = nnb.nn_chain(a, x, p=2, max_iters=1, final_residual=False)
+if which in ("all", "mimo"):
+    am = W.mimo_gram_device(262144, seed=1)
+    for _ in range(2):
+        xm, em = nnb.nn_batched(am, p=2, iters=4)
+if which in ("all", "sparse"):
+    rp, col, val = W.laplacian_5pt(4096)
+    dev = lambda v: torch.from_numpy(v).cuda()
+    csr = nnb.Csr(dev(rp), dev(col), dev(val), n=4096 * 4096, nnz=col.size)
+    b = dev(W.rhs(4096 * 4096, seed=7))
+    for _ in range(2):
+        xs, _ = nnb.solve_sparse_factorized(csr, b, 63, nnb.Normalization(theta=0.2, valid=True))
+torch.cuda.synchronize()
+print("prof_drive ok", which)
