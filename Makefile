@@ -14,7 +14,7 @@ build/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 
 $(PKG)/libnnb.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared $(OBJS) -o $@ -lcudart
+	$(NVCC) $(ARCH) -shared $(OBJS) -o $@ -lcudart -ldl
 
 oracle:
 	$(MAKE) -s -C oracle $(if $(wildcard /root/reference/proj/src/solver.cpp),all,lib/libnn_oracle.so)

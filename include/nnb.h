@@ -166,6 +166,35 @@ int nnb_sparse_factorized_d(const int64_t* row_ptr, const int32_t* col, const do
                             double theta, double* X_out, int64_t* spmv_count_out,
                             int32_t* fail_factor_out, void* stream);
 
+/* ---- row-sharded chain across GPUs (one process per GPU) ---------------- */
+/* rank g owns rows [row0_g, row0_g+rows_g) of A and X.  Per
+ * nest: ring all-gather of X (NCCL send/recv on a side stream) overlapped
+ * block by block with the K-split partial GEMMs of R_g = I_g − A_g·X, eps from
+ * the per-rank Σ‖R_g‖² gathered and summed in rank order (identical on every
+ * rank), ring all-gather of R overlapped with V_g = X_g + V_g·R (p×).
+ * Not in the reference (single-process). */
+typedef struct nnb_comm* nnb_comm_t;
+#define NNB_UNIQUE_ID_BYTES 128
+/* Partition used by the sharded entry points: blocks of whole 8-row units,
+ * balanced, rank order.  Pure host arithmetic (no device needed). */
+void nnb_partition_rows(int64_t n, int32_t world, int32_t rank, int64_t* row0, int64_t* rows);
+int nnb_comm_unique_id(void* id_out /* NNB_UNIQUE_ID_BYTES */);
+/* NCCL communicator on the calling thread's current CUDA device. */
+int nnb_comm_init(const void* id, int32_t world, int32_t rank, nnb_comm_t* comm_out);
+int nnb_comm_destroy(nnb_comm_t comm);
+/* A_rows / X0_rows / X_rows_out: this rank's rows_g × n block (row-major).
+ * X0 kinds: GIVEN, SCALED_IDENTITY, JACOBI, and TRANSPOSE_NORM (which
+ * gathers A to form the transposed block). */
+int nnb_nn_chain_sharded_d(nnb_comm_t comm, const double* A_rows, int64_t n,
+                           const double* X0_rows, const nnb_chain_config* cfg, double* X_rows_out,
+                           double* eps_hist, nnb_chain_result* result, void* stream);
+/* The same schedule with `world` virtual ranks executed by this process on
+ * this GPU (shared buffers replace the ring): validates the partition, the
+ * K-split accumulation and the rank-ordered eps on one device. */
+int nnb_nn_chain_sharded_emulated_d(const double* A, int64_t n, int32_t world, const double* X0,
+                                    const nnb_chain_config* cfg, double* X_out, double* eps_hist,
+                                    nnb_chain_result* result, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -108,6 +108,14 @@ _SIGS = {
     "nnb_spmv_block_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _dp, _dp], C.c_int),
     "nnb_sparse_factorized_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _i64, C.c_double, _dp, _dp, _dp,
                                  _dp], C.c_int),
+    "nnb_partition_rows": ([_i64, _i32, _i32, C.POINTER(_i64), C.POINTER(_i64)], None),
+    "nnb_comm_unique_id": ([_dp], C.c_int),
+    "nnb_comm_init": ([_dp, _i32, _i32, C.POINTER(C.c_void_p)], C.c_int),
+    "nnb_comm_destroy": ([C.c_void_p], C.c_int),
+    "nnb_nn_chain_sharded_d": ([C.c_void_p, _dp, _i64, _dp, C.POINTER(ChainConfig), _dp, _dp,
+                                C.POINTER(ChainResult), _dp], C.c_int),
+    "nnb_nn_chain_sharded_emulated_d": ([_dp, _i64, _i32, _dp, C.POINTER(ChainConfig), _dp, _dp,
+                                         C.POINTER(ChainResult), _dp], C.c_int),
 }
 
 _lib: Optional[C.CDLL] = None
@@ -430,6 +438,92 @@ def x0(a, kind: int = X0_TRANSPOSE_NORM, scale_: float = 1.0):
     out = _empty_like(a)
     _check(lib().nnb_x0_d(_ptr(a), a.shape[0], kind, scale_, _ptr(out), _stream(a)))
     return out
+
+
+# ------------------------------------------------------------ multi-GPU (C4)
+def partition_rows(n: int, world: int, rank: int) -> tuple[int, int]:
+    """(row0, rows) of `rank`'s block in the sharded chain (8-row units, balanced)."""
+    r0, rs = C.c_int64(), C.c_int64()
+    lib().nnb_partition_rows(n, world, rank, C.byref(r0), C.byref(rs))
+    return r0.value, rs.value
+
+
+class Comm:
+    """NCCL communicator owned by libnnb (one process per GPU)."""
+
+    def __init__(self, world: int, rank: int, unique_id: bytes):
+        self.world, self.rank = world, rank
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(lib().nnb_comm_init(C.addressof(buf), world, rank, C.byref(h)))
+        self.handle = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().nnb_comm_unique_id(C.addressof(buf)))
+        return buf.raw
+
+    @classmethod
+    def from_torch_distributed(cls):
+        """Rank 0 creates the NCCL id, torch.distributed broadcasts it (plumbing only)."""
+        import torch
+        import torch.distributed as dist
+
+        world, rank = dist.get_world_size(), dist.get_rank()
+        t = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(cls.unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        return cls(world, rank, bytes(t.cpu().numpy().tobytes()))
+
+    def close(self):
+        if self.handle:
+            lib().nnb_comm_destroy(self.handle)
+            self.handle = None
+
+
+def _sharded_report(hist, res, p, final_residual):
+    recorded = res.iters + (1 if final_residual or res.stopped == 0 else 0)
+    return ChainReport(history=[(k, float(hist[k])) for k in range(recorded)], iters=res.iters,
+                       stopped_reason="tolerance" if res.stopped == 0 else "max_nests", products=res.products,
+                       device_ms=res.device_ms, fail_iter=res.fail_iter, n3_multiplies=float(res.iters * (p + 1)),
+                       n2_ops=res.iters * (p + 1))
+
+
+def nn_chain_sharded(comm: Comm, a_rows, n: int, x0_rows=None, *, p: int, max_iters: int, tol: float = 0.0,
+                     x0_kind: Optional[int] = None, x0_scale: float = 1.0, final_residual: bool = True):
+    """Row-sharded chain: this rank's rows of A in, its rows of X out."""
+    a_rows = _prep(a_rows, False)
+    if x0_kind is None:
+        x0_kind = X0_GIVEN if x0_rows is not None else X0_TRANSPOSE_NORM
+    x0p = _prep(x0_rows, False) if x0_rows is not None else None
+    out = _empty_like(a_rows)
+    hist = np.zeros(max_iters + 1)
+    cfg = ChainConfig(p, max_iters, tol, ORDER_NORTHSTAR, x0_kind, x0_scale, int(final_residual))
+    res = ChainResult()
+    st = lib().nnb_nn_chain_sharded_d(comm.handle, _ptr(a_rows), n, _ptr(x0p), C.byref(cfg), _ptr(out),
+                                      hist.ctypes.data, C.byref(res), _stream(a_rows))
+    _check(st, res.fail_iter)
+    return out, _sharded_report(hist, res, p, final_residual)
+
+
+def nn_chain_sharded_emulated(a, world: int, x0=None, *, p: int, max_iters: int, tol: float = 0.0,
+                              x0_kind: Optional[int] = None, x0_scale: float = 1.0, final_residual: bool = True):
+    """The sharded schedule with `world` virtual ranks on this GPU (validation on one device)."""
+    a = _prep(a, False)
+    n = a.shape[0]
+    if x0_kind is None:
+        x0_kind = X0_GIVEN if x0 is not None else X0_TRANSPOSE_NORM
+    x0p = _prep(x0, False) if x0 is not None else None
+    out = _empty_like(a)
+    hist = np.zeros(max_iters + 1)
+    cfg = ChainConfig(p, max_iters, tol, ORDER_NORTHSTAR, x0_kind, x0_scale, int(final_residual))
+    res = ChainResult()
+    st = lib().nnb_nn_chain_sharded_emulated_d(_ptr(a), n, world, _ptr(x0p), C.byref(cfg), _ptr(out),
+                                               hist.ctypes.data, C.byref(res), _stream(a))
+    _check(st, res.fail_iter)
+    return out, _sharded_report(hist, res, p, final_residual)
 
 
 # ------------------------------------------------------------ batched (C2)

@@ -129,6 +129,7 @@ struct ChainOut {
   int products = 0;
   double last_eps = 0.0;
   float device_ms = 0.f;
+  int x_index = 0;  // sharded driver: which ping-pong buffer holds the final X
 };
 // Real chain on device buffers with ld == ldn (ldn even, >= n).  X holds X0
 // on entry and the final iterate on exit.  eps_hist host (nullable).

@@ -1,0 +1,554 @@
+// Row-sharded Nested Neumann chain across GPUs (BASELINE config 3:
+// N=32768 on 1/2/4/8 B200s) — SURVEY.md §8(e).
+//
+// Rank g owns the rows J_g = [row0_g, row0_g+rows_g) of A and X (8-row units,
+// balanced).  Per nest, with full-size ping-pong buffers XF[2] and RF:
+//   1. ring all-gather of X (NCCL send/recv on a side stream, G−1 steps);
+//      overlapped with the K-split product
+//        R_g = I_g − Σ_j A_g[:, J_j]·X_j,   own block first, then in ring order,
+//      each partial GEMM waiting only for the ring step that delivers X_j;
+//   2. eps = sqrt(Σ_g ‖R_g‖²)/√N with the per-rank partials all-gathered and
+//      summed in rank order (bit-identical on every rank → identical stop
+//      decisions), non-finite counts likewise;
+//   3. ring all-gather of R overlapped with V_g = X_g + Σ_j X_g[:, J_j]·R_j,
+//      then V_g = X_g + V_g·R (p−1 more) and X_{k+1, g} = V_g.
+// p+1 local (rows_g × N × N) products per nest, 2 ring all-gathers.
+// R_g is written straight into its slot of RF and the last Horner product
+// straight into XF[next], so the gathers move data in place.
+//
+// Emulation mode runs all `world` virtual ranks in this process on one GPU:
+// the buffers are shared, the ring is a no-op, and every other step (the
+// partition, the K-split accumulation order, the rank-ordered eps) is the
+// same code — that is how the partition logic is exercised on a 1-GPU box.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/nnb.h"
+#include "engine.cuh"
+
+namespace nnb {
+namespace {
+
+// ---- NCCL, loaded at first use (reuses torch's libnccl when already loaded) ----
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+#define LOAD(field, sym) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, sym))
+    LOAD(getUniqueId, "ncclGetUniqueId");
+    LOAD(commInitRank, "ncclCommInitRank");
+    LOAD(commDestroy, "ncclCommDestroy");
+    LOAD(send, "ncclSend");
+    LOAD(recv, "ncclRecv");
+    LOAD(allGather, "ncclAllGather");
+    LOAD(groupStart, "ncclGroupStart");
+    LOAD(groupEnd, "ncclGroupEnd");
+    LOAD(errorString, "ncclGetErrorString");
+#undef LOAD
+    api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.send && api.recv &&
+             api.allGather && api.groupStart && api.groupEnd && api.errorString;
+  });
+  return api;
+}
+
+#define NNB_NCCL(x)                                                                   \
+  do {                                                                                \
+    ncclResult_t _r = (x);                                                            \
+    if (_r != ncclSuccess)                                                            \
+      return fail(NNB_ERR_NCCL, std::string("NCCL error: ") + nccl().errorString(_r) + \
+                                    " in " #x);                                       \
+  } while (0)
+
+int64_t pad8(int64_t c) { return (c + 7) / 8 * 8; }
+
+__global__ void combine_ranks_kernel(const double* gathered, int world, double* eps_out,
+                                     int* nf_out, double scale) {
+  if (threadIdx.x == 0) {
+    double ss = 0.0, nf = 0.0;
+    for (int r = 0; r < world; ++r) {  // rank order: identical on every rank
+      ss += gathered[2 * r];
+      nf += gathered[2 * r + 1];
+    }
+    *eps_out = sqrt(ss) * scale;
+    *nf_out = static_cast<int>(nf);
+  }
+}
+
+__global__ void pack_pair_kernel(const double* ss, const int* nf, double* dst) {
+  if (threadIdx.x == 0) {
+    dst[0] = *ss;
+    dst[1] = static_cast<double>(*nf);
+  }
+}
+
+// X0 = diag(A)^-1 restricted to rows [row0, row0+rows): X[i][row0+i] = 1/A[i][row0+i].
+__global__ void jacobi_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t rows,
+                                   int64_t row0, int64_t n, double* __restrict__ X, int64_t ldx) {
+  const int64_t total = rows * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / n, c = idx % n;
+    X[r * ldx + c] = (row0 + r == c) ? 1.0 / A[r * lda + c] : 0.0;
+  }
+}
+
+}  // namespace
+}  // namespace nnb
+
+struct nnb_comm {
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0, device = 0;
+  cudaStream_t cs = nullptr;  // communication stream
+};
+
+namespace nnb {
+namespace {
+
+struct Shard {
+  int64_t n = 0, ld = 0;
+  int world = 1;
+  std::vector<int64_t> row0, rows;
+  nnb_comm* comm = nullptr;  // null => emulation
+  std::vector<int> local;    // ranks executed by this process
+  cudaStream_t s = nullptr;
+  std::vector<cudaEvent_t> ev;  // ev[q]: ring step q delivered its block
+  cudaEvent_t ready = nullptr;
+  RedWs red;
+};
+
+void partition(int64_t n, int world, std::vector<int64_t>& row0, std::vector<int64_t>& rows) {
+  const int64_t units = (n + 7) / 8;
+  row0.assign(world, 0);
+  rows.assign(world, 0);
+  int64_t u0 = 0;
+  for (int g = 0; g < world; ++g) {
+    const int64_t u = units / world + (g < units % world ? 1 : 0);
+    row0[g] = std::min<int64_t>(n, u0 * 8);
+    rows[g] = std::min<int64_t>(n, (u0 + u) * 8) - row0[g];
+    u0 += u;
+  }
+}
+
+// In-place ring all-gather of the row blocks of `full` (n × ld) on the comm
+// stream; ev[q] records after step q (block (me−q) mod G arrived).
+int ring_allgather(Shard& sh, double* full) {
+  if (!sh.comm || sh.world == 1) return 0;
+  auto& api = nccl();
+  const int G = sh.world, me = sh.comm->rank;
+  NNB_CUDA(cudaEventRecord(sh.ready, sh.s));
+  NNB_CUDA(cudaStreamWaitEvent(sh.comm->cs, sh.ready, 0));
+  for (int q = 1; q < G; ++q) {
+    const int send_blk = ((me - q + 1) % G + G) % G, recv_blk = ((me - q) % G + G) % G;
+    NNB_NCCL(api.groupStart());
+    NNB_NCCL(api.send(full + sh.row0[send_blk] * sh.ld, (size_t)(sh.rows[send_blk] * sh.ld),
+                      ncclDouble, (me + 1) % G, sh.comm->comm, sh.comm->cs));
+    NNB_NCCL(api.recv(full + sh.row0[recv_blk] * sh.ld, (size_t)(sh.rows[recv_blk] * sh.ld),
+                      ncclDouble, (me - 1 + G) % G, sh.comm->comm, sh.comm->cs));
+    NNB_NCCL(api.groupEnd());
+    NNB_CUDA(cudaEventRecord(sh.ev[q], sh.comm->cs));
+  }
+  return 0;
+}
+
+// C_g = alpha·Σ_j L[:, J_j]·F_j + beta·D + gamma·I(row0_g), K split by the
+// ranks' row blocks, own block first then ring order; the last partial
+// carries the Σ C² / non-finite reduction when ss_out != null.
+int ksplit_product(Shard& sh, int g, const double* L, int64_t ldl, const double* F, double alpha,
+                   const double* D, double beta, double gamma, double* C, int64_t ldc,
+                   bool wait_ring, double* ss_out, int* nf_out) {
+  const int G = sh.world;
+  int last = -1;  // the reduction rides on the last non-empty partial
+  for (int q = 0; q < G; ++q)
+    if (sh.rows[((g - q) % G + G) % G]) last = q;
+  for (int q = 0; q < G; ++q) {
+    const int j = ((g - q) % G + G) % G;
+    if (sh.rows[j] == 0) continue;
+    if (wait_ring && sh.comm && q > 0) NNB_CUDA(cudaStreamWaitEvent(sh.s, sh.ev[q], 0));
+    GemmOp op;
+    op.A = L + sh.row0[j];
+    op.lda = ldl;
+    op.B = F + sh.row0[j] * sh.ld;
+    op.ldb = sh.ld;
+    op.M = sh.rows[g];
+    op.N = sh.n;
+    op.K = sh.rows[j];
+    op.ep.C = C;
+    op.ep.ldc = ldc;
+    op.ep.alpha = alpha;
+    if (q == 0) {
+      op.ep.D = D;
+      op.ep.ldd = ldc;
+      op.ep.beta = beta;
+      op.ep.gamma = gamma;
+      op.ep.diag_offset = sh.row0[g];
+    } else {
+      op.ep.D = C;
+      op.ep.ldd = ldc;
+      op.ep.beta = 1.0;
+    }
+    const bool reduce = (last == q) && nf_out;
+    if (reduce) {
+      op.ep.ss_out = ss_out;
+      op.ep.nf_out = nf_out;
+    }
+    NNB_TRY(gemm(op, reduce ? &sh.red : nullptr, sh.s));
+  }
+  return 0;
+}
+
+int run_sharded(Shard& sh, const double* A_local, int64_t lda_rows_stride, bool a_full,
+                double* XF0, double* XF1, double* RF, double* Vbase, const ChainCfg& cfg,
+                double* eps_hist, ChainOut* out) {
+  const int G = sh.world, p = cfg.p;
+  const int64_t ld = sh.ld;
+  const int slots = cfg.max_iters + 1;
+  const double scale = 1.0 / std::sqrt(static_cast<double>(sh.n));
+  NNB_TRY(sh.red.init(max_tiles_for(sh.n, sh.n), sh.s));
+  DevBuf scal;
+  const size_t nf_count = (size_t)slots * (p + 1);
+  // per-rank [ss, nf] pairs, gathered pairs, eps history, nf history, temp scalars
+  NNB_TRY(scal.alloc(sizeof(double) * (2 * G + 2 * G + slots + 8) + sizeof(int) * (nf_count + 8 + G),
+                     sh.s));
+  NNB_CUDA(cudaMemsetAsync(scal.p, 0, scal.bytes, sh.s));
+  double* pairs = scal.as<double>();      // [2G] this process's per-rank pairs
+  double* gathered = pairs + 2 * G;       // [2G] all ranks' pairs
+  double* eps_dev = gathered + 2 * G;     // [slots]
+  double* ss_tmp = eps_dev + slots;       // [8]
+  int* nf_dev = reinterpret_cast<int*>(ss_tmp + 8);  // [nf_count]
+  int* nf_tmp = nf_dev + nf_count;        // [8 + G]
+
+  double* XF[2] = {XF0, XF1};
+  int cur = 0;
+  cudaEvent_t e0, e1;
+  NNB_CUDA(cudaEventCreate(&e0));
+  NNB_CUDA(cudaEventCreate(&e1));
+  NNB_CUDA(cudaEventRecord(e0, sh.s));
+
+  auto a_rows = [&](int g) -> const double* {
+    return a_full ? A_local + sh.row0[g] * lda_rows_stride : A_local;
+  };
+  auto vbuf = [&](int g, int which) -> double* {
+    // emulation: full-size V buffers sliced per rank; real: rows_g × ld buffers
+    const int64_t rows_total = a_full ? sh.n : sh.rows[g];
+    return Vbase + (size_t)which * rows_total * ld + (a_full ? sh.row0[g] * ld : 0);
+  };
+
+  std::vector<double> eps_h(slots, 0.0);
+  std::vector<int> nf_h(nf_count, 0);
+  int k = 0, products = 0, stopped = 1, recorded = 0;
+  for (;; ++k) {
+    const bool last = k >= cfg.max_iters;
+    if (last && !cfg.final_residual) break;
+    // ---- R_g = I_g − A_g·X (ring all-gather of X overlapped) ----
+    NNB_TRY(ring_allgather(sh, XF[cur]));
+    for (int g : sh.local) {
+      NNB_TRY(ksplit_product(sh, g, a_rows(g), lda_rows_stride, XF[cur], -1.0, nullptr, 0.0, 1.0,
+                             RF + sh.row0[g] * ld, ld, true, ss_tmp, nf_tmp));
+      pack_pair_kernel<<<1, 32, 0, sh.s>>>(ss_tmp, nf_tmp, pairs + 2 * g);
+      count_launch();
+    }
+    // ---- eps: per-rank pairs gathered, summed in rank order ----
+    if (sh.comm && G > 1) {
+      NNB_NCCL(nccl().allGather(pairs + 2 * sh.comm->rank, gathered, 2, ncclDouble, sh.comm->comm,
+                                sh.s));
+    } else {
+      NNB_CUDA(cudaMemcpyAsync(gathered, pairs, sizeof(double) * 2 * G, cudaMemcpyDeviceToDevice,
+                               sh.s));
+    }
+    combine_ranks_kernel<<<1, 32, 0, sh.s>>>(gathered, G, eps_dev + k, nf_dev + k * (p + 1), scale);
+    count_launch();
+    ++products;
+    recorded = k + 1;
+    if (cfg.tol > 0.0) {
+      NNB_CUDA(cudaMemcpyAsync(eps_h.data(), eps_dev, sizeof(double) * slots,
+                               cudaMemcpyDeviceToHost, sh.s));
+      NNB_CUDA(cudaMemcpyAsync(nf_h.data(), nf_dev, sizeof(int) * nf_count,
+                               cudaMemcpyDeviceToHost, sh.s));
+      NNB_CUDA(cudaStreamSynchronize(sh.s));
+      bool bad = false;
+      for (int q = 0; q <= k * (p + 1); ++q) bad |= nf_h[q] != 0;
+      if (bad) break;
+      if (eps_h[k] < cfg.tol) {
+        stopped = 0;
+        break;
+      }
+    }
+    if (last) break;
+    if (p == 0) continue;
+    // ---- Horner: V_g = X_g + V_g·R (ring all-gather of R overlapped with the first) ----
+    NNB_TRY(ring_allgather(sh, RF));
+    const int nxt = cur ^ 1;
+    for (int g : sh.local) {
+      const double* xg = XF[cur] + sh.row0[g] * ld;
+      const double* v = xg;
+      for (int j = 1; j <= p; ++j) {
+        double* dst = (j == p) ? XF[nxt] + sh.row0[g] * ld : vbuf(g, (j - 1) & 1);
+        // the nf of a Horner product on rank g is folded into slot j via nf_tmp[g]
+        NNB_TRY(ksplit_product(sh, g, v, ld, RF, 1.0, xg, 1.0, 0.0, dst, ld, j == 1, ss_tmp + 1,
+                               nf_tmp + 8 + g));
+        v = dst;
+      }
+    }
+    products += p;  // global N^3-equivalent products (each rank did its row share)
+    // fold this nest's Horner non-finite flags (all local ranks; gathered over ranks below)
+    for (int g : sh.local) {
+      pack_pair_kernel<<<1, 32, 0, sh.s>>>(ss_tmp + 1, nf_tmp + 8 + g, pairs + 2 * g);
+      count_launch();
+    }
+    if (sh.comm && G > 1) {
+      NNB_NCCL(nccl().allGather(pairs + 2 * sh.comm->rank, gathered, 2, ncclDouble, sh.comm->comm,
+                                sh.s));
+    } else {
+      NNB_CUDA(cudaMemcpyAsync(gathered, pairs, sizeof(double) * 2 * G, cudaMemcpyDeviceToDevice,
+                               sh.s));
+    }
+    combine_ranks_kernel<<<1, 32, 0, sh.s>>>(gathered, G, ss_tmp + 2, nf_dev + k * (p + 1) + p,
+                                             scale);
+    count_launch();
+    cur = nxt;
+  }
+  NNB_CUDA(cudaEventRecord(e1, sh.s));
+  NNB_CUDA(cudaMemcpyAsync(eps_h.data(), eps_dev, sizeof(double) * slots, cudaMemcpyDeviceToHost,
+                           sh.s));
+  NNB_CUDA(cudaMemcpyAsync(nf_h.data(), nf_dev, sizeof(int) * nf_count, cudaMemcpyDeviceToHost,
+                           sh.s));
+  NNB_CUDA(cudaStreamSynchronize(sh.s));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (eps_hist)
+    for (int q = 0; q < recorded; ++q) eps_hist[q] = eps_h[q];
+  out->iters = std::min(k, cfg.max_iters);
+  out->products = products;
+  out->stopped = stopped;
+  out->last_eps = recorded ? eps_h[recorded - 1] : 0.0;
+  out->device_ms = ms;
+  out->fail_iter = 0;
+  // the final iterate lives in XF[cur]; the caller copies it out
+  out->x_index = cur;
+  for (int kk = 0; kk <= out->iters && kk < slots; ++kk)
+    for (int j = 0; j <= p; ++j) {
+      if (!nf_h[kk * (p + 1) + j]) continue;
+      if (j == 0) return fail(NNB_ERR_DOMAIN, "sharded chain: residual product went non-finite at nest " + std::to_string(kk));
+      out->fail_iter = kk + 1;
+      return fail(NNB_ERR_DIVERGENCE, "sharded chain: non-finite iterate at nest " + std::to_string(kk + 1));
+    }
+  return 0;
+}
+
+}  // namespace
+}  // namespace nnb
+
+using namespace nnb;
+
+extern "C" {
+
+void nnb_partition_rows(int64_t n, int32_t world, int32_t rank, int64_t* row0, int64_t* rows) {
+  std::vector<int64_t> r0, rs;
+  partition(n, world < 1 ? 1 : world, r0, rs);
+  const int g = rank < 0 ? 0 : (rank >= world ? world - 1 : rank);
+  if (row0) *row0 = r0[g];
+  if (rows) *rows = rs[g];
+}
+
+int nnb_comm_unique_id(void* id_out) {
+  auto& api = nccl();
+  if (!api.ok) return fail(NNB_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  NNB_NCCL(api.getUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == NNB_UNIQUE_ID_BYTES, "unique id size");
+  std::memcpy(id_out, &id, sizeof(id));
+  return 0;
+}
+
+int nnb_comm_init(const void* id, int32_t world, int32_t rank, nnb_comm_t* comm_out) {
+  NNB_TRY(require_device());
+  auto& api = nccl();
+  if (!api.ok) return fail(NNB_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  if (world < 1 || rank < 0 || rank >= world) return fail(NNB_ERR_DOMAIN, "comm: bad rank/world");
+  auto* c = new nnb_comm();
+  c->world = world;
+  c->rank = rank;
+  cudaGetDevice(&c->device);
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  ncclResult_t r = api.commInitRank(&c->comm, world, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(NNB_ERR_NCCL, std::string("ncclCommInitRank: ") + api.errorString(r));
+  }
+  cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking);
+  *comm_out = c;
+  return 0;
+}
+
+int nnb_comm_destroy(nnb_comm_t comm) {
+  if (!comm) return 0;
+  if (comm->comm) nccl().commDestroy(comm->comm);
+  if (comm->cs) cudaStreamDestroy(comm->cs);
+  delete comm;
+  return 0;
+}
+
+static int chain_cfg_sharded(const nnb_chain_config* cfg, ChainCfg* c) {
+  if (!cfg) return fail(NNB_ERR_DOMAIN, "sharded chain: config is NULL");
+  if (cfg->depth_p < 0 || cfg->max_iters < 0) return fail(NNB_ERR_DOMAIN, "sharded chain: bad depth/budget");
+  c->p = cfg->depth_p;
+  c->max_iters = cfg->max_iters;
+  c->tol = cfg->tol;
+  c->order = cfg->order;
+  c->final_residual = cfg->final_residual;
+  return 0;
+}
+
+static void fill(nnb_chain_result* r, const ChainOut& o) {
+  if (!r) return;
+  r->iters = o.iters;
+  r->fail_iter = o.fail_iter;
+  r->stopped = o.stopped;
+  r->products = o.products;
+  r->last_eps = o.last_eps;
+  r->device_ms = o.device_ms;
+}
+
+int nnb_nn_chain_sharded_d(nnb_comm_t comm, const double* A_rows, int64_t n, const double* X0_rows,
+                           const nnb_chain_config* cfg, double* X_rows_out, double* eps_hist,
+                           nnb_chain_result* result, void* stream) {
+  NNB_TRY(require_device());
+  if (!comm) return fail(NNB_ERR_DOMAIN, "sharded chain: comm is NULL");
+  if (n < 1) return fail(NNB_ERR_SHAPE, "sharded chain: n must be >= 1");
+  ChainCfg c;
+  NNB_TRY(chain_cfg_sharded(cfg, &c));
+  if (cfg->order != NNB_ORDER_NORTHSTAR)
+    return fail(NNB_ERR_DOMAIN, "sharded chain: only the row-sharded NORTHSTAR order is supported");
+  Shard sh;
+  sh.n = n;
+  sh.ld = pad8(n);
+  sh.world = comm->world;
+  sh.comm = comm;
+  sh.local = {comm->rank};
+  sh.s = resolve(stream);
+  partition(n, sh.world, sh.row0, sh.rows);
+  const int me = comm->rank;
+  const int64_t ld = sh.ld, rows = sh.rows[me], row0 = sh.row0[me];
+  sh.ev.resize(sh.world);
+  for (auto& e : sh.ev) NNB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  NNB_CUDA(cudaEventCreateWithFlags(&sh.ready, cudaEventDisableTiming));
+
+  DevBuf big;  // A_g | XF0 | XF1 | RF | V0 | V1
+  const size_t full = (size_t)n * ld, blk = (size_t)std::max<int64_t>(rows, 1) * ld;
+  NNB_TRY(big.alloc(sizeof(double) * (3 * full + 3 * blk), sh.s));
+  double* Ag = big.as<double>();
+  double* XF0 = Ag + blk;
+  double* XF1 = XF0 + full;
+  double* RF = XF1 + full;
+  double* V = RF + full;
+  if (rows)
+    NNB_CUDA(cudaMemcpy2DAsync(Ag, ld * 8, A_rows, n * 8, n * 8, rows, cudaMemcpyDefault, sh.s));
+  double* Xg = XF0 + row0 * ld;
+  switch (cfg->x0_kind) {
+    case NNB_X0_GIVEN:
+      if (!X0_rows) return fail(NNB_ERR_DOMAIN, "sharded chain: X0 required");
+      if (rows)
+        NNB_CUDA(cudaMemcpy2DAsync(Xg, ld * 8, X0_rows, n * 8, n * 8, rows, cudaMemcpyDefault, sh.s));
+      break;
+    case NNB_X0_SCALED_IDENTITY:
+      NNB_TRY(axpby(0.0, Xg, ld, 0.0, nullptr, 0, cfg->x0_scale, row0, Xg, ld, rows, n, sh.s));
+      break;
+    case NNB_X0_JACOBI:
+      jacobi_rows_kernel<<<1184, 256, 0, sh.s>>>(Ag, ld, rows, row0, n, Xg, ld);
+      count_launch();
+      break;
+    case NNB_X0_TRANSPOSE_NORM: {
+      // gather A into RF (free before the first nest), build the full X0 in XF1, keep our rows
+      NNB_TRY(copy2d(Ag, ld, RF + row0 * ld, ld, rows, n, sh.s));
+      NNB_TRY(ring_allgather(sh, RF));
+      if (sh.world > 1) NNB_CUDA(cudaStreamWaitEvent(sh.s, sh.ev[sh.world - 1], 0));
+      NNB_TRY(x0_build(RF, ld, n, NNB_X0_TRANSPOSE_NORM, 1.0, XF1, ld, sh.s));
+      NNB_TRY(copy2d(XF1 + row0 * ld, ld, Xg, ld, rows, n, sh.s));
+      break;
+    }
+    default:
+      return fail(NNB_ERR_DOMAIN, "sharded chain: unknown X0 kind");
+  }
+  ChainOut o;
+  const int st = run_sharded(sh, Ag, ld, false, XF0, XF1, RF, V, c, eps_hist, &o);
+  fill(result, o);
+  for (auto& e : sh.ev) cudaEventDestroy(e);
+  cudaEventDestroy(sh.ready);
+  if (st != 0 && st != NNB_ERR_DIVERGENCE && st != NNB_ERR_DOMAIN) return st;
+  double* xf = o.x_index ? XF1 : XF0;
+  if (rows)
+    NNB_CUDA(cudaMemcpy2DAsync(X_rows_out, n * 8, xf + row0 * ld, ld * 8, n * 8, rows,
+                               cudaMemcpyDefault, sh.s));
+  NNB_CUDA(cudaStreamSynchronize(sh.s));
+  return st;
+}
+
+int nnb_nn_chain_sharded_emulated_d(const double* A, int64_t n, int32_t world, const double* X0,
+                                    const nnb_chain_config* cfg, double* X_out, double* eps_hist,
+                                    nnb_chain_result* result, void* stream) {
+  NNB_TRY(require_device());
+  if (n < 1 || world < 1) return fail(NNB_ERR_SHAPE, "sharded emulation: bad n/world");
+  ChainCfg c;
+  NNB_TRY(chain_cfg_sharded(cfg, &c));
+  if (cfg->order != NNB_ORDER_NORTHSTAR)
+    return fail(NNB_ERR_DOMAIN, "sharded chain: only the row-sharded NORTHSTAR order is supported");
+  Shard sh;
+  sh.n = n;
+  sh.ld = pad8(n);
+  sh.world = world;
+  sh.s = resolve(stream);
+  partition(n, world, sh.row0, sh.rows);
+  for (int g = 0; g < world; ++g) sh.local.push_back(g);
+  sh.ev.resize(world);
+  const int64_t ld = sh.ld;
+  const size_t full = (size_t)n * ld;
+  DevBuf big;  // A | XF0 | XF1 | RF | V0 | V1 (full-size, sliced per virtual rank)
+  NNB_TRY(big.alloc(sizeof(double) * 6 * full, sh.s));
+  double* Af = big.as<double>();
+  double* XF0 = Af + full;
+  double* XF1 = XF0 + full;
+  double* RF = XF1 + full;
+  double* V = RF + full;
+  NNB_CUDA(cudaMemcpy2DAsync(Af, ld * 8, A, n * 8, n * 8, n, cudaMemcpyDefault, sh.s));
+  if (cfg->x0_kind == NNB_X0_GIVEN) {
+    if (!X0) return fail(NNB_ERR_DOMAIN, "sharded emulation: X0 required");
+    NNB_CUDA(cudaMemcpy2DAsync(XF0, ld * 8, X0, n * 8, n * 8, n, cudaMemcpyDefault, sh.s));
+  } else {
+    NNB_TRY(x0_build(Af, ld, n, cfg->x0_kind, cfg->x0_scale, XF0, ld, sh.s));
+  }
+  ChainOut o;
+  const int st = run_sharded(sh, Af, ld, true, XF0, XF1, RF, V, c, eps_hist, &o);
+  fill(result, o);
+  if (st != 0 && st != NNB_ERR_DIVERGENCE && st != NNB_ERR_DOMAIN) return st;
+  NNB_CUDA(cudaMemcpy2DAsync(X_out, n * 8, o.x_index ? XF1 : XF0, ld * 8, n * 8, n,
+                             cudaMemcpyDefault, sh.s));
+  NNB_CUDA(cudaStreamSynchronize(sh.s));
+  return st;
+}
+
+}  // extern "C"

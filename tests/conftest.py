@@ -25,9 +25,13 @@ def rel_frob(a, b) -> float:
 
 @pytest.fixture(scope="session")
 def port():
+    import os
+
     from oracle import Port
 
-    return Port()
+    p = Port()
+    p.set_threads(os.cpu_count() or 1)  # row-partitioned like the reference; bit-identical for any count
+    return p
 
 
 @pytest.fixture(scope="session")

@@ -1,0 +1,66 @@
+"""Row-sharded chain (config 3 path) on the GPU: the emulated multi-rank schedule
+(virtual ranks on one device) and the real NCCL path at world size 1."""
+import numpy as np
+import pytest
+
+from conftest import rel_frob
+
+pytestmark = pytest.mark.gpu
+nnb = pytest.importorskip("paper_2212_02406_b200")
+from paper_2212_02406_b200 import workloads as W  # noqa: E402
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_emulated_sharded_matches_single_gpu_and_oracle(port, world):
+    n = 1000  # ragged: 125 8-row units over 3 or 8 ranks
+    a = W.gram_shifted(n, seed=3, shift=1.0)
+    x1, r1 = nnb.nn_chain(a, None, p=2, max_iters=8)
+    xs, rs = nnb.nn_chain_sharded_emulated(a, world, None, p=2, max_iters=8)
+    assert rs.iters == r1.iters == 8 and rs.products == r1.products
+    assert rel_frob(xs, x1) < 1e-12
+    e1 = np.array([e for _, e in r1.history])
+    es = np.array([e for _, e in rs.history])
+    assert np.allclose(es, e1, rtol=1e-10, atol=1e-15)
+    if world in (1, 3):  # oracle cross-check at a CPU-friendly size
+        a2 = W.gram_shifted(264, seed=3, shift=1.0)
+        xs2, _ = nnb.nn_chain_sharded_emulated(a2, world, None, p=2, max_iters=8)
+        xr, hr, _ = port.chain(a2, W.x0_transpose_norm(a2), 2, 8)
+        assert rel_frob(xs2, xr.real) < 1e-10
+
+
+def test_emulated_sharded_tolerance_stop(ref):
+    a = W.spd_conditioned(256, 1e3, seed=5)
+    x0 = W.x0_transpose_norm(a)
+    xr, hr, ir, _ = ref.chain(a, x0, 2, 60, tol=1e-12)
+    xs, rs = nnb.nn_chain_sharded_emulated(a, 4, None, p=2, max_iters=60, tol=1e-12)
+    assert rs.iters == ir and rs.stopped_reason == "tolerance"
+    assert rel_frob(xs, xr.real) < 1e-10
+
+
+@pytest.mark.parametrize("kind", [nnb.X0_TRANSPOSE_NORM, nnb.X0_JACOBI, nnb.X0_SCALED_IDENTITY])
+def test_nccl_world1_matches_single_gpu(kind):
+    import torch
+
+    # strongly diagonally dominant so that the Jacobi start contracts too
+    a = W.gram_shifted(512, seed=4, shift=40.0)
+    comm = nnb.Comm(1, 0, nnb.Comm.unique_id())
+    try:
+        scale = 1.0 / np.abs(a).sum(axis=1).max()
+        xs, rs = nnb.nn_chain_sharded(comm, a, 512, None, p=2, max_iters=10, x0_kind=kind, x0_scale=scale)
+        x1, r1 = nnb.nn_chain(a, None, p=2, max_iters=10, x0_kind=kind, x0_scale=scale)
+        assert rel_frob(xs, x1) < 1e-12
+        assert np.allclose([e for _, e in rs.history], [e for _, e in r1.history], rtol=1e-10, atol=1e-15)
+        # device-resident rows, as bench.py uses them
+        ad = torch.from_numpy(a).cuda()
+        xd, rd = nnb.nn_chain_sharded(comm, ad, 512, None, p=2, max_iters=10, x0_kind=kind, x0_scale=scale)
+        torch.cuda.synchronize()
+        assert rel_frob(xd.cpu().numpy(), x1) < 1e-12
+    finally:
+        comm.close()
+
+
+def test_sharded_divergence_reported():
+    a = W.gram_shifted(64, seed=1, shift=1.0)
+    with pytest.raises(nnb.DivergenceError) as e:
+        nnb.nn_chain_sharded_emulated(a, 2, None, p=2, max_iters=30, x0_kind=nnb.X0_SCALED_IDENTITY, x0_scale=1e160)
+    assert e.value.nest_index >= 1
