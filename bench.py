@@ -164,17 +164,45 @@ def dense_inputs(n: int, seed: int):
     return a
 
 
+def dense_rows(n: int, seed: int, row0: int, rows: int):
+    """Rows [row0, row0+rows) of A = B·B^T/N + I (B regenerated identically on every rank)."""
+    import torch
+
+    import paper_2212_02406_b200 as nnb
+
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    b = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
+    bt = b.t().contiguous()
+    bg = b[row0:row0 + rows].contiguous()
+    del b
+    a = nnb.matmul(bg, bt)
+    del bt, bg
+    a = nnb.scale(a, 1.0 / n)
+    idx = torch.arange(rows, device="cuda")
+    a[idx, idx + row0] += 1.0
+    torch.cuda.synchronize()
+    return a
+
+
 def run_dense(args, world, rank):
     import torch
 
     import paper_2212_02406_b200 as nnb
 
     n, p = args.n, args.p
-    a = dense_inputs(n, seed=2212)
-    x = nnb.x0(a)  # A^T/(|A|_1 |A|_inf) on device
+    flops_step = (p + 1) * 2.0 * n ** 3  # whole-job work of one nest (strong scaling)
+    if world > 1:
+        comm = nnb.Comm.from_torch_distributed()
+        row0, rows = nnb.partition_rows(n, world, rank)
+        a = dense_rows(n, 2212, row0, rows)
+        # X0 = A^T/(|A|_1|A|_inf) (A symmetric), built by the sharded driver's first call
+        x, _ = nnb.nn_chain_sharded(comm, a, n, None, p=p, max_iters=0, x0_kind=nnb.X0_TRANSPOSE_NORM)
+        step = lambda xx: nnb.nn_chain_sharded(comm, a, n, xx, p=p, max_iters=1, final_residual=False)
+    else:
+        a = dense_inputs(n, seed=2212)
+        x = nnb.x0(a)  # A^T/(|A|_1 |A|_inf) on device
+        step = lambda xx: nnb.nn_chain(a, xx, p=p, max_iters=1, final_residual=False)
     torch.cuda.synchronize()
-    flops_step = (p + 1) * 2.0 * n ** 3
-    step = lambda xx: nnb.nn_chain(a, xx, p=p, max_iters=1, final_residual=False)
     for _ in range(args.warmup):
         x, rep = step(x)
     torch.cuda.synchronize()
@@ -196,37 +224,48 @@ def run_dense(args, world, rank):
     ms = max_over_ranks(world, e0.elapsed_time(e1))
     barrier(world)
     ms_step = ms / args.steps
-    value = sum_over_ranks(world, flops_step * args.steps) / (ms * 1e-3) / 1e12
-    # dominant kernel: the fused DMMA GEMM — the chain's device time is (p+1) GEMM launches per step
-    gemm_ms = statistics.mean(lib_ms) / (p + 1)
-    achieved = 2.0 * n ** 3 / (gemm_ms * 1e-3) / 1e12
+    value = flops_step * args.steps / (ms * 1e-3) / 1e12  # whole job: one N^3 nest per step
+    # dominant kernel: the fused DMMA GEMM — the library's device time of a nest is its
+    # (p+1) GEMM launches (per rank: its row share of each product)
+    dev_ms = statistics.mean(lib_ms)
+    achieved = flops_step / world / (dev_ms * 1e-3) / 1e12
+    rows_here = nnb.partition_rows(n, world, rank)[1] if world > 1 else n
     out = dict(value=value, ms_per_step=ms_step, launches=launches, clocks=clk.summary(),
                eps_first=eps[0], eps_last=eps[-1],
                roofline={"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": None,
                          "kernel": "gemm_f64_kernel<128x128x16, 2x4 warps, 4 stages> (DMMA.8x8x4 + TMA)",
-                         "per_launch": f"2N^3 = {2.0 * n ** 3:.4g} flop, N={n}",
+                         "per_launch": f"2*rows*N^2 = {2.0 * rows_here * n * n:.4g} flop (rows={rows_here}, N={n}), "
+                                       f"{p + 1} launches per nest" + (f" x {world} K-split partials" if world > 1 else ""),
                          "peak_source": FP64_PEAK_SOURCE})
     # e2e through the C-ABI with HOST buffers (pinned): H2D of A and X, one nest, D2H of X
     if args.e2e:
-        a_h = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-        x_h = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-        xo_h = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        shape = tuple(a.shape)
+        a_h = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+        x_h = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+        xo_h = torch.empty(shape, dtype=torch.float64, pin_memory=True)
         a_h.copy_(a)
         x_h.copy_(x)
-        del a
+        del a, x
         torch.cuda.empty_cache()
         a_np, x_np, xo_np = a_h.numpy(), x_h.numpy(), xo_h.numpy()
-        nnb.nn_chain(a_np, x_np, p=p, max_iters=1, final_residual=False)  # warm staging path
+        if world > 1:
+            call = lambda: nnb.nn_chain_sharded(comm, a_np, n, x_np, p=p, max_iters=1, final_residual=False, out=xo_np)
+        else:
+            call = lambda: nnb.nn_chain(a_np, x_np, p=p, max_iters=1, final_residual=False, out=xo_np)
+        call()  # warm the staging path
         barrier(world)
         t0 = time.perf_counter()
         k_e2e = max(1, min(args.steps, 3))
         for _ in range(k_e2e):
-            xo, _ = nnb.nn_chain(a_np, x_np, p=p, max_iters=1, final_residual=False)
+            call()
         t = max_over_ranks(world, time.perf_counter() - t0)
-        out["e2e"] = {"value": round(sum_over_ranks(world, flops_step * k_e2e) / t / 1e12, 3), "unit": "TFLOP/s",
-                      "h2d_bytes_per_step": 2 * 8 * n * n, "d2h_bytes_per_step": 8 * n * n,
-                      "path": "nnb_nn_chain_d with pinned host A, X0, X_out"}
+        out["e2e"] = {"value": round(flops_step * k_e2e / t / 1e12, 3), "unit": "TFLOP/s",
+                      "h2d_bytes_per_step": 2 * 8 * shape[0] * n * world, "d2h_bytes_per_step": 8 * shape[0] * n * world,
+                      "path": ("nnb_nn_chain_sharded_d" if world > 1 else "nnb_nn_chain_d")
+                              + " with pinned host A, X0 and X_out"}
+    if world > 1:
+        comm.close()
     return out
 
 
@@ -298,15 +337,17 @@ def run_mimo(args, world, rank):
                              "speedup_nn_over_ns": round(ms_ns / ms, 3)},
            "accuracy": {"nn_max_rel_err": rel(x), "ns80_max_rel_err": rel(xs), "eps_max": eps.max().item()}}
     if args.e2e:
-        a_h = a.cpu().numpy()
-        x_np = np.empty_like(a_h)
-        nnb.nn_batched(a_h, p=2, iters=4, want_eps=False)
+        a_h = torch.empty(tuple(a.shape), dtype=torch.complex128, pin_memory=True)
+        x_h = torch.empty(tuple(a.shape), dtype=torch.complex128, pin_memory=True)
+        a_h.copy_(a)
+        a_np, x_np = a_h.numpy(), x_h.numpy()
+        nnb.nn_batched(a_np, p=2, iters=4, want_eps=False, out=x_np)
         t0 = time.perf_counter()
         for _ in range(3):
-            nnb.nn_batched(a_h, p=2, iters=4, want_eps=False)
+            nnb.nn_batched(a_np, p=2, iters=4, want_eps=False, out=x_np)
         t = (time.perf_counter() - t0) / 3
         out["e2e"] = {"value": round(batch / t, 1), "unit": "inversions/s", "h2d_bytes_per_step": batch * 4096,
-                      "d2h_bytes_per_step": batch * 4096, "path": "nnb_nn_batched_z with pageable host A, X"}
+                      "d2h_bytes_per_step": batch * 4096, "path": "nnb_nn_batched_z with pinned host A and X"}
     return out
 
 
@@ -385,8 +426,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=32768)
-    ap.add_argument("--p", type=int, default=2)
+    ap.add_argument("--matrix-n", dest="n", type=int, default=32768)
+    ap.add_argument("--depth", dest="p", type=int, default=2)
     ap.add_argument("--mimo-batch", type=int, default=262144)
     ap.add_argument("--grid", type=int, default=4096)
     ap.add_argument("--legs", default="dense,mimo,sparse")
@@ -401,11 +442,14 @@ def main():
                           f"(A=B·B^T/N+I, X0=A^T/(|A|_1|A|_inf))",
               "n": args.n, "depth_p": args.p, "products_per_step": args.p + 1,
               "l2": "inputs (8*N^2 bytes per matrix) exceed the 126 MB L2; no flush",
-              "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+              "parallelism": f"row-sharded x{world} (NCCL ring all-gather overlapped with K-split GEMMs)"
+                             if world > 1 else "single GPU",
               "host_cpu": f"{cores} x {model}"}
     base = {"metric": "NN inversion FP64 TFLOP/s", "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded)", "config": config}
+    if world > 1:
+        base["scaling"] = "strong"  # the N=32768 matrix is fixed; ranks split its rows
 
     if args.impl == "reference":
         if rank != 0:

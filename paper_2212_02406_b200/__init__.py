@@ -366,7 +366,7 @@ class ChainReport:
 
 
 def nn_chain(a, x0=None, *, p: int, max_iters: int, tol: float = 0.0, order: int = ORDER_NORTHSTAR,
-             x0_kind: Optional[int] = None, x0_scale: float = 1.0, final_residual: bool = True):
+             x0_kind: Optional[int] = None, x0_scale: float = 1.0, final_residual: bool = True, out=None):
     """Nested Neumann chain from X0; returns (X, ChainReport).
 
     eps is recorded before every nest and after the last one; stops when
@@ -380,7 +380,7 @@ def nn_chain(a, x0=None, *, p: int, max_iters: int, tol: float = 0.0, order: int
     if x0_kind is None:
         x0_kind = X0_GIVEN if x0 is not None else X0_TRANSPOSE_NORM
     x0p = _prep(x0, z) if x0 is not None else None
-    out = _empty_like(a)
+    out = _empty_like(a) if out is None else out
     hist = np.zeros(max_iters + 1)
     cfg = ChainConfig(p, max_iters, tol, order, x0_kind, x0_scale, int(final_residual))
     res = ChainResult()
@@ -492,13 +492,13 @@ def _sharded_report(hist, res, p, final_residual):
 
 
 def nn_chain_sharded(comm: Comm, a_rows, n: int, x0_rows=None, *, p: int, max_iters: int, tol: float = 0.0,
-                     x0_kind: Optional[int] = None, x0_scale: float = 1.0, final_residual: bool = True):
+                     x0_kind: Optional[int] = None, x0_scale: float = 1.0, final_residual: bool = True, out=None):
     """Row-sharded chain: this rank's rows of A in, its rows of X out."""
     a_rows = _prep(a_rows, False)
     if x0_kind is None:
         x0_kind = X0_GIVEN if x0_rows is not None else X0_TRANSPOSE_NORM
     x0p = _prep(x0_rows, False) if x0_rows is not None else None
-    out = _empty_like(a_rows)
+    out = _empty_like(a_rows) if out is None else out
     hist = np.zeros(max_iters + 1)
     cfg = ChainConfig(p, max_iters, tol, ORDER_NORTHSTAR, x0_kind, x0_scale, int(final_residual))
     res = ChainResult()
@@ -527,11 +527,11 @@ def nn_chain_sharded_emulated(a, world: int, x0=None, *, p: int, max_iters: int,
 
 
 # ------------------------------------------------------------ batched (C2)
-def nn_batched(a, p: int = 2, iters: int = 4, want_eps: bool = True):
+def nn_batched(a, p: int = 2, iters: int = 4, want_eps: bool = True, out=None):
     """Batched 16×16 complex NN inversion with Jacobi X0; returns (X, eps_last)."""
     a = _prep(a, True)
     b, n = a.shape[0], a.shape[1]
-    out = _empty_like(a)
+    out = _empty_like(a) if out is None else out
     eps = None
     if want_eps:
         if _is_torch(a):
