@@ -7,7 +7,7 @@ SRCS    := $(wildcard $(PKG)/csrc/*.cu)
 HDRS    := $(wildcard $(PKG)/csrc/*.cuh) include/nnb.h
 OBJS    := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
 
-all: $(PKG)/libnnb.so oracle
+all: $(PKG)/libnnb.so oracle dropin
 
 build/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p build
@@ -24,3 +24,16 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean
+
+# C++ drop-in surface (namespace nn) over libnnb, and its test executable
+DROPIN_INC := -I$(PKG)/dropin/include -Iinclude
+$(PKG)/libnn_b200.so: $(PKG)/dropin/src/dropin.cpp $(wildcard $(PKG)/dropin/include/nn/*.hpp) include/nnb.h $(PKG)/libnnb.so
+	g++ -O2 -std=c++20 -fPIC -shared $(DROPIN_INC) $(PKG)/dropin/src/dropin.cpp -o $@ \
+	    -L$(PKG) -lnnb -Wl,-rpath,'$$ORIGIN'
+
+build/test_dropin: tests/cpp/test_dropin.cpp $(PKG)/libnn_b200.so
+	@mkdir -p build
+	g++ -O2 -std=c++20 $(DROPIN_INC) $< -o $@ -L$(PKG) -lnn_b200 -lnnb -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+dropin: $(PKG)/libnn_b200.so build/test_dropin
+.PHONY: dropin

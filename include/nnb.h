@@ -166,6 +166,20 @@ int nnb_sparse_factorized_d(const int64_t* row_ptr, const int32_t* col, const do
                             double theta, double* X_out, int64_t* spmv_count_out,
                             int32_t* fail_factor_out, void* stream);
 
+/* ---- contraction measurement (theta_trace's spectral estimate) ---------- */
+/* Power iteration on M^H M from the unit probe v0 (complex128, length n):
+ * nn::spectral_norm_estimate (proj/include/nn/kernels.hpp:51-53,
+ * proj/src/kernels.cpp:244-269).  M complex128 n×n, host or device. */
+int nnb_spectral_norm_z(const double* M, int64_t n, const double* v0, double tol,
+                        int32_t max_iters, double* value, int32_t* converged, int32_t* iterations,
+                        void* stream);
+/* The same for the matrix-free shifted operator I − theta·W, W real CSR
+ * (symmetric): nn::spectral_norm_estimate_shifted (kernels.hpp:57-61). */
+int nnb_spectral_norm_shifted_csr(const int64_t* row_ptr, const int32_t* col, const double* val,
+                                  int64_t n, int64_t nnz, double theta, const double* v0,
+                                  double tol, int32_t max_iters, double* value,
+                                  int32_t* converged, int32_t* iterations, void* stream);
+
 /* ---- row-sharded chain across GPUs (one process per GPU) ---------------- */
 /* rank g owns rows [row0_g, row0_g+rows_g) of A and X.  Per
  * nest: ring all-gather of X (NCCL send/recv on a side stream) overlapped

@@ -1,0 +1,4 @@
+#pragma once
+// Drop-in header name of /root/reference/proj/include/nn/rng.hpp; the B200
+// declarations live in nnb_dropin.hpp.
+#include "nn/nnb_dropin.hpp"

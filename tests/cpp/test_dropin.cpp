@@ -1,0 +1,348 @@
+// Drop-in API tests: the reference's hot-path unit tests (proj/tests/test_solver.cpp,
+// test_matrix_core.cpp, test_factorized.cpp, test_preconditioning.cpp) restated
+// against the nn:: drop-in (every matrix op on the GPU through libnnb).
+//   ./test_dropin            all tests (needs a GPU)
+//   ./test_dropin --host     host-only checks (GaussianStream, CSR build, BigInt, formulas)
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "nn/factorized.hpp"
+#include "nn/kernels.hpp"
+#include "nn/normalization.hpp"
+#include "nn/rng.hpp"
+#include "nn/solver.hpp"
+
+using namespace nn;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(c)                                                              \
+  do {                                                                        \
+    ++g_checks;                                                               \
+    if (!(c)) {                                                               \
+      ++g_fail;                                                               \
+      std::printf("  FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);              \
+    }                                                                         \
+  } while (0)
+#define CHECK_THROWS(expr, Type)                                              \
+  do {                                                                        \
+    ++g_checks;                                                               \
+    bool ok_ = false;                                                         \
+    try { (void)(expr); } catch (const Type&) { ok_ = true; } catch (...) {}  \
+    if (!ok_) { ++g_fail; std::printf("  FAIL %s:%d: %s did not throw %s\n", __FILE__, __LINE__, #expr, #Type); } \
+  } while (0)
+
+static double rel(const DenseMatrix& a, const DenseMatrix& b) {
+  double d = 0, n = 0;
+  for (std::size_t i = 0; i < a.size(); ++i) {
+    d += std::norm(a.data()[i] - b.data()[i]);
+    n += std::norm(b.data()[i]);
+  }
+  return n > 0 ? std::sqrt(d / n) : std::sqrt(d);
+}
+
+static DenseMatrix gauss(std::size_t r, std::size_t c, std::uint64_t seed, bool cplx = false) {
+  GaussianStream g(seed);
+  DenseMatrix m(r, c);
+  for (auto& v : m.data()) {
+    const double re = g.next();
+    v = Scalar{re, cplx ? g.next() : 0.0};
+  }
+  return m;
+}
+
+// SPD test matrix B·B^T/n + shift·I (the reference's random_spd is out of scope)
+static DenseMatrix spd(std::size_t n, double shift, std::uint64_t seed) {
+  DenseMatrix b = gauss(n, n, seed);
+  DenseMatrix bt(n, n);
+  for (std::size_t i = 0; i < n; ++i)
+    for (std::size_t j = 0; j < n; ++j) bt(j, i) = b(i, j);
+  DenseMatrix a = scale(matmul(b, bt), Scalar{1.0 / n, 0});
+  for (std::size_t i = 0; i < n; ++i) a(i, i) += shift;
+  for (std::size_t i = 0; i < n; ++i)
+    for (std::size_t j = i + 1; j < n; ++j) a(j, i) = a(i, j);
+  return a;
+}
+
+static DenseMatrix normalized(std::size_t n, double shift, std::uint64_t seed) {
+  const DenseMatrix w = spd(n, shift, seed);
+  return normalize(w, theta_trace(w));
+}
+
+static DenseMatrix s1(double v) { return DenseMatrix::diagonal({Scalar{v, 0}}); }
+
+static void host_tests() {
+  // GaussianStream: mt19937_64 + Box-Muller (values printed for the pytest cross-check)
+  GaussianStream g(42);
+  std::printf("gaussian42:");
+  for (int i = 0; i < 6; ++i) std::printf(" %.17g", g.next());
+  std::printf("\n");
+  // CSR canonicalisation (proj/tests/test_matrix_core.cpp:275-290)
+  const SparseMatrixCsr m = SparseMatrixCsr::build(
+      2, 3, {{1, 2, Scalar{5, 0}}, {0, 1, Scalar{2, 0}}, {0, 1, Scalar{-2, 0}}, {1, 0, Scalar{1, 0}}, {1, 2, Scalar{3, 0}}});
+  CHECK(m.nnz() == 2);
+  CHECK((m.row_ptr() == std::vector<std::size_t>{0, 0, 2}));
+  CHECK((m.col_idx() == std::vector<std::size_t>{0, 2}));
+  CHECK(m.values()[1] == (Scalar{8, 0}));
+  CHECK_THROWS(SparseMatrixCsr::build(2, 2, {{2, 0, Scalar{1, 0}}}), ShapeError);
+  // order formulas (proj/tests/test_solver.cpp:297-320)
+  CHECK(equivalent_ns_order(1, 2) == BigInt(8));
+  CHECK(equivalent_ns_order(3, 2) == BigInt(80));
+  CHECK(equivalent_ns_order(50, 2).str() == "2153693963075557766310746");
+  CHECK(equivalent_ns_order(37, 2).str() == "1350851717672992088");
+  CHECK(estimate_nests(1e6, 2) == 18);
+  CHECK(estimate_nests(1e4, 2) == 12);
+  CHECK(estimate_nests(1.0, 1) == 1);
+  CHECK_THROWS(estimate_nests(0.5, 2), DomainError);
+  CHECK(FactorizedPlan::for_order(15, FactorizedMode::DenseStored).num_factors == 4);
+  CHECK_THROWS(FactorizedPlan::for_order(6, FactorizedMode::DenseStored), PlanError);
+  CHECK_THROWS(FactorizedPlan::for_order(0, FactorizedMode::DenseStored), PlanError);
+  CHECK_THROWS(DenseMatrix(1, 1, {Scalar{INFINITY, 0}}), DomainError);
+  CHECK_THROWS((DenseMatrix{{Scalar{1, 0}}, {Scalar{1, 0}, Scalar{2, 0}}}), ShapeError);
+}
+
+static void device_tests() {
+  // ---- matrix core
+  {
+    const DenseMatrix m = gauss(3, 3, 11);
+    CHECK(rel(matmul(DenseMatrix::identity(3), m), m) == 0.0);
+    const DenseMatrix p = matmul(DenseMatrix::diagonal({Scalar{2, 0}, Scalar{3, 0}}),
+                                 DenseMatrix::diagonal({Scalar{5, 0}, Scalar{7, 0}}));
+    CHECK(p(0, 0) == (Scalar{10, 0}) && p(1, 1) == (Scalar{21, 0}) && p(0, 1) == (Scalar{0, 0}));
+    const DenseMatrix a = gauss(4, 4, 21, true), b = gauss(4, 4, 22, true);
+    DenseMatrix naive(4, 4);
+    for (int j = 0; j < 4; ++j)
+      for (int k = 0; k < 4; ++k)
+        for (int i = 0; i < 4; ++i) naive(i, j) += a(i, k) * b(k, j);
+    CHECK(rel(matmul(a, b), naive) < 1e-15);
+    CHECK_THROWS(matmul(gauss(2, 3, 1), gauss(2, 2, 2)), ShapeError);
+    OpCounter c;
+    matmul(gauss(8, 8, 3), gauss(8, 8, 4), &c);
+    CHECK(c.n3_multiplies() == 1.0);
+    matmul(gauss(8, 2, 5), gauss(2, 8, 6), &c);
+    CHECK(std::fabs(c.n3_multiplies() - 1.25) < 1e-15);
+    CHECK(trace(DenseMatrix::identity(3)) == (Scalar{3, 0}));
+    CHECK(std::fabs(frobenius_norm(DenseMatrix::identity(4)) - 2.0) < 1e-15);
+    CHECK(frobenius_norm(DenseMatrix(4, 4)) == 0.0);
+    // associativity at kernel scale (complex)
+    const DenseMatrix x = gauss(32, 32, 1, true), y = gauss(32, 32, 101, true), z = gauss(32, 32, 201, true);
+    CHECK(rel(matmul(matmul(x, y), z), matmul(x, matmul(y, z))) < 1e-12);
+  }
+  // ---- preconditioning (proj/tests/test_preconditioning.cpp:13-27)
+  {
+    const DenseMatrix w = DenseMatrix::diagonal({Scalar{1, 0}, Scalar{3, 0}});
+    const Normalization n = theta_trace(w);
+    CHECK(std::fabs(n.theta - 0.25) < 1e-15);
+    CHECK(std::fabs(n.contraction_norm - 0.75) < 1e-9);
+    CHECK(n.valid);
+    CHECK(std::fabs(trace(normalize(w, n)).real() - 1.0) < 1e-14);
+    Normalization bad = n;
+    bad.valid = false;
+    CHECK_THROWS(normalize(w, bad), ContractionError);
+  }
+  // ---- ns_sum (proj/tests/test_solver.cpp:30-71)
+  {
+    const DenseMatrix wt = normalized(4, 1.0, 1), phi0 = spd(4, 2.0, 2);
+    CHECK(ns_sum(phi0, wt, 0) == phi0);
+    const DenseMatrix s = ns_sum(DenseMatrix::identity(2), DenseMatrix::diagonal({Scalar{0.25, 0}, Scalar{0.75, 0}}), 3);
+    CHECK(std::fabs(s(0, 0).real() - (1 + 0.75 + 0.75 * 0.75 + 0.75 * 0.75 * 0.75)) < 1e-15);
+    CHECK(std::fabs(s(1, 1).real() - (1 + 0.25 + 0.25 * 0.25 + 0.25 * 0.25 * 0.25)) < 1e-15);
+    const DenseMatrix w6 = normalized(6, 0.5, 4);
+    const DenseMatrix p0 = scale(DenseMatrix::identity(6), Scalar{1.5, 0});
+    for (std::size_t order : {1, 2, 5, 17}) {  // vs explicit power accumulation
+      const DenseMatrix P = identity_minus(matmul(p0, w6));
+      DenseMatrix acc = DenseMatrix::identity(6), pw = DenseMatrix::identity(6);
+      for (std::size_t k = 1; k <= order; ++k) {
+        pw = matmul(pw, P);
+        acc = add(acc, pw);
+      }
+      CHECK(rel(ns_sum(p0, w6, order), matmul(acc, p0)) < 1e-13);
+    }
+    OpCounter c;
+    ns_sum(DenseMatrix::identity(6), w6, 7, &c);
+    CHECK(c.n3_multiplies() == 6.0);
+    c.reset();
+    ns_sum(scale(DenseMatrix::identity(6), Scalar{0.9, 0}), w6, 7, &c);
+    CHECK(c.n3_multiplies() == 8.0);
+  }
+  // ---- nn_step / newton / chebyshev (proj/tests/test_solver.cpp:73-132)
+  {
+    for (std::uint64_t seed : {1ULL, 9ULL}) {
+      const DenseMatrix wt = normalized(16, 0.3, seed);
+      DenseMatrix z = DenseMatrix::identity(16);
+      const DenseMatrix I = DenseMatrix::identity(16);
+      for (int step = 0; step < 4; ++step) {
+        // the closed forms, composed from separate device ops
+        const DenseMatrix y = matmul(wt, z);
+        const DenseMatrix newton = matmul(z, sub(scale(I, Scalar{2, 0}), y));
+        const DenseMatrix inner = matmul(y, sub(scale(I, Scalar{3, 0}), y));
+        const DenseMatrix cheby = matmul(z, sub(scale(I, Scalar{3, 0}), inner));
+        CHECK(rel(nn_step(z, wt, 1), newton) < 1e-13);
+        CHECK(rel(nn_step(z, wt, 2), cheby) < 1e-13);
+        CHECK(rel(newton_step(z, wt), newton) < 1e-13);
+        CHECK(rel(chebyshev_step(z, wt), cheby) < 1e-13);
+        z = newton;
+      }
+    }
+    const DenseMatrix wt = normalized(8, 0.5, 7);
+    DenseMatrix phi = DenseMatrix::identity(8);
+    for (std::size_t depth : {1, 2, 3, 5}) {
+      OpCounter c;
+      phi = nn_step(phi, wt, depth, &c);
+      CHECK(c.n3_multiplies() == static_cast<double>(depth + 1));
+    }
+    CHECK(nn_step(phi, wt, 0) == phi);
+    OpCounter c;
+    DenseMatrix zz = newton_step(s1(1.0), s1(0.5), &c);
+    CHECK(std::fabs(zz(0, 0).real() - 1.5) < 1e-15);
+    zz = newton_step(zz, s1(0.5), &c);
+    CHECK(std::fabs(zz(0, 0).real() - 1.875) < 1e-15);
+    CHECK(c.n3_multiplies() == 4.0);
+    OpCounter c2;
+    CHECK(std::fabs(chebyshev_step(s1(1.0), s1(0.5), &c2)(0, 0).real() - 1.75) < 1e-15);
+    CHECK(c2.n3_multiplies() == 3.0);
+    CHECK_THROWS(nn_step(DenseMatrix::identity(3), DenseMatrix::identity(4), 1), ShapeError);
+  }
+  // ---- equivalence chain: recursive NN == plain series (proj/tests/test_solver.cpp:278-295)
+  {
+    const DenseMatrix wt = normalized(8, 0.5, 20), id = DenseMatrix::identity(8);
+    for (std::size_t depth = 1; depth <= 5; ++depth)
+      for (std::size_t nests = 0;; ++nests) {
+        const BigInt order = equivalent_ns_order(nests, depth);
+        if (order > BigInt(200)) break;
+        DenseMatrix rec = id;
+        for (std::size_t j = 0; j <= nests; ++j) rec = nn_step(rec, wt, depth);
+        CHECK(rel(rec, ns_sum(id, wt, static_cast<std::size_t>(order))) < 1e-11);
+      }
+  }
+  // ---- nn_invert (proj/tests/test_solver.cpp:134-228, 378-386)
+  {
+    const DenseMatrix w = DenseMatrix::identity(12);
+    SolverConfig cfg;
+    cfg.depth_L = 2;
+    cfg.tol = 1e-12;
+    cfg.max_nests = 40;
+    const auto [inv, rep] = nn_invert(w, theta_trace(w), cfg);
+    CHECK(rep.stopped_reason == StopReason::Tolerance);
+    CHECK(rel(inv, w) < 1e-12);
+
+    const DenseMatrix w16 = spd(16, 0.01, 13);
+    const Normalization nm = theta_trace(w16);
+    for (std::size_t depth = 1; depth <= 3; ++depth)
+      for (std::size_t nests = 1; nests <= 4; ++nests) {
+        SolverConfig c;
+        c.depth_L = depth;
+        c.max_nests = nests;
+        c.tol = 1e-15;
+        OpCounter cnt;
+        const auto [x, r] = nn_invert(w16, nm, c, &cnt);
+        CHECK(r.stopped_reason == StopReason::MaxNests);
+        CHECK(r.n3_multiplies == static_cast<double>(nests * (depth + 1)));
+        CHECK(cnt.n3_multiplies() == static_cast<double>(nests * (depth + 1)));
+        CHECK(r.history.size() == nests + 1);
+      }
+    // deeper nests converge in fewer iterations; history strictly decreasing above 1e-12
+    SolverConfig c;
+    c.tol = 1e-10;
+    c.max_nests = 64;
+    c.depth_L = 1;
+    const auto r1 = nn_invert(w16, nm, c).second;
+    c.depth_L = 2;
+    const auto r2 = nn_invert(w16, nm, c).second;
+    CHECK(r1.stopped_reason == StopReason::Tolerance && r2.stopped_reason == StopReason::Tolerance);
+    CHECK(r1.history.back().first > r2.history.back().first);
+    for (std::size_t k = 0; k + 1 < r2.history.size(); ++k)
+      if (r2.history[k].second > 1e-12) CHECK(r2.history[k + 1].second < r2.history[k].second);
+    // inverse quality
+    c.tol = 1e-12;
+    const auto [inv16, rep16] = nn_invert(w16, nm, c);
+    const DenseMatrix resid = sub(matmul(w16, inv16), DenseMatrix::identity(16));
+    CHECK(frobenius_norm(resid) / 4.0 < 1e-10);
+    // json report keys
+    const std::string js = report_to_json(rep16);
+    CHECK(js.find("\"stopped_reason\": \"tolerance\"") != std::string::npos);
+    CHECK(js.find("\"history\"") != std::string::npos && js.find("\"n3_multiplies\"") != std::string::npos);
+    // errors
+    Normalization bad = nm;
+    bad.valid = false;
+    CHECK_THROWS(nn_invert(w16, bad, c), ContractionError);
+    Normalization absurd = nm;
+    absurd.theta = 1e160;
+    try {
+      nn_invert(w16, absurd, SolverConfig{});
+      CHECK(false);
+    } catch (const DivergenceError& e) {
+      CHECK(e.nest_index >= 1);
+    }
+    SolverConfig v;
+    v.tol = 1e-16;
+    CHECK_THROWS(nn_invert(w16, nm, v), DomainError);
+    v.tol = 1e-10;
+    v.max_nests = 0;
+    CHECK_THROWS(nn_invert(w16, nm, v), DomainError);
+  }
+  // ---- sparse path (proj/tests/test_matrix_core.cpp:242-273, test_factorized.cpp:150-207)
+  {
+    const DenseMatrix b = gauss(6, 3, 81, true);
+    CHECK(spmv_block(SparseMatrixCsr::identity(6), b) == b);
+    std::vector<SparseMatrixCsr::Triplet> t;
+    const std::size_t n = 64;
+    for (std::size_t i = 0; i < n; ++i) {
+      t.push_back({i, i, Scalar{4.5, 0}});
+      if (i + 1 < n) {
+        t.push_back({i, i + 1, Scalar{-1, 0}});
+        t.push_back({i + 1, i, Scalar{-1, 0}});
+      }
+      if (i + 8 < n) {
+        t.push_back({i, i + 8, Scalar{-1, 0}});
+        t.push_back({i + 8, i, Scalar{-1, 0}});
+      }
+    }
+    const SparseMatrixCsr w = SparseMatrixCsr::build(n, n, t);
+    const DenseMatrix x = gauss(n, 4, 92, true);
+    OpCounter c;
+    CHECK(rel(spmv_block(w, x, &c), matmul(w.densify(), x)) < 1e-15);
+    CHECK(c.spmv_count() == 4);
+    const Normalization nm = theta_trace(w);
+    CHECK(nm.valid);
+    DenseMatrix rhs(n, 2);
+    for (std::size_t i = 0; i < rhs.size(); ++i) rhs.data()[i] = Scalar{std::cos(double(i)), 0};
+    OpCounter cs;
+    const DenseMatrix xs = solve_sparse_factorized({w, rhs, false}, 15, nm, &cs);
+    CHECK(cs.spmv_count() == 15 * 2);
+    // dense factorized series theta * prod_{f<4} (I + P^{2^f}) B, composed from device products
+    const DenseMatrix P = identity_minus(scale(w.densify(), Scalar{nm.theta, 0}));
+    DenseMatrix acc = DenseMatrix::identity(n), pw = P;
+    for (int f = 0; f < 4; ++f) {
+      acc = matmul(acc, plus_identity(pw));
+      pw = matmul(pw, pw);
+    }
+    CHECK(rel(xs, scale(matmul(acc, rhs), Scalar{nm.theta, 0})) < 1e-11);
+    // identity system: theta = 1/8, x = (1 - (7/8)^16) B
+    const SparseMatrixCsr I8 = SparseMatrixCsr::identity(8);
+    const DenseMatrix b8 = gauss(8, 8, 10);
+    const DenseMatrix x8 = solve_sparse_factorized({I8, b8, false}, 15, theta_trace(I8));
+    CHECK(rel(x8, scale(b8, Scalar{1 - std::pow(7.0 / 8.0, 16.0), 0})) < 1e-12);
+    // rejections
+    CHECK_THROWS(solve_sparse_factorized({w, rhs, false}, 6, nm), PlanError);
+    CHECK_THROWS(solve_sparse_factorized({w, DenseMatrix(5, 1), false}, 7, nm), ShapeError);
+    CHECK_THROWS(solve_sparse_factorized({rhs, rhs, false}, 7, nm), ShapeError);
+    Normalization inv = nm;
+    inv.valid = false;
+    CHECK_THROWS(solve_sparse_factorized({w, rhs, false}, 7, inv), ContractionError);
+    Normalization absurd = nm;
+    absurd.theta = 1e150;
+    CHECK_THROWS(solve_sparse_factorized({w, rhs, false}, 32767, absurd), DivergenceError);
+  }
+}
+
+int main(int argc, char** argv) {
+  const bool host_only = argc > 1 && std::strcmp(argv[1], "--host") == 0;
+  host_tests();
+  if (!host_only) device_tests();
+  std::printf("%s: %d checks, %d failures\n", host_only ? "host" : "all", g_checks, g_fail);
+  return g_fail == 0 ? 0 : 1;
+}
