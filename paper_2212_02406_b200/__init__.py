@@ -108,6 +108,9 @@ _SIGS = {
     "nnb_spmv_block_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _dp, _dp], C.c_int),
     "nnb_sparse_factorized_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _i64, C.c_double, _dp, _dp, _dp,
                                  _dp], C.c_int),
+    "nnb_spectral_norm_z": ([_dp, _i64, _dp, C.c_double, _i32, _dp, _dp, _dp, _dp], C.c_int),
+    "nnb_spectral_norm_shifted_csr": ([_dp, _dp, _dp, _i64, _i64, C.c_double, _dp, C.c_double, _i32, _dp, _dp,
+                                       _dp, _dp], C.c_int),
     "nnb_partition_rows": ([_i64, _i32, _i32, C.POINTER(_i64), C.POINTER(_i64)], None),
     "nnb_comm_unique_id": ([_dp], C.c_int),
     "nnb_comm_init": ([_dp, _i32, _i32, C.POINTER(C.c_void_p)], C.c_int),
