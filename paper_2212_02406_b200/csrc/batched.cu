@@ -1,9 +1,12 @@
 // Batched Nested Neumann inversion of small complex systems (massive-MIMO
 // Gram matrices, BASELINE config 1: 262144 × 16×16 complex128).
 //
-// One warp owns one system at a time (grid-stride over systems):
+// One warp owns one system at a time (grid-stride over systems, persistent
+// grid sized to the measured occupancy):
 //   * A is read once from HBM (coalesced 16-byte loads) straight into the
-//     DMMA B-operand registers it occupies for the whole solve;
+//     DMMA B-operand registers it occupies for the whole solve; the next
+//     system's A is prefetched into registers while the current one iterates
+//     (PREFETCH), hiding the HBM latency behind ~13k cycles of DMMA work;
 //   * X0 = diag(A)^-1 (Jacobi) is formed in shared memory;
 //   * every iterate (X, P, V) stays in per-warp shared memory, planar re/im,
 //     16×16 doubles with the XOR swizzle  (r, c) -> r*16 + (c ^ 4*(r&3)),
@@ -11,21 +14,27 @@
 //     (row=t, col=g) fragment loads of mma.m8n8k4 conflict-free (2
 //     wavefronts per 32 doubles) and keeps the epilogue's double2 stores
 //     at the 4-wavefront minimum;
-//   * each complex 16×16×16 product is 64 DMMA.8x8x4 (4M: re·re − im·im,
-//     re·im + im·re) with the "I −", "+X" and ‖·‖² terms in the epilogue;
+//   * each complex 16×16×16 product runs on DMMA.8x8x4 either as 4M
+//     (re·re − im·im, re·im + im·re: 64 DMMA) or as 3M (Gauss:
+//     P1 = re·re, P2 = im·im, P3 = (re+im)·(re+im); re = P1 − P2,
+//     im = P3 − P1 − P2: 48 DMMA), with the "I −", "+X" and ‖·‖² terms in
+//     the epilogue;
 //   * X is written once (coalesced) and, for the NN chain, eps of the final
 //     residual is written per system.
 // The nest follows the reference's operand order (proj/src/solver.cpp:93-103):
 //   P = I − X·A;  V = X + P·X;  V = X + P·V (p−1 more);  X = V,
 // and the Neumann-series baseline follows ns_sum (proj/src/solver.cpp:77-91):
 //   P = I − X0·A;  T = I + P;  T = T·P + I (order−1 times);  X = T·X0.
+#include <cstdlib>
+#include <cstring>
+
 #include "engine.cuh"
 
 namespace nnb {
 namespace {
 
 constexpr int kN = 16;
-constexpr int kMat = kN * kN;            // doubles per plane
+constexpr int kMat = kN * kN;  // doubles per plane
 constexpr int kWarpsPerCta = 4;
 constexpr int kThreads = kWarpsPerCta * 32;
 
@@ -36,20 +45,63 @@ struct SMat {
   double* im;
 };
 
-// acc[mt][nt][plane][i]: C[8mt+g][8nt+2t+i] (plane 0 = re, 1 = im)
-using Acc = double[2][2][2][2];
+// Accumulators for C[8mt+g][8nt+2t+i]: 4M keeps (re, im); 3M keeps (P1, P2, P3).
+template <bool M3>
+struct ZAcc {
+  double v[2][2][M3 ? 3 : 2][2];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int p = 0; p < (M3 ? 3 : 2); ++p) v[a][b][p][0] = v[a][b][p][1] = 0.0;
+  }
+  // one k-step: L fragments (lr, li) for 2 m-tiles, R fragments (rr, ri) for 2 n-tiles
+  __device__ __forceinline__ void step(const double (&lr)[2], const double (&li)[2], const double (&rr)[2],
+                                       const double (&ri)[2]) {
+    if constexpr (M3) {
+      double ls[2], rs[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        ls[i] = lr[i] + li[i];
+        rs[i] = rr[i] + ri[i];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          dmma_8x8x4(v[mt][nt][0][0], v[mt][nt][0][1], lr[mt], rr[nt]);
+          dmma_8x8x4(v[mt][nt][1][0], v[mt][nt][1][1], li[mt], ri[nt]);
+          dmma_8x8x4(v[mt][nt][2][0], v[mt][nt][2][1], ls[mt], rs[nt]);
+        }
+    } else {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const double nli = -li[mt];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          dmma_8x8x4(v[mt][nt][0][0], v[mt][nt][0][1], lr[mt], rr[nt]);
+          dmma_8x8x4(v[mt][nt][0][0], v[mt][nt][0][1], nli, ri[nt]);
+          dmma_8x8x4(v[mt][nt][1][0], v[mt][nt][1][1], lr[mt], ri[nt]);
+          dmma_8x8x4(v[mt][nt][1][0], v[mt][nt][1][1], li[mt], rr[nt]);
+        }
+      }
+    }
+  }
+  __device__ __forceinline__ double re(int mt, int nt, int i) const {
+    if constexpr (M3) return v[mt][nt][0][i] - v[mt][nt][1][i];
+    else return v[mt][nt][0][i];
+  }
+  __device__ __forceinline__ double im(int mt, int nt, int i) const {
+    if constexpr (M3) return v[mt][nt][2][i] - v[mt][nt][0][i] - v[mt][nt][1][i];
+    else return v[mt][nt][1][i];
+  }
+};
 
-__device__ __forceinline__ void acc_zero(Acc& acc) {
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 2; ++b)
-#pragma unroll
-      for (int p = 0; p < 2; ++p) acc[a][b][p][0] = acc[a][b][p][1] = 0.0;
-}
-
-// acc += L·R, L from shared (A-operand), R from shared (B-operand).
-__device__ __forceinline__ void zmma_ss(Acc& acc, const SMat& L, const SMat& R, int g, int t) {
+// acc += L·R, L (A-operand) and R (B-operand) from shared memory.
+template <bool M3>
+__device__ __forceinline__ void zmma_ss(ZAcc<M3>& acc, const SMat& L, const SMat& R, int g, int t) {
 #pragma unroll
   for (int kb = 0; kb < 4; ++kb) {
     double lr[2], li[2], rr[2], ri[2];
@@ -65,24 +117,14 @@ __device__ __forceinline__ void zmma_ss(Acc& acc, const SMat& L, const SMat& R, 
       rr[nt] = R.re[idx];
       ri[nt] = R.im[idx];
     }
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      const double nli = -li[mt];
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        dmma_8x8x4(acc[mt][nt][0][0], acc[mt][nt][0][1], lr[mt], rr[nt]);
-        dmma_8x8x4(acc[mt][nt][0][0], acc[mt][nt][0][1], nli, ri[nt]);
-        dmma_8x8x4(acc[mt][nt][1][0], acc[mt][nt][1][1], lr[mt], ri[nt]);
-        dmma_8x8x4(acc[mt][nt][1][0], acc[mt][nt][1][1], li[mt], rr[nt]);
-      }
-    }
+    acc.step(lr, li, rr, ri);
   }
 }
 
-// acc += L·A with A's B-operand fragments held in registers:
-// areg[nt][kb][plane] = A[4kb+t][8nt+g].
-__device__ __forceinline__ void zmma_sr(Acc& acc, const SMat& L, const double (&areg)[2][4][2],
-                                        int g, int t) {
+// acc += L·A with A's B-operand fragments in registers: areg[nt][kb][plane] = A[4kb+t][8nt+g].
+template <bool M3>
+__device__ __forceinline__ void zmma_sr(ZAcc<M3>& acc, const SMat& L, const double (&areg)[2][4][2], int g,
+                                        int t) {
 #pragma unroll
   for (int kb = 0; kb < 4; ++kb) {
     double lr[2], li[2];
@@ -92,26 +134,16 @@ __device__ __forceinline__ void zmma_sr(Acc& acc, const SMat& L, const double (&
       lr[mt] = L.re[idx];
       li[mt] = L.im[idx];
     }
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      const double nli = -li[mt];
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        dmma_8x8x4(acc[mt][nt][0][0], acc[mt][nt][0][1], lr[mt], areg[nt][kb][0]);
-        dmma_8x8x4(acc[mt][nt][0][0], acc[mt][nt][0][1], nli, areg[nt][kb][1]);
-        dmma_8x8x4(acc[mt][nt][1][0], acc[mt][nt][1][1], lr[mt], areg[nt][kb][1]);
-        dmma_8x8x4(acc[mt][nt][1][0], acc[mt][nt][1][1], li[mt], areg[nt][kb][0]);
-      }
-    }
+    const double rr[2] = {areg[0][kb][0], areg[1][kb][0]};
+    const double ri[2] = {areg[0][kb][1], areg[1][kb][1]};
+    acc.step(lr, li, rr, ri);
   }
 }
 
 // out = alpha·acc + (D ? D : 0) + gamma·I, stored to shared `out` (may alias D).
-// Returns this lane's Σ|out|² when `want_ss`.
-__device__ __forceinline__ double epilogue(const Acc& acc, double alpha, const SMat* D,
-                                           double gamma, const SMat& out, int g, int t,
-                                           bool want_ss) {
-  double ss = 0.0;
+template <bool M3>
+__device__ __forceinline__ void epilogue(const ZAcc<M3>& acc, double alpha, const SMat* D, double gamma,
+                                         const SMat& out, int g, int t) {
   __syncwarp();  // every lane finished reading operands that `out` may overwrite
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
@@ -119,48 +151,62 @@ __device__ __forceinline__ double epilogue(const Acc& acc, double alpha, const S
     for (int nt = 0; nt < 2; ++nt) {
       const int r = 8 * mt + g, c = 8 * nt + 2 * t;
       const int idx = swz(r, c);
-      double2 vr = make_double2(alpha * acc[mt][nt][0][0], alpha * acc[mt][nt][0][1]);
-      double2 vi = make_double2(alpha * acc[mt][nt][1][0], alpha * acc[mt][nt][1][1]);
+      double2 vr = make_double2(alpha * acc.re(mt, nt, 0), alpha * acc.re(mt, nt, 1));
+      double2 vi = make_double2(alpha * acc.im(mt, nt, 0), alpha * acc.im(mt, nt, 1));
       if (D) {
         const double2 dr = *reinterpret_cast<const double2*>(D->re + idx);
         const double2 di = *reinterpret_cast<const double2*>(D->im + idx);
-        vr.x += dr.x; vr.y += dr.y;
-        vi.x += di.x; vi.y += di.y;
+        vr.x += dr.x;
+        vr.y += dr.y;
+        vi.x += di.x;
+        vi.y += di.y;
       }
       if (r == c) vr.x += gamma;
       if (r == c + 1) vr.y += gamma;
       *reinterpret_cast<double2*>(out.re + idx) = vr;
       *reinterpret_cast<double2*>(out.im + idx) = vi;
-      if (want_ss) {
-        ss = fma(vr.x, vr.x, ss); ss = fma(vi.x, vi.x, ss);
-        ss = fma(vr.y, vr.y, ss); ss = fma(vi.y, vi.y, ss);
-      }
     }
   __syncwarp();
-  return ss;
 }
 
 // Σ|I − X·A|² without storing the residual.
-__device__ __forceinline__ double residual_ss(const Acc& acc, int g, int t) {
+template <bool M3>
+__device__ __forceinline__ double residual_ss(const ZAcc<M3>& acc, int g, int t) {
   double ss = 0.0;
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
       const int r = 8 * mt + g, c = 8 * nt + 2 * t;
-      double v0 = -acc[mt][nt][0][0], v1 = -acc[mt][nt][0][1];
-      if (r == c) v0 += 1.0;
-      if (r == c + 1) v1 += 1.0;
-      ss = fma(v0, v0, ss);
-      ss = fma(v1, v1, ss);
-      ss = fma(acc[mt][nt][1][0], acc[mt][nt][1][0], ss);
-      ss = fma(acc[mt][nt][1][1], acc[mt][nt][1][1], ss);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        double vr = -acc.re(mt, nt, i);
+        if (r == c + i) vr += 1.0;
+        const double vi = acc.im(mt, nt, i);
+        ss = fma(vr, vr, ss);
+        ss = fma(vi, vi, ss);
+      }
     }
   return ss;
 }
 
-template <int P>
-__global__ void __launch_bounds__(kThreads)
+__device__ __forceinline__ void load_a_frags(const double2* __restrict__ As, int g, int t, double (&areg)[2][4][2]) {
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {
+      const double2 v = __ldg(As + (4 * kb + t) * kN + 8 * nt + g);
+      areg[nt][kb][0] = v.x;
+      areg[nt][kb][1] = v.y;
+    }
+}
+
+// NNB_BATCHED_MINB (compile-time) caps registers so that MINB CTAs fit per SM.
+#ifndef NNB_BATCHED_MINB
+#define NNB_BATCHED_MINB 4
+#endif
+template <int P, bool M3, bool PREFETCH>
+__global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
     batched_z16_kernel(const double2* __restrict__ A, int64_t batch, int iters, int ns_order,
                        double2* __restrict__ Xout, double* __restrict__ eps_last, int ns_mode) {
   __shared__ __align__(16) double smem[kWarpsPerCta][3][2][kMat];
@@ -172,18 +218,22 @@ __global__ void __launch_bounds__(kThreads)
 
   const int64_t gw = blockIdx.x * (int64_t)kWarpsPerCta + warp;
   const int64_t nw = (int64_t)gridDim.x * kWarpsPerCta;
+  double areg[2][4][2], anext[2][4][2];
+  if (PREFETCH && gw < batch) load_a_frags(A + gw * kMat, g, t, anext);
   for (int64_t s = gw; s < batch; s += nw) {
     const double2* As = A + s * kMat;
-    // A's B-operand fragments: A[4kb+t][8nt+g]
-    double areg[2][4][2];
+    if (PREFETCH) {
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+      for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-      for (int kb = 0; kb < 4; ++kb) {
-        const double2 v = __ldg(As + (4 * kb + t) * kN + 8 * nt + g);
-        areg[nt][kb][0] = v.x;
-        areg[nt][kb][1] = v.y;
-      }
+        for (int kb = 0; kb < 4; ++kb) {
+          areg[nt][kb][0] = anext[nt][kb][0];
+          areg[nt][kb][1] = anext[nt][kb][1];
+        }
+      if (s + nw < batch) load_a_frags(A + (s + nw) * kMat, g, t, anext);
+    } else {
+      load_a_frags(As, g, t, areg);
+    }
     // X0 = diag(A)^-1 (Smith's complex reciprocal, as libgcc's __divdc3)
     for (int i = lane; i < kMat; i += 32) {
       X.re[i] = 0.0;
@@ -207,35 +257,34 @@ __global__ void __launch_bounds__(kThreads)
     }
     __syncwarp();
 
-    Acc acc;
+    ZAcc<M3> acc;
     if (!ns_mode) {
       // ---- Nested Neumann: `iters` nests of depth P ----
       for (int it = 0; it < iters; ++it) {
-        acc_zero(acc);
-        zmma_sr(acc, X, areg, g, t);                    // X·A
-        epilogue(acc, -1.0, nullptr, 1.0, Pm, g, t, false);  // P = I − X·A
+        acc.zero();
+        zmma_sr(acc, X, areg, g, t);               // X·A
+        epilogue(acc, -1.0, nullptr, 1.0, Pm, g, t);  // P = I − X·A
         const SMat* v = &X;
 #pragma unroll
         for (int j = 1; j <= P; ++j) {
-          acc_zero(acc);
-          zmma_ss(acc, Pm, *v, g, t);                   // P·V
-          const SMat& dst = (j == P) ? X : V;           // last Horner step lands in X
-          epilogue(acc, 1.0, &X, 0.0, dst, g, t, false);  // V = X + P·V
+          acc.zero();
+          zmma_ss(acc, Pm, *v, g, t);                 // P·V
+          const SMat& dst = (j == P) ? X : V;         // last Horner step lands in X
+          epilogue(acc, 1.0, &X, 0.0, dst, g, t);     // V = X + P·V
           v = &V;
         }
       }
       // final residual eps = ‖I − X·A‖_F / √n
-      acc_zero(acc);
+      acc.zero();
       zmma_sr(acc, X, areg, g, t);
-      double ss = warp_sum(residual_ss(acc, g, t));
+      const double ss = warp_sum(residual_ss(acc, g, t));
       if (lane == 0 && eps_last) eps_last[s] = sqrt(ss) * 0.25;  // 1/sqrt(16)
     } else if (ns_order > 0) {
       // ---- Neumann-series baseline of `ns_order` terms from X0 ----
-      acc_zero(acc);
+      acc.zero();
       zmma_sr(acc, X, areg, g, t);
-      epilogue(acc, -1.0, nullptr, 1.0, Pm, g, t, false);  // P = I − X0·A
-      // T = I + P  (into V)
-      for (int i = lane; i < kMat; i += 32) {
+      epilogue(acc, -1.0, nullptr, 1.0, Pm, g, t);  // P = I − X0·A
+      for (int i = lane; i < kMat; i += 32) {      // T = I + P (into V)
         V.re[i] = Pm.re[i];
         V.im[i] = Pm.im[i];
       }
@@ -243,13 +292,13 @@ __global__ void __launch_bounds__(kThreads)
       if (lane < kN) V.re[swz(lane, lane)] += 1.0;
       __syncwarp();
       for (int step = 2; step <= ns_order; ++step) {
-        acc_zero(acc);
-        zmma_ss(acc, V, Pm, g, t);                      // T·P
-        epilogue(acc, 1.0, nullptr, 1.0, V, g, t, false);  // T = T·P + I
+        acc.zero();
+        zmma_ss(acc, V, Pm, g, t);                  // T·P
+        epilogue(acc, 1.0, nullptr, 1.0, V, g, t);  // T = T·P + I
       }
-      acc_zero(acc);
-      zmma_ss(acc, V, X, g, t);                         // T·X0
-      epilogue(acc, 1.0, nullptr, 0.0, X, g, t, false);
+      acc.zero();
+      zmma_ss(acc, V, X, g, t);                     // T·X0
+      epilogue(acc, 1.0, nullptr, 0.0, X, g, t);
     }
     // store X (planar swizzled shared -> interleaved global, coalesced 16B)
     double2* Xs = Xout + s * kMat;
@@ -263,30 +312,60 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+template <int P, bool M3, bool PF>
+int launch_variant(const double2* a, int64_t batch, int iters, int ns_order, double2* x, double* eps,
+                   int ns_mode, cudaStream_t s) {
+  static int blocks_per_sm = 0;
+  static int sms = 0;
+  if (!blocks_per_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, batched_z16_kernel<P, M3, PF>, kThreads, 0);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const int64_t want = (batch + kWarpsPerCta - 1) / kWarpsPerCta;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(want, (int64_t)sms * blocks_per_sm));
+  batched_z16_kernel<P, M3, PF><<<grid, kThreads, 0, s>>>(a, batch, iters, ns_order, x, eps, ns_mode);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// Product method: 3M (default, 25 % fewer DMMA) or 4M; register prefetch of the
+// next A off by default (measured on B200: 3M 3.16-3.21 ms, 3M+prefetch 3.26-3.29,
+// 4M 3.45, 4M+prefetch 3.47-3.57 ms per 262144-system batch).
+// NNB_BATCHED_VARIANT = "4m", "3m", "4m_nopf", "3m_nopf" overrides (A/B measurement).
+template <int P>
+int launch_p(const double2* a, int64_t batch, int iters, int ns_order, double2* x, double* eps, int ns_mode,
+             cudaStream_t s) {
+  static const char* env = std::getenv("NNB_BATCHED_VARIANT");
+  const bool m4 = env && env[0] == '4';
+  const bool nopf = !env || std::strstr(env, "nopf");
+  if (m4) {
+    return nopf ? launch_variant<P, false, false>(a, batch, iters, ns_order, x, eps, ns_mode, s)
+                : launch_variant<P, false, true>(a, batch, iters, ns_order, x, eps, ns_mode, s);
+  }
+  return nopf ? launch_variant<P, true, false>(a, batch, iters, ns_order, x, eps, ns_mode, s)
+              : launch_variant<P, true, true>(a, batch, iters, ns_order, x, eps, ns_mode, s);
+}
+
 }  // namespace
 
 int batched_nn_z16(const double* A, int64_t batch, int p, int iters, int ns_order, double* X,
                    double* eps_last, cudaStream_t s) {
+  if (batch <= 0) return 0;
   // ns_order < 0: Nested Neumann chain; ns_order >= 0: Neumann series of that order
   const int ns_mode = ns_order >= 0 ? 1 : 0;
-  if (batch <= 0) return 0;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t want = (batch + kWarpsPerCta - 1) / kWarpsPerCta;
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(want, (int64_t)sms * 4));
   const double2* a = reinterpret_cast<const double2*>(A);
   double2* x = reinterpret_cast<double2*>(X);
   switch (ns_mode ? 1 : p) {
-    case 1: batched_z16_kernel<1><<<grid, kThreads, 0, s>>>(a, batch, iters, ns_order, x, eps_last, ns_mode); break;
-    case 2: batched_z16_kernel<2><<<grid, kThreads, 0, s>>>(a, batch, iters, ns_order, x, eps_last, ns_mode); break;
-    case 3: batched_z16_kernel<3><<<grid, kThreads, 0, s>>>(a, batch, iters, ns_order, x, eps_last, ns_mode); break;
-    case 4: batched_z16_kernel<4><<<grid, kThreads, 0, s>>>(a, batch, iters, ns_order, x, eps_last, ns_mode); break;
+    case 1: return launch_p<1>(a, batch, iters, ns_order, x, eps_last, ns_mode, s);
+    case 2: return launch_p<2>(a, batch, iters, ns_order, x, eps_last, ns_mode, s);
+    case 3: return launch_p<3>(a, batch, iters, ns_order, x, eps_last, ns_mode, s);
+    case 4: return launch_p<4>(a, batch, iters, ns_order, x, eps_last, ns_mode, s);
     default: return fail(2, "batched: depth p must be in 1..4");
   }
-  count_launch();
-  NNB_CUDA(cudaGetLastError());
-  return 0;
 }
 
 }  // namespace nnb
