@@ -436,6 +436,54 @@ int nnb_ns_sum_z(const double* phi0, const double* w, int64_t n, int64_t order, 
 }
 
 // ---------------------------------------------------------------- batched
+// Host-to-host calls stream the batch through the device in chunks on three
+// rotating lanes (stream per lane): H2D of chunk i+1, the kernel on chunk i
+// and D2H of chunk i-1 overlap, so the PCIe traffic in both directions (full
+// duplex) hides behind itself and the compute instead of adding up.
+static constexpr int64_t kChunkSystems = 16384;  // 64 MB in + 64 MB out per chunk
+
+static int batched_pipelined(const double* A, int64_t batch, int p, int iters, int ns_order, double* X_out,
+                             double* eps_last, cudaStream_t s) {
+  constexpr int kLanes = 3;
+  const size_t sys_doubles = 2 * 256;
+  static thread_local cudaStream_t lanes[kLanes] = {nullptr, nullptr, nullptr};
+  for (auto& l : lanes)
+    if (!l) NNB_CUDA(cudaStreamCreateWithFlags(&l, cudaStreamNonBlocking));
+  DevBuf buf;
+  const size_t per_lane = kChunkSystems * sys_doubles * 2 + kChunkSystems;  // A, X, eps
+  NNB_TRY(buf.alloc(sizeof(double) * per_lane * kLanes, s));
+  cudaEvent_t start, done[kLanes];
+  NNB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  for (auto& d : done) NNB_CUDA(cudaEventCreateWithFlags(&d, cudaEventDisableTiming));
+  NNB_CUDA(cudaEventRecord(start, s));  // buffers are allocated in stream order on s
+  for (auto& l : lanes) NNB_CUDA(cudaStreamWaitEvent(l, start, 0));
+  int st = 0;
+  for (int64_t c0 = 0, i = 0; c0 < batch && st == 0; c0 += kChunkSystems, ++i) {
+    const int64_t nb = std::min<int64_t>(kChunkSystems, batch - c0);
+    const int lane = static_cast<int>(i % kLanes);
+    cudaStream_t ls = lanes[lane];
+    double* da = buf.as<double>() + lane * per_lane;
+    double* dx = da + kChunkSystems * sys_doubles;
+    double* de = dx + kChunkSystems * sys_doubles;
+    NNB_CUDA(cudaMemcpyAsync(da, A + c0 * sys_doubles, sizeof(double) * nb * sys_doubles,
+                             cudaMemcpyHostToDevice, ls));
+    st = batched_nn_z16(da, nb, p, iters, ns_order, dx, eps_last ? de : nullptr, ls);
+    NNB_CUDA(cudaMemcpyAsync(X_out + c0 * sys_doubles, dx, sizeof(double) * nb * sys_doubles,
+                             cudaMemcpyDeviceToHost, ls));
+    if (eps_last)
+      NNB_CUDA(cudaMemcpyAsync(eps_last + c0, de, sizeof(double) * nb, cudaMemcpyDeviceToHost, ls));
+  }
+  for (int l = 0; l < kLanes; ++l) {
+    NNB_CUDA(cudaEventRecord(done[l], lanes[l]));
+    NNB_CUDA(cudaStreamWaitEvent(s, done[l], 0));  // buffer release is ordered after every lane
+  }
+  buf.release();
+  NNB_CUDA(cudaStreamSynchronize(s));
+  cudaEventDestroy(start);
+  for (auto& d : done) cudaEventDestroy(d);
+  return st;
+}
+
 static int batched(const double* A, int64_t batch, int32_t n, int p, int iters, int ns_order,
                    double* X_out, double* eps_last, void* stream) {
   NNB_TRY(require_device());
@@ -443,6 +491,10 @@ static int batched(const double* A, int64_t batch, int32_t n, int p, int iters, 
   if (batch < 0) return fail(NNB_ERR_SHAPE, "batched: negative batch");
   cudaStream_t s = resolve(stream);
   const size_t cnt = (size_t)batch * 2 * 256;
+  const bool host_in = !is_device_ptr(A), host_out = !is_device_ptr(X_out) ||
+                                                     (eps_last && !is_device_ptr(eps_last));
+  if (host_in && host_out && batch > 2 * kChunkSystems)
+    return batched_pipelined(A, batch, p, iters, ns_order, X_out, eps_last, s);
   In a;
   NNB_TRY(a.stage(A, cnt, s));
   Out x, e;
