@@ -209,6 +209,26 @@ int nnb_nn_chain_sharded_emulated_d(const double* A, int64_t n, int32_t world, c
                                     const nnb_chain_config* cfg, double* X_out, double* eps_hist,
                                     nnb_chain_result* result, void* stream);
 
+/* ---- row-slab sharded sparse solve (one process per GPU) ---------------- */
+/* rank g owns the rows nnb_partition_rows(n, world, g) of W,
+ * B and x.  row_ptr: this rank's rows_g+1 offsets into col/val (col holds
+ * GLOBAL column indices); B_rows / X_rows: rows_g × k.  Per application the
+ * halo rows (the columns a slab references in its neighbours' slabs) move by
+ * NCCL send/recv while the interior rows compute.  Bit-identical to
+ * nnb_sparse_factorized_d for any world size.  The operator's bandwidth must
+ * not exceed a neighbour slab (halos come from adjacent ranks only). */
+int nnb_sparse_factorized_sharded_d(nnb_comm_t comm, const int64_t* row_ptr, const int32_t* col,
+                                    const double* val, int64_t n, const double* B_rows, int64_t k,
+                                    int64_t gamma, double theta, double* X_rows,
+                                    int64_t* spmv_count_out, int32_t* fail_factor_out, void* stream);
+/* The same schedule with `world` virtual ranks (device copies move the halos). */
+int nnb_sparse_factorized_sharded_emulated_d(const int64_t* row_ptr, const int32_t* col,
+                                             const double* val, int64_t n, int64_t nnz,
+                                             const double* B, int64_t k, int64_t gamma,
+                                             double theta, int32_t world, double* X_out,
+                                             int64_t* spmv_count_out, int32_t* fail_factor_out,
+                                             void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -119,6 +119,10 @@ _SIGS = {
                                 C.POINTER(ChainResult), _dp], C.c_int),
     "nnb_nn_chain_sharded_emulated_d": ([_dp, _i64, _i32, _dp, C.POINTER(ChainConfig), _dp, _dp,
                                          C.POINTER(ChainResult), _dp], C.c_int),
+    "nnb_sparse_factorized_sharded_d": ([C.c_void_p, _dp, _dp, _dp, _i64, _dp, _i64, _i64, C.c_double, _dp, _dp,
+                                         _dp, _dp], C.c_int),
+    "nnb_sparse_factorized_sharded_emulated_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _i64, C.c_double, _i32,
+                                                  _dp, _dp, _dp, _dp], C.c_int),
 }
 
 _lib: Optional[C.CDLL] = None
@@ -584,6 +588,38 @@ def solve_sparse_factorized(csr: Csr, b, gamma: int, norm: Normalization):
     st = lib().nnb_sparse_factorized_d(_ptr(csr.row_ptr), _ptr(csr.col), _ptr(csr.val), csr.n, csr.nnz, _ptr(b), k,
                                        int(gamma), float(norm.theta), _ptr(out), C.addressof(cnt), C.addressof(ff),
                                        _stream(b))
+    _check(st, ff.value)
+    return out, cnt.value
+
+
+def solve_sparse_factorized_sharded(comm: Comm, csr_rows: Csr, n: int, b_rows, gamma: int, norm: Normalization):
+    """Row-slab sharded solve: this rank's CSR rows (global columns,
+    row_ptr offsets into col/val), its rows of B in, its rows of x out."""
+    if not norm.valid:
+        raise ContractionError("solve_sparse_factorized: invalid normalization")
+    b_rows = _prep(b_rows, False)
+    k = 1 if b_rows.ndim == 1 else b_rows.shape[1]
+    out = _empty_like(b_rows)
+    cnt, ff = C.c_int64(), C.c_int32(-1)
+    st = lib().nnb_sparse_factorized_sharded_d(comm.handle, _ptr(csr_rows.row_ptr), _ptr(csr_rows.col),
+                                               _ptr(csr_rows.val), n, _ptr(b_rows), k, int(gamma),
+                                               float(norm.theta), _ptr(out), C.addressof(cnt), C.addressof(ff),
+                                               _stream(b_rows))
+    _check(st, ff.value)
+    return out, cnt.value
+
+
+def solve_sparse_factorized_sharded_emulated(csr: Csr, b, gamma: int, norm: Normalization, world: int):
+    """The row-slab schedule with `world` virtual ranks on this GPU."""
+    if not norm.valid:
+        raise ContractionError("solve_sparse_factorized: invalid normalization")
+    b = _prep(b, False)
+    k = 1 if b.ndim == 1 else b.shape[1]
+    out = _empty_like(b)
+    cnt, ff = C.c_int64(), C.c_int32(-1)
+    st = lib().nnb_sparse_factorized_sharded_emulated_d(_ptr(csr.row_ptr), _ptr(csr.col), _ptr(csr.val), csr.n,
+                                                        csr.nnz, _ptr(b), k, int(gamma), float(norm.theta), world,
+                                                        _ptr(out), C.addressof(cnt), C.addressof(ff), _stream(b))
     _check(st, ff.value)
     return out, cnt.value
 

@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "../../include/nnb.h"
+#include "comm.cuh"
 #include "engine.cuh"
 
 namespace nnb {
@@ -115,15 +116,20 @@ __global__ void jacobi_rows_kernel(const double* __restrict__ A, int64_t lda, in
 }
 
 }  // namespace
-}  // namespace nnb
 
-struct nnb_comm {
-  ncclComm_t comm = nullptr;
-  int world = 1, rank = 0, device = 0;
-  cudaStream_t cs = nullptr;  // communication stream
-};
+// wrappers shared with sparse_sharded.cu (comm.cuh)
+ncclResult_t nccl_send(const void* buf, size_t count, int peer, nnb_comm* c, cudaStream_t s) {
+  return nccl().send(buf, count, ncclDouble, peer, c->comm, s);
+}
+ncclResult_t nccl_recv(void* buf, size_t count, int peer, nnb_comm* c, cudaStream_t s) {
+  return nccl().recv(buf, count, ncclDouble, peer, c->comm, s);
+}
+ncclResult_t nccl_group(bool start) { return start ? nccl().groupStart() : nccl().groupEnd(); }
+ncclResult_t nccl_allgather(const void* send, void* recv, size_t count, nnb_comm* c, cudaStream_t s) {
+  return nccl().allGather(send, recv, count, ncclDouble, c->comm, s);
+}
+const char* nccl_error(ncclResult_t r) { return nccl().errorString ? nccl().errorString(r) : "NCCL unavailable"; }
 
-namespace nnb {
 namespace {
 
 struct Shard {

@@ -11,181 +11,62 @@
 //   X     = θ·(Z + (t_in − θ·W·t_in))               (last application overall)
 // so y never exists and the factor update and the final scale ride along.
 //
-// Row-group kernel: a warp owns 32 consecutive rows; its lanes stream the
-// group's contiguous nonzero range with coalesced loads of val/col, gather
-// t_in[col], and stage the products in shared memory; each lane then sums
-// its own row in ascending nonzero order.  Every operation is explicitly
-// rounded (no FMA contraction) and ordered exactly as the reference's
-// std::complex<double> arithmetic (spmv sum += v·x from 0, t = z − θ·y,
-// Z + t, Z·θ), so the GPU result is BIT-IDENTICAL to the reference's.
-// Row offsets are narrowed to int32 on the device when nnz < 2^31 (one
-// conversion pass per solve, −4 B per row per application).
-// HBM-bound: ≈12 B per nonzero + 4 B per row of CSR, 8 B in + 8 B out per row.
-#include <cstdlib>
-
+// Every operation is explicitly rounded (no FMA contraction) and ordered as
+// the reference's std::complex<double> arithmetic evaluates it for real W:
+// spmv sum += v·x from 0 in ascending nonzero order, t = z − θ·y, Z + t, Z·θ.
+// The GPU result is therefore BIT-IDENTICAL to the reference's, for any row
+// partition (the multi-GPU path, sparse_sharded.cu, relies on this).
+//
+// Kernel: one thread per row, persistent grid of exactly the resident blocks.
+// Measured on B200 (config 4): 14.2 ms per solve = 91 % of HBM; a row-group
+// variant with coalesced shared staging (20.1 ms) and an 8-way unrolled
+// per-row variant (19.2 ms) lost to the occupancy of this 40-register loop.
+// Row offsets are narrowed to int32 on the device when nnz < 2^31.
+// HBM-bound: 12 B per nonzero + 4 B per row of CSR, 8 B in + 8 B out per row.
 #include "engine.cuh"
+#include "sparse.cuh"
 
 namespace nnb {
-namespace {
-
-enum Mode { kInner = 0, kFactorEnd = 1, kFinal = 2 };
-
-constexpr int kWarps = 8;           // warps per CTA
-constexpr int kStage = 32 * 8;      // staged products per warp per column (avg ≤ 8 nnz/row)
 
 template <int MODE>
-__device__ __forceinline__ double finish(double tin, double y, double theta, const double* zold, int64_t i,
-                                         bool& bad) {
+__device__ __forceinline__ double finish(double tin, double y, double theta, double zold, bool& bad) {
   const double t = __dsub_rn(tin, __dmul_rn(theta, y));  // fused_axpy_sub, factorized.cpp:21-30
   double o;
   if (MODE == kInner) {
     o = t;
   } else if (MODE == kFactorEnd) {
-    o = __dadd_rn(zold[i], t);                           // add(z, t), factorized.cpp:136
+    o = __dadd_rn(zold, t);                              // add(z, t), factorized.cpp:136
   } else {
-    o = __dmul_rn(__dadd_rn(zold[i], t), theta);         // scale(z, theta), factorized.cpp:139
+    o = __dmul_rn(__dadd_rn(zold, t), theta);            // scale(z, theta), factorized.cpp:139
   }
   bad |= !isfinite(y) || !isfinite(t) || !isfinite(o);
   return o;
 }
 
-// k columns (k ≤ 2) per row; rows grouped 32 per warp.
-template <typename Idx, int MODE, int K>
-__global__ void __launch_bounds__(kWarps * 32)
-    spmv_group_kernel(const Idx* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
-                      int64_t n, const double* __restrict__ tin, double* __restrict__ out,
-                      const double* __restrict__ zold, double theta, int* __restrict__ flag) {
-  __shared__ double prod[kWarps][K][kStage];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  bool bad = false;
-  const int64_t groups = (n + 31) / 32;
-  for (int64_t grp = blockIdx.x * (int64_t)kWarps + warp; grp < groups; grp += (int64_t)gridDim.x * kWarps) {
-    const int64_t r = grp * 32 + lane;
-    const bool live = r < n;
-    const int64_t my_b = live ? (int64_t)rp[r] : 0;
-    const int64_t my_e = live ? (int64_t)rp[r + 1] : 0;
-    const int64_t g_b = __shfl_sync(0xffffffffu, my_b, 0);
-    const int64_t rem = n - 1 - grp * 32;
-    const int last = rem < 31 ? static_cast<int>(rem) : 31;
-    const int64_t g_e = __shfl_sync(0xffffffffu, my_e, last);
-    const int64_t cnt = g_e - g_b;
-    double y[K];
-#pragma unroll
-    for (int c = 0; c < K; ++c) y[c] = 0.0;
-    if (cnt <= kStage) {
-      // coalesced stream of the group's nonzeros, fully unrolled so every lane has
-      // kStage/32 value/column loads and then as many gathers in flight;
-      // products rounded as v*x
-      constexpr int kPer = kStage / 32;
-      double v[kPer];
-      int32_t ci[kPer];
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int64_t j = lane + 32 * u;
-        if (j < cnt) {
-          v[u] = __ldg(val + g_b + j);
-          ci[u] = __ldg(col + g_b + j);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int64_t j = lane + 32 * u;
-        if (j < cnt) {
-#pragma unroll
-          for (int c = 0; c < K; ++c) prod[warp][c][j] = __dmul_rn(v[u], __ldg(tin + (int64_t)ci[u] * K + c));
-        }
-      }
-      __syncwarp();
-      if (live)
-        for (int64_t e = my_b - g_b; e < my_e - g_b; ++e)
-#pragma unroll
-          for (int c = 0; c < K; ++c) y[c] = __dadd_rn(y[c], prod[warp][c][e]);
-      __syncwarp();
-    } else if (live) {
-      // long rows in this group: plain per-row loop, same rounding and order
-      for (int64_t e = my_b; e < my_e; ++e) {
-        const double v = __ldg(val + e);
-        const int64_t cidx = __ldg(col + e);
-#pragma unroll
-        for (int c = 0; c < K; ++c) y[c] = __dadd_rn(y[c], __dmul_rn(v, __ldg(tin + cidx * K + c)));
-      }
-    }
-    if (live) {
-#pragma unroll
-      for (int c = 0; c < K; ++c) out[r * K + c] = finish<MODE>(tin[r * K + c], y[c], theta, zold, r * K + c, bad);
-    }
-  }
-  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
-}
-
-// One thread per row, K ≤ 2 columns, the first 8 nonzeros of a row loaded with
-// full memory-level parallelism (8 value/column loads, then 8 gathers in
-// flight) before the ordered, explicitly rounded sum; longer rows continue
-// sequentially.  Same arithmetic as the row-group kernel (bit-exact).
-template <typename Idx, int MODE, int K>
-__global__ void __launch_bounds__(256)
-    spmv_row8_kernel(const Idx* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
-                     int64_t n, const double* __restrict__ tin, double* __restrict__ out,
-                     const double* __restrict__ zold, double theta, int* __restrict__ flag) {
-  bool bad = false;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e0 = __ldg(rp + r), e1 = __ldg(rp + r + 1);
-    double v[8], xv[8][K];
-    int32_t ci[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (e0 + u < e1) {
-        v[u] = __ldg(val + e0 + u);
-        ci[u] = __ldg(col + e0 + u);
-      }
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (e0 + u < e1) {
-#pragma unroll
-        for (int c = 0; c < K; ++c) xv[u][c] = __ldg(tin + (int64_t)ci[u] * K + c);
-      }
-    double y[K];
-#pragma unroll
-    for (int c = 0; c < K; ++c) y[c] = 0.0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (e0 + u < e1) {
-#pragma unroll
-        for (int c = 0; c < K; ++c) y[c] = __dadd_rn(y[c], __dmul_rn(v[u], xv[u][c]));
-      }
-    for (int64_t e = e0 + 8; e < e1; ++e) {
-      const double vv = __ldg(val + e);
-      const int64_t cc = __ldg(col + e);
-#pragma unroll
-      for (int c = 0; c < K; ++c) y[c] = __dadd_rn(y[c], __dmul_rn(vv, __ldg(tin + cc * K + c)));
-    }
-#pragma unroll
-    for (int c = 0; c < K; ++c) out[r * K + c] = finish<MODE>(tin[r * K + c], y[c], theta, zold, r * K + c, bad);
-  }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
-}
-
-// Generic k: one thread per row, all columns (used for k > 2).
+// Rows [r_begin, r_end) of one application.  Gathers read t_ext through the
+// (possibly halo-remapped) column indices; the diagonal term, z and the
+// output are indexed by row.
 template <typename Idx, int MODE>
 __global__ void __launch_bounds__(256)
     spmv_rows_kernel(const Idx* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
-                     int64_t n, int64_t k, const double* __restrict__ tin, double* __restrict__ out,
-                     const double* __restrict__ zold, double theta, int* __restrict__ flag) {
+                     int64_t r_begin, int64_t r_end, int64_t k, const double* __restrict__ t_ext,
+                     const double* __restrict__ t_own, double* __restrict__ out, const double* __restrict__ zold,
+                     double theta, int* __restrict__ flag) {
   bool bad = false;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t r = r_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < r_end;
+       r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e0 = rp[r], e1 = rp[r + 1];
     for (int64_t c = 0; c < k; ++c) {
       double y = 0.0;
-      for (int64_t e = e0; e < e1; ++e) y = __dadd_rn(y, __dmul_rn(val[e], tin[(int64_t)col[e] * k + c]));
-      out[r * k + c] = finish<MODE>(tin[r * k + c], y, theta, zold, r * k + c, bad);
+      for (int64_t e = e0; e < e1; ++e) y = __dadd_rn(y, __dmul_rn(val[e], t_ext[(int64_t)col[e] * k + c]));
+      out[r * k + c] = finish<MODE>(t_own[r * k + c], y, theta, MODE == kInner ? 0.0 : zold[r * k + c], bad);
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
 // Plain Y = W·X for nn::spmv_block (same rounding as the reference's sum).
-template <typename Idx>
-__global__ void spmv_plain_kernel(const Idx* __restrict__ rp, const int32_t* __restrict__ col,
+__global__ void spmv_plain_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                                   const double* __restrict__ val, int64_t n, int64_t k,
                                   const double* __restrict__ x, double* __restrict__ y) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
@@ -198,60 +79,73 @@ __global__ void spmv_plain_kernel(const Idx* __restrict__ rp, const int32_t* __r
   }
 }
 
-__global__ void narrow_offsets_kernel(const int64_t* __restrict__ in, int32_t* __restrict__ out, int64_t count) {
+__global__ void narrow_offsets_kernel(const int64_t* __restrict__ in, int32_t* __restrict__ out, int64_t count,
+                                      int64_t base) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = static_cast<int32_t>(in[i]);
+    out[i] = static_cast<int32_t>(in[i] - base);
 }
+
+namespace {
 
 unsigned rows_grid(int64_t n) {
-  static const int64_t cap = std::getenv("NNB_SPMV_GRID") ? std::atoll(std::getenv("NNB_SPMV_GRID")) : 148 * 8 * 4;
   const int64_t want = (n + 255) / 256;
-  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, cap)));
-}
-
-unsigned group_grid(int64_t n) {
-  const int64_t groups = (n + 31) / 32;
-  const int64_t want = (groups + kWarps - 1) / kWarps;
-  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, 148 * 8)));
-}
-
-// 0 = row-group (shared staging), 1 = row8 (per-row, unrolled MLP), 2 = per-row
-// loop (default).  Measured on B200, 4096² Laplacian, γ=63: 20.1 / 19.2 / 15.3 ms
-// per solve — the 40-register per-row loop keeps 48 warps/SM resident and wins.
-int spmv_variant() {
-  static const int v = std::getenv("NNB_SPMV_VARIANT") ? std::atoi(std::getenv("NNB_SPMV_VARIANT")) : 2;
-  return v;
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, 148 * 8 * 4)));
 }
 
 template <typename Idx, int MODE>
-void launch_step(const Idx* rp, const int32_t* col, const double* val, int64_t n, int64_t k, const double* tin,
-                 double* out, const double* zold, double theta, int* flag, cudaStream_t s) {
-  if (spmv_variant() == 2) {
-    // persistent grid = exactly the resident blocks (grid-stride rows, no partial
-    // last wave): 14.2 ms vs 15.4 ms with 4736 blocks (B200, config 4)
-    static unsigned resident = 0;
-    if (!resident) {
-      int dev = 0, sms = 148, per = 1;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, spmv_rows_kernel<Idx, MODE>, 256, 0);
-      resident = static_cast<unsigned>(sms * std::max(1, per));
-    }
-    const unsigned grid = std::min<unsigned>(resident, rows_grid(n));
-    spmv_rows_kernel<Idx, MODE><<<grid, 256, 0, s>>>(rp, col, val, n, k, tin, out, zold, theta, flag);
-  } else if (spmv_variant() == 1 && k <= 2) {
-    if (k == 1)
-      spmv_row8_kernel<Idx, MODE, 1><<<rows_grid(n), 256, 0, s>>>(rp, col, val, n, tin, out, zold, theta, flag);
-    else
-      spmv_row8_kernel<Idx, MODE, 2><<<rows_grid(n), 256, 0, s>>>(rp, col, val, n, tin, out, zold, theta, flag);
-  } else if (k == 1)
-    spmv_group_kernel<Idx, MODE, 1><<<group_grid(n), kWarps * 32, 0, s>>>(rp, col, val, n, tin, out, zold, theta, flag);
-  else if (k == 2)
-    spmv_group_kernel<Idx, MODE, 2><<<group_grid(n), kWarps * 32, 0, s>>>(rp, col, val, n, tin, out, zold, theta, flag);
-  else
-    spmv_rows_kernel<Idx, MODE><<<rows_grid(n), 256, 0, s>>>(rp, col, val, n, k, tin, out, zold, theta, flag);
+unsigned resident_grid(int64_t rows) {
+  static unsigned resident = 0;
+  if (!resident) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, spmv_rows_kernel<Idx, MODE>, 256, 0);
+    resident = static_cast<unsigned>(sms * std::max(1, per));
+  }
+  return std::min<unsigned>(resident, rows_grid(rows));
+}
+
+}  // namespace
+
+template <typename Idx>
+void spmv_apply(const SpmvOp<Idx>& op, int mode, int64_t r_begin, int64_t r_end, cudaStream_t s) {
+  if (r_end <= r_begin) return;
+  const int64_t rows = r_end - r_begin;
+  switch (mode) {
+    case kInner:
+      spmv_rows_kernel<Idx, kInner><<<resident_grid<Idx, kInner>(rows), 256, 0, s>>>(
+          op.rp, op.col, op.val, r_begin, r_end, op.k, op.t_ext, op.t_own, op.out, op.zold, op.theta, op.flag);
+      break;
+    case kFactorEnd:
+      spmv_rows_kernel<Idx, kFactorEnd><<<resident_grid<Idx, kFactorEnd>(rows), 256, 0, s>>>(
+          op.rp, op.col, op.val, r_begin, r_end, op.k, op.t_ext, op.t_own, op.out, op.zold, op.theta, op.flag);
+      break;
+    default:
+      spmv_rows_kernel<Idx, kFinal><<<resident_grid<Idx, kFinal>(rows), 256, 0, s>>>(
+          op.rp, op.col, op.val, r_begin, r_end, op.k, op.t_ext, op.t_own, op.out, op.zold, op.theta, op.flag);
+  }
   count_launch();
 }
+template void spmv_apply<int32_t>(const SpmvOp<int32_t>&, int, int64_t, int64_t, cudaStream_t);
+template void spmv_apply<int64_t>(const SpmvOp<int64_t>&, int, int64_t, int64_t, cudaStream_t);
+
+int narrow_offsets(const int64_t* in, int32_t* out, int64_t count, int64_t base, cudaStream_t s) {
+  narrow_offsets_kernel<<<rows_grid(count), 256, 0, s>>>(in, out, count, base);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int spmv_csr(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n, const double* X, int64_t k,
+             double* Y, cudaStream_t s) {
+  if (n == 0) return 0;
+  spmv_plain_kernel<<<rows_grid(n), 256, 0, s>>>(row_ptr, col, val, n, k, X, Y);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+namespace {
 
 template <typename Idx>
 void run_factors(const Idx* rp, const int32_t* col, const double* val, int64_t n, const double* B, int64_t k,
@@ -263,15 +157,23 @@ void run_factors(const Idx* rp, const int32_t* col, const double* val, int64_t n
     const double* tin = zcur;  // t = Z
     int ti = 0;
     for (int64_t r = 0; r < reps; ++r) {
-      const bool last_app = (r == reps - 1);
-      if (!last_app) {
-        launch_step<Idx, kInner>(rp, col, val, n, k, tin, tb[ti], nullptr, theta, flags + f, s);
+      SpmvOp<Idx> op{rp, col, val, k, tin, tin, nullptr, zcur, theta, flags + f};
+      int mode;
+      if (r < reps - 1) {
+        mode = kInner;
+        op.out = tb[ti];
+      } else if (f == s_factors - 1) {
+        mode = kFinal;
+        op.out = X;
+      } else {
+        mode = kFactorEnd;
+        op.out = z[zi];
+      }
+      spmv_apply(op, mode, 0, n, s);
+      if (mode == kInner) {
         tin = tb[ti];
         ti ^= 1;
-      } else if (f == s_factors - 1) {
-        launch_step<Idx, kFinal>(rp, col, val, n, k, tin, X, zcur, theta, flags + f, s);
-      } else {
-        launch_step<Idx, kFactorEnd>(rp, col, val, n, k, tin, z[zi], zcur, theta, flags + f, s);
+      } else if (mode == kFactorEnd) {
         zcur = z[zi];
         zi ^= 1;
       }
@@ -281,15 +183,6 @@ void run_factors(const Idx* rp, const int32_t* col, const double* val, int64_t n
 }
 
 }  // namespace
-
-int spmv_csr(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n, const double* X, int64_t k,
-             double* Y, cudaStream_t s) {
-  if (n == 0) return 0;
-  spmv_plain_kernel<int64_t><<<rows_grid(n), 256, 0, s>>>(row_ptr, col, val, n, k, X, Y);
-  count_launch();
-  NNB_CUDA(cudaGetLastError());
-  return 0;
-}
 
 int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n, const double* B,
                       int64_t k, int s_factors, double theta, double* X, int* fail_factor, cudaStream_t s) {
@@ -306,8 +199,7 @@ int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* 
   NNB_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 64, s));
   if (narrow) {
     int32_t* rp32 = flags + 64;
-    narrow_offsets_kernel<<<rows_grid(n + 1), 256, 0, s>>>(row_ptr, rp32, n + 1);
-    count_launch();
+    NNB_TRY(narrow_offsets(row_ptr, rp32, n + 1, 0, s));
     run_factors<int32_t>(rp32, col, val, n, B, k, s_factors, theta, X, z, tb, flags, s);
   } else {
     run_factors<int64_t>(row_ptr, col, val, n, B, k, s_factors, theta, X, z, tb, flags, s);

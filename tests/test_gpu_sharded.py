@@ -64,3 +64,66 @@ def test_sharded_divergence_reported():
     with pytest.raises(nnb.DivergenceError) as e:
         nnb.nn_chain_sharded_emulated(a, 2, None, p=2, max_iters=30, x0_kind=nnb.X0_SCALED_IDENTITY, x0_scale=1e160)
     assert e.value.nest_index >= 1
+
+
+# ---------------------------------------------------------------- sparse row slabs (config 4 path)
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_sparse_sharded_emulated_bitexact(ref, world):
+    """Halo exchange + interior/boundary split: bit-identical to the reference for any world."""
+    rp, col, val = W.laplacian_5pt(100)
+    b = W.rhs(10000, seed=world)
+    csr = nnb.Csr(rp, col, val, n=10000)
+    norm = nnb.Normalization(theta=0.2, valid=True)
+    xs, cnt = nnb.solve_sparse_factorized_sharded_emulated(csr, b, 63, norm, world)
+    xr, cr, _ = ref.sparse_factorized(rp, col, val, b, 63, 0.2)
+    assert cnt == cr == 63 and np.array_equal(xs, xr.real)
+    b2 = np.random.default_rng(world).standard_normal((10000, 2))
+    xs2, _ = nnb.solve_sparse_factorized_sharded_emulated(csr, b2, 15, norm, world)
+    xr2, _, _ = ref.sparse_factorized(rp, col, val, b2, 15, 0.2)
+    assert np.array_equal(xs2, xr2.real)
+
+
+def test_sparse_sharded_emulated_full_size_matches_single():
+    import torch
+
+    rp, col, val = W.laplacian_5pt(4096)
+    n = 4096 * 4096
+    dev = lambda a: torch.from_numpy(a).cuda()
+    csr = nnb.Csr(dev(rp), dev(col), dev(val), n=n, nnz=col.size)
+    b = dev(W.rhs(n, seed=4))
+    norm = nnb.Normalization(theta=0.2, valid=True)
+    x1, _ = nnb.solve_sparse_factorized(csr, b, 63, norm)
+    x8, _ = nnb.solve_sparse_factorized_sharded_emulated(csr, b, 63, norm, 8)
+    torch.cuda.synchronize()
+    assert torch.equal(x1, x8)
+
+
+def test_sparse_sharded_nccl_world1(ref):
+    rp, col, val = W.laplacian_5pt(40)
+    b = W.rhs(1600, seed=2)
+    comm = nnb.Comm(1, 0, nnb.Comm.unique_id())
+    try:
+        xs, cnt = nnb.solve_sparse_factorized_sharded(comm, nnb.Csr(rp, col, val, n=1600), 1600, b, 31,
+                                                      nnb.Normalization(theta=0.2, valid=True))
+    finally:
+        comm.close()
+    xr, _, _ = ref.sparse_factorized(rp, col, val, b, 31, 0.2)
+    assert cnt == 31 and np.array_equal(xs, xr.real)
+
+
+def test_sparse_sharded_rejects_wide_halo():
+    # a dense coupling between the first and last rows spans every slab
+    n = 64
+    rows, cols = np.arange(n), np.arange(n)
+    dense = np.eye(n) * 4.0
+    dense[0, n - 1] = dense[n - 1, 0] = -1.0
+    rp = np.zeros(n + 1, np.int64)
+    cl, vl = [], []
+    for i in range(n):
+        nz = np.nonzero(dense[i])[0]
+        cl.extend(nz)
+        vl.extend(dense[i, nz])
+        rp[i + 1] = len(cl)
+    csr = nnb.Csr(rp, np.array(cl, np.int32), np.array(vl), n=n)
+    with pytest.raises(nnb.DomainError):
+        nnb.solve_sparse_factorized_sharded_emulated(csr, np.ones(n), 7, nnb.Normalization(theta=0.2, valid=True), 4)
