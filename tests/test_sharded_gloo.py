@@ -125,3 +125,87 @@ def test_sharded_schedule_gloo_world2(port, world):
     xr, hr, _ = port.chain(a, W.x0_transpose_norm(a), p, iters)
     assert np.linalg.norm(X - xr.real) / np.linalg.norm(xr.real) < 1e-12
     assert np.allclose(eps[0], hr, rtol=1e-9, atol=1e-15)
+
+
+# ---------------------------------------------------------------- sparse row slabs over gloo
+def _sparse_worker(rank, world, port, grid, gamma, theta, out_q):
+    """The halo schedule of csrc/sparse_sharded.cu with gloo send/recv and scalar IEEE arithmetic in
+    the reference's order (sum += v*x from 0; t = z - theta*y; Z + t; Z*theta)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2212_02406_b200 as nnb
+
+    n = grid * grid
+    rp, col, val = W.laplacian_5pt(grid)
+    b = W.rhs(n, seed=9)
+    r0, rows = nnb.partition_rows(n, world, rank)
+    lo, hi = rp[r0], rp[r0 + rows]
+    mycols = col[lo:hi]
+    h_lo = max(0, r0 - int(mycols.min()))
+    h_hi = max(0, int(mycols.max()) - (r0 + rows - 1))
+    sizes = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([h_lo, h_hi], dtype=torch.int64))
+    send_prev = int(sizes[rank - 1][1]) if rank > 0 else 0
+    send_next = int(sizes[rank + 1][0]) if rank < world - 1 else 0
+
+    def exchange(ext):  # ext = [h_lo | own | h_hi]
+        reqs, bufs = [], []
+        if rank > 0:
+            reqs.append(dist.isend(torch.tensor(ext[h_lo:h_lo + send_prev], dtype=torch.float64), rank - 1))
+            buf = torch.empty(h_lo, dtype=torch.float64)
+            reqs.append(dist.irecv(buf, rank - 1))
+            bufs.append((0, buf))
+        if rank < world - 1:
+            reqs.append(dist.isend(torch.tensor(ext[h_lo + rows - send_next:h_lo + rows], dtype=torch.float64), rank + 1))
+            buf = torch.empty(h_hi, dtype=torch.float64)
+            reqs.append(dist.irecv(buf, rank + 1))
+            bufs.append((h_lo + rows, buf))
+        for r in reqs:
+            r.wait()
+        for off, buf in bufs:
+            ext[off:off + len(buf)] = buf.tolist()
+
+    def apply(ext):
+        exchange(ext)
+        out = [0.0] * rows
+        for i in range(rows):
+            y = 0.0
+            for e in range(rp[r0 + i], rp[r0 + i + 1]):
+                y = y + float(val[e]) * ext[int(col[e]) - r0 + h_lo]
+            out[i] = ext[h_lo + i] - theta * y
+        return out
+
+    pad = lambda own: [0.0] * h_lo + list(own) + [0.0] * h_hi
+    z = [float(v) for v in b[r0:r0 + rows]]
+    s = 0
+    while (1 << s) - 1 < gamma:
+        s += 1
+    reps = 1
+    for _ in range(s):
+        t = z
+        for _ in range(reps):
+            t = apply(pad(t))
+        z = [zi + ti for zi, ti in zip(z, t)]
+        reps <<= 1
+    x = [zi * theta for zi in z]
+    out_q.put((rank, r0, x))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sparse_halo_schedule_gloo_world2(port):
+    world, grid, gamma, theta = 2, 12, 15, 0.2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    portn = _free_port()
+    procs = [ctx.Process(target=_sparse_worker, args=(r, world, portn, grid, gamma, theta, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    x = np.concatenate([np.array(r[2]) for r in res])
+    rp, col, val = W.laplacian_5pt(grid)
+    xr, _ = port.sparse_factorized(rp, col, val, W.rhs(grid * grid, seed=9), gamma, theta)
+    assert np.array_equal(x, xr.real)  # bit-identical across the partition
