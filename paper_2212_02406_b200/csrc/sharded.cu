@@ -178,6 +178,22 @@ int ring_allgather(Shard& sh, double* full) {
   return 0;
 }
 
+// All-gather of the per-rank [Σ‖·‖², non-finite] pairs.  Every NCCL call of a
+// communicator goes to its one communication stream (issue order = execution
+// order on every rank); the compute stream hands over and waits by events.
+int gather_pairs(Shard& sh, const double* pairs, double* gathered) {
+  if (!sh.comm || sh.world == 1) {
+    NNB_CUDA(cudaMemcpyAsync(gathered, pairs, sizeof(double) * 2 * sh.world, cudaMemcpyDeviceToDevice, sh.s));
+    return 0;
+  }
+  NNB_CUDA(cudaEventRecord(sh.ready, sh.s));
+  NNB_CUDA(cudaStreamWaitEvent(sh.comm->cs, sh.ready, 0));
+  NNB_NCCL(nccl().allGather(pairs + 2 * sh.comm->rank, gathered, 2, ncclDouble, sh.comm->comm, sh.comm->cs));
+  NNB_CUDA(cudaEventRecord(sh.ev[0], sh.comm->cs));  // ev[0] is free: ring events use q >= 1
+  NNB_CUDA(cudaStreamWaitEvent(sh.s, sh.ev[0], 0));
+  return 0;
+}
+
 // C_g = alpha·Σ_j L[:, J_j]·F_j + beta·D + gamma·I(row0_g), K split by the
 // ranks' row blocks, own block first then ring order; the last partial
 // carries the Σ C² / non-finite reduction when ss_out != null.
@@ -276,13 +292,7 @@ int run_sharded(Shard& sh, const double* A_local, int64_t lda_rows_stride, bool 
       count_launch();
     }
     // ---- eps: per-rank pairs gathered, summed in rank order ----
-    if (sh.comm && G > 1) {
-      NNB_NCCL(nccl().allGather(pairs + 2 * sh.comm->rank, gathered, 2, ncclDouble, sh.comm->comm,
-                                sh.s));
-    } else {
-      NNB_CUDA(cudaMemcpyAsync(gathered, pairs, sizeof(double) * 2 * G, cudaMemcpyDeviceToDevice,
-                               sh.s));
-    }
+    NNB_TRY(gather_pairs(sh, pairs, gathered));
     combine_ranks_kernel<<<1, 32, 0, sh.s>>>(gathered, G, eps_dev + k, nf_dev + k * (p + 1), scale);
     count_launch();
     ++products;
@@ -323,13 +333,7 @@ int run_sharded(Shard& sh, const double* A_local, int64_t lda_rows_stride, bool 
       pack_pair_kernel<<<1, 32, 0, sh.s>>>(ss_tmp + 1, nf_tmp + 8 + g, pairs + 2 * g);
       count_launch();
     }
-    if (sh.comm && G > 1) {
-      NNB_NCCL(nccl().allGather(pairs + 2 * sh.comm->rank, gathered, 2, ncclDouble, sh.comm->comm,
-                                sh.s));
-    } else {
-      NNB_CUDA(cudaMemcpyAsync(gathered, pairs, sizeof(double) * 2 * G, cudaMemcpyDeviceToDevice,
-                               sh.s));
-    }
+    NNB_TRY(gather_pairs(sh, pairs, gathered));
     combine_ranks_kernel<<<1, 32, 0, sh.s>>>(gathered, G, ss_tmp + 2, nf_dev + k * (p + 1) + p,
                                              scale);
     count_launch();
