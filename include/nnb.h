@@ -151,6 +151,14 @@ int nnb_nn_batched_z(const double* A, int64_t batch, int32_t n, int32_t p, int32
 int nnb_ns_batched_z(const double* A, int64_t batch, int32_t n, int32_t order, double* X_out,
                      void* stream);
 
+/* Fused massive-MIMO detection: per system
+ * A = Hᴴ·H + sigma2·I (H: antennas × users, row-major complex128), z = Hᴴ·y,
+ * X = NN inverse of A (Jacobi X0, `iters` nests of depth p), x̂ = X·z.
+ * users == 16, antennas % 4 == 0.  X_out / eps_last nullable. */
+int nnb_mimo_detect_z(const double* H, const double* y, int64_t batch, int32_t antennas, int32_t users,
+                      double sigma2, int32_t p, int32_t iters, double* xhat_out, double* X_out,
+                      double* eps_last, void* stream);
+
 /* ---- sparse matrix-free factorized solve -------------------------------- */
 /* Y = W·X for CSR W (int64 row_ptr, int32 col, float64 values) and an n×k
  * row-major block X: nn::spmv_block (proj/include/nn/kernels.hpp:91-92). */

@@ -105,6 +105,7 @@ _SIGS = {
     "nnb_ns_sum_z": ([_dp, _dp, _i64, _i64, _dp, _dp, _dp], C.c_int),
     "nnb_nn_batched_z": ([_dp, _i64, _i32, _i32, _i32, _dp, _dp, _dp], C.c_int),
     "nnb_ns_batched_z": ([_dp, _i64, _i32, _i32, _dp, _dp], C.c_int),
+    "nnb_mimo_detect_z": ([_dp, _dp, _i64, _i32, _i32, C.c_double, _i32, _i32, _dp, _dp, _dp, _dp], C.c_int),
     "nnb_spmv_block_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _dp, _dp], C.c_int),
     "nnb_sparse_factorized_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _i64, C.c_double, _dp, _dp, _dp,
                                  _dp], C.c_int),
@@ -549,6 +550,28 @@ def nn_batched(a, p: int = 2, iters: int = 4, want_eps: bool = True, out=None):
             eps = np.empty(b)
     _check(lib().nnb_nn_batched_z(_ptr(a), b, n, p, iters, _ptr(out), _ptr(eps), _stream(a)))
     return out, eps
+
+
+def mimo_detect(h, y, sigma2: float = 0.1, p: int = 2, iters: int = 4, want_x: bool = False,
+                want_eps: bool = False):
+    """Fused MIMO detection: A = HᴴH + σ²I, X = NN⁻¹(A), x̂ = X·Hᴴy per system.
+    h: (batch, antennas, 16) complex, y: (batch, antennas) complex. Returns (x̂, X or None, eps or None)."""
+    h = _prep(h, True)
+    y = _prep(y, True)
+    b, ant, users = h.shape
+    xh = _empty_like(h, (b, users))
+    x = _empty_like(h, (b, users, users)) if want_x else None
+    eps = None
+    if want_eps:
+        if _is_torch(h):
+            import torch
+
+            eps = torch.empty(b, dtype=torch.float64, device=h.device)
+        else:
+            eps = np.empty(b)
+    _check(lib().nnb_mimo_detect_z(_ptr(h), _ptr(y), b, ant, users, float(sigma2), p, iters, _ptr(xh), _ptr(x),
+                                   _ptr(eps), _stream(h)))
+    return xh, x, eps
 
 
 def ns_batched(a, order: int):

@@ -312,6 +312,139 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused massive-MIMO detection (the step either side
+// of the batched inversion; §4 motivates NN with mMIMO detection):
+//   A = Hᴴ·H + σ²·I        (16×128 · 128×16, DMMA from coalesced H fragments)
+//   z = Hᴴ·y               (accumulated from the same H fragments)
+//   X = NN inverse of A    (Jacobi X0, `iters` nests of depth P, as above)
+//   x̂ = X·z                (written per system; X and eps optional)
+// H (32 KB per system) is read exactly once; A never touches HBM.
+template <int P>
+__global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
+    mimo_detect_kernel(const double2* __restrict__ H, const double2* __restrict__ Y, int64_t batch, int ant,
+                       double sigma2, int iters, double2* __restrict__ xhat, double2* __restrict__ Xout,
+                       double* __restrict__ eps_last) {
+  constexpr bool M3 = true;
+  __shared__ __align__(16) double smem[kWarpsPerCta][3][2][kMat];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  SMat X{smem[warp][0][0], smem[warp][0][1]};
+  SMat Pm{smem[warp][1][0], smem[warp][1][1]};
+  SMat V{smem[warp][2][0], smem[warp][2][1]};
+  const int64_t gw = blockIdx.x * (int64_t)kWarpsPerCta + warp;
+  const int64_t nw = (int64_t)gridDim.x * kWarpsPerCta;
+  for (int64_t s = gw; s < batch; s += nw) {
+    const double2* Hs = H + s * (int64_t)ant * kN;
+    const double2* Ys = Y + s * (int64_t)ant;
+    // ---- Gram A = Hᴴ·H and z = Hᴴ·y from one pass over H ----
+    ZAcc<M3> acc;
+    acc.zero();
+    double zr[2] = {0.0, 0.0}, zi[2] = {0.0, 0.0};  // z[8mt+g], partial over this lane's antennas
+#pragma unroll 4
+    for (int kb = 0; kb < ant / 4; ++kb) {
+      const int a = 4 * kb + t;
+      const double2 h0 = __ldg(Hs + a * kN + g), h1 = __ldg(Hs + a * kN + 8 + g), y = __ldg(Ys + a);
+      const double lr[2] = {h0.x, h1.x}, li[2] = {-h0.y, -h1.y};  // A-operand: conj(H)[i][a]
+      const double rr[2] = {h0.x, h1.x}, ri[2] = {h0.y, h1.y};    // B-operand: H[a][j]
+      acc.step(lr, li, rr, ri);
+      // conj(h)·y
+      zr[0] = fma(h0.x, y.x, fma(h0.y, y.y, zr[0]));
+      zi[0] = fma(h0.x, y.y, fma(-h0.y, y.x, zi[0]));
+      zr[1] = fma(h1.x, y.x, fma(h1.y, y.y, zr[1]));
+      zi[1] = fma(h1.x, y.y, fma(-h1.y, y.x, zi[1]));
+    }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1)  // sum the 4 antenna phases t (lanes with equal g)
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        zr[m] += __shfl_xor_sync(0xffffffffu, zr[m], o);
+        zi[m] += __shfl_xor_sync(0xffffffffu, zi[m], o);
+      }
+    epilogue(acc, 1.0, nullptr, sigma2, V, g, t);  // A = HᴴH + σ²I (shared, planar)
+    // A's B-operand fragments in registers and X0 = diag(A)^-1
+    double areg[2][4][2];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int kb = 0; kb < 4; ++kb) {
+        const int idx = swz(4 * kb + t, 8 * nt + g);
+        areg[nt][kb][0] = V.re[idx];
+        areg[nt][kb][1] = V.im[idx];
+      }
+    for (int i = lane; i < kMat; i += 32) {
+      X.re[i] = 0.0;
+      X.im[i] = 0.0;
+    }
+    __syncwarp();
+    if (lane < kN) {
+      const double dr = V.re[swz(lane, lane)], di = V.im[swz(lane, lane)];
+      double xr, xi;
+      if (fabs(dr) >= fabs(di)) {
+        const double r = di / dr, den = dr + di * r;
+        xr = 1.0 / den;
+        xi = -r / den;
+      } else {
+        const double r = dr / di, den = dr * r + di;
+        xr = r / den;
+        xi = -1.0 / den;
+      }
+      X.re[swz(lane, lane)] = xr;
+      X.im[swz(lane, lane)] = xi;
+    }
+    __syncwarp();
+    // ---- Nested Neumann inversion ----
+    for (int it = 0; it < iters; ++it) {
+      acc.zero();
+      zmma_sr(acc, X, areg, g, t);
+      epilogue(acc, -1.0, nullptr, 1.0, Pm, g, t);
+      const SMat* v = &X;
+#pragma unroll
+      for (int j = 1; j <= P; ++j) {
+        acc.zero();
+        zmma_ss(acc, Pm, *v, g, t);
+        const SMat& dst = (j == P) ? X : V;
+        epilogue(acc, 1.0, &X, 0.0, dst, g, t);
+        v = &V;
+      }
+    }
+    if (eps_last) {
+      acc.zero();
+      zmma_sr(acc, X, areg, g, t);
+      const double ss = warp_sum(residual_ss(acc, g, t));
+      if (lane == 0) eps_last[s] = sqrt(ss) * 0.25;
+    }
+    // ---- x̂ = X·z: two lanes per row, 8 columns each ----
+    {
+      const int row = lane & 15, half = lane >> 4;
+      double sr = 0.0, si = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = 8 * half + jj;
+        const double z0r = __shfl_sync(0xffffffffu, zr[0], 4 * jj), z1r = __shfl_sync(0xffffffffu, zr[1], 4 * jj);
+        const double z0i = __shfl_sync(0xffffffffu, zi[0], 4 * jj), z1i = __shfl_sync(0xffffffffu, zi[1], 4 * jj);
+        const double vr = half ? z1r : z0r, vi = half ? z1i : z0i;
+        const double xr = X.re[swz(row, j)], xi = X.im[swz(row, j)];
+        sr = fma(xr, vr, fma(-xi, vi, sr));
+        si = fma(xr, vi, fma(xi, vr, si));
+      }
+      sr += __shfl_xor_sync(0xffffffffu, sr, 16);
+      si += __shfl_xor_sync(0xffffffffu, si, 16);
+      if (lane < kN) xhat[s * kN + lane] = make_double2(sr, si);
+    }
+    if (Xout) {
+      double2* Xs = Xout + s * kMat;
+#pragma unroll
+      for (int q = 0; q < kMat / 32; ++q) {
+        const int e = q * 32 + lane;
+        const int idx = swz(e / kN, e % kN);
+        Xs[e] = make_double2(X.re[idx], X.im[idx]);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 template <int P, bool M3, bool PF>
 int launch_variant(const double2* a, int64_t batch, int iters, int ns_order, double2* x, double* eps,
                    int ns_mode, cudaStream_t s) {
@@ -350,7 +483,42 @@ int launch_p(const double2* a, int64_t batch, int iters, int ns_order, double2* 
               : launch_variant<P, true, true>(a, batch, iters, ns_order, x, eps, ns_mode, s);
 }
 
+template <int P>
+int launch_mimo(const double2* h, const double2* y, int64_t batch, int ant, double sigma2, int iters,
+                double2* xhat, double2* X, double* eps, cudaStream_t s) {
+  static int blocks_per_sm = 0, sms = 0;
+  if (!blocks_per_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, mimo_detect_kernel<P>, kThreads, 0);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const int64_t want = (batch + kWarpsPerCta - 1) / kWarpsPerCta;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(want, (int64_t)sms * blocks_per_sm));
+  mimo_detect_kernel<P><<<grid, kThreads, 0, s>>>(h, y, batch, ant, sigma2, iters, xhat, X, eps);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
 }  // namespace
+
+int mimo_detect_z16(const double* H, const double* y, int64_t batch, int antennas, double sigma2, int p, int iters,
+                    double* xhat, double* X, double* eps_last, cudaStream_t s) {
+  if (batch <= 0) return 0;
+  const double2* h = reinterpret_cast<const double2*>(H);
+  const double2* yy = reinterpret_cast<const double2*>(y);
+  double2* xh = reinterpret_cast<double2*>(xhat);
+  double2* x = reinterpret_cast<double2*>(X);
+  switch (p) {
+    case 1: return launch_mimo<1>(h, yy, batch, antennas, sigma2, iters, xh, x, eps_last, s);
+    case 2: return launch_mimo<2>(h, yy, batch, antennas, sigma2, iters, xh, x, eps_last, s);
+    case 3: return launch_mimo<3>(h, yy, batch, antennas, sigma2, iters, xh, x, eps_last, s);
+    case 4: return launch_mimo<4>(h, yy, batch, antennas, sigma2, iters, xh, x, eps_last, s);
+    default: return fail(2, "mimo detect: depth p must be in 1..4");
+  }
+}
 
 int batched_nn_z16(const double* A, int64_t batch, int p, int iters, int ns_order, double* X,
                    double* eps_last, cudaStream_t s) {

@@ -513,6 +513,30 @@ int nnb_nn_batched_z(const double* A, int64_t batch, int32_t n, int32_t p, int32
   return batched(A, batch, n, p, iters, -1, X_out, eps_last, stream);
 }
 
+int nnb_mimo_detect_z(const double* H, const double* y, int64_t batch, int32_t antennas, int32_t users,
+                      double sigma2, int32_t p, int32_t iters, double* xhat_out, double* X_out, double* eps_last,
+                      void* stream) {
+  NNB_TRY(require_device());
+  if (users != 16) return fail(NNB_ERR_SHAPE, "mimo detect: only 16 users (16x16 Gram systems) are supported");
+  if (antennas < 4 || antennas % 4) return fail(NNB_ERR_SHAPE, "mimo detect: antennas must be a positive multiple of 4");
+  if (p < 1 || p > 4 || iters < 0) return fail(NNB_ERR_DOMAIN, "mimo detect: depth p in 1..4, iters >= 0");
+  if (batch < 0) return fail(NNB_ERR_SHAPE, "mimo detect: negative batch");
+  cudaStream_t s = resolve(stream);
+  In h, yy;
+  NNB_TRY(h.stage(H, (size_t)batch * antennas * users * 2, s));
+  NNB_TRY(yy.stage(y, (size_t)batch * antennas * 2, s));
+  Out xh, x, e;
+  NNB_TRY(xh.prepare(xhat_out, (size_t)batch * users * 2, s));
+  if (X_out) NNB_TRY(x.prepare(X_out, (size_t)batch * 512, s));
+  if (eps_last) NNB_TRY(e.prepare(eps_last, (size_t)batch, s));
+  NNB_TRY(mimo_detect_z16(h.d, yy.d, batch, antennas, sigma2, p, iters, xh.d, X_out ? x.d : nullptr,
+                          eps_last ? e.d : nullptr, s));
+  NNB_TRY(xh.finish(s));
+  if (X_out) NNB_TRY(x.finish(s));
+  if (eps_last) NNB_TRY(e.finish(s));
+  return 0;
+}
+
 int nnb_ns_batched_z(const double* A, int64_t batch, int32_t n, int32_t order, double* X_out,
                      void* stream) {
   if (order < 0) return fail(NNB_ERR_DOMAIN, "batched ns: order must be >= 0");

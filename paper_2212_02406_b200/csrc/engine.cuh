@@ -157,6 +157,8 @@ int axpby_z(double ar, double ai, const double* A, double br, double bi, const d
 // ---- batched / sparse (separate translation units) -------------------------------
 int batched_nn_z16(const double* A, int64_t batch, int p, int iters, int ns_order, double* X,
                    double* eps_last, cudaStream_t s);
+int mimo_detect_z16(const double* H, const double* y, int64_t batch, int antennas, double sigma2, int p,
+                    int iters, double* xhat, double* X, double* eps_last, cudaStream_t s);
 int spmv_csr(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n,
              const double* X, int64_t k, double* Y, cudaStream_t s);
 int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n,

@@ -70,6 +70,38 @@ def mimo_gram_device(batch: int, seed: int, antennas: int = 128, users: int = 16
     return out
 
 
+def mimo_uplink_host(batch: int, seed: int, antennas: int = 128, users: int = 16, sigma2: float = 0.1):
+    """Uplink y = H·s + n per system: H ~ CN(0, 1/antennas), QPSK symbols s (unit energy),
+    noise n ~ CN(0, sigma2/antennas).  Returns (H, y, s)."""
+    rng = np.random.default_rng(seed)
+    sh = np.sqrt(0.5 / antennas)
+    h = (rng.standard_normal((batch, antennas, users)) + 1j * rng.standard_normal((batch, antennas, users))) * sh
+    s = (rng.choice([-1.0, 1.0], (batch, users)) + 1j * rng.choice([-1.0, 1.0], (batch, users))) / np.sqrt(2)
+    sn = np.sqrt(0.5 * sigma2 / antennas)
+    noise = (rng.standard_normal((batch, antennas)) + 1j * rng.standard_normal((batch, antennas))) * sn
+    y = np.einsum("bau,bu->ba", h, s) + noise
+    return h, y, s
+
+
+def mimo_uplink_device(batch: int, seed: int, antennas: int = 128, users: int = 16, sigma2: float = 0.1,
+                       device: str = "cuda"):
+    """The same uplink on the GPU (torch Philox), for full-size runs."""
+    import torch
+
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    sh = (0.5 / antennas) ** 0.5
+    h = torch.complex(torch.randn((batch, antennas, users), dtype=torch.float64, device=device, generator=gen),
+                      torch.randn((batch, antennas, users), dtype=torch.float64, device=device, generator=gen)) * sh
+    bits = torch.randint(0, 2, (batch, users, 2), device=device, generator=gen).to(torch.float64) * 2 - 1
+    s = torch.complex(bits[..., 0], bits[..., 1]) / 2 ** 0.5
+    sn = (0.5 * sigma2 / antennas) ** 0.5
+    noise = torch.complex(torch.randn((batch, antennas), dtype=torch.float64, device=device, generator=gen),
+                          torch.randn((batch, antennas), dtype=torch.float64, device=device, generator=gen)) * sn
+    y = torch.einsum("bau,bu->ba", h, s) + noise
+    return h, y, s
+
+
 def laplacian_5pt(grid: int, shift: float = 1.0):
     """C5: Dirichlet 5-point Laplacian on a grid×grid mesh plus shift·I, CSR with
     ascending columns (row_ptr int64, col int32, val float64).  nnz = 5N − 4·grid."""

@@ -331,3 +331,34 @@ def test_sparse_full_size_property():
     # residual b − W x = P^64 b with ||P||_2 <= 0.8 (spec(W) in (1, 9), theta = 0.2)
     r = torch.linalg.norm(b - wx) / torch.linalg.norm(b)
     assert 0 < r.item() < 1.001 * 0.8 ** 64
+
+
+# ----------------------------------------------------------------- fused MIMO detection (§8(f) item 1)
+def test_mimo_detect_vs_oracle(port):
+    h, y, s = W.mimo_uplink_host(96, seed=4)
+    xh, X, eps = nnb.mimo_detect(h, y, sigma2=0.1, p=2, iters=4, want_x=True, want_eps=True)
+    # oracle: Gram formed on the host, the reference's batched chain, then X·(Hᴴy)
+    a = np.conj(np.transpose(h, (0, 2, 1))) @ h + 0.1 * np.eye(16)
+    xr, er = port.batched("nn", a, 2, 4, threads=8)
+    z = np.einsum("bau,ba->bu", np.conj(h), y)
+    xhr = np.einsum("bij,bj->bi", xr, z)
+    assert max(rel_frob(X[b], xr[b]) for b in range(96)) < TOL_X
+    assert max(rel_frob(xh[b], xhr[b]) for b in range(96)) < TOL_X
+    eps_close(eps, er)
+    # the detector recovers the QPSK symbols (SNR 10 dB, 128 antennas, 16 users)
+    det = (np.sign(xh.real) + 1j * np.sign(xh.imag)) / np.sqrt(2)
+    assert np.mean(det == s) > 0.999
+
+
+def test_mimo_detect_full_size():
+    import torch
+
+    h, y, s = W.mimo_uplink_device(262144, seed=2)
+    xh1, _, _ = nnb.mimo_detect(h, y)
+    xh2, _, _ = nnb.mimo_detect(h, y)
+    torch.cuda.synchronize()
+    assert torch.equal(xh1, xh2)
+    a = h.conj().transpose(1, 2) @ h + 0.1 * torch.eye(16, dtype=torch.complex128, device="cuda")
+    xref = torch.linalg.solve(a[::4096], torch.einsum("bau,ba->bu", h[::4096].conj(), y[::4096]))
+    rel = (torch.linalg.norm(xh1[::4096] - xref, dim=1) / torch.linalg.norm(xref, dim=1)).max().item()
+    assert rel < 1e-9
