@@ -141,6 +141,26 @@ int nnb_ns_sum_d(const double* phi0, const double* w, int64_t n, int64_t order, 
 int nnb_ns_sum_z(const double* phi0, const double* w, int64_t n, int64_t order, double* out,
                  double* products_out, void* stream);
 
+/* ---- product-form schedules on the same GEMM -- */
+/* Factorized Neumann series of order gamma = 2^s − 1,
+ * prod_{n<s} (I + P^{2^n}) phi0 with P = I − phi0 W~: nn::ns_factorized
+ * (proj/include/nn/factorized.hpp:48-54, proj/src/factorized.cpp:42-61). */
+int nnb_ns_factorized_d(const double* phi0, const double* w, int64_t n, int64_t gamma, double* out,
+                        double* products_out, void* stream);
+int nnb_ns_factorized_z(const double* phi0, const double* w, int64_t n, int64_t gamma, double* out,
+                        double* products_out, void* stream);
+/* p^exponent by square-and-multiply: nn::power_ladder (kernels.hpp:86-89). */
+int nnb_power_ladder_d(const double* p, int64_t n, uint64_t exponent, double* out, double* products_out,
+                       void* stream);
+int nnb_power_ladder_z(const double* p, int64_t n, uint64_t exponent, double* out, double* products_out,
+                       void* stream);
+/* Non-recursive product form of i nests of depth L: nn::nn_explicit
+ * (proj/include/nn/solver.hpp:87-92, proj/src/solver.cpp:176-199). */
+int nnb_nn_explicit_d(const double* phi0, const double* w, int64_t n, int64_t nests_i, int64_t depth_L,
+                      double* out, double* products_out, void* stream);
+int nnb_nn_explicit_z(const double* phi0, const double* w, int64_t n, int64_t nests_i, int64_t depth_L,
+                      double* out, double* products_out, void* stream);
+
 /* ---- batched small complex systems (massive-MIMO Gram inversion) ------- */
 /* batch independent n×n complex128 systems (n == 16), X0 = diag(A)^-1,
  * `iters` nests of depth p in reference order (nn_step per system) and the

@@ -234,6 +234,30 @@ class Reference(_Lib):
         self._check(st, fail.value)
         return out.reshape(b.shape), int(counts[0]), secs.value
 
+    def ns_factorized(self, phi0, w, gamma: int):
+        phi0, w = _z(phi0), _z(w)
+        out = np.empty_like(w)
+        n3 = C.c_double()
+        f = self.fn("ns_factorized_z", [_dp, _dp, C.c_int64, C.c_int64, _dp, _dp])
+        self._check(f(_ptr(phi0), _ptr(w), w.shape[0], gamma, _ptr(out), C.byref(n3)))
+        return out, n3.value
+
+    def power_ladder(self, p, e: int):
+        p = _z(p)
+        out = np.empty_like(p)
+        n3 = C.c_double()
+        f = self.fn("power_ladder_z", [_dp, C.c_int64, C.c_uint64, _dp, _dp])
+        self._check(f(_ptr(p), p.shape[0], e, _ptr(out), C.byref(n3)))
+        return out, n3.value
+
+    def nn_explicit(self, phi0, w, nests: int, depth: int):
+        phi0, w = _z(phi0), _z(w)
+        out = np.empty_like(w)
+        n3 = C.c_double()
+        f = self.fn("nn_explicit_z", [_dp, _dp, C.c_int64, C.c_int64, C.c_int64, _dp, _dp])
+        self._check(f(_ptr(phi0), _ptr(w), w.shape[0], nests, depth, _ptr(out), C.byref(n3)))
+        return out, n3.value
+
     def equivalent_ns_order(self, nests: int, depth: int) -> int:
         return self.fn("equivalent_ns_order", [C.c_int64, C.c_int64], C.c_uint64)(nests, depth)
 

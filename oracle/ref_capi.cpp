@@ -321,6 +321,35 @@ int nnref_sparse_factorized(const int64_t* row_ptr, const int32_t* col, const do
   }, fail_index);
 }
 
+// nn::ns_factorized (proj/src/factorized.cpp:42-61), nn::power_ladder
+// (proj/src/kernels.cpp:434-452), nn::nn_explicit (proj/src/solver.cpp:176-199).
+int nnref_ns_factorized_z(const double* phi0, const double* w, int64_t n, int64_t gamma, double* out,
+                          double* n3) {
+  return guarded([&] {
+    nn::OpCounter cnt;
+    const auto plan = nn::FactorizedPlan::for_order(nn::BigInt(gamma), nn::FactorizedMode::DenseStored);
+    store(nn::ns_factorized(load(phi0, n, n), load(w, n, n), plan, &cnt), out);
+    if (n3) *n3 = cnt.n3_multiplies();
+  });
+}
+int nnref_power_ladder_z(const double* p, int64_t n, uint64_t e, double* out, double* n3) {
+  return guarded([&] {
+    nn::OpCounter cnt;
+    store(nn::power_ladder(load(p, n, n), e, &cnt), out);
+    if (n3) *n3 = cnt.n3_multiplies();
+  });
+}
+int nnref_nn_explicit_z(const double* phi0, const double* w, int64_t n, int64_t nests, int64_t depth,
+                        double* out, double* n3) {
+  return guarded([&] {
+    nn::OpCounter cnt;
+    store(nn::nn_explicit(load(phi0, n, n), load(w, n, n), static_cast<std::size_t>(nests),
+                          static_cast<std::size_t>(depth), &cnt),
+          out);
+    if (n3) *n3 = cnt.n3_multiplies();
+  });
+}
+
 // nn::equivalent_ns_order (proj/src/solver.cpp:201-205), saturating.
 uint64_t nnref_equivalent_ns_order(int64_t nests, int64_t depth) {
   const auto v = nn::equivalent_ns_order(static_cast<std::size_t>(nests),

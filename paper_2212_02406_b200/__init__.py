@@ -105,6 +105,12 @@ _SIGS = {
     "nnb_ns_sum_z": ([_dp, _dp, _i64, _i64, _dp, _dp, _dp], C.c_int),
     "nnb_nn_batched_z": ([_dp, _i64, _i32, _i32, _i32, _dp, _dp, _dp], C.c_int),
     "nnb_ns_batched_z": ([_dp, _i64, _i32, _i32, _dp, _dp], C.c_int),
+    "nnb_ns_factorized_d": ([_dp, _dp, _i64, _i64, _dp, _dp, _dp], C.c_int),
+    "nnb_ns_factorized_z": ([_dp, _dp, _i64, _i64, _dp, _dp, _dp], C.c_int),
+    "nnb_power_ladder_d": ([_dp, _i64, C.c_uint64, _dp, _dp, _dp], C.c_int),
+    "nnb_power_ladder_z": ([_dp, _i64, C.c_uint64, _dp, _dp, _dp], C.c_int),
+    "nnb_nn_explicit_d": ([_dp, _dp, _i64, _i64, _i64, _dp, _dp, _dp], C.c_int),
+    "nnb_nn_explicit_z": ([_dp, _dp, _i64, _i64, _i64, _dp, _dp, _dp], C.c_int),
     "nnb_mimo_detect_z": ([_dp, _dp, _i64, _i32, _i32, C.c_double, _i32, _i32, _dp, _dp, _dp, _dp], C.c_int),
     "nnb_spmv_block_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _dp, _dp], C.c_int),
     "nnb_sparse_factorized_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _i64, C.c_double, _dp, _dp, _dp,
@@ -352,6 +358,43 @@ def ns_sum(phi0, w_tilde, order: int):
     prods = C.c_double()
     f = lib().nnb_ns_sum_z if z else lib().nnb_ns_sum_d
     _check(f(_ptr(phi0), _ptr(w), w.shape[0], int(order), _ptr(out), C.addressof(prods), _stream(w)))
+    return out, prods.value
+
+
+def ns_factorized(phi0, w_tilde, gamma: int):
+    """Factorized Neumann series of order gamma = 2^s-1 (proj/src/factorized.cpp:42-61). Returns (sum, products)."""
+    _square_conform(phi0, w_tilde, "ns_factorized")
+    z = _is_complex(phi0, w_tilde)
+    phi0, w = _prep(phi0, z), _prep(w_tilde, z)
+    out = _empty_like(phi0)
+    prods = C.c_double()
+    f = lib().nnb_ns_factorized_z if z else lib().nnb_ns_factorized_d
+    _check(f(_ptr(phi0), _ptr(w), w.shape[0], int(gamma), _ptr(out), C.addressof(prods), _stream(w)))
+    return out, prods.value
+
+
+def power_ladder(p, exponent: int):
+    """p^exponent by square-and-multiply (proj/src/kernels.cpp:434-452). Returns (power, products)."""
+    if p.shape[0] != p.shape[1]:
+        raise ShapeError("power_ladder: matrix must be square")
+    z = _is_complex(p)
+    p = _prep(p, z)
+    out = _empty_like(p)
+    prods = C.c_double()
+    f = lib().nnb_power_ladder_z if z else lib().nnb_power_ladder_d
+    _check(f(_ptr(p), p.shape[0], int(exponent), _ptr(out), C.addressof(prods), _stream(p)))
+    return out, prods.value
+
+
+def nn_explicit(phi0, w_tilde, nests_i: int, depth_L: int):
+    """Non-recursive product form of nests_i+1 nests of depth L (proj/src/solver.cpp:176-199)."""
+    _square_conform(phi0, w_tilde, "nn_explicit")
+    z = _is_complex(phi0, w_tilde)
+    phi0, w = _prep(phi0, z), _prep(w_tilde, z)
+    out = _empty_like(phi0)
+    prods = C.c_double()
+    f = lib().nnb_nn_explicit_z if z else lib().nnb_nn_explicit_d
+    _check(f(_ptr(phi0), _ptr(w), w.shape[0], int(nests_i), int(depth_L), _ptr(out), C.addressof(prods), _stream(w)))
     return out, prods.value
 
 

@@ -435,6 +435,108 @@ int nnb_ns_sum_z(const double* phi0, const double* w, int64_t n, int64_t order, 
   return o.store(out, s);
 }
 
+// ---------------------------------------------------------------- product-form schedules
+// (the same fused GEMM, different schedules)
+namespace {
+enum class Sched { Factorized, Ladder, Explicit };
+
+int sched_d(Sched which, const double* phi0, const double* w, int64_t n, int64_t a, int64_t b, double* out,
+            double* products, void* stream) {
+  NNB_TRY(require_device());
+  cudaStream_t s = resolve(stream);
+  DMat p, wm, o;
+  NNB_TRY(p.load(phi0, n, n, n, s, false));
+  if (w) NNB_TRY(wm.load(w, n, n, n, s, false));
+  NNB_TRY(o.alloc(n, n, s));
+  bool ident = false;
+  if (which != Sched::Ladder) NNB_TRY(is_identity_dev(p.d, nullptr, n, p.ld, &ident, s));
+  switch (which) {
+    case Sched::Factorized:
+      NNB_TRY(ns_factorized_dev(p.d, nullptr, wm.d, nullptr, n, p.ld, (int)a, ident, o.d, nullptr, products, s));
+      break;
+    case Sched::Ladder:
+      NNB_TRY(power_ladder_dev(p.d, nullptr, n, p.ld, (uint64_t)a, o.d, nullptr, products, s));
+      break;
+    default:
+      NNB_TRY(nn_explicit_dev(p.d, nullptr, wm.d, nullptr, n, p.ld, (int)a, (int)b, ident, o.d, nullptr, products, s));
+  }
+  NNB_TRY(o.store(out, n, s));
+  return sync(s);
+}
+
+int sched_z(Sched which, const double* phi0, const double* w, int64_t n, int64_t a, int64_t b, double* out,
+            double* products, void* stream) {
+  NNB_TRY(require_device());
+  cudaStream_t s = resolve(stream);
+  ZMat p, wm, o;
+  NNB_TRY(p.load(phi0, n, n, s));
+  if (w) NNB_TRY(wm.load(w, n, n, s));
+  NNB_TRY(o.alloc(n, n, s));
+  bool ident = false;
+  if (which != Sched::Ladder) NNB_TRY(is_identity_dev(p.re, p.im, n, p.ld, &ident, s));
+  switch (which) {
+    case Sched::Factorized:
+      NNB_TRY(ns_factorized_dev(p.re, p.im, wm.re, wm.im, n, p.ld, (int)a, ident, o.re, o.im, products, s));
+      break;
+    case Sched::Ladder:
+      NNB_TRY(power_ladder_dev(p.re, p.im, n, p.ld, (uint64_t)a, o.re, o.im, products, s));
+      break;
+    default:
+      NNB_TRY(nn_explicit_dev(p.re, p.im, wm.re, wm.im, n, p.ld, (int)a, (int)b, ident, o.re, o.im, products, s));
+  }
+  return o.store(out, s);
+}
+
+int factor_count(int64_t gamma, int64_t* s_factors) {
+  if (gamma < 1 || ((gamma + 1) & gamma) != 0)
+    return fail(NNB_ERR_PLAN, "FactorizedPlan: order + 1 must be a power of two");
+  *s_factors = 0;
+  for (int64_t g = gamma + 1; g > 1; g >>= 1) ++*s_factors;
+  return 0;
+}
+
+int explicit_budget(int64_t nests_i, int64_t depth_L) {
+  // (L+1)^i must stay below 2^62 (proj/src/solver.cpp:182-185)
+  long double v = 1.0L;
+  for (int64_t i = 0; i < nests_i; ++i) {
+    v *= static_cast<long double>(depth_L + 1);
+    if (v > 4611686018427387904.0L) return fail(NNB_ERR_BUDGET, "nn_explicit: inner power (L+1)^i is not representable");
+  }
+  return 0;
+}
+}  // namespace
+
+int nnb_ns_factorized_d(const double* phi0, const double* w, int64_t n, int64_t gamma, double* out,
+                        double* products_out, void* stream) {
+  int64_t sf = 0;
+  NNB_TRY(factor_count(gamma, &sf));
+  return sched_d(Sched::Factorized, phi0, w, n, sf, 0, out, products_out, stream);
+}
+int nnb_ns_factorized_z(const double* phi0, const double* w, int64_t n, int64_t gamma, double* out,
+                        double* products_out, void* stream) {
+  int64_t sf = 0;
+  NNB_TRY(factor_count(gamma, &sf));
+  return sched_z(Sched::Factorized, phi0, w, n, sf, 0, out, products_out, stream);
+}
+int nnb_power_ladder_d(const double* p, int64_t n, uint64_t exponent, double* out, double* products_out,
+                       void* stream) {
+  return sched_d(Sched::Ladder, p, nullptr, n, (int64_t)exponent, 0, out, products_out, stream);
+}
+int nnb_power_ladder_z(const double* p, int64_t n, uint64_t exponent, double* out, double* products_out,
+                       void* stream) {
+  return sched_z(Sched::Ladder, p, nullptr, n, (int64_t)exponent, 0, out, products_out, stream);
+}
+int nnb_nn_explicit_d(const double* phi0, const double* w, int64_t n, int64_t nests_i, int64_t depth_L,
+                      double* out, double* products_out, void* stream) {
+  NNB_TRY(explicit_budget(nests_i, depth_L));
+  return sched_d(Sched::Explicit, phi0, w, n, nests_i, depth_L, out, products_out, stream);
+}
+int nnb_nn_explicit_z(const double* phi0, const double* w, int64_t n, int64_t nests_i, int64_t depth_L,
+                      double* out, double* products_out, void* stream) {
+  NNB_TRY(explicit_budget(nests_i, depth_L));
+  return sched_z(Sched::Explicit, phi0, w, n, nests_i, depth_L, out, products_out, stream);
+}
+
 // ---------------------------------------------------------------- batched
 // Host-to-host calls stream the batch through the device in chunks on three
 // rotating lanes (stream per lane): H2D of chunk i+1, the kernel on chunk i

@@ -284,7 +284,239 @@ int run_ns_sum(Ctx& c, const Plane& phi0, const Plane& W, int64_t order, bool id
   return 0;
 }
 
+// ---- product-form schedules on the same GEMM ----
+struct Pool {  // n×ld plane sets carved from one allocation
+  DevBuf buf;
+  int count = 0;
+  int64_t mat = 0;
+  bool cplx = false;
+  int init(Ctx& c, int k) {
+    count = k;
+    mat = c.n * c.ld;
+    cplx = c.cplx;
+    NNB_TRY(buf.alloc(sizeof(double) * (size_t)mat * (cplx ? 2 : 1) * k, c.s));
+    return 0;
+  }
+  Plane at(int i) const {
+    double* base = buf.as<double>() + (size_t)i * mat * (cplx ? 2 : 1);
+    return Plane{base, cplx ? base + mat : nullptr};
+  }
+};
+
+int copy_plane(Ctx& c, const Plane& src, const Plane& dst) {
+  NNB_TRY(copy2d(src.re, c.ld, dst.re, c.ld, c.n, c.n, c.s));
+  if (c.cplx) NNB_TRY(copy2d(src.im, c.ld, dst.im, c.ld, c.n, c.n, c.s));
+  return 0;
+}
+
+// dst = alpha·src + gamma·I (per plane; gamma on the real plane only)
+int shift_plane(Ctx& c, const Plane& src, double alpha, double gamma, const Plane& dst) {
+  NNB_TRY(axpby(alpha, src.re, c.ld, 0.0, nullptr, 0, gamma, 0, dst.re, c.ld, c.n, c.n, c.s));
+  if (c.cplx) NNB_TRY(axpby(alpha, src.im, c.ld, 0.0, nullptr, 0, 0.0, 0, dst.im, c.ld, c.n, c.n, c.s));
+  return 0;
+}
+
+int nf_slot(Ctx& c, std::vector<int>& slots_used) {
+  slots_used.push_back(0);
+  return static_cast<int>(slots_used.size()) - 1;
+}
+
+// p^e by binary square-and-multiply (power_ladder, proj/src/kernels.cpp:434-452);
+// result into `out`; products counted as the reference does.
+int ladder(Ctx& c, const Plane& p, uint64_t e, const Plane& out, Pool& tmp, int t0, double* prods, int* nf) {
+  if (e == 0) return shift_plane(c, p, 0.0, 1.0, out);
+  // running square in tmp[t0 .. t0+1], accumulator in tmp[t0+2 .. t0+3] (ping-pong)
+  Plane sq = p;
+  int sq_i = -1, acc_i = -1;
+  while (e > 0) {
+    if (e & 1) {
+      if (acc_i >= 0) {
+        const int dst = acc_i == t0 + 2 ? t0 + 3 : t0 + 2;
+        NNB_TRY(product(c, tmp.at(acc_i), sq, 1.0, nullptr, 0.0, 0.0, tmp.at(dst), nullptr, nf));
+        *prods += 1;
+        acc_i = dst;
+      } else {
+        acc_i = t0 + 2;  // acc = sq (a value copy, like the reference's assignment)
+        NNB_TRY(copy_plane(c, sq, tmp.at(acc_i)));
+      }
+    }
+    e >>= 1;
+    if (e > 0) {
+      const int dst = sq_i == t0 ? t0 + 1 : t0;
+      NNB_TRY(product(c, sq, sq, 1.0, nullptr, 0.0, 0.0, tmp.at(dst), nullptr, nf));
+      *prods += 1;
+      sq = tmp.at(dst);
+      sq_i = dst;
+    }
+  }
+  return copy_plane(c, tmp.at(acc_i), out);
+}
+
+// S = sum_{n=0}^{L} q^n as I + q(I + q(...)) (horner_power_sum, proj/src/solver.cpp:27-36)
+int horner_sum(Ctx& c, const Plane& q, int L, const Plane& out, Pool& tmp, int t0, double* prods, int* nf) {
+  if (L == 0) return shift_plane(c, q, 0.0, 1.0, out);
+  NNB_TRY(shift_plane(c, q, 1.0, 1.0, tmp.at(t0)));  // I + q
+  int cur = t0;
+  for (int j = 2; j <= L; ++j) {
+    const int dst = cur == t0 ? t0 + 1 : t0;
+    NNB_TRY(product(c, q, tmp.at(cur), 1.0, nullptr, 0.0, 1.0, tmp.at(dst), nullptr, nf));  // I + q·S
+    *prods += 1;
+    cur = dst;
+  }
+  return copy_plane(c, tmp.at(cur), out);
+}
+
 }  // namespace
+
+// ns_factorized (proj/src/factorized.cpp:42-61): P = I − phi0·W~ (skipped when
+// phi0 = I), acc = Π_{n<s} (I + P^{2^n}) by acc ← acc + acc·P and P ← P·P,
+// then acc·phi0.  Tally: 2s−1 from the identity, 2s+1 otherwise.
+int ns_factorized_dev(const double* phi_re, const double* phi_im, const double* w_re, const double* w_im,
+                      int64_t n, int64_t ldn, int s_factors, bool identity_start, double* out_re, double* out_im,
+                      double* products, cudaStream_t s) {
+  Ctx c;
+  c.n = n;
+  c.ld = ldn;
+  c.cplx = w_im != nullptr;
+  c.s = s;
+  NNB_TRY(c.red.init(max_tiles_for(n, n), s));
+  DevBuf nfb;
+  NNB_TRY(nfb.alloc(sizeof(int) * 8 + sizeof(double) * 8, s));
+  NNB_CUDA(cudaMemsetAsync(nfb.p, 0, nfb.bytes, s));
+  int* nf = nfb.as<int>();
+  c.nf2 = nf + 2;
+  c.ss2 = reinterpret_cast<double*>(nf + 4);
+  Pool pool;
+  NNB_TRY(pool.init(c, 4));  // P0 P1 A0 A1
+  Plane phi{const_cast<double*>(phi_re), const_cast<double*>(phi_im)};
+  Plane w{const_cast<double*>(w_re), const_cast<double*>(w_im)};
+  double prods = 0;
+  int pi = 0, ai = 2;
+  if (identity_start) {
+    NNB_TRY(shift_plane(c, w, -1.0, 1.0, pool.at(0)));
+  } else {
+    NNB_TRY(product(c, phi, w, -1.0, nullptr, 0.0, 1.0, pool.at(0), nullptr, nf));
+    prods += 1;
+  }
+  for (int f = 0; f < s_factors; ++f) {
+    if (f == 0) {
+      NNB_TRY(shift_plane(c, pool.at(pi), 1.0, 1.0, pool.at(ai)));  // I·(I + P)
+    } else {
+      const int dst = ai == 2 ? 3 : 2;
+      const Plane acc = pool.at(ai);
+      NNB_TRY(product(c, acc, pool.at(pi), 1.0, &acc, 1.0, 0.0, pool.at(dst), nullptr, nf));  // acc + acc·P
+      ai = dst;
+    }
+    prods += 1;  // the reference multiplies acc·(I+P) on every factor
+    if (f + 1 < s_factors) {
+      const int dst = pi == 0 ? 1 : 0;
+      NNB_TRY(product(c, pool.at(pi), pool.at(pi), 1.0, nullptr, 0.0, 0.0, pool.at(dst), nullptr, nf));
+      pi = dst;
+      prods += 1;
+    }
+  }
+  Plane out{out_re, out_im};
+  if (identity_start) {
+    NNB_TRY(copy_plane(c, pool.at(ai), out));
+  } else {
+    NNB_TRY(product(c, pool.at(ai), phi, 1.0, nullptr, 0.0, 0.0, out, nullptr, nf));
+    prods += 1;
+  }
+  int h = 0;
+  NNB_CUDA(cudaMemcpyAsync(&h, nf, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  if (products) *products = prods;
+  if (h) return fail(2, "ns_factorized: matmul produced a non-finite entry");
+  return 0;
+}
+
+// power_ladder (proj/src/kernels.cpp:434-452) on the device.
+int power_ladder_dev(const double* p_re, const double* p_im, int64_t n, int64_t ldn, uint64_t e, double* out_re,
+                     double* out_im, double* products, cudaStream_t s) {
+  Ctx c;
+  c.n = n;
+  c.ld = ldn;
+  c.cplx = p_im != nullptr;
+  c.s = s;
+  NNB_TRY(c.red.init(max_tiles_for(n, n), s));
+  DevBuf nfb;
+  NNB_TRY(nfb.alloc(sizeof(int) * 8 + sizeof(double) * 8, s));
+  NNB_CUDA(cudaMemsetAsync(nfb.p, 0, nfb.bytes, s));
+  int* nf = nfb.as<int>();
+  c.nf2 = nf + 2;
+  c.ss2 = reinterpret_cast<double*>(nf + 4);
+  Pool pool;
+  NNB_TRY(pool.init(c, 4));
+  double prods = 0;
+  NNB_TRY(ladder(c, Plane{const_cast<double*>(p_re), const_cast<double*>(p_im)}, e, Plane{out_re, out_im}, pool, 0,
+                 &prods, nf));
+  int h = 0;
+  NNB_CUDA(cudaMemcpyAsync(&h, nf, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  if (products) *products = prods;
+  if (h) return fail(2, "power_ladder: matmul produced a non-finite entry");
+  return 0;
+}
+
+// nn_explicit (proj/src/solver.cpp:176-199): Q = I − phi0·W~, acc = Π_{j=0}^{i}
+// S_L(Q^{(L+1)^j}) with the inner powers by the ladder, then acc·phi0.
+int nn_explicit_dev(const double* phi_re, const double* phi_im, const double* w_re, const double* w_im, int64_t n,
+                    int64_t ldn, int nests_i, int depth_L, bool identity_start, double* out_re, double* out_im,
+                    double* products, cudaStream_t s) {
+  Ctx c;
+  c.n = n;
+  c.ld = ldn;
+  c.cplx = w_im != nullptr;
+  c.s = s;
+  NNB_TRY(c.red.init(max_tiles_for(n, n), s));
+  DevBuf nfb;
+  NNB_TRY(nfb.alloc(sizeof(int) * 8 + sizeof(double) * 8, s));
+  NNB_CUDA(cudaMemsetAsync(nfb.p, 0, nfb.bytes, s));
+  int* nf = nfb.as<int>();
+  c.nf2 = nf + 2;
+  c.ss2 = reinterpret_cast<double*>(nf + 4);
+  Pool pool;
+  NNB_TRY(pool.init(c, 10));  // Q0 Q1 | F | A0 A1 | horner tmp (2) | ladder tmp (4) share 5..9
+  Plane phi{const_cast<double*>(phi_re), const_cast<double*>(phi_im)};
+  Plane w{const_cast<double*>(w_re), const_cast<double*>(w_im)};
+  double prods = 0;
+  int qi = 0, ai = 3;
+  if (identity_start) {
+    NNB_TRY(shift_plane(c, w, -1.0, 1.0, pool.at(0)));
+  } else {
+    NNB_TRY(product(c, phi, w, -1.0, nullptr, 0.0, 1.0, pool.at(0), nullptr, nf));
+    prods += 1;
+  }
+  for (int j = 0; j <= nests_i; ++j) {
+    NNB_TRY(horner_sum(c, pool.at(qi), depth_L, pool.at(2), pool, 5, &prods, nf));
+    if (j == 0) {
+      NNB_TRY(copy_plane(c, pool.at(2), pool.at(ai)));
+    } else {
+      const int dst = ai == 3 ? 4 : 3;
+      NNB_TRY(product(c, pool.at(2), pool.at(ai), 1.0, nullptr, 0.0, 0.0, pool.at(dst), nullptr, nf));
+      ai = dst;
+      prods += 1;
+    }
+    if (j < nests_i) {
+      const int dst = qi == 0 ? 1 : 0;
+      NNB_TRY(ladder(c, pool.at(qi), static_cast<uint64_t>(depth_L) + 1, pool.at(dst), pool, 5, &prods, nf));
+      qi = dst;
+    }
+  }
+  Plane out{out_re, out_im};
+  if (identity_start) {
+    NNB_TRY(copy_plane(c, pool.at(ai), out));
+  } else {
+    NNB_TRY(product(c, pool.at(ai), phi, 1.0, nullptr, 0.0, 0.0, out, nullptr, nf));
+    prods += 1;
+  }
+  int h = 0;
+  NNB_CUDA(cudaMemcpyAsync(&h, nf, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  if (products) *products = prods;
+  if (h) return fail(2, "nn_explicit: matmul produced a non-finite entry");
+  return 0;
+}
 
 int ns_sum_dev(const double* phi0_re, const double* phi0_im, const double* w_re,
                const double* w_im, int64_t n, int64_t ldn, int64_t order, bool identity_start,

@@ -145,6 +145,14 @@ int chain_complex(const double* Ar, const double* Ai, int64_t n, int64_t ldn, do
 int ns_sum_dev(const double* phi0_re, const double* phi0_im, const double* w_re,
                const double* w_im, int64_t n, int64_t ldn, int64_t order, bool identity_start,
                double* out_re, double* out_im, double* products, cudaStream_t s);
+int ns_factorized_dev(const double* phi_re, const double* phi_im, const double* w_re, const double* w_im,
+                      int64_t n, int64_t ldn, int s_factors, bool identity_start, double* out_re, double* out_im,
+                      double* products, cudaStream_t s);
+int power_ladder_dev(const double* p_re, const double* p_im, int64_t n, int64_t ldn, uint64_t e, double* out_re,
+                     double* out_im, double* products, cudaStream_t s);
+int nn_explicit_dev(const double* phi_re, const double* phi_im, const double* w_re, const double* w_im, int64_t n,
+                    int64_t ldn, int nests_i, int depth_L, bool identity_start, double* out_re, double* out_im,
+                    double* products, cudaStream_t s);
 int is_identity_dev(const double* re, const double* im, int64_t n, int64_t ld, bool* result,
                     cudaStream_t s);
 int deinterleave2d(const double* z, int64_t rows, int64_t cols, double* re, double* im,

@@ -9,10 +9,9 @@
 // bookkeeping (reports, nest estimates, order fits).
 //
 // Out of scope (not declared; link the reference's nncore for them):
-// direct_inverse_oracle, random_* generators, power_ladder, matvec,
-// conjugate_transpose, theta_power, contraction_check, nn_explicit,
-// ns_factorized, solve_normal_equations, cns_invert, the cost model and
-// Matrix Market I/O.
+// direct_inverse_oracle, random_* generators, matvec, conjugate_transpose,
+// theta_power, contraction_check, solve_normal_equations, cns_invert, the
+// cost model and Matrix Market I/O.
 #pragma once
 
 #include <atomic>
@@ -235,6 +234,8 @@ SpectralEstimate spectral_norm_estimate_shifted(const SparseMatrixCsr& w, Scalar
                                                 std::uint64_t seed = 0x5eed5eedULL);
 DenseMatrix spmv_block(const SparseMatrixCsr& p, const DenseMatrix& x,
                        OpCounter* counter = nullptr);
+/// p^exponent by square-and-multiply; floor(log2 e) + popcount(e) − 1 products.
+DenseMatrix power_ladder(const DenseMatrix& p, std::uint64_t exponent, OpCounter* counter = nullptr);
 
 // ------------------------------------------------------------------ normalization
 enum class ThetaKind { TraceTheta1, PowerTheta2 };
@@ -288,6 +289,8 @@ DenseMatrix chebyshev_step(const DenseMatrix& z, const DenseMatrix& w_tilde,
 std::pair<DenseMatrix, ConvergenceReport> nn_invert(const DenseMatrix& w, const Normalization& norm,
                                                     const SolverConfig& config,
                                                     OpCounter* counter = nullptr);
+DenseMatrix nn_explicit(const DenseMatrix& phi0, const DenseMatrix& w_tilde, std::size_t nests_i,
+                        std::size_t depth_L, OpCounter* counter = nullptr);
 BigInt equivalent_ns_order(std::size_t nests_i, std::size_t depth_L);
 std::size_t estimate_nests(double kappa, std::size_t depth_L);
 double convergence_order_estimate(const ConvergenceReport& report);
@@ -315,6 +318,8 @@ struct NonConvergenceError : Error {
       : Error(what), report(std::move(rep)) {}
   ConvergenceReport report;
 };
+DenseMatrix ns_factorized(const DenseMatrix& phi, const DenseMatrix& w_tilde, const FactorizedPlan& plan,
+                          OpCounter* counter = nullptr);
 DenseMatrix solve_sparse_factorized(const LinearSystem& sys, const BigInt& gamma,
                                     const Normalization& norm, OpCounter* counter = nullptr);
 

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <numeric>
+#include <functional>
 #include <sstream>
 
 #include "nn/nnb_dropin.hpp"
@@ -127,6 +128,24 @@ DenseMatrix device_nest(const DenseMatrix& phi, const DenseMatrix& w, std::size_
   }
   DenseMatrix out(n, n);
   check(nnb_nn_step_z(zp(phi), zp(w), (int64_t)n, (int32_t)depth, zp(out), nullptr), who);
+  return out;
+}
+
+// Product-form schedules through the C-ABI (real data → _d, complex → _z).
+using SchedD = int (*)(const double*, const double*, int64_t, int64_t, int64_t, double*, double*);
+DenseMatrix run_schedule(const DenseMatrix& a, const DenseMatrix* b, int64_t x, int64_t y,
+                         const std::function<int(const double*, const double*, double*, double*, bool)>& call,
+                         double* products, const char* who) {
+  const std::size_t n = a.rows();
+  DenseMatrix out(n, n);
+  if (real_valued(a) && (!b || real_valued(*b))) {
+    const auto ar = real_part(a);
+    std::vector<double> br = b ? real_part(*b) : std::vector<double>();
+    std::vector<double> o(n * n);
+    check(call(ar.data(), b ? br.data() : nullptr, o.data(), products, false), who);
+    return from_real(n, n, o);
+  }
+  check(call(zp(a), b ? zp(*b) : nullptr, zp(out), products, true), who);
   return out;
 }
 
@@ -389,6 +408,22 @@ DenseMatrix spmv_block(const SparseMatrixCsr& p, const DenseMatrix& x, OpCounter
   return out;
 }
 
+DenseMatrix power_ladder(const DenseMatrix& p, std::uint64_t exponent, OpCounter* counter) {
+  // proj/src/kernels.cpp:434-452 on the device
+  if (!p.square()) throw ShapeError("power_ladder: matrix must be square");
+  if (exponent == 0) return DenseMatrix::identity(p.rows());
+  double prods = 0;
+  const int64_t n = (int64_t)p.rows();
+  DenseMatrix out = run_schedule(
+      p, nullptr, 0, 0,
+      [&](const double* a, const double*, double* o, double* pr, bool z) {
+        return z ? nnb_power_ladder_z(a, n, exponent, o, pr, nullptr) : nnb_power_ladder_d(a, n, exponent, o, pr, nullptr);
+      },
+      &prods, "power_ladder");
+  if (counter) counter->add_n3(prods);
+  return out;
+}
+
 // ====================================================================== normalization
 static double positive_real_trace(Scalar t, const char* who) {
   // proj/src/normalization.cpp:25-33
@@ -576,6 +611,28 @@ std::pair<DenseMatrix, ConvergenceReport> nn_invert(const DenseMatrix& w, const 
   return {scale(phi, Scalar{norm.theta, 0.0}, counter), report};
 }
 
+DenseMatrix nn_explicit(const DenseMatrix& phi0, const DenseMatrix& w_tilde, std::size_t nests_i,
+                        std::size_t depth_L, OpCounter* counter) {
+  // proj/src/solver.cpp:176-199 on the device (BudgetError as the reference)
+  conform_square(phi0, w_tilde, "nn_explicit");
+  if (pow_big(BigInt(depth_L + 1), static_cast<unsigned>(nests_i)) > (BigInt(1) << 62))
+    throw BudgetError("nn_explicit: inner power (L+1)^i is not representable");
+  double prods = 0;
+  const int64_t n = (int64_t)w_tilde.rows();
+  DenseMatrix out = run_schedule(
+      phi0, &w_tilde, 0, 0,
+      [&](const double* a, const double* b, double* o, double* pr, bool z) {
+        return z ? nnb_nn_explicit_z(a, b, n, (int64_t)nests_i, (int64_t)depth_L, o, pr, nullptr)
+                 : nnb_nn_explicit_d(a, b, n, (int64_t)nests_i, (int64_t)depth_L, o, pr, nullptr);
+      },
+      &prods, "nn_explicit");
+  if (counter) {
+    counter->add_n3(prods);
+    counter->add_n2(1 + static_cast<std::int64_t>((nests_i + 1) * depth_L));  // identity_minus + plus_identity's
+  }
+  return out;
+}
+
 BigInt equivalent_ns_order(std::size_t nests_i, std::size_t depth_L) {
   return pow_big(BigInt(depth_L + 1), static_cast<unsigned>(nests_i + 1)) - 1;
 }
@@ -630,6 +687,27 @@ FactorizedPlan FactorizedPlan::for_order(const BigInt& gamma, FactorizedMode mod
   plan.num_factors = msb_of(gamma + BigInt(1));
   plan.mode = mode;
   return plan;
+}
+
+DenseMatrix ns_factorized(const DenseMatrix& phi, const DenseMatrix& w_tilde, const FactorizedPlan& plan,
+                          OpCounter* counter) {
+  // proj/src/factorized.cpp:42-61 on the device: 2s−1 products from the identity, 2s+1 otherwise
+  if (plan.mode != FactorizedMode::DenseStored) throw PlanError("ns_factorized: plan must be in dense mode");
+  conform_square(phi, w_tilde, "ns_factorized");
+  double prods = 0;
+  const int64_t n = (int64_t)w_tilde.rows();
+  const int64_t gamma = static_cast<int64_t>(static_cast<unsigned long long>(plan.gamma));
+  DenseMatrix out = run_schedule(
+      phi, &w_tilde, 0, 0,
+      [&](const double* a, const double* b, double* o, double* pr, bool z) {
+        return z ? nnb_ns_factorized_z(a, b, n, gamma, o, pr, nullptr) : nnb_ns_factorized_d(a, b, n, gamma, o, pr, nullptr);
+      },
+      &prods, "ns_factorized");
+  if (counter) {
+    counter->add_n3(prods);
+    counter->add_n2(static_cast<std::int64_t>(plan.num_factors) + 1);  // identity_minus + s plus_identity
+  }
+  return out;
 }
 
 DenseMatrix solve_sparse_factorized(const LinearSystem& sys, const BigInt& gamma, const Normalization& norm,

@@ -321,6 +321,11 @@ static void device_tests() {
       pw = matmul(pw, pw);
     }
     CHECK(rel(xs, scale(matmul(acc, rhs), Scalar{nm.theta, 0})) < 1e-11);
+    // the same through the dense factorized series (proj/tests/test_factorized.cpp:170-186)
+    const auto plan15 = FactorizedPlan::for_order(15, FactorizedMode::DenseStored);
+    const DenseMatrix wt_dense = scale(w.densify(), Scalar{nm.theta, 0});
+    CHECK(rel(xs, scale(matmul(ns_factorized(DenseMatrix::identity(n), wt_dense, plan15), rhs),
+                        Scalar{nm.theta, 0})) < 1e-11);
     // identity system: theta = 1/8, x = (1 - (7/8)^16) B
     const SparseMatrixCsr I8 = SparseMatrixCsr::identity(8);
     const DenseMatrix b8 = gauss(8, 8, 10);
@@ -339,10 +344,53 @@ static void device_tests() {
   }
 }
 
+// ns_factorized / power_ladder / nn_explicit (proj/tests/test_factorized.cpp:33-72,
+// test_matrix_core.cpp:220-240, test_solver.cpp:257-300)
+static void schedule_tests() {
+  const DenseMatrix wt = normalized(16, 0.5, 2), id = DenseMatrix::identity(16);
+  CHECK(rel(ns_factorized(DenseMatrix::identity(6), normalized(6, 0.5, 1),
+                          FactorizedPlan::for_order(1, FactorizedMode::DenseStored)),
+            ns_sum(DenseMatrix::identity(6), normalized(6, 0.5, 1), 1)) < 1e-15);
+  const DenseMatrix out = ns_factorized(s1(1.0), s1(0.5), FactorizedPlan::for_order(7, FactorizedMode::DenseStored));
+  CHECK(std::fabs(out(0, 0).real() - 1.9921875) < 1e-15);
+  for (long g : {1L, 3L, 7L, 15L, 31L, 63L}) {
+    const auto plan = FactorizedPlan::for_order(g, FactorizedMode::DenseStored);
+    CHECK(rel(ns_factorized(id, wt, plan), ns_sum(id, wt, static_cast<std::size_t>(g))) < 1e-12);
+    const double s = static_cast<double>(plan.num_factors);
+    OpCounter ci, cg;
+    ns_factorized(id, wt, plan, &ci);
+    ns_factorized(scale(id, Scalar{0.5, 0}), wt, plan, &cg);
+    CHECK(ci.n3_multiplies() == 2 * s - 1);
+    CHECK(cg.n3_multiplies() == 2 * s + 1);
+  }
+  CHECK_THROWS(ns_factorized(id, wt, FactorizedPlan::for_order(3, FactorizedMode::SparseMatrixFree)), PlanError);
+  OpCounter c;
+  const DenseMatrix p14 = power_ladder(DenseMatrix::diagonal({Scalar{2, 0}}), 14, &c);
+  CHECK(p14(0, 0) == (Scalar{16384, 0}));
+  CHECK(c.n3_multiplies() == 5.0);
+  const DenseMatrix m = gauss(4, 4, 61);
+  OpCounter c1;
+  CHECK(power_ladder(m, 1, &c1) == m && c1.n3_multiplies() == 0.0);
+  CHECK(power_ladder(m, 0) == DenseMatrix::identity(4));
+  const DenseMatrix base = scale(gauss(8, 8, 71, true), Scalar{0.3, 0});
+  DenseMatrix seq = base;
+  for (std::uint64_t e = 2; e <= 37; ++e) {
+    seq = matmul(seq, base);
+    if (e == 2 || e == 14 || e == 37) CHECK(rel(power_ladder(base, e), seq) < 1e-12);
+  }
+  for (std::size_t depth : {1, 2, 4}) CHECK(rel(nn_explicit(id, wt, 0, depth), ns_sum(id, wt, depth)) < 1e-13);
+  CHECK(std::fabs(nn_explicit(s1(1.0), s1(0.5), 1, 1)(0, 0).real() - 1.875) < 1e-15);
+  CHECK(rel(nn_explicit(id, wt, 2, 2), ns_sum(id, wt, 26)) < 1e-11);
+  CHECK_THROWS(nn_explicit(DenseMatrix::identity(2), normalized(2, 0.5, 21), 40, 2), BudgetError);
+}
+
 int main(int argc, char** argv) {
   const bool host_only = argc > 1 && std::strcmp(argv[1], "--host") == 0;
   host_tests();
-  if (!host_only) device_tests();
+  if (!host_only) {
+    device_tests();
+    schedule_tests();
+  }
   std::printf("%s: %d checks, %d failures\n", host_only ? "host" : "all", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }

@@ -333,6 +333,44 @@ def test_sparse_full_size_property():
     assert 0 < r.item() < 1.001 * 0.8 ** 64
 
 
+# ----------------------------------------------------------------- product-form schedules (§8(f) item 3)
+def test_ns_factorized_power_ladder_nn_explicit_vs_reference(ref):
+    g = golden("steps_spd8.npz")
+    wt = g["wt"]
+    big = W.spd_conditioned(96, 1e2, seed=6)
+    big = big / np.trace(big)
+    for w in (wt, big):
+        n = w.shape[0]
+        for phi0 in (np.eye(n), 0.5 * np.eye(n)):
+            for gamma in (1, 3, 7, 15, 63):
+                s, prods = nnb.ns_factorized(phi0, w, gamma)
+                r, rp = ref.ns_factorized(phi0, w, gamma)
+                assert prods == rp and rel_frob(s, r.real) < 1e-12
+        for e in (0, 1, 2, 3, 14, 37, 64):
+            p, prods = nnb.power_ladder(w, e)
+            r, rp = ref.power_ladder(w, e)
+            assert prods == rp and rel_frob(p, r.real) < 1e-12
+        for (i, L) in [(0, 1), (1, 2), (2, 2), (3, 1), (1, 4)]:
+            x, prods = nnb.nn_explicit(np.eye(n), w, i, L)
+            r, rp = ref.nn_explicit(np.eye(n), w, i, L)
+            assert prods == rp and rel_frob(x, r.real) < 1e-11
+            # the paper's identity: explicit product form == recursive NN == NS of order (L+1)^(i+1)-1
+            s, _ = nnb.ns_sum(np.eye(n), w, (L + 1) ** (i + 1) - 1)
+            assert rel_frob(x, s) < 1e-11
+    with pytest.raises(nnb.PlanError):
+        nnb.ns_factorized(np.eye(8), wt, 6)
+    with pytest.raises(nnb.BudgetError):
+        nnb.nn_explicit(np.eye(8), wt, 40, 2)
+    # complex operands take the planar 4-GEMM path
+    rng = np.random.default_rng(2)
+    hc = rng.standard_normal((24, 8)) + 1j * rng.standard_normal((24, 8))
+    ac = np.conj(hc.T) @ hc
+    ac = ac / np.trace(ac).real
+    s, _ = nnb.ns_factorized(np.eye(8), ac, 31)
+    r, _ = ref.ns_factorized(np.eye(8), ac, 31)
+    assert rel_frob(s, r) < 1e-12
+
+
 # ----------------------------------------------------------------- fused MIMO detection (§8(f) item 1)
 def test_mimo_detect_vs_oracle(port):
     h, y, s = W.mimo_uplink_host(96, seed=4)
