@@ -289,6 +289,73 @@ def cpu_dense_sample(n_sample: int, p: int):
                       f"({p + 3} complex<double> products, {secs:.2f} s)"}
 
 
+# ------------------------------------------------------------------ configs 0 and 2 (small / mid dense)
+def run_c1(args, rank):
+    """BASELINE config 0: N=256 Gram + 0.5 I, X0 = A^T/(|A|_1|A|_inf), Newton (p=1), 30 nests,
+    eps per nest.  GPU (device-resident, CUDA events) next to the reference's own loop on the
+    same input in the same run (oracle/_ref, all host threads), with the live parity check."""
+    import torch
+
+    import paper_2212_02406_b200 as nnb
+    from paper_2212_02406_b200 import workloads as W
+
+    a_h = W.gram_shifted(256, seed=2212, shift=0.5)
+    a = torch.from_numpy(a_h).cuda()
+    for _ in range(3):
+        x, rep = nnb.nn_chain(a, None, p=1, max_iters=30)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(10):
+        x, rep = nnb.nn_chain(a, None, p=1, max_iters=30)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) / 10 * 1e3
+    out = {"metric": "config 0 wall time per 30-nest Newton run (N=256), eps history included", "value": round(ms, 3),
+           "unit": "ms", "device_ms": round(rep.device_ms, 3), "products": rep.products,
+           "eps_first_last": [rep.history[0][1], rep.history[-1][1]]}
+    if rank == 0 and args.cpu:
+        from oracle import Reference
+
+        cores, _ = cpu_info()
+        os.environ["NN_WORKERS"] = str(cores)
+        ref = Reference()
+        xr, hr, ir, secs = ref.chain(a_h, W.x0_transpose_norm(a_h), 1, 30)
+        xg = x.cpu().numpy()
+        out["cpu_reference"] = {"value": round(secs * 1e3, 1), "unit": "ms", "cores": cores, "kind": "reference",
+                                "speedup": round(secs * 1e3 / ms, 1)}
+        eg = np.array([e for _, e in rep.history])
+        above = hr > 1e-12  # floor-region entries compare only as "both below 1e-12"
+        out["parity"] = {"x_rel_frob": float(np.linalg.norm(xg - xr.real) / np.linalg.norm(xr.real)),
+                         "eps_max_rel_above_floor": float(np.max(np.abs(eg[above] - hr[above]) / hr[above])),
+                         "floor_entries_both_below_1e-12": bool(np.all(eg[~above] < 1e-12)),
+                         "iterations_equal": rep.iters == ir}
+    return out
+
+
+def run_c3(args):
+    """BASELINE config 2: N=4096, A = Q diag(lambda) Q^T (kappa 1e3), X0 = A^T/(|A|_1|A|_inf),
+    p in {1,2,3}, iterate to eps < 1e-12 — nests needed and TFLOP/s per depth."""
+    import torch
+
+    import paper_2212_02406_b200 as nnb
+    from paper_2212_02406_b200 import workloads as W
+
+    a = torch.from_numpy(W.spd_conditioned(4096, 1e3, seed=3)).cuda()
+    res = {}
+    for p in (1, 2, 3):
+        x, rep = nnb.nn_chain(a, None, p=p, max_iters=80, tol=1e-12)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x, rep = nnb.nn_chain(a, None, p=p, max_iters=80, tol=1e-12)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        flops = rep.products * 2.0 * 4096 ** 3
+        res[f"p{p}"] = {"nests": rep.iters, "products": rep.products, "stopped": rep.stopped_reason,
+                        "eps_last": rep.history[-1][1], "wall_ms": round(wall * 1e3, 2),
+                        "device_ms": round(rep.device_ms, 2),
+                        "tflops_device": round(flops / (rep.device_ms * 1e-3) / 1e12, 3)}
+    return {"metric": "config 2: nests to eps < 1e-12 and FP64 TFLOP/s at N=4096 (kappa 1e3)", "depths": res}
+
+
 # ------------------------------------------------------------------ MIMO leg (config 1)
 def run_mimo(args, world, rank):
     import torch
@@ -467,7 +534,7 @@ def main():
     ap.add_argument("--depth", dest="p", type=int, default=2)
     ap.add_argument("--mimo-batch", type=int, default=262144)
     ap.add_argument("--grid", type=int, default=4096)
-    ap.add_argument("--legs", default="dense,mimo,sparse")
+    ap.add_argument("--legs", default="dense,mimo,sparse,c1,c3")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
     args = ap.parse_args()
@@ -525,6 +592,10 @@ def main():
         line["legs"]["mimo"] = run_mimo(args, world, rank)
     if "sparse" in legs:
         line["legs"]["sparse"] = run_sparse(args, world, rank)
+    if "c1" in legs and world == 1:
+        line["legs"]["c1"] = run_c1(args, rank)
+    if "c3" in legs and world == 1:
+        line["legs"]["c3"] = run_c3(args)
     if rank == 0 and args.cpu:
         line["cpu_baseline"] = cpu_dense_sample(512, args.p)
         if "mimo" in legs:
