@@ -156,9 +156,8 @@ def dense_inputs(n: int, seed: int):
 
     g = torch.Generator(device="cuda").manual_seed(seed)
     b = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
-    bt = b.t().contiguous()
-    a = nnb.matmul(b, bt)
-    del b, bt
+    a = nnb.matmul_nt(b, b)  # B·Bᵀ on the K-major GEMM, no transposed copy
+    del b
     a = nnb._axpby(1.0 / n, a, 0.0, None, 1.0)  # A/N + I on device
     torch.cuda.synchronize()
     return a
@@ -172,11 +171,9 @@ def dense_rows(n: int, seed: int, row0: int, rows: int):
 
     g = torch.Generator(device="cuda").manual_seed(seed)
     b = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
-    bt = b.t().contiguous()
     bg = b[row0:row0 + rows].contiguous()
-    del b
-    a = nnb.matmul(bg, bt)
-    del bt, bg
+    a = nnb.matmul_nt(bg, b)  # B_g·Bᵀ
+    del b, bg
     a = nnb.scale(a, 1.0 / n)
     idx = torch.arange(rows, device="cuda")
     a[idx, idx + row0] += 1.0

@@ -93,6 +93,10 @@ int nnb_gemm_d(const double* A, int64_t lda, const double* B, int64_t ldb, doubl
                int64_t ldc, int64_t m, int64_t k, int64_t n, void* stream);
 int nnb_gemm_z(const double* A, const double* B, double* C, int64_t m, int64_t k, int64_t n,
                void* stream);
+/* C = A·Bᵀ with Bᵀ given as the n×k row-major matrix Bt (K-major B operand:
+ * conflict-free fragment loads; also the Gram product B·Bᵀ without a copy). */
+int nnb_gemm_nt_d(const double* A, int64_t lda, const double* Bt, int64_t ldbt, double* C, int64_t ldc,
+                  int64_t m, int64_t k, int64_t n, void* stream);
 
 /* out = alpha*A + beta*B + gamma*I (B nullable).  Replaces nn::add / sub /
  * scale / identity_minus / plus_identity (proj/include/nn/kernels.hpp:26-35). */

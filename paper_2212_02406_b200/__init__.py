@@ -87,6 +87,7 @@ _SIGS = {
     "nnb_kernel_launches": ([], C.c_uint64),
     "nnb_gemm_d": ([_dp, _i64, _dp, _i64, _dp, _i64, _i64, _i64, _i64, _dp], C.c_int),
     "nnb_gemm_z": ([_dp, _dp, _dp, _i64, _i64, _i64, _dp], C.c_int),
+    "nnb_gemm_nt_d": ([_dp, _i64, _dp, _i64, _dp, _i64, _i64, _i64, _i64, _dp], C.c_int),
     "nnb_axpby_d": ([C.c_double, _dp, C.c_double, _dp, C.c_double, _dp, _i64, _i64, _dp], C.c_int),
     "nnb_axpby_z": ([_dp, _dp, _dp, _dp, _dp, _dp, _i64, _i64, _dp], C.c_int),
     "nnb_frobenius_d": ([_dp, _i64, _dp, _dp], C.c_int),
@@ -234,6 +235,18 @@ def matmul(a, b):
         _check(lib().nnb_gemm_z(_ptr(a), _ptr(b), _ptr(out), m, k, n, _stream(a)))
     else:
         _check(lib().nnb_gemm_d(_ptr(a), k, _ptr(b), n, _ptr(out), n, m, k, n, _stream(a)))
+    return out
+
+
+def matmul_nt(a, bt):
+    """C = A·Bᵀ for real A (m×k) and Bᵀ (n×k): the K-major GEMM (also B·Bᵀ without a transpose)."""
+    if a.shape[1] != bt.shape[1]:
+        raise ShapeError("matmul_nt: inner dimensions disagree")
+    a, bt = _prep(a, False), _prep(bt, False)
+    m, k = a.shape
+    n = bt.shape[0]
+    out = _empty_like(a, (m, n))
+    _check(lib().nnb_gemm_nt_d(_ptr(a), k, _ptr(bt), k, _ptr(out), n, m, k, n, _stream(a)))
     return out
 
 

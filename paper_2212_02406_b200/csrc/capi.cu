@@ -163,6 +163,39 @@ int nnb_gemm_d(const double* A, int64_t lda, const double* B, int64_t ldb, doubl
   return 0;
 }
 
+int nnb_gemm_nt_d(const double* A, int64_t lda, const double* Bt, int64_t ldbt, double* C, int64_t ldc,
+                  int64_t m, int64_t k, int64_t n, void* stream) {
+  NNB_TRY(require_device());
+  if (m < 0 || k < 0 || n < 0 || lda < k || ldbt < k || ldc < n)
+    return fail(NNB_ERR_SHAPE, "matmul: inner dimensions disagree or bad leading dimension");
+  cudaStream_t s = resolve(stream);
+  DMat a, b, c;
+  NNB_TRY(a.load(A, m, k, lda, s));
+  NNB_TRY(b.load(Bt, n, k, ldbt, s));
+  const bool direct = is_device_ptr(C) && !(reinterpret_cast<uintptr_t>(C) & 15) && !(ldc & 1);
+  if (direct) {
+    c.d = C; c.ld = ldc; c.rows = m; c.cols = n;
+  } else {
+    NNB_TRY(c.alloc(m, n, s));
+  }
+  RedWs red;
+  NNB_TRY(red.init(max_tiles_for(m, n), s));
+  DevBuf nf;
+  NNB_TRY(nf.alloc(sizeof(int), s));
+  GemmOp op;
+  op.A = a.d; op.lda = a.ld; op.B = b.d; op.ldb = b.ld; op.b_kmajor = true;
+  op.M = m; op.N = n; op.K = k;
+  op.ep.C = c.d; op.ep.ldc = c.ld;
+  op.ep.nf_out = nf.as<int>();
+  NNB_TRY(gemm(op, &red, s));
+  if (!direct) NNB_TRY(c.store(C, ldc, s));
+  int h = 0;
+  NNB_CUDA(cudaMemcpyAsync(&h, nf.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NNB_TRY(sync(s));
+  if (h) return fail(NNB_ERR_DOMAIN, "matmul: produced a non-finite entry");
+  return 0;
+}
+
 int nnb_gemm_z(const double* A, const double* B, double* C, int64_t m, int64_t k, int64_t n,
                void* stream) {
   NNB_TRY(require_device());

@@ -166,6 +166,8 @@ static int make_tmap(CUtensorMap* map, const double* base, int64_t rows, int64_t
 // ============================ GEMM ============================
 using BigCfg = GemmCfg<128, 128, 16, 2, 4, 4>;
 using SmallCfg = GemmCfg<64, 64, 16, 2, 2, 4>;
+using BigCfgT = GemmCfg<128, 128, 16, 2, 4, 4, true>;
+using SmallCfgT = GemmCfg<64, 64, 16, 2, 2, 4, true>;
 
 static bool use_big(int64_t M, int64_t N) {
   static const char* force = std::getenv("NNB_GEMM_CFG");  // debug override: "big" / "small"
@@ -188,7 +190,10 @@ template <class Cfg>
 static int launch_cfg(const GemmOp& op, cudaStream_t s) {
   CUtensorMap ta, tb;
   NNB_TRY(make_tmap(&ta, op.A, op.M, op.K, op.lda, Cfg::kBM, Cfg::kBK, true));
-  NNB_TRY(make_tmap(&tb, op.B, op.K, op.N, op.ldb, Cfg::kBK, Cfg::kBN, false));
+  if (Cfg::kBKMajor)
+    NNB_TRY(make_tmap(&tb, op.B, op.N, op.K, op.ldb, Cfg::kBN, Cfg::kBK, true));
+  else
+    NNB_TRY(make_tmap(&tb, op.B, op.K, op.N, op.ldb, Cfg::kBK, Cfg::kBN, false));
   const int smem = Cfg::kSmemBytes + smem_pad();
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
@@ -223,6 +228,7 @@ int gemm(GemmOp op, RedWs* red, cudaStream_t s) {
     return axpby(0.0, op.ep.C, op.ep.ldc, op.ep.beta, op.ep.D, op.ep.ldd, op.ep.gamma,
                  op.ep.diag_offset, op.ep.C, op.ep.ldc, op.M, op.N, s);
   }
+  if (op.b_kmajor) return use_big(op.M, op.N) ? launch_cfg<BigCfgT>(op, s) : launch_cfg<SmallCfgT>(op, s);
   return use_big(op.M, op.N) ? launch_cfg<BigCfg>(op, s) : launch_cfg<SmallCfg>(op, s);
 }
 

@@ -91,6 +91,7 @@ struct GemmOp {
   int64_t ldb = 0;
   int64_t M = 0, N = 0, K = 0;
   GemmEpilogue ep;
+  bool b_kmajor = false;  // B points at Bᵀ (N×K row-major, leading dimension ldb)
 };
 
 int max_tiles_for(int64_t M, int64_t N);

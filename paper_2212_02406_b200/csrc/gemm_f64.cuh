@@ -44,8 +44,12 @@ struct GemmEpilogue {
   double eps_scale = 1.0;
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+// B_KMAJOR: the B operand is supplied transposed (Bᵀ, N×K row-major) and its
+// tiles are 128B-swizzled like A's, which makes the B-fragment loads
+// conflict-free (2 wavefronts instead of 4 per 32 doubles).
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool B_KMAJOR = false>
 struct GemmCfg {
+  static constexpr bool kBKMajor = B_KMAJOR;
   static constexpr int kBM = BM, kBN = BN, kBK = BK, kWM = WM, kWN = WN, kStages = STAGES;
   static constexpr int kConsumerWarps = WM * WN;
   static constexpr int kThreads = (kConsumerWarps + 1) * 32;
@@ -111,7 +115,10 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
         uint8_t* sb = sa + Cfg::kABytes;
         mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
         tma_load_2d(sa, &tmA, &full[s], kt * BK, m0);
-        tma_load_2d(sb, &tmB, &full[s], n0, kt * BK);
+        if (Cfg::kBKMajor)
+          tma_load_2d(sb, &tmB, &full[s], kt * BK, n0);
+        else
+          tma_load_2d(sb, &tmB, &full[s], n0, kt * BK);
       }
     }
     return;
@@ -130,7 +137,8 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
   // A (128B swizzle): (r,k) -> r*128 + ((k>>1) ^ (r&7))*16 + (k&1)*8, r&7 == g.
   // B (linear):       (k,n) -> (k*BN + n)*8.
   const uint32_t a_row_off = (wm * Cfg::kWarpM + g) * 128;
-  const uint32_t b_col_off = (wn * Cfg::kWarpN + g) * 8 + t * BN * 8;
+  // B (K-major, swizzled as A): (n,k) -> n*128 + ((k>>1) ^ (n&7))*16 + (k&1)*8.
+  const uint32_t b_col_off = Cfg::kBKMajor ? (wn * Cfg::kWarpN + g) * 128 : (wn * Cfg::kWarpN + g) * 8 + t * BN * 8;
 
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % STAGES;
@@ -147,7 +155,8 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
         af[i] = *reinterpret_cast<const double*>(sa + a_row_off + i * 8 * 128 + a_chunk);
 #pragma unroll
       for (int j = 0; j < NI; ++j)
-        bf[j] = *reinterpret_cast<const double*>(sb + b_col_off + kk * 4 * BN * 8 + j * 64);
+        bf[j] = Cfg::kBKMajor ? *reinterpret_cast<const double*>(sb + b_col_off + j * 8 * 128 + a_chunk)
+                              : *reinterpret_cast<const double*>(sb + b_col_off + kk * 4 * BN * 8 + j * 64);
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll

@@ -59,6 +59,15 @@ def test_gemm_device_pointers_and_determinism():
     assert (torch.linalg.norm(c1 - ref) / torch.linalg.norm(ref)).item() < 1e-14
 
 
+@pytest.mark.parametrize("m,k,n", [(5, 3, 7), (200, 130, 96), (1024, 1024, 1024)])
+def test_gemm_nt_vs_oracle(port, m, k, n):
+    rng = np.random.default_rng(m + k)
+    a, bt = rng.standard_normal((m, k)), rng.standard_normal((n, k))
+    c = nnb.matmul_nt(a, bt)
+    assert rel_frob(c, port.matmul(a, bt.T.copy()).real) < 1e-14
+    assert np.array_equal(c, nnb.matmul(a, bt.T.copy()))  # same k order as the row-major B kernel
+
+
 def test_gemm_complex_vs_oracle(port):
     rng = np.random.default_rng(3)
     a = rng.standard_normal((33, 20)) + 1j * rng.standard_normal((33, 20))
