@@ -168,6 +168,13 @@ using BigCfg = GemmCfg<128, 128, 16, 2, 4, 4>;
 using SmallCfg = GemmCfg<64, 64, 16, 2, 2, 4>;
 using BigCfgT = GemmCfg<128, 128, 16, 2, 4, 4, true>;
 using SmallCfgT = GemmCfg<64, 64, 16, 2, 2, 4, true>;
+using TinyCfg = GemmCfg<32, 32, 16, 2, 2, 4>;  // latency-bound sizes (config 0: N=256 -> 64 CTAs)
+
+static bool use_tiny(int64_t M, int64_t N) {
+  static const char* force = std::getenv("NNB_GEMM_CFG");
+  if (force) return force[0] == 't';
+  return ((M + 63) / 64) * ((N + 63) / 64) < 148;
+}
 
 static bool use_big(int64_t M, int64_t N) {
   static const char* force = std::getenv("NNB_GEMM_CFG");  // debug override: "big" / "small"
@@ -182,8 +189,8 @@ static int smem_pad() {
   return pad;
 }
 
-int max_tiles_for(int64_t M, int64_t N) {
-  return static_cast<int>(((M + 63) / 64) * ((N + 63) / 64));
+int max_tiles_for(int64_t M, int64_t N) {  // upper bound over every tile configuration
+  return static_cast<int>(((M + 31) / 32) * ((N + 31) / 32));
 }
 
 template <class Cfg>
@@ -229,6 +236,7 @@ int gemm(GemmOp op, RedWs* red, cudaStream_t s) {
                  op.ep.diag_offset, op.ep.C, op.ep.ldc, op.M, op.N, s);
   }
   if (op.b_kmajor) return use_big(op.M, op.N) ? launch_cfg<BigCfgT>(op, s) : launch_cfg<SmallCfgT>(op, s);
+  if (use_tiny(op.M, op.N)) return launch_cfg<TinyCfg>(op, s);
   return use_big(op.M, op.N) ? launch_cfg<BigCfg>(op, s) : launch_cfg<SmallCfg>(op, s);
 }
 
