@@ -28,3 +28,9 @@ if which in ("all", "sparse"):
         xs, _ = nnb.solve_sparse_factorized(csr, b, 63, nnb.Normalization(theta=0.2, valid=True))
 torch.cuda.synchronize()
 print("prof_drive ok", which)
+if which == "detect":
+    h, y, s = W.mimo_uplink_device(262144, seed=2)
+    for _ in range(2):
+        xh, _, _ = nnb.mimo_detect(h, y)
+    torch.cuda.synchronize()
+    print("prof_drive ok detect")
