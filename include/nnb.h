@@ -86,6 +86,18 @@ int nnb_device_count(void);
 /* Launch count of this library's kernels since load (for bench gpu_launches). */
 uint64_t nnb_kernel_launches(void);
 
+/* Arithmetic mode of the calling thread.
+ * NNB_ARITH_FAST (default): DMMA products, tile-parallel reductions —
+ *   agrees with the reference to ~1e-15 relative.
+ * NNB_ARITH_REFERENCE: real dense products as ascending-k, explicitly
+ *   rounded CUDA-core loops, serial Frobenius sums and the reference's own
+ *   nest sequence — BIT-IDENTICAL to the reference for real data
+ *   (a verification mode; complex products keep the 4-GEMM path).
+ * The sparse path is bit-identical in both modes. */
+enum nnb_arith { NNB_ARITH_FAST = 0, NNB_ARITH_REFERENCE = 1 };
+int nnb_set_arithmetic(int32_t mode);
+int32_t nnb_get_arithmetic(void);
+
 /* ---- dense kernels ------------------------------------------------------ */
 /* C = A·B.  Replaces nn::matmul (proj/include/nn/kernels.hpp:20-21,
  * proj/src/kernels.cpp:137-162).  ld* are leading dimensions in elements. */

@@ -85,6 +85,8 @@ _SIGS = {
     "nnb_last_error": ([], C.c_char_p),
     "nnb_device_count": ([], C.c_int),
     "nnb_kernel_launches": ([], C.c_uint64),
+    "nnb_set_arithmetic": ([_i32], C.c_int),
+    "nnb_get_arithmetic": ([], C.c_int32),
     "nnb_gemm_d": ([_dp, _i64, _dp, _i64, _dp, _i64, _i64, _i64, _i64, _dp], C.c_int),
     "nnb_gemm_z": ([_dp, _dp, _dp, _i64, _i64, _i64, _dp], C.c_int),
     "nnb_gemm_nt_d": ([_dp, _i64, _dp, _i64, _dp, _i64, _i64, _i64, _i64, _dp], C.c_int),
@@ -157,6 +159,22 @@ def exported_symbols() -> list[str]:
 
 def kernel_launches() -> int:
     return int(lib().nnb_kernel_launches())
+
+
+ARITH_FAST, ARITH_REFERENCE = 0, 1
+
+
+class reference_arithmetic:
+    """Context manager: run real dense products in the reference-exact mode
+    (bit-identical to the reference; CUDA-core FP64, a verification mode)."""
+
+    def __enter__(self):
+        self._prev = lib().nnb_get_arithmetic()
+        _check(lib().nnb_set_arithmetic(ARITH_REFERENCE))
+        return self
+
+    def __exit__(self, *exc):
+        lib().nnb_set_arithmetic(self._prev)
 
 
 def _check(status: int, index: int = 0) -> None:

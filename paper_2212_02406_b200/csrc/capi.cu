@@ -129,6 +129,14 @@ int nnb_device_count(void) {
 }
 uint64_t nnb_kernel_launches(void) { return launches(); }
 
+int nnb_set_arithmetic(int32_t mode) {
+  if (mode != NNB_ARITH_FAST && mode != NNB_ARITH_REFERENCE)
+    return fail(NNB_ERR_DOMAIN, "nnb_set_arithmetic: unknown mode");
+  set_arith(mode);
+  return 0;
+}
+int32_t nnb_get_arithmetic(void) { return arith(); }
+
 // ---------------------------------------------------------------- dense kernels
 int nnb_gemm_d(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                int64_t m, int64_t k, int64_t n, void* stream) {

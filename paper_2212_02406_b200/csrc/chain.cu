@@ -138,6 +138,9 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
   NNB_CUDA(cudaEventRecord(e0, c.s));
 
   const bool tol_mode = cfg.tol > 0.0;
+  // reference-exact mode (real data): the reference's operand order and nest sequence
+  const bool exact = arith() == 1 && !c.cplx;
+  const int order = exact ? 1 : cfg.order;
   std::vector<double> eps_h(slots, 0.0);
   std::vector<int> nf_h(nf_count, 0);
   int k = 0, products = 0, stopped = 1, recorded = 0;
@@ -145,8 +148,8 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
     const bool last = (k >= cfg.max_iters);
     if (last && !cfg.final_residual) break;
     const Plane& Xk = bufs[xi];
-    const Plane& lhs = cfg.order == 0 ? A : Xk;
-    const Plane& rhs = cfg.order == 0 ? Xk : A;
+    const Plane& lhs = order == 0 ? A : Xk;
+    const Plane& rhs = order == 0 ? Xk : A;
     NNB_TRY(product(c, lhs, rhs, -1.0, nullptr, 0.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1)));
     ++products;
     recorded = k + 1;
@@ -165,7 +168,22 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
       }
     }
     if (last) break;
-    if (p > 0) {
+    if (p > 0 && exact) {
+      // the reference's own sequence (solver.cpp:27-36,93-103): S = I + P, S = I + P·S, X' = S·X
+      const int a_i = (xi + 1) % 3, b_i = (xi + 2) % 3;
+      NNB_TRY(axpby(1.0, R.re, c.ld, 0.0, nullptr, 0, 1.0, 0, bufs[a_i].re, c.ld, n, n, c.s));
+      int si = a_i;
+      for (int j = 2; j <= p; ++j) {
+        const int dst = si == a_i ? b_i : a_i;
+        NNB_TRY(product(c, R, bufs[si], 1.0, nullptr, 0.0, 1.0, bufs[dst], nullptr, nf_dev + k * (p + 1) + j - 1));
+        ++products;
+        si = dst;
+      }
+      const int dst = 3 - xi - si;
+      NNB_TRY(product(c, bufs[si], Xk, 1.0, nullptr, 0.0, 0.0, bufs[dst], nullptr, nf_dev + k * (p + 1) + p));
+      ++products;
+      xi = dst;
+    } else if (p > 0) {
       Plane v = Xk;
       int vi = xi;
       int dst_i = (xi + 1) % 3;

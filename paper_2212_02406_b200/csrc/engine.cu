@@ -235,6 +235,7 @@ int gemm(GemmOp op, RedWs* red, cudaStream_t s) {
     return axpby(0.0, op.ep.C, op.ep.ldc, op.ep.beta, op.ep.D, op.ep.ldd, op.ep.gamma,
                  op.ep.diag_offset, op.ep.C, op.ep.ldc, op.M, op.N, s);
   }
+  if (arith() == 1 && !op.b_kmajor) return gemm_exact(op, s);  // reference-exact mode (exact.cu)
   if (op.b_kmajor) return use_big(op.M, op.N) ? launch_cfg<BigCfgT>(op, s) : launch_cfg<SmallCfgT>(op, s);
   if (use_tiny(op.M, op.N)) return launch_cfg<TinyCfg>(op, s);
   return use_big(op.M, op.N) ? launch_cfg<BigCfg>(op, s) : launch_cfg<SmallCfg>(op, s);

@@ -95,6 +95,10 @@ struct GemmOp {
 };
 
 int max_tiles_for(int64_t M, int64_t N);
+// Arithmetic mode (thread-local): 0 = fast DMMA path, 1 = reference-exact (exact.cu).
+void set_arith(int mode);
+int arith();
+int gemm_exact(const GemmOp& op, cudaStream_t s);
 // Launches C = epilogue(A·B).  If `red` is non-null the Σ C² / non-finite
 // reduction is wired to it (ep.ss_out / nf_out / eps_out chosen by caller).
 int gemm(GemmOp op, RedWs* red, cudaStream_t s);
