@@ -11,7 +11,6 @@ GPU and raises otherwise.
 from __future__ import annotations
 
 import ctypes as C
-import math
 from dataclasses import dataclass, field
 from pathlib import Path
 from typing import Optional

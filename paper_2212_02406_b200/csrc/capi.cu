@@ -378,7 +378,6 @@ int nnb_nn_chain_z(const double* A, int64_t n, const double* X0, const nnb_chain
 
 int nnb_residual_eps_d(const double* X, const double* A, int64_t n, double* eps, void* stream) {
   nnb_chain_config cfg{0, 0, 0.0, NNB_ORDER_REFERENCE, NNB_X0_GIVEN, 0.0, 1};
-  std::vector<double> scratch((size_t)0);
   nnb_chain_result r{};
   double h[1] = {0.0};
   // X_out must be distinct from the inputs; a residual-only chain leaves X unchanged

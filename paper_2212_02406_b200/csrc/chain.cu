@@ -38,8 +38,8 @@ struct Ctx {
   int64_t n, ld;
   bool cplx;
   RedWs red;
-  DevBuf scratch;  // complex combine scalars
-  double* ss2 = nullptr;
+  double* ss2 = nullptr;  // complex products: per-plane Σ² / non-finite scalars
+
   int* nf2 = nullptr;
   cudaStream_t s;
 };
@@ -332,11 +332,6 @@ int shift_plane(Ctx& c, const Plane& src, double alpha, double gamma, const Plan
   NNB_TRY(axpby(alpha, src.re, c.ld, 0.0, nullptr, 0, gamma, 0, dst.re, c.ld, c.n, c.n, c.s));
   if (c.cplx) NNB_TRY(axpby(alpha, src.im, c.ld, 0.0, nullptr, 0, 0.0, 0, dst.im, c.ld, c.n, c.n, c.s));
   return 0;
-}
-
-int nf_slot(Ctx& c, std::vector<int>& slots_used) {
-  slots_used.push_back(0);
-  return static_cast<int>(slots_used.size()) - 1;
 }
 
 // p^e by binary square-and-multiply (power_ladder, proj/src/kernels.cpp:434-452);

@@ -15,13 +15,6 @@ namespace nnb {
 void set_error(const std::string& msg);
 const char* last_error();
 
-struct Status {
-  int code = 0;
-  Status() = default;
-  Status(int c) : code(c) {}
-  bool ok() const { return code == 0; }
-};
-
 int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
 #define NNB_CUDA(x)                                                            \
   do {                                                                         \

@@ -132,7 +132,6 @@ DenseMatrix device_nest(const DenseMatrix& phi, const DenseMatrix& w, std::size_
 }
 
 // Product-form schedules through the C-ABI (real data → _d, complex → _z).
-using SchedD = int (*)(const double*, const double*, int64_t, int64_t, int64_t, double*, double*);
 DenseMatrix run_schedule(const DenseMatrix& a, const DenseMatrix* b, int64_t x, int64_t y,
                          const std::function<int(const double*, const double*, double*, double*, bool)>& call,
                          double* products, const char* who) {
