@@ -103,11 +103,11 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def dist_setup():
+def dist_setup(force: bool = False):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or force:
         import torch
         import torch.distributed as dist
 
@@ -187,7 +187,8 @@ def run_dense(args, world, rank):
 
     n, p = args.n, args.p
     flops_step = (p + 1) * 2.0 * n ** 3  # whole-job work of one nest (strong scaling)
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
         comm = nnb.Comm.from_torch_distributed()
         row0, rows = nnb.partition_rows(n, world, rank)
         a = dense_rows(n, 2212, row0, rows)
@@ -245,7 +246,7 @@ def run_dense(args, world, rank):
         del a, x
         torch.cuda.empty_cache()
         a_np, x_np, xo_np = a_h.numpy(), x_h.numpy(), xo_h.numpy()
-        if world > 1:
+        if sharded:
             call = lambda: nnb.nn_chain_sharded(comm, a_np, n, x_np, p=p, max_iters=1, final_residual=False, out=xo_np)
         else:
             call = lambda: nnb.nn_chain(a_np, x_np, p=p, max_iters=1, final_residual=False, out=xo_np)
@@ -258,9 +259,9 @@ def run_dense(args, world, rank):
         t = max_over_ranks(world, time.perf_counter() - t0)
         out["e2e"] = {"value": round(flops_step * k_e2e / t / 1e12, 3), "unit": "TFLOP/s",
                       "h2d_bytes_per_step": 2 * 8 * shape[0] * n * world, "d2h_bytes_per_step": 8 * shape[0] * n * world,
-                      "path": ("nnb_nn_chain_sharded_d" if world > 1 else "nnb_nn_chain_d")
+                      "path": ("nnb_nn_chain_sharded_d" if sharded else "nnb_nn_chain_d")
                               + " with pinned host A, X0 and X_out"}
-    if world > 1:
+    if sharded:
         comm.close()
     return out
 
@@ -469,13 +470,15 @@ def run_sparse(args, world, rank):
     dev = lambda v: torch.from_numpy(v).cuda()
     b_full = W.rhs(n, seed=7)
     norm = nnb.Normalization(theta=0.2, valid=True)
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
         # row slabs with halo exchange (strong scaling: the 4096^2 problem is fixed)
         comm = nnb.Comm.from_torch_distributed()
         r0, rows = nnb.partition_rows(n, world, rank)
         csr = nnb.Csr(dev(rp[r0:r0 + rows + 1].copy()), dev(col), dev(val), n=rows, nnz=col.size)
         b = dev(b_full[r0:r0 + rows].copy())
-        solve = lambda: nnb.solve_sparse_factorized_sharded(comm, csr, n, b, 63, norm)
+        plan = nnb.SparseShardedPlan(comm, csr, n, k=1, stream_like=b)  # slab setup once, outside the timing
+        solve = lambda: plan.solve(b, 63, norm)
     else:
         csr = nnb.Csr(dev(rp), dev(col), dev(val), n=n, nnz=col.size)
         b = dev(b_full)
@@ -491,13 +494,14 @@ def run_sparse(args, world, rank):
     e1.record()
     torch.cuda.synchronize()
     ms = max_over_ranks(world, e0.elapsed_time(e1)) / steps
-    if world > 1:
+    if sharded:
+        plan.close()
         comm.close()
     alg = 63 * sparse_bytes(n, col.size)  # whole-job algorithmic bytes per solve
     gbs = alg / (ms * 1e-3) / 1e9
     return {"metric": "sparse factorized solve, 4096^2 5-pt Laplacian+I, gamma=63", "value": round(gbs, 1),
             "unit": "GB/s", "ms_per_step": round(ms, 3),
-            "parallelism": f"row slabs x{world}, NCCL halo exchange" if world > 1 else "single GPU",
+            "parallelism": f"row slabs x{world}, NCCL halo exchange" if sharded else "single GPU",
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": HBM_PEAK * world, "unit": "GB/s",
                          "frac": round(gbs / (HBM_PEAK * world), 4), "traffic": None,
                          "per_launch": "nnz*(8+4) + (N+1)*4 + 2N*8 bytes per application (x63)"}}
@@ -533,9 +537,11 @@ def main():
     ap.add_argument("--legs", default="dense,mimo,sparse,c1,c3")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU (sharded) dense/sparse paths even at one rank (code-path check)")
     args = ap.parse_args()
     legs = set(args.legs.split(","))
-    world, rank, local = dist_setup() if args.impl == "ours" else (int(os.environ.get("WORLD_SIZE", "1")),
+    world, rank, local = dist_setup(args.sharded) if args.impl == "ours" else (int(os.environ.get("WORLD_SIZE", "1")),
                                                                    int(os.environ.get("RANK", "0")), 0)
     cores, model = cpu_info()
     config = {"workload": f"BASELINE config 3: dense NN inversion N={args.n}, p={args.p}, one nest per step "
@@ -600,7 +606,7 @@ def main():
             line["legs"]["sparse"]["cpu_baseline"] = cpu_sparse_sample(512)
     if rank == 0:
         print(json.dumps(line))
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch.distributed as dist
 
         dist.destroy_process_group()

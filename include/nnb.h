@@ -265,6 +265,16 @@ int nnb_sparse_factorized_sharded_d(nnb_comm_t comm, const int64_t* row_ptr, con
                                     const double* val, int64_t n, const double* B_rows, int64_t k,
                                     int64_t gamma, double theta, double* X_rows,
                                     int64_t* spmv_count_out, int32_t* fail_factor_out, void* stream);
+/* Reusable form for repeated solves on one operator: the slab's staged CSR,
+ * remapped columns, halo sizes and extended vectors are built once
+ * (k right-hand-side columns fixed at creation). */
+typedef struct nnb_sparse_plan* nnb_sparse_plan_t;
+int nnb_sparse_plan_create(nnb_comm_t comm, const int64_t* row_ptr, const int32_t* col, const double* val,
+                           int64_t n, int64_t k, nnb_sparse_plan_t* plan_out, void* stream);
+int nnb_sparse_plan_solve(nnb_sparse_plan_t plan, const double* B_rows, int64_t gamma, double theta,
+                          double* X_rows, int64_t* spmv_count_out, int32_t* fail_factor_out,
+                          void* stream);
+int nnb_sparse_plan_destroy(nnb_sparse_plan_t plan);
 /* The same schedule with `world` virtual ranks (device copies move the halos). */
 int nnb_sparse_factorized_sharded_emulated_d(const int64_t* row_ptr, const int32_t* col,
                                              const double* val, int64_t n, int64_t nnz,

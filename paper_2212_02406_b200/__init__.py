@@ -132,6 +132,9 @@ _SIGS = {
                                          _dp, _dp], C.c_int),
     "nnb_sparse_factorized_sharded_emulated_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _i64, C.c_double, _i32,
                                                   _dp, _dp, _dp, _dp], C.c_int),
+    "nnb_sparse_plan_create": ([C.c_void_p, _dp, _dp, _dp, _i64, _i64, C.POINTER(C.c_void_p), _dp], C.c_int),
+    "nnb_sparse_plan_solve": ([C.c_void_p, _dp, _i64, C.c_double, _dp, _dp, _dp, _dp], C.c_int),
+    "nnb_sparse_plan_destroy": ([C.c_void_p], C.c_int),
 }
 
 _lib: Optional[C.CDLL] = None
@@ -703,6 +706,34 @@ def solve_sparse_factorized_sharded(comm: Comm, csr_rows: Csr, n: int, b_rows, g
                                                _stream(b_rows))
     _check(st, ff.value)
     return out, cnt.value
+
+
+class SparseShardedPlan:
+    """Prepared row slab for repeated sharded solves (nnb_sparse_plan_*)."""
+
+    def __init__(self, comm: Comm, csr_rows: Csr, n: int, k: int = 1, stream_like=None):
+        self.comm, self.n, self.k = comm, n, k
+        self._keep = csr_rows  # the CSR arrays must outlive the plan when borrowed
+        h = C.c_void_p()
+        _check(lib().nnb_sparse_plan_create(comm.handle, _ptr(csr_rows.row_ptr), _ptr(csr_rows.col),
+                                            _ptr(csr_rows.val), n, k, C.byref(h), _stream(stream_like)))
+        self.handle = h
+
+    def solve(self, b_rows, gamma: int, norm: Normalization):
+        if not norm.valid:
+            raise ContractionError("solve_sparse_factorized: invalid normalization")
+        b_rows = _prep(b_rows, False)
+        out = _empty_like(b_rows)
+        cnt, ff = C.c_int64(), C.c_int32(-1)
+        st = lib().nnb_sparse_plan_solve(self.handle, _ptr(b_rows), int(gamma), float(norm.theta), _ptr(out),
+                                         C.addressof(cnt), C.addressof(ff), _stream(b_rows))
+        _check(st, ff.value)
+        return out, cnt.value
+
+    def close(self):
+        if self.handle:
+            lib().nnb_sparse_plan_destroy(self.handle)
+            self.handle = None
 
 
 def solve_sparse_factorized_sharded_emulated(csr: Csr, b, gamma: int, norm: Normalization, world: int):

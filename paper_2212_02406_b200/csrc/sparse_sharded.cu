@@ -20,6 +20,7 @@
 // interior/boundary split on a single device.
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "../../include/nnb.h"
@@ -28,7 +29,7 @@
 #include "sparse.cuh"
 
 namespace nnb {
-namespace {
+namespace sparse_detail {
 
 #define NNB_NCCL2(x)                                                                             \
   do {                                                                                           \
@@ -194,34 +195,49 @@ int check_order(int64_t gamma, int* s_factors) {
   return 0;
 }
 
-}  // namespace
+}  // namespace sparse_detail
 }  // namespace nnb
 
 using namespace nnb;
+using namespace nnb::sparse_detail;
 
 extern "C" {
 
-int nnb_sparse_factorized_sharded_d(nnb_comm_t comm, const int64_t* row_ptr, const int32_t* col, const double* val,
-                                    int64_t n, const double* B_rows, int64_t k, int64_t gamma, double theta,
-                                    double* X_rows, int64_t* spmv_count_out, int32_t* fail_factor_out,
-                                    void* stream) {
+// A prepared slab: partition, staged CSR, remapped columns, halo sizes and
+// the extended vectors — built once, reused by every solve on the operator.
+struct nnb_sparse_plan {
+  nnb_comm* comm = nullptr;
+  int64_t n = 0, k = 0;
+  Slab sl;
+  DevBuf csr;
+  cudaEvent_t ready = nullptr, landed = nullptr;
+  ~nnb_sparse_plan() {
+    if (ready) cudaEventDestroy(ready);
+    if (landed) cudaEventDestroy(landed);
+  }
+};
+
+int nnb_sparse_plan_create(nnb_comm_t comm, const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n,
+                           int64_t k, nnb_sparse_plan_t* plan_out, void* stream) {
   NNB_TRY(require_device());
   if (!comm) return fail(NNB_ERR_DOMAIN, "sharded sparse: comm is NULL");
-  int s_factors = 0;
-  NNB_TRY(check_order(gamma, &s_factors));
+  if (k < 1) return fail(NNB_ERR_SHAPE, "sharded sparse: k must be >= 1");
   cudaStream_t s = resolve(stream);
+  auto plan = std::make_unique<nnb_sparse_plan>();
+  plan->comm = comm;
+  plan->n = n;
+  plan->k = k;
   const int G = comm->world, me = comm->rank;
-  Slab sl;
+  Slab& sl = plan->sl;
   nnb_partition_rows(n, G, me, &sl.row0, &sl.rows);
   // stage the slab's CSR (host or device) on this device
-  DevBuf csr;
   const int64_t* rp_d = row_ptr;
   const int32_t* col_d = col;
   const double* val_d = val;
   if (!is_device_ptr(row_ptr) || !is_device_ptr(col) || !is_device_ptr(val)) {
     const int64_t base = row_ptr[0], nnz = row_ptr[sl.rows] - base;
-    NNB_TRY(csr.alloc(sizeof(int64_t) * (sl.rows + 1) + sizeof(double) * nnz + sizeof(int32_t) * nnz + 64, s));
-    char* b = csr.as<char>();
+    NNB_TRY(plan->csr.alloc(sizeof(int64_t) * (sl.rows + 1) + sizeof(double) * nnz + sizeof(int32_t) * nnz + 64, s));
+    char* b = plan->csr.as<char>();
     NNB_CUDA(cudaMemcpyAsync(b, row_ptr, sizeof(int64_t) * (sl.rows + 1), cudaMemcpyDefault, s));
     NNB_CUDA(cudaMemcpyAsync(b + sizeof(int64_t) * (sl.rows + 1), val + base, sizeof(double) * nnz, cudaMemcpyDefault, s));
     NNB_CUDA(cudaMemcpyAsync(b + sizeof(int64_t) * (sl.rows + 1) + sizeof(double) * nnz, col + base,
@@ -247,20 +263,40 @@ int nnb_sparse_factorized_sharded_d(nnb_comm_t comm, const int64_t* row_ptr, con
       return fail(NNB_ERR_DOMAIN, "sharded sparse: operator bandwidth exceeds a neighbour slab (halo wider than one rank)");
   sl.send_prev = me > 0 ? halos[2 * (me - 1) + 1] : 0;
   sl.send_next = me < G - 1 ? halos[2 * (me + 1)] : 0;
+  NNB_CUDA(cudaEventCreateWithFlags(&plan->ready, cudaEventDisableTiming));
+  NNB_CUDA(cudaEventCreateWithFlags(&plan->landed, cudaEventDisableTiming));
+  *plan_out = plan.release();
+  return 0;
+}
+
+int nnb_sparse_plan_destroy(nnb_sparse_plan_t plan) {
+  delete plan;
+  return 0;
+}
+
+int nnb_sparse_plan_solve(nnb_sparse_plan_t plan, const double* B_rows, int64_t gamma, double theta, double* X_rows,
+                          int64_t* spmv_count_out, int32_t* fail_factor_out, void* stream) {
+  NNB_TRY(require_device());
+  if (!plan) return fail(NNB_ERR_DOMAIN, "sharded sparse: plan is NULL");
+  int s_factors = 0;
+  NNB_TRY(check_order(gamma, &s_factors));
+  cudaStream_t s = resolve(stream);
+  nnb_comm* comm = plan->comm;
+  const int G = comm->world, me = comm->rank;
+  const int64_t k = plan->k;
+  Slab& sl = plan->sl;
+  NNB_CUDA(cudaMemsetAsync(sl.flags, 0, sizeof(int) * 64, s));
   // Z = B in the extended layout
   NNB_CUDA(cudaMemcpyAsync(sl.ext[4] + sl.h_lo * k, B_rows, sizeof(double) * sl.rows * k, cudaMemcpyDefault, s));
   Out x;
   NNB_TRY(x.prepare(X_rows, (size_t)(sl.rows * k), s));
   std::vector<Slab*> slabs{&sl};
   std::vector<double*> xo{x.d};
-  cudaEvent_t ready, landed;
-  NNB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-  NNB_CUDA(cudaEventCreateWithFlags(&landed, cudaEventDisableTiming));
   auto exchange = [&](int e) -> int {
     if (G == 1) return 0;
     double* ext = sl.ext[e];
-    NNB_CUDA(cudaEventRecord(ready, s));
-    NNB_CUDA(cudaStreamWaitEvent(comm->cs, ready, 0));
+    NNB_CUDA(cudaEventRecord(plan->ready, s));
+    NNB_CUDA(cudaStreamWaitEvent(comm->cs, plan->ready, 0));
     NNB_NCCL2(nccl_group(true));
     if (me > 0) {
       if (sl.send_prev) NNB_NCCL2(nccl_send(ext + sl.h_lo * k, sl.send_prev * k, me - 1, comm, comm->cs));
@@ -272,11 +308,11 @@ int nnb_sparse_factorized_sharded_d(nnb_comm_t comm, const int64_t* row_ptr, con
       if (sl.h_hi) NNB_NCCL2(nccl_recv(ext + (sl.h_lo + sl.rows) * k, sl.h_hi * k, me + 1, comm, comm->cs));
     }
     NNB_NCCL2(nccl_group(false));
-    NNB_CUDA(cudaEventRecord(landed, comm->cs));
+    NNB_CUDA(cudaEventRecord(plan->landed, comm->cs));
     return 0;
   };
   auto wait = [&](size_t) -> int {
-    if (G > 1) NNB_CUDA(cudaStreamWaitEvent(s, landed, 0));
+    if (G > 1) NNB_CUDA(cudaStreamWaitEvent(s, plan->landed, 0));
     return 0;
   };
   int st = run_slabs(slabs, k, s_factors, theta, xo, exchange, wait, s);
@@ -293,8 +329,6 @@ int nnb_sparse_factorized_sharded_d(nnb_comm_t comm, const int64_t* row_ptr, con
     for (int g = 0; g < G; ++g)
       for (int i = 0; i < 64; ++i) all[i] |= h[64 * g + i];
   }
-  cudaEventDestroy(ready);
-  cudaEventDestroy(landed);
   if (st) return st;
   int ff = -1;
   st = collect_flags(slabs, s_factors, &ff, s, &all);
@@ -302,6 +336,19 @@ int nnb_sparse_factorized_sharded_d(nnb_comm_t comm, const int64_t* row_ptr, con
   if (st) return st;
   if (spmv_count_out) *spmv_count_out = gamma * k;
   return x.finish(s);
+}
+
+int nnb_sparse_factorized_sharded_d(nnb_comm_t comm, const int64_t* row_ptr, const int32_t* col, const double* val,
+                                    int64_t n, const double* B_rows, int64_t k, int64_t gamma, double theta,
+                                    double* X_rows, int64_t* spmv_count_out, int32_t* fail_factor_out,
+                                    void* stream) {
+  int s_factors = 0;
+  NNB_TRY(check_order(gamma, &s_factors));
+  nnb_sparse_plan_t plan = nullptr;
+  NNB_TRY(nnb_sparse_plan_create(comm, row_ptr, col, val, n, k, &plan, stream));
+  const int st = nnb_sparse_plan_solve(plan, B_rows, gamma, theta, X_rows, spmv_count_out, fail_factor_out, stream);
+  nnb_sparse_plan_destroy(plan);
+  return st;
 }
 
 int nnb_sparse_factorized_sharded_emulated_d(const int64_t* row_ptr, const int32_t* col, const double* val,

@@ -127,3 +127,19 @@ def test_sparse_sharded_rejects_wide_halo():
     csr = nnb.Csr(rp, np.array(cl, np.int32), np.array(vl), n=n)
     with pytest.raises(nnb.DomainError):
         nnb.solve_sparse_factorized_sharded_emulated(csr, np.ones(n), 7, nnb.Normalization(theta=0.2, valid=True), 4)
+
+
+def test_sparse_plan_reuse_nccl_world1(ref):
+    """The prepared slab (nnb_sparse_plan_*) serves repeated solves, bit-exact each time."""
+    rp, col, val = W.laplacian_5pt(50)
+    comm = nnb.Comm(1, 0, nnb.Comm.unique_id())
+    plan = nnb.SparseShardedPlan(comm, nnb.Csr(rp, col, val, n=2500), 2500, k=1)
+    try:
+        for seed in (1, 2, 3):
+            b = W.rhs(2500, seed=seed)
+            x, cnt = plan.solve(b, 63, nnb.Normalization(theta=0.2, valid=True))
+            xr, _, _ = ref.sparse_factorized(rp, col, val, b, 63, 0.2)
+            assert cnt == 63 and np.array_equal(x, xr.real)
+    finally:
+        plan.close()
+        comm.close()
