@@ -34,3 +34,14 @@ if which == "detect":
         xh, _, _ = nnb.mimo_detect(h, y)
     torch.cuda.synchronize()
     print("prof_drive ok detect")
+if which == "dense32k":
+    # the headline workload: one nest of BASELINE config 3 (N=32768, p=2)
+    g = torch.Generator(device="cuda").manual_seed(2212)
+    b = torch.randn((32768, 32768), dtype=torch.float64, device="cuda", generator=g)
+    a = nnb.matmul_nt(b, b)
+    del b
+    a = nnb._axpby(1.0 / 32768, a, 0.0, None, 1.0)
+    x = nnb.x0(a)
+    x, rep = nnb.nn_chain(a, x, p=2, max_iters=1, final_residual=False)
+    torch.cuda.synchronize()
+    print("prof_drive ok dense32k", rep.device_ms)
