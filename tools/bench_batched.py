@@ -25,3 +25,15 @@ for _ in range(3):
 e1.record(); torch.cuda.synchronize()
 ms_ns = e0.elapsed_time(e1) / 3
 print(f"{os.environ.get('NNB_BATCHED_VARIANT','default'):10s} NN {ms:.3f} ms  {262144/ms/1e3:.1f} M inv/s  {262144*13*8*4096/ms/1e9:.2f} TF(4M-equiv)  maxrel {rel:.2e}  NS80 {ms_ns:.2f} ms")
+
+# fused detection
+h, y, s = W.mimo_uplink_device(262144, seed=2)
+for _ in range(3):
+    xh, _, _ = nnb.mimo_detect(h, y, 0.1, 2, 4)
+e0.record()
+for _ in range(10):
+    xh, _, _ = nnb.mimo_detect(h, y, 0.1, 2, 4)
+e1.record(); torch.cuda.synchronize()
+ms_d = e0.elapsed_time(e1) / 10
+ser = (torch.sign(xh.real) != torch.sign(s.real)).double().mean().item()
+print(f"{'':10s} detect {ms_d:.3f} ms  {262144/ms_d/1e3:.1f} M det/s  sign-err {ser:.2e}")
