@@ -468,10 +468,19 @@ def cpu_mimo_sample(sample: int):
 
 
 # ------------------------------------------------------------------ sparse leg (config 4)
-def sparse_bytes(n, nnz):
-    """Algorithmic bytes of one application: f64 values + int32 columns per
-    nonzero, int32 row offsets (the device narrows them), t read + t written per row."""
-    return nnz * (8 + 4) + (n + 1) * 4 + 2 * n * 8
+def sparse_bytes(n, nnz, col_bytes=4):
+    """Algorithmic bytes of one application in the format the kernel consumes:
+    f64 values + columns per nonzero (int16 deltas from the row when the band fits, else int32),
+    int32 row offsets (the device narrows them), t read + t written per row."""
+    return nnz * (8 + col_bytes) + (n + 1) * 4 + 2 * n * 8
+
+
+def csr_col_bytes(rp, col):
+    """2 when every |column - row| fits the device's int16 deltas (csrc/sparse.cu compact_csr), else 4."""
+    import numpy as np
+
+    rows = np.repeat(np.arange(rp.size - 1, dtype=np.int64), np.diff(rp))
+    return 2 if col.size == 0 or np.abs(col.astype(np.int64) - rows).max() <= 32767 else 4
 
 
 def run_sparse(args, world, rank):
@@ -513,7 +522,7 @@ def run_sparse(args, world, rank):
     if sharded:
         plan.close()
         comm.close()
-    alg = 63 * sparse_bytes(n, col.size)  # whole-job algorithmic bytes per solve
+    alg = 63 * sparse_bytes(n, col.size, csr_col_bytes(rp, col))  # whole-job bytes per solve
     gbs = alg / (ms * 1e-3) / 1e9
     return {"metric": "sparse factorized solve, 4096^2 5-pt Laplacian+I, gamma=63", "value": round(gbs, 1),
             "unit": "GB/s", "ms_per_step": round(ms, 3),
@@ -536,7 +545,7 @@ def cpu_sparse_sample(grid: int):
     rp, col, val = W.laplacian_5pt(grid)
     b = W.rhs(grid * grid, seed=7)
     _, _, secs = ref.sparse_factorized(rp, col, val, b, 63, 0.2)
-    gbs = 63 * sparse_bytes(grid * grid, col.size) / secs / 1e9
+    gbs = 63 * sparse_bytes(grid * grid, col.size, csr_col_bytes(rp, col)) / secs / 1e9  # same unit as the GPU leg
     return {"value": round(gbs, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
             "sample": f"reference solve_sparse_factorized gamma=63 on a {grid}^2 grid ({secs:.2f} s)"}
 

@@ -68,7 +68,8 @@ struct Slab {
   int64_t send_prev = 0, send_next = 0; // rows g−1 / g+1 need from us
   DevBuf mem;
   int32_t* rp = nullptr;                // local int32 offsets
-  int32_t* col = nullptr;               // remapped into the extended layout
+  int32_t* col = nullptr;               // remapped into the extended layout (wide operators)
+  int16_t* col16 = nullptr;             // column − global row (banded operators), else null
   const double* val = nullptr;
   double* ext[5] = {};                  // T0, T1, Z0, Z1, B (extended)
   int* flags = nullptr;                 // [64]
@@ -102,22 +103,28 @@ int setup_slab(Slab& sl, const int64_t* rp_dev, const int32_t* col_dev, const do
   sl.hi_start = h[3];
   if (sl.lo_end > sl.hi_start) sl.lo_end = sl.hi_start = sl.rows;  // no clean interior: all boundary (after halo)
   const size_t ext = (size_t)sl.ext_len() * k;
-  const size_t bytes = sizeof(int32_t) * (sl.rows + 1 + sl.nnz) + sizeof(double) * 5 * ext + sizeof(int) * 64 + 256;
+  const size_t bytes = sizeof(int32_t) * (sl.rows + 1 + sl.nnz) + sizeof(int16_t) * sl.nnz +
+                       sizeof(double) * 5 * ext + sizeof(int) * 64 + 256;
   NNB_TRY(sl.mem.alloc(bytes, s));
   char* p = sl.mem.as<char>();
   double* d = reinterpret_cast<double*>(p);
   for (int i = 0; i < 5; ++i) sl.ext[i] = d + i * ext;
   sl.rp = reinterpret_cast<int32_t*>(d + 5 * ext);
   sl.col = sl.rp + sl.rows + 1;
-  sl.flags = reinterpret_cast<int*>(sl.col + sl.nnz + 1);
+  int16_t* c16 = reinterpret_cast<int16_t*>(sl.col + sl.nnz + 1);
+  sl.flags = reinterpret_cast<int*>(c16 + sl.nnz + 8);
   sl.flags = reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(sl.flags) + 15) & ~uintptr_t(15));
   NNB_CUDA(cudaMemsetAsync(sl.flags, 0, sizeof(int) * 64, s));
   NNB_CUDA(cudaMemsetAsync(d, 0, sizeof(double) * 5 * ext, s));
-  NNB_TRY(narrow_offsets(rp_dev, sl.rp, sl.rows + 1, base, s));
-  if (sl.nnz)
+  bool fits = false;
+  NNB_TRY(compact_csr(rp_dev, col_dev, sl.rows, sl.row0, sl.rp, c16, &fits, s));
+  if (fits) {
+    sl.col16 = c16;
+  } else if (sl.nnz) {
     remap_cols_kernel<<<std::max<int64_t>(1, std::min<int64_t>(4736, (sl.nnz + 255) / 256)), 256, 0, s>>>(
         col_dev + base, sl.nnz, sl.h_lo - sl.row0, sl.col);
-  count_launch();
+    count_launch();
+  }
   sl.val = val_dev + base;
   NNB_CUDA(cudaGetLastError());
   return 0;
@@ -146,7 +153,7 @@ int run_slabs(std::vector<Slab*>& slabs, int64_t k, int s_factors, double theta,
       NNB_TRY(exchange(tin));
       for (size_t g = 0; g < slabs.size(); ++g) {
         Slab& sl = *slabs[g];
-        SpmvOp<int32_t> op{sl.rp, sl.col, sl.val, k, sl.ext[tin], sl.ext[tin] + sl.h_lo * k,
+        SpmvOp<int32_t> op{sl.rp, sl.col, sl.col16, sl.h_lo, sl.val, k, sl.ext[tin], sl.ext[tin] + sl.h_lo * k,
                            out < 0 ? x_own[g] : sl.ext[out] + sl.h_lo * k, sl.ext[zcur] + sl.h_lo * k, theta,
                            sl.flags + f};
         spmv_apply(op, mode, sl.lo_end, sl.hi_start, s);  // interior, while the halo is in flight

@@ -308,6 +308,34 @@ def test_sparse_long_rows_fallback(ref):
     assert np.array_equal(x, xr.real)
 
 
+def wide_band_csr(n: int = 100000, far: int = 40000):
+    """Tridiagonal plus a symmetric coupling at distance `far` > 32767: the column
+    deltas do not fit int16, so the solve must take the int32-column kernels."""
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        for j, v in ((i - far, -0.5), (i - 1, -1.0), (i, 6.0), (i + 1, -1.0), (i + far, -0.5)):
+            if 0 <= j < n:
+                rows.append(i)
+                cols.append(j)
+                vals.append(v)
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, np.array(rows) + 1, 1)
+    return np.cumsum(rp), np.array(cols, np.int32), np.array(vals)
+
+
+def test_sparse_wide_band_int32_columns(ref):
+    rp, col, val = wide_band_csr()
+    n = rp.size - 1
+    b = W.rhs(n, seed=12)
+    norm = nnb.Normalization(theta=1.0 / 9.0, valid=True)
+    xr, _, _ = ref.sparse_factorized(rp, col, val, b, 15, 1.0 / 9.0)
+    x, _ = nnb.solve_sparse_factorized(nnb.Csr(rp, col, val, n=n), b, 15, norm)
+    assert np.array_equal(x, xr.real)
+    # two slabs: each remaps its wide columns into the halo-extended layout
+    xs, _ = nnb.solve_sparse_factorized_sharded_emulated(nnb.Csr(rp, col, val, n=n), b, 15, norm, 2)
+    assert np.array_equal(xs, xr.real)
+
+
 def test_sparse_errors():
     rp, col, val = W.laplacian_5pt(8)
     csr = nnb.Csr(rp, col, val, n=64)
