@@ -7,6 +7,7 @@
 // point computes anything on the host.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/nnb.h"
@@ -111,6 +112,95 @@ void fill_result(nnb_chain_result* r, const ChainOut& o) {
   r->products = o.products;
   r->last_eps = o.last_eps;
   r->device_ms = o.device_ms;
+}
+
+// nnb_nn_chain_d with host A and/or host X_out, n >= kStreamMinN, fast
+// arithmetic.  X0, then A's row chunks, go host→device on a copy stream with
+// an event per chunk, so the first residual product starts once X0 and A's
+// first chunk have landed rather than after all 2·8·n² bytes.  The final X
+// leaves per chunk of the last Horner product (ChainIo).  NNB_STREAM_CHUNKS
+// sets the chunk count (default 8, 1..64).
+constexpr int64_t kStreamMinN = 8192;
+
+struct CopyLane {
+  cudaStream_t cs = nullptr;
+  std::vector<cudaEvent_t> ev;
+  CopyLane() = default;
+  CopyLane(const CopyLane&) = delete;
+  CopyLane& operator=(const CopyLane&) = delete;
+  ~CopyLane() {
+    if (cs) cudaStreamSynchronize(cs);
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+    if (cs) cudaStreamDestroy(cs);
+  }
+  int init(int events) {
+    NNB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    ev.assign(events, nullptr);
+    for (cudaEvent_t& e : ev) NNB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return 0;
+  }
+};
+
+int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_chain_config* cfg,
+                     const ChainCfg& c, double* X_out, double* eps_hist, nnb_chain_result* result,
+                     cudaStream_t s) {
+  static const int chunks = [] {
+    const char* e = std::getenv("NNB_STREAM_CHUNKS");
+    return std::min(64, std::max(1, e ? std::atoi(e) : 8));
+  }();
+  const bool host_a = !is_device_ptr(A), host_out = X_out && !is_device_ptr(X_out);
+  const bool x0_given = cfg->x0_kind == NNB_X0_GIVEN;
+  if (x0_given && !X0) return fail(NNB_ERR_DOMAIN, "nn chain: X0 required for NNB_X0_GIVEN");
+  DMat a, x;
+  if (host_a) NNB_TRY(a.alloc(n, n, s));
+  else NNB_TRY(a.load(A, n, n, n, s));
+  x.rows = x.cols = n;
+  x.ld = a.ld;
+  NNB_TRY(x.own.alloc(sizeof(double) * n * a.ld, s));
+  x.d = x.own.as<double>();
+  CopyLane lane;  // declared after the buffers: its destructor drains the copies before they are freed
+  NNB_TRY(lane.init(2 * chunks + 3));
+  cudaEvent_t* a_ready = lane.ev.data();
+  cudaEvent_t* out_done = a_ready + chunks;
+  cudaEvent_t alloc_ev = out_done[chunks], copy_done = out_done[chunks + 1], in_done = out_done[chunks + 2];
+  // the copy stream may touch the stream-ordered allocations only once they exist
+  NNB_CUDA(cudaEventRecord(alloc_ev, s));
+  NNB_CUDA(cudaStreamWaitEvent(lane.cs, alloc_ev, 0));
+  const int64_t rows_per = ((n + chunks - 1) / chunks + 127) / 128 * 128;
+  const int used = static_cast<int>((n + rows_per - 1) / rows_per);
+  // X0 first: every row chunk of the first product needs all of it
+  if (x0_given)
+    NNB_CUDA(cudaMemcpy2DAsync(x.d, x.ld * 8, X0, n * 8, n * 8, n, cudaMemcpyDefault, lane.cs));
+  if (host_a)
+    for (int q = 0; q < used; ++q) {
+      const int64_t r0 = q * rows_per, rows = std::min<int64_t>(rows_per, n - r0);
+      NNB_CUDA(cudaMemcpy2DAsync(a.d + r0 * a.ld, a.ld * 8, A + r0 * n, n * 8, n * 8, rows, cudaMemcpyHostToDevice,
+                                 lane.cs));
+      NNB_CUDA(cudaEventRecord(a_ready[q], lane.cs));
+    }
+  NNB_CUDA(cudaEventRecord(in_done, lane.cs));
+  ChainIo io;
+  io.chunks = used;
+  io.chunk_rows = rows_per;
+  io.copy = lane.cs;
+  io.out_done = out_done;
+  io.copy_done = copy_done;
+  io.host_out = host_out ? X_out : nullptr;
+  if (host_a && x0_given && cfg->order == NNB_ORDER_NORTHSTAR) {
+    io.a_ready = a_ready;  // the first product consumes A chunk by chunk
+  } else {
+    NNB_CUDA(cudaStreamWaitEvent(s, in_done, 0));
+    if (!x0_given) NNB_TRY(x0_build(a.d, a.ld, n, cfg->x0_kind, cfg->x0_scale, x.d, x.ld, s));
+  }
+  ChainOut o;
+  const int st = chain_real(a.d, n, a.ld, x.d, c, eps_hist, &o, s, &io);
+  fill_result(result, o);
+  if (st != 0 && st != NNB_ERR_DIVERGENCE && st != NNB_ERR_DOMAIN) return st;
+  if (X_out && !io.out_streamed) NNB_TRY(x.store(X_out, n, s));
+  NNB_TRY(sync(s));
+  NNB_CUDA(cudaStreamSynchronize(lane.cs));
+  return st;
 }
 
 }  // namespace
@@ -328,6 +418,9 @@ int nnb_nn_chain_d(const double* A, int64_t n, const double* X0, const nnb_chain
   ChainCfg c;
   NNB_TRY(chain_cfg(cfg, &c));
   cudaStream_t s = resolve(stream);
+  const bool host_a = !is_device_ptr(A), host_out = X_out && !is_device_ptr(X_out);
+  if ((host_a || host_out) && n >= kStreamMinN && arith() == 0)
+    return chain_d_streamed(A, n, X0, cfg, c, X_out, eps_hist, result, s);
   DMat a;
   NNB_TRY(a.load(A, n, n, n, s));
   DMat x;  // working X with A's leading dimension

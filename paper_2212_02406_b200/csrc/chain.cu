@@ -29,6 +29,20 @@ __global__ void combine_eps_kernel(const double* ss2, const int* nf2, double* ep
   }
 }
 
+__global__ void combine_chunks_kernel(const double* ss, const int* nf, int m, double* eps_out, int* nf_out,
+                                      double scale) {
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    int f = 0;
+    for (int q = 0; q < m; ++q) {  // fixed order: deterministic for a fixed chunking
+      t += ss[q];
+      f += nf[q];
+    }
+    if (eps_out) *eps_out = sqrt(t) * scale;
+    *nf_out = f;
+  }
+}
+
 struct Plane {
   double* re = nullptr;
   double* im = nullptr;  // null for real
@@ -101,8 +115,60 @@ int product(Ctx& c, const Plane& A, const Plane& B, double alpha, const Plane* D
   return 0;
 }
 
+// A real product in io.chunks row chunks (see ChainIo): chunk q first waits for
+// io.a_ready[q] (wait_in), and its rows are copied to io.host_out once written
+// (stream_out).  Σ C² is reduced per chunk and combined in chunk order.
+int product_chunked(Ctx& c, const Plane& A, const Plane& B, double alpha, const Plane* D, double beta,
+                    double gamma, const Plane& C, double* eps_out, int* nf_out, ChainIo& io, bool wait_in,
+                    bool stream_out, double* chunk_ss, int* chunk_nf) {
+  int m = 0;
+  for (int q = 0; q < io.chunks; ++q) {
+    const int64_t r0 = q * io.chunk_rows, rows = std::min<int64_t>(io.chunk_rows, c.n - r0);
+    if (rows <= 0) break;
+    if (wait_in) NNB_CUDA(cudaStreamWaitEvent(c.s, io.a_ready[q], 0));
+    GemmOp op;
+    op.M = rows;
+    op.N = op.K = c.n;
+    op.lda = op.ldb = c.ld;
+    op.A = A.re + r0 * c.ld;
+    op.B = B.re;
+    op.ep.alpha = alpha;
+    op.ep.D = D ? D->re + r0 * c.ld : nullptr;
+    op.ep.ldd = c.ld;
+    op.ep.beta = beta;
+    op.ep.gamma = gamma;
+    op.ep.diag_offset = r0;
+    op.ep.C = C.re + r0 * c.ld;
+    op.ep.ldc = c.ld;
+    if (nf_out) {
+      op.ep.ss_out = chunk_ss + q;
+      op.ep.nf_out = chunk_nf + q;
+    }
+    NNB_TRY(gemm(op, nf_out ? &c.red : nullptr, c.s));
+    if (stream_out) {
+      NNB_CUDA(cudaEventRecord(io.out_done[q], c.s));
+      NNB_CUDA(cudaStreamWaitEvent(io.copy, io.out_done[q], 0));
+      NNB_CUDA(cudaMemcpy2DAsync(io.host_out + r0 * c.n, c.n * sizeof(double), C.re + r0 * c.ld,
+                                 c.ld * sizeof(double), c.n * sizeof(double), rows, cudaMemcpyDeviceToHost,
+                                 io.copy));
+    }
+    ++m;
+  }
+  if (stream_out) {  // nothing on c.s may free or overwrite C before the copies finish
+    NNB_CUDA(cudaEventRecord(io.copy_done, io.copy));
+    NNB_CUDA(cudaStreamWaitEvent(c.s, io.copy_done, 0));
+  }
+  if (nf_out) {
+    combine_chunks_kernel<<<1, 32, 0, c.s>>>(chunk_ss, chunk_nf, m, eps_out, nf_out,
+                                             1.0 / std::sqrt(static_cast<double>(c.n)));
+    count_launch();
+    NNB_CUDA(cudaGetLastError());
+  }
+  return 0;
+}
+
 int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_hist,
-              ChainOut* out) {
+              ChainOut* out, ChainIo* io = nullptr) {
   const int64_t n = c.n, mat = n * c.ld;
   const int planes = c.cplx ? 2 : 1;
   const int p = cfg.p;
@@ -113,11 +179,15 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
   NNB_TRY(work.alloc(sizeof(double) * (size_t)mat * planes * 3, c.s));
   DevBuf scal;
   const size_t nf_count = (size_t)slots * (p + 1);
-  NNB_TRY(scal.alloc(sizeof(double) * (slots + 8) + sizeof(int) * (nf_count + 8), c.s));
+  constexpr int kMaxChunks = 64;
+  if (io && (io->chunks < 1 || io->chunks > kMaxChunks || c.cplx)) io = nullptr;
+  NNB_TRY(scal.alloc(sizeof(double) * (slots + 8 + kMaxChunks) + sizeof(int) * (nf_count + 8 + kMaxChunks), c.s));
   double* eps_dev = scal.as<double>();
   c.ss2 = eps_dev + slots;
-  int* nf_dev = reinterpret_cast<int*>(c.ss2 + 8);
+  double* chunk_ss = c.ss2 + 8;
+  int* nf_dev = reinterpret_cast<int*>(chunk_ss + kMaxChunks);
   c.nf2 = nf_dev + nf_count;
+  int* chunk_nf = c.nf2 + 8;
   NNB_CUDA(cudaMemsetAsync(scal.p, 0, scal.bytes, c.s));
 
   auto plane_at = [&](int i) {
@@ -150,7 +220,11 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
     const Plane& Xk = bufs[xi];
     const Plane& lhs = order == 0 ? A : Xk;
     const Plane& rhs = order == 0 ? Xk : A;
-    NNB_TRY(product(c, lhs, rhs, -1.0, nullptr, 0.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1)));
+    if (k == 0 && io && io->a_ready && order == 0)  // R_0 = I − A·X_0 as A's rows arrive
+      NNB_TRY(product_chunked(c, lhs, rhs, -1.0, nullptr, 0.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1), *io, true,
+                              false, chunk_ss, chunk_nf));
+    else
+      NNB_TRY(product(c, lhs, rhs, -1.0, nullptr, 0.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1)));
     ++products;
     recorded = k + 1;
     if (tol_mode) {
@@ -191,7 +265,14 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
         const Plane& dst = bufs[dst_i];
         const Plane& l = cfg.order == 0 ? v : R;
         const Plane& r = cfg.order == 0 ? R : v;
-        NNB_TRY(product(c, l, r, 1.0, &Xk, 1.0, 0.0, dst, nullptr, nf_dev + k * (p + 1) + j));
+        if (io && io->host_out && !tol_mode && j == p && k == cfg.max_iters - 1 && cfg.order == 0) {
+          // the final X: rows leave for the host as their chunk completes
+          NNB_TRY(product_chunked(c, l, r, 1.0, &Xk, 1.0, 0.0, dst, nullptr, nf_dev + k * (p + 1) + j, *io, false,
+                                  true, chunk_ss, chunk_nf));
+          io->out_streamed = true;
+        } else {
+          NNB_TRY(product(c, l, r, 1.0, &Xk, 1.0, 0.0, dst, nullptr, nf_dev + k * (p + 1) + j));
+        }
         ++products;
         v = dst;
         vi = dst_i;
@@ -203,7 +284,7 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
   }
   NNB_CUDA(cudaEventRecord(e1, c.s));
   // copy the final iterate into the caller's X buffer if it lives elsewhere
-  if (bufs[xi].re != caller_x.re) {
+  if (bufs[xi].re != caller_x.re && !(io && io->out_streamed)) {
     NNB_TRY(copy2d(bufs[xi].re, c.ld, caller_x.re, c.ld, n, n, c.s));
     if (c.cplx) NNB_TRY(copy2d(bufs[xi].im, c.ld, caller_x.im, c.ld, n, n, c.s));
   }
@@ -546,14 +627,14 @@ int ns_sum_dev(const double* phi0_re, const double* phi0_im, const double* w_re,
 }
 
 int chain_real(const double* A, int64_t n, int64_t ldn, double* X, const ChainCfg& cfg,
-               double* eps_hist, ChainOut* out, cudaStream_t s) {
+               double* eps_hist, ChainOut* out, cudaStream_t s, ChainIo* io) {
   Ctx c;
   c.n = n;
   c.ld = ldn;
   c.cplx = false;
   c.s = s;
   Plane a{const_cast<double*>(A), nullptr}, x{X, nullptr};
-  return run_chain(c, a, x, cfg, eps_hist, out);
+  return run_chain(c, a, x, cfg, eps_hist, out, io);
 }
 
 int chain_complex(const double* Ar, const double* Ai, int64_t n, int64_t ldn, double* Xr,

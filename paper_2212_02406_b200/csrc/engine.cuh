@@ -129,10 +129,26 @@ struct ChainOut {
   float device_ms = 0.f;
   int x_index = 0;  // sharded driver: which ping-pong buffer holds the final X
 };
+// Host-streaming hooks of the real chain (nnb_nn_chain_d with host buffers):
+// the first residual product runs in row chunks as A's rows land (NORTHSTAR
+// order, R = I − A·X: row chunk q needs only A's rows of q), and the last
+// Horner product runs in row chunks whose rows go device→host on `copy` as
+// soon as they are written.  PCIe then overlaps the DMMA work instead of
+// bracketing it.
+struct ChainIo {
+  int chunks = 0;
+  int64_t chunk_rows = 0;
+  cudaEvent_t* a_ready = nullptr;  // [chunks] rows of chunk q (and X0) are on the device; null: all present
+  double* host_out = nullptr;      // row-major n×n host destination of the final X (nullable)
+  cudaStream_t copy = nullptr;
+  cudaEvent_t* out_done = nullptr; // [chunks] scratch
+  cudaEvent_t copy_done = nullptr; // scratch
+  bool out_streamed = false;       // run_chain delivered the final X to host_out (X itself is then stale)
+};
 // Real chain on device buffers with ld == ldn (ldn even, >= n).  X holds X0
 // on entry and the final iterate on exit.  eps_hist host (nullable).
 int chain_real(const double* A, int64_t n, int64_t ldn, double* X, const ChainCfg& cfg,
-               double* eps_hist, ChainOut* out, cudaStream_t s);
+               double* eps_hist, ChainOut* out, cudaStream_t s, ChainIo* io = nullptr);
 // Complex chain on planar device buffers (re/im each n×ldn).
 int chain_complex(const double* Ar, const double* Ai, int64_t n, int64_t ldn, double* Xr,
                   double* Xi, const ChainCfg& cfg, double* eps_hist, ChainOut* out,

@@ -207,6 +207,46 @@ def test_chain_large_properties():
     assert (torch.linalg.norm(r) / 64).item() < 1e-11
 
 
+def _gram_device(n, seed):
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    b = torch.randn(n, n, device="cuda", dtype=torch.float64, generator=g)
+    a = b @ b.T / n + torch.eye(n, device="cuda", dtype=torch.float64)
+    x0 = a.T / (a.abs().sum(0).max() * a.abs().sum(1).max())
+    return a, x0.contiguous()
+
+
+@pytest.mark.parametrize("pinned_out", [False, True])
+def test_chain_host_streaming_matches_device(pinned_out):
+    """Host A (n >= 8192): X0 and A's row chunks stream in under the first product and the
+    final X streams out under the last one (capi.cu chain_d_streamed).  The row-chunked
+    GEMMs compute the same tiles in the same K order, so X is bit-identical to the
+    device-buffer run; only eps's Σ is combined per chunk."""
+    import torch
+
+    n = 8192
+    a, x0 = _gram_device(n, seed=6)
+    ah, x0h = a.cpu().pin_memory().numpy(), x0.cpu().numpy()
+    for kw in (dict(p=2, max_iters=2, final_residual=False), dict(p=1, max_iters=3),
+               dict(p=2, max_iters=40, tol=1e-9), dict(p=2, max_iters=2, order=nnb.ORDER_REFERENCE)):
+        xd, rd = nnb.nn_chain(a, x0, **kw)
+        out = torch.empty((n, n), dtype=torch.float64).pin_memory().numpy() if pinned_out else None
+        xh, rh = nnb.nn_chain(ah, x0h, out=out, **kw)
+        if out is not None:
+            assert xh is out
+        assert np.array_equal(xh, xd.cpu().numpy()), kw
+        assert rh.iters == rd.iters and rh.products == rd.products and rh.stopped_reason == rd.stopped_reason
+        eh, ed = np.array([e for _, e in rh.history]), np.array([e for _, e in rd.history])
+        assert eh.shape == ed.shape and np.allclose(eh, ed, rtol=1e-12, atol=0)
+    # device A with a host X_out streams only the output
+    xo = torch.empty((n, n), dtype=torch.float64).pin_memory().numpy()
+    xd, _ = nnb.nn_chain(a, x0, p=2, max_iters=1, final_residual=False)
+    xh, _ = nnb.nn_chain(a, x0, p=2, max_iters=1, final_residual=False, out=xo)
+    torch.cuda.synchronize()
+    assert np.array_equal(xo, xd.cpu().numpy())
+
+
 # ----------------------------------------------------------------- batched MIMO (C2)
 def test_batched_vs_golden():
     g = golden("c2_mimo16.npz")
