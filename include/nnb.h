@@ -117,6 +117,12 @@ int nnb_axpby_d(double alpha, const double* A, double beta, const double* B, dou
 int nnb_axpby_z(const double* alpha2, const double* A, const double* beta2, const double* B,
                 const double* gamma2, double* out, int64_t rows, int64_t cols, void* stream);
 
+/* out (cols×rows) = M^T (real) or M^H (complex interleaved), a tiled device
+ * transpose.  Replaces nn::conjugate_transpose (proj/include/nn/kernels.hpp:37,
+ * proj/src/kernels.cpp:223-229); used by the normal-equations solve. */
+int nnb_transpose_d(const double* M, int64_t rows, int64_t cols, double* out, void* stream);
+int nnb_conj_transpose_z(const double* M, int64_t rows, int64_t cols, double* out, void* stream);
+
 /* ||M||_F (proj/include/nn/kernels.hpp:42) and trace (:40). */
 int nnb_frobenius_d(const double* M, int64_t count, double* out, void* stream);
 int nnb_frobenius_z(const double* M, int64_t count, double* out, void* stream);

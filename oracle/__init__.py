@@ -187,6 +187,25 @@ class Reference(_Lib):
                          stopped="tolerance" if sr.value == 0 else "max_nests",
                          alpha=None if alpha.value < 0 else alpha.value)
 
+    def solve_normal(self, a, b, depth: int, max_nests: int, tol: float):
+        """nn::solve_normal_equations; raises OracleError(20) on NonConvergenceError."""
+        a, b = _z(a), _z(b)
+        n, k = a.shape[0], b.shape[1]
+        x = np.empty((n, k), np.complex128)
+        hist = np.zeros(max_nests + 2)
+        hl, sr, bw, fail = C.c_int64(), C.c_int(), C.c_double(), C.c_int(-1)
+        counts = np.zeros(2)
+        f = self.fn("solve_normal_z", [_dp, C.c_int64, _dp, C.c_int64, C.c_int64, C.c_int64, C.c_double, _dp, _dp,
+                                       _i64p, _dp, _ip, _dp, _ip])
+        st = f(_ptr(a), n, _ptr(b), k, depth, max_nests, tol, _ptr(x), _ptr(hist), C.byref(hl), _ptr(counts),
+               C.byref(sr), C.byref(bw), C.byref(fail))
+        rep = dict(history=hist[: hl.value].copy(), n3=counts[0], n2=int(counts[1]),
+                   stopped="tolerance" if sr.value == 0 else "max_nests")
+        if st == 20:
+            raise OracleError(st, "NonConvergenceError", rep)
+        self._check(st, fail.value)
+        return x, rep, bw.value
+
     def theta_trace(self, w):
         w = _z(w)
         th, con, va = C.c_double(), C.c_double(), C.c_int()

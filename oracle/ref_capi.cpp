@@ -204,6 +204,40 @@ int nnref_chain_z(const double* a, int64_t n, const double* x0, int p, int max_i
   }, fail_iter);
 }
 
+// nn::solve_normal_equations (proj/src/factorized.cpp:63-99) on a dense n×n A
+// and n×k B.  Returns 20 (with the report's history and counts filled) when
+// the reference raises NonConvergenceError.
+int nnref_solve_normal_z(const double* a, int64_t n, const double* b, int64_t k, int64_t depth_l,
+                         int64_t max_nests, double tol, double* x_out, double* hist, int64_t* hist_len,
+                         double* counts, int* stop_reason, double* backward, int* fail_iter) {
+  int nonconv = 0;
+  const int st = guarded([&] {
+    nn::SolverConfig cfg;
+    cfg.depth_L = static_cast<std::size_t>(depth_l);
+    cfg.max_nests = static_cast<std::size_t>(max_nests);
+    cfg.tol = tol;
+    nn::OpCounter cnt;
+    auto report_out = [&](const nn::ConvergenceReport& rep) {
+      for (std::size_t i = 0; i < rep.history.size(); ++i) hist[i] = rep.history[i].second;
+      *hist_len = static_cast<int64_t>(rep.history.size());
+      *stop_reason = rep.stopped_reason == nn::StopReason::Tolerance ? 0 : 1;
+    };
+    try {
+      nn::LinearSystem sys{load(a, n, n), load(b, n, k), false};
+      auto res = nn::solve_normal_equations(sys, cfg, &cnt);
+      store(res.x, x_out);
+      report_out(res.report);
+      *backward = res.backward_error;
+    } catch (const nn::NonConvergenceError& e) {
+      report_out(e.report);
+      nonconv = 1;
+    }
+    counts[0] = cnt.n3_multiplies();
+    counts[1] = static_cast<double>(cnt.n2_ops());
+  }, fail_iter);
+  return st == kOk && nonconv ? 20 : st;
+}
+
 // nn::nn_invert (proj/src/solver.cpp:123-174) with an explicit Normalization.
 // hist gets (eps) per recorded nest; counts[0]=n3, counts[1]=n2.
 int nnref_nn_invert_z(const double* w, int64_t n, double theta, int valid, int64_t depth_l,

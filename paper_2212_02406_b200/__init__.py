@@ -117,6 +117,8 @@ _SIGS = {
     "nnb_spmv_block_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _dp, _dp], C.c_int),
     "nnb_sparse_factorized_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _i64, C.c_double, _dp, _dp, _dp,
                                  _dp], C.c_int),
+    "nnb_transpose_d": ([_dp, _i64, _i64, _dp, _dp], C.c_int),
+    "nnb_conj_transpose_z": ([_dp, _i64, _i64, _dp, _dp], C.c_int),
     "nnb_spectral_norm_z": ([_dp, _i64, _dp, C.c_double, _i32, _dp, _dp, _dp, _dp], C.c_int),
     "nnb_spectral_norm_shifted_csr": ([_dp, _dp, _dp, _i64, _i64, C.c_double, _dp, C.c_double, _i32, _dp, _dp,
                                        _dp, _dp], C.c_int),
@@ -313,6 +315,16 @@ def plus_identity(m):
     if m.shape[0] != m.shape[1]:
         raise ShapeError("plus_identity: matrix must be square")
     return _axpby(1.0, m, 0.0, None, 1.0)
+
+
+def conjugate_transpose(a):
+    """nn::conjugate_transpose (proj/include/nn/kernels.hpp:37): Aᵀ for real, Aᴴ for complex, on the device."""
+    z = _is_complex(a)
+    a = _prep(a, z)
+    out = _empty_like(a, (a.shape[1], a.shape[0]))
+    f = lib().nnb_conj_transpose_z if z else lib().nnb_transpose_d
+    _check(f(_ptr(a), a.shape[0], a.shape[1], _ptr(out), _stream(a)))
+    return out
 
 
 def frobenius_norm(m) -> float:

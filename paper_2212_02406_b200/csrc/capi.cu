@@ -364,6 +364,29 @@ int nnb_axpby_z(const double* alpha2, const double* A, const double* beta2, cons
   return sync(s);
 }
 
+static int transpose_call(const double* M, int64_t rows, int64_t cols, int cplx, double* out, void* stream) {
+  NNB_TRY(require_device());
+  if (rows < 0 || cols < 0) return fail(NNB_ERR_SHAPE, "conjugate_transpose: negative shape");
+  if (M == out && rows * cols) return fail(NNB_ERR_DOMAIN, "conjugate_transpose: out must not alias M");
+  cudaStream_t s = resolve(stream);
+  const size_t cnt = (size_t)((cplx ? 2 : 1) * rows * cols);
+  In m;
+  NNB_TRY(m.stage(M, cnt, s));
+  Out o;
+  NNB_TRY(o.prepare(out, cnt, s));
+  NNB_TRY(transpose(m.d, rows, cols, cplx, o.d, s));
+  NNB_TRY(o.finish(s));
+  return sync(s);
+}
+
+int nnb_transpose_d(const double* M, int64_t rows, int64_t cols, double* out, void* stream) {
+  return transpose_call(M, rows, cols, 0, out, stream);
+}
+
+int nnb_conj_transpose_z(const double* M, int64_t rows, int64_t cols, double* out, void* stream) {
+  return transpose_call(M, rows, cols, 1, out, stream);
+}
+
 static int frob(const double* M, int64_t count, double* out, cudaStream_t s) {
   In m;
   NNB_TRY(m.stage(M, (size_t)count, s));

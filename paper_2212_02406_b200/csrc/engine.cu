@@ -242,6 +242,46 @@ int gemm(GemmOp op, RedWs* red, cudaStream_t s) {
 }
 
 // ============================ auxiliary kernels ============================
+// 32×32 tiles through shared memory (+1 column of padding): coalesced reads of
+// M's rows and coalesced writes of out's rows; the conjugate rides along.
+template <typename T, bool CONJ>
+__global__ void transpose_kernel(const T* __restrict__ in, int64_t rows, int64_t cols, T* __restrict__ out) {
+  __shared__ T tile[32][33];
+  const int64_t tiles_c = (cols + 31) / 32, tiles = tiles_c * ((rows + 31) / 32);
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t r0 = (t / tiles_c) * 32, c0 = (t % tiles_c) * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const int64_t r = r0 + i, c = c0 + threadIdx.x;
+      if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const int64_t c = c0 + i, r = r0 + threadIdx.x;  // out row c, column r
+      if (r < rows && c < cols) {
+        T v = tile[threadIdx.x][i];
+        if constexpr (CONJ) v.y = -v.y;
+        out[c * rows + r] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+int transpose(const double* M, int64_t rows, int64_t cols, int cplx, double* out, cudaStream_t s) {
+  if (rows * cols == 0) return 0;
+  const int64_t tiles = ((rows + 31) / 32) * ((cols + 31) / 32);
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(tiles, 148 * 16));
+  const dim3 block(32, 8);
+  if (cplx)
+    transpose_kernel<double2, true><<<grid, block, 0, s>>>(reinterpret_cast<const double2*>(M), rows, cols,
+                                                           reinterpret_cast<double2*>(out));
+  else
+    transpose_kernel<double, false><<<grid, block, 0, s>>>(M, rows, cols, out);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
 __global__ void axpby_kernel(double alpha, const double* __restrict__ A, int64_t lda, double beta,
                              const double* __restrict__ B, int64_t ldb, double gamma, int64_t off,
                              double* out, int64_t ldo, int64_t rows, int64_t cols) {

@@ -111,6 +111,8 @@ int trace_dev(const double* M, int64_t n, int64_t ld, int complex_stride, double
 int deinterleave(const double* z, int64_t count, double* re, double* im, cudaStream_t s);
 int interleave(const double* re, const double* im, int64_t count, double* z, cudaStream_t s);
 int fill_identity(double* X, int64_t n, int64_t ld, double val, cudaStream_t s);
+// out (cols×rows) = Mᵀ (cplx = 0) or Mᴴ of interleaved complex M (cplx = 1)
+int transpose(const double* M, int64_t rows, int64_t cols, int cplx, double* out, cudaStream_t s);
 
 // ---- dense chain -----------------------------------------------------------------
 struct ChainCfg {

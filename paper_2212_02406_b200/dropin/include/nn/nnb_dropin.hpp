@@ -9,9 +9,8 @@
 // bookkeeping (reports, nest estimates, order fits).
 //
 // Out of scope (not declared; link the reference's nncore for them):
-// direct_inverse_oracle, random_* generators, matvec, conjugate_transpose,
-// theta_power, contraction_check, solve_normal_equations, cns_invert, the
-// cost model and Matrix Market I/O.
+// direct_inverse_oracle, random_* generators, matvec, theta_power,
+// contraction_check, cns_invert and the cost model.
 #pragma once
 
 #include <atomic>
@@ -218,6 +217,7 @@ DenseMatrix sub(const DenseMatrix& a, const DenseMatrix& b, OpCounter* counter =
 DenseMatrix scale(const DenseMatrix& m, Scalar factor, OpCounter* counter = nullptr);
 DenseMatrix identity_minus(const DenseMatrix& m, OpCounter* counter = nullptr);
 DenseMatrix plus_identity(const DenseMatrix& m, OpCounter* counter = nullptr);
+DenseMatrix conjugate_transpose(const DenseMatrix& m, OpCounter* counter = nullptr);
 Scalar trace(const DenseMatrix& m);
 double frobenius_norm(const DenseMatrix& m);
 
@@ -322,5 +322,15 @@ DenseMatrix ns_factorized(const DenseMatrix& phi, const DenseMatrix& w_tilde, co
                           OpCounter* counter = nullptr);
 DenseMatrix solve_sparse_factorized(const LinearSystem& sys, const BigInt& gamma,
                                     const Normalization& norm, OpCounter* counter = nullptr);
+
+struct NormalSolveResult {
+  DenseMatrix x;
+  ConvergenceReport report;
+  double backward_error = 0.0;  // ||W x - rhs||_F / ||rhs||_F on the normal equations
+};
+/// A x = B through W = A^H A (Hermitian PSD), theta_trace(W), nn_invert(W)
+/// and x = W^-1 A^H B, every product on the GPU.
+NormalSolveResult solve_normal_equations(const LinearSystem& sys, const SolverConfig& config,
+                                         OpCounter* counter = nullptr);
 
 }  // namespace nn

@@ -54,6 +54,14 @@ DenseMatrix from_real(std::size_t r, std::size_t c, const std::vector<double>& v
 const double* zp(const DenseMatrix& m) { return reinterpret_cast<const double*>(m.data().data()); }
 double* zp(DenseMatrix& m) { return reinterpret_cast<double*>(m.data().data()); }
 
+// The reference tallies one n3 unit per product as it runs; replaying the
+// fused device schedule's count the same way keeps the atomic double sum
+// bit-identical when fractional (non-square) products are mixed in.
+void add_products(OpCounter* counter, double count) {
+  if (!counter) return;
+  for (double i = 0.0; i < count; i += 1.0) counter->add_n3(1.0);
+}
+
 void require_finite(const DenseMatrix& m, const char* op) {
   if (!m.all_finite()) throw DomainError(std::string(op) + ": produced a non-finite entry");
 }
@@ -345,6 +353,15 @@ DenseMatrix plus_identity(const DenseMatrix& m, OpCounter* counter) {
   return out;
 }
 
+DenseMatrix conjugate_transpose(const DenseMatrix& m, OpCounter* counter) {
+  DenseMatrix out(m.cols(), m.rows());
+  if (m.size())
+    check(nnb_conj_transpose_z(zp(m), (int64_t)m.rows(), (int64_t)m.cols(), zp(out), nullptr),
+          "conjugate_transpose");
+  if (counter) counter->add_n2();  // one O(n^2) pass, as kernels.cpp:223-229 tallies it
+  return out;
+}
+
 Scalar trace(const DenseMatrix& m) {
   if (!m.square()) throw ShapeError("trace: matrix must be square");
   double t[2] = {0.0, 0.0};
@@ -419,7 +436,7 @@ DenseMatrix power_ladder(const DenseMatrix& p, std::uint64_t exponent, OpCounter
         return z ? nnb_power_ladder_z(a, n, exponent, o, pr, nullptr) : nnb_power_ladder_d(a, n, exponent, o, pr, nullptr);
       },
       &prods, "power_ladder");
-  if (counter) counter->add_n3(prods);
+  add_products(counter, prods);
   return out;
 }
 
@@ -519,7 +536,7 @@ DenseMatrix ns_sum(const DenseMatrix& phi0, const DenseMatrix& w_tilde, std::siz
     check(nnb_ns_sum_z(zp(phi0), zp(w_tilde), (int64_t)n, (int64_t)order, zp(out), &products, nullptr), "ns_sum");
   }
   if (counter) {
-    counter->add_n3(products);  // order-1 chain products (+2 when phi0 != I)
+    add_products(counter, products);  // order-1 chain products (+2 when phi0 != I)
     counter->add_n2(static_cast<std::int64_t>(order) + 1);  // identity_minus + order plus_identity
   }
   return out;
@@ -531,7 +548,7 @@ DenseMatrix nn_step(const DenseMatrix& phi, const DenseMatrix& w_tilde, std::siz
   if (depth_L == 0) return phi;
   DenseMatrix out = device_nest(phi, w_tilde, depth_L, "nn_step");
   if (counter) {
-    counter->add_n3(static_cast<double>(depth_L + 1));
+    add_products(counter, static_cast<double>(depth_L + 1));
     counter->add_n2(static_cast<std::int64_t>(depth_L + 1));
   }
   return out;
@@ -542,7 +559,7 @@ DenseMatrix newton_step(const DenseMatrix& z, const DenseMatrix& w_tilde, OpCoun
   conform_square(z, w_tilde, "newton_step");
   DenseMatrix out = device_nest(z, w_tilde, 1, "newton_step");
   if (counter) {
-    counter->add_n3(2.0);
+    add_products(counter, 2.0);
     counter->add_n2(1);
   }
   return out;
@@ -553,7 +570,7 @@ DenseMatrix chebyshev_step(const DenseMatrix& z, const DenseMatrix& w_tilde, OpC
   conform_square(z, w_tilde, "chebyshev_step");
   DenseMatrix out = device_nest(z, w_tilde, 2, "chebyshev_step");
   if (counter) {
-    counter->add_n3(3.0);
+    add_products(counter, 3.0);
     counter->add_n2(2);
   }
   return out;
@@ -595,7 +612,7 @@ std::pair<DenseMatrix, ConvergenceReport> nn_invert(const DenseMatrix& w, const 
   const double n3 = static_cast<double>(nests * (config.depth_L + 1));
   const std::int64_t n2 = static_cast<std::int64_t>(nests * (config.depth_L + 1));
   if (counter) {
-    counter->add_n3(n3);
+    add_products(counter, n3);
     counter->add_n2(n2);
     report.n3_multiplies = n3;
     report.n2_ops = n2;
@@ -626,7 +643,7 @@ DenseMatrix nn_explicit(const DenseMatrix& phi0, const DenseMatrix& w_tilde, std
       },
       &prods, "nn_explicit");
   if (counter) {
-    counter->add_n3(prods);
+    add_products(counter, prods);
     counter->add_n2(1 + static_cast<std::int64_t>((nests_i + 1) * depth_L));  // identity_minus + plus_identity's
   }
   return out;
@@ -703,10 +720,36 @@ DenseMatrix ns_factorized(const DenseMatrix& phi, const DenseMatrix& w_tilde, co
       },
       &prods, "ns_factorized");
   if (counter) {
-    counter->add_n3(prods);
+    add_products(counter, prods);
     counter->add_n2(static_cast<std::int64_t>(plan.num_factors) + 1);  // identity_minus + s plus_identity
   }
   return out;
+}
+
+// proj/src/factorized.cpp:63-99: W = A^H A and rhs = A^H B (unless the caller
+// already formed them), theta from theta_trace(W), W^-1 from nn_invert, then
+// x = W^-1 rhs.  The backward error on the normal equations is diagnostic and
+// untallied; NonConvergenceError when the nest budget ran out above tol.
+NormalSolveResult solve_normal_equations(const LinearSystem& sys, const SolverConfig& config, OpCounter* counter) {
+  const DenseMatrix a = std::holds_alternative<DenseMatrix>(sys.a) ? std::get<DenseMatrix>(sys.a)
+                                                                    : std::get<SparseMatrixCsr>(sys.a).densify();
+  if (!a.square()) throw ShapeError("solve_normal_equations: A must be square");
+  if (sys.b.rows() != a.rows()) throw ShapeError("solve_normal_equations: B row count does not match A");
+  DenseMatrix w = a, rhs = sys.b;
+  if (!sys.hermitian_normal) {
+    const DenseMatrix ah = conjugate_transpose(a, counter);
+    w = matmul(ah, a, counter);
+    rhs = matmul(ah, sys.b, counter);
+  }
+  auto [w_inv, report] = nn_invert(w, theta_trace(w), config, counter);
+  NormalSolveResult res{matmul(w_inv, rhs, counter), std::move(report), 0.0};
+  const double rn = frobenius_norm(rhs), en = frobenius_norm(sub(matmul(w, res.x), rhs));
+  res.backward_error = rn > 0.0 ? en / rn : en;
+  if (res.report.stopped_reason == StopReason::MaxNests && res.backward_error > config.tol)
+    throw NonConvergenceError("solve_normal_equations: nest budget exhausted with backward error " +
+                                  std::to_string(res.backward_error),
+                              res.report);
+  return res;
 }
 
 DenseMatrix solve_sparse_factorized(const LinearSystem& sys, const BigInt& gamma, const Normalization& norm,

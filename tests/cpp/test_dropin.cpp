@@ -384,12 +384,130 @@ static void schedule_tests() {
   CHECK_THROWS(nn_explicit(DenseMatrix::identity(2), normalized(2, 0.5, 21), 40, 2), BudgetError);
 }
 
+// conjugate_transpose and solve_normal_equations (proj/tests/test_factorized.cpp:80-148,
+// test_matrix_core.cpp conjugate_transpose cases), inputs from this file's generators.
+static void normal_equation_tests() {
+  const DenseMatrix z = gauss(5, 3, 91, true);
+  const DenseMatrix zh = conjugate_transpose(z);
+  CHECK(zh.rows() == 3 && zh.cols() == 5);
+  bool conj_ok = true;
+  for (std::size_t i = 0; i < 5; ++i)
+    for (std::size_t j = 0; j < 3; ++j) conj_ok &= zh(j, i) == std::conj(z(i, j));
+  CHECK(conj_ok);
+  CHECK(conjugate_transpose(zh) == z);
+  OpCounter ct;
+  conjugate_transpose(z, &ct);
+  CHECK(ct.n2_ops() == 1 && ct.n3_multiplies() == 0.0);
+
+  SolverConfig cfg;
+  cfg.depth_L = 2;
+  cfg.tol = 1e-12;
+  cfg.max_nests = 40;
+  const DenseMatrix b6 = spd(6, 3.0, 5);
+  CHECK(rel(solve_normal_equations({DenseMatrix::identity(6), b6, false}, cfg).x, b6) < 1e-12);
+
+  const DenseMatrix d = DenseMatrix::diagonal({Scalar{1, 0}, Scalar{2, 0}, Scalar{4, 0}});
+  DenseMatrix ones(3, 1);
+  ones(0, 0) = ones(1, 0) = ones(2, 0) = Scalar{1, 0};
+  cfg.tol = 1e-13;
+  cfg.max_nests = 60;
+  const auto rd = solve_normal_equations({d, ones, false}, cfg);
+  CHECK(std::fabs(rd.x(0, 0).real() - 1.0) < 1e-10 && std::fabs(rd.x(1, 0).real() - 0.5) < 1e-10 &&
+        std::fabs(rd.x(2, 0).real() - 0.25) < 1e-10);
+  CHECK(rd.backward_error < 1e-12);
+
+  // W = A^H A is Hermitian to rounding
+  DenseMatrix a = gauss(12, 12, 93, true);
+  for (std::size_t i = 0; i < 12; ++i) a(i, i) += Scalar{4.0, 0};
+  const DenseMatrix w = matmul(conjugate_transpose(a), a);
+  CHECK(rel(conjugate_transpose(w), w) < 1e-12);
+
+  // a complex system: x solves A x = B, tallies as the reference counts them
+  const DenseMatrix bb = gauss(12, 2, 95, true);
+  cfg.depth_L = 2;
+  cfg.tol = 1e-11;
+  cfg.max_nests = 40;
+  OpCounter cs;
+  const auto rs = solve_normal_equations({a, bb, false}, cfg, &cs);
+  CHECK(rel(matmul(a, rs.x), bb) < 1e-9);
+  CHECK(rs.report.stopped_reason == StopReason::Tolerance);
+  const double nests = static_cast<double>(rs.report.history.size() - 1);
+  CHECK(std::fabs(cs.n3_multiplies() - (1.0 + 2.0 * (2.0 / 12.0) + 3.0 * nests)) < 1e-12);
+  CHECK(cs.n2_ops() == static_cast<std::int64_t>(1 + 3 * nests + 1));
+
+  // the pre-formed normal equations take the same path minus the W/rhs products
+  const DenseMatrix ah = conjugate_transpose(a);
+  const auto rh = solve_normal_equations({matmul(ah, a), matmul(ah, bb), true}, cfg);
+  CHECK(rel(rh.x, rs.x) < 1e-12);
+
+  // the nest budget runs out: NonConvergenceError carries the report
+  cfg.depth_L = 1;
+  cfg.tol = 1e-12;
+  cfg.max_nests = 2;
+  DenseMatrix e0(12, 1);
+  e0(0, 0) = Scalar{1, 0};
+  bool threw = false;
+  try {
+    solve_normal_equations({gauss(12, 12, 97, true), e0, false}, cfg);
+  } catch (const NonConvergenceError& e) {
+    threw = e.report.stopped_reason == StopReason::MaxNests && e.report.history.size() == 3;
+  }
+  CHECK(threw);
+  CHECK_THROWS(solve_normal_equations({gauss(3, 4, 1), ones, false}, cfg), ShapeError);
+  CHECK_THROWS(solve_normal_equations({d, DenseMatrix(4, 1), false}, cfg), ShapeError);
+}
+
+// --normal IN OUT: solve_normal_equations on a system from a binary file
+//   IN:  int64 n, k, depth_L, max_nests; double tol; complex A (n×n); complex B (n×k)
+//   OUT: int64 status (0 ok, 20 NonConvergenceError), history length h; double history[h],
+//        n3, n2, backward; complex x (n×k)
+static int normal_cli(const char* in_path, const char* out_path) {
+  std::FILE* f = std::fopen(in_path, "rb");
+  if (!f) return 2;
+  std::int64_t hdr[4];
+  double tol = 0.0;
+  bool ok = std::fread(hdr, sizeof(hdr), 1, f) == 1 && std::fread(&tol, sizeof(tol), 1, f) == 1;
+  const std::size_t n = static_cast<std::size_t>(hdr[0]), k = static_cast<std::size_t>(hdr[1]);
+  DenseMatrix a(n, n), b(n, k);
+  ok = ok && std::fread(a.data().data(), sizeof(Scalar), n * n, f) == n * n &&
+       std::fread(b.data().data(), sizeof(Scalar), n * k, f) == n * k;
+  std::fclose(f);
+  if (!ok) return 2;
+  SolverConfig cfg;
+  cfg.depth_L = static_cast<std::size_t>(hdr[2]);
+  cfg.max_nests = static_cast<std::size_t>(hdr[3]);
+  cfg.tol = tol;
+  OpCounter cnt;
+  std::int64_t status = 0;
+  NormalSolveResult res;
+  try {
+    res = solve_normal_equations({a, b, false}, cfg, &cnt);
+  } catch (const NonConvergenceError& e) {
+    status = 20;
+    res.report = e.report;
+    res.x = DenseMatrix(n, k);
+  }
+  std::FILE* o = std::fopen(out_path, "wb");
+  if (!o) return 2;
+  const std::int64_t h = static_cast<std::int64_t>(res.report.history.size());
+  std::fwrite(&status, sizeof(status), 1, o);
+  std::fwrite(&h, sizeof(h), 1, o);
+  for (const auto& e : res.report.history) std::fwrite(&e.second, sizeof(double), 1, o);
+  const double tail[3] = {cnt.n3_multiplies(), static_cast<double>(cnt.n2_ops()), res.backward_error};
+  std::fwrite(tail, sizeof(tail), 1, o);
+  std::fwrite(res.x.data().data(), sizeof(Scalar), n * k, o);
+  std::fclose(o);
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc == 4 && std::strcmp(argv[1], "--normal") == 0) return normal_cli(argv[2], argv[3]);
   const bool host_only = argc > 1 && std::strcmp(argv[1], "--host") == 0;
   host_tests();
   if (!host_only) {
     device_tests();
     schedule_tests();
+    normal_equation_tests();
   }
   std::printf("%s: %d checks, %d failures\n", host_only ? "host" : "all", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;

@@ -31,3 +31,35 @@ def test_dropin_device_suite():
     print(out.stdout[-3000:])
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
     assert ", 0 failures" in out.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,k,depth,cond_shift", [(12, 2, 2, 4.0), (40, 3, 1, 6.0), (64, 1, 3, 9.0)])
+def test_dropin_normal_equations_vs_reference(ref, tmp_path, n, k, depth, cond_shift):
+    """nn::solve_normal_equations of the drop-in against the reference's on the same system:
+    same nest count and stop reason, same tallies, x within the north_star tolerance."""
+    rng = np.random.default_rng(n + k)
+    a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)) + cond_shift * np.eye(n)
+    b = rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k))
+    tol, max_nests = 1e-11, 60
+    inp, out = tmp_path / "in.bin", tmp_path / "out.bin"
+    with open(inp, "wb") as f:
+        np.array([n, k, depth, max_nests], np.int64).tofile(f)
+        np.array([tol]).tofile(f)
+        a.astype(np.complex128).tofile(f)
+        b.astype(np.complex128).tofile(f)
+    r = subprocess.run([_bin(), "--normal", str(inp), str(out)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    raw = out.read_bytes()
+    status, h = np.frombuffer(raw[:16], np.int64)
+    hist = np.frombuffer(raw[16:16 + 8 * h], np.float64)
+    n3, n2, backward = np.frombuffer(raw[16 + 8 * h:40 + 8 * h], np.float64)
+    x = np.frombuffer(raw[40 + 8 * h:], np.complex128).reshape(n, k)
+    xr, rep, bwr = ref.solve_normal(a, b, depth, max_nests, tol)
+    assert status == 0 and rep["stopped"] == "tolerance"
+    assert h == len(rep["history"])  # identical nest count
+    assert n3 == rep["n3"] and int(n2) == rep["n2"]
+    assert np.linalg.norm(x - xr) / np.linalg.norm(xr) < 1e-10
+    big = rep["history"] > 1e-12
+    assert np.allclose(hist[big], rep["history"][big], rtol=1e-6, atol=1e-13)
+    assert backward < 1e-10 and bwr < 1e-10

@@ -96,6 +96,20 @@ def test_elementwise_bitexact_vs_reference(ref):
     assert abs(nnb.frobenius_norm(a) - ref.frobenius(a)) < 1e-14 * ref.frobenius(a)
 
 
+@pytest.mark.parametrize("shape", [(1, 1), (5, 3), (37, 65), (256, 256), (1000, 33)])
+def test_conjugate_transpose_exact(shape):
+    """nn::conjugate_transpose (kernels.cpp:223-229) is pure data movement: exact."""
+    import torch
+
+    rng = np.random.default_rng(shape[0])
+    a = rng.standard_normal(shape)
+    z = a + 1j * rng.standard_normal(shape)
+    assert np.array_equal(nnb.conjugate_transpose(a), a.T)
+    assert np.array_equal(nnb.conjugate_transpose(z), z.conj().T)
+    zd = torch.from_numpy(z).cuda()
+    assert torch.equal(nnb.conjugate_transpose(zd), zd.conj().T.contiguous())
+
+
 # ----------------------------------------------------------------- residual / step / ns_sum
 def test_residual_and_steps_vs_golden():
     g = golden("steps_spd8.npz")
