@@ -27,13 +27,19 @@ clean:
 
 # C++ drop-in surface (namespace nn) over libnnb, and its test executable
 DROPIN_INC := -I$(PKG)/dropin/include -Iinclude
-$(PKG)/libnn_b200.so: $(PKG)/dropin/src/dropin.cpp $(wildcard $(PKG)/dropin/include/nn/*.hpp) include/nnb.h $(PKG)/libnnb.so
-	g++ -O2 -std=c++20 -fPIC -shared $(DROPIN_INC) $(PKG)/dropin/src/dropin.cpp -o $@ \
+DROPIN_SRC := $(wildcard $(PKG)/dropin/src/*.cpp)
+$(PKG)/libnn_b200.so: $(DROPIN_SRC) $(wildcard $(PKG)/dropin/include/nn/*.hpp) include/nnb.h $(PKG)/libnnb.so
+	g++ -O2 -std=c++20 -fPIC -shared $(DROPIN_INC) $(DROPIN_SRC) -o $@ \
 	    -L$(PKG) -lnnb -Wl,-rpath,'$$ORIGIN'
+
+# nnbench-compatible CLI over the drop-in
+build/nnbench: $(PKG)/dropin/tools/nnbench.cpp $(PKG)/libnn_b200.so
+	@mkdir -p build
+	g++ -O2 -std=c++20 $(DROPIN_INC) $< -o $@ -L$(PKG) -lnn_b200 -lnnb -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 build/test_dropin: tests/cpp/test_dropin.cpp $(PKG)/libnn_b200.so
 	@mkdir -p build
 	g++ -O2 -std=c++20 $(DROPIN_INC) $< -o $@ -L$(PKG) -lnn_b200 -lnnb -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
-dropin: $(PKG)/libnn_b200.so build/test_dropin
+dropin: $(PKG)/libnn_b200.so build/test_dropin build/nnbench
 .PHONY: dropin

@@ -123,6 +123,25 @@ int nnb_axpby_z(const double* alpha2, const double* A, const double* beta2, cons
 int nnb_transpose_d(const double* M, int64_t rows, int64_t cols, double* out, void* stream);
 int nnb_conj_transpose_z(const double* M, int64_t rows, int64_t cols, double* out, void* stream);
 
+/* Seeded test-matrix generators.
+ * nnb_gaussian_stream: `count` draws of the reference's GaussianStream
+ *   (proj/include/nn/rng.hpp:15-52; host code, the stream is sequential).
+ * nnb_householder_q_d/_z: Q of the Householder QR of the n×n matrix A
+ *   (proj/src/kernels.cpp:64-105), on the device.
+ * nnb_random_spd_d: W = (Q·diag(lam))·Q^T symmetrised, Q = householder_q(G);
+ *   with G drawn row-major from GaussianStream(seed) and lam the reference's
+ *   log_uniform_spectrum this is nn::random_spd (kernels.cpp:352-381),
+ *   bit-identical.
+ * nnb_random_conditioned_z: A = (U·diag(sigma))·V^H, U, V = householder_q of
+ *   the complex Gaussians GU, GV — nn::random_conditioned_complex
+ *   (kernels.cpp:383-407), equal to a few ulps. */
+int nnb_gaussian_stream(uint64_t seed, int64_t count, double* out);
+int nnb_householder_q_d(const double* A, int64_t n, double* Q, void* stream);
+int nnb_householder_q_z(const double* A, int64_t n, double* Q, void* stream);
+int nnb_random_spd_d(const double* G, const double* lam, int64_t n, double* W, void* stream);
+int nnb_random_conditioned_z(const double* GU, const double* GV, const double* sigma, int64_t n, double* A,
+                             void* stream);
+
 /* ||M||_F (proj/include/nn/kernels.hpp:42) and trace (:40). */
 int nnb_frobenius_d(const double* M, int64_t count, double* out, void* stream);
 int nnb_frobenius_z(const double* M, int64_t count, double* out, void* stream);

@@ -103,6 +103,20 @@ class Reference(_Lib):
         self._check(self.fn("random_spd", [C.c_int64, C.c_double, C.c_uint64, _dp])(n, cond, seed, _ptr(out)))
         return out
 
+    def random_conditioned_complex(self, n: int, cond: float, seed: int) -> np.ndarray:
+        out = np.empty((n, n), np.complex128)
+        f = self.fn("random_conditioned_complex", [C.c_int64, C.c_double, C.c_uint64, _dp])
+        self._check(f(n, cond, seed, _ptr(out)))
+        return out
+
+    def random_sparse_spd(self, n: int, density: float, seed: int):
+        f = self.fn("random_sparse_spd", [C.c_int64, C.c_double, C.c_uint64, _i64p, _dp, _dp, _dp])
+        nnz = C.c_int64()
+        self._check(f(n, density, seed, C.byref(nnz), None, None, None))
+        rp, col, val = np.empty(n + 1, np.int64), np.empty(nnz.value, np.int64), np.empty(nnz.value)
+        self._check(f(n, density, seed, C.byref(nnz), _ptr(rp), _ptr(col), _ptr(val)))
+        return rp, col, val
+
     def matmul(self, a, b):
         a, b = _z(a), _z(b)
         out = np.empty((a.shape[0], b.shape[1]), np.complex128)

@@ -118,6 +118,27 @@ int nnref_random_spd(int64_t n, double cond, uint64_t seed, double* out) {
   return guarded([&] { store(nn::random_spd(static_cast<std::size_t>(n), cond, seed), out); });
 }
 
+// nn::random_conditioned_complex (proj/src/kernels.cpp:383-407).
+int nnref_random_conditioned_complex(int64_t n, double cond, uint64_t seed, double* out) {
+  return guarded([&] { store(nn::random_conditioned_complex(static_cast<std::size_t>(n), cond, seed), out); });
+}
+
+// nn::random_sparse_spd (proj/src/kernels.cpp:409-432) as CSR arrays; nnz_out
+// first (call with row_ptr == nullptr to size the buffers).
+int nnref_random_sparse_spd(int64_t n, double density, uint64_t seed, int64_t* nnz_out, int64_t* row_ptr,
+                            int64_t* col, double* val) {
+  return guarded([&] {
+    const nn::SparseMatrixCsr m = nn::random_sparse_spd(static_cast<std::size_t>(n), density, seed);
+    *nnz_out = static_cast<int64_t>(m.nnz());
+    if (!row_ptr) return;
+    for (std::size_t i = 0; i <= m.rows(); ++i) row_ptr[i] = static_cast<int64_t>(m.row_ptr()[i]);
+    for (std::size_t k = 0; k < m.nnz(); ++k) {
+      col[k] = static_cast<int64_t>(m.col_idx()[k]);
+      val[k] = m.values()[k].real();
+    }
+  });
+}
+
 // nn::matmul (proj/src/kernels.cpp:137-162).
 int nnref_matmul_z(const double* a, const double* b, int64_t m, int64_t k, int64_t n,
                    double* c, double* n3) {

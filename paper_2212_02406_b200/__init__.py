@@ -117,6 +117,11 @@ _SIGS = {
     "nnb_spmv_block_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _dp, _dp], C.c_int),
     "nnb_sparse_factorized_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _i64, C.c_double, _dp, _dp, _dp,
                                  _dp], C.c_int),
+    "nnb_gaussian_stream": ([C.c_uint64, _i64, _dp], C.c_int),
+    "nnb_householder_q_d": ([_dp, _i64, _dp, _dp], C.c_int),
+    "nnb_householder_q_z": ([_dp, _i64, _dp, _dp], C.c_int),
+    "nnb_random_spd_d": ([_dp, _dp, _i64, _dp, _dp], C.c_int),
+    "nnb_random_conditioned_z": ([_dp, _dp, _dp, _i64, _dp, _dp], C.c_int),
     "nnb_transpose_d": ([_dp, _i64, _i64, _dp, _dp], C.c_int),
     "nnb_conj_transpose_z": ([_dp, _i64, _i64, _dp, _dp], C.c_int),
     "nnb_spectral_norm_z": ([_dp, _i64, _dp, C.c_double, _i32, _dp, _dp, _dp, _dp], C.c_int),
@@ -533,6 +538,64 @@ def x0(a, kind: int = X0_TRANSPOSE_NORM, scale_: float = 1.0):
     a = _prep(a, False)
     out = _empty_like(a)
     _check(lib().nnb_x0_d(_ptr(a), a.shape[0], kind, scale_, _ptr(out), _stream(a)))
+    return out
+
+
+# ------------------------------------------------------------ generators (§8(a) A14)
+def gaussian_stream(seed: int, count: int) -> np.ndarray:
+    """`count` draws of nn::GaussianStream(seed) (proj/include/nn/rng.hpp:15-52)."""
+    out = np.empty(count)
+    _check(lib().nnb_gaussian_stream(seed, count, out.ctypes.data if count else None))
+    return out
+
+
+def log_uniform_spectrum(n: int, cond: float) -> np.ndarray:
+    """cond^-(n-1-j)/(n-1), j = 0..n-1, through C pow like the reference (kernels.cpp:116-124)."""
+    if n == 1:
+        return np.ones(1)
+    return np.array([cond ** (-((n - 1 - j) / (n - 1))) for j in range(n)])
+
+
+def householder_q(a):
+    """Unitary factor of the Householder QR (kernels.cpp:64-105), on the device."""
+    z = _is_complex(a)
+    a = _prep(a, z)
+    if a.shape[0] != a.shape[1]:
+        raise ShapeError("householder_q: matrix must be square")
+    out = _empty_like(a)
+    f = lib().nnb_householder_q_z if z else lib().nnb_householder_q_d
+    _check(f(_ptr(a), a.shape[0], _ptr(out), _stream(a)))
+    return out
+
+
+def random_spd(n: int, cond: float, seed: int) -> np.ndarray:
+    """nn::random_spd (kernels.cpp:352-381), bit-identical: Q·diag(λ)·Qᵀ with Q from the
+    Householder QR of a GaussianStream(seed) matrix, QR and products on the device."""
+    if n < 1:
+        raise DomainError("random_spd: n must be >= 1")
+    if cond < 1.0:
+        raise DomainError("random_spd: cond must be >= 1")
+    g = gaussian_stream(seed, n * n).reshape(n, n)
+    lam = log_uniform_spectrum(n, cond)
+    out = np.empty((n, n))
+    _check(lib().nnb_random_spd_d(g.ctypes.data, lam.ctypes.data, n, out.ctypes.data, None))
+    return out
+
+
+def random_conditioned_complex(n: int, cond: float, seed: int) -> np.ndarray:
+    """nn::random_conditioned_complex (kernels.cpp:383-407): U·diag(σ)·Vᴴ, U and V the
+    Householder Q of two complex GaussianStream(seed) draws (equal to a few ulps)."""
+    if n < 1:
+        raise DomainError("random_conditioned_complex: n must be >= 1")
+    if cond < 1.0:
+        raise DomainError("random_conditioned_complex: cond must be >= 1")
+    g = gaussian_stream(seed, 4 * n * n)
+    gu = np.ascontiguousarray(g[: 2 * n * n])
+    gv = np.ascontiguousarray(g[2 * n * n:])
+    sig = log_uniform_spectrum(n, cond)
+    out = np.empty((n, n), np.complex128)
+    _check(lib().nnb_random_conditioned_z(gu.ctypes.data, gv.ctypes.data, sig.ctypes.data, n, out.ctypes.data,
+                                          None))
     return out
 
 

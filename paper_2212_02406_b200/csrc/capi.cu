@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <random>
 #include <vector>
 
 #include "../../include/nnb.h"
@@ -361,6 +362,80 @@ int nnb_axpby_z(const double* alpha2, const double* A, const double* beta2, cons
   NNB_TRY(axpby_z(alpha2[0], alpha2[1], a.d, beta2 ? beta2[0] : 0.0, beta2 ? beta2[1] : 0.0,
                   B ? b.d : nullptr, g0, g1, o.d, rows, cols, s));
   NNB_TRY(o.finish(s));
+  return sync(s);
+}
+
+int nnb_gaussian_stream(uint64_t seed, int64_t count, double* out) {
+  // mt19937_64, 53-bit uniforms in (0, 1] for the radius, Box–Muller pairs
+  // with the cosine returned first and the sine kept as the spare
+  if (count < 0 || (count && !out)) return fail(NNB_ERR_DOMAIN, "gaussian_stream: bad output");
+  std::mt19937_64 eng(seed);
+  auto unit = [&eng] { return static_cast<double>(eng() >> 11) * 0x1.0p-53; };
+  for (int64_t i = 0; i < count; i += 2) {
+    double u1 = unit();
+    while (u1 <= 0.0) u1 = unit();
+    const double u2 = unit();
+    const double rad = std::sqrt(-2.0 * std::log(u1));
+    const double ang = 2.0 * 3.14159265358979323846 * u2;
+    out[i] = rad * std::cos(ang);
+    if (i + 1 < count) out[i + 1] = rad * std::sin(ang);
+  }
+  return 0;
+}
+
+int nnb_householder_q_d(const double* A, int64_t n, double* Q, void* stream) {
+  NNB_TRY(require_device());
+  if (n < 1) return fail(NNB_ERR_DOMAIN, "householder_q: n must be >= 1");
+  cudaStream_t s = resolve(stream);
+  In a;
+  NNB_TRY(a.stage(A, (size_t)(n * n), s));
+  Out q;
+  NNB_TRY(q.prepare(Q, (size_t)(n * n), s));
+  NNB_TRY(householder_q(a.d, n, 0, q.d, s));
+  NNB_TRY(q.finish(s));
+  return sync(s);
+}
+
+int nnb_householder_q_z(const double* A, int64_t n, double* Q, void* stream) {
+  NNB_TRY(require_device());
+  if (n < 1) return fail(NNB_ERR_DOMAIN, "householder_q: n must be >= 1");
+  cudaStream_t s = resolve(stream);
+  In a;
+  NNB_TRY(a.stage(A, (size_t)(2 * n * n), s));
+  Out q;
+  NNB_TRY(q.prepare(Q, (size_t)(2 * n * n), s));
+  NNB_TRY(householder_q(a.d, n, 1, q.d, s));
+  NNB_TRY(q.finish(s));
+  return sync(s);
+}
+
+int nnb_random_spd_d(const double* G, const double* lam, int64_t n, double* W, void* stream) {
+  NNB_TRY(require_device());
+  if (n < 1) return fail(NNB_ERR_DOMAIN, "random_spd: n must be >= 1");
+  cudaStream_t s = resolve(stream);
+  In g, l;
+  NNB_TRY(g.stage(G, (size_t)(n * n), s));
+  NNB_TRY(l.stage(lam, (size_t)n, s));
+  Out w;
+  NNB_TRY(w.prepare(W, (size_t)(n * n), s));
+  NNB_TRY(random_spd_dev(g.d, l.d, n, w.d, s));
+  NNB_TRY(w.finish(s));
+  return sync(s);
+}
+
+int nnb_random_conditioned_z(const double* GU, const double* GV, const double* sigma, int64_t n, double* A,
+                             void* stream) {
+  NNB_TRY(require_device());
+  if (n < 1) return fail(NNB_ERR_DOMAIN, "random_conditioned_complex: n must be >= 1");
+  cudaStream_t s = resolve(stream);
+  In gu, gv, sg;
+  NNB_TRY(gu.stage(GU, (size_t)(2 * n * n), s));
+  NNB_TRY(gv.stage(GV, (size_t)(2 * n * n), s));
+  NNB_TRY(sg.stage(sigma, (size_t)n, s));
+  Out a;
+  NNB_TRY(a.prepare(A, (size_t)(2 * n * n), s));
+  NNB_TRY(random_conditioned_dev(gu.d, gv.d, sg.d, n, a.d, s));
+  NNB_TRY(a.finish(s));
   return sync(s);
 }
 

@@ -111,6 +111,11 @@ int trace_dev(const double* M, int64_t n, int64_t ld, int complex_stride, double
 int deinterleave(const double* z, int64_t count, double* re, double* im, cudaStream_t s);
 int interleave(const double* re, const double* im, int64_t count, double* z, cudaStream_t s);
 int fill_identity(double* X, int64_t n, int64_t ld, double val, cudaStream_t s);
+// generators.cu: Householder Q (device in/out, cplx: interleaved), random_spd / random_conditioned_complex
+int householder_q(const double* A, int64_t n, int cplx, double* Q, cudaStream_t s);
+int random_spd_dev(const double* G, const double* lam, int64_t n, double* W, cudaStream_t s);
+int random_conditioned_dev(const double* GU, const double* GV, const double* sigma, int64_t n, double* A,
+                           cudaStream_t s);
 // out (cols×rows) = Mᵀ (cplx = 0) or Mᴴ of interleaved complex M (cplx = 1)
 int transpose(const double* M, int64_t rows, int64_t cols, int cplx, double* out, cudaStream_t s);
 

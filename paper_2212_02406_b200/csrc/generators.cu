@@ -1,0 +1,265 @@
+// Seeded test-matrix generators on the device.
+//
+// Reference: proj/src/kernels.cpp:64-105 (householder_q), :116-124
+// (log_uniform_spectrum), :352-381 (random_spd), :383-407
+// (random_conditioned_complex).  The reference runs these as naive
+// single-threaded O(n^3) loops — minutes at the C3 size (N = 4096).  Here:
+//   * the Gaussian matrix comes from the host-side GaussianStream (a
+//     sequential mt19937_64 stream; the caller draws it) and λ from the
+//     host's std::pow, so both are the reference's bits;
+//   * Householder QR and the backward accumulation of Q run one reflector at
+//     a time: a single-thread kernel forms v and β with the reference's
+//     sequential sums, then one thread per column computes its dot product
+//     (ascending i) and applies the rank-1 update to its own column
+//     (coalesced across the warp);
+//   * W = (Q·diag λ)·Qᵀ goes through the reference-exact GEMM (ascending k,
+//     one rounded multiply and add per term) and the averaging
+//     symmetrisation.
+// Real data: every operation is explicitly rounded (no contraction) in the
+// reference's order, so random_spd is BIT-IDENTICAL to the reference's.
+// Complex data (random_conditioned_complex): the reference's std::norm and
+// std::abs go through hypot; here |z|² = re² + im², so results agree to a
+// few ulps rather than bit for bit.
+#include "engine.cuh"
+
+namespace nnb {
+namespace {
+
+// ---- real --------------------------------------------------------------------
+// Reflector k of A (n×n, row-major, in place): v (row k of V, zero left of k) and β
+// (0 marks a skipped reflector: zero column or zero v, as the reference's `continue`).
+__global__ void reflector_d_kernel(const double* __restrict__ a, int64_t n, int64_t k, double* __restrict__ v,
+                                   double* __restrict__ beta) {
+  if (threadIdx.x | blockIdx.x) return;
+  double xnorm2 = 0.0;
+  for (int64_t i = k; i < n; ++i) {
+    const double x = a[i * n + k];
+    xnorm2 = __dadd_rn(xnorm2, __dmul_rn(x, x));
+  }
+  for (int64_t i = 0; i < n; ++i) v[i] = 0.0;
+  *beta = 0.0;
+  const double xnorm = __dsqrt_rn(xnorm2);
+  if (xnorm == 0.0) return;
+  const double x0 = a[k * n + k];
+  const double x0abs = fabs(x0);
+  const double phase = x0abs > 0.0 ? __ddiv_rn(x0, x0abs) : 1.0;
+  const double alpha = __dmul_rn(-phase, xnorm);
+  for (int64_t i = k; i < n; ++i) v[i] = a[i * n + k];
+  v[k] = __dsub_rn(v[k], alpha);
+  double vnorm2 = 0.0;
+  for (int64_t i = k; i < n; ++i) vnorm2 = __dadd_rn(vnorm2, __dmul_rn(v[i], v[i]));
+  if (vnorm2 == 0.0) return;
+  *beta = __ddiv_rn(2.0, vnorm2);
+}
+
+// M ← (I − β v vᵀ) M on rows [k, n) of columns [j0, n): one thread per column.
+__global__ void reflect_columns_d_kernel(double* __restrict__ m, int64_t n, int64_t k, int64_t j0,
+                                         const double* __restrict__ v, const double* __restrict__ beta) {
+  const double b = *beta;
+  const int64_t j = j0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b == 0.0 || j >= n) return;
+  double dot = 0.0;
+  for (int64_t i = k; i < n; ++i) dot = __dadd_rn(dot, __dmul_rn(v[i], m[i * n + j]));
+  dot = __dmul_rn(dot, b);
+  for (int64_t i = k; i < n; ++i) m[i * n + j] = __dsub_rn(m[i * n + j], __dmul_rn(v[i], dot));
+}
+
+__global__ void identity_d_kernel(double* q, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x)
+    q[e] = (e / n == e % n) ? 1.0 : 0.0;
+}
+
+__global__ void scale_columns_d_kernel(const double* __restrict__ q, const double* __restrict__ lam, int64_t n,
+                                       double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = __dmul_rn(q[e], lam[e % n]);
+}
+
+// w(i,j) = w(j,i) = (w(i,j) + w(j,i))·0.5 for i < j; counts non-finite entries.
+__global__ void symmetrize_d_kernel(double* w, int64_t n, int* nonfinite) {
+  int bad = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e % n;
+    if (i < j) {
+      const double avg = __dmul_rn(__dadd_rn(w[i * n + j], w[j * n + i]), 0.5);
+      w[i * n + j] = avg;
+      w[j * n + i] = avg;
+      bad += !isfinite(avg);
+    } else if (i == j) {
+      bad += !isfinite(w[e]);
+    }
+  }
+  if (bad) atomicAdd(nonfinite, bad);
+}
+
+// ---- complex (interleaved double2) ----------------------------------------------
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {  // (ac − bd) + i(ad + bc), each op rounded
+  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
+                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double cnorm(double2 a) { return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y)); }
+
+__global__ void reflector_z_kernel(const double2* __restrict__ a, int64_t n, int64_t k, double2* __restrict__ v,
+                                   double* __restrict__ beta) {
+  if (threadIdx.x | blockIdx.x) return;
+  double xnorm2 = 0.0;
+  for (int64_t i = k; i < n; ++i) xnorm2 = __dadd_rn(xnorm2, cnorm(a[i * n + k]));
+  for (int64_t i = 0; i < n; ++i) v[i] = make_double2(0.0, 0.0);
+  *beta = 0.0;
+  const double xnorm = __dsqrt_rn(xnorm2);
+  if (xnorm == 0.0) return;
+  const double2 x0 = a[k * n + k];
+  const double x0abs = hypot(x0.x, x0.y);
+  const double2 phase = x0abs > 0.0 ? make_double2(__ddiv_rn(x0.x, x0abs), __ddiv_rn(x0.y, x0abs))
+                                    : make_double2(1.0, 0.0);
+  const double2 alpha = make_double2(__dmul_rn(-phase.x, xnorm), __dmul_rn(-phase.y, xnorm));
+  for (int64_t i = k; i < n; ++i) v[i] = a[i * n + k];
+  v[k] = make_double2(__dsub_rn(v[k].x, alpha.x), __dsub_rn(v[k].y, alpha.y));
+  double vnorm2 = 0.0;
+  for (int64_t i = k; i < n; ++i) vnorm2 = __dadd_rn(vnorm2, cnorm(v[i]));
+  if (vnorm2 == 0.0) return;
+  *beta = __ddiv_rn(2.0, vnorm2);
+}
+
+__global__ void reflect_columns_z_kernel(double2* __restrict__ m, int64_t n, int64_t k, int64_t j0,
+                                         const double2* __restrict__ v, const double* __restrict__ beta) {
+  const double b = *beta;
+  const int64_t j = j0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b == 0.0 || j >= n) return;
+  double2 dot = make_double2(0.0, 0.0);
+  for (int64_t i = k; i < n; ++i) {
+    const double2 t = cmul(cconj(v[i]), m[i * n + j]);
+    dot = make_double2(__dadd_rn(dot.x, t.x), __dadd_rn(dot.y, t.y));
+  }
+  dot = make_double2(__dmul_rn(dot.x, b), __dmul_rn(dot.y, b));
+  for (int64_t i = k; i < n; ++i) {
+    const double2 t = cmul(v[i], dot);
+    m[i * n + j] = make_double2(__dsub_rn(m[i * n + j].x, t.x), __dsub_rn(m[i * n + j].y, t.y));
+  }
+}
+
+__global__ void identity_z_kernel(double2* q, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x)
+    q[e] = make_double2((e / n == e % n) ? 1.0 : 0.0, 0.0);
+}
+
+// a(i,j) = Σ_k u(i,k)·σ_k·conj(v(j,k)), ascending k (random_conditioned_complex's product).
+__global__ void usvh_z_kernel(const double2* __restrict__ u, const double2* __restrict__ v,
+                              const double* __restrict__ sigma, int64_t n, double2* __restrict__ a, int* nonfinite) {
+  int bad = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e % n;
+    double2 sum = make_double2(0.0, 0.0);
+    for (int64_t k = 0; k < n; ++k) {
+      const double2 us = make_double2(__dmul_rn(u[i * n + k].x, sigma[k]), __dmul_rn(u[i * n + k].y, sigma[k]));
+      const double2 t = cmul(us, cconj(v[j * n + k]));
+      sum = make_double2(__dadd_rn(sum.x, t.x), __dadd_rn(sum.y, t.y));
+    }
+    a[e] = sum;
+    bad += !(isfinite(sum.x) && isfinite(sum.y));
+  }
+  if (bad) atomicAdd(nonfinite, bad);
+}
+
+unsigned grid_n2(int64_t n) {
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((n * n + 255) / 256, 148 * 16)));
+}
+
+// Q of A's Householder QR in `q` (A is consumed).  V holds one reflector per row.
+template <typename T, bool CPLX>
+int householder_q_dev(T* a, int64_t n, T* q, T* vmat, double* betas, cudaStream_t s) {
+  constexpr int kCols = 128;
+  for (int64_t k = 0; k + 1 < n; ++k) {
+    T* v = vmat + k * n;
+    if constexpr (CPLX) {
+      reflector_z_kernel<<<1, 32, 0, s>>>(a, n, k, v, betas + k);
+      reflect_columns_z_kernel<<<(unsigned)((n - k + kCols - 1) / kCols), kCols, 0, s>>>(a, n, k, k, v, betas + k);
+    } else {
+      reflector_d_kernel<<<1, 32, 0, s>>>(a, n, k, v, betas + k);
+      reflect_columns_d_kernel<<<(unsigned)((n - k + kCols - 1) / kCols), kCols, 0, s>>>(a, n, k, k, v, betas + k);
+    }
+  }
+  if constexpr (CPLX) identity_z_kernel<<<grid_n2(n), 256, 0, s>>>(q, n);
+  else identity_d_kernel<<<grid_n2(n), 256, 0, s>>>(q, n);
+  // Q = H_0 H_1 … H_{n−2}: apply the reflectors to I from the last to the first
+  for (int64_t r = n - 2; r >= 0; --r) {
+    const unsigned blocks = (unsigned)((n + kCols - 1) / kCols);
+    if constexpr (CPLX) reflect_columns_z_kernel<<<blocks, kCols, 0, s>>>(q, n, r, 0, vmat + r * n, betas + r);
+    else reflect_columns_d_kernel<<<blocks, kCols, 0, s>>>(q, n, r, 0, vmat + r * n, betas + r);
+  }
+  count_launch(n > 1 ? 3 * (n - 1) + 1 : 1);
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace
+
+int householder_q(const double* A, int64_t n, int cplx, double* Q, cudaStream_t s) {
+  const size_t el = cplx ? 2 : 1, mat = (size_t)(n * n) * el;
+  DevBuf work;
+  NNB_TRY(work.alloc(sizeof(double) * (2 * mat + n), s));
+  double* a = work.as<double>();
+  double* vmat = a + mat;
+  double* betas = vmat + mat;
+  NNB_CUDA(cudaMemcpyAsync(a, A, sizeof(double) * mat, cudaMemcpyDeviceToDevice, s));
+  if (cplx)
+    return householder_q_dev<double2, true>(reinterpret_cast<double2*>(a), n, reinterpret_cast<double2*>(Q),
+                                            reinterpret_cast<double2*>(vmat), betas, s);
+  return householder_q_dev<double, false>(a, n, Q, vmat, betas, s);
+}
+
+int random_spd_dev(const double* G, const double* lam, int64_t n, double* W, cudaStream_t s) {
+  const size_t mat = (size_t)(n * n);
+  DevBuf work;
+  NNB_TRY(work.alloc(sizeof(double) * 3 * mat + 64, s));
+  double* q = work.as<double>();
+  double* ql = q + mat;
+  double* qt = ql + mat;
+  int* nonfinite = reinterpret_cast<int*>(qt + mat);
+  NNB_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), s));
+  NNB_TRY(householder_q(G, n, 0, q, s));
+  scale_columns_d_kernel<<<grid_n2(n), 256, 0, s>>>(q, lam, n, ql);  // Q·diag(λ)
+  NNB_TRY(transpose(q, n, n, 0, qt, s));
+  GemmOp op;  // W = (Q·diag λ)·Qᵀ in the reference's ascending-k rounding
+  op.A = ql;
+  op.lda = n;
+  op.B = qt;
+  op.ldb = n;
+  op.M = op.N = op.K = n;
+  op.ep.C = W;
+  op.ep.ldc = n;
+  NNB_TRY(gemm_exact(op, s));
+  symmetrize_d_kernel<<<grid_n2(n), 256, 0, s>>>(W, n, nonfinite);
+  count_launch(2);
+  NNB_CUDA(cudaGetLastError());
+  int bad = 0;
+  NNB_CUDA(cudaMemcpyAsync(&bad, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  if (bad) return fail(2, "random_spd: non-finite entry");
+  return 0;
+}
+
+int random_conditioned_dev(const double* GU, const double* GV, const double* sigma, int64_t n, double* A,
+                           cudaStream_t s) {
+  const size_t mat = (size_t)(2 * n * n);
+  DevBuf work;
+  NNB_TRY(work.alloc(sizeof(double) * 2 * mat + 64, s));
+  double* u = work.as<double>();
+  double* v = u + mat;
+  int* nonfinite = reinterpret_cast<int*>(v + mat);
+  NNB_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), s));
+  NNB_TRY(householder_q(GU, n, 1, u, s));
+  NNB_TRY(householder_q(GV, n, 1, v, s));
+  usvh_z_kernel<<<grid_n2(n), 256, 0, s>>>(reinterpret_cast<const double2*>(u), reinterpret_cast<const double2*>(v),
+                                           sigma, n, reinterpret_cast<double2*>(A), nonfinite);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  int bad = 0;
+  NNB_CUDA(cudaMemcpyAsync(&bad, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  if (bad) return fail(2, "random_conditioned_complex: non-finite entry");
+  return 0;
+}
+
+}  // namespace nnb

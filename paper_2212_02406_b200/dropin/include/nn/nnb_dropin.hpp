@@ -9,8 +9,8 @@
 // bookkeeping (reports, nest estimates, order fits).
 //
 // Out of scope (not declared; link the reference's nncore for them):
-// direct_inverse_oracle, random_* generators, matvec, theta_power,
-// contraction_check, cns_invert and the cost model.
+// direct_inverse_oracle, matvec, theta_power, contraction_check, cns_invert
+// and the cost model.
 #pragma once
 
 #include <atomic>
@@ -232,6 +232,13 @@ SpectralEstimate spectral_norm_estimate(const DenseMatrix& m, double tol = 1e-12
 SpectralEstimate spectral_norm_estimate_shifted(const SparseMatrixCsr& w, Scalar theta,
                                                 double tol = 1e-12, int max_iters = 2000,
                                                 std::uint64_t seed = 0x5eed5eedULL);
+/// Seeded test matrices of proj/include/nn/kernels.hpp:69-82.  random_spd and
+/// random_conditioned_complex run the Householder QR and the products on the
+/// GPU (random_spd bit-identical to the reference); random_sparse_spd is the
+/// reference's sequential pattern/value stream on the host.
+DenseMatrix random_spd(std::size_t n, double cond, std::uint64_t seed);
+DenseMatrix random_conditioned_complex(std::size_t n, double cond, std::uint64_t seed);
+SparseMatrixCsr random_sparse_spd(std::size_t n, double density, std::uint64_t seed);
 DenseMatrix spmv_block(const SparseMatrixCsr& p, const DenseMatrix& x,
                        OpCounter* counter = nullptr);
 /// p^exponent by square-and-multiply; floor(log2 e) + popcount(e) − 1 products.

@@ -726,6 +726,62 @@ DenseMatrix ns_factorized(const DenseMatrix& phi, const DenseMatrix& w_tilde, co
   return out;
 }
 
+// ==================================================================== generators
+namespace {
+std::vector<double> log_uniform_spectrum(std::size_t n, double cond) {
+  std::vector<double> lam(n, 1.0);  // kernels.cpp:116-124: cond^-t, t from 1 down to 0
+  if (n > 1)
+    for (std::size_t j = 0; j < n; ++j)
+      lam[j] = std::pow(cond, -(static_cast<double>(n - 1 - j) / static_cast<double>(n - 1)));
+  return lam;
+}
+}  // namespace
+
+DenseMatrix random_spd(std::size_t n, double cond, std::uint64_t seed) {
+  if (n < 1) throw DomainError("random_spd: n must be >= 1");
+  if (cond < 1.0) throw DomainError("random_spd: cond must be >= 1");
+  GaussianStream g(seed);
+  const std::vector<double> gauss = g.take(n * n);  // row-major, as the reference fills it
+  const std::vector<double> lam = log_uniform_spectrum(n, cond);
+  std::vector<double> w(n * n);
+  check(nnb_random_spd_d(gauss.data(), lam.data(), (int64_t)n, w.data(), nullptr), "random_spd");
+  return from_real(n, n, w);
+}
+
+DenseMatrix random_conditioned_complex(std::size_t n, double cond, std::uint64_t seed) {
+  if (n < 1) throw DomainError("random_conditioned_complex: n must be >= 1");
+  if (cond < 1.0) throw DomainError("random_conditioned_complex: cond must be >= 1");
+  GaussianStream g(seed);
+  const std::vector<double> gu = g.take(2 * n * n), gv = g.take(2 * n * n);  // (re, im) pairs, U's draw first
+  const std::vector<double> sigma = log_uniform_spectrum(n, cond);
+  DenseMatrix out(n, n);
+  check(nnb_random_conditioned_z(gu.data(), gv.data(), sigma.data(), (int64_t)n, zp(out), nullptr),
+        "random_conditioned_complex");
+  return out;
+}
+
+SparseMatrixCsr random_sparse_spd(std::size_t n, double density, std::uint64_t seed) {
+  if (n < 1) throw DomainError("random_sparse_spd: n must be >= 1");
+  if (density < 0.0 || density > 1.0) throw DomainError("random_sparse_spd: density must be in [0,1]");
+  // kernels.cpp:409-432: an upper-triangle pattern stream and a value stream,
+  // mirrored, with a diagonal 1 + Σ|off-diagonal| for strict dominance
+  std::mt19937_64 pattern(seed);
+  GaussianStream values(seed ^ 0x9e3779b97f4a7c15ULL);
+  std::vector<SparseMatrixCsr::Triplet> t;
+  std::vector<double> offsum(n, 0.0);
+  for (std::size_t i = 0; i < n; ++i)
+    for (std::size_t j = i + 1; j < n; ++j) {
+      if (static_cast<double>(pattern() >> 11) * 0x1.0p-53 >= density) continue;
+      const double x = values.next();
+      t.push_back({i, j, Scalar{x, 0.0}});
+      t.push_back({j, i, Scalar{x, 0.0}});
+      offsum[i] += std::fabs(x);
+      offsum[j] += std::fabs(x);
+    }
+  for (std::size_t i = 0; i < n; ++i) t.push_back({i, i, Scalar{1.0 + offsum[i], 0.0}});
+  return SparseMatrixCsr::build(n, n, std::move(t));
+}
+
 // proj/src/factorized.cpp:63-99: W = A^H A and rhs = A^H B (unless the caller
 // already formed them), theta from theta_trace(W), W^-1 from nn_invert, then
 // x = W^-1 rhs.  The backward error on the normal equations is diagnostic and

@@ -10,7 +10,11 @@
 #include <string>
 #include <vector>
 
+#include <filesystem>
+#include <sstream>
+
 #include "nn/factorized.hpp"
+#include "nn/matrix_market.hpp"
 #include "nn/kernels.hpp"
 #include "nn/normalization.hpp"
 #include "nn/rng.hpp"
@@ -74,6 +78,73 @@ static DenseMatrix normalized(std::size_t n, double shift, std::uint64_t seed) {
 
 static DenseMatrix s1(double v) { return DenseMatrix::diagonal({Scalar{v, 0}}); }
 
+// Matrix Market I/O (proj/tests/test_matrix_market.cpp restated; host only)
+static void mm_tests() {
+  GaussianStream g(7);
+  DenseMatrix m(5, 3);
+  for (auto& v : m.data()) v = Scalar{g.next() * 1e-7, g.next() * 1e9};
+  std::stringstream ss;
+  mm::write_dense(ss, m);
+  CHECK(mm::read_dense(ss) == m);  // 17 significant digits: bit-exact round trip
+
+  DenseMatrix r(2, 2);
+  r(0, 0) = Scalar{1.5, 0};
+  std::stringstream sr;
+  mm::write_dense(sr, r);
+  CHECK(sr.str().find("array real general") != std::string::npos);
+  CHECK(mm::read_dense(sr) == r);
+
+  std::istringstream colmajor("%%MatrixMarket matrix array real general\n% a comment line\n2 3\n1\n2\n3\n4\n5\n6\n");
+  const DenseMatrix cm = mm::read_dense(colmajor);
+  CHECK(cm(0, 0) == (Scalar{1, 0}) && cm(1, 0) == (Scalar{2, 0}) && cm(0, 1) == (Scalar{3, 0}) &&
+        cm(1, 2) == (Scalar{6, 0}));
+
+  const SparseMatrixCsr sp = random_sparse_spd(24, 0.15, 3);
+  std::stringstream ssp;
+  mm::write_sparse(ssp, sp);
+  const SparseMatrixCsr back = mm::read_sparse(ssp);
+  CHECK(back.row_ptr() == sp.row_ptr() && back.col_idx() == sp.col_idx() && back.values() == sp.values());
+
+  std::istringstream sym("%%MatrixMarket matrix coordinate real symmetric\n3 3 2\n2 1 5.0\n3 3 1.0\n");
+  const SparseMatrixCsr s3 = mm::read_sparse(sym);
+  CHECK(s3.nnz() == 3 && s3.densify()(1, 0) == (Scalar{5, 0}) && s3.densify()(0, 1) == (Scalar{5, 0}));
+  std::istringstream her("%%MatrixMarket matrix coordinate complex hermitian\n2 2 1\n2 1 1.0 2.0\n");
+  const DenseMatrix h = mm::read_sparse(her).densify();
+  CHECK(h(1, 0) == (Scalar{1, 2}) && h(0, 1) == (Scalar{1, -2}));
+  std::istringstream icoord("%%MatrixMarket matrix coordinate integer general\n2 2 1\n1 2 7\n");
+  const DenseMatrix dc = mm::read_dense(icoord);
+  CHECK(dc(0, 1) == (Scalar{7, 0}) && dc(1, 0) == (Scalar{0, 0}));
+  std::istringstream symarr("%%MATRIXMARKET matrix ARRAY real Symmetric\n2 2\n1\n2\n3\n");
+  CHECK_THROWS(mm::read_dense(symarr), IoError);  // the tag itself is case-sensitive
+  std::istringstream symarr2("%%MatrixMarket matrix ARRAY real Symmetric\n2 2\n1\n2\n3\n");
+  const DenseMatrix sa = mm::read_dense(symarr2);
+  CHECK(sa(1, 0) == (Scalar{2, 0}) && sa(0, 1) == (Scalar{2, 0}) && sa(1, 1) == (Scalar{3, 0}));
+
+  std::istringstream bad_banner("%%NotMatrixMarket\n1 1\n1\n");
+  CHECK_THROWS(mm::read_dense(bad_banner), IoError);
+  std::istringstream truncated("%%MatrixMarket matrix array real general\n3 3\n1\n2\n");
+  CHECK_THROWS(mm::read_dense(truncated), IoError);
+  std::istringstream out_of_range("%%MatrixMarket matrix coordinate real general\n2 2 1\n5 1 1.0\n");
+  CHECK_THROWS(mm::read_sparse(out_of_range), IoError);
+  std::istringstream array_as_sparse("%%MatrixMarket matrix array real general\n1 1\n1\n");
+  CHECK_THROWS(mm::read_sparse(array_as_sparse), IoError);
+  std::istringstream missing_im("%%MatrixMarket matrix array complex general\n1 1\n1.0\n");
+  CHECK_THROWS(mm::read_dense(missing_im), IoError);
+
+  namespace fs = std::filesystem;
+  const fs::path dir = fs::temp_directory_path() / "nnb_mm_test";
+  fs::create_directories(dir);
+  const std::string path = (dir / "w.mtx").string(), spath = (dir / "s.mtx").string();
+  mm::write_dense_file(path, m);
+  CHECK(mm::read_dense_file(path) == m);
+  CHECK(!fs::exists(path + ".tmp"));
+  CHECK(!mm::file_is_coordinate(path));
+  mm::write_sparse_file(spath, random_sparse_spd(6, 0.3, 6));
+  CHECK(mm::file_is_coordinate(spath));
+  CHECK_THROWS(mm::read_dense_file((dir / "missing.mtx").string()), IoError);
+  fs::remove_all(dir);
+}
+
 static void host_tests() {
   // GaussianStream: mt19937_64 + Box-Muller (values printed for the pytest cross-check)
   GaussianStream g(42);
@@ -102,6 +173,7 @@ static void host_tests() {
   CHECK_THROWS(FactorizedPlan::for_order(0, FactorizedMode::DenseStored), PlanError);
   CHECK_THROWS(DenseMatrix(1, 1, {Scalar{INFINITY, 0}}), DomainError);
   CHECK_THROWS((DenseMatrix{{Scalar{1, 0}}, {Scalar{1, 0}, Scalar{2, 0}}}), ShapeError);
+  mm_tests();
 }
 
 static void device_tests() {

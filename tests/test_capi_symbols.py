@@ -4,6 +4,7 @@ import ctypes
 import re
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
@@ -43,3 +44,11 @@ def test_abi_version_and_no_cpu_fallback():
         a = np.eye(4)
         with pytest.raises(nnb.DeviceError):
             nnb.matmul(a, a)
+
+
+def test_gaussian_stream_matches_reference(ref):
+    """nnb_gaussian_stream (host) reproduces nn::GaussianStream bit for bit."""
+    import paper_2212_02406_b200 as nnb
+
+    for seed, count in ((42, 7), (1, 1), (99, 10001)):
+        assert np.array_equal(nnb.gaussian_stream(seed, count), ref.gaussian(seed, count))

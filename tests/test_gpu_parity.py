@@ -491,3 +491,40 @@ def test_mimo_detect_full_size():
     xref = torch.linalg.solve(a[::4096], torch.einsum("bau,ba->bu", h[::4096].conj(), y[::4096]))
     rel = (torch.linalg.norm(xh1[::4096] - xref, dim=1) / torch.linalg.norm(xref, dim=1)).max().item()
     assert rel < 1e-9
+
+
+# ----------------------------------------------------------------- generators (§8(a) row A14)
+@pytest.mark.parametrize("n,cond,seed", [(1, 10.0, 3), (2, 5.0, 1), (3, 1e3, 7), (17, 1e2, 11), (64, 1e3, 5),
+                                         (130, 1e6, 2)])
+def test_random_spd_bitexact(ref, n, cond, seed):
+    """nn::random_spd on the device (Householder QR + exact-order products) is
+    bit-identical to the reference's O(n³) host loops."""
+    w = nnb.random_spd(n, cond, seed)
+    assert np.array_equal(w, ref.random_spd(n, cond, seed).real)
+
+
+def test_random_spd_c3_size_properties():
+    """The C3 generator at a larger size: symmetric, spectrum = the log-uniform λ."""
+    n, cond = 512, 1e3
+    w = nnb.random_spd(n, cond, 4)
+    assert np.array_equal(w, w.T)
+    ev = np.linalg.eigvalsh(w)
+    assert np.allclose(ev, np.sort(nnb.log_uniform_spectrum(n, cond)), rtol=1e-10, atol=1e-13)
+
+
+@pytest.mark.parametrize("n", [1, 4, 12, 40])
+def test_random_conditioned_complex(ref, n):
+    a = nnb.random_conditioned_complex(n, 50.0, 8)
+    r = ref.random_conditioned_complex(n, 50.0, 8)
+    assert rel_frob(a, r) < 1e-13  # hypot-based |z| in the reference: a few ulps, not bit-exact
+    s = np.linalg.svd(a, compute_uv=False)
+    assert abs(s[0] / s[-1] - 50.0) < 1e-8 * 50.0 if n > 1 else True
+
+
+def test_householder_q_unitary():
+    rng = np.random.default_rng(2)
+    for a in (rng.standard_normal((70, 70)), rng.standard_normal((33, 33)) + 1j * rng.standard_normal((33, 33))):
+        q = nnb.householder_q(a)
+        assert np.linalg.norm(q.conj().T @ q - np.eye(a.shape[0])) < 1e-13
+        r = q.conj().T @ a  # upper triangular R
+        assert np.linalg.norm(np.tril(r, -1)) < 1e-12 * np.linalg.norm(a)
