@@ -526,7 +526,8 @@ def run_sparse(args, world, rank):
     if sharded:
         plan.close()
         comm.close()
-    alg = 63 * sparse_bytes(n, col.size, csr_col_bytes(rp, col))  # whole-job bytes per solve
+    cb = csr_col_bytes(rp, col)
+    alg = 63 * sparse_bytes(n, col.size, cb)  # whole-job algorithmic bytes per solve
     gbs = alg / (ms * 1e-3) / 1e9
     return {"metric": "sparse factorized solve, 4096^2 5-pt Laplacian+I, gamma=63", "value": round(gbs, 1),
             "unit": "GB/s", "ms_per_step": round(ms, 3),
@@ -535,7 +536,9 @@ def run_sparse(args, world, rank):
                          "frac": round(gbs / (HBM_PEAK * world), 4),
                          "traffic": ncu_traffic("sparse_application") if grid == 4096 and not sharded else None,
                          "traffic_unit": "bytes per application (63 per solve)",
-                         "per_launch": "nnz*(8+4) + (N+1)*4 + 2N*8 bytes per application (x63)"}}
+                         "per_launch": f"nnz*(8+{cb}) + (N+1)*4 + 2N*8 bytes per application (x63): f64 values, "
+                                       f"{'int16 column deltas' if cb == 2 else 'int32 columns'}, int32 row offsets, "
+                                       "t in + t out"}}
 
 
 def cpu_sparse_sample(grid: int):

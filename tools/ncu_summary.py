@@ -41,23 +41,37 @@ def full(paths):
 
 
 def launches(path, what):
+    """Per-kernel totals of gpu__time_duration.sum (and DRAM bytes when the list carries them)."""
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     hdr = rows[hi]
-    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    agg = defaultdict(lambda: [0, 0.0])
+    ki, mi, vi, ui = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+    scale = {"ns": 1.0, "nsecond": 1.0, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6,
+             "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    agg = defaultdict(lambda: defaultdict(float))
+    count = defaultdict(int)
     for r in rows[hi + 1:]:
-        if len(r) > vi:
-            scale = {"ns": 1.0, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6, "nsecond": 1.0}.get(r[ui], 1.0)
-            name = r[ki].split("(")[0][:80]
-            agg[name][0] += 1
-            agg[name][1] += float(r[vi].replace(",", "")) * scale
-    tot = sum(v for _, v in agg.values())
-    print("ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised launches)")
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0][:80]
+        v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+        agg[name][r[mi]] += v
+        if r[mi] == "gpu__time_duration.sum":
+            count[name] += 1
+    tot = sum(a["gpu__time_duration.sum"] for a in agg.values())
+    has_dram = any("dram__bytes_read.sum" in a for a in agg.values())
+    print("ncu --metrics gpu__time_duration.sum" + (",dram__bytes_read.sum,dram__bytes_write.sum" if has_dram else "")
+          + " --clock-control none (cold-cache, serialised launches)")
     print(f"workload: {what}\n")
-    print(f"{'total ms':>10} {'share':>7} {'launches':>9}  kernel")
-    for k, (c, v) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-        print(f"{v / 1e6:10.3f} {100 * v / tot:6.2f}% {c:9d}  {k}")
+    print(f"{'total ms':>10} {'share':>7} {'launches':>9} " + (f"{'GB/launch':>10} {'TB/s':>6} " if has_dram else "")
+          + " kernel")
+    for k, a in sorted(agg.items(), key=lambda kv: -kv[1]["gpu__time_duration.sum"]):
+        t, c = a["gpu__time_duration.sum"], max(count[k], 1)
+        extra = ""
+        if has_dram:
+            by = a["dram__bytes_read.sum"] + a["dram__bytes_write.sum"]
+            extra = f"{by / c / 1e9:10.3f} {by / t / 1e3 if t else 0:6.2f} "
+        print(f"{t / 1e6:10.3f} {100 * t / tot:6.2f}% {count[k]:9d} {extra} {k}")
 
 
 if __name__ == "__main__":
