@@ -24,8 +24,9 @@
 // One pass per solve (compact_csr) narrows the row offsets to int32 and, for
 // banded operators, the columns to int16 deltas from the row.
 // HBM-bound: 10 (int16) or 12 (int32 columns) B per nonzero + 4 B per row of
-// CSR, 8 B in + 8 B out per row.  Measured on B200 (config 4): 13.7 ms per
-// solve, 209.5 µs per inner application at 5.56 TB/s.
+// CSR, 8 B in + 8 B out per row.  The register cap (32, for 8 resident blocks
+// = 64 warps per SM) buys the memory-level parallelism: 13.0 vs 13.7 ms per
+// C5 solve at 6 blocks/SM.
 #include <cstdlib>
 #include <cstring>
 
@@ -52,8 +53,12 @@ __device__ __forceinline__ double finish(double tin, double y, double theta, dou
 // Rows [r_begin, r_end) of one application.  Gathers read t_ext through the
 // (possibly halo-remapped) column indices; the diagonal term, z and the
 // output are indexed by row.
+// NNB_SPMV_MINB: resident 256-thread blocks per SM the register budget must allow.
+#ifndef NNB_SPMV_MINB
+#define NNB_SPMV_MINB 8
+#endif
 template <typename Idx, typename C, int MODE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, NNB_SPMV_MINB)
     spmv_rows_kernel(const Idx* __restrict__ rp, const C* __restrict__ col, const double* __restrict__ val,
                      int64_t r_begin, int64_t r_end, int64_t diag_off, int64_t k, const double* __restrict__ t_ext,
                      const double* __restrict__ t_own, double* __restrict__ out, const double* __restrict__ zold,
