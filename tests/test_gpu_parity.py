@@ -528,3 +528,31 @@ def test_householder_q_unitary():
         assert np.linalg.norm(q.conj().T @ q - np.eye(a.shape[0])) < 1e-13
         r = q.conj().T @ a  # upper triangular R
         assert np.linalg.norm(np.tril(r, -1)) < 1e-12 * np.linalg.norm(a)
+
+
+def test_c4_full_size_nest_cubes_the_residual():
+    """BASELINE config 3 at full size (N=32768, p=2): one nest maps R = I − A·X to
+    R' = R³ exactly in exact arithmetic (I − A·X(I+R+R²) = I − (I−R)(I+R+R²)), so the
+    fused eps after the nest must equal ‖R³‖_F/√N formed independently with torch
+    (cuBLAS) — a size-independent property of the whole chain at the headline size."""
+    import torch
+
+    n = 32768
+    g = torch.Generator(device="cuda").manual_seed(2212)
+    b = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
+    a = torch.addmm(torch.eye(n, dtype=torch.float64, device="cuda"), b, b.T, alpha=1.0 / n)
+    del b
+    torch.cuda.empty_cache()
+    x0 = (a.T / (a.abs().sum(0).max() * a.abs().sum(1).max())).contiguous()
+    for _ in range(3):  # from X0 the residual is far from small; advance to the asymptotic regime
+        x0, _ = nnb.nn_chain(a, x0, p=2, max_iters=1, final_residual=False)
+    x1, rep = nnb.nn_chain(a, x0, p=2, max_iters=1)
+    eps0, eps1 = rep.history[0][1], rep.history[1][1]
+    r = torch.eye(n, dtype=torch.float64, device="cuda") - a @ x0
+    assert abs(torch.linalg.norm(r).item() / n ** 0.5 - eps0) < 1e-12 * max(eps0, 1e-300) + 1e-15
+    r3 = r @ (r @ r)
+    del r
+    expect = torch.linalg.norm(r3).item() / n ** 0.5
+    assert eps1 < eps0
+    assert abs(eps1 - expect) <= 1e-9 * expect  # rounding of the cubed residual
+    assert rep.products == 4
