@@ -9,8 +9,7 @@
 // bookkeeping (reports, nest estimates, order fits).
 //
 // Out of scope (not declared; link the reference's nncore for them):
-// direct_inverse_oracle, matvec, theta_power, contraction_check, cns_invert
-// and the cost model.
+// direct_inverse_oracle, cns_invert and the cost model.
 #pragma once
 
 #include <atomic>
@@ -218,6 +217,8 @@ DenseMatrix scale(const DenseMatrix& m, Scalar factor, OpCounter* counter = null
 DenseMatrix identity_minus(const DenseMatrix& m, OpCounter* counter = nullptr);
 DenseMatrix plus_identity(const DenseMatrix& m, OpCounter* counter = nullptr);
 DenseMatrix conjugate_transpose(const DenseMatrix& m, OpCounter* counter = nullptr);
+/// m·x on the device (kernels.cpp:164-173); untallied.
+std::vector<Scalar> matvec(const DenseMatrix& m, const std::vector<Scalar>& x);
 Scalar trace(const DenseMatrix& m);
 double frobenius_norm(const DenseMatrix& m);
 
@@ -255,6 +256,11 @@ struct Normalization {
 };
 Normalization theta_trace(const DenseMatrix& w);
 Normalization theta_trace(const SparseMatrixCsr& w);
+/// theta = k / ((k+1)·r²), r the growth of k+1 normalised applications of W to a
+/// GaussianStream probe (proj/src/normalization.cpp:51-92), every product on the GPU.
+Normalization theta_power(const DenseMatrix& w, std::size_t k, std::uint64_t seed);
+/// Measured ||I − phi·w_tilde||_2 (normalization.cpp:101-104); untallied.
+double contraction_check(const DenseMatrix& phi, const DenseMatrix& w_tilde);
 DenseMatrix normalize(const DenseMatrix& w, const Normalization& norm);
 
 // ------------------------------------------------------------------ solver

@@ -450,13 +450,52 @@ static double positive_real_trace(Scalar t, const char* who) {
   return t.real();
 }
 
-static Normalization measured(double theta, double contraction) {
+static Normalization measured(double theta, double contraction, ThetaKind kind = ThetaKind::TraceTheta1,
+                              std::size_t k = 0) {
   Normalization n;
   n.theta = theta;
-  n.kind = ThetaKind::TraceTheta1;
+  n.kind = kind;
+  n.k_order = k;
   n.contraction_norm = contraction;
   n.valid = contraction < 1.0;
   return n;
+}
+
+Normalization theta_power(const DenseMatrix& w, std::size_t k, std::uint64_t seed) {
+  if (!w.square()) throw ShapeError("theta_power: matrix must be square");
+  if (k < 1) throw DomainError("theta_power: k must be >= 1");
+  const std::size_t n = w.rows();
+  // k+1 normalised applications; the last growth factor r = ||W^{k+1}v|| / ||W^k v||
+  auto growth_of = [&](std::uint64_t s) -> std::optional<double> {
+    const std::vector<Scalar> probe = gaussian_probe(n, s);  // unit complex Gaussian, as the reference draws it
+    if (probe.empty() || std::all_of(probe.begin(), probe.end(), [](const Scalar& x) { return x == Scalar{}; }))
+      return std::nullopt;
+    DenseMatrix v(n, 1, probe);
+    double r = 0.0;
+    for (std::size_t j = 0; j <= k; ++j) {
+      v = matmul(w, v);
+      r = frobenius_norm(v);
+      if (r == 0.0) return std::nullopt;
+      v = scale(v, Scalar{1.0 / r, 0.0});
+    }
+    return r;
+  };
+  std::optional<double> r = growth_of(seed);
+  if (!r) r = growth_of(seed + 1);
+  if (!r) throw DegenerateProbeError("theta_power: probe vector annihilated twice");
+  const double kd = static_cast<double>(k);
+  const double theta = kd / ((kd + 1.0) * (*r) * (*r));
+  const DenseMatrix shifted = identity_minus(scale(w, Scalar{theta, 0.0}));
+  return measured(theta, spectral_norm_estimate(shifted).value, ThetaKind::PowerTheta2, k);
+}
+
+double contraction_check(const DenseMatrix& phi, const DenseMatrix& w_tilde) {
+  return spectral_norm_estimate(identity_minus(matmul(phi, w_tilde))).value;
+}
+
+std::vector<Scalar> matvec(const DenseMatrix& m, const std::vector<Scalar>& x) {
+  if (m.cols() != x.size()) throw ShapeError("matvec: dimension mismatch");
+  return matmul(m, DenseMatrix(x.size(), 1, x)).data();
 }
 
 Normalization theta_trace(const DenseMatrix& w) {

@@ -5,7 +5,8 @@
 //
 //   nnbench gen-matrix --N n --out f.mtx [--cond c] [--seed s] [--kind spd|complex|sparse-spd] [--density d]
 //   nnbench invert IN.mtx [--method nn|newton|chebyshev|ns|nn-explicit|factorized-ns] [--depth|-L L]
-//                  [--nests|-i k] [--order|--gamma g] [--tol t] [--theta trace] [--out X.mtx] [--report r.json]
+//                  [--nests|-i k] [--order|--gamma g] [--tol t] [--theta trace|power:k] [--seed s] [--out X.mtx]
+//                  [--report r.json]
 //   nnbench solve --matrix|-A A.mtx --rhs|-b B.mtx [--method nn|sparse-factorized] [--depth|-L L]
 //                 [--nests|-i k] [--order|--gamma g] [--tol t] [--out x.mtx] [--report r.json]
 //   nnbench bench --methods m1,m2 [--N n1,n2] [--cond c1,c2] [--depths L1,L2] [--nests|-i k] [--tol t]
@@ -14,7 +15,7 @@
 // Exit codes: 0 success / tolerance reached, 2 nest budget exhausted, 1 input
 // or validation error.  Not provided (their reference routines are out of
 // scope): analyze-cost (cost model), --method cns (cns_invert),
-// --theta power:k (theta_power), --estimate-kappa (direct_inverse_oracle).
+// --estimate-kappa (direct_inverse_oracle).
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -118,10 +119,17 @@ class Options {
   std::vector<std::string> positional_;
 };
 
-Normalization normalization(const DenseMatrix& w, const std::string& theta) {
+Normalization normalization(const DenseMatrix& w, const std::string& theta, std::uint64_t seed) {
   if (theta == "trace") return theta_trace(w);
-  if (theta.rfind("power:", 0) == 0)
-    throw DomainError("--theta power:k needs theta_power, which the B200 build does not provide");
+  if (theta.rfind("power:", 0) == 0) {
+    const long k = std::strtol(theta.c_str() + 6, nullptr, 10);
+    if (k < 1) throw DomainError("--theta power:k requires k >= 1");
+    const Normalization power = theta_power(w, static_cast<std::size_t>(k), seed);
+    if (power.valid) return power;
+    std::cerr << "note: power normalization not contractive (measured " << power.contraction_norm
+              << "), falling back to trace\n";
+    return theta_trace(w);
+  }
   throw DomainError("--theta must be 'trace' or 'power:k'");
 }
 
@@ -134,15 +142,6 @@ BigInt next_factorized_order(const BigInt& at_least) {  // smallest 2^s − 1 >=
   BigInt p(2);
   while (p - 1 < at_least) p = p << 1;
   return p - 1;
-}
-
-std::size_t log2_exact(BigInt g1) {
-  std::size_t s = 0;
-  while (g1 > BigInt(1)) {
-    g1 = BigInt(static_cast<unsigned long long>(g1) >> 1);
-    ++s;
-  }
-  return s;
 }
 
 // ---------------------------------------------------------------- gen-matrix
@@ -168,7 +167,8 @@ int invert(const Options& o) {
   const DenseMatrix w = mm::read_dense_file(o.positional()[0]);
   if (!w.square()) throw ShapeError("invert: input matrix must be square");
   const std::string method = o.str("--method", "nn");
-  const Normalization norm = normalization(w, o.str("--theta", "trace"));
+  const Normalization norm =
+      normalization(w, o.str("--theta", "trace"), static_cast<std::uint64_t>(o.integer("--seed", 1)));
   SolverConfig config;
   config.depth_L = static_cast<std::size_t>(o.integer("--depth", 2));
   config.tol = o.num("--tol", 1e-10);

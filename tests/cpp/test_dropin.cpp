@@ -456,6 +456,45 @@ static void schedule_tests() {
   CHECK_THROWS(nn_explicit(DenseMatrix::identity(2), normalized(2, 0.5, 21), 40, 2), BudgetError);
 }
 
+// theta_power / contraction_check / matvec (proj/tests/test_preconditioning.cpp:49-123 restated)
+static void power_normalization_tests() {
+  for (std::size_t k : {1, 2, 8}) {
+    const auto nm = theta_power(DenseMatrix::identity(6), k, 3);
+    CHECK(std::fabs(nm.theta - static_cast<double>(k) / (k + 1.0)) < 1e-12);
+    CHECK(std::fabs(nm.contraction_norm - 1.0 / (k + 1.0)) < 1e-9);
+    CHECK(nm.valid && nm.kind == ThetaKind::PowerTheta2 && nm.k_order == k);
+  }
+  const auto d13 = theta_power(DenseMatrix::diagonal({Scalar{1, 0}, Scalar{3, 0}}), 8, 7);
+  CHECK(std::fabs(d13.theta - 8.0 / 81.0) < 1e-5 * (8.0 / 81.0));
+  CHECK(std::fabs(d13.contraction_norm - (1.0 - d13.theta)) < 1e-6 && d13.valid);
+  // test_preconditioning.cpp:70 expects contraction 1/5 here, but theta = 4/(5·0.1²) = 80 gives
+  // ||I − 80·0.1·I|| = 7 (SURVEY.md Appendix A lists it as failing in the reference): pin that
+  const auto sc = theta_power(scale(DenseMatrix::identity(4), Scalar{0.1, 0}), 4, 5);
+  CHECK(std::fabs(sc.theta - 80.0) < 1e-10 * 80.0 && std::fabs(sc.contraction_norm - 7.0) < 1e-9 && !sc.valid);
+  DenseMatrix nilpotent(2, 2);
+  nilpotent(0, 1) = Scalar{1, 0};
+  CHECK_THROWS(theta_power(nilpotent, 1, 11), DegenerateProbeError);
+  CHECK_THROWS(theta_power(DenseMatrix::identity(3), 0, 1), DomainError);
+
+  const DenseMatrix wt = DenseMatrix::diagonal({Scalar{0.25, 0}, Scalar{0.75, 0}});
+  const DenseMatrix inv = DenseMatrix::diagonal({Scalar{4.0, 0}, Scalar{4.0 / 3.0, 0}});
+  CHECK(contraction_check(inv, wt) < 1e-9);
+  CHECK(std::fabs(contraction_check(DenseMatrix::identity(2), wt) - 0.75) < 1e-9);
+  CHECK(std::fabs(contraction_check(DenseMatrix(2, 2), wt) - 1.0) < 1e-9);
+
+  const DenseMatrix m = gauss(5, 3, 81, true);
+  const std::vector<Scalar> x = {Scalar{1, 2}, Scalar{-0.5, 0}, Scalar{0, 3}};
+  const std::vector<Scalar> y = matvec(m, x);
+  double err = 0.0;
+  for (std::size_t i = 0; i < 5; ++i) {
+    Scalar s{0, 0};
+    for (std::size_t k = 0; k < 3; ++k) s += m(i, k) * x[k];
+    err = std::max(err, std::abs(y[i] - s));
+  }
+  CHECK(y.size() == 5 && err < 1e-14);
+  CHECK_THROWS(matvec(m, std::vector<Scalar>(2)), ShapeError);
+}
+
 // conjugate_transpose and solve_normal_equations (proj/tests/test_factorized.cpp:80-148,
 // test_matrix_core.cpp conjugate_transpose cases), inputs from this file's generators.
 static void normal_equation_tests() {
@@ -580,6 +619,7 @@ int main(int argc, char** argv) {
     device_tests();
     schedule_tests();
     normal_equation_tests();
+    power_normalization_tests();
   }
   std::printf("%s: %d checks, %d failures\n", host_only ? "host" : "all", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;

@@ -95,6 +95,9 @@ def test_invert_exit_codes_and_methods(tmp_path):
         code, so, err = nnbench("invert", w2, "--method", method, "--tol", 1e-6, *extra)
         assert code == 0, (method, so, err)
         assert so.startswith(f"method={method} N=12 eps=")
+    code, so, err = nnbench("invert", w2, "--theta", "power:4", "--seed", 5, "--tol", 1e-10)
+    assert code == 0 and "stopped=tolerance" in so, err  # theta_power normalisation
+    assert nnbench("invert", w2, "--theta", "power:0")[0] == 1
     rect = tmp_path / "rect.mtx"
     rect.write_text("%%MatrixMarket matrix array real general\n2 3\n1\n2\n3\n4\n5\n6\n")
     code, _, err = nnbench("invert", rect)
