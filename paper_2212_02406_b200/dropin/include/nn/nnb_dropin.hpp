@@ -9,7 +9,7 @@
 // bookkeeping (reports, nest estimates, order fits).
 //
 // Out of scope (not declared; link the reference's nncore for them):
-// direct_inverse_oracle, cns_invert and the cost model.
+// direct_inverse_oracle and the cost model.
 #pragma once
 
 #include <atomic>
@@ -335,6 +335,12 @@ DenseMatrix ns_factorized(const DenseMatrix& phi, const DenseMatrix& w_tilde, co
                           OpCounter* counter = nullptr);
 DenseMatrix solve_sparse_factorized(const LinearSystem& sys, const BigInt& gamma,
                                     const Normalization& norm, OpCounter* counter = nullptr);
+
+/// Chebyshev–Neumann hybrid (proj/src/factorized.cpp:142-158): ci_steps
+/// Chebyshev steps from I build the preconditioner, then an outer series of
+/// ns_terms terms (product form when factorize_outer and ns_terms + 1 = 2^s).
+/// Effective series order 3^ci_steps·(ns_terms + 1) − 1; every product on the GPU.
+DenseMatrix cns_invert(const DenseMatrix& w_tilde, const CnsConfig& cns, OpCounter* counter = nullptr);
 
 struct NormalSolveResult {
   DenseMatrix x;

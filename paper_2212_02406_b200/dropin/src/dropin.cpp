@@ -821,6 +821,17 @@ SparseMatrixCsr random_sparse_spd(std::size_t n, double density, std::uint64_t s
   return SparseMatrixCsr::build(n, n, std::move(t));
 }
 
+DenseMatrix cns_invert(const DenseMatrix& w_tilde, const CnsConfig& cns, OpCounter* counter) {
+  if (!w_tilde.square()) throw ShapeError("cns_invert: matrix must be square");
+  if (cns.ns_terms < 1) throw DomainError("cns_invert: ns_terms must be >= 1");
+  DenseMatrix pre = DenseMatrix::identity(w_tilde.rows());  // order 3^ci_steps − 1 after the steps
+  for (std::size_t i = 0; i < cns.ci_steps; ++i) pre = chebyshev_step(pre, w_tilde, counter);
+  const std::size_t t = cns.ns_terms;
+  if (cns.factorize_outer && ((t + 1) & t) == 0)  // t + 1 a power of two: the product form applies
+    return ns_factorized(pre, w_tilde, FactorizedPlan::for_order(BigInt(t), FactorizedMode::DenseStored), counter);
+  return ns_sum(pre, w_tilde, t, counter);
+}
+
 // proj/src/factorized.cpp:63-99: W = A^H A and rhs = A^H B (unless the caller
 // already formed them), theta from theta_trace(W), W^-1 from nn_invert, then
 // x = W^-1 rhs.  The backward error on the normal equations is diagnostic and

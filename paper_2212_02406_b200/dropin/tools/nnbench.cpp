@@ -4,7 +4,7 @@
 // the GPU through libnn_b200 → libnnb.
 //
 //   nnbench gen-matrix --N n --out f.mtx [--cond c] [--seed s] [--kind spd|complex|sparse-spd] [--density d]
-//   nnbench invert IN.mtx [--method nn|newton|chebyshev|ns|nn-explicit|factorized-ns] [--depth|-L L]
+//   nnbench invert IN.mtx [--method nn|newton|chebyshev|ns|nn-explicit|factorized-ns|cns] [--depth|-L L]
 //                  [--nests|-i k] [--order|--gamma g] [--tol t] [--theta trace|power:k] [--seed s] [--out X.mtx]
 //                  [--report r.json]
 //   nnbench solve --matrix|-A A.mtx --rhs|-b B.mtx [--method nn|sparse-factorized] [--depth|-L L]
@@ -14,8 +14,8 @@
 //
 // Exit codes: 0 success / tolerance reached, 2 nest budget exhausted, 1 input
 // or validation error.  Not provided (their reference routines are out of
-// scope): analyze-cost (cost model), --method cns (cns_invert),
-// --estimate-kappa (direct_inverse_oracle).
+// scope): analyze-cost (cost model) and --estimate-kappa
+// (direct_inverse_oracle).
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -195,7 +195,10 @@ int invert(const Options& o) {
       if (order < 0) throw DomainError("--order is required for --method factorized-ns");
       phi = ns_factorized(id, wt, FactorizedPlan::for_order(BigInt(order), FactorizedMode::DenseStored), &counter);
     } else if (method == "cns") {
-      throw DomainError("--method cns needs cns_invert, which the B200 build does not provide");
+      CnsConfig cns;
+      cns.ci_steps = nests > 0 ? static_cast<std::size_t>(nests) : 1;
+      cns.ns_terms = order >= 1 ? static_cast<std::size_t>(order) : 1;
+      phi = cns_invert(wt, cns, &counter);
     } else {
       throw DomainError("unknown --method '" + method + "'");
     }
@@ -305,7 +308,12 @@ std::string bench_point(const std::string& method, std::size_t n, double cond, s
       const unsigned long long twice = depth_eff * (i * (i + 1) * (i + 2) + 1) + 2 * (2 * i * (i + 1) + 1);
       predicted = twice % 2 ? std::to_string(twice) + "/2" : std::to_string(twice / 2);
     } else if (method == "cns") {
-      throw DomainError("bench: cns needs cns_invert, which the B200 build does not provide");
+      CnsConfig cns;
+      cns.ci_steps = 2;
+      cns.ns_terms = std::max<std::size_t>(nests, 1);
+      inverse = scale(cns_invert(wt, cns, &counter), Scalar{norm.theta, 0.0}, &counter);
+      gamma = BigInt(9) * BigInt(cns.ns_terms + 1) - 1;
+      predicted = "0";
     } else {
       throw DomainError("unknown bench method '" + method + "'");
     }

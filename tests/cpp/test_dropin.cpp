@@ -495,6 +495,35 @@ static void power_normalization_tests() {
   CHECK_THROWS(matvec(m, std::vector<Scalar>(2)), ShapeError);
 }
 
+// cns_invert (proj/tests/test_factorized.cpp:209-250 restated)
+static void cns_tests() {
+  const DenseMatrix wt = normalized(8, 0.5, 14), id = DenseMatrix::identity(8);
+  CnsConfig plain;
+  plain.ci_steps = 0;
+  plain.ns_terms = 5;
+  CHECK(rel(cns_invert(wt, plain), ns_sum(id, wt, 5)) < 1e-14);
+  CnsConfig two;
+  two.ci_steps = 2;
+  two.ns_terms = 1;
+  double expect = 0.0;  // Σ_{n=0}^{17} 0.5^n
+  for (int k = 17; k >= 0; --k) expect += std::pow(0.5, k);
+  CHECK(std::fabs(cns_invert(s1(0.5), two)(0, 0).real() - expect) < 1e-14 * expect);
+  CHECK(std::fabs(chebyshev_step(chebyshev_step(s1(1.0), s1(0.5)), s1(0.5))(0, 0).real() - 1.99609375) < 1e-15);
+  CnsConfig eff;
+  eff.ci_steps = 2;
+  eff.ns_terms = 2;  // effective order 3^2·3 − 1 = 26
+  CHECK(rel(cns_invert(wt, eff), ns_sum(id, wt, 26)) < 1e-11);
+  CnsConfig p3;
+  p3.ci_steps = 1;
+  p3.ns_terms = 3;
+  CnsConfig f3 = p3;
+  f3.factorize_outer = true;
+  CHECK(rel(cns_invert(wt, f3), cns_invert(wt, p3)) < 1e-12);
+  CnsConfig bad;
+  bad.ns_terms = 0;
+  CHECK_THROWS(cns_invert(wt, bad), DomainError);
+}
+
 // conjugate_transpose and solve_normal_equations (proj/tests/test_factorized.cpp:80-148,
 // test_matrix_core.cpp conjugate_transpose cases), inputs from this file's generators.
 static void normal_equation_tests() {
@@ -620,6 +649,7 @@ int main(int argc, char** argv) {
     schedule_tests();
     normal_equation_tests();
     power_normalization_tests();
+    cns_tests();
   }
   std::printf("%s: %d checks, %d failures\n", host_only ? "host" : "all", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;

@@ -102,7 +102,8 @@ def test_invert_exit_codes_and_methods(tmp_path):
     rect.write_text("%%MatrixMarket matrix array real general\n2 3\n1\n2\n3\n4\n5\n6\n")
     code, _, err = nnbench("invert", rect)
     assert code == 1 and "square" in err
-    assert nnbench("invert", a, "--method", "cns")[0] == 1
+    code, so, err = nnbench("invert", w2, "--method", "cns", "-i", 3, "--order", 40, "--tol", 1e-6)
+    assert code == 0 and so.startswith("method=cns N=12 eps="), err
 
 
 @pytest.mark.gpu
