@@ -44,7 +44,8 @@ enum nnb_status {
   NNB_ERR_CUDA = 7,
   NNB_ERR_NCCL = 8,
   NNB_ERR_OOM = 9,
-  NNB_ERR_NODEVICE = 10
+  NNB_ERR_NODEVICE = 10,
+  NNB_ERR_SINGULAR = 11     /* nn::SingularMatrixError errors.hpp (pivot index out-param) */
 };
 
 /* Operand order of the nest ("Product order").
@@ -141,6 +142,13 @@ int nnb_householder_q_z(const double* A, int64_t n, double* Q, void* stream);
 int nnb_random_spd_d(const double* G, const double* lam, int64_t n, double* W, void* stream);
 int nnb_random_conditioned_z(const double* GU, const double* GV, const double* sigma, int64_t n, double* A,
                              void* stream);
+
+/* Gauss–Jordan inverse with partial pivoting: nn::direct_inverse_oracle
+ * (proj/include/nn/kernels.hpp:67, proj/src/kernels.cpp:317-350), on the
+ * device; bit-identical to the reference for real input.  NNB_ERR_SINGULAR
+ * with *pivot_index when a pivot magnitude is <= 1e-13·||M||_F. */
+int nnb_direct_inverse_d(const double* M, int64_t n, double* out, int32_t* pivot_index, void* stream);
+int nnb_direct_inverse_z(const double* M, int64_t n, double* out, int32_t* pivot_index, void* stream);
 
 /* ||M||_F (proj/include/nn/kernels.hpp:42) and trace (:40). */
 int nnb_frobenius_d(const double* M, int64_t count, double* out, void* stream);

@@ -103,6 +103,17 @@ class Reference(_Lib):
         self._check(self.fn("random_spd", [C.c_int64, C.c_double, C.c_uint64, _dp])(n, cond, seed, _ptr(out)))
         return out
 
+    def direct_inverse(self, m):
+        """nn::direct_inverse_oracle; OracleError(11, ..., pivot) on SingularMatrixError."""
+        m = _z(m)
+        out = np.empty_like(m)
+        piv = C.c_int(-1)
+        st = self.fn("direct_inverse_z", [_dp, C.c_int64, _dp, _ip])(_ptr(m), m.shape[0], _ptr(out), C.byref(piv))
+        if st == 11:
+            raise OracleError(st, self._err().decode(), piv.value)
+        self._check(st)
+        return out
+
     def random_conditioned_complex(self, n: int, cond: float, seed: int) -> np.ndarray:
         out = np.empty((n, n), np.complex128)
         f = self.fn("random_conditioned_complex", [C.c_int64, C.c_double, C.c_uint64, _dp])

@@ -118,6 +118,21 @@ int nnref_random_spd(int64_t n, double cond, uint64_t seed, double* out) {
   return guarded([&] { store(nn::random_spd(static_cast<std::size_t>(n), cond, seed), out); });
 }
 
+// nn::direct_inverse_oracle (proj/src/kernels.cpp:317-350); pivot index on SingularMatrixError (status 11).
+int nnref_direct_inverse_z(const double* m, int64_t n, double* out, int* pivot) {
+  try {
+    store(nn::direct_inverse_oracle(load(m, n, n)), out);
+    return kOk;
+  } catch (const nn::SingularMatrixError& e) {
+    g_err = e.what();
+    *pivot = static_cast<int>(e.pivot_index);
+    return 11;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return kOther;
+  }
+}
+
 // nn::random_conditioned_complex (proj/src/kernels.cpp:383-407).
 int nnref_random_conditioned_complex(int64_t n, double cond, uint64_t seed, double* out) {
   return guarded([&] { store(nn::random_conditioned_complex(static_cast<std::size_t>(n), cond, seed), out); });

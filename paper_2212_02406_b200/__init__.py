@@ -58,8 +58,14 @@ class DeviceError(Error):
     """CUDA / NCCL / OOM / no device (the library has no CPU fallback)."""
 
 
+class SingularMatrixError(Error):
+    def __init__(self, msg: str, pivot_index: int):
+        super().__init__(msg)
+        self.pivot_index = pivot_index
+
+
 _STATUS = {1: ShapeError, 2: DomainError, 3: DivergenceError, 4: ContractionError, 5: PlanError,
-           6: BudgetError, 7: DeviceError, 8: DeviceError, 9: DeviceError, 10: DeviceError}
+           6: BudgetError, 7: DeviceError, 8: DeviceError, 9: DeviceError, 10: DeviceError, 11: SingularMatrixError}
 
 ORDER_NORTHSTAR, ORDER_REFERENCE = 0, 1
 X0_GIVEN, X0_SCALED_IDENTITY, X0_TRANSPOSE_NORM, X0_JACOBI = 0, 1, 2, 3
@@ -122,6 +128,8 @@ _SIGS = {
     "nnb_householder_q_z": ([_dp, _i64, _dp, _dp], C.c_int),
     "nnb_random_spd_d": ([_dp, _dp, _i64, _dp, _dp], C.c_int),
     "nnb_random_conditioned_z": ([_dp, _dp, _dp, _i64, _dp, _dp], C.c_int),
+    "nnb_direct_inverse_d": ([_dp, _i64, _dp, C.POINTER(C.c_int32), _dp], C.c_int),
+    "nnb_direct_inverse_z": ([_dp, _i64, _dp, C.POINTER(C.c_int32), _dp], C.c_int),
     "nnb_transpose_d": ([_dp, _i64, _i64, _dp, _dp], C.c_int),
     "nnb_conj_transpose_z": ([_dp, _i64, _i64, _dp, _dp], C.c_int),
     "nnb_spectral_norm_z": ([_dp, _i64, _dp, C.c_double, _i32, _dp, _dp, _dp, _dp], C.c_int),
@@ -191,8 +199,8 @@ def _check(status: int, index: int = 0) -> None:
         return
     msg = lib().nnb_last_error().decode(errors="replace")
     cls = _STATUS.get(status, Error)
-    if cls is DivergenceError:
-        raise DivergenceError(msg, index)
+    if cls in (DivergenceError, SingularMatrixError):
+        raise cls(msg, index)
     raise cls(msg)
 
 
@@ -329,6 +337,20 @@ def conjugate_transpose(a):
     out = _empty_like(a, (a.shape[1], a.shape[0]))
     f = lib().nnb_conj_transpose_z if z else lib().nnb_transpose_d
     _check(f(_ptr(a), a.shape[0], a.shape[1], _ptr(out), _stream(a)))
+    return out
+
+
+def direct_inverse_oracle(a):
+    """nn::direct_inverse_oracle (kernels.hpp:67): Gauss–Jordan with partial pivoting on the
+    device, bit-identical to the reference for real input; SingularMatrixError(pivot_index)."""
+    if a.shape[0] != a.shape[1]:
+        raise ShapeError("direct_inverse_oracle: matrix must be square")
+    z = _is_complex(a)
+    a = _prep(a, z)
+    out = _empty_like(a)
+    piv = C.c_int32(-1)
+    f = lib().nnb_direct_inverse_z if z else lib().nnb_direct_inverse_d
+    _check(f(_ptr(a), a.shape[0], _ptr(out), C.byref(piv), _stream(a)), piv.value)
     return out
 
 

@@ -439,6 +439,41 @@ int nnb_random_conditioned_z(const double* GU, const double* GV, const double* s
   return sync(s);
 }
 
+static int direct_inverse_call(const double* M, int64_t n, int cplx, double* out, int32_t* pivot_index,
+                               void* stream) {
+  NNB_TRY(require_device());
+  if (n < 0) return fail(NNB_ERR_SHAPE, "direct_inverse_oracle: matrix must be square");
+  if (n == 0) return 0;
+  cudaStream_t s = resolve(stream);
+  const size_t cnt = (size_t)((cplx ? 2 : 1) * n * n);
+  In m;
+  NNB_TRY(m.stage(M, cnt, s));
+  DevBuf fro;
+  NNB_TRY(fro.alloc(sizeof(double), s));
+  NNB_TRY(sumsq(m.d, (int64_t)cnt, fro.as<double>(), s));
+  double ss = 0.0;
+  NNB_CUDA(cudaMemcpyAsync(&ss, fro.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  Out o;
+  NNB_TRY(o.prepare(out, cnt, s));
+  int singular = -1;
+  NNB_TRY(direct_inverse(m.d, n, cplx, 1e-13 * std::sqrt(ss), o.d, &singular, s));
+  if (singular >= 0) {
+    if (pivot_index) *pivot_index = singular;
+    return fail(NNB_ERR_SINGULAR, "direct_inverse_oracle: singular pivot at index " + std::to_string(singular));
+  }
+  NNB_TRY(o.finish(s));
+  return sync(s);
+}
+
+int nnb_direct_inverse_d(const double* M, int64_t n, double* out, int32_t* pivot_index, void* stream) {
+  return direct_inverse_call(M, n, 0, out, pivot_index, stream);
+}
+
+int nnb_direct_inverse_z(const double* M, int64_t n, double* out, int32_t* pivot_index, void* stream) {
+  return direct_inverse_call(M, n, 1, out, pivot_index, stream);
+}
+
 static int transpose_call(const double* M, int64_t rows, int64_t cols, int cplx, double* out, void* stream) {
   NNB_TRY(require_device());
   if (rows < 0 || cols < 0) return fail(NNB_ERR_SHAPE, "conjugate_transpose: negative shape");

@@ -114,6 +114,9 @@ int fill_identity(double* X, int64_t n, int64_t ld, double val, cudaStream_t s);
 // generators.cu: Householder Q (device in/out, cplx: interleaved), random_spd / random_conditioned_complex
 int householder_q(const double* A, int64_t n, int cplx, double* Q, cudaStream_t s);
 int random_spd_dev(const double* G, const double* lam, int64_t n, double* W, cudaStream_t s);
+// Gauss–Jordan inverse (direct_inverse_oracle); *singular_col = first singular pivot column or −1
+int direct_inverse(const double* M, int64_t n, int cplx, double pivot_floor, double* inv, int* singular_col,
+                   cudaStream_t s);
 int random_conditioned_dev(const double* GU, const double* GV, const double* sigma, int64_t n, double* A,
                            cudaStream_t s);
 // out (cols×rows) = Mᵀ (cplx = 0) or Mᴴ of interleaved complex M (cplx = 1)

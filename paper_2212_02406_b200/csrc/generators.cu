@@ -306,4 +306,180 @@ int random_conditioned_dev(const double* GU, const double* GV, const double* sig
   return 0;
 }
 
+
+// ---------------------------------------------------------------------------
+// Gauss–Jordan inverse with partial pivoting (nn::direct_inverse_oracle,
+// proj/src/kernels.cpp:317-350): the small-scale ground truth.  Columns run in
+// order; per column one block finds the pivot (largest |a(r,col)|, the first
+// on ties as the reference's strict `>`), then row swap + pivot-row scaling and
+// the elimination run element-parallel — each element still sees the
+// reference's single rounded operation, so real inputs give BIT-IDENTICAL
+// inverses.  Complex |z| and division follow hypot / Smith (a few ulps).
+namespace {
+
+template <typename T>
+__device__ __forceinline__ double mag(T v) {
+  if constexpr (sizeof(T) == 16) return hypot(v.x, v.y);
+  else return fabs(v);
+}
+
+// pivot search over rows [col, n) of column col; state[0] = pivot row, scal[0] = d (as doubles)
+template <typename T>
+__global__ void gj_pivot_kernel(const T* __restrict__ a, int64_t n, int64_t col, double floor_,
+                                long long* __restrict__ piv, T* __restrict__ d, int* __restrict__ singular) {
+  __shared__ double best[1024];
+  __shared__ long long who[1024];
+  double b = -1.0;
+  long long w = col;
+  for (int64_t r = col + threadIdx.x; r < n; r += blockDim.x) {
+    const double c = mag(a[r * n + col]);
+    if (c > b) {  // strided scan: the first (smallest r) maximum of this thread's rows
+      b = c;
+      w = r;
+    }
+  }
+  best[threadIdx.x] = b;
+  who[threadIdx.x] = w;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double ob = best[threadIdx.x + s];
+      const long long ow = who[threadIdx.x + s];
+      if (ob > best[threadIdx.x] || (ob == best[threadIdx.x] && ow < who[threadIdx.x])) {
+        best[threadIdx.x] = ob;
+        who[threadIdx.x] = ow;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *piv = who[0];
+    *d = a[who[0] * n + col];
+    if (!(best[0] > floor_) && *singular < 0) *singular = static_cast<int>(col);
+  }
+}
+
+__device__ __forceinline__ double gj_div(double x, double d) { return __ddiv_rn(x, d); }
+__device__ __forceinline__ double2 gj_div(double2 x, double2 d) {  // Smith, as libgcc's __divdc3
+  if (fabs(d.x) >= fabs(d.y)) {
+    const double r = __ddiv_rn(d.y, d.x), den = __dadd_rn(__dmul_rn(d.y, r), d.x);
+    return make_double2(__ddiv_rn(__dadd_rn(__dmul_rn(x.y, r), x.x), den),
+                        __ddiv_rn(__dsub_rn(x.y, __dmul_rn(x.x, r)), den));
+  }
+  const double r = __ddiv_rn(d.x, d.y), den = __dadd_rn(__dmul_rn(d.x, r), d.y);
+  return make_double2(__ddiv_rn(__dadd_rn(__dmul_rn(x.x, r), x.y), den),
+                      __ddiv_rn(__dsub_rn(__dmul_rn(x.y, r), x.x), den));
+}
+__device__ __forceinline__ double gj_fms(double a, double f, double x) { return __dsub_rn(a, __dmul_rn(f, x)); }
+__device__ __forceinline__ double2 gj_fms(double2 a, double2 f, double2 x) {
+  const double2 p = cmul(f, x);
+  return make_double2(__dsub_rn(a.x, p.x), __dsub_rn(a.y, p.y));
+}
+template <typename T>
+__device__ __forceinline__ bool is_zero(T v) {
+  if constexpr (sizeof(T) == 16) return v.x == 0.0 && v.y == 0.0;
+  else return v == 0.0;
+}
+
+// swap rows col and piv, scale the pivot row by 1/d
+template <typename T>
+__global__ void gj_swap_scale_kernel(T* __restrict__ a, T* __restrict__ inv, int64_t n, int64_t col,
+                                     const long long* __restrict__ piv, const T* __restrict__ d,
+                                     const int* __restrict__ singular) {
+  if (*singular >= 0) return;
+  const long long p = *piv;
+  const T dv = *d;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const T pa = a[p * n + j], pi = inv[p * n + j];
+    if (p != col) {
+      a[p * n + j] = a[col * n + j];
+      inv[p * n + j] = inv[col * n + j];
+    }
+    a[col * n + j] = gj_div(pa, dv);
+    inv[col * n + j] = gj_div(pi, dv);
+  }
+}
+
+template <typename T>
+__global__ void gj_save_column_kernel(const T* __restrict__ a, int64_t n, int64_t col, const int* __restrict__ singular,
+                                      T* __restrict__ fcol) {
+  if (*singular >= 0) return;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    fcol[r] = a[r * n + col];
+}
+
+template <typename T>
+__global__ void gj_eliminate_kernel(T* __restrict__ a, T* __restrict__ inv, int64_t n, int64_t col,
+                                    const T* __restrict__ fcol, const int* __restrict__ singular) {
+  if (*singular >= 0) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / n, j = e % n;
+    if (r == col) continue;
+    const T f = fcol[r];
+    if (is_zero(f)) continue;  // the reference skips zero multipliers
+    a[e] = gj_fms(a[e], f, a[col * n + j]);
+    inv[e] = gj_fms(inv[e], f, inv[col * n + j]);
+  }
+}
+
+template <typename T>
+__global__ void gj_identity_kernel(T* q, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    if constexpr (sizeof(T) == 16) q[e] = make_double2((e / n == e % n) ? 1.0 : 0.0, 0.0);
+    else q[e] = (e / n == e % n) ? 1.0 : 0.0;
+  }
+}
+
+template <typename T>
+__global__ void gj_nonfinite_kernel(const T* __restrict__ q, int64_t n, int* __restrict__ count) {
+  int bad = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    if constexpr (sizeof(T) == 16) bad += !(isfinite(q[e].x) && isfinite(q[e].y));
+    else bad += !isfinite(q[e]);
+  }
+  if (bad) atomicAdd(count, bad);
+}
+
+template <typename T>
+int direct_inverse_dev(const T* m, int64_t n, double pivot_floor, T* inv, int* singular_col, cudaStream_t s) {
+  DevBuf work;
+  NNB_TRY(work.alloc(sizeof(T) * (size_t)(n * n + n + 2) + 64, s));
+  T* a = work.as<T>();
+  T* fcol = a + n * n;
+  T* d = fcol + n;
+  long long* piv = reinterpret_cast<long long*>(d + 1);
+  int* singular = reinterpret_cast<int*>(piv + 1);
+  int* nonfinite = singular + 1;
+  NNB_CUDA(cudaMemcpyAsync(a, m, sizeof(T) * n * n, cudaMemcpyDeviceToDevice, s));
+  NNB_CUDA(cudaMemsetAsync(singular, 0xff, sizeof(int), s));  // -1
+  NNB_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), s));
+  gj_identity_kernel<T><<<grid_n2(n), 256, 0, s>>>(inv, n);
+  const unsigned rows_grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 4)));
+  for (int64_t col = 0; col < n; ++col) {
+    gj_pivot_kernel<T><<<1, 1024, 0, s>>>(a, n, col, pivot_floor, piv, d, singular);
+    gj_swap_scale_kernel<T><<<rows_grid, 256, 0, s>>>(a, inv, n, col, piv, d, singular);
+    gj_save_column_kernel<T><<<rows_grid, 256, 0, s>>>(a, n, col, singular, fcol);
+    gj_eliminate_kernel<T><<<grid_n2(n), 256, 0, s>>>(a, inv, n, col, fcol, singular);
+  }
+  gj_nonfinite_kernel<T><<<grid_n2(n), 256, 0, s>>>(inv, n, nonfinite);
+  count_launch(4 * n + 2);
+  NNB_CUDA(cudaGetLastError());
+  int h[2];
+  NNB_CUDA(cudaMemcpyAsync(h, singular, sizeof(h), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  *singular_col = h[0];
+  if (h[0] < 0 && h[1]) return fail(2, "direct_inverse_oracle: produced a non-finite entry");
+  return 0;
+}
+
+}  // namespace
+
+int direct_inverse(const double* M, int64_t n, int cplx, double pivot_floor, double* inv, int* singular_col,
+                   cudaStream_t s) {
+  if (cplx)
+    return direct_inverse_dev<double2>(reinterpret_cast<const double2*>(M), n, pivot_floor,
+                                       reinterpret_cast<double2*>(inv), singular_col, s);
+  return direct_inverse_dev<double>(M, n, pivot_floor, inv, singular_col, s);
+}
+
 }  // namespace nnb

@@ -8,8 +8,8 @@
 // synthesises the reference's operation counts and keeps the host-side
 // bookkeeping (reports, nest estimates, order fits).
 //
-// Out of scope (not declared; link the reference's nncore for them):
-// direct_inverse_oracle and the cost model.
+// Out of scope (not declared; link the reference's nncore for it): the exact
+// rational cost model (analytic only).
 #pragma once
 
 #include <atomic>
@@ -217,6 +217,10 @@ DenseMatrix scale(const DenseMatrix& m, Scalar factor, OpCounter* counter = null
 DenseMatrix identity_minus(const DenseMatrix& m, OpCounter* counter = nullptr);
 DenseMatrix plus_identity(const DenseMatrix& m, OpCounter* counter = nullptr);
 DenseMatrix conjugate_transpose(const DenseMatrix& m, OpCounter* counter = nullptr);
+/// Gauss–Jordan inverse with partial pivoting on the device (kernels.cpp:317-350):
+/// the small-scale ground truth, bit-identical for real input; SingularMatrixError
+/// with the pivot index when a pivot is <= 1e-13·||m||_F.
+DenseMatrix direct_inverse_oracle(const DenseMatrix& m);
 /// m·x on the device (kernels.cpp:164-173); untallied.
 std::vector<Scalar> matvec(const DenseMatrix& m, const std::vector<Scalar>& x);
 Scalar trace(const DenseMatrix& m);

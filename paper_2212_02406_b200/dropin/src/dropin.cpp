@@ -493,6 +493,26 @@ double contraction_check(const DenseMatrix& phi, const DenseMatrix& w_tilde) {
   return spectral_norm_estimate(identity_minus(matmul(phi, w_tilde))).value;
 }
 
+DenseMatrix direct_inverse_oracle(const DenseMatrix& m) {
+  if (!m.square()) throw ShapeError("direct_inverse_oracle: matrix must be square");
+  const std::size_t n = m.rows();
+  if (real_valued(m)) {
+    const auto r = real_part(m);
+    std::vector<double> out(n * n);
+    int32_t piv = -1;
+    const int st = nnb_direct_inverse_d(r.data(), (int64_t)n, out.data(), &piv, nullptr);
+    if (st == NNB_ERR_SINGULAR) throw SingularMatrixError(nnb_last_error(), static_cast<std::size_t>(piv));
+    check(st, "direct_inverse_oracle");
+    return from_real(n, n, out);
+  }
+  DenseMatrix out(n, n);
+  int32_t piv = -1;
+  const int st = nnb_direct_inverse_z(zp(m), (int64_t)n, zp(out), &piv, nullptr);
+  if (st == NNB_ERR_SINGULAR) throw SingularMatrixError(nnb_last_error(), static_cast<std::size_t>(piv));
+  check(st, "direct_inverse_oracle");
+  return out;
+}
+
 std::vector<Scalar> matvec(const DenseMatrix& m, const std::vector<Scalar>& x) {
   if (m.cols() != x.size()) throw ShapeError("matvec: dimension mismatch");
   return matmul(m, DenseMatrix(x.size(), 1, x)).data();

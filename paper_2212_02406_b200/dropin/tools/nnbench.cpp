@@ -6,16 +6,15 @@
 //   nnbench gen-matrix --N n --out f.mtx [--cond c] [--seed s] [--kind spd|complex|sparse-spd] [--density d]
 //   nnbench invert IN.mtx [--method nn|newton|chebyshev|ns|nn-explicit|factorized-ns|cns] [--depth|-L L]
 //                  [--nests|-i k] [--order|--gamma g] [--tol t] [--theta trace|power:k] [--seed s] [--out X.mtx]
-//                  [--report r.json]
+//                  [--report r.json] [--estimate-kappa]
 //   nnbench solve --matrix|-A A.mtx --rhs|-b B.mtx [--method nn|sparse-factorized] [--depth|-L L]
 //                 [--nests|-i k] [--order|--gamma g] [--tol t] [--out x.mtx] [--report r.json]
 //   nnbench bench --methods m1,m2 [--N n1,n2] [--cond c1,c2] [--depths L1,L2] [--nests|-i k] [--tol t]
 //                 [--seed s] [--out grid.csv]
 //
 // Exit codes: 0 success / tolerance reached, 2 nest budget exhausted, 1 input
-// or validation error.  Not provided (their reference routines are out of
-// scope): analyze-cost (cost model) and --estimate-kappa
-// (direct_inverse_oracle).
+// or validation error.  Not provided: analyze-cost (the exact-rational cost
+// model is out of scope).
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -162,10 +161,13 @@ int gen_matrix(const Options& o) {
 // ---------------------------------------------------------------- invert
 int invert(const Options& o) {
   if (o.positional().size() != 1) throw UsageError("invert takes exactly one input matrix");
-  if (o.has("--estimate-kappa"))
-    throw DomainError("--estimate-kappa needs direct_inverse_oracle, which the B200 build does not provide");
   const DenseMatrix w = mm::read_dense_file(o.positional()[0]);
   if (!w.square()) throw ShapeError("invert: input matrix must be square");
+  std::optional<double> kappa;
+  if (o.has("--estimate-kappa")) {  // ||W||_2 · ||W^-1||_2 with the Gauss–Jordan oracle, as the reference
+    if (w.rows() > 128) throw DomainError("--estimate-kappa is limited to N <= 128");
+    kappa = spectral_norm_estimate(w).value * spectral_norm_estimate(direct_inverse_oracle(w)).value;
+  }
   const std::string method = o.str("--method", "nn");
   const Normalization norm =
       normalization(w, o.str("--theta", "trace"), static_cast<std::uint64_t>(o.integer("--seed", 1)));
@@ -173,7 +175,9 @@ int invert(const Options& o) {
   config.depth_L = static_cast<std::size_t>(o.integer("--depth", 2));
   config.tol = o.num("--tol", 1e-10);
   const long long nests = o.integer("--nests", 0), order = o.integer("--order", -1);
-  config.max_nests = nests > 0 ? static_cast<std::size_t>(nests) : 64;
+  config.max_nests = nests > 0 ? static_cast<std::size_t>(nests)
+                     : kappa   ? estimate_nests(*kappa, std::max<std::size_t>(config.depth_L, 1))
+                               : 64;
 
   OpCounter counter;
   DenseMatrix inverse;
@@ -209,6 +213,7 @@ int invert(const Options& o) {
     report.n3_multiplies = counter.n3_multiplies();
     report.n2_ops = counter.n2_ops();
   }
+  report.kappa_used = kappa;
   if (o.has("--out")) mm::write_dense_file(o.str("--out"), inverse);
   if (o.has("--report")) mm::write_file_atomic(o.str("--report"), report_to_json(report));
   const double final_eps = report.history.empty() ? inverse_quality(w, inverse) : report.history.back().second;

@@ -477,8 +477,18 @@ static void power_normalization_tests() {
   CHECK_THROWS(theta_power(DenseMatrix::identity(3), 0, 1), DomainError);
 
   const DenseMatrix wt = DenseMatrix::diagonal({Scalar{0.25, 0}, Scalar{0.75, 0}});
-  const DenseMatrix inv = DenseMatrix::diagonal({Scalar{4.0, 0}, Scalar{4.0 / 3.0, 0}});
+  const DenseMatrix inv = direct_inverse_oracle(wt);
+  CHECK(inv(0, 0) == (Scalar{4.0, 0}) && std::fabs(inv(1, 1).real() - 4.0 / 3.0) < 1e-15);
   CHECK(contraction_check(inv, wt) < 1e-9);
+  DenseMatrix sing(3, 3);
+  sing(0, 0) = Scalar{1, 0};
+  bool threw = false;
+  try {
+    direct_inverse_oracle(sing);
+  } catch (const SingularMatrixError& e) {
+    threw = e.pivot_index == 1;
+  }
+  CHECK(threw);
   CHECK(std::fabs(contraction_check(DenseMatrix::identity(2), wt) - 0.75) < 1e-9);
   CHECK(std::fabs(contraction_check(DenseMatrix(2, 2), wt) - 1.0) < 1e-9);
 

@@ -98,6 +98,11 @@ def test_invert_exit_codes_and_methods(tmp_path):
     code, so, err = nnbench("invert", w2, "--theta", "power:4", "--seed", 5, "--tol", 1e-10)
     assert code == 0 and "stopped=tolerance" in so, err  # theta_power normalisation
     assert nnbench("invert", w2, "--theta", "power:0")[0] == 1
+    # --estimate-kappa: ||W||·||W⁻¹|| through the Gauss–Jordan oracle sets the nest budget
+    # (estimate_nests(2, 2) = 1 nest, too few under theta = 1/Tr(W): exit 2, as the reference)
+    code, so, err = nnbench("invert", w2, "--estimate-kappa", "--report", tmp_path / "k.json")
+    rep = json.loads((tmp_path / "k.json").read_text())
+    assert abs(rep["kappa_used"] - 2.0) < 1e-6 and rep["config"]["max_nests"] == 1 and code == 2, (so, err)
     rect = tmp_path / "rect.mtx"
     rect.write_text("%%MatrixMarket matrix array real general\n2 3\n1\n2\n3\n4\n5\n6\n")
     code, _, err = nnbench("invert", rect)

@@ -556,3 +556,26 @@ def test_c4_full_size_nest_cubes_the_residual():
     assert eps1 < eps0
     assert abs(eps1 - expect) <= 1e-9 * expect  # rounding of the cubed residual
     assert rep.products == 4
+
+
+# ----------------------------------------------------------------- direct inverse oracle
+@pytest.mark.parametrize("n,seed", [(1, 1), (5, 2), (64, 3), (200, 4)])
+def test_direct_inverse_bitexact(ref, n, seed):
+    """Gauss–Jordan with partial pivoting on the device: bit-identical to the reference
+    (kernels.cpp:317-350) for real input, a few ulps for complex."""
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((n, n)) + np.eye(n) * 0.1
+    assert np.array_equal(nnb.direct_inverse_oracle(a), ref.direct_inverse(a).real)
+    z = a + 1j * rng.standard_normal((n, n))
+    assert rel_frob(nnb.direct_inverse_oracle(z), ref.direct_inverse(z)) < 1e-13
+
+
+def test_direct_inverse_singular_pivot_index(ref):
+    from oracle import OracleError
+
+    a = np.arange(16.0).reshape(4, 4)  # rank 2
+    with pytest.raises(OracleError) as er:
+        ref.direct_inverse(a)
+    with pytest.raises(nnb.SingularMatrixError) as eg:
+        nnb.direct_inverse_oracle(a)
+    assert eg.value.pivot_index == er.value.index == 2
