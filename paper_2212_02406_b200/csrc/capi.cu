@@ -308,6 +308,31 @@ int nnb_gemm_z(const double* A, const double* B, double* C, int64_t m, int64_t k
   NNB_TRY(red.init(max_tiles_for(m, n), s));
   DevBuf nf;
   NNB_TRY(nf.alloc(2 * sizeof(int), s));
+  NNB_CUDA(cudaMemsetAsync(nf.p, 0, 2 * sizeof(int), s));
+  if (arith() != 1 && k > 0) {  // 3M on DMMA (zgemm3m); the exact mode keeps the 4M form
+    ZGemm z;
+    z.M = m;
+    z.N = n;
+    z.K = k;
+    z.Ar = a.re;
+    z.Ai = a.im;
+    z.lda = a.ld;
+    z.Br = b.re;
+    z.Bi = b.im;
+    z.ldb = b.ld;
+    z.Cr = c.re;
+    z.Ci = c.im;
+    z.ldc = c.ld;
+    z.ss_out = nullptr;
+    z.nf_out = nf.as<int>();
+    NNB_TRY(zgemm3m(z, &red, s));
+    NNB_TRY(c.store(C, s));
+    int h = 0;
+    NNB_CUDA(cudaMemcpyAsync(&h, nf.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    NNB_TRY(sync(s));
+    if (h) return fail(NNB_ERR_DOMAIN, "matmul: produced a non-finite entry");
+    return 0;
+  }
   auto run = [&](const double* x, int64_t ldx, const double* y, int64_t ldy, double alpha,
                  const double* d, double* out, int* nfo) {
     GemmOp op;

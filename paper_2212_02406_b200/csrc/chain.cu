@@ -82,7 +82,30 @@ int product(Ctx& c, const Plane& A, const Plane& B, double alpha, const Plane* D
     return gemm(op, nf_out ? &c.red : nullptr, c.s);
   }
   const bool red = nf_out != nullptr;
-  // real plane: Cr = alpha Ar·Br + beta Dr + gamma I ; Cr += -alpha Ai·Bi
+  if (arith() != 1) {  // 3M: three DMMA GEMMs (zgemm3m); the 4M form below is the exact-mode path
+    ZGemm z;
+    z.M = z.N = z.K = c.n;
+    z.Ar = A.re;
+    z.Ai = A.im;
+    z.lda = c.ld;
+    z.Br = B.re;
+    z.Bi = B.im;
+    z.ldb = c.ld;
+    z.alpha = alpha;
+    z.beta = beta;
+    z.gamma = gamma;
+    z.Dr = D ? D->re : nullptr;
+    z.Di = D ? D->im : nullptr;
+    z.ldd = c.ld;
+    z.Cr = C.re;
+    z.Ci = C.im;
+    z.ldc = c.ld;
+    z.nf_out = nf_out;
+    z.eps_out = eps_out;
+    z.eps_scale = eps_scale;
+    return zgemm3m(z, red ? &c.red : nullptr, c.s);
+  }
+  // 4M, real plane: Cr = alpha Ar·Br + beta Dr + gamma I ; Cr += -alpha Ai·Bi
   GemmOp o1 = op;
   o1.A = A.re; o1.B = B.re;
   o1.ep.alpha = alpha; o1.ep.D = D ? D->re : nullptr; o1.ep.ldd = c.ld; o1.ep.beta = beta;

@@ -221,8 +221,11 @@ int gemm(GemmOp op, RedWs* red, cudaStream_t s) {
   if (op.M > INT32_MAX || op.N > INT32_MAX || op.K > INT32_MAX)
     return fail(1, "gemm: dimension exceeds int32");
   if ((reinterpret_cast<uintptr_t>(op.ep.C) & 15) || (op.ep.ldc & 1) ||
-      (op.ep.D && ((reinterpret_cast<uintptr_t>(op.ep.D) & 15) || (op.ep.ldd & 1))))
+      (op.ep.D && ((reinterpret_cast<uintptr_t>(op.ep.D) & 15) || (op.ep.ldd & 1))) ||
+      (op.ep.C2 && ((reinterpret_cast<uintptr_t>(op.ep.C2) & 15) || (op.ep.ldc2 & 1))) ||
+      (op.ep.D2 && ((reinterpret_cast<uintptr_t>(op.ep.D2) & 15) || (op.ep.ldd2 & 1))))
     return fail(7, "gemm: epilogue operands need 16B alignment and even leading dimensions");
+  if (op.ep.C2 && arith() == 1) return fail(7, "gemm: the dual-output epilogue has no reference-exact form");
   if (red) {
     if (red->capacity < max_tiles_for(op.M, op.N)) return fail(7, "gemm: reduction workspace too small");
     op.ep.ss_partial = red->ss_partial;
@@ -239,6 +242,69 @@ int gemm(GemmOp op, RedWs* red, cudaStream_t s) {
   if (op.b_kmajor) return use_big(op.M, op.N) ? launch_cfg<BigCfgT>(op, s) : launch_cfg<SmallCfgT>(op, s);
   if (use_tiny(op.M, op.N)) return launch_cfg<TinyCfg>(op, s);
   return use_big(op.M, op.N) ? launch_cfg<BigCfg>(op, s) : launch_cfg<SmallCfg>(op, s);
+}
+
+// Complex C = α·A·B + β·D + γ·I(diag_offset) on planar operands, 3M (Gauss):
+//   SA = Ar + Ai, SB = Br + Bi                       (two elementwise passes)
+//   Ci  = α·SA·SB + β·Di
+//   Cr  = α·Ar·Br + β·Dr + γ·I,   Ci −= α·Ar·Br      (one GEMM, dual epilogue)
+//   Cr −= α·Ai·Bi,                Ci −= α·Ai·Bi      (one GEMM, dual epilogue + Σ|C|²)
+// = α(ArBr − AiBi) + β·Dr + γI  and  α(SA·SB − ArBr − AiBi) + β·Di: three DMMA
+// GEMMs instead of four; the last epilogue reduces |Cr|² + |Ci|² (eps, non-finite).
+int zgemm3m(const ZGemm& z, RedWs* red, cudaStream_t s) {
+  const int64_t M = z.M, N = z.N, K = z.K;
+  if (M <= 0 || N <= 0) return 0;
+  const int64_t lsa = (K + 7) / 8 * 8, lsb = (N + 7) / 8 * 8;
+  DevBuf sums;
+  NNB_TRY(sums.alloc(sizeof(double) * std::max<int64_t>(1, M * lsa + K * lsb), s));
+  double* sa = sums.as<double>();
+  double* sb = sa + M * lsa;
+  NNB_TRY(axpby(1.0, z.Ar, z.lda, 1.0, z.Ai, z.lda, 0.0, 0, sa, lsa, M, K, s));
+  NNB_TRY(axpby(1.0, z.Br, z.ldb, 1.0, z.Bi, z.ldb, 0.0, 0, sb, lsb, K, N, s));
+  GemmOp g1;
+  g1.A = sa;
+  g1.lda = lsa;
+  g1.B = sb;
+  g1.ldb = lsb;
+  g1.M = M;
+  g1.N = N;
+  g1.K = K;
+  g1.ep.alpha = z.alpha;
+  g1.ep.D = z.Di;
+  g1.ep.ldd = z.ldd;
+  g1.ep.beta = z.beta;
+  g1.ep.C = z.Ci;
+  g1.ep.ldc = z.ldc;
+  NNB_TRY(gemm(g1, nullptr, s));
+  GemmOp g2 = g1;
+  g2.A = z.Ar;
+  g2.lda = z.lda;
+  g2.B = z.Br;
+  g2.ldb = z.ldb;
+  g2.ep.D = z.Dr;
+  g2.ep.C = z.Cr;
+  g2.ep.gamma = z.gamma;
+  g2.ep.diag_offset = z.diag_offset;
+  g2.ep.C2 = z.Ci;
+  g2.ep.ldc2 = z.ldc;
+  g2.ep.D2 = z.Ci;
+  g2.ep.ldd2 = z.ldc;
+  g2.ep.alpha2 = -z.alpha;
+  g2.ep.beta2 = 1.0;
+  NNB_TRY(gemm(g2, nullptr, s));
+  GemmOp g3 = g2;
+  g3.A = z.Ai;
+  g3.B = z.Bi;
+  g3.ep.alpha = -z.alpha;
+  g3.ep.D = z.Cr;
+  g3.ep.ldd = z.ldc;
+  g3.ep.beta = 1.0;
+  g3.ep.gamma = 0.0;
+  g3.ep.ss_out = z.ss_out;
+  g3.ep.nf_out = z.nf_out;
+  g3.ep.eps_out = z.eps_out;
+  g3.ep.eps_scale = z.eps_scale;
+  return gemm(g3, z.nf_out ? red : nullptr, s);
 }
 
 // ============================ auxiliary kernels ============================

@@ -96,6 +96,26 @@ int gemm_exact(const GemmOp& op, cudaStream_t s);
 // reduction is wired to it (ep.ss_out / nf_out / eps_out chosen by caller).
 int gemm(GemmOp op, RedWs* red, cudaStream_t s);
 
+// Complex product on planar operands, 3M on the DMMA GEMM (engine.cu).
+struct ZGemm {
+  int64_t M = 0, N = 0, K = 0;
+  const double *Ar = nullptr, *Ai = nullptr;
+  int64_t lda = 0;
+  const double *Br = nullptr, *Bi = nullptr;
+  int64_t ldb = 0;
+  double alpha = 1.0, beta = 0.0, gamma = 0.0;
+  const double *Dr = nullptr, *Di = nullptr;  // may alias Cr / Ci
+  int64_t ldd = 0;
+  int64_t diag_offset = 0;
+  double *Cr = nullptr, *Ci = nullptr;
+  int64_t ldc = 0;
+  double* ss_out = nullptr;   // Σ |C|² (with nf_out and a reduction workspace)
+  int* nf_out = nullptr;
+  double* eps_out = nullptr;  // sqrt(Σ|C|²)·eps_scale
+  double eps_scale = 1.0;
+};
+int zgemm3m(const ZGemm& z, RedWs* red, cudaStream_t s);
+
 // ---- auxiliary kernels ----------------------------------------------------------
 int axpby(double alpha, const double* A, int64_t lda, double beta, const double* B, int64_t ldb,
           double gamma, int64_t diag_offset, double* out, int64_t ldo, int64_t rows, int64_t cols,

@@ -34,6 +34,14 @@ struct GemmEpilogue {
   int64_t diag_offset = 0;
   double* C = nullptr;
   int64_t ldc = 0;
+  // optional second output from the same product P (3M complex products):
+  // C2 = alpha2·P + beta2·D2 (D2 may alias C2); the Σ C² reduction then covers
+  // both outputs
+  double* C2 = nullptr;
+  int64_t ldc2 = 0;
+  const double* D2 = nullptr;
+  int64_t ldd2 = 0;
+  double alpha2 = 0.0, beta2 = 0.0;
   // Σ C² / non-finite reduction (all nullable => skipped)
   double* ss_partial = nullptr;  // [num_tiles]
   int* nf_partial = nullptr;     // [num_tiles]
@@ -207,6 +215,34 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
         if (two) {
           ss = fma(v1, v1, ss);
           nf += !isfinite(v1);
+        }
+      }
+      if (ep.C2) {
+        double w0 = ep.alpha2 * acc[i][j][0];
+        double w1 = ep.alpha2 * acc[i][j][1];
+        if (ep.D2) {
+          const double* dp = ep.D2 + (int64_t)r * ep.ldd2 + c;
+          if (two) {
+            const double2 d = *reinterpret_cast<const double2*>(dp);
+            w0 = fma(ep.beta2, d.x, w0);
+            w1 = fma(ep.beta2, d.y, w1);
+          } else {
+            w0 = fma(ep.beta2, dp[0], w0);
+          }
+        }
+        double* cp2 = ep.C2 + (int64_t)r * ep.ldc2 + c;
+        if (two) {
+          *reinterpret_cast<double2*>(cp2) = make_double2(w0, w1);
+        } else {
+          cp2[0] = w0;
+        }
+        if (want_red) {
+          ss = fma(w0, w0, ss);
+          nf += !isfinite(w0);
+          if (two) {
+            ss = fma(w1, w1, ss);
+            nf += !isfinite(w1);
+          }
         }
       }
     }
