@@ -89,6 +89,33 @@ struct ZAcc {
       }
     }
   }
+  // 3M only: seed the accumulators with s·(D + γ·I), s = −1 when NEG, as
+  // P1 = re, P2 = 0, P3 = re + im — the "+D" and "γI" then cost 2 DADD per
+  // element pair instead of 4 after the product, and the sign folds into
+  // epilogue_seeded's operand order (DADD shares the FP64 pipe with DMMA).
+  template <bool NEG>
+  __device__ __forceinline__ void seed(const SMat* D, double gamma, int g, int t) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int r = 8 * mt + g, c = 8 * nt + 2 * t;
+        double2 dr = make_double2(0.0, 0.0), di = make_double2(0.0, 0.0);
+        if (D) {
+          const int idx = swz(r, c);
+          dr = *reinterpret_cast<const double2*>(D->re + idx);
+          di = *reinterpret_cast<const double2*>(D->im + idx);
+        }
+        if (r == c) dr.x += gamma;
+        if (r == c + 1) dr.y += gamma;
+        double2 ds = D ? make_double2(dr.x + di.x, dr.y + di.y) : dr;
+        v[mt][nt][0][0] = NEG ? -dr.x : dr.x;
+        v[mt][nt][0][1] = NEG ? -dr.y : dr.y;
+        v[mt][nt][1][0] = v[mt][nt][1][1] = 0.0;
+        v[mt][nt][2][0] = NEG ? -ds.x : ds.x;
+        v[mt][nt][2][1] = NEG ? -ds.y : ds.y;
+      }
+  }
   __device__ __forceinline__ double re(int mt, int nt, int i) const {
     if constexpr (M3) return v[mt][nt][0][i] - v[mt][nt][1][i];
     else return v[mt][nt][0][i];
@@ -163,6 +190,32 @@ __device__ __forceinline__ void epilogue(const ZAcc<M3>& acc, double alpha, cons
       }
       if (r == c) vr.x += gamma;
       if (r == c + 1) vr.y += gamma;
+      *reinterpret_cast<double2*>(out.re + idx) = vr;
+      *reinterpret_cast<double2*>(out.im + idx) = vi;
+    }
+  __syncwarp();
+}
+
+// 3M with seeded accumulators: out = s·acc (s = −1 when NEG), stored to shared `out`.
+template <bool NEG>
+__device__ __forceinline__ void epilogue_seeded(const ZAcc<true>& acc, const SMat& out, int g, int t) {
+  __syncwarp();  // every lane finished reading operands that `out` may overwrite
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int idx = swz(8 * mt + g, 8 * nt + 2 * t);
+      double2 vr, vi;
+      const double* p0 = acc.v[mt][nt][0];
+      const double* p1 = acc.v[mt][nt][1];
+      const double* p2 = acc.v[mt][nt][2];
+      if (NEG) {
+        vr = make_double2(p1[0] - p0[0], p1[1] - p0[1]);
+        vi = make_double2((p0[0] + p1[0]) - p2[0], (p0[1] + p1[1]) - p2[1]);
+      } else {
+        vr = make_double2(p0[0] - p1[0], p0[1] - p1[1]);
+        vi = make_double2(p2[0] - (p0[0] + p1[0]), p2[1] - (p0[1] + p1[1]));
+      }
       *reinterpret_cast<double2*>(out.re + idx) = vr;
       *reinterpret_cast<double2*>(out.im + idx) = vi;
     }
@@ -261,17 +314,30 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
     if (!ns_mode) {
       // ---- Nested Neumann: `iters` nests of depth P ----
       for (int it = 0; it < iters; ++it) {
-        acc.zero();
-        zmma_sr(acc, X, areg, g, t);               // X·A
-        epilogue(acc, -1.0, nullptr, 1.0, Pm, g, t);  // P = I − X·A
         const SMat* v = &X;
+        if constexpr (M3) {
+          acc.template seed<true>(nullptr, 1.0, g, t);  // −I
+          zmma_sr(acc, X, areg, g, t);                  // −I + X·A
+          epilogue_seeded<true>(acc, Pm, g, t);         // P = I − X·A
 #pragma unroll
-        for (int j = 1; j <= P; ++j) {
+          for (int j = 1; j <= P; ++j) {
+            acc.template seed<false>(&X, 0.0, g, t);    // X
+            zmma_ss(acc, Pm, *v, g, t);                 // X + P·V
+            epilogue_seeded<false>(acc, (j == P) ? X : V, g, t);  // the last Horner step lands in X
+            v = &V;
+          }
+        } else {
           acc.zero();
-          zmma_ss(acc, Pm, *v, g, t);                 // P·V
-          const SMat& dst = (j == P) ? X : V;         // last Horner step lands in X
-          epilogue(acc, 1.0, &X, 0.0, dst, g, t);     // V = X + P·V
-          v = &V;
+          zmma_sr(acc, X, areg, g, t);                  // X·A
+          epilogue(acc, -1.0, nullptr, 1.0, Pm, g, t);  // P = I − X·A
+#pragma unroll
+          for (int j = 1; j <= P; ++j) {
+            acc.zero();
+            zmma_ss(acc, Pm, *v, g, t);                 // P·V
+            const SMat& dst = (j == P) ? X : V;         // last Horner step lands in X
+            epilogue(acc, 1.0, &X, 0.0, dst, g, t);     // V = X + P·V
+            v = &V;
+          }
         }
       }
       // final residual eps = ‖I − X·A‖_F / √n
@@ -393,18 +459,17 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
       X.im[swz(lane, lane)] = xi;
     }
     __syncwarp();
-    // ---- Nested Neumann inversion ----
+    // ---- Nested Neumann inversion (seeded 3M products, as batched_z16_kernel) ----
     for (int it = 0; it < iters; ++it) {
-      acc.zero();
+      acc.template seed<true>(nullptr, 1.0, g, t);
       zmma_sr(acc, X, areg, g, t);
-      epilogue(acc, -1.0, nullptr, 1.0, Pm, g, t);
+      epilogue_seeded<true>(acc, Pm, g, t);  // P = I − X·A
       const SMat* v = &X;
 #pragma unroll
       for (int j = 1; j <= P; ++j) {
-        acc.zero();
+        acc.template seed<false>(&X, 0.0, g, t);
         zmma_ss(acc, Pm, *v, g, t);
-        const SMat& dst = (j == P) ? X : V;
-        epilogue(acc, 1.0, &X, 0.0, dst, g, t);
+        epilogue_seeded<false>(acc, (j == P) ? X : V, g, t);  // V = X + P·V
         v = &V;
       }
     }
