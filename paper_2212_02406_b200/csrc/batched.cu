@@ -9,11 +9,10 @@
 //     (PREFETCH), hiding the HBM latency behind ~13k cycles of DMMA work;
 //   * X0 = diag(A)^-1 (Jacobi) is formed in shared memory;
 //   * every iterate (X, P, V) stays in per-warp shared memory, planar re/im,
-//     16×16 doubles with the XOR swizzle  (r, c) -> r*16 + (c ^ 4*(r&3)),
-//     which makes both the A-operand (row=g, col=t) and the B-operand
-//     (row=t, col=g) fragment loads of mma.m8n8k4 conflict-free (2
-//     wavefronts per 32 doubles) and keeps the epilogue's double2 stores
-//     at the 4-wavefront minimum;
+//     16×16 doubles with an XOR swizzle (swz below) that makes both the
+//     A-operand (row=g, col=t) and the B-operand (row=t, col=g) fragment
+//     loads of mma.m8n8k4 conflict-free (2 wavefronts per 32 doubles) and
+//     keeps the epilogue's double2 stores at the 4-wavefront minimum;
 //   * each complex 16×16×16 product runs on DMMA.8x8x4 either as 4M
 //     (re·re − im·im, re·im + im·re: 64 DMMA) or as 3M (Gauss:
 //     P1 = re·re, P2 = im·im, P3 = (re+im)·(re+im); re = P1 − P2,
@@ -38,7 +37,12 @@ constexpr int kMat = kN * kN;  // doubles per plane
 constexpr int kWarpsPerCta = 4;
 constexpr int kThreads = kWarpsPerCta * 32;
 
-__device__ __forceinline__ int swz(int r, int c) { return r * kN + (c ^ (4 * (r & 3))); }
+// (r, c) -> 16r + (c ^ key(r)), key = 4·(r bits 0 and 1 swapped) ∈ {0, 8, 4, 12}:
+// conflict-free for the m8n8k4 A- and B-fragment loads (2 wavefronts per 32
+// doubles) and for the epilogue's double2 stores / seed loads (4 wavefronts),
+// because rows 2q and 2q+1 differ in key bit 3 (ncu: the plain 4·(r&3) key
+// doubled those 16-byte accesses).
+__device__ __forceinline__ int swz(int r, int c) { return r * kN + (c ^ (4 * (((r & 1) << 1) | ((r >> 1) & 1)))); }
 
 struct SMat {
   double* re;
