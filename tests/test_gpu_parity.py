@@ -579,3 +579,19 @@ def test_direct_inverse_singular_pivot_index(ref):
     with pytest.raises(nnb.SingularMatrixError) as eg:
         nnb.direct_inverse_oracle(a)
     assert eg.value.pivot_index == er.value.index == 2
+
+
+@pytest.mark.parametrize("n,p", [(333, 2), (97, 3)])
+def test_chain_odd_sizes_vs_reference(ref, n, p):
+    """Sizes off the 8-element padding and the 32/64/128 tile grids: padded leading
+    dimensions, TMA edge tiles and the masked epilogue against the reference."""
+    a = W.spd_conditioned(n, 50.0, seed=n)
+    x0 = W.x0_transpose_norm(a)
+    xr, hr, ir, _ = ref.chain(a, x0, p, 40, tol=1e-12)
+    for order in (nnb.ORDER_REFERENCE, nnb.ORDER_NORTHSTAR):
+        x, rep = nnb.nn_chain(a, x0, p=p, max_iters=40, tol=1e-12, order=order)
+        assert rep.iters == ir
+        eps_close([e for _, e in rep.history], hr)
+        assert rel_frob(x, xr.real) < TOL_X
+    z = (np.random.default_rng(n).standard_normal((n, n)) + 1j * np.random.default_rng(n + 1).standard_normal((n, n)))
+    assert rel_frob(nnb.matmul(z, z.T.copy()), ref.matmul(z, z.T.copy())[0]) < 1e-14  # 3M complex at an odd size
