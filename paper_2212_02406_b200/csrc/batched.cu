@@ -258,6 +258,70 @@ __device__ __forceinline__ void load_a_frags(const double2* __restrict__ As, int
     }
 }
 
+// Nest 0 from the diagonal (Jacobi) X0: P = I − X0·A is a row scaling of A and
+// V1 = X0 + P·X0 a column scaling of P, so both are elementwise on the lane's
+// A fragments (rows 4kb+t, columns 8nt+g) — the reference's products add only
+// zeros to x_r·a_rc and p_rc·x_c.  The remaining p − 1 Horner steps are
+// products: nest 0 costs p − 1 products instead of p + 1 (11 instead of 13 per
+// C2 system).  Returns with X = X1 and P holding I − X0·A.
+template <int P, bool M3>
+__device__ __forceinline__ void first_nest_diag(ZAcc<M3>& acc, const SMat& X, const SMat& Pm, const SMat& V,
+                                                const double (&areg)[2][4][2], int g, int t) {
+  double2 xr[4], xc[2], pv[2][4];
+#pragma unroll
+  for (int kb = 0; kb < 4; ++kb) {
+    const int r = 4 * kb + t;
+    xr[kb] = make_double2(X.re[swz(r, r)], X.im[swz(r, r)]);
+  }
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    const int c = 8 * nt + g;
+    xc[nt] = make_double2(X.re[swz(c, c)], X.im[swz(c, c)]);
+  }
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {
+      const int r = 4 * kb + t, c = 8 * nt + g, idx = swz(r, c);
+      const double ar = areg[nt][kb][0], ai = areg[nt][kb][1];
+      const double2 p = make_double2((r == c ? 1.0 : 0.0) - (xr[kb].x * ar - xr[kb].y * ai),
+                                     -(xr[kb].x * ai + xr[kb].y * ar));
+      Pm.re[idx] = p.x;
+      Pm.im[idx] = p.y;
+      pv[nt][kb] = p;
+    }
+  __syncwarp();  // every lane has read X0's diagonal before V1 (X itself when p = 1) is written
+  const SMat& d1 = (P == 1) ? X : V;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {
+      const int r = 4 * kb + t, c = 8 * nt + g, idx = swz(r, c);
+      const double2 p = pv[nt][kb];
+      double vr = p.x * xc[nt].x - p.y * xc[nt].y, vi = p.x * xc[nt].y + p.y * xc[nt].x;
+      if (r == c) {
+        vr += xr[kb].x;
+        vi += xr[kb].y;
+      }
+      d1.re[idx] = vr;
+      d1.im[idx] = vi;
+    }
+  __syncwarp();
+  const SMat* v = &V;
+#pragma unroll
+  for (int j = 2; j <= P; ++j) {  // V = X0 + P·V; the last step lands in X
+    if constexpr (M3) {
+      acc.template seed<false>(&X, 0.0, g, t);
+      zmma_ss(acc, Pm, *v, g, t);
+      epilogue_seeded<false>(acc, (j == P) ? X : V, g, t);
+    } else {
+      acc.zero();
+      zmma_ss(acc, Pm, *v, g, t);
+      epilogue(acc, 1.0, &X, 0.0, (j == P) ? X : V, g, t);
+    }
+  }
+}
+
 // NNB_BATCHED_MINB (compile-time) caps registers so that MINB CTAs fit per SM.
 #ifndef NNB_BATCHED_MINB
 #define NNB_BATCHED_MINB 4
@@ -316,8 +380,9 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
 
     ZAcc<M3> acc;
     if (!ns_mode) {
-      // ---- Nested Neumann: `iters` nests of depth P ----
-      for (int it = 0; it < iters; ++it) {
+      // ---- Nested Neumann: `iters` nests of depth P (nest 0 from the diagonal X0) ----
+      if (iters > 0) first_nest_diag<P, M3>(acc, X, Pm, V, areg, g, t);
+      for (int it = 1; it < iters; ++it) {
         const SMat* v = &X;
         if constexpr (M3) {
           acc.template seed<true>(nullptr, 1.0, g, t);  // −I
@@ -350,10 +415,22 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
       const double ss = warp_sum(residual_ss(acc, g, t));
       if (lane == 0 && eps_last) eps_last[s] = sqrt(ss) * 0.25;  // 1/sqrt(16)
     } else if (ns_order > 0) {
-      // ---- Neumann-series baseline of `ns_order` terms from X0 ----
-      acc.zero();
-      zmma_sr(acc, X, areg, g, t);
-      epilogue(acc, -1.0, nullptr, 1.0, Pm, g, t);  // P = I − X0·A
+      // ---- Neumann-series baseline of `ns_order` terms from X0 (the same
+      // diagonal-X0 shortcuts: P = I − X0·A and X = T·X0 are scalings) ----
+      double2 xc[2];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) xc[nt] = make_double2(X.re[swz(8 * nt + g, 8 * nt + g)], X.im[swz(8 * nt + g, 8 * nt + g)]);
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb) {  // P = I − X0·A
+          const int r = 4 * kb + t, c = 8 * nt + g, idx = swz(r, c);
+          const double xr = X.re[swz(r, r)], xi = X.im[swz(r, r)];
+          const double ar = areg[nt][kb][0], ai = areg[nt][kb][1];
+          Pm.re[idx] = (r == c ? 1.0 : 0.0) - (xr * ar - xi * ai);
+          Pm.im[idx] = -(xr * ai + xi * ar);
+        }
+      __syncwarp();
       for (int i = lane; i < kMat; i += 32) {      // T = I + P (into V)
         V.re[i] = Pm.re[i];
         V.im[i] = Pm.im[i];
@@ -366,9 +443,16 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
         zmma_ss(acc, V, Pm, g, t);                  // T·P
         epilogue(acc, 1.0, nullptr, 1.0, V, g, t);  // T = T·P + I
       }
-      acc.zero();
-      zmma_ss(acc, V, X, g, t);                     // T·X0
-      epilogue(acc, 1.0, nullptr, 0.0, X, g, t);
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb) {  // X = T·X0: column c scaled by x_c
+          const int r = 4 * kb + t, c = 8 * nt + g, idx = swz(r, c);
+          const double tr = V.re[idx], ti = V.im[idx];
+          X.re[idx] = tr * xc[nt].x - ti * xc[nt].y;
+          X.im[idx] = tr * xc[nt].y + ti * xc[nt].x;
+        }
+      __syncwarp();
     }
     // store X (planar swizzled shared -> interleaved global, coalesced 16B)
     double2* Xs = Xout + s * kMat;
@@ -463,8 +547,9 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
       X.im[swz(lane, lane)] = xi;
     }
     __syncwarp();
-    // ---- Nested Neumann inversion (seeded 3M products, as batched_z16_kernel) ----
-    for (int it = 0; it < iters; ++it) {
+    // ---- Nested Neumann inversion (seeded 3M products, nest 0 from the diagonal X0) ----
+    if (iters > 0) first_nest_diag<P, true>(acc, X, Pm, V, areg, g, t);
+    for (int it = 1; it < iters; ++it) {
       acc.template seed<true>(nullptr, 1.0, g, t);
       zmma_sr(acc, X, areg, g, t);
       epilogue_seeded<true>(acc, Pm, g, t);  // P = I − X·A
