@@ -93,6 +93,20 @@ struct ZAcc {
       }
     }
   }
+  // 3M, Hermitian result (HᴴH): the upper tiles (0,0), (0,1), (1,1) only — the
+  // (1,0) tile is the conjugate transpose of (0,1) (gram_epilogue mirrors it)
+  __device__ __forceinline__ void step_herm(const double (&lr)[2], const double (&li)[2], const double (&rr)[2],
+                                            const double (&ri)[2]) {
+    const double ls[2] = {lr[0] + li[0], lr[1] + li[1]}, rs[2] = {rr[0] + ri[0], rr[1] + ri[1]};
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = mt; nt < 2; ++nt) {
+        dmma_8x8x4(v[mt][nt][0][0], v[mt][nt][0][1], lr[mt], rr[nt]);
+        dmma_8x8x4(v[mt][nt][1][0], v[mt][nt][1][1], li[mt], ri[nt]);
+        dmma_8x8x4(v[mt][nt][2][0], v[mt][nt][2][1], ls[mt], rs[nt]);
+      }
+  }
   // 3M only: seed the accumulators with s·(D + γ·I), s = −1 when NEG, as
   // P1 = re, P2 = 0, P3 = re + im — the "+D" and "γI" then cost 2 DADD per
   // element pair instead of 4 after the product, and the sign folds into
@@ -196,6 +210,30 @@ __device__ __forceinline__ void epilogue(const ZAcc<M3>& acc, double alpha, cons
       if (r == c + 1) vr.y += gamma;
       *reinterpret_cast<double2*>(out.re + idx) = vr;
       *reinterpret_cast<double2*>(out.im + idx) = vi;
+    }
+  __syncwarp();
+}
+
+// A = HᴴH + σ²·I from step_herm's three tiles; tile (1,0) = conj(tile (0,1))ᵀ.
+__device__ __forceinline__ void gram_epilogue(const ZAcc<true>& acc, double sigma2, const SMat& out, int g, int t) {
+  __syncwarp();
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = mt; nt < 2; ++nt) {
+      const int r = 8 * mt + g, c = 8 * nt + 2 * t;
+      double2 vr = make_double2(acc.re(mt, nt, 0), acc.re(mt, nt, 1));
+      const double2 vi = make_double2(acc.im(mt, nt, 0), acc.im(mt, nt, 1));
+      if (r == c) vr.x += sigma2;
+      if (r == c + 1) vr.y += sigma2;
+      *reinterpret_cast<double2*>(out.re + swz(r, c)) = vr;
+      *reinterpret_cast<double2*>(out.im + swz(r, c)) = vi;
+      if (mt != nt) {  // mirror: A[c+i][r] = conj(A[r][c+i])
+        out.re[swz(c, r)] = vr.x;
+        out.im[swz(c, r)] = -vi.x;
+        out.re[swz(c + 1, r)] = vr.y;
+        out.im[swz(c + 1, r)] = -vi.y;
+      }
     }
   __syncwarp();
 }
@@ -501,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
       const double2 h0 = __ldg(Hs + a * kN + g), h1 = __ldg(Hs + a * kN + 8 + g), y = __ldg(Ys + a);
       const double lr[2] = {h0.x, h1.x}, li[2] = {-h0.y, -h1.y};  // A-operand: conj(H)[i][a]
       const double rr[2] = {h0.x, h1.x}, ri[2] = {h0.y, h1.y};    // B-operand: H[a][j]
-      acc.step(lr, li, rr, ri);
+      acc.step_herm(lr, li, rr, ri);  // HᴴH is Hermitian: three of the four 8×8 tiles
       // conj(h)·y
       zr[0] = fma(h0.x, y.x, fma(h0.y, y.y, zr[0]));
       zi[0] = fma(h0.x, y.y, fma(-h0.y, y.x, zi[0]));
@@ -515,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
         zr[m] += __shfl_xor_sync(0xffffffffu, zr[m], o);
         zi[m] += __shfl_xor_sync(0xffffffffu, zi[m], o);
       }
-    epilogue(acc, 1.0, nullptr, sigma2, V, g, t);  // A = HᴴH + σ²I (shared, planar)
+    gram_epilogue(acc, sigma2, V, g, t);  // A = HᴴH + σ²I (shared, planar)
     // A's B-operand fragments in registers and X0 = diag(A)^-1
     double areg[2][4][2];
 #pragma unroll
