@@ -6,5 +6,5 @@ timeout 1200 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_fu
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 600 python tools/prof_drive.py all > gpurun_out/prof_all_plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    --csv --log-file gpurun_out/launches_r01e.csv python tools/prof_drive.py all > gpurun_out/ncu_launches.log 2>&1
+    --csv --log-file gpurun_out/launches_r01g.csv python tools/prof_drive.py all > gpurun_out/ncu_launches.log 2>&1
 tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; tail -1 gpurun_out/bench_full.err
