@@ -833,13 +833,15 @@ int nnb_nn_explicit_z(const double* phi0, const double* w, int64_t n, int64_t ne
 // rotating lanes (stream per lane): H2D of chunk i+1, the kernel on chunk i
 // and D2H of chunk i-1 overlap, so the PCIe traffic in both directions (full
 // duplex) hides behind itself and the compute instead of adding up.
-static constexpr int64_t kChunkSystems = 16384;  // 64 MB in + 64 MB out per chunk
+// 32 MB in + 32 MB out per chunk on 4 lanes: PCIe in and out overlap the DMMA
+// work and each other; smaller chunks shorten the pipeline's fill and drain.
+static constexpr int64_t kChunkSystems = 8192;
 
 static int batched_pipelined(const double* A, int64_t batch, int p, int iters, int ns_order, double* X_out,
                              double* eps_last, cudaStream_t s) {
-  constexpr int kLanes = 3;
+  constexpr int kLanes = 4;
   const size_t sys_doubles = 2 * 256;
-  static thread_local cudaStream_t lanes[kLanes] = {nullptr, nullptr, nullptr};
+  static thread_local cudaStream_t lanes[kLanes] = {};
   for (auto& l : lanes)
     if (!l) NNB_CUDA(cudaStreamCreateWithFlags(&l, cudaStreamNonBlocking));
   DevBuf buf;
