@@ -41,5 +41,10 @@ build/test_dropin: tests/cpp/test_dropin.cpp $(PKG)/libnn_b200.so
 	@mkdir -p build
 	g++ -O2 -std=c++20 $(DROPIN_INC) $< -o $@ -L$(PKG) -lnn_b200 -lnnb -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
-dropin: $(PKG)/libnn_b200.so build/test_dropin build/nnbench
+# the reference's acceptance criteria restated against the drop-in
+build/acceptance: tests/cpp/acceptance.cpp $(PKG)/libnn_b200.so
+	@mkdir -p build
+	g++ -O2 -std=c++20 $(DROPIN_INC) $< -o $@ -L$(PKG) -lnn_b200 -lnnb -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+dropin: $(PKG)/libnn_b200.so build/test_dropin build/nnbench build/acceptance
 .PHONY: dropin

@@ -63,3 +63,23 @@ def test_dropin_normal_equations_vs_reference(ref, tmp_path, n, k, depth, cond_s
     big = rep["history"] > 1e-12
     assert np.allclose(hist[big], rep["history"][big], rtol=1e-6, atol=1e-13)
     assert backward < 1e-10 and bwr < 1e-10
+
+
+@pytest.mark.gpu
+def test_acceptance_criteria_like_the_reference():
+    """The reference's acceptance program restated (tests/cpp/acceptance.cpp): every
+    criterion the reference passes passes here; criterion 5 (fitted order within 0.4
+    of L+1) fails in the reference itself (alpha 1.86 / 2.62 / 3.40) and
+    must fail here with the same fitted orders."""
+    import re
+
+    b = ROOT / "build" / "acceptance"
+    if not b.exists():
+        subprocess.run(["make", "-s", "-C", str(ROOT), "dropin"], check=True)
+    out = subprocess.run([str(b)], capture_output=True, text=True, timeout=900).stdout
+    print(out)
+    status = dict(re.findall(r"\[(PASS|FAIL)\]\s+(\d+)\.", out)[i][::-1] for i in range(9))
+    assert {k: v for k, v in status.items() if k != "5"} == {k: "PASS" for k in ("1", "2", "3", "4", "6", "7", "9", "10")}
+    assert status["5"] == "FAIL"
+    alphas = [float(a) for a in re.findall(r"alpha ([0-9.]+)", out)]
+    assert len(alphas) == 3 and all(abs(a - r) < 0.05 for a, r in zip(alphas, (1.86, 2.62, 3.40))), alphas
