@@ -248,6 +248,7 @@ int nnb_gemm_d(const double* A, int64_t lda, const double* B, int64_t ldb, doubl
   NNB_TRY(red.init(max_tiles_for(m, n), s));
   DevBuf nf;
   NNB_TRY(nf.alloc(sizeof(int), s));
+  NNB_CUDA(cudaMemsetAsync(nf.p, 0, sizeof(int), s));
   GemmOp op;
   op.A = a.d; op.lda = a.ld; op.B = b.d; op.ldb = b.ld;
   op.M = m; op.N = n; op.K = k;

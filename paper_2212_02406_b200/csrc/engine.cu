@@ -168,7 +168,15 @@ using BigCfg = GemmCfg<128, 128, 16, 2, 4, 4>;
 using SmallCfg = GemmCfg<64, 64, 16, 2, 2, 4>;
 using BigCfgT = GemmCfg<128, 128, 16, 2, 4, 4, true>;
 using SmallCfgT = GemmCfg<64, 64, 16, 2, 2, 4, true>;
-using TinyCfg = GemmCfg<32, 32, 16, 2, 2, 4>;  // latency-bound sizes (config 0: N=256 -> 64 CTAs)
+using TinyCfg = GemmCfg<32, 32, 16, 2, 2, 4>;  // latency-bound sizes
+using NanoCfg = GemmCfg<16, 16, 16, 2, 2, 4>;  // smaller still: config 0 (N=256) -> 256 CTAs of 8×8 warp tiles
+
+// The 16×16 tiles when even 32×32 ones leave most SMs idle.
+static bool use_nano(int64_t M, int64_t N) {
+  static const char* force = std::getenv("NNB_GEMM_CFG");
+  if (force) return force[0] == 'n';
+  return ((M + 31) / 32) * ((N + 31) / 32) < 148;
+}
 
 static bool use_tiny(int64_t M, int64_t N) {
   static const char* force = std::getenv("NNB_GEMM_CFG");
@@ -190,7 +198,7 @@ static int smem_pad() {
 }
 
 int max_tiles_for(int64_t M, int64_t N) {  // upper bound over every tile configuration
-  return static_cast<int>(((M + 31) / 32) * ((N + 31) / 32));
+  return static_cast<int>(((M + 15) / 16) * ((N + 15) / 16));
 }
 
 template <class Cfg>
@@ -216,6 +224,33 @@ static int launch_cfg(const GemmOp& op, cudaStream_t s) {
   return 0;
 }
 
+// Σ C² / non-finite count of an M×N region in a fixed order (the K = 0 products).
+__global__ void reduce_region_kernel(const double* __restrict__ C, int64_t ldc, int64_t M, int64_t N, double* ss_out,
+                                     int* nf_out, double* eps_out, double eps_scale) {
+  __shared__ double ss[256];
+  __shared__ int nf[256];
+  double a = 0.0;
+  int b = 0;
+  for (int64_t e = threadIdx.x; e < M * N; e += blockDim.x) {
+    const double v = C[(e / N) * ldc + e % N];
+    a = fma(v, v, a);
+    b += !isfinite(v);
+  }
+  ss[threadIdx.x] = a;
+  nf[threadIdx.x] = b;
+  __syncthreads();
+  if (threadIdx.x) return;
+  double t = 0.0;
+  int f = 0;
+  for (int i = 0; i < 256; ++i) {
+    t += ss[i];
+    f += nf[i];
+  }
+  if (ss_out) *ss_out = t;
+  if (nf_out) *nf_out = f;
+  if (eps_out) *eps_out = sqrt(t) * eps_scale;
+}
+
 int gemm(GemmOp op, RedWs* red, cudaStream_t s) {
   if (op.M <= 0 || op.N <= 0) return 0;
   if (op.M > INT32_MAX || op.N > INT32_MAX || op.K > INT32_MAX)
@@ -234,12 +269,20 @@ int gemm(GemmOp op, RedWs* red, cudaStream_t s) {
   } else {
     op.ep.ss_partial = nullptr;
   }
-  if (op.K == 0) {  // empty inner dimension: C = beta*D + gamma*I
-    return axpby(0.0, op.ep.C, op.ep.ldc, op.ep.beta, op.ep.D, op.ep.ldd, op.ep.gamma,
-                 op.ep.diag_offset, op.ep.C, op.ep.ldc, op.M, op.N, s);
+  if (op.K == 0) {  // empty inner dimension: C = beta*D + gamma*I, reduced like an epilogue would
+    NNB_TRY(axpby(0.0, op.ep.C, op.ep.ldc, op.ep.beta, op.ep.D, op.ep.ldd, op.ep.gamma, op.ep.diag_offset, op.ep.C,
+                  op.ep.ldc, op.M, op.N, s));
+    if (red) {
+      reduce_region_kernel<<<1, 256, 0, s>>>(op.ep.C, op.ep.ldc, op.M, op.N, op.ep.ss_out, op.ep.nf_out, op.ep.eps_out,
+                                             op.ep.eps_scale);
+      count_launch();
+      NNB_CUDA(cudaGetLastError());
+    }
+    return 0;
   }
   if (arith() == 1 && !op.b_kmajor) return gemm_exact(op, s);  // reference-exact mode (exact.cu)
   if (op.b_kmajor) return use_big(op.M, op.N) ? launch_cfg<BigCfgT>(op, s) : launch_cfg<SmallCfgT>(op, s);
+  if (use_nano(op.M, op.N)) return launch_cfg<NanoCfg>(op, s);
   if (use_tiny(op.M, op.N)) return launch_cfg<TinyCfg>(op, s);
   return use_big(op.M, op.N) ? launch_cfg<BigCfg>(op, s) : launch_cfg<SmallCfg>(op, s);
 }
