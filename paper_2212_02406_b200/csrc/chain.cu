@@ -237,7 +237,17 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
   std::vector<double> eps_h(slots, 0.0);
   std::vector<int> nf_h(nf_count, 0);
   int k = 0, products = 0, stopped = 1, recorded = 0;
-  for (;; ++k) {
+  // small real N: the whole loop in one cooperative kernel (chain_small.cu)
+  const bool small = !c.cplx && !exact && !io && small_chain_eligible(n, c.ld, cfg);
+  if (small) {
+    int st[4];
+    NNB_TRY(small_chain_real(A.re, X.re, R.re, bufs[1].re, bufs[2].re, n, c.ld, cfg, eps_dev, nf_dev, st, c.s));
+    k = st[0];
+    products = st[1];
+    stopped = st[2];
+    recorded = st[3];
+  }
+  for (; !small; ++k) {
     const bool last = (k >= cfg.max_iters);
     if (last && !cfg.final_residual) break;
     const Plane& Xk = bufs[xi];

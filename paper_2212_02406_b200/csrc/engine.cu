@@ -145,7 +145,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // Row-major rows×cols FP64 matrix with leading dimension ld, box = box_rows×box_cols.
-static int make_tmap(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+int make_tmap(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
                      int box_rows, int box_cols, bool swizzle128) {
   auto fn = encode_fn();
   if (!fn) return fail(7, "cuTensorMapEncodeTiled unavailable");

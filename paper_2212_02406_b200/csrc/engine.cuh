@@ -88,6 +88,10 @@ struct GemmOp {
 };
 
 int max_tiles_for(int64_t M, int64_t N);
+// 2D FP64 TMA descriptor over a row-major rows×cols matrix (leading dimension ld):
+// box_rows×box_cols boxes, 128B swizzle or none, zero fill out of bounds.
+int make_tmap(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+              int box_cols, bool swizzle128);
 // Arithmetic mode (thread-local): 0 = fast DMMA path, 1 = reference-exact (exact.cu).
 void set_arith(int mode);
 int arith();
@@ -179,6 +183,14 @@ struct ChainIo {
 // on entry and the final iterate on exit.  eps_hist host (nullable).
 int chain_real(const double* A, int64_t n, int64_t ldn, double* X, const ChainCfg& cfg,
                double* eps_hist, ChainOut* out, cudaStream_t s, ChainIo* io = nullptr);
+// Small real chains (n <= small_chain_max_n(), NNB_SMALL_CHAIN_MAX, 0 = off): the
+// nn_invert loop as one cooperative kernel (chain_small.cu).  X holds X0 on entry
+// and the final iterate on exit; R, w1, w2 are n×ld scratch; eps_dev / nf_dev
+// are filled as run_chain fills them; status_h = {k, products, stopped, recorded}.
+int small_chain_max_n();
+bool small_chain_eligible(int64_t n, int64_t ld, const ChainCfg& cfg);
+int small_chain_real(const double* A, double* X, double* R, double* w1, double* w2, int64_t n, int64_t ld,
+                     const ChainCfg& cfg, double* eps_dev, int* nf_dev, int status_h[4], cudaStream_t s);
 // Complex chain on planar device buffers (re/im each n×ldn).
 int chain_complex(const double* Ar, const double* Ai, int64_t n, int64_t ldn, double* Xr,
                   double* Xi, const ChainCfg& cfg, double* eps_hist, ChainOut* out,
