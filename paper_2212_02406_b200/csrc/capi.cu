@@ -582,11 +582,17 @@ int nnb_nn_chain_d(const double* A, int64_t n, const double* X0, const nnb_chain
     return chain_d_streamed(A, n, X0, cfg, c, X_out, eps_hist, result, s);
   DMat a;
   NNB_TRY(a.load(A, n, n, n, s));
-  DMat x;  // working X with A's leading dimension
+  DMat x;  // working X with A's leading dimension: the caller's device X_out when it fits
   x.rows = x.cols = n;
   x.ld = a.ld;
-  NNB_TRY(x.own.alloc(sizeof(double) * n * a.ld, s));
-  x.d = x.own.as<double>();
+  const bool direct = X_out && !host_out && a.ld == n && !(reinterpret_cast<uintptr_t>(X_out) & 15) &&
+                      X_out != A && X_out != X0;
+  if (direct) {
+    x.d = X_out;
+  } else {
+    NNB_TRY(x.own.alloc(sizeof(double) * n * a.ld, s));
+    x.d = x.own.as<double>();
+  }
   if (cfg->x0_kind == NNB_X0_GIVEN) {
     if (!X0) return fail(NNB_ERR_DOMAIN, "nn chain: X0 required for NNB_X0_GIVEN");
     NNB_CUDA(cudaMemcpy2DAsync(x.d, x.ld * 8, X0, n * 8, n * 8, n, cudaMemcpyDefault, s));
@@ -597,8 +603,10 @@ int nnb_nn_chain_d(const double* A, int64_t n, const double* X0, const nnb_chain
   const int st = chain_real(a.d, n, a.ld, x.d, c, eps_hist, &o, s);
   fill_result(result, o);
   if (st != 0 && st != NNB_ERR_DIVERGENCE && st != NNB_ERR_DOMAIN) return st;
-  NNB_TRY(x.store(X_out, n, s));
-  NNB_TRY(sync(s));
+  if (!direct) {
+    NNB_TRY(x.store(X_out, n, s));
+    NNB_TRY(sync(s));
+  }
   return st;
 }
 

@@ -13,6 +13,7 @@
 // complex product being four real DMMA GEMMs (4M) whose epilogues carry the
 // ±, "+D", "+γI" and reduction terms.
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "engine.cuh"
@@ -197,21 +198,43 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
   const int p = cfg.p;
   const int slots = cfg.max_iters + 1;
 
-  NNB_TRY(c.red.init(max_tiles_for(n, n), c.s));
+  constexpr int kMaxChunks = 64;
+  if (io && (io->chunks < 1 || io->chunks > kMaxChunks || c.cplx)) io = nullptr;
+  // reference-exact mode (real data): the reference's operand order and nest sequence
+  const bool exact = arith() == 1 && !c.cplx;
+  // small real N: the whole loop in one cooperative kernel (chain_small.cu)
+  const bool small = !c.cplx && !exact && !io && small_chain_eligible(n, c.ld, cfg);
+  if (!small) NNB_TRY(c.red.init(max_tiles_for(n, n), c.s));
   DevBuf work;
   NNB_TRY(work.alloc(sizeof(double) * (size_t)mat * planes * 3, c.s));
   DevBuf scal;
   const size_t nf_count = (size_t)slots * (p + 1);
-  constexpr int kMaxChunks = 64;
-  if (io && (io->chunks < 1 || io->chunks > kMaxChunks || c.cplx)) io = nullptr;
-  NNB_TRY(scal.alloc(sizeof(double) * (slots + 8 + kMaxChunks) + sizeof(int) * (nf_count + 8 + kMaxChunks), c.s));
+  // device scalars, one block (one D2H copy): ε per nest | complex Σ² | chunk Σ² | non-finite
+  // counts | complex counts | chunk counts | small-kernel status
+  NNB_TRY(scal.alloc(sizeof(double) * (slots + 8 + kMaxChunks) + sizeof(int) * (nf_count + 8 + kMaxChunks + 8), c.s));
   double* eps_dev = scal.as<double>();
   c.ss2 = eps_dev + slots;
   double* chunk_ss = c.ss2 + 8;
   int* nf_dev = reinterpret_cast<int*>(chunk_ss + kMaxChunks);
   c.nf2 = nf_dev + nf_count;
   int* chunk_nf = c.nf2 + 8;
+  int* status_dev = chunk_nf + kMaxChunks;
   NNB_CUDA(cudaMemsetAsync(scal.p, 0, scal.bytes, c.s));
+  std::vector<double> eps_h(slots, 0.0);
+  std::vector<int> nf_h(nf_count, 0);
+  int status_h[4] = {0, 0, 0, 0};
+  // scal -> host through a pinned staging block (one copy, one sync)
+  auto fetch = [&]() -> int {
+    uint8_t* h = static_cast<uint8_t*>(pinned_stage(scal.bytes));
+    if (!h) return fail(6, "nn chain: pinned staging allocation failed");
+    NNB_CUDA(cudaMemcpyAsync(h, scal.p, scal.bytes, cudaMemcpyDeviceToHost, c.s));
+    NNB_CUDA(cudaStreamSynchronize(c.s));
+    std::memcpy(eps_h.data(), h, sizeof(double) * slots);
+    const uint8_t* hi = h + sizeof(double) * (slots + 8 + kMaxChunks);
+    std::memcpy(nf_h.data(), hi, sizeof(int) * nf_count);
+    std::memcpy(status_h, hi + sizeof(int) * (nf_count + 8 + kMaxChunks), sizeof(status_h));
+    return 0;
+  };
 
   auto plane_at = [&](int i) {
     Plane pl;
@@ -231,22 +254,10 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
   NNB_CUDA(cudaEventRecord(e0, c.s));
 
   const bool tol_mode = cfg.tol > 0.0;
-  // reference-exact mode (real data): the reference's operand order and nest sequence
-  const bool exact = arith() == 1 && !c.cplx;
   const int order = exact ? 1 : cfg.order;
-  std::vector<double> eps_h(slots, 0.0);
-  std::vector<int> nf_h(nf_count, 0);
   int k = 0, products = 0, stopped = 1, recorded = 0;
-  // small real N: the whole loop in one cooperative kernel (chain_small.cu)
-  const bool small = !c.cplx && !exact && !io && small_chain_eligible(n, c.ld, cfg);
-  if (small) {
-    int st[4];
-    NNB_TRY(small_chain_real(A.re, X.re, R.re, bufs[1].re, bufs[2].re, n, c.ld, cfg, eps_dev, nf_dev, st, c.s));
-    k = st[0];
-    products = st[1];
-    stopped = st[2];
-    recorded = st[3];
-  }
+  if (small)
+    NNB_TRY(small_chain_real(A.re, X.re, R.re, bufs[1].re, bufs[2].re, n, c.ld, cfg, eps_dev, nf_dev, status_dev, c.s));
   for (; !small; ++k) {
     const bool last = (k >= cfg.max_iters);
     if (last && !cfg.final_residual) break;
@@ -261,11 +272,7 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
     ++products;
     recorded = k + 1;
     if (tol_mode) {
-      NNB_CUDA(cudaMemcpyAsync(eps_h.data(), eps_dev, sizeof(double) * slots,
-                               cudaMemcpyDeviceToHost, c.s));
-      NNB_CUDA(cudaMemcpyAsync(nf_h.data(), nf_dev, sizeof(int) * nf_count,
-                               cudaMemcpyDeviceToHost, c.s));
-      NNB_CUDA(cudaStreamSynchronize(c.s));
+      NNB_TRY(fetch());
       bool bad = false;
       for (int q = 0; q <= k * (p + 1); ++q) bad |= nf_h[q] != 0;
       if (bad) break;  // reported below
@@ -321,11 +328,13 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
     NNB_TRY(copy2d(bufs[xi].re, c.ld, caller_x.re, c.ld, n, n, c.s));
     if (c.cplx) NNB_TRY(copy2d(bufs[xi].im, c.ld, caller_x.im, c.ld, n, n, c.s));
   }
-  NNB_CUDA(cudaMemcpyAsync(eps_h.data(), eps_dev, sizeof(double) * slots, cudaMemcpyDeviceToHost,
-                           c.s));
-  NNB_CUDA(cudaMemcpyAsync(nf_h.data(), nf_dev, sizeof(int) * nf_count, cudaMemcpyDeviceToHost,
-                           c.s));
-  NNB_CUDA(cudaStreamSynchronize(c.s));
+  NNB_TRY(fetch());
+  if (small) {
+    k = status_h[0];
+    products = status_h[1];
+    stopped = status_h[2];
+    recorded = status_h[3];
+  }
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);

@@ -417,7 +417,7 @@ static int small_tm(int64_t n) {
 }
 
 int small_chain_real(const double* A, double* X, double* R, double* w1, double* w2, int64_t n, int64_t ld,
-                     const ChainCfg& cfg, double* eps_dev, int* nf_dev, int status_h[4], cudaStream_t s) {
+                     const ChainCfg& cfg, double* eps_dev, int* nf_dev, int* status_dev, cudaStream_t s) {
   if (n < 1 || n > 512 || (ld & 1)) return fail(1, "small chain: unsupported size");
   const int tm = small_tm(n);
   const int tiles = static_cast<int>(((n + tm - 1) / tm) * ((n + kT - 1) / kT));
@@ -449,14 +449,12 @@ int small_chain_real(const double* A, double* X, double* R, double* w1, double* 
   a.ss_part = ws.as<double>();
   a.nf_part = reinterpret_cast<int*>(a.ss_part + slots * tiles);
   a.bar = reinterpret_cast<unsigned*>(a.nf_part + slots * tiles);
-  a.status = reinterpret_cast<int*>(a.bar + 1);
-  NNB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(int) * 8, s));
+  a.status = status_dev;
+  NNB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned), s));
   if (tm == 32)
     NNB_TRY(launch<32>(maps, a, s));
   else
     NNB_TRY(launch<16>(maps, a, s));
-  NNB_CUDA(cudaMemcpyAsync(status_h, a.status, sizeof(int) * 4, cudaMemcpyDeviceToHost, s));
-  NNB_CUDA(cudaStreamSynchronize(s));
   return 0;
 }
 

@@ -72,6 +72,20 @@ cudaStream_t resolve(void* stream) {
   return static_cast<cudaStream_t>(stream);
 }
 
+void* pinned_stage(size_t bytes) {
+  thread_local void* p = nullptr;
+  thread_local size_t cap = 0;
+  if (bytes > cap) {
+    if (p) cudaFreeHost(p);
+    cap = std::max<size_t>(bytes, size_t(64) << 10);
+    if (cudaHostAlloc(&p, cap, cudaHostAllocDefault) != cudaSuccess) {
+      p = nullptr;
+      cap = 0;
+    }
+  }
+  return p;
+}
+
 int DevBuf::alloc(size_t b, cudaStream_t st) {
   release();
   s = st;

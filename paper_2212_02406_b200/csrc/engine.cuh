@@ -186,11 +186,14 @@ int chain_real(const double* A, int64_t n, int64_t ldn, double* X, const ChainCf
 // Small real chains (n <= small_chain_max_n(), NNB_SMALL_CHAIN_MAX, 0 = off): the
 // nn_invert loop as one cooperative kernel (chain_small.cu).  X holds X0 on entry
 // and the final iterate on exit; R, w1, w2 are n×ld scratch; eps_dev / nf_dev
-// are filled as run_chain fills them; status_h = {k, products, stopped, recorded}.
+// are filled as run_chain fills them; status_dev = {k, products, stopped, recorded}
+// (device ints, read by the caller after its own synchronisation).
 int small_chain_max_n();
 bool small_chain_eligible(int64_t n, int64_t ld, const ChainCfg& cfg);
 int small_chain_real(const double* A, double* X, double* R, double* w1, double* w2, int64_t n, int64_t ld,
-                     const ChainCfg& cfg, double* eps_dev, int* nf_dev, int status_h[4], cudaStream_t s);
+                     const ChainCfg& cfg, double* eps_dev, int* nf_dev, int* status_dev, cudaStream_t s);
+// Page-locked host block of at least `bytes` (per thread, grown on demand; null on failure).
+void* pinned_stage(size_t bytes);
 // Complex chain on planar device buffers (re/im each n×ldn).
 int chain_complex(const double* Ar, const double* Ai, int64_t n, int64_t ldn, double* Xr,
                   double* Xi, const ChainCfg& cfg, double* eps_hist, ChainOut* out,
