@@ -1,5 +1,5 @@
-"""Small fixed workload for ncu captures: one dense nest (N=8192, p=2), one C2 batch,
-one C5 solve.  Run plainly first (must exit 0), then under ncu with the same arguments."""
+"""Small fixed workload for ncu captures: one dense nest (N=8192, p=2), one config-0
+chain (N=256), one C2 batch, one C5 solve.  Run plainly first (must exit 0), then under ncu with the same arguments."""
 import sys
 from pathlib import Path
 
@@ -15,6 +15,11 @@ if which in ("all", "dense"):
     x = nnb.x0(a)
     for _ in range(2):
         x, rep = nnb.nn_chain(a, x, p=2, max_iters=1, final_residual=False)
+if which in ("all", "c1"):
+    # config 0: the device-resident small chain (one cooperative kernel per run)
+    a1 = torch.from_numpy(W.gram_shifted(256, seed=2212, shift=0.5)).cuda()
+    for _ in range(2):
+        x1, rep1 = nnb.nn_chain(a1, None, p=1, max_iters=30)
 if which in ("all", "mimo"):
     am = W.mimo_gram_device(262144, seed=1)
     for _ in range(2):
