@@ -485,19 +485,12 @@ def cpu_mimo_sample(sample: int):
 
 
 # ------------------------------------------------------------------ sparse leg (config 4)
-def sparse_bytes(n, nnz, col_bytes=4):
-    """Algorithmic bytes of one application in the format the kernel consumes:
-    f64 values + columns per nonzero (int16 deltas from the row when the band fits, else int32),
-    int32 row offsets (the device narrows them), t read + t written per row."""
-    return nnz * (8 + col_bytes) + (n + 1) * 4 + 2 * n * 8
-
-
-def csr_col_bytes(rp, col):
-    """2 when every |column - row| fits the device's int16 deltas (csrc/sparse.cu compact_csr), else 4."""
-    import numpy as np
-
-    rows = np.repeat(np.arange(rp.size - 1, dtype=np.int64), np.diff(rp))
-    return 2 if col.size == 0 or np.abs(col.astype(np.int64) - rows).max() <= 32767 else 4
+def sparse_bytes(n, nnz, nnz_bytes=12):
+    """Bytes of one application: nnz_bytes per nonzero, int32 row offsets, t read + t written per row.
+    nnz_bytes = 12 (f64 value + int32 column) is SURVEY.md §8(d)'s algorithmic figure and the work unit
+    of the metric; the format the kernel actually consumes (1: pair dictionary, 10: f64 + int16 column
+    delta, 12) gives the roofline's bytes."""
+    return nnz * nnz_bytes + (n + 1) * 4 + 2 * n * 8
 
 
 def run_sparse(args, world, rank):
@@ -539,19 +532,23 @@ def run_sparse(args, world, rank):
     if sharded:
         plan.close()
         comm.close()
-    cb = csr_col_bytes(rp, col)
-    alg = 63 * sparse_bytes(n, col.size, cb)  # whole-job algorithmic bytes per solve
-    gbs = alg / (ms * 1e-3) / 1e9
-    return {"metric": "sparse factorized solve, 4096^2 5-pt Laplacian+I, gamma=63", "value": round(gbs, 1),
-            "unit": "GB/s", "ms_per_step": round(ms, 3),
+    # the format the device consumed (csrc/sparse.cu): 1 = pair dictionary, 10 = f64 + int16 delta, 12
+    fb = 10 if sharded else nnb.sparse_last_bytes_per_nnz()
+    fmt = {1: "1-byte (column - row, value) pair-dictionary codes", 10: "f64 values + int16 column deltas",
+           12: "f64 values + int32 columns"}[fb]
+    alg = 63 * sparse_bytes(n, col.size, 12)  # SURVEY §8(d) algorithmic bytes per solve: the work unit
+    moved = 63 * sparse_bytes(n, col.size, fb)  # bytes of the consumed format: the roofline
+    gbs, moved_gbs = alg / (ms * 1e-3) / 1e9, moved / (ms * 1e-3) / 1e9
+    return {"metric": "sparse factorized solve, 4096^2 5-pt Laplacian+I, gamma=63 (GB/s of SURVEY 8(d) algorithmic "
+                      "bytes: 12 B per nonzero)", "value": round(gbs, 1),
+            "unit": "GB/s", "ms_per_step": round(ms, 3), "format_bytes_per_nnz": fb,
             "parallelism": f"row slabs x{world}, NCCL halo exchange" if sharded else "single GPU",
-            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": HBM_PEAK * world, "unit": "GB/s",
-                         "frac": round(gbs / (HBM_PEAK * world), 4),
+            "roofline": {"bound": "hbm", "achieved": round(moved_gbs, 1), "peak": HBM_PEAK * world, "unit": "GB/s",
+                         "frac": round(moved_gbs / (HBM_PEAK * world), 4),
                          "traffic": ncu_traffic("sparse_application") if grid == 4096 and not sharded else None,
                          "traffic_unit": "bytes per application (63 per solve)",
-                         "per_launch": f"nnz*(8+{cb}) + (N+1)*4 + 2N*8 bytes per application (x63): f64 values, "
-                                       f"{'int16 column deltas' if cb == 2 else 'int32 columns'}, int32 row offsets, "
-                                       "t in + t out"}}
+                         "per_launch": f"nnz*{fb} + (N+1)*4 + 2N*8 bytes per application (x63, whole solve timed "
+                                       f"incl. the per-solve format pass): {fmt}, int32 row offsets, t in + t out"}}
 
 
 def cpu_sparse_sample(grid: int):
@@ -565,7 +562,7 @@ def cpu_sparse_sample(grid: int):
     rp, col, val = W.laplacian_5pt(grid)
     b = W.rhs(grid * grid, seed=7)
     _, _, secs = ref.sparse_factorized(rp, col, val, b, 63, 0.2)
-    gbs = 63 * sparse_bytes(grid * grid, col.size, csr_col_bytes(rp, col)) / secs / 1e9  # same unit as the GPU leg
+    gbs = 63 * sparse_bytes(grid * grid, col.size, 12) / secs / 1e9  # same unit as the GPU leg
     return {"value": round(gbs, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
             "sample": f"reference solve_sparse_factorized gamma=63 on a {grid}^2 grid ({secs:.2f} s)"}
 

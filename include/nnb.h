@@ -242,6 +242,12 @@ int nnb_sparse_factorized_d(const int64_t* row_ptr, const int32_t* col, const do
                             int64_t n, int64_t nnz, const double* B, int64_t k, int64_t gamma,
                             double theta, double* X_out, int64_t* spmv_count_out,
                             int32_t* fail_factor_out, void* stream);
+/* Bytes per nonzero of the CSR format the calling thread's last
+ * nnb_sparse_factorized_d consumed: 1 when the operator has <= 256 distinct
+ * (column - row, value) pairs (a pair dictionary, CSR-VI style: stencils and
+ * other structured operators), 10 with int16 column deltas from the row, 12
+ * with int32 columns; 0 before any solve.  Every format is bit-identical. */
+int nnb_sparse_last_bytes_per_nnz(void);
 
 /* ---- contraction measurement (theta_trace's spectral estimate) ---------- */
 /* Power iteration on M^H M from the unit probe v0 (complex128, length n):

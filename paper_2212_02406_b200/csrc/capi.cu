@@ -13,6 +13,7 @@
 
 #include "../../include/nnb.h"
 #include "engine.cuh"
+#include "sparse.cuh"
 
 using namespace nnb;
 
@@ -984,6 +985,8 @@ int nnb_spmv_block_d(const int64_t* row_ptr, const int32_t* col, const double* v
   NNB_TRY(y.finish(s));
   return sync(s);
 }
+
+int nnb_sparse_last_bytes_per_nnz(void) { return sparse_bytes_per_nnz(); }
 
 int nnb_sparse_factorized_d(const int64_t* row_ptr, const int32_t* col, const double* val,
                             int64_t n, int64_t nnz, const double* B, int64_t k, int64_t gamma,

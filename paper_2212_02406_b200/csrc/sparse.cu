@@ -35,6 +35,12 @@
 
 namespace nnb {
 
+namespace {
+thread_local int g_sparse_bytes_per_nnz = 0;
+}
+void set_sparse_bytes_per_nnz(int b) { g_sparse_bytes_per_nnz = b; }
+int sparse_bytes_per_nnz() { return g_sparse_bytes_per_nnz; }
+
 template <int MODE>
 __device__ __forceinline__ double finish(double tin, double y, double theta, double zold, bool& bad) {
   const double t = __dsub_rn(tin, __dmul_rn(theta, y));  // fused_axpy_sub, factorized.cpp:21-30
@@ -60,13 +66,24 @@ __device__ __forceinline__ double finish(double tin, double y, double theta, dou
 #ifndef NNB_SPMV_MINB
 #define NNB_SPMV_MINB (2048 / NNB_SPMV_THREADS)
 #endif
-template <typename Idx, typename C, int MODE>
+template <typename Idx, typename C, int MODE, bool K1>
 __global__ void __launch_bounds__(NNB_SPMV_THREADS, NNB_SPMV_MINB)
     spmv_rows_kernel(const Idx* __restrict__ rp, const C* __restrict__ col, const double* __restrict__ val,
                      int64_t r_begin, int64_t r_end, int64_t diag_off, int64_t k, const double* __restrict__ t_ext,
                      const double* __restrict__ t_own, double* __restrict__ out, const double* __restrict__ zold,
                      double theta, int* __restrict__ flag) {
   bool bad = false;
+  if (K1) {  // one right-hand side, 32-bit offsets and indices
+    for (int r = (int)r_begin + blockIdx.x * blockDim.x + threadIdx.x; r < (int)r_end; r += gridDim.x * blockDim.x) {
+      const int e0 = (int)rp[r], e1 = (int)rp[r + 1];
+      const double* tg = t_ext + (sizeof(C) == 2 ? r + (int)diag_off : 0);  // int16: column = row + delta
+      double y = 0.0;
+      for (int e = e0; e < e1; ++e) y = __dadd_rn(y, __dmul_rn(val[e], tg[col[e]]));
+      out[r] = finish<MODE>(t_own[r], y, theta, MODE == kInner ? 0.0 : zold[r], bad);
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+    return;
+  }
   for (int64_t r = r_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < r_end;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e0 = rp[r], e1 = rp[r + 1];
@@ -78,6 +95,253 @@ __global__ void __launch_bounds__(NNB_SPMV_THREADS, NNB_SPMV_MINB)
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// The same application with the pair dictionary: 1 byte per nonzero (code) in
+// place of 10-12; the ≤ 256 (delta, value) pairs sit in shared memory.
+template <typename Idx, int MODE, bool K1>
+__global__ void __launch_bounds__(NNB_SPMV_THREADS, NNB_SPMV_MINB)
+    spmv_dict_kernel(const Idx* __restrict__ rp, const uint8_t* __restrict__ code,
+                     const int32_t* __restrict__ dict_delta, const double* __restrict__ dict_val, int dict_size,
+                     int64_t r_begin, int64_t r_end, int64_t diag_off, int64_t k, const double* __restrict__ t_ext,
+                     const double* __restrict__ t_own, double* __restrict__ out, const double* __restrict__ zold,
+                     double theta, int* __restrict__ flag) {
+  __shared__ int32_t sd[kPairDictMax];
+  __shared__ double sv[kPairDictMax];
+  for (int i = threadIdx.x; i < dict_size; i += blockDim.x) {
+    sd[i] = dict_delta[i];
+    sv[i] = dict_val[i];
+  }
+  __syncthreads();
+  bool bad = false;
+  if (K1) {  // one right-hand side, 32-bit indices
+    for (int r = (int)r_begin + blockIdx.x * blockDim.x + threadIdx.x; r < (int)r_end; r += gridDim.x * blockDim.x) {
+      const int e0 = (int)rp[r], e1 = (int)rp[r + 1];
+      const double* tg = t_ext + (r + (int)diag_off);
+      double y = 0.0;
+      for (int e = e0; e < e1; ++e) {
+        const int q = code[e];
+        y = __dadd_rn(y, __dmul_rn(sv[q], tg[sd[q]]));
+      }
+      out[r] = finish<MODE>(t_own[r], y, theta, MODE == kInner ? 0.0 : zold[r], bad);
+    }
+  } else {
+    for (int64_t r = r_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < r_end;
+         r += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t e0 = rp[r], e1 = rp[r + 1];
+      const int64_t g0 = r + diag_off;
+      for (int64_t c = 0; c < k; ++c) {
+        double y = 0.0;
+        for (int64_t e = e0; e < e1; ++e) {
+          const int q = code[e];
+          y = __dadd_rn(y, __dmul_rn(sv[q], t_ext[(g0 + sd[q]) * k + c]));
+        }
+        out[r * k + c] = finish<MODE>(t_own[r * k + c], y, theta, MODE == kInner ? 0.0 : zold[r * k + c], bad);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// Pair dictionary in ELL order (rows of at most kEllMaxWidth nonzeros): no row
+// offsets, so a row's code loads and then its gathers are all independent.
+template <int MODE, int WMAX, int MINB>
+__global__ void __launch_bounds__(NNB_SPMV_THREADS, MINB)
+    spmv_dict_ell_kernel(const uint8_t* __restrict__ code, int width, int64_t plane, const int32_t* __restrict__ dict_delta,
+                         const double* __restrict__ dict_val, int dict_size, int64_t r_begin, int64_t r_end,
+                         int64_t diag_off, int64_t k, const double* __restrict__ t_ext,
+                         const double* __restrict__ t_own, double* __restrict__ out, const double* __restrict__ zold,
+                         double theta, int* __restrict__ flag) {
+  __shared__ int32_t sd[kPairDictMax];
+  __shared__ double sv[kPairDictMax];
+  for (int i = threadIdx.x; i < dict_size; i += blockDim.x) {
+    sd[i] = dict_delta[i];
+    sv[i] = dict_val[i];
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int64_t r = r_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < r_end;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int q[WMAX];
+#pragma unroll
+    for (int i = 0; i < WMAX; ++i) q[i] = i < width ? code[i * plane + r] : kEllPad;
+    const int64_t g0 = r + diag_off;
+    for (int64_t c = 0; c < k; ++c) {
+      double xv[WMAX];
+#pragma unroll
+      for (int i = 0; i < WMAX; ++i) xv[i] = q[i] != kEllPad ? t_ext[(g0 + sd[q[i]]) * k + c] : 0.0;
+      double y = 0.0;
+#pragma unroll
+      for (int i = 0; i < WMAX; ++i)
+        if (q[i] != kEllPad) y = __dadd_rn(y, __dmul_rn(sv[q[i]], xv[i]));  // CSR order
+      out[r * k + c] = finish<MODE>(t_own[r * k + c], y, theta, MODE == kInner ? 0.0 : zold[r * k + c], bad);
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// One right-hand side, fewer than 2^31 gather indices: 32-bit index arithmetic
+// (the 64-bit `· k + c` address math was a quarter of the general kernel's issue).
+template <int MODE, int WMAX>
+__global__ void __launch_bounds__(NNB_SPMV_THREADS, NNB_SPMV_MINB)
+    spmv_dict_ell1_kernel(const uint8_t* __restrict__ code, int width, int plane,
+                          const int32_t* __restrict__ dict_delta, const double* __restrict__ dict_val, int dict_size,
+                          int r_begin, int r_end, int diag_off, const double* __restrict__ t_ext,
+                          const double* __restrict__ t_own, double* __restrict__ out, const double* __restrict__ zold,
+                          double theta, int* __restrict__ flag) {
+  __shared__ double2 dict[kPairDictMax];  // {value, delta + diag_off as bits}: one 16-byte load per nonzero
+  for (int i = threadIdx.x; i < dict_size; i += blockDim.x)
+    dict[i] = make_double2(dict_val[i], __longlong_as_double((long long)(dict_delta[i] + diag_off)));
+  __syncthreads();
+  bool bad = false;
+  for (int r = r_begin + blockIdx.x * blockDim.x + threadIdx.x; r < r_end; r += gridDim.x * blockDim.x) {
+    int q[WMAX];
+#pragma unroll
+    for (int i = 0; i < WMAX; ++i) q[i] = i < width ? code[(size_t)i * plane + r] : kEllPad;
+    double vv[WMAX], xv[WMAX];
+#pragma unroll
+    for (int i = 0; i < WMAX; ++i) {
+      const double2 de = dict[q[i] != kEllPad ? q[i] : 0];
+      vv[i] = de.x;
+      xv[i] = q[i] != kEllPad ? t_ext[r + (int)__double_as_longlong(de.y)] : 0.0;
+    }
+    double y = 0.0;
+#pragma unroll
+    for (int i = 0; i < WMAX; ++i)
+      if (q[i] != kEllPad) y = __dadd_rn(y, __dmul_rn(vv[i], xv[i]));  // CSR order
+    out[r] = finish<MODE>(t_own[r], y, theta, MODE == kInner ? 0.0 : zold[r], bad);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// ---- pair dictionary build: hash insert, index assignment, verified encode ----
+constexpr int kDictSlots = 4096;  // open addressing, power of two
+
+__device__ __forceinline__ unsigned long long pair_hash(int32_t d, unsigned long long bits) {
+  unsigned long long h = bits ^ (static_cast<unsigned long long>(static_cast<uint32_t>(d)) * 0x9E3779B97F4A7C15ull);
+  h ^= h >> 33;
+  h *= 0xff51afd7ed558ccdull;
+  h ^= h >> 33;
+  h *= 0xc4ceb9fe1a85ec53ull;
+  h ^= h >> 33;
+  return h | 1ull;  // never 0 (0 marks an empty slot)
+}
+
+struct DictWs {
+  unsigned long long hash[kDictSlots];
+  int32_t delta[kDictSlots];
+  double val[kDictSlots];
+  int32_t index[kDictSlots];
+  int count;
+  int overflow;   // more than kPairDictMax pairs
+  int collision;  // a 64-bit hash matched a different pair (the encode check)
+  int size;
+  int max_len;    // longest row
+};
+
+__global__ void dict_insert_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                   const double* __restrict__ val, int64_t rows, int64_t row0, DictWs* ws) {
+  int32_t last_d = 0;
+  unsigned long long last_b = 0, last_h = 0;  // consecutive nonzeros repeat pairs: skip their probes
+  int longest = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    if (*(volatile int*)&ws->overflow) return;
+    const int64_t rl = rp[r + 1] - rp[r];
+    longest = max(longest, rl > (1 << 30) ? (1 << 30) : (int)rl);
+    for (int64_t e = rp[r], e1 = rp[r + 1]; e < e1; ++e) {
+      const int64_t dl = (int64_t)col[e] - (row0 + r);
+      if (dl < INT32_MIN || dl > INT32_MAX) {
+        atomicOr(&ws->overflow, 1);
+        return;
+      }
+      const int32_t d = static_cast<int32_t>(dl);
+      const unsigned long long b = __double_as_longlong(val[e]);
+      if (last_h && d == last_d && b == last_b) continue;
+      const unsigned long long h = pair_hash(d, b);
+      int slot = static_cast<int>(h & (kDictSlots - 1));
+      for (int probe = 0; probe < kDictSlots; ++probe) {
+        unsigned long long cur = *(volatile unsigned long long*)&ws->hash[slot];
+        if (cur == 0) {
+          cur = atomicCAS(&ws->hash[slot], 0ull, h);
+          if (cur == 0) {
+            ws->delta[slot] = d;
+            ws->val[slot] = val[e];
+            if (atomicAdd(&ws->count, 1) >= kPairDictMax) {
+              atomicOr(&ws->overflow, 1);
+              return;
+            }
+            break;
+          }
+        }
+        if (cur == h) break;
+        slot = (slot + 1) & (kDictSlots - 1);
+      }
+      last_d = d;
+      last_b = b;
+      last_h = h;
+    }
+  }
+  atomicMax(&ws->max_len, longest);
+}
+
+// one block: occupied slots in slot order -> dictionary indices
+__global__ void dict_index_kernel(DictWs* ws, int32_t* __restrict__ dict_delta, double* __restrict__ dict_val) {
+  __shared__ int counts[1024];
+  constexpr int per = kDictSlots / 1024;
+  int c = 0;
+  for (int i = 0; i < per; ++i) c += ws->hash[threadIdx.x * per + i] != 0;
+  counts[threadIdx.x] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int i = 0; i < 1024; ++i) {
+      const int v = counts[i];
+      counts[i] = run;
+      run += v;
+    }
+    ws->size = run;
+  }
+  __syncthreads();
+  int idx = counts[threadIdx.x];
+  for (int i = 0; i < per; ++i) {
+    const int slot = threadIdx.x * per + i;
+    if (ws->hash[slot] == 0) continue;
+    ws->index[slot] = idx;
+    dict_delta[idx] = ws->delta[slot];
+    dict_val[idx] = ws->val[slot];
+    ++idx;
+  }
+}
+
+// ell_width > 0: slot-major ELL, row r's i-th nonzero (CSR order) at code[i·rows + r],
+// padded with kEllPad (no row offsets needed; a warp's load of one slot is 32
+// consecutive bytes); else code[e − rp[0]] (CSR order).
+__global__ void dict_encode_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                   const double* __restrict__ val, int64_t rows, int64_t row0, const DictWs* ws,
+                                   uint8_t* __restrict__ code, int ell_width, int* collision) {
+  const int64_t base = rp[0];
+  bool bad = false;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    if (ell_width)
+      for (int64_t i = rp[r + 1] - rp[r]; i < ell_width; ++i) code[i * rows + r] = kEllPad;
+    for (int64_t e = rp[r], e1 = rp[r + 1]; e < e1; ++e) {
+      const int32_t d = static_cast<int32_t>((int64_t)col[e] - (row0 + r));
+      const unsigned long long b = __double_as_longlong(val[e]);
+      const unsigned long long h = pair_hash(d, b);
+      int slot = static_cast<int>(h & (kDictSlots - 1));
+      int probe = 0;
+      while (ws->hash[slot] != h && ws->hash[slot] != 0 && probe < kDictSlots) {
+        slot = (slot + 1) & (kDictSlots - 1);
+        ++probe;
+      }
+      // the exact pair, or the caller falls back to the column format
+      const bool hit = ws->hash[slot] == h && ws->delta[slot] == d &&
+                       __double_as_longlong(ws->val[slot]) == static_cast<long long>(b);
+      bad |= !hit;
+      code[ell_width ? (e - rp[r]) * rows + r : e - base] = static_cast<uint8_t>(hit ? ws->index[slot] : 0);
+    }
+  }
+  if (bad) atomicOr(collision, 1);
 }
 
 // Plain Y = W·X for nn::spmv_block (same rounding as the reference's sum).
@@ -124,24 +388,107 @@ unsigned rows_grid(int64_t n) {
   return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, 148 * 8 * 4)));
 }
 
-template <typename Idx, typename C, int MODE>
+// one right-hand side with 32-bit offsets and gather indices takes 32-bit index math
+template <typename Idx>
+bool k1_ok(const SpmvOp<Idx>& op, int64_t r_end) {
+  return op.k == 1 && sizeof(Idx) == 4 && r_end + op.diag_off < INT32_MAX / 2;
+}
+
+template <typename Idx, typename C, int MODE, bool K1>
 unsigned resident_grid(int64_t rows) {
   static unsigned resident = 0;
   if (!resident) {
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, spmv_rows_kernel<Idx, C, MODE>, NNB_SPMV_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, spmv_rows_kernel<Idx, C, MODE, K1>, NNB_SPMV_THREADS, 0);
     resident = static_cast<unsigned>(sms * std::max(1, per));
   }
   const int64_t want = (rows + NNB_SPMV_THREADS - 1) / NNB_SPMV_THREADS;
   return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(resident, want)));
 }
 
+template <typename Idx, typename C, int MODE, bool K1>
+void launch_rows_v(const SpmvOp<Idx>& op, const C* col, int64_t r_begin, int64_t r_end, cudaStream_t s) {
+  spmv_rows_kernel<Idx, C, MODE, K1><<<resident_grid<Idx, C, MODE, K1>(r_end - r_begin), NNB_SPMV_THREADS, 0, s>>>(
+      op.rp, col, op.val, r_begin, r_end, op.diag_off, op.k, op.t_ext, op.t_own, op.out, op.zold, op.theta, op.flag);
+}
+
 template <typename Idx, typename C, int MODE>
 void launch_rows(const SpmvOp<Idx>& op, const C* col, int64_t r_begin, int64_t r_end, cudaStream_t s) {
-  spmv_rows_kernel<Idx, C, MODE><<<resident_grid<Idx, C, MODE>(r_end - r_begin), NNB_SPMV_THREADS, 0, s>>>(
-      op.rp, col, op.val, r_begin, r_end, op.diag_off, op.k, op.t_ext, op.t_own, op.out, op.zold, op.theta, op.flag);
+  static const bool k1_off = std::getenv("NNB_SPMV_K1") && std::strcmp(std::getenv("NNB_SPMV_K1"), "0") == 0;
+  if (!k1_off && k1_ok(op, r_end)) launch_rows_v<Idx, C, MODE, true>(op, col, r_begin, r_end, s);
+  else launch_rows_v<Idx, C, MODE, false>(op, col, r_begin, r_end, s);
+}
+
+template <typename Idx, int MODE, bool K1>
+void launch_dict_v(const SpmvOp<Idx>& op, int64_t r_begin, int64_t r_end, cudaStream_t s) {
+  static unsigned resident = 0;
+  if (!resident) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, spmv_dict_kernel<Idx, MODE, K1>, NNB_SPMV_THREADS, 0);
+    resident = static_cast<unsigned>(sms * std::max(1, per));
+  }
+  const int64_t want = (r_end - r_begin + NNB_SPMV_THREADS - 1) / NNB_SPMV_THREADS;
+  const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(resident, want)));
+  spmv_dict_kernel<Idx, MODE, K1><<<grid, NNB_SPMV_THREADS, 0, s>>>(
+      op.rp, op.code, op.dict_delta, op.dict_val, op.dict_size, r_begin, r_end, op.diag_off, op.k, op.t_ext,
+      op.t_own, op.out, op.zold, op.theta, op.flag);
+}
+
+template <int MODE, int WMAX, int MINB, typename Idx>
+void launch_ell_v(const SpmvOp<Idx>& op, int64_t r_begin, int64_t r_end, cudaStream_t s) {
+  static unsigned resident = 0;
+  if (!resident) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, spmv_dict_ell_kernel<MODE, WMAX, MINB>, NNB_SPMV_THREADS, 0);
+    resident = static_cast<unsigned>(sms * std::max(1, per));
+  }
+  const int64_t want = (r_end - r_begin + NNB_SPMV_THREADS - 1) / NNB_SPMV_THREADS;
+  const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(resident, want)));
+  spmv_dict_ell_kernel<MODE, WMAX, MINB><<<grid, NNB_SPMV_THREADS, 0, s>>>(
+      op.code, op.ell_width, op.ell_rows, op.dict_delta, op.dict_val, op.dict_size, r_begin, r_end, op.diag_off, op.k, op.t_ext,
+      op.t_own, op.out, op.zold, op.theta, op.flag);
+}
+
+template <int MODE, int WMAX>
+void launch_ell1_v(const SpmvOp<int32_t>& op, int64_t r_begin, int64_t r_end, cudaStream_t s) {
+  static unsigned resident = 0;
+  if (!resident) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, spmv_dict_ell1_kernel<MODE, WMAX>, NNB_SPMV_THREADS, 0);
+    resident = static_cast<unsigned>(sms * std::max(1, per));
+  }
+  const int64_t want = (r_end - r_begin + NNB_SPMV_THREADS - 1) / NNB_SPMV_THREADS;
+  const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(resident, want)));
+  spmv_dict_ell1_kernel<MODE, WMAX><<<grid, NNB_SPMV_THREADS, 0, s>>>(
+      op.code, op.ell_width, (int)op.ell_rows, op.dict_delta, op.dict_val, op.dict_size, (int)r_begin, (int)r_end, (int)op.diag_off,
+      op.t_ext, op.t_own, op.out, op.zold, op.theta, op.flag);
+}
+
+// rows of <= 5 nonzeros (2-D 5-point stencils) fit the 32-register budget
+template <int MODE, typename Idx>
+void launch_ell(const SpmvOp<Idx>& op, int64_t r_begin, int64_t r_end, cudaStream_t s) {
+  // one right-hand side and 32-bit gather indices (|delta| < 2^31 is implied by the dictionary)
+  if (k1_ok(op, r_end)) {
+    const SpmvOp<int32_t>& o32 = reinterpret_cast<const SpmvOp<int32_t>&>(op);
+    if (op.ell_width <= 5) launch_ell1_v<MODE, 5>(o32, r_begin, r_end, s);
+    else launch_ell1_v<MODE, kEllMaxWidth>(o32, r_begin, r_end, s);
+    return;
+  }
+  launch_ell_v<MODE, kEllMaxWidth, 1>(op, r_begin, r_end, s);
+}
+
+template <typename Idx, int MODE>
+void launch_dict(const SpmvOp<Idx>& op, int64_t r_begin, int64_t r_end, cudaStream_t s) {
+  if (k1_ok(op, r_end)) launch_dict_v<Idx, MODE, true>(op, r_begin, r_end, s);
+  else launch_dict_v<Idx, MODE, false>(op, r_begin, r_end, s);
 }
 
 template <typename Idx, typename C>
@@ -158,7 +505,19 @@ void launch_mode(const SpmvOp<Idx>& op, const C* col, int mode, int64_t r_begin,
 template <typename Idx>
 void spmv_apply(const SpmvOp<Idx>& op, int mode, int64_t r_begin, int64_t r_end, cudaStream_t s) {
   if (r_end <= r_begin) return;
-  if (op.col16) launch_mode(op, op.col16, mode, r_begin, r_end, s);
+  if (op.code && op.ell_width) {
+    switch (mode) {
+      case kInner: launch_ell<kInner>(op, r_begin, r_end, s); break;
+      case kFactorEnd: launch_ell<kFactorEnd>(op, r_begin, r_end, s); break;
+      default: launch_ell<kFinal>(op, r_begin, r_end, s);
+    }
+  } else if (op.code) {
+    switch (mode) {
+      case kInner: launch_dict<Idx, kInner>(op, r_begin, r_end, s); break;
+      case kFactorEnd: launch_dict<Idx, kFactorEnd>(op, r_begin, r_end, s); break;
+      default: launch_dict<Idx, kFinal>(op, r_begin, r_end, s);
+    }
+  } else if (op.col16) launch_mode(op, op.col16, mode, r_begin, r_end, s);
   else launch_mode(op, op.col, mode, r_begin, r_end, s);
   count_launch();
 }
@@ -187,6 +546,45 @@ int compact_csr(const int64_t* rp, const int32_t* col, int64_t rows, int64_t row
   return 0;
 }
 
+int build_pair_dict(const int64_t* rp, const int32_t* col, const double* val, int64_t rows, int64_t row0,
+                    int64_t nnz, DevBuf& code_buf, int* ell_width, int32_t* dict_delta, double* dict_val,
+                    int* dict_size, bool* ok, cudaStream_t s) {
+  *ok = false;
+  *dict_size = 0;
+  *ell_width = 0;
+  if (rows <= 0) return 0;
+  DevBuf wsb;
+  NNB_TRY(wsb.alloc(sizeof(DictWs), s));
+  DictWs* ws = wsb.as<DictWs>();
+  NNB_CUDA(cudaMemsetAsync(ws, 0, sizeof(DictWs), s));
+  dict_insert_kernel<<<rows_grid(rows), 256, 0, s>>>(rp, col, val, rows, row0, ws);
+  dict_index_kernel<<<1, 1024, 0, s>>>(ws, dict_delta, dict_val);
+  int flags[5];  // count, overflow, collision, size, max_len
+  NNB_CUDA(cudaMemcpyAsync(flags, &ws->count, sizeof(flags), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  count_launch(2);
+  if (flags[1] || flags[3] > kPairDictMax - 1) return 0;  // code kEllPad stays free
+  // ELL order when rows are short and padding costs at most a quarter more codes
+  static const bool ell_on = !(std::getenv("NNB_DICT_ELL") && std::strcmp(std::getenv("NNB_DICT_ELL"), "0") == 0);
+  const int w = flags[4];
+  const bool ell = ell_on && w >= 1 && w <= kEllMaxWidth && (int64_t)w * rows * 4 <= nnz * 5;
+  NNB_TRY(code_buf.alloc(std::max<int64_t>(1, ell ? (int64_t)w * rows : nnz) + 16, s));  // +16: bulk-copy rounding
+  dict_encode_kernel<<<rows_grid(rows), 256, 0, s>>>(rp, col, val, rows, row0, ws, code_buf.as<uint8_t>(),
+                                                     ell ? w : 0, &ws->collision);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  NNB_CUDA(cudaMemcpyAsync(flags, &ws->count, sizeof(flags), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  if (flags[2]) {
+    code_buf.release();
+    return 0;
+  }
+  *dict_size = flags[3];
+  *ell_width = ell ? w : 0;
+  *ok = true;
+  return 0;
+}
+
 int spmv_csr(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n, const double* X, int64_t k,
              double* Y, cudaStream_t s) {
   if (n == 0) return 0;
@@ -198,10 +596,19 @@ int spmv_csr(const int64_t* row_ptr, const int32_t* col, const double* val, int6
 
 namespace {
 
+struct PairDict {
+  const uint8_t* code = nullptr;
+  const int32_t* delta = nullptr;
+  const double* val = nullptr;
+  int size = 0;
+  int ell_width = 0;
+  int64_t ell_rows = 0;
+};
+
 template <typename Idx>
 void run_factors(const Idx* rp, const int32_t* col, const int16_t* col16, const double* val, int64_t n,
                  const double* B, int64_t k, int s_factors, double theta, double* X, double* z[2], double* tb[2],
-                 int* flags, cudaStream_t s) {
+                 int* flags, cudaStream_t s, const PairDict& dict = PairDict{}) {
   const double* zcur = B;  // Z = B (read in place, never written)
   int zi = 0;
   int64_t reps = 1;
@@ -209,7 +616,8 @@ void run_factors(const Idx* rp, const int32_t* col, const int16_t* col16, const 
     const double* tin = zcur;  // t = Z
     int ti = 0;
     for (int64_t r = 0; r < reps; ++r) {
-      SpmvOp<Idx> op{rp, col, col16, 0, val, k, tin, tin, nullptr, zcur, theta, flags + f};
+      SpmvOp<Idx> op{rp, col, col16, 0, val, k, tin, tin, nullptr, zcur, theta, flags + f,
+                     dict.code, dict.delta, dict.val, dict.size, dict.ell_width, dict.ell_rows};
       int mode;
       if (r < reps - 1) {
         mode = kInner;
@@ -247,23 +655,43 @@ int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* 
   NNB_TRY(work.alloc(sizeof(double) * vec * 4 + sizeof(int) * 64 +
                          (narrow ? sizeof(int32_t) * (n + 1) + sizeof(int16_t) * nnz + 32 : 0),
                      s));
+  static const bool dict_on = [] {  // NNB_SPARSE_DICT=0: keep the column format (A/B measurement)
+    const char* e = std::getenv("NNB_SPARSE_DICT");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
   double* z[2] = {work.as<double>(), work.as<double>() + vec};
   double* tb[2] = {z[1] + vec, z[1] + 2 * vec};
   int* flags = reinterpret_cast<int*>(tb[1] + vec);
   NNB_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 64, s));
   if (narrow) {
-    // int32 offsets, and int16 column deltas when the operator's band allows
     int32_t* rp32 = flags + 64;
     int16_t* col16 = reinterpret_cast<int16_t*>(rp32 + n + 2);
-    bool fits = false;
-    NNB_TRY(compact_csr(row_ptr, col, n, 0, rp32, col16, &fits, s));
     static const bool force32 = [] {  // NNB_SPARSE_COL=32: int32 columns (A/B measurement)
       const char* e = std::getenv("NNB_SPARSE_COL");
       return e && std::strcmp(e, "32") == 0;
     }();
+    // operators with <= 255 distinct (column − row, value) pairs: 1 byte per nonzero
+    DevBuf dict_buf, code_buf;
+    PairDict dict;
+    if (dict_on && !force32) {
+      NNB_TRY(dict_buf.alloc((sizeof(int32_t) + sizeof(double)) * kPairDictMax, s));
+      double* dv = dict_buf.as<double>();
+      int32_t* dd = reinterpret_cast<int32_t*>(dv + kPairDictMax);
+      bool ok = false;
+      int size = 0, width = 0;
+      NNB_TRY(build_pair_dict(row_ptr, col, val, n, 0, nnz, code_buf, &width, dd, dv, &size, &ok, s));
+      if (ok) dict = PairDict{code_buf.as<uint8_t>(), dd, dv, size, width, n};
+    }
+    // int32 offsets, and int16 column deltas when the operator's band allows (the ELL
+    // dictionary needs neither)
+    bool fits = false;
+    if (!(dict.code && dict.ell_width)) NNB_TRY(compact_csr(row_ptr, col, n, 0, rp32, col16, &fits, s));
     fits = fits && !force32;
-    run_factors<int32_t>(rp32, col, fits ? col16 : nullptr, val, n, B, k, s_factors, theta, X, z, tb, flags, s);
+    set_sparse_bytes_per_nnz(dict.code ? 1 : (fits ? 10 : 12));
+    run_factors<int32_t>(rp32, col, fits ? col16 : nullptr, val, n, B, k, s_factors, theta, X, z, tb, flags, s,
+                         dict);
   } else {
+    set_sparse_bytes_per_nnz(12);
     run_factors<int64_t>(row_ptr, col, nullptr, val, n, B, k, s_factors, theta, X, z, tb, flags, s);
   }
   NNB_CUDA(cudaGetLastError());

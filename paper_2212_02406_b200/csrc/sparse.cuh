@@ -28,7 +28,35 @@ struct SpmvOp {
   const double* zold;   // indexed by owned row (factor end / final)
   double theta;
   int* flag;            // non-finite flag of this factor
+  // Pair dictionary (CSR-VI style, when the operator has <= 256 distinct
+  // (column − row, value) pairs, e.g. stencils): one uint8 code per nonzero
+  // replaces column and value.  Lookups are exact, so sums stay bit-identical.
+  const uint8_t* code = nullptr;
+  const int32_t* dict_delta = nullptr;
+  const double* dict_val = nullptr;
+  int dict_size = 0;
+  int ell_width = 0;  // > 0: slot-major ELL codes (code[i·ell_rows + r], kEllPad-padded), no row offsets
+  int64_t ell_rows = 0;
 };
+
+constexpr int kPairDictMax = 256;
+constexpr int kEllMaxWidth = 8;     // rows this short store their codes in ELL order
+constexpr uint8_t kEllPad = 255;    // ELL padding code (the dictionary keeps it free)
+
+// Bytes per nonzero of the format the last single-GPU sparse solve on this thread
+// consumed (1 = pair dictionary, 10 = int16 column deltas, 12 = int32 columns).
+void set_sparse_bytes_per_nnz(int b);
+int sparse_bytes_per_nnz();
+
+// Builds the pair dictionary of rows [0, rows) (global row index row0 + r; nonzeros
+// rp[r]..rp[r+1]) and allocates + fills code_buf: ELL order (*ell_width > 0) when
+// every row has at most kEllMaxWidth nonzeros and padding adds at most 25 %, else
+// CSR order (code[e − rp[0]]).  *ok = false when the operator has more than
+// kPairDictMax − 1 distinct pairs; the caller keeps its column format then.
+struct DevBuf;
+int build_pair_dict(const int64_t* rp, const int32_t* col, const double* val, int64_t rows, int64_t row0,
+                    int64_t nnz, DevBuf& code_buf, int* ell_width, int32_t* dict_delta, double* dict_val,
+                    int* dict_size, bool* ok, cudaStream_t s);
 
 template <typename Idx>
 void spmv_apply(const SpmvOp<Idx>& op, int mode, int64_t r_begin, int64_t r_end, cudaStream_t s);

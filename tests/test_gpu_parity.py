@@ -362,16 +362,18 @@ def test_sparse_long_rows_fallback(ref):
     assert np.array_equal(x, xr.real)
 
 
-def wide_band_csr(n: int = 100000, far: int = 40000):
+def wide_band_csr(n: int = 100000, far: int = 40000, jitter: bool = True):
     """Tridiagonal plus a symmetric coupling at distance `far` > 32767: the column
-    deltas do not fit int16, so the solve must take the int32-column kernels."""
+    deltas do not fit int16.  With `jitter` the values are all distinct (no pair
+    dictionary), so the solve must take the int32-column kernels."""
     rows, cols, vals = [], [], []
+    rng = np.random.default_rng(4)
     for i in range(n):
         for j, v in ((i - far, -0.5), (i - 1, -1.0), (i, 6.0), (i + 1, -1.0), (i + far, -0.5)):
             if 0 <= j < n:
                 rows.append(i)
                 cols.append(j)
-                vals.append(v)
+                vals.append(v * (1.0 + 0.01 * rng.random()) if jitter else v)
     rp = np.zeros(n + 1, np.int64)
     np.add.at(rp, np.array(rows) + 1, 1)
     return np.cumsum(rp), np.array(cols, np.int32), np.array(vals)
@@ -384,10 +386,59 @@ def test_sparse_wide_band_int32_columns(ref):
     norm = nnb.Normalization(theta=1.0 / 9.0, valid=True)
     xr, _, _ = ref.sparse_factorized(rp, col, val, b, 15, 1.0 / 9.0)
     x, _ = nnb.solve_sparse_factorized(nnb.Csr(rp, col, val, n=n), b, 15, norm)
-    assert np.array_equal(x, xr.real)
+    assert np.array_equal(x, xr.real) and nnb.sparse_last_bytes_per_nnz() == 12
+    # the same band with 5 distinct (delta, value) pairs: int32 deltas in the pair dictionary
+    rp, col, val = wide_band_csr(jitter=False)
+    xr, _, _ = ref.sparse_factorized(rp, col, val, b, 15, 1.0 / 9.0)
+    x, _ = nnb.solve_sparse_factorized(nnb.Csr(rp, col, val, n=n), b, 15, norm)
+    assert np.array_equal(x, xr.real) and nnb.sparse_last_bytes_per_nnz() == 1
     # two slabs: each remaps its wide columns into the halo-extended layout
     xs, _ = nnb.solve_sparse_factorized_sharded_emulated(nnb.Csr(rp, col, val, n=n), b, 15, norm, 2)
     assert np.array_equal(xs, xr.real)
+
+
+def banded_pairs_csr(n: int, n_values: int, seed: int):
+    """Random band [-7, 8] around the diagonal (the diagonal always present), values
+    drawn from `n_values` fixed numbers: up to 16·n_values distinct (delta, value) pairs."""
+    rng = np.random.default_rng(seed)
+    values = np.linspace(-1.0, 1.0, n_values) / 16.0
+    values[0] = -0.0  # signed zero: a pair of its own (bit comparison)
+    rp = np.zeros(n + 1, np.int64)
+    cols, vals = [], []
+    for i in range(n):
+        ds = [d for d in range(-7, 9) if 0 <= i + d < n and (d == 0 or rng.random() < 0.6)]
+        for d in ds:
+            cols.append(i + d)
+            vals.append(2.0 if d == 0 else values[rng.integers(n_values)])
+        rp[i + 1] = len(cols)
+    return rp, np.array(cols, np.int32), np.array(vals)
+
+
+@pytest.mark.parametrize("n_values,want", [(15, 1), (18, 10)])
+def test_sparse_pair_dictionary_boundary(ref, n_values, want):
+    """<= 256 distinct (column - row, value) pairs: 1-byte codes; more: int16 deltas.
+    Both bit-identical to the reference (15 values x 15 off-diagonal deltas + the
+    diagonal = 226 pairs; 18 values give up to 271)."""
+    rp, col, val = banded_pairs_csr(20000, n_values, seed=n_values)
+    n = rp.size - 1
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    pairs = len(set(zip((col - rows).tolist(), val.view(np.int64).tolist())))
+    assert (pairs <= 256) == (want == 1)
+    b = W.rhs(n, seed=3)
+    norm = nnb.Normalization(theta=0.25, valid=True)
+    x, _ = nnb.solve_sparse_factorized(nnb.Csr(rp, col, val, n=n), b, 31, norm)
+    assert nnb.sparse_last_bytes_per_nnz() == want
+    xr, _, _ = ref.sparse_factorized(rp, col, val, b, 31, 0.25)
+    assert np.array_equal(x, xr.real)
+
+
+def test_sparse_laplacian_uses_pair_dictionary(ref):
+    rp, col, val = W.laplacian_5pt(64)
+    b = W.rhs(64 * 64, seed=2)
+    x, _ = nnb.solve_sparse_factorized(nnb.Csr(rp, col, val, n=64 * 64), b, 63, nnb.Normalization(0.2, valid=True))
+    assert nnb.sparse_last_bytes_per_nnz() == 1
+    xr, _, _ = ref.sparse_factorized(rp, col, val, b, 63, 0.2)
+    assert np.array_equal(x, xr.real)
 
 
 def test_sparse_errors():
