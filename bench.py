@@ -534,10 +534,11 @@ def run_sparse(args, world, rank):
         comm.close()
     # the format the device consumed (csrc/sparse.cu): 1 = pair dictionary, 10 = f64 + int16 delta, 12
     fb = 10 if sharded else nnb.sparse_last_bytes_per_nnz()
-    fmt = {1: "1-byte (column - row, value) pair-dictionary codes", 10: "f64 values + int16 column deltas",
-           12: "f64 values + int32 columns"}[fb]
+    fmt = {1: "1-byte (column - row, value) pair-dictionary codes, slot-major ELL (no row offsets)",
+           10: "f64 values + int16 column deltas, int32 row offsets", 12: "f64 values + int32 columns, row offsets"}[fb]
+    mat = sparse_bytes(n, col.size, 10) - 2 * n * 8 if sharded else nnb.sparse_last_matrix_bytes()
     alg = 63 * sparse_bytes(n, col.size, 12)  # SURVEY §8(d) algorithmic bytes per solve: the work unit
-    moved = 63 * sparse_bytes(n, col.size, fb)  # bytes of the consumed format: the roofline
+    moved = 63 * (mat + 2 * n * 8)  # bytes of the consumed format (operator + t in + t out): the roofline
     gbs, moved_gbs = alg / (ms * 1e-3) / 1e9, moved / (ms * 1e-3) / 1e9
     return {"metric": "sparse factorized solve, 4096^2 5-pt Laplacian+I, gamma=63 (GB/s of SURVEY 8(d) algorithmic "
                       "bytes: 12 B per nonzero)", "value": round(gbs, 1),
@@ -547,8 +548,8 @@ def run_sparse(args, world, rank):
                          "frac": round(moved_gbs / (HBM_PEAK * world), 4),
                          "traffic": ncu_traffic("sparse_application") if grid == 4096 and not sharded else None,
                          "traffic_unit": "bytes per application (63 per solve)",
-                         "per_launch": f"nnz*{fb} + (N+1)*4 + 2N*8 bytes per application (x63, whole solve timed "
-                                       f"incl. the per-solve format pass): {fmt}, int32 row offsets, t in + t out"}}
+                         "per_launch": f"{mat} operator bytes + 2N*8 per application (x63, whole solve timed "
+                                       f"incl. the per-solve format pass): {fmt}; t in + t out"}}
 
 
 def cpu_sparse_sample(grid: int):

@@ -124,6 +124,7 @@ _SIGS = {
     "nnb_sparse_factorized_d": ([_dp, _dp, _dp, _i64, _i64, _dp, _i64, _i64, C.c_double, _dp, _dp, _dp,
                                  _dp], C.c_int),
     "nnb_sparse_last_bytes_per_nnz": ([], C.c_int),
+    "nnb_sparse_last_matrix_bytes": ([], C.c_int64),
     "nnb_gaussian_stream": ([C.c_uint64, _i64, _dp], C.c_int),
     "nnb_householder_q_d": ([_dp, _i64, _dp, _dp], C.c_int),
     "nnb_householder_q_z": ([_dp, _i64, _dp, _dp], C.c_int),
@@ -793,6 +794,11 @@ def sparse_last_bytes_per_nnz() -> int:
     """CSR bytes per nonzero the calling thread's last solve_sparse_factorized consumed:
     1 (pair dictionary), 10 (int16 column deltas) or 12 (int32 columns)."""
     return int(lib().nnb_sparse_last_bytes_per_nnz())
+
+
+def sparse_last_matrix_bytes() -> int:
+    """Operator bytes one application of the calling thread's last solve streamed."""
+    return int(lib().nnb_sparse_last_matrix_bytes())
 
 
 def solve_sparse_factorized_sharded(comm: Comm, csr_rows: Csr, n: int, b_rows, gamma: int, norm: Normalization):

@@ -37,9 +37,12 @@ namespace nnb {
 
 namespace {
 thread_local int g_sparse_bytes_per_nnz = 0;
+thread_local int64_t g_sparse_matrix_bytes = 0;
 }
 void set_sparse_bytes_per_nnz(int b) { g_sparse_bytes_per_nnz = b; }
 int sparse_bytes_per_nnz() { return g_sparse_bytes_per_nnz; }
+void set_sparse_matrix_bytes(int64_t b) { g_sparse_matrix_bytes = b; }
+int64_t sparse_matrix_bytes() { return g_sparse_matrix_bytes; }
 
 template <int MODE>
 __device__ __forceinline__ double finish(double tin, double y, double theta, double zold, bool& bad) {
@@ -322,8 +325,13 @@ __global__ void dict_encode_kernel(const int64_t* __restrict__ rp, const int32_t
   const int64_t base = rp[0];
   bool bad = false;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
-    if (ell_width)
+    if (ell_width) {
+      if (rp[r + 1] - rp[r] > ell_width) {  // longer than the sampled width: the caller retries in full
+        bad = true;
+        continue;
+      }
       for (int64_t i = rp[r + 1] - rp[r]; i < ell_width; ++i) code[i * rows + r] = kEllPad;
+    }
     for (int64_t e = rp[r], e1 = rp[r + 1]; e < e1; ++e) {
       const int32_t d = static_cast<int32_t>((int64_t)col[e] - (row0 + r));
       const unsigned long long b = __double_as_longlong(val[e]);
@@ -472,6 +480,7 @@ void launch_ell1_v(const SpmvOp<int32_t>& op, int64_t r_begin, int64_t r_end, cu
       op.t_ext, op.t_own, op.out, op.zold, op.theta, op.flag);
 }
 
+
 // rows of <= 5 nonzeros (2-D 5-point stencils) fit the 32-register budget
 template <int MODE, typename Idx>
 void launch_ell(const SpmvOp<Idx>& op, int64_t r_begin, int64_t r_end, cudaStream_t s) {
@@ -556,32 +565,52 @@ int build_pair_dict(const int64_t* rp, const int32_t* col, const double* val, in
   DevBuf wsb;
   NNB_TRY(wsb.alloc(sizeof(DictWs), s));
   DictWs* ws = wsb.as<DictWs>();
-  NNB_CUDA(cudaMemsetAsync(ws, 0, sizeof(DictWs), s));
-  dict_insert_kernel<<<rows_grid(rows), 256, 0, s>>>(rp, col, val, rows, row0, ws);
-  dict_index_kernel<<<1, 1024, 0, s>>>(ws, dict_delta, dict_val);
-  int flags[5];  // count, overflow, collision, size, max_len
-  NNB_CUDA(cudaMemcpyAsync(flags, &ws->count, sizeof(flags), cudaMemcpyDeviceToHost, s));
-  NNB_CUDA(cudaStreamSynchronize(s));
-  count_launch(2);
-  if (flags[1] || flags[3] > kPairDictMax - 1) return 0;  // code kEllPad stays free
-  // ELL order when rows are short and padding costs at most a quarter more codes
   static const bool ell_on = !(std::getenv("NNB_DICT_ELL") && std::strcmp(std::getenv("NNB_DICT_ELL"), "0") == 0);
-  const int w = flags[4];
-  const bool ell = ell_on && w >= 1 && w <= kEllMaxWidth && (int64_t)w * rows * 4 <= nnz * 5;
-  NNB_TRY(code_buf.alloc(std::max<int64_t>(1, ell ? (int64_t)w * rows : nnz) + 16, s));  // +16: bulk-copy rounding
-  dict_encode_kernel<<<rows_grid(rows), 256, 0, s>>>(rp, col, val, rows, row0, ws, code_buf.as<uint8_t>(),
-                                                     ell ? w : 0, &ws->collision);
-  count_launch();
-  NNB_CUDA(cudaGetLastError());
-  NNB_CUDA(cudaMemcpyAsync(flags, &ws->count, sizeof(flags), cudaMemcpyDeviceToHost, s));
-  NNB_CUDA(cudaStreamSynchronize(s));
-  if (flags[2]) {
-    code_buf.release();
+  // First try a dictionary (and ELL width) from the first and last kSample rows only:
+  // structured operators show every pair there (a stencil's boundary rows recur every
+  // grid row).  The encode pass verifies every nonzero against it; a missing pair or a
+  // longer row sends the build round again over all rows.  Results are bit-identical
+  // either way; only the order of the dictionary can differ.
+  constexpr int64_t kSample = 65536;
+  const bool can_sample = rows > 4 * kSample;
+  for (int full = can_sample ? 0 : 1; full < 2; ++full) {
+    NNB_CUDA(cudaMemsetAsync(ws, 0, sizeof(DictWs), s));
+    if (full) {
+      dict_insert_kernel<<<rows_grid(rows), 256, 0, s>>>(rp, col, val, rows, row0, ws);
+    } else {
+      dict_insert_kernel<<<rows_grid(kSample), 256, 0, s>>>(rp, col, val, kSample, row0, ws);
+      dict_insert_kernel<<<rows_grid(kSample), 256, 0, s>>>(rp + (rows - kSample), col, val, kSample,
+                                                            row0 + rows - kSample, ws);
+      count_launch();
+    }
+    dict_index_kernel<<<1, 1024, 0, s>>>(ws, dict_delta, dict_val);
+    int flags[5];  // count, overflow, collision, size, max_len
+    NNB_CUDA(cudaMemcpyAsync(flags, &ws->count, sizeof(flags), cudaMemcpyDeviceToHost, s));
+    NNB_CUDA(cudaStreamSynchronize(s));
+    count_launch(2);
+    if (flags[1] || flags[3] > kPairDictMax - 1) {  // code kEllPad stays free
+      if (full) return 0;
+      continue;
+    }
+    // ELL order when rows are short and padding costs at most a quarter more codes
+    const int w = flags[4];
+    const bool ell = ell_on && w >= 1 && w <= kEllMaxWidth && (int64_t)w * rows * 4 <= nnz * 5;
+    NNB_TRY(code_buf.alloc(std::max<int64_t>(1, ell ? (int64_t)w * rows : nnz), s));
+    dict_encode_kernel<<<rows_grid(rows), 256, 0, s>>>(rp, col, val, rows, row0, ws, code_buf.as<uint8_t>(),
+                                                       ell ? w : 0, &ws->collision);
+    count_launch();
+    NNB_CUDA(cudaGetLastError());
+    NNB_CUDA(cudaMemcpyAsync(flags, &ws->count, sizeof(flags), cudaMemcpyDeviceToHost, s));
+    NNB_CUDA(cudaStreamSynchronize(s));
+    if (flags[2]) {
+      code_buf.release();
+      continue;  // a pair (or row length) outside the sample; the full round decides
+    }
+    *dict_size = flags[3];
+    *ell_width = ell ? w : 0;
+    *ok = true;
     return 0;
   }
-  *dict_size = flags[3];
-  *ell_width = ell ? w : 0;
-  *ok = true;
   return 0;
 }
 
@@ -688,10 +717,15 @@ int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* 
     if (!(dict.code && dict.ell_width)) NNB_TRY(compact_csr(row_ptr, col, n, 0, rp32, col16, &fits, s));
     fits = fits && !force32;
     set_sparse_bytes_per_nnz(dict.code ? 1 : (fits ? 10 : 12));
+    // operator bytes one application streams: codes (ELL: width·n, no offsets) or values +
+    // columns, plus int32 row offsets
+    set_sparse_matrix_bytes(dict.ell_width ? (int64_t)dict.ell_width * n
+                                           : nnz * (dict.code ? 1 : (fits ? 10 : 12)) + (n + 1) * 4);
     run_factors<int32_t>(rp32, col, fits ? col16 : nullptr, val, n, B, k, s_factors, theta, X, z, tb, flags, s,
                          dict);
   } else {
     set_sparse_bytes_per_nnz(12);
+    set_sparse_matrix_bytes(nnz * 12 + (n + 1) * 8);
     run_factors<int64_t>(row_ptr, col, nullptr, val, n, B, k, s_factors, theta, X, z, tb, flags, s);
   }
   NNB_CUDA(cudaGetLastError());

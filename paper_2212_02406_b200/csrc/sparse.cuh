@@ -47,6 +47,9 @@ constexpr uint8_t kEllPad = 255;    // ELL padding code (the dictionary keeps it
 // consumed (1 = pair dictionary, 10 = int16 column deltas, 12 = int32 columns).
 void set_sparse_bytes_per_nnz(int b);
 int sparse_bytes_per_nnz();
+// Operator bytes (codes or values + columns, plus row offsets) one application of that solve streams.
+void set_sparse_matrix_bytes(int64_t b);
+int64_t sparse_matrix_bytes();
 
 // Builds the pair dictionary of rows [0, rows) (global row index row0 + r; nonzeros
 // rp[r]..rp[r+1]) and allocates + fills code_buf: ELL order (*ell_width > 0) when

@@ -432,6 +432,33 @@ def test_sparse_pair_dictionary_boundary(ref, n_values, want):
     assert np.array_equal(x, xr.real)
 
 
+def test_sparse_pair_dictionary_sample_miss(ref):
+    """The dictionary is first built from the first and last 65536 rows; a pair (and a
+    longer row) that only occurs in the middle must send the build round again over
+    all rows -- still 1 byte per nonzero, still bit-identical."""
+    n = 400000
+    mid = n // 2
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        ents = [(i - 1, -1.0), (i, 4.0), (i + 1, -1.0)]
+        if i == mid:
+            ents = [(i - 2, 0.125), (i - 1, -1.0), (i, 4.0), (i + 1, -1.0), (i + 2, 0.375)]  # new pairs, width 5
+        for j, v in ents:
+            if 0 <= j < n:
+                rows.append(i)
+                cols.append(j)
+                vals.append(v)
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, np.array(rows) + 1, 1)
+    rp = np.cumsum(rp)
+    col, val = np.array(cols, np.int32), np.array(vals)
+    b = W.rhs(n, seed=5)
+    x, _ = nnb.solve_sparse_factorized(nnb.Csr(rp, col, val, n=n), b, 15, nnb.Normalization(0.25, valid=True))
+    assert nnb.sparse_last_bytes_per_nnz() == 1
+    xr, _, _ = ref.sparse_factorized(rp, col, val, b, 15, 0.25)
+    assert np.array_equal(x, xr.real)
+
+
 def test_sparse_laplacian_uses_pair_dictionary(ref):
     rp, col, val = W.laplacian_5pt(64)
     b = W.rhs(64 * 64, seed=2)
