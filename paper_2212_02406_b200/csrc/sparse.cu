@@ -29,6 +29,7 @@
 // 48 warps; 1024-thread blocks shave another 1.6 % (12.8 ms).
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "engine.cuh"
 #include "sparse.cuh"
@@ -316,12 +317,12 @@ __global__ void dict_index_kernel(DictWs* ws, int32_t* __restrict__ dict_delta, 
   }
 }
 
-// ell_width > 0: slot-major ELL, row r's i-th nonzero (CSR order) at code[i·rows + r],
+// ell_width > 0: slot-major ELL, row r's i-th nonzero (CSR order) at code[i·plane + r],
 // padded with kEllPad (no row offsets needed; a warp's load of one slot is 32
 // consecutive bytes); else code[e − rp[0]] (CSR order).
 __global__ void dict_encode_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                                    const double* __restrict__ val, int64_t rows, int64_t row0, const DictWs* ws,
-                                   uint8_t* __restrict__ code, int ell_width, int* collision) {
+                                   uint8_t* __restrict__ code, int ell_width, int64_t plane, int* collision) {
   const int64_t base = rp[0];
   bool bad = false;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
@@ -330,7 +331,7 @@ __global__ void dict_encode_kernel(const int64_t* __restrict__ rp, const int32_t
         bad = true;
         continue;
       }
-      for (int64_t i = rp[r + 1] - rp[r]; i < ell_width; ++i) code[i * rows + r] = kEllPad;
+      for (int64_t i = rp[r + 1] - rp[r]; i < ell_width; ++i) code[i * plane + r] = kEllPad;
     }
     for (int64_t e = rp[r], e1 = rp[r + 1]; e < e1; ++e) {
       const int32_t d = static_cast<int32_t>((int64_t)col[e] - (row0 + r));
@@ -346,7 +347,7 @@ __global__ void dict_encode_kernel(const int64_t* __restrict__ rp, const int32_t
       const bool hit = ws->hash[slot] == h && ws->delta[slot] == d &&
                        __double_as_longlong(ws->val[slot]) == static_cast<long long>(b);
       bad |= !hit;
-      code[ell_width ? (e - rp[r]) * rows + r : e - base] = static_cast<uint8_t>(hit ? ws->index[slot] : 0);
+      code[ell_width ? (e - rp[r]) * plane + r : e - base] = static_cast<uint8_t>(hit ? ws->index[slot] : 0);
     }
   }
   if (bad) atomicOr(collision, 1);
@@ -556,11 +557,12 @@ int compact_csr(const int64_t* rp, const int32_t* col, int64_t rows, int64_t row
 }
 
 int build_pair_dict(const int64_t* rp, const int32_t* col, const double* val, int64_t rows, int64_t row0,
-                    int64_t nnz, DevBuf& code_buf, int* ell_width, int32_t* dict_delta, double* dict_val,
-                    int* dict_size, bool* ok, cudaStream_t s) {
+                    int64_t nnz, DevBuf& code_buf, int* ell_width, int64_t* ell_plane, int* band_lo, int* band_hi,
+                    int32_t* dict_delta, double* dict_val, int* dict_size, bool* ok, cudaStream_t s) {
   *ok = false;
   *dict_size = 0;
   *ell_width = 0;
+  *ell_plane = 0;
   if (rows <= 0) return 0;
   DevBuf wsb;
   NNB_TRY(wsb.alloc(sizeof(DictWs), s));
@@ -595,9 +597,10 @@ int build_pair_dict(const int64_t* rp, const int32_t* col, const double* val, in
     // ELL order when rows are short and padding costs at most a quarter more codes
     const int w = flags[4];
     const bool ell = ell_on && w >= 1 && w <= kEllMaxWidth && (int64_t)w * rows * 4 <= nnz * 5;
-    NNB_TRY(code_buf.alloc(std::max<int64_t>(1, ell ? (int64_t)w * rows : nnz), s));
+    const int64_t plane = (rows + 15) / 16 * 16;  // 16-byte aligned slot planes
+    NNB_TRY(code_buf.alloc(std::max<int64_t>(1, ell ? (int64_t)w * plane : nnz), s));
     dict_encode_kernel<<<rows_grid(rows), 256, 0, s>>>(rp, col, val, rows, row0, ws, code_buf.as<uint8_t>(),
-                                                       ell ? w : 0, &ws->collision);
+                                                       ell ? w : 0, plane, &ws->collision);
     count_launch();
     NNB_CUDA(cudaGetLastError());
     NNB_CUDA(cudaMemcpyAsync(flags, &ws->count, sizeof(flags), cudaMemcpyDeviceToHost, s));
@@ -608,6 +611,14 @@ int build_pair_dict(const int64_t* rp, const int32_t* col, const double* val, in
     }
     *dict_size = flags[3];
     *ell_width = ell ? w : 0;
+    *ell_plane = ell ? plane : 0;
+    std::vector<int32_t> dh(flags[3]);
+    NNB_CUDA(cudaMemcpy(dh.data(), dict_delta, sizeof(int32_t) * dh.size(), cudaMemcpyDeviceToHost));
+    *band_lo = *band_hi = 0;
+    for (int32_t d : dh) {
+      *band_lo = std::min(*band_lo, d);
+      *band_hi = std::max(*band_hi, d);
+    }
     *ok = true;
     return 0;
   }
@@ -631,7 +642,8 @@ struct PairDict {
   const double* val = nullptr;
   int size = 0;
   int ell_width = 0;
-  int64_t ell_rows = 0;
+  int64_t ell_rows = 0;  // slot-plane stride
+  int band_lo = 0, band_hi = 0;
 };
 
 template <typename Idx>
@@ -646,7 +658,8 @@ void run_factors(const Idx* rp, const int32_t* col, const int16_t* col16, const 
     int ti = 0;
     for (int64_t r = 0; r < reps; ++r) {
       SpmvOp<Idx> op{rp, col, col16, 0, val, k, tin, tin, nullptr, zcur, theta, flags + f,
-                     dict.code, dict.delta, dict.val, dict.size, dict.ell_width, dict.ell_rows};
+                     dict.code, dict.delta, dict.val, dict.size, dict.ell_width, dict.ell_rows, dict.band_lo,
+                     dict.band_hi};
       int mode;
       if (r < reps - 1) {
         mode = kInner;
@@ -707,9 +720,11 @@ int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* 
       double* dv = dict_buf.as<double>();
       int32_t* dd = reinterpret_cast<int32_t*>(dv + kPairDictMax);
       bool ok = false;
-      int size = 0, width = 0;
-      NNB_TRY(build_pair_dict(row_ptr, col, val, n, 0, nnz, code_buf, &width, dd, dv, &size, &ok, s));
-      if (ok) dict = PairDict{code_buf.as<uint8_t>(), dd, dv, size, width, n};
+      int size = 0, width = 0, lo = 0, hi = 0;
+      int64_t plane = 0;
+      NNB_TRY(build_pair_dict(row_ptr, col, val, n, 0, nnz, code_buf, &width, &plane, &lo, &hi, dd, dv, &size, &ok,
+                              s));
+      if (ok) dict = PairDict{code_buf.as<uint8_t>(), dd, dv, size, width, plane, lo, hi};
     }
     // int32 offsets, and int16 column deltas when the operator's band allows (the ELL
     // dictionary needs neither)

@@ -36,7 +36,8 @@ struct SpmvOp {
   const double* dict_val = nullptr;
   int dict_size = 0;
   int ell_width = 0;  // > 0: slot-major ELL codes (code[i·ell_rows + r], kEllPad-padded), no row offsets
-  int64_t ell_rows = 0;
+  int64_t ell_rows = 0;  // slot-plane stride (rows rounded up to 16)
+  int band_lo = 0, band_hi = 0;  // min / max (column − row) over the dictionary
 };
 
 constexpr int kPairDictMax = 256;
@@ -58,8 +59,8 @@ int64_t sparse_matrix_bytes();
 // kPairDictMax − 1 distinct pairs; the caller keeps its column format then.
 struct DevBuf;
 int build_pair_dict(const int64_t* rp, const int32_t* col, const double* val, int64_t rows, int64_t row0,
-                    int64_t nnz, DevBuf& code_buf, int* ell_width, int32_t* dict_delta, double* dict_val,
-                    int* dict_size, bool* ok, cudaStream_t s);
+                    int64_t nnz, DevBuf& code_buf, int* ell_width, int64_t* ell_plane, int* band_lo, int* band_hi,
+                    int32_t* dict_delta, double* dict_val, int* dict_size, bool* ok, cudaStream_t s);
 
 template <typename Idx>
 void spmv_apply(const SpmvOp<Idx>& op, int mode, int64_t r_begin, int64_t r_end, cudaStream_t s);

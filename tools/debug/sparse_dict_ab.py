@@ -24,6 +24,6 @@ for gamma in (1, 63):
     torch.cuda.synchronize()
     res[gamma] = e0.elapsed_time(e1) / 10
 per = (res[63] - res[1]) / 62
-print("dict=%s contig=%s bytes/nnz=%d solve63=%.3f ms  per-application=%.1f us  fixed=%.3f ms" % (
-    os.environ.get("NNB_SPARSE_DICT", "1"), os.environ.get("NNB_ELL_CONTIG", "1"), nnb.sparse_last_bytes_per_nnz(),
+print("dict=%s win=%s bytes/nnz=%d solve63=%.3f ms  per-application=%.1f us  fixed=%.3f ms" % (
+    os.environ.get("NNB_SPARSE_DICT", "1"), os.environ.get("NNB_DICT_WIN", "1"), nnb.sparse_last_bytes_per_nnz(),
     res[63], per * 1e3, res[1] - per))
