@@ -257,6 +257,10 @@ def run_dense(args, world, rank):
                          "per_launch": f"2*rows*N^2 = {2.0 * rows_here * n * n:.4g} flop (rows={rows_here}, N={n}), "
                                        f"{p + 1} launches per nest" + (f" x {world} K-split partials" if world > 1 else ""),
                          "peak_source": FP64_PEAK_SOURCE})
+    # NNB_ORDER_SYMMETRIC on the same nest (A == A^T, X a polynomial in A): upper
+    # tile triangles, mirrored — time per nest, reported beside the headline
+    if not sharded and args.symmetric:
+        out["symmetric"] = run_dense_symmetric(nnb, torch, a, n, p, args)
     # e2e through the C-ABI with HOST buffers (pinned): H2D of A and X, one nest, D2H of X
     if args.e2e:
         shape = tuple(a.shape)
@@ -286,6 +290,25 @@ def run_dense(args, world, rank):
     if sharded:
         comm.close()
     return out
+
+
+def run_dense_symmetric(nnb, torch, a, n, p, args):
+    """The same nests in NNB_ORDER_SYMMETRIC (the order requires the chain to
+    build X0 = A^T/(|A|_1|A|_inf) itself, so the K nests run as one call)."""
+    k = max(1, min(args.steps, 3))
+    nnb.nn_chain(a, None, p=p, max_iters=1, final_residual=False, order=nnb.ORDER_SYMMETRIC)  # warm
+    torch.cuda.synchronize()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        xs, rs = nnb.nn_chain(a, None, p=p, max_iters=k, final_residual=False, order=nnb.ORDER_SYMMETRIC)
+        torch.cuda.synchronize()
+    ms_nest = rs.device_ms / k
+    full = (p + 1) * 2.0 * n ** 3
+    return {"order": "NNB_ORDER_SYMMETRIC (upper tile triangle of every product, mirrored)",
+            "nests": k, "ms_per_nest": round(ms_nest, 2),
+            "tflops_executed": round(full * sym_fraction(n) / (ms_nest * 1e-3) / 1e12, 3),
+            "full_product_equivalent_tflops": round(full / (ms_nest * 1e-3) / 1e12, 3),
+            "eps_first_last": [rs.history[0][1], rs.history[-1][1]], "clocks": clk.summary(),
+            "note": "not the headline: the headline times full products, valid for any X0"}
 
 
 def cpu_dense_sample(n_sample: int, p: int):
@@ -350,6 +373,12 @@ def run_c1(args, rank):
     return out
 
 
+def sym_fraction(n: int, tile: int = 128) -> float:
+    """Share of an n×n product's tiles the symmetric order computes (tm <= tn)."""
+    t = (n + tile - 1) // tile
+    return (t * (t + 1) / 2) / (t * t)
+
+
 def run_c3(args):
     """BASELINE config 2: N=4096, A = Q diag(lambda) Q^T (kappa 1e3), X0 = A^T/(|A|_1|A|_inf),
     p in {1,2,3}, iterate to eps < 1e-12 — nests needed and TFLOP/s per depth."""
@@ -374,6 +403,20 @@ def run_c3(args):
                         "eps_last": rep.history[-1][1], "wall_ms": round(wall * 1e3, 2),
                         "device_ms": round(rep.device_ms, 2),
                         "tflops_device": round(flops / (rep.device_ms * 1e-3) / 1e12, 3)}
+        # NNB_ORDER_SYMMETRIC: the same chain computing each product's upper tile triangle
+        xs, rs = nnb.nn_chain(a, None, p=p, max_iters=80, tol=1e-12, order=nnb.ORDER_SYMMETRIC)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        xs, rs = nnb.nn_chain(a, None, p=p, max_iters=80, tol=1e-12, order=nnb.ORDER_SYMMETRIC)
+        torch.cuda.synchronize()
+        wall_s = time.perf_counter() - t0
+        executed = rs.products * 2.0 * 4096 ** 3 * sym_fraction(4096)
+        res[f"p{p}"]["symmetric"] = {
+            "nests": rs.iters, "stopped": rs.stopped_reason, "eps_last": rs.history[-1][1],
+            "wall_ms": round(wall_s * 1e3, 2), "device_ms": round(rs.device_ms, 2),
+            "tflops_executed": round(executed / (rs.device_ms * 1e-3) / 1e12, 3),
+            "x_rel_frob_vs_full": float(torch.linalg.norm(xs - x) / torch.linalg.norm(x)),
+            "speedup_time_to_solution": round(rep.device_ms / rs.device_ms, 3)}
     return {"metric": "config 2: nests to eps < 1e-12 and FP64 TFLOP/s at N=4096 (kappa 1e3)", "depths": res,
             "input": f"nn::random_spd(4096, 1e3, seed=3) on the device, bit-identical to the reference's "
                      f"({gen_s:.2f} s incl. the host GaussianStream)"}
@@ -581,6 +624,8 @@ def main():
     ap.add_argument("--grid", type=int, default=4096)
     ap.add_argument("--legs", default="dense,mimo,sparse,c1,c3")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-symmetric", dest="symmetric", action="store_false",
+                    help="skip the NNB_ORDER_SYMMETRIC timing beside the headline nest")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU (sharded) dense/sparse paths even at one rank (code-path check)")
@@ -634,6 +679,8 @@ def main():
                     roofline=d["roofline"], clocks=d["clocks"], gpu_launches=d["launches"])
         if "e2e" in d:
             line["e2e"] = d["e2e"]
+        if "symmetric" in d:
+            line["legs"]["dense_symmetric"] = d["symmetric"]
         config["eps_first_last"] = [d["eps_first"], d["eps_last"]]
     if "mimo" in legs:
         line["legs"]["mimo"] = run_mimo(args, world, rank)

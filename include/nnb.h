@@ -51,7 +51,13 @@ enum nnb_status {
 /* Operand order of the nest ("Product order").
  * NORTHSTAR: R = I - A X,  X' = X (I + R + ... + R^p)  (right-multiply Horner)
  * REFERENCE: P = I - X A,  X' = (I + P + ... + P^p) X  (proj/src/solver.cpp:93-103) */
-enum nnb_order { NNB_ORDER_NORTHSTAR = 0, NNB_ORDER_REFERENCE = 1 };
+/* SYMMETRIC: the NORTHSTAR order for real A == A^T with X0 a scaled identity
+ *   or A^T/(||A||_1 ||A||_inf).  Every iterate and residual is then a
+ *   polynomial in A, hence symmetric, and each product computes only its
+ *   upper tile triangle and mirrors it (about half the DMMA work; results
+ *   agree with NORTHSTAR to rounding).  Checked on entry: NNB_ERR_DOMAIN
+ *   otherwise (and for complex chains and the sharded chain). */
+enum nnb_order { NNB_ORDER_NORTHSTAR = 0, NNB_ORDER_REFERENCE = 1, NNB_ORDER_SYMMETRIC = 2 };
 
 /* Initial iterate. */
 enum nnb_x0 {

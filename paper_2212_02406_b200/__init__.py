@@ -67,7 +67,7 @@ class SingularMatrixError(Error):
 _STATUS = {1: ShapeError, 2: DomainError, 3: DivergenceError, 4: ContractionError, 5: PlanError,
            6: BudgetError, 7: DeviceError, 8: DeviceError, 9: DeviceError, 10: DeviceError, 11: SingularMatrixError}
 
-ORDER_NORTHSTAR, ORDER_REFERENCE = 0, 1
+ORDER_NORTHSTAR, ORDER_REFERENCE, ORDER_SYMMETRIC = 0, 1, 2
 X0_GIVEN, X0_SCALED_IDENTITY, X0_TRANSPOSE_NORM, X0_JACOBI = 0, 1, 2, 3
 
 

@@ -96,13 +96,26 @@ int chain_cfg(const nnb_chain_config* cfg, ChainCfg* c) {
   if (!cfg) return fail(NNB_ERR_DOMAIN, "nn chain: config is NULL");
   if (cfg->depth_p < 0) return fail(NNB_ERR_DOMAIN, "nn chain: depth must be >= 0");
   if (cfg->max_iters < 0) return fail(NNB_ERR_DOMAIN, "nn chain: max_iters must be >= 0");
-  if (cfg->order != NNB_ORDER_NORTHSTAR && cfg->order != NNB_ORDER_REFERENCE)
+  if (cfg->order != NNB_ORDER_NORTHSTAR && cfg->order != NNB_ORDER_REFERENCE && cfg->order != NNB_ORDER_SYMMETRIC)
     return fail(NNB_ERR_DOMAIN, "nn chain: unknown operand order");
   c->p = cfg->depth_p;
   c->max_iters = cfg->max_iters;
   c->tol = cfg->tol;
   c->order = cfg->order;
   c->final_residual = cfg->final_residual;
+  return 0;
+}
+
+// NNB_ORDER_SYMMETRIC preconditions: X0 a polynomial in A (scaled identity or
+// Aᵀ/(‖A‖₁‖A‖∞)) and A exactly symmetric, so that every iterate and residual is
+// symmetric and the products may compute their upper tile triangle only.
+int symmetric_check(const nnb_chain_config* cfg, const double* A, int64_t n, int64_t ld, cudaStream_t s) {
+  if (cfg->order != NNB_ORDER_SYMMETRIC) return 0;
+  if (cfg->x0_kind != NNB_X0_SCALED_IDENTITY && cfg->x0_kind != NNB_X0_TRANSPOSE_NORM)
+    return fail(NNB_ERR_DOMAIN, "nn chain: the symmetric order needs X0 = scaled identity or A^T/(|A|_1|A|_inf)");
+  bool sym = false;
+  NNB_TRY(is_symmetric_dev(A, n, ld, &sym, s));
+  if (!sym) return fail(NNB_ERR_DOMAIN, "nn chain: the symmetric order needs A == A^T");
   return 0;
 }
 
@@ -193,6 +206,7 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
     io.a_ready = a_ready;  // the first product consumes A chunk by chunk
   } else {
     NNB_CUDA(cudaStreamWaitEvent(s, in_done, 0));
+    NNB_TRY(symmetric_check(cfg, a.d, n, a.ld, s));
     if (!x0_given) NNB_TRY(x0_build(a.d, a.ld, n, cfg->x0_kind, cfg->x0_scale, x.d, x.ld, s));
   }
   ChainOut o;
@@ -583,6 +597,7 @@ int nnb_nn_chain_d(const double* A, int64_t n, const double* X0, const nnb_chain
     return chain_d_streamed(A, n, X0, cfg, c, X_out, eps_hist, result, s);
   DMat a;
   NNB_TRY(a.load(A, n, n, n, s));
+  NNB_TRY(symmetric_check(cfg, a.d, n, a.ld, s));
   DMat x;  // working X with A's leading dimension: the caller's device X_out when it fits
   x.rows = x.cols = n;
   x.ld = a.ld;
@@ -617,6 +632,8 @@ int nnb_nn_chain_z(const double* A, int64_t n, const double* X0, const nnb_chain
   if (n < 1) return fail(NNB_ERR_SHAPE, "nn chain: matrix must be square and non-empty");
   ChainCfg c;
   NNB_TRY(chain_cfg(cfg, &c));
+  if (cfg->order == NNB_ORDER_SYMMETRIC)
+    return fail(NNB_ERR_DOMAIN, "nn chain (complex): the symmetric order is real-only");
   cudaStream_t s = resolve(stream);
   ZMat a, x;
   NNB_TRY(a.load(A, n, n, s));

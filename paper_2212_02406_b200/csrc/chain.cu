@@ -57,6 +57,7 @@ struct Ctx {
 
   int* nf2 = nullptr;
   cudaStream_t s;
+  bool sym = false;  // real products with symmetric output (upper tiles + mirror)
 };
 
 // C = alpha·(A·B) + beta·D + gamma·I, with optional Σ|C|² → eps_out and
@@ -80,6 +81,7 @@ int product(Ctx& c, const Plane& A, const Plane& B, double alpha, const Plane* D
     op.ep.eps_out = eps_out;
     op.ep.eps_scale = eps_scale;
     op.ep.nf_out = nf_out;
+    op.ep.sym = c.sym;
     return gemm(op, nf_out ? &c.red : nullptr, c.s);
   }
   const bool red = nf_out != nullptr;
@@ -254,7 +256,11 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
   NNB_CUDA(cudaEventRecord(e0, c.s));
 
   const bool tol_mode = cfg.tol > 0.0;
-  const int order = exact ? 1 : cfg.order;
+  // SYMMETRIC (order 2): the NORTHSTAR operand order with every product's
+  // upper tile triangle computed and mirrored (the caller checked that A is
+  // symmetric and X0 a polynomial in A, so every iterate and residual is)
+  const int order = exact ? 1 : (cfg.order == 2 ? 0 : cfg.order);
+  c.sym = !exact && !c.cplx && cfg.order == 2;
   int k = 0, products = 0, stopped = 1, recorded = 0;
   if (small)
     NNB_TRY(small_chain_real(A.re, X.re, R.re, bufs[1].re, bufs[2].re, n, c.ld, cfg, eps_dev, nf_dev, status_dev, c.s));
@@ -303,9 +309,9 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
       int dst_i = (xi + 1) % 3;
       for (int j = 1; j <= p; ++j) {
         const Plane& dst = bufs[dst_i];
-        const Plane& l = cfg.order == 0 ? v : R;
-        const Plane& r = cfg.order == 0 ? R : v;
-        if (io && io->host_out && !tol_mode && j == p && k == cfg.max_iters - 1 && cfg.order == 0) {
+        const Plane& l = order == 0 ? v : R;
+        const Plane& r = order == 0 ? R : v;
+        if (io && io->host_out && !tol_mode && j == p && k == cfg.max_iters - 1 && order == 0) {
           // the final X: rows leave for the host as their chunk completes
           NNB_TRY(product_chunked(c, l, r, 1.0, &Xk, 1.0, 0.0, dst, nullptr, nf_dev + k * (p + 1) + j, *io, false,
                                   true, chunk_ss, chunk_nf));

@@ -440,7 +440,7 @@ int small_chain_real(const double* A, double* X, double* R, double* w1, double* 
   a.p = cfg.p;
   a.max_iters = cfg.max_iters;
   a.final_residual = cfg.final_residual;
-  a.order = cfg.order;
+  a.order = cfg.order == 1 ? 1 : 0;  // SYMMETRIC runs the NORTHSTAR order with full products here
   a.tol_mode = cfg.tol > 0.0;
   a.tol = cfg.tol;
   a.eps_scale = 1.0 / std::sqrt(static_cast<double>(n));

@@ -230,7 +230,8 @@ static int launch_cfg(const GemmOp& op, cudaStream_t s) {
                                   smem));
     attr_set = true;
   }
-  const int64_t tiles = ((op.M + Cfg::kBM - 1) / Cfg::kBM) * ((op.N + Cfg::kBN - 1) / Cfg::kBN);
+  const int64_t tm = (op.M + Cfg::kBM - 1) / Cfg::kBM;
+  const int64_t tiles = op.ep.sym ? tm * (tm + 1) / 2 : tm * ((op.N + Cfg::kBN - 1) / Cfg::kBN);
   gemm_f64_kernel<Cfg><<<static_cast<unsigned>(tiles), Cfg::kThreads, smem, s>>>(
       ta, tb, static_cast<int>(op.M), static_cast<int>(op.N), static_cast<int>(op.K), op.ep);
   count_launch();
@@ -275,6 +276,9 @@ int gemm(GemmOp op, RedWs* red, cudaStream_t s) {
       (op.ep.D2 && ((reinterpret_cast<uintptr_t>(op.ep.D2) & 15) || (op.ep.ldd2 & 1))))
     return fail(7, "gemm: epilogue operands need 16B alignment and even leading dimensions");
   if (op.ep.C2 && arith() == 1) return fail(7, "gemm: the dual-output epilogue has no reference-exact form");
+  if (op.ep.sym && (op.M != op.N || op.b_kmajor || op.ep.C2 || op.ep.diag_offset != 0))
+    return fail(7, "gemm: symmetric output needs a square product, one output and no diagonal offset");
+  if (op.ep.sym && arith() == 1) op.ep.sym = 0;  // the exact loops compute every element
   if (red) {
     if (red->capacity < max_tiles_for(op.M, op.N)) return fail(7, "gemm: reduction workspace too small");
     op.ep.ss_partial = red->ss_partial;
@@ -682,6 +686,45 @@ int is_identity_dev(const double* re, const double* im, int64_t n, int64_t ld, b
   NNB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
   is_identity_kernel<<<grid_for(n * n), 256, 0, s>>>(re, im, n, ld, flag.as<int>());
   count_launch();
+  int h = 0;
+  NNB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  *result = h == 0;
+  return 0;
+}
+
+// A == Aᵀ, bit for bit (a NaN equal to its mirror counts as symmetric, so
+// non-finite input still reaches the chain's divergence check).  32×32 tile
+// pairs through shared memory: both sides of the diagonal read coalesced.
+__global__ void is_symmetric_kernel(const double* __restrict__ A, int64_t n, int64_t ld, int* __restrict__ bad) {
+  __shared__ double t[32][33];
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;
+  if (bj < bi) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int k = ty; k < 32; k += 8) {  // tile (bj, bi), stored transposed
+    const int64_t r = bj * 32 + k, c = bi * 32 + tx;
+    t[tx][k] = (r < n && c < n) ? A[r * ld + c] : 0.0;
+  }
+  __syncthreads();
+  bool b = false;
+  for (int k = ty; k < 32; k += 8) {  // tile (bi, bj) against it
+    const int64_t r = bi * 32 + k, c = bj * 32 + tx;
+    if (r < n && c < n) {
+      const double v = A[r * ld + c], w = t[k][tx];
+      b |= !(v == w || __double_as_longlong(v) == __double_as_longlong(w));
+    }
+  }
+  if (__syncthreads_or(b) && tx == 0 && ty == 0) atomicOr(bad, 1);
+}
+
+int is_symmetric_dev(const double* A, int64_t n, int64_t ld, bool* result, cudaStream_t s) {
+  DevBuf flag;
+  NNB_TRY(flag.alloc(sizeof(int), s));
+  NNB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+  const unsigned tiles = static_cast<unsigned>((n + 31) / 32);
+  is_symmetric_kernel<<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(A, n, ld, flag.as<int>());
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
   int h = 0;
   NNB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   NNB_CUDA(cudaStreamSynchronize(s));

@@ -214,6 +214,8 @@ int nn_explicit_dev(const double* phi_re, const double* phi_im, const double* w_
                     double* products, cudaStream_t s);
 int is_identity_dev(const double* re, const double* im, int64_t n, int64_t ld, bool* result,
                     cudaStream_t s);
+// A == Aᵀ exactly (synchronises s)
+int is_symmetric_dev(const double* A, int64_t n, int64_t ld, bool* result, cudaStream_t s);
 int deinterleave2d(const double* z, int64_t rows, int64_t cols, double* re, double* im,
                    int64_t ldp, cudaStream_t s);
 int interleave2d(const double* re, const double* im, int64_t rows, int64_t cols, int64_t ldp,

@@ -42,6 +42,11 @@ struct GemmEpilogue {
   const double* D2 = nullptr;
   int64_t ldd2 = 0;
   double alpha2 = 0.0, beta2 = 0.0;
+  // symmetric output (square C, no C2, diag_offset 0): only tiles tm <= tn are
+  // computed; off-diagonal tiles also store their transpose and count twice in
+  // the Σ C² / non-finite reduction.  Valid when A·B is symmetric, e.g. both
+  // operands polynomials in one symmetric matrix (DESIGN.md §3 K1-K3).
+  int sym = 0;
   // Σ C² / non-finite reduction (all nullable => skipped)
   double* ss_partial = nullptr;  // [num_tiles]
   int* nf_partial = nullptr;     // [num_tiles]
@@ -93,11 +98,37 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
   constexpr int GROUP_M = 8;
   const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
   const int pid = blockIdx.x;
-  const int group = pid / (GROUP_M * tiles_n);
-  const int first_m = group * GROUP_M;
-  const int gsz = min(tiles_m - first_m, GROUP_M);
-  const int tm = first_m + (pid % gsz);
-  const int tn = (pid % (GROUP_M * tiles_n)) / gsz;
+  int tm, tn;
+  if (!ep.sym) {
+    const int group = pid / (GROUP_M * tiles_n);
+    const int first_m = group * GROUP_M;
+    const int gsz = min(tiles_m - first_m, GROUP_M);
+    tm = first_m + (pid % gsz);
+    tn = (pid % (GROUP_M * tiles_n)) / gsz;
+  } else {
+    // upper-triangular tiles, same grouping: a group of gsz tile-rows starting
+    // at f owns a gsz-row triangle (column-major) then a gsz-row rectangle
+    int f = 0, rem = pid, gsz = min(tiles_m, GROUP_M);
+    for (;;) {
+      gsz = min(tiles_m - f, GROUP_M);
+      const int cnt = gsz * (gsz + 1) / 2 + gsz * (tiles_n - f - gsz);
+      if (rem < cnt) break;
+      rem -= cnt;
+      f += gsz;
+    }
+    const int tri = gsz * (gsz + 1) / 2;
+    if (rem < tri) {
+      int c = 0;
+      while (rem >= c + 1) rem -= ++c;
+      tn = f + c;
+      tm = f + rem;
+    } else {
+      rem -= tri;
+      tn = f + gsz + rem / gsz;
+      tm = f + rem % gsz;
+    }
+  }
+  const bool mirror = ep.sym && tm != tn;
   const int m0 = tm * BM, n0 = tn * BN;
   const int KT = (K + BK - 1) / BK;
 
@@ -209,6 +240,10 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
       } else {
         cp[0] = v0;
       }
+      if (mirror) {  // the transposed element of the tile below the diagonal
+        ep.C[(int64_t)c * ep.ldc + r] = v0;
+        if (two) ep.C[(int64_t)(c + 1) * ep.ldc + r] = v1;
+      }
       if (want_red) {
         ss = fma(v0, v0, ss);
         nf += !isfinite(v0);
@@ -265,8 +300,8 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
       tss += red[w];
       tnf += redi[w];
     }
-    ep.ss_partial[pid] = tss;
-    ep.nf_partial[pid] = tnf;
+    ep.ss_partial[pid] = mirror ? 2.0 * tss : tss;
+    ep.nf_partial[pid] = mirror ? 2 * tnf : tnf;
     __threadfence();
     const unsigned done = atomicAdd(ep.tile_counter, 1u);
     *last_flag = (done == (unsigned)(ntiles - 1));

@@ -1,0 +1,132 @@
+"""NNB_ORDER_SYMMETRIC: upper-tile products mirrored (GPU only; run with -m gpu).
+
+For A == Aᵀ and X0 = θI or Aᵀ/(‖A‖₁‖A‖∞) every iterate X_k and residual
+R_k = I − A·X_k is a polynomial in A, so each product is symmetric and the
+chain computes only its upper tile triangle.  The bar is the same as the
+NORTHSTAR chain's (tests/test_gpu_parity.py): X within 1e-10 relative
+Frobenius of the reference oracle at equal nest count, identical nest counts
+to reach eps, eps history within 1e-6 relative + 1e-13.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_frob
+
+pytestmark = pytest.mark.gpu
+
+nnb = pytest.importorskip("paper_2212_02406_b200")
+from paper_2212_02406_b200 import workloads as W  # noqa: E402
+
+TOL_X = 1e-10
+
+
+def eps_close(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.shape == b.shape, (a.shape, b.shape)
+    floor = (a < 1e-12) & (b < 1e-12)
+    ok = floor | (np.abs(a - b) <= 1e-6 * b + 1e-13)
+    assert ok.all(), np.c_[a, b][~ok]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test selected but no CUDA device")
+    nnb.lib()
+
+
+# sizes cover every tile configuration the GEMM picks (16/32/64/128 tiles)
+# and ragged edge tiles; N <= 384 runs the one-kernel small chain instead
+@pytest.mark.parametrize("n,p,iters", [(400, 1, 12), (777, 2, 6), (1100, 3, 4), (2500, 2, 3)])
+def test_symmetric_fixed_nests_vs_reference(ref, n, p, iters):
+    a = W.gram_shifted(n, seed=n, shift=0.5)
+    x0 = W.x0_transpose_norm(a)
+    xr, hr, ir, _ = ref.chain(a, x0, p, iters)
+    x, rep = nnb.nn_chain(a, None, p=p, max_iters=iters, order=nnb.ORDER_SYMMETRIC)
+    assert rep.iters == ir == iters
+    assert rep.products == iters * (p + 1) + 1
+    eps_close([e for _, e in rep.history], hr)
+    assert rel_frob(x, xr.real) < TOL_X
+    assert np.array_equal(x, x.T)  # mirrored, bit for bit
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_symmetric_tolerance_stop_identical_iterations(ref, p):
+    a = W.spd_conditioned(520, 1e3, seed=5)
+    x0 = W.x0_transpose_norm(a)
+    xr, hr, ir, _ = ref.chain(a, x0, p, 60, tol=1e-12)
+    x, rep = nnb.nn_chain(a, None, p=p, max_iters=60, tol=1e-12, order=nnb.ORDER_SYMMETRIC)
+    assert rep.iters == ir and rep.stopped_reason == "tolerance"
+    eps_close([e for _, e in rep.history], hr)
+    assert rel_frob(x, xr.real) < TOL_X
+
+
+def test_symmetric_scaled_identity_start(ref):
+    """phi0 = theta·I (nn_invert's start) is a polynomial in A too."""
+    a = W.spd_conditioned(640, 50.0, seed=8)
+    theta = 1.0 / np.abs(a).sum(1).max()
+    x0 = theta * np.eye(640)
+    xr, hr, ir, _ = ref.chain(a, x0, 2, 8)
+    x, rep = nnb.nn_chain(a, None, p=2, max_iters=8, order=nnb.ORDER_SYMMETRIC,
+                          x0_kind=nnb.X0_SCALED_IDENTITY, x0_scale=theta)
+    eps_close([e for _, e in rep.history], hr)
+    assert rel_frob(x, xr.real) < TOL_X
+
+
+def test_symmetric_c3_size_matches_northstar():
+    """N=4096 (config 2): same nest count to eps < 1e-12 as the full-product
+    chain, X equal to rounding, and X·A ≈ I checked independently."""
+    import torch
+
+    a = torch.from_numpy(W.spd_conditioned(4096, 1e3, seed=4)).cuda()
+    xs, rs = nnb.nn_chain(a, None, p=2, max_iters=60, tol=1e-12, order=nnb.ORDER_SYMMETRIC)
+    xn, rn = nnb.nn_chain(a, None, p=2, max_iters=60, tol=1e-12)
+    xs2, rs2 = nnb.nn_chain(a, None, p=2, max_iters=60, tol=1e-12, order=nnb.ORDER_SYMMETRIC)
+    torch.cuda.synchronize()
+    assert torch.equal(xs, xs2) and rs.history == rs2.history  # run-to-run bit-reproducible
+    assert rs.iters == rn.iters and rs.stopped_reason == "tolerance"
+    eps_close([e for _, e in rs.history], [e for _, e in rn.history])
+    assert (torch.linalg.norm(xs - xn) / torch.linalg.norm(xn)).item() < TOL_X
+    assert torch.equal(xs, xs.T)
+    r = torch.eye(4096, dtype=torch.float64, device="cuda") - xs @ a
+    assert (torch.linalg.norm(r) / 64).item() < 1e-11
+
+
+def test_symmetric_host_streaming():
+    """Host buffers at n >= 8192 take the streamed path; the symmetric order
+    runs there too and matches the device-resident NORTHSTAR chain."""
+    import torch
+
+    n = 8192
+    a = torch.from_numpy(W.gram_shifted(n, seed=9, shift=1.0))
+    xs, rs = nnb.nn_chain(a.numpy(), None, p=1, max_iters=3, order=nnb.ORDER_SYMMETRIC)
+    xn, rn = nnb.nn_chain(a.cuda(), None, p=1, max_iters=3)
+    xn = xn.cpu().numpy()
+    eps_close([e for _, e in rs.history], [e for _, e in rn.history])
+    assert rel_frob(xs, xn) < TOL_X
+
+
+def test_symmetric_preconditions():
+    a = W.spd_conditioned(300, 10.0, seed=1)
+    b = a.copy()
+    b[3, 7] = np.nextafter(b[3, 7], np.inf)  # one element one ulp off its mirror
+    with pytest.raises(nnb.DomainError):
+        nnb.nn_chain(b, None, p=1, max_iters=2, order=nnb.ORDER_SYMMETRIC)
+    with pytest.raises(nnb.DomainError):  # a caller's X0 need not commute with A
+        nnb.nn_chain(a, W.x0_transpose_norm(a), p=1, max_iters=2, order=nnb.ORDER_SYMMETRIC)
+    with pytest.raises(nnb.DomainError):  # diag(A)^-1 does not commute with A
+        nnb.nn_chain(a, None, p=1, max_iters=2, order=nnb.ORDER_SYMMETRIC, x0_kind=nnb.X0_JACOBI)
+    with pytest.raises(nnb.DomainError):
+        nnb.nn_chain(a.astype(np.complex128), None, p=1, max_iters=2, order=nnb.ORDER_SYMMETRIC,
+                     x0_kind=nnb.X0_SCALED_IDENTITY, x0_scale=0.01)
+
+
+def test_symmetric_nonfinite_input_diverges():
+    """A NaN mirrored by a NaN is still symmetric; the chain then reports the
+    non-finite residual as the reference's error class does."""
+    a = W.spd_conditioned(500, 10.0, seed=2)
+    a[10, 20] = a[20, 10] = np.nan
+    with pytest.raises((nnb.DivergenceError, nnb.DomainError)):
+        nnb.nn_chain(a, None, p=1, max_iters=3, order=nnb.ORDER_SYMMETRIC)
