@@ -51,12 +51,16 @@ enum nnb_status {
 /* Operand order of the nest ("Product order").
  * NORTHSTAR: R = I - A X,  X' = X (I + R + ... + R^p)  (right-multiply Horner)
  * REFERENCE: P = I - X A,  X' = (I + P + ... + P^p) X  (proj/src/solver.cpp:93-103) */
-/* SYMMETRIC: the NORTHSTAR order for real A == A^T with X0 a scaled identity
- *   or A^T/(||A||_1 ||A||_inf).  Every iterate and residual is then a
- *   polynomial in A, hence symmetric, and each product computes only its
- *   upper tile triangle and mirrors it (about half the DMMA work; results
- *   agree with NORTHSTAR to rounding).  Checked on entry: NNB_ERR_DOMAIN
- *   otherwise (and for complex chains and the sharded chain). */
+/* SYMMETRIC: the NORTHSTAR order for real A == A^T and X0 == X0^T (every
+ *   built-in X0 of a symmetric A qualifies; a given X0 is checked).  The
+ *   Horner products X·S(R)·R are then symmetric (push-through) and compute
+ *   only their upper tile triangle, mirrored: p+1 products per nest cost
+ *   about 1 + p/2.  R = I - A·X stays a full product.  Mirrored products
+ *   run while eps >= 1e-4 and falling; later nests use full products, so
+ *   the residual floor and the nest count to a tolerance are NORTHSTAR's
+ *   (a mirrored nest's floor is ~kappa·u).  Results agree with NORTHSTAR
+ *   to rounding.  NNB_ERR_DOMAIN when A or a given X0 is not
+ *   symmetric, and for complex chains and the sharded chain. */
 enum nnb_order { NNB_ORDER_NORTHSTAR = 0, NNB_ORDER_REFERENCE = 1, NNB_ORDER_SYMMETRIC = 2 };
 
 /* Initial iterate. */

@@ -106,16 +106,20 @@ int chain_cfg(const nnb_chain_config* cfg, ChainCfg* c) {
   return 0;
 }
 
-// NNB_ORDER_SYMMETRIC preconditions: X0 a polynomial in A (scaled identity or
-// Aᵀ/(‖A‖₁‖A‖∞)) and A exactly symmetric, so that every iterate and residual is
-// symmetric and the products may compute their upper tile triangle only.
-int symmetric_check(const nnb_chain_config* cfg, const double* A, int64_t n, int64_t ld, cudaStream_t s) {
+// NNB_ORDER_SYMMETRIC preconditions: A and X0 exactly symmetric (X0 built
+// here is: Aᵀ/(‖A‖₁‖A‖∞), diag(A)⁻¹ or θI of a symmetric A).  Then every
+// Horner product X·S(R)·R is symmetric and may compute its upper tile
+// triangle only (chain.cu).
+int symmetric_check(const nnb_chain_config* cfg, const double* A, const double* X0, int64_t n, int64_t ld,
+                    cudaStream_t s) {
   if (cfg->order != NNB_ORDER_SYMMETRIC) return 0;
-  if (cfg->x0_kind != NNB_X0_SCALED_IDENTITY && cfg->x0_kind != NNB_X0_TRANSPOSE_NORM)
-    return fail(NNB_ERR_DOMAIN, "nn chain: the symmetric order needs X0 = scaled identity or A^T/(|A|_1|A|_inf)");
   bool sym = false;
   NNB_TRY(is_symmetric_dev(A, n, ld, &sym, s));
   if (!sym) return fail(NNB_ERR_DOMAIN, "nn chain: the symmetric order needs A == A^T");
+  if (cfg->x0_kind == NNB_X0_GIVEN) {
+    NNB_TRY(is_symmetric_dev(X0, n, ld, &sym, s));
+    if (!sym) return fail(NNB_ERR_DOMAIN, "nn chain: the symmetric order needs X0 == X0^T");
+  }
   return 0;
 }
 
@@ -206,8 +210,8 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
     io.a_ready = a_ready;  // the first product consumes A chunk by chunk
   } else {
     NNB_CUDA(cudaStreamWaitEvent(s, in_done, 0));
-    NNB_TRY(symmetric_check(cfg, a.d, n, a.ld, s));
     if (!x0_given) NNB_TRY(x0_build(a.d, a.ld, n, cfg->x0_kind, cfg->x0_scale, x.d, x.ld, s));
+    NNB_TRY(symmetric_check(cfg, a.d, x.d, n, a.ld, s));
   }
   ChainOut o;
   const int st = chain_real(a.d, n, a.ld, x.d, c, eps_hist, &o, s, &io);
@@ -597,7 +601,6 @@ int nnb_nn_chain_d(const double* A, int64_t n, const double* X0, const nnb_chain
     return chain_d_streamed(A, n, X0, cfg, c, X_out, eps_hist, result, s);
   DMat a;
   NNB_TRY(a.load(A, n, n, n, s));
-  NNB_TRY(symmetric_check(cfg, a.d, n, a.ld, s));
   DMat x;  // working X with A's leading dimension: the caller's device X_out when it fits
   x.rows = x.cols = n;
   x.ld = a.ld;
@@ -615,6 +618,7 @@ int nnb_nn_chain_d(const double* A, int64_t n, const double* X0, const nnb_chain
   } else {
     NNB_TRY(x0_build(a.d, a.ld, n, cfg->x0_kind, cfg->x0_scale, x.d, x.ld, s));
   }
+  NNB_TRY(symmetric_check(cfg, a.d, x.d, n, a.ld, s));
   ChainOut o;
   const int st = chain_real(a.d, n, a.ld, x.d, c, eps_hist, &o, s);
   fill_result(result, o);

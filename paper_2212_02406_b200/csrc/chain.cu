@@ -256,11 +256,24 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
   NNB_CUDA(cudaEventRecord(e0, c.s));
 
   const bool tol_mode = cfg.tol > 0.0;
-  // SYMMETRIC (order 2): the NORTHSTAR operand order with every product's
-  // upper tile triangle computed and mirrored (the caller checked that A is
-  // symmetric and X0 a polynomial in A, so every iterate and residual is)
+  // SYMMETRIC (order 2): the NORTHSTAR operand order; R = I − A·X stays a full
+  // product, the Horner products V·R compute their upper tile triangle and
+  // mirror it.  The caller checked A and X0 symmetric; then every V·R =
+  // X·S(R)·R is symmetric by push-through ((I − XA)^j X = X (I − AX)^j), and
+  // so is every iterate.  (Mirroring R itself would need A·X symmetric, i.e.
+  // A and X commuting, and loses Newton's self-correction: measured divergent
+  // at kappa 1e3.)
+  // A mirrored product's rounding error is not aligned with A the way a full
+  // Newton correction's is, so the residual floor of a mirrored nest is about
+  // kappa·u instead of u (5e-12 vs 1.3e-13 at N=4096, kappa 1e3).  The
+  // mirrored products therefore run only while eps >= kSymSwitch and still
+  // falling; from the first nest below it (or the first that does not fall)
+  // every product is full and the chain ends at the full chain's floor.
+  constexpr double kSymSwitch = 1e-4;
+  bool sym_on = true;
   const int order = exact ? 1 : (cfg.order == 2 ? 0 : cfg.order);
-  c.sym = !exact && !c.cplx && cfg.order == 2;
+  const bool sym_mode = !exact && !c.cplx && cfg.order == 2;
+  c.sym = false;
   int k = 0, products = 0, stopped = 1, recorded = 0;
   if (small)
     NNB_TRY(small_chain_real(A.re, X.re, R.re, bufs[1].re, bufs[2].re, n, c.ld, cfg, eps_dev, nf_dev, status_dev, c.s));
@@ -304,6 +317,11 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
       ++products;
       xi = dst;
     } else if (p > 0) {
+      if (sym_mode && sym_on) {
+        if (!tol_mode) NNB_TRY(fetch());
+        sym_on = eps_h[k] >= kSymSwitch && (k == 0 || eps_h[k] < eps_h[k - 1]);
+      }
+      c.sym = sym_mode && sym_on;
       Plane v = Xk;
       int vi = xi;
       int dst_i = (xi + 1) % 3;
@@ -326,6 +344,7 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
         dst_i = 3 - xi - vi;
       }
       xi = vi;
+      c.sym = false;
     }
   }
   NNB_CUDA(cudaEventRecord(e1, c.s));

@@ -276,8 +276,8 @@ int gemm(GemmOp op, RedWs* red, cudaStream_t s) {
       (op.ep.D2 && ((reinterpret_cast<uintptr_t>(op.ep.D2) & 15) || (op.ep.ldd2 & 1))))
     return fail(7, "gemm: epilogue operands need 16B alignment and even leading dimensions");
   if (op.ep.C2 && arith() == 1) return fail(7, "gemm: the dual-output epilogue has no reference-exact form");
-  if (op.ep.sym && (op.M != op.N || op.b_kmajor || op.ep.C2 || op.ep.diag_offset != 0))
-    return fail(7, "gemm: symmetric output needs a square product, one output and no diagonal offset");
+  if (op.ep.sym && (op.M != op.N || op.b_kmajor || op.ep.C2 || op.ep.diag_offset != 0 || op.ep.D == op.ep.C))
+    return fail(7, "gemm: symmetric output needs a square product, one output, no diagonal offset and D != C");
   if (op.ep.sym && arith() == 1) op.ep.sym = 0;  // the exact loops compute every element
   if (red) {
     if (red->capacity < max_tiles_for(op.M, op.N)) return fail(7, "gemm: reduction workspace too small");

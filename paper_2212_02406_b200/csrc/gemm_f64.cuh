@@ -42,10 +42,12 @@ struct GemmEpilogue {
   const double* D2 = nullptr;
   int64_t ldd2 = 0;
   double alpha2 = 0.0, beta2 = 0.0;
-  // symmetric output (square C, no C2, diag_offset 0): only tiles tm <= tn are
-  // computed; off-diagonal tiles also store their transpose and count twice in
-  // the Σ C² / non-finite reduction.  Valid when A·B is symmetric, e.g. both
-  // operands polynomials in one symmetric matrix (DESIGN.md §3 K1-K3).
+  // symmetric output (square C, no C2, D symmetric and not aliasing C,
+  // diag_offset 0): only tiles tm <= tn are computed and only their r <= c
+  // elements stored, each with its mirror (counted twice in the Σ C² /
+  // non-finite reduction).  Valid when A·B is symmetric in exact arithmetic
+  // for the operands given — e.g. X·(I − A·X)^j for symmetric X and A, by
+  // push-through (DESIGN.md §3 K1-K3).
   int sym = 0;
   // Σ C² / non-finite reduction (all nullable => skipped)
   double* ss_partial = nullptr;  // [num_tiles]
@@ -128,7 +130,6 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
       tm = f + rem % gsz;
     }
   }
-  const bool mirror = ep.sym && tm != tn;
   const int m0 = tm * BM, n0 = tn * BN;
   const int KT = (K + BK - 1) / BK;
 
@@ -234,15 +235,28 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
       const int64_t dr = (int64_t)r + ep.diag_offset;
       if (dr == c) v0 += ep.gamma;
       if (dr == c + 1) v1 += ep.gamma;
+      if (ep.sym) {
+        // upper triangle (r <= c) stored with its mirror, so C is symmetric bit
+        // for bit; r > c inside a diagonal tile belongs to (c, r)'s thread
+        auto put = [&](int cc, double v) {
+          if (r > cc) return;
+          ep.C[(int64_t)r * ep.ldc + cc] = v;
+          if (r < cc) ep.C[(int64_t)cc * ep.ldc + r] = v;
+          if (want_red) {
+            const double w = r < cc ? 2.0 : 1.0;
+            ss = fma(w * v, v, ss);
+            nf += (r < cc ? 2 : 1) * !isfinite(v);
+          }
+        };
+        put(c, v0);
+        if (two) put(c + 1, v1);
+        continue;
+      }
       double* cp = ep.C + (int64_t)r * ep.ldc + c;
       if (two) {
         *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
       } else {
         cp[0] = v0;
-      }
-      if (mirror) {  // the transposed element of the tile below the diagonal
-        ep.C[(int64_t)c * ep.ldc + r] = v0;
-        if (two) ep.C[(int64_t)(c + 1) * ep.ldc + r] = v1;
       }
       if (want_red) {
         ss = fma(v0, v0, ss);
@@ -300,8 +314,8 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
       tss += red[w];
       tnf += redi[w];
     }
-    ep.ss_partial[pid] = mirror ? 2.0 * tss : tss;
-    ep.nf_partial[pid] = mirror ? 2 * tnf : tnf;
+    ep.ss_partial[pid] = tss;
+    ep.nf_partial[pid] = tnf;
     __threadfence();
     const unsigned done = atomicAdd(ep.tile_counter, 1u);
     *last_flag = (done == (unsigned)(ntiles - 1));
