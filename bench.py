@@ -579,15 +579,19 @@ def run_sparse(args, world, rank):
         comm.close()
     # the format the device consumed (csrc/sparse.cu): 1 = pair dictionary, 10 = f64 + int16 delta, 12
     fb = 10 if sharded else nnb.sparse_last_bytes_per_nnz()
-    fmt = {1: "1-byte (column - row, value) pair-dictionary codes, slot-major ELL (no row offsets)",
-           10: "f64 values + int16 column deltas, int32 row offsets", 12: "f64 values + int32 columns, row offsets"}[fb]
+    fname = "csr-int16-delta" if sharded else nnb.sparse_last_format()
+    fmt = {"row-dictionary": "1-byte row-pattern codes (<= 256 distinct (column - row, value) rows), no row offsets",
+           "pair-dictionary-ell": "1-byte (column - row, value) pair-dictionary codes, slot-major ELL (no row offsets)",
+           "pair-dictionary-csr": "1-byte pair-dictionary codes, int32 row offsets",
+           "csr-int16-delta": "f64 values + int16 column deltas, int32 row offsets",
+           "csr-int32": "f64 values + int32 columns, row offsets"}.get(fname, fname)
     mat = sparse_bytes(n, col.size, 10) - 2 * n * 8 if sharded else nnb.sparse_last_matrix_bytes()
     alg = 63 * sparse_bytes(n, col.size, 12)  # SURVEY §8(d) algorithmic bytes per solve: the work unit
     moved = 63 * (mat + 2 * n * 8)  # bytes of the consumed format (operator + t in + t out): the roofline
     gbs, moved_gbs = alg / (ms * 1e-3) / 1e9, moved / (ms * 1e-3) / 1e9
     return {"metric": "sparse factorized solve, 4096^2 5-pt Laplacian+I, gamma=63 (GB/s of SURVEY 8(d) algorithmic "
                       "bytes: 12 B per nonzero)", "value": round(gbs, 1),
-            "unit": "GB/s", "ms_per_step": round(ms, 3), "format_bytes_per_nnz": fb,
+            "unit": "GB/s", "ms_per_step": round(ms, 3), "format": fname, "format_bytes_per_nnz": fb,
             "parallelism": f"row slabs x{world}, NCCL halo exchange" if sharded else "single GPU",
             "roofline": {"bound": "hbm", "achieved": round(moved_gbs, 1), "peak": HBM_PEAK * world, "unit": "GB/s",
                          "frac": round(moved_gbs / (HBM_PEAK * world), 4),

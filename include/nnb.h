@@ -258,9 +258,15 @@ int nnb_sparse_factorized_d(const int64_t* row_ptr, const int32_t* col, const do
  * other structured operators), 10 with int16 column deltas from the row, 12
  * with int32 columns; 0 before any solve.  Every format is bit-identical. */
 int nnb_sparse_last_bytes_per_nnz(void);
-/* Operator bytes one application of that solve streams from HBM: the codes (slot-major
- * ELL: width*n bytes, no row offsets) or values and columns, plus row offsets. */
+/* Operator bytes one application of that solve streams from HBM: one code per row
+ * (row dictionary: n bytes), the pair codes (slot-major ELL: width*n bytes, no row
+ * offsets) or values and columns, plus row offsets. */
 int64_t nnb_sparse_last_matrix_bytes(void);
+/* That format by name: "row-dictionary" (<= 256 distinct whole rows over the ELL
+ * pair codes, e.g. stencils: one uint8 code per row), "pair-dictionary-ell",
+ * "pair-dictionary-csr", "csr-int16-delta", "csr-int32", "csr-int64-offsets";
+ * "" before any solve. */
+const char* nnb_sparse_last_format(void);
 
 /* ---- contraction measurement (theta_trace's spectral estimate) ---------- */
 /* Power iteration on M^H M from the unit probe v0 (complex128, length n):

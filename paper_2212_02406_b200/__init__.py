@@ -125,6 +125,7 @@ _SIGS = {
                                  _dp], C.c_int),
     "nnb_sparse_last_bytes_per_nnz": ([], C.c_int),
     "nnb_sparse_last_matrix_bytes": ([], C.c_int64),
+    "nnb_sparse_last_format": ([], C.c_char_p),
     "nnb_gaussian_stream": ([C.c_uint64, _i64, _dp], C.c_int),
     "nnb_householder_q_d": ([_dp, _i64, _dp, _dp], C.c_int),
     "nnb_householder_q_z": ([_dp, _i64, _dp, _dp], C.c_int),
@@ -799,6 +800,11 @@ def sparse_last_bytes_per_nnz() -> int:
 def sparse_last_matrix_bytes() -> int:
     """Operator bytes one application of the calling thread's last solve streamed."""
     return int(lib().nnb_sparse_last_matrix_bytes())
+
+
+def sparse_last_format() -> str:
+    """Name of the operator format the calling thread's last sparse solve consumed."""
+    return lib().nnb_sparse_last_format().decode()
 
 
 def solve_sparse_factorized_sharded(comm: Comm, csr_rows: Csr, n: int, b_rows, gamma: int, norm: Normalization):

@@ -1009,6 +1009,7 @@ int nnb_spmv_block_d(const int64_t* row_ptr, const int32_t* col, const double* v
 
 int nnb_sparse_last_bytes_per_nnz(void) { return sparse_bytes_per_nnz(); }
 int64_t nnb_sparse_last_matrix_bytes(void) { return sparse_matrix_bytes(); }
+const char* nnb_sparse_last_format(void) { return sparse_format(); }
 
 int nnb_sparse_factorized_d(const int64_t* row_ptr, const int32_t* col, const double* val,
                             int64_t n, int64_t nnz, const double* B, int64_t k, int64_t gamma,

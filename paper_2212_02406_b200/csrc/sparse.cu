@@ -43,6 +43,11 @@ thread_local int64_t g_sparse_matrix_bytes = 0;
 void set_sparse_bytes_per_nnz(int b) { g_sparse_bytes_per_nnz = b; }
 int sparse_bytes_per_nnz() { return g_sparse_bytes_per_nnz; }
 void set_sparse_matrix_bytes(int64_t b) { g_sparse_matrix_bytes = b; }
+namespace {
+thread_local const char* g_sparse_format = "";
+}
+void set_sparse_format(const char* f) { g_sparse_format = f; }
+const char* sparse_format() { return g_sparse_format; }
 int64_t sparse_matrix_bytes() { return g_sparse_matrix_bytes; }
 
 template <int MODE>
@@ -218,6 +223,52 @@ __global__ void __launch_bounds__(NNB_SPMV_THREADS, NNB_SPMV_MINB)
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
+// Row dictionary: operators whose rows repeat a few whole (column − row,
+// value) sequences — a stencil has one per boundary case — store one uint8
+// pattern code per row.  pat[p·W + i] = {value, delta as bits} of pattern p's
+// i-th nonzero (CSR order), len[p] its length; exact lookups, so the sum keeps
+// the reference's order and rounding.  1 B per row instead of 5 code bytes.
+template <int MODE, int WMAX>
+__global__ void __launch_bounds__(NNB_SPMV_THREADS, NNB_SPMV_MINB)
+    spmv_rowdict_kernel(const uint8_t* __restrict__ rcode, const double2* __restrict__ pat,
+                        const uint8_t* __restrict__ plen, int npat, int width, int r_begin, int r_end, int diag_off,
+                        const double* __restrict__ t_ext, const double* __restrict__ t_own, double* __restrict__ out,
+                        const double* __restrict__ zold, double theta, int* __restrict__ flag) {
+  extern __shared__ double2 spat[];  // [npat·width] patterns, then npat lengths
+  int* slen = reinterpret_cast<int*>(spat + npat * width);
+  for (int i = threadIdx.x; i < npat * width; i += blockDim.x) {
+    const double2 e = pat[i];
+    spat[i] = make_double2(e.x, __longlong_as_double(__double_as_longlong(e.y) + diag_off));
+  }
+  for (int i = threadIdx.x; i < npat; i += blockDim.x) slen[i] = plen[i];
+  __syncthreads();
+  bool bad = false;
+  // The next row's code is loaded a row ahead: its HBM latency overlaps this
+  // row's gathers instead of heading the next row's dependent chain (inner
+  // application 76.6 -> 68.8 us).  Tried and reverted: codes two rows ahead
+  // with the next row's gathers prefetched into L2 (prefetch.global.L2):
+  // 103 us, the prefetches cost more issue and L2 bandwidth than they hide.
+  const int stride = gridDim.x * blockDim.x;
+  int r = r_begin + blockIdx.x * blockDim.x + threadIdx.x;
+  int p_next = r < r_end ? rcode[r] : 0;
+  for (; r < r_end; r += stride) {
+    const int p = p_next;
+    if (r + stride < r_end) p_next = rcode[r + stride];
+    const int len = slen[p];
+    const double2* pe = spat + p * width;
+    double xv[WMAX];  // every gather in flight first; the values are re-read from shared memory
+#pragma unroll
+    for (int i = 0; i < WMAX; ++i)
+      if (i < len) xv[i] = t_ext[r + (int)__double_as_longlong(pe[i].y)];
+    double y = 0.0;
+#pragma unroll
+    for (int i = 0; i < WMAX; ++i)
+      if (i < len) y = __dadd_rn(y, __dmul_rn(pe[i].x, xv[i]));  // CSR order
+    out[r] = finish<MODE>(t_own[r], y, theta, MODE == kInner ? 0.0 : zold[r], bad);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 // ---- pair dictionary build: hash insert, index assignment, verified encode ----
 constexpr int kDictSlots = 4096;  // open addressing, power of two
 
@@ -353,6 +404,130 @@ __global__ void dict_encode_kernel(const int64_t* __restrict__ rp, const int32_t
   if (bad) atomicOr(collision, 1);
 }
 
+// ---- row dictionary over the ELL pair codes: a row's key is its W code bytes
+// (kEllPad-padded) packed into 64 bits, so equal keys are equal (delta, value)
+// sequences exactly ----
+struct RowDictWs {
+  unsigned long long hash[kDictSlots];
+  unsigned long long key[kDictSlots];
+  int32_t index[kDictSlots];
+  int count;
+  int overflow;   // more than kRowDictMax patterns
+  int collision;  // equal hashes of different keys (the encode check)
+  int size;
+};
+
+__device__ __forceinline__ unsigned long long row_key(const uint8_t* __restrict__ code, int width, int64_t plane,
+                                                       int64_t r) {
+  unsigned long long k = ~0ull;  // unused bytes read as kEllPad
+  for (int i = 0; i < width; ++i)
+    k = (k & ~(0xffull << (8 * i))) | (static_cast<unsigned long long>(code[i * plane + r]) << (8 * i));
+  return k;
+}
+
+__device__ __forceinline__ unsigned long long key_hash(unsigned long long k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k | 1ull;
+}
+
+__global__ void rowdict_insert_kernel(const uint8_t* __restrict__ code, int width, int64_t plane, int64_t rows,
+                                      RowDictWs* ws) {
+  unsigned long long last = 0;
+  bool have = false;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = row_key(code, width, plane, r);
+    if (have && k == last) continue;  // interior rows repeat one key
+    if (*(volatile int*)&ws->overflow) return;
+    const unsigned long long h = key_hash(k);
+    int slot = static_cast<int>(h & (kDictSlots - 1));
+    for (int probe = 0; probe < kDictSlots; ++probe) {
+      unsigned long long cur = *(volatile unsigned long long*)&ws->hash[slot];
+      if (cur == 0) {
+        cur = atomicCAS(&ws->hash[slot], 0ull, h);
+        if (cur == 0) {
+          ws->key[slot] = k;
+          if (atomicAdd(&ws->count, 1) >= kRowDictMax) {
+            atomicOr(&ws->overflow, 1);
+            return;
+          }
+          break;
+        }
+      }
+      if (cur == h) break;
+      slot = (slot + 1) & (kDictSlots - 1);
+    }
+    last = k;
+    have = true;
+  }
+}
+
+// one block: occupied slots in slot order -> pattern indices; pattern p expanded
+// to {value, delta} entries through the pair dictionary
+__global__ void rowdict_index_kernel(RowDictWs* ws, int width, const int32_t* __restrict__ dict_delta,
+                                     const double* __restrict__ dict_val, double2* __restrict__ pat,
+                                     uint8_t* __restrict__ plen) {
+  __shared__ int counts[1024];
+  constexpr int per = kDictSlots / 1024;
+  int c = 0;
+  for (int i = 0; i < per; ++i) c += ws->hash[threadIdx.x * per + i] != 0;
+  counts[threadIdx.x] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int i = 0; i < 1024; ++i) {
+      const int v = counts[i];
+      counts[i] = run;
+      run += v;
+    }
+    ws->size = run;
+  }
+  __syncthreads();
+  int idx = counts[threadIdx.x];
+  for (int i = 0; i < per; ++i) {
+    const int slot = threadIdx.x * per + i;
+    if (ws->hash[slot] == 0) continue;
+    ws->index[slot] = idx;
+    if (idx < kRowDictMax) {
+      const unsigned long long k = ws->key[slot];
+      int len = width;
+      for (int j = 0; j < width; ++j) {
+        const int q = static_cast<int>((k >> (8 * j)) & 0xff);
+        if (q == kEllPad) {
+          if (len == width) len = j;
+          pat[idx * width + j] = make_double2(0.0, __longlong_as_double(0));
+        } else {
+          pat[idx * width + j] = make_double2(dict_val[q], __longlong_as_double((long long)dict_delta[q]));
+        }
+      }
+      plen[idx] = static_cast<uint8_t>(len);
+    }
+    ++idx;
+  }
+}
+
+__global__ void rowdict_encode_kernel(const uint8_t* __restrict__ code, int width, int64_t plane, int64_t rows,
+                                      const RowDictWs* ws, uint8_t* __restrict__ rcode, int* collision) {
+  bool bad = false;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = row_key(code, width, plane, r);
+    const unsigned long long h = key_hash(k);
+    int slot = static_cast<int>(h & (kDictSlots - 1));
+    int probe = 0;
+    while (ws->hash[slot] != h && ws->hash[slot] != 0 && probe < kDictSlots) {
+      slot = (slot + 1) & (kDictSlots - 1);
+      ++probe;
+    }
+    const bool hit = ws->hash[slot] == h && ws->key[slot] == k;
+    bad |= !hit;
+    rcode[r] = static_cast<uint8_t>(hit ? ws->index[slot] : 0);
+  }
+  if (bad) atomicOr(collision, 1);
+}
+
 // Plain Y = W·X for nn::spmv_block (same rounding as the reference's sum).
 __global__ void spmv_plain_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                                   const double* __restrict__ val, int64_t n, int64_t k,
@@ -482,6 +657,34 @@ void launch_ell1_v(const SpmvOp<int32_t>& op, int64_t r_begin, int64_t r_end, cu
 }
 
 
+template <int MODE, int WMAX>
+void launch_rowdict_v(const SpmvOp<int32_t>& op, int64_t r_begin, int64_t r_end, cudaStream_t s) {
+  const int smem = op.npat * op.ell_width * (int)sizeof(double2) + op.npat * (int)sizeof(int);
+  static unsigned resident = 0;
+  static int resident_smem = -1;
+  if (resident_smem != smem) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(spmv_rowdict_kernel<MODE, WMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, spmv_rowdict_kernel<MODE, WMAX>, NNB_SPMV_THREADS, smem);
+    resident = static_cast<unsigned>(sms * std::max(1, per));
+    resident_smem = smem;
+  }
+  const int64_t want = (r_end - r_begin + NNB_SPMV_THREADS - 1) / NNB_SPMV_THREADS;
+  const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(resident, want)));
+  spmv_rowdict_kernel<MODE, WMAX><<<grid, NNB_SPMV_THREADS, smem, s>>>(
+      op.rcode, op.rpat, op.rlen, op.npat, op.ell_width, (int)r_begin, (int)r_end, (int)op.diag_off, op.t_ext,
+      op.t_own, op.out, op.zold, op.theta, op.flag);
+}
+
+template <int MODE, typename Idx>
+void launch_rowdict(const SpmvOp<Idx>& op, int64_t r_begin, int64_t r_end, cudaStream_t s) {
+  const SpmvOp<int32_t>& o32 = reinterpret_cast<const SpmvOp<int32_t>&>(op);
+  if (op.ell_width <= 5) launch_rowdict_v<MODE, 5>(o32, r_begin, r_end, s);
+  else launch_rowdict_v<MODE, kEllMaxWidth>(o32, r_begin, r_end, s);
+}
+
 // rows of <= 5 nonzeros (2-D 5-point stencils) fit the 32-register budget
 template <int MODE, typename Idx>
 void launch_ell(const SpmvOp<Idx>& op, int64_t r_begin, int64_t r_end, cudaStream_t s) {
@@ -515,7 +718,13 @@ void launch_mode(const SpmvOp<Idx>& op, const C* col, int mode, int64_t r_begin,
 template <typename Idx>
 void spmv_apply(const SpmvOp<Idx>& op, int mode, int64_t r_begin, int64_t r_end, cudaStream_t s) {
   if (r_end <= r_begin) return;
-  if (op.code && op.ell_width) {
+  if (op.rcode && k1_ok(op, r_end)) {  // built for one right-hand side only
+    switch (mode) {
+      case kInner: launch_rowdict<kInner>(op, r_begin, r_end, s); break;
+      case kFactorEnd: launch_rowdict<kFactorEnd>(op, r_begin, r_end, s); break;
+      default: launch_rowdict<kFinal>(op, r_begin, r_end, s);
+    }
+  } else if (op.code && op.ell_width) {
     switch (mode) {
       case kInner: launch_ell<kInner>(op, r_begin, r_end, s); break;
       case kFactorEnd: launch_ell<kFactorEnd>(op, r_begin, r_end, s); break;
@@ -625,6 +834,35 @@ int build_pair_dict(const int64_t* rp, const int32_t* col, const double* val, in
   return 0;
 }
 
+int build_row_dict(const uint8_t* code, int width, int64_t plane, int64_t rows, const int32_t* dict_delta,
+                   const double* dict_val, uint8_t* rcode, double2* pat, uint8_t* plen, int* npat, bool* ok,
+                   cudaStream_t s) {
+  *ok = false;
+  *npat = 0;
+  if (rows <= 0 || width < 1 || width > kEllMaxWidth) return 0;
+  DevBuf wsb;
+  NNB_TRY(wsb.alloc(sizeof(RowDictWs), s));
+  RowDictWs* ws = wsb.as<RowDictWs>();
+  NNB_CUDA(cudaMemsetAsync(ws, 0, sizeof(RowDictWs), s));
+  rowdict_insert_kernel<<<rows_grid(rows), 256, 0, s>>>(code, width, plane, rows, ws);
+  rowdict_index_kernel<<<1, 1024, 0, s>>>(ws, width, dict_delta, dict_val, pat, plen);
+  count_launch(2);
+  NNB_CUDA(cudaGetLastError());
+  int flags[4];  // count, overflow, collision, size
+  NNB_CUDA(cudaMemcpyAsync(flags, &ws->count, sizeof(flags), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  if (flags[1] || flags[3] > kRowDictMax) return 0;
+  rowdict_encode_kernel<<<rows_grid(rows), 256, 0, s>>>(code, width, plane, rows, ws, rcode, &ws->collision);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  NNB_CUDA(cudaMemcpyAsync(flags, &ws->count, sizeof(flags), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  if (flags[2]) return 0;
+  *npat = flags[3];
+  *ok = true;
+  return 0;
+}
+
 int spmv_csr(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n, const double* X, int64_t k,
              double* Y, cudaStream_t s) {
   if (n == 0) return 0;
@@ -644,6 +882,10 @@ struct PairDict {
   int ell_width = 0;
   int64_t ell_rows = 0;  // slot-plane stride
   int band_lo = 0, band_hi = 0;
+  const uint8_t* rcode = nullptr;  // row dictionary (over the ELL codes)
+  const double2* rpat = nullptr;
+  const uint8_t* rlen = nullptr;
+  int npat = 0;
 };
 
 template <typename Idx>
@@ -659,7 +901,7 @@ void run_factors(const Idx* rp, const int32_t* col, const int16_t* col16, const 
     for (int64_t r = 0; r < reps; ++r) {
       SpmvOp<Idx> op{rp, col, col16, 0, val, k, tin, tin, nullptr, zcur, theta, flags + f,
                      dict.code, dict.delta, dict.val, dict.size, dict.ell_width, dict.ell_rows, dict.band_lo,
-                     dict.band_hi};
+                     dict.band_hi, dict.rcode, dict.rpat, dict.rlen, dict.npat};
       int mode;
       if (r < reps - 1) {
         mode = kInner;
@@ -713,7 +955,7 @@ int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* 
       return e && std::strcmp(e, "32") == 0;
     }();
     // operators with <= 255 distinct (column − row, value) pairs: 1 byte per nonzero
-    DevBuf dict_buf, code_buf;
+    DevBuf dict_buf, code_buf, rowdict_buf;
     PairDict dict;
     if (dict_on && !force32) {
       NNB_TRY(dict_buf.alloc((sizeof(int32_t) + sizeof(double)) * kPairDictMax, s));
@@ -725,6 +967,26 @@ int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* 
       NNB_TRY(build_pair_dict(row_ptr, col, val, n, 0, nnz, code_buf, &width, &plane, &lo, &hi, dd, dv, &size, &ok,
                               s));
       if (ok) dict = PairDict{code_buf.as<uint8_t>(), dd, dv, size, width, plane, lo, hi};
+      // ELL codes with few distinct rows (stencils): one pattern code per row
+      static const bool rowdict_on = [] {  // NNB_SPARSE_ROWDICT=0: keep the ELL pair codes (A/B measurement)
+        const char* e = std::getenv("NNB_SPARSE_ROWDICT");
+        return !(e && std::strcmp(e, "0") == 0);
+      }();
+      if (ok && width && k == 1 && rowdict_on) {
+        NNB_TRY(rowdict_buf.alloc(sizeof(double2) * kRowDictMax * kEllMaxWidth + kRowDictMax + n, s));
+        double2* pat = rowdict_buf.as<double2>();
+        uint8_t* plen = reinterpret_cast<uint8_t*>(pat + kRowDictMax * kEllMaxWidth);
+        uint8_t* rcode = plen + kRowDictMax;
+        bool rok = false;
+        int npat = 0;
+        NNB_TRY(build_row_dict(dict.code, width, plane, n, dd, dv, rcode, pat, plen, &npat, &rok, s));
+        if (rok) {
+          dict.rcode = rcode;
+          dict.rpat = pat;
+          dict.rlen = plen;
+          dict.npat = npat;
+        }
+      }
     }
     // int32 offsets, and int16 column deltas when the operator's band allows (the ELL
     // dictionary needs neither)
@@ -732,14 +994,20 @@ int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* 
     if (!(dict.code && dict.ell_width)) NNB_TRY(compact_csr(row_ptr, col, n, 0, rp32, col16, &fits, s));
     fits = fits && !force32;
     set_sparse_bytes_per_nnz(dict.code ? 1 : (fits ? 10 : 12));
-    // operator bytes one application streams: codes (ELL: width·n, no offsets) or values +
-    // columns, plus int32 row offsets
-    set_sparse_matrix_bytes(dict.ell_width ? (int64_t)dict.ell_width * n
-                                           : nnz * (dict.code ? 1 : (fits ? 10 : 12)) + (n + 1) * 4);
+    set_sparse_format(dict.rcode ? "row-dictionary"
+                      : dict.ell_width ? "pair-dictionary-ell"
+                      : dict.code ? "pair-dictionary-csr"
+                      : fits ? "csr-int16-delta" : "csr-int32");
+    // operator bytes one application streams: one code per row (row dictionary), codes
+    // (ELL: width·n, no offsets) or values + columns, plus int32 row offsets
+    set_sparse_matrix_bytes(dict.rcode ? n
+                            : dict.ell_width ? (int64_t)dict.ell_width * n
+                                             : nnz * (dict.code ? 1 : (fits ? 10 : 12)) + (n + 1) * 4);
     run_factors<int32_t>(rp32, col, fits ? col16 : nullptr, val, n, B, k, s_factors, theta, X, z, tb, flags, s,
                          dict);
   } else {
     set_sparse_bytes_per_nnz(12);
+    set_sparse_format("csr-int64-offsets");
     set_sparse_matrix_bytes(nnz * 12 + (n + 1) * 8);
     run_factors<int64_t>(row_ptr, col, nullptr, val, n, B, k, s_factors, theta, X, z, tb, flags, s);
   }

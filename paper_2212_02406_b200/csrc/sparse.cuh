@@ -38,11 +38,18 @@ struct SpmvOp {
   int ell_width = 0;  // > 0: slot-major ELL codes (code[i·ell_rows + r], kEllPad-padded), no row offsets
   int64_t ell_rows = 0;  // slot-plane stride (rows rounded up to 16)
   int band_lo = 0, band_hi = 0;  // min / max (column − row) over the dictionary
+  // Row dictionary (over the ELL pair codes, <= kRowDictMax distinct rows): one
+  // uint8 pattern code per row; rpat[p·ell_width + i] = {value, delta as bits}
+  const uint8_t* rcode = nullptr;
+  const double2* rpat = nullptr;
+  const uint8_t* rlen = nullptr;
+  int npat = 0;
 };
 
 constexpr int kPairDictMax = 256;
 constexpr int kEllMaxWidth = 8;     // rows this short store their codes in ELL order
 constexpr uint8_t kEllPad = 255;    // ELL padding code (the dictionary keeps it free)
+constexpr int kRowDictMax = 256;    // row patterns (uint8 row codes)
 
 // Bytes per nonzero of the format the last single-GPU sparse solve on this thread
 // consumed (1 = pair dictionary, 10 = int16 column deltas, 12 = int32 columns).
@@ -50,6 +57,10 @@ void set_sparse_bytes_per_nnz(int b);
 int sparse_bytes_per_nnz();
 // Operator bytes (codes or values + columns, plus row offsets) one application of that solve streams.
 void set_sparse_matrix_bytes(int64_t b);
+// Name of that format: "row-dictionary", "pair-dictionary-ell", "pair-dictionary-csr",
+// "csr-int16-delta", "csr-int32", "csr-int64-offsets" ("" before any solve).
+void set_sparse_format(const char* f);
+const char* sparse_format();
 int64_t sparse_matrix_bytes();
 
 // Builds the pair dictionary of rows [0, rows) (global row index row0 + r; nonzeros
@@ -61,6 +72,13 @@ struct DevBuf;
 int build_pair_dict(const int64_t* rp, const int32_t* col, const double* val, int64_t rows, int64_t row0,
                     int64_t nnz, DevBuf& code_buf, int* ell_width, int64_t* ell_plane, int* band_lo, int* band_hi,
                     int32_t* dict_delta, double* dict_val, int* dict_size, bool* ok, cudaStream_t s);
+
+// Row dictionary over ELL pair codes (code, width, plane from build_pair_dict):
+// fills rcode[rows], pat[npat·width] ({value, delta as bits}) and plen[npat];
+// *ok = false when the operator has more than kRowDictMax distinct rows.
+int build_row_dict(const uint8_t* code, int width, int64_t plane, int64_t rows, const int32_t* dict_delta,
+                   const double* dict_val, uint8_t* rcode, double2* pat, uint8_t* plen, int* npat, bool* ok,
+                   cudaStream_t s);
 
 template <typename Idx>
 void spmv_apply(const SpmvOp<Idx>& op, int mode, int64_t r_begin, int64_t r_end, cudaStream_t s);

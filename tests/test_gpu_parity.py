@@ -464,7 +464,66 @@ def test_sparse_laplacian_uses_pair_dictionary(ref):
     b = W.rhs(64 * 64, seed=2)
     x, _ = nnb.solve_sparse_factorized(nnb.Csr(rp, col, val, n=64 * 64), b, 63, nnb.Normalization(0.2, valid=True))
     assert nnb.sparse_last_bytes_per_nnz() == 1
+    # 9 distinct rows (interior, 4 edges, 4 corners): one code per row
+    assert nnb.sparse_last_format() == "row-dictionary"
+    assert nnb.sparse_last_matrix_bytes() == 64 * 64
     xr, _, _ = ref.sparse_factorized(rp, col, val, b, 63, 0.2)
+    assert np.array_equal(x, xr.real)
+
+
+def laplacian_7pt(m: int):
+    """3-D 7-point Dirichlet Laplacian + I on an m^3 grid (diagonal 7): width 7 rows."""
+    n = m ** 3
+    idx = np.arange(n).reshape(m, m, m)
+    rows, cols, vals = [], [], []
+    for di, dj, dk, v in ((-1, 0, 0, -1.0), (0, -1, 0, -1.0), (0, 0, -1, -1.0), (0, 0, 0, 7.0),
+                          (0, 0, 1, -1.0), (0, 1, 0, -1.0), (1, 0, 0, -1.0)):
+        src = idx[max(0, -di):m - max(0, di), max(0, -dj):m - max(0, dj), max(0, -dk):m - max(0, dk)]
+        dst = idx[max(0, di):m - max(0, -di) or None, max(0, dj):m - max(0, -dj) or None,
+                  max(0, dk):m - max(0, -dk) or None]
+        rows.append(src.ravel())
+        cols.append(dst.ravel())
+        vals.append(np.full(src.size, v))
+    rows, cols, vals = map(np.concatenate, (rows, cols, vals))
+    order = np.lexsort((cols, rows))
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, rows + 1, 1)
+    return np.cumsum(rp), cols.astype(np.int32), vals
+
+
+def test_sparse_row_dictionary_width7(ref):
+    """7-point 3-D stencil: 27 distinct rows of up to 7 nonzeros (the 8-wide kernel)."""
+    rp, col, val = laplacian_7pt(24)
+    n = rp.size - 1
+    b = W.rhs(n, seed=4)
+    norm = nnb.Normalization(theta=1.0 / 7.0, valid=True)
+    x, _ = nnb.solve_sparse_factorized(nnb.Csr(rp, col, val, n=n), b, 31, norm)
+    assert nnb.sparse_last_format() == "row-dictionary"
+    xr, _, _ = ref.sparse_factorized(rp, col, val, b, 31, 1.0 / 7.0)
+    assert np.array_equal(x, xr.real)
+
+
+def test_sparse_row_dictionary_overflow_keeps_pair_codes(ref):
+    """Five nonzeros per row, each off-diagonal value one of four: 17 pairs but far
+    more than 256 distinct rows -- the ELL pair codes stay, still bit-identical."""
+    n = 50000
+    rng = np.random.default_rng(7)
+    choices = np.array([-0.25, -0.125, 0.0625, 0.1875])
+    rp = np.zeros(n + 1, np.int64)
+    cols, vals = [], []
+    for i in range(n):
+        for d in (-3, -1, 0, 1, 3):
+            if 0 <= i + d < n:
+                cols.append(i + d)
+                vals.append(2.0 if d == 0 else choices[rng.integers(4)])
+        rp[i + 1] = len(cols)
+    col, val = np.array(cols, np.int32), np.array(vals)
+    b = W.rhs(n, seed=8)
+    norm = nnb.Normalization(theta=0.25, valid=True)
+    x, _ = nnb.solve_sparse_factorized(nnb.Csr(rp, col, val, n=n), b, 15, norm)
+    assert nnb.sparse_last_format() == "pair-dictionary-ell"
+    xr, _, _ = ref.sparse_factorized(rp, col, val, b, 15, 0.25)
     assert np.array_equal(x, xr.real)
 
 
