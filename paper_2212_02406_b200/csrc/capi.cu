@@ -188,16 +188,22 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
   NNB_CUDA(cudaStreamWaitEvent(lane.cs, alloc_ev, 0));
   const int64_t rows_per = ((n + chunks - 1) / chunks + 127) / 128 * 128;
   const int used = static_cast<int>((n + rows_per - 1) / rows_per);
-  // X0 first: every row chunk of the first product needs all of it
-  if (x0_given)
-    NNB_CUDA(cudaMemcpy2DAsync(x.d, x.ld * 8, X0, n * 8, n * 8, n, cudaMemcpyDefault, lane.cs));
-  if (host_a)
+  // block q of the first product's inner dimension: X0's rows and A's columns of q
+  const bool ksplit = host_a && x0_given && cfg->order == NNB_ORDER_NORTHSTAR;
+  if (ksplit) {
     for (int q = 0; q < used; ++q) {
-      const int64_t r0 = q * rows_per, rows = std::min<int64_t>(rows_per, n - r0);
-      NNB_CUDA(cudaMemcpy2DAsync(a.d + r0 * a.ld, a.ld * 8, A + r0 * n, n * 8, n * 8, rows, cudaMemcpyHostToDevice,
+      const int64_t k0 = q * rows_per, kq = std::min<int64_t>(rows_per, n - k0);
+      NNB_CUDA(cudaMemcpy2DAsync(x.d + k0 * x.ld, x.ld * 8, X0 + k0 * n, n * 8, n * 8, kq, cudaMemcpyDefault,
                                  lane.cs));
+      NNB_CUDA(cudaMemcpy2DAsync(a.d + k0, a.ld * 8, A + k0, n * 8, kq * 8, n, cudaMemcpyHostToDevice, lane.cs));
       NNB_CUDA(cudaEventRecord(a_ready[q], lane.cs));
     }
+  } else {
+    if (x0_given)
+      NNB_CUDA(cudaMemcpy2DAsync(x.d, x.ld * 8, X0, n * 8, n * 8, n, cudaMemcpyDefault, lane.cs));
+    if (host_a)
+      NNB_CUDA(cudaMemcpy2DAsync(a.d, a.ld * 8, A, n * 8, n * 8, n, cudaMemcpyHostToDevice, lane.cs));
+  }
   NNB_CUDA(cudaEventRecord(in_done, lane.cs));
   ChainIo io;
   io.chunks = used;
@@ -206,8 +212,8 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
   io.out_done = out_done;
   io.copy_done = copy_done;
   io.host_out = host_out ? X_out : nullptr;
-  if (host_a && x0_given && cfg->order == NNB_ORDER_NORTHSTAR) {
-    io.a_ready = a_ready;  // the first product consumes A chunk by chunk
+  if (ksplit) {
+    io.a_ready = a_ready;  // the first product consumes A and X0 block by block
   } else {
     NNB_CUDA(cudaStreamWaitEvent(s, in_done, 0));
     if (!x0_given) NNB_TRY(x0_build(a.d, a.ld, n, cfg->x0_kind, cfg->x0_scale, x.d, x.ld, s));

@@ -193,6 +193,45 @@ int product_chunked(Ctx& c, const Plane& A, const Plane& B, double alpha, const 
   return 0;
 }
 
+// R = alpha·(A·B) + gamma·I with the inner dimension in io.chunks column
+// blocks of A (rows of B): block q waits for io.a_ready[q] (A's columns and
+// B's rows of q are on the device), and each non-final launch stores the raw
+// accumulator that the next one resumes from (GemmEpilogue::acc_in), so C is
+// bit-identical to one launch.  The copy of the inputs then overlaps all but
+// the first block's share of the product.
+int product_ksplit(Ctx& c, const Plane& A, const Plane& B, double alpha, double gamma, const Plane& C,
+                   double* eps_out, int* nf_out, ChainIo& io) {
+  for (int q = 0; q < io.chunks; ++q) {
+    const int64_t k0 = q * io.chunk_rows, kq = std::min<int64_t>(io.chunk_rows, c.n - k0);
+    if (kq <= 0) break;
+    const bool last = k0 + kq >= c.n;
+    NNB_CUDA(cudaStreamWaitEvent(c.s, io.a_ready[q], 0));
+    GemmOp op;
+    op.M = op.N = c.n;
+    op.K = kq;
+    op.lda = op.ldb = c.ld;
+    op.A = A.re + k0;
+    op.B = B.re + k0 * c.ld;
+    op.ep.C = C.re;
+    op.ep.ldc = c.ld;
+    if (q > 0) {
+      op.ep.acc_in = C.re;
+      op.ep.ld_acc_in = c.ld;
+    }
+    if (last) {
+      op.ep.alpha = alpha;
+      op.ep.gamma = gamma;
+      op.ep.eps_out = eps_out;
+      op.ep.eps_scale = 1.0 / std::sqrt(static_cast<double>(c.n));
+      op.ep.nf_out = nf_out;
+      return gemm(op, nf_out ? &c.red : nullptr, c.s);
+    }
+    op.ep.alpha = 1.0;  // raw accumulator
+    NNB_TRY(gemm(op, nullptr, c.s));
+  }
+  return 0;
+}
+
 int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_hist,
               ChainOut* out, ChainIo* io = nullptr) {
   const int64_t n = c.n, mat = n * c.ld;
@@ -283,9 +322,8 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
     const Plane& Xk = bufs[xi];
     const Plane& lhs = order == 0 ? A : Xk;
     const Plane& rhs = order == 0 ? Xk : A;
-    if (k == 0 && io && io->a_ready && order == 0)  // R_0 = I − A·X_0 as A's rows arrive
-      NNB_TRY(product_chunked(c, lhs, rhs, -1.0, nullptr, 0.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1), *io, true,
-                              false, chunk_ss, chunk_nf));
+    if (k == 0 && io && io->a_ready && order == 0)  // R_0 = I − A·X_0 as A's columns and X_0's rows arrive
+      NNB_TRY(product_ksplit(c, lhs, rhs, -1.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1), *io));
     else
       NNB_TRY(product(c, lhs, rhs, -1.0, nullptr, 0.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1)));
     ++products;

@@ -164,15 +164,16 @@ struct ChainOut {
   int x_index = 0;  // sharded driver: which ping-pong buffer holds the final X
 };
 // Host-streaming hooks of the real chain (nnb_nn_chain_d with host buffers):
-// the first residual product runs in row chunks as A's rows land (NORTHSTAR
-// order, R = I − A·X: row chunk q needs only A's rows of q), and the last
+// the first residual product runs split along K as A's column blocks and
+// X0's row blocks land (NORTHSTAR order, R = I − A·X0; bit-identical to one
+// launch through the accumulator seed), and the last
 // Horner product runs in row chunks whose rows go device→host on `copy` as
 // soon as they are written.  PCIe then overlaps the DMMA work instead of
 // bracketing it.
 struct ChainIo {
   int chunks = 0;
   int64_t chunk_rows = 0;
-  cudaEvent_t* a_ready = nullptr;  // [chunks] rows of chunk q (and X0) are on the device; null: all present
+  cudaEvent_t* a_ready = nullptr;  // [chunks] A's columns and X0's rows of chunk q are on the device; null: all present
   double* host_out = nullptr;      // row-major n×n host destination of the final X (nullable)
   cudaStream_t copy = nullptr;
   cudaEvent_t* out_done = nullptr; // [chunks] scratch

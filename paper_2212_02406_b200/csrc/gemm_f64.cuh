@@ -49,6 +49,12 @@ struct GemmEpilogue {
   // for the operands given — e.g. X·(I − A·X)^j for symmetric X and A, by
   // push-through (DESIGN.md §3 K1-K3).
   int sym = 0;
+  // accumulator seed (nullable, may alias C): the K loop starts from acc_in's
+  // tile instead of 0.  A product split along K into launches whose non-final
+  // parts store the raw accumulator (alpha 1, beta 0, gamma 0) then runs the
+  // same DMMA sequence as one launch, bit for bit.
+  const double* acc_in = nullptr;
+  int64_t ld_acc_in = 0;
   // Σ C² / non-finite reduction (all nullable => skipped)
   double* ss_partial = nullptr;  // [num_tiles]
   int* nf_partial = nullptr;     // [num_tiles]
@@ -172,6 +178,21 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
   for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (ep.acc_in) {
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      const int r = m0 + wm * Cfg::kWarpM + i * 8 + g;
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        const int c = n0 + wn * Cfg::kWarpN + j * 8 + 2 * t;
+        if (r < M && c < N) {
+          const double* ap = ep.acc_in + (int64_t)r * ep.ld_acc_in + c;
+          acc[i][j][0] = ap[0];
+          if (c + 1 < N) acc[i][j][1] = ap[1];
+        }
+      }
+    }
+  }
 
   // Per-thread fragment byte offsets inside a stage.
   // A (128B swizzle): (r,k) -> r*128 + ((k>>1) ^ (r&7))*16 + (k&1)*8, r&7 == g.

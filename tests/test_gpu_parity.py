@@ -233,10 +233,12 @@ def _gram_device(n, seed):
 
 @pytest.mark.parametrize("pinned_out", [False, True])
 def test_chain_host_streaming_matches_device(pinned_out):
-    """Host A (n >= 8192): X0 and A's row chunks stream in under the first product and the
-    final X streams out under the last one (capi.cu chain_d_streamed).  The row-chunked
-    GEMMs compute the same tiles in the same K order, so X is bit-identical to the
-    device-buffer run; only eps's Σ is combined per chunk."""
+    """Host A (n >= 8192): X0's row blocks and A's column blocks stream in under the first
+    product, split along K, and the final X streams out under the last one (capi.cu
+    chain_d_streamed).  The K-split launches resume each other's raw accumulator and
+    the row-chunked output GEMMs compute the same tiles in the same K order, so X is
+    bit-identical to the device-buffer run; only the last product's eps Σ is combined
+    per chunk."""
     import torch
 
     n = 8192
