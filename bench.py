@@ -578,14 +578,14 @@ def run_sparse(args, world, rank):
         plan.close()
         comm.close()
     # the format the device consumed (csrc/sparse.cu): 1 = pair dictionary, 10 = f64 + int16 delta, 12
-    fb = 10 if sharded else nnb.sparse_last_bytes_per_nnz()
-    fname = "csr-int16-delta" if sharded else nnb.sparse_last_format()
+    fb = nnb.sparse_last_bytes_per_nnz()
+    fname = nnb.sparse_last_format()
     fmt = {"row-dictionary": "1-byte row-pattern codes (<= 256 distinct (column - row, value) rows), no row offsets",
            "pair-dictionary-ell": "1-byte (column - row, value) pair-dictionary codes, slot-major ELL (no row offsets)",
            "pair-dictionary-csr": "1-byte pair-dictionary codes, int32 row offsets",
            "csr-int16-delta": "f64 values + int16 column deltas, int32 row offsets",
            "csr-int32": "f64 values + int32 columns, row offsets"}.get(fname, fname)
-    mat = sparse_bytes(n, col.size, 10) - 2 * n * 8 if sharded else nnb.sparse_last_matrix_bytes()
+    mat = sum_over_ranks(world, float(nnb.sparse_last_matrix_bytes())) if sharded else nnb.sparse_last_matrix_bytes()
     alg = 63 * sparse_bytes(n, col.size, 12)  # SURVEY §8(d) algorithmic bytes per solve: the work unit
     moved = 63 * (mat + 2 * n * 8)  # bytes of the consumed format (operator + t in + t out): the roofline
     gbs, moved_gbs = alg / (ms * 1e-3) / 1e9, moved / (ms * 1e-3) / 1e9
@@ -597,8 +597,9 @@ def run_sparse(args, world, rank):
                          "frac": round(moved_gbs / (HBM_PEAK * world), 4),
                          "traffic": ncu_traffic("sparse_application") if grid == 4096 and not sharded else None,
                          "traffic_unit": "bytes per application (63 per solve)",
-                         "per_launch": f"{mat} operator bytes + 2N*8 per application (x63, whole solve timed "
-                                       f"incl. the per-solve format pass): {fmt}; t in + t out"}}
+                         "per_launch": f"{mat:.0f} operator bytes + 2N*8 per application (x63, whole solve timed "
+                                       + ("excl. the slab plan's one-time format pass" if sharded else
+                                          "incl. the per-solve format pass") + f"): {fmt}; t in + t out"}}
 
 
 def cpu_sparse_sample(grid: int):

@@ -441,6 +441,12 @@ __global__ void rowdict_insert_kernel(const uint8_t* __restrict__ code, int widt
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long k = row_key(code, width, plane, r);
     if (have && k == last) continue;  // interior rows repeat one key
+    // one insert per distinct key per warp (the lanes' first rows all start here)
+    const unsigned active = __activemask();
+    const unsigned peers = __match_any_sync(active, k);
+    last = k;
+    have = true;
+    if ((threadIdx.x & 31) != __ffs(peers) - 1) continue;
     if (*(volatile int*)&ws->overflow) return;
     const unsigned long long h = key_hash(k);
     int slot = static_cast<int>(h & (kDictSlots - 1));
@@ -460,8 +466,6 @@ __global__ void rowdict_insert_kernel(const uint8_t* __restrict__ code, int widt
       if (cur == h) break;
       slot = (slot + 1) & (kDictSlots - 1);
     }
-    last = k;
-    have = true;
   }
 }
 
@@ -511,19 +515,25 @@ __global__ void rowdict_index_kernel(RowDictWs* ws, int width, const int32_t* __
 
 __global__ void rowdict_encode_kernel(const uint8_t* __restrict__ code, int width, int64_t plane, int64_t rows,
                                       const RowDictWs* ws, uint8_t* __restrict__ rcode, int* collision) {
-  bool bad = false;
+  bool bad = false, have = false;
+  unsigned long long last = 0;
+  int last_idx = -1;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long k = row_key(code, width, plane, r);
-    const unsigned long long h = key_hash(k);
-    int slot = static_cast<int>(h & (kDictSlots - 1));
-    int probe = 0;
-    while (ws->hash[slot] != h && ws->hash[slot] != 0 && probe < kDictSlots) {
-      slot = (slot + 1) & (kDictSlots - 1);
-      ++probe;
+    if (!have || k != last) {  // a thread's rows repeat one key (interior rows): look up only on change
+      const unsigned long long h = key_hash(k);
+      int slot = static_cast<int>(h & (kDictSlots - 1));
+      int probe = 0;
+      while (ws->hash[slot] != h && ws->hash[slot] != 0 && probe < kDictSlots) {
+        slot = (slot + 1) & (kDictSlots - 1);
+        ++probe;
+      }
+      last_idx = (ws->hash[slot] == h && ws->key[slot] == k) ? ws->index[slot] : -1;
+      last = k;
+      have = true;
     }
-    const bool hit = ws->hash[slot] == h && ws->key[slot] == k;
-    bad |= !hit;
-    rcode[r] = static_cast<uint8_t>(hit ? ws->index[slot] : 0);
+    bad |= last_idx < 0;
+    rcode[r] = static_cast<uint8_t>(last_idx < 0 ? 0 : last_idx);
   }
   if (bad) atomicOr(collision, 1);
 }
@@ -843,23 +853,40 @@ int build_row_dict(const uint8_t* code, int width, int64_t plane, int64_t rows, 
   DevBuf wsb;
   NNB_TRY(wsb.alloc(sizeof(RowDictWs), s));
   RowDictWs* ws = wsb.as<RowDictWs>();
-  NNB_CUDA(cudaMemsetAsync(ws, 0, sizeof(RowDictWs), s));
-  rowdict_insert_kernel<<<rows_grid(rows), 256, 0, s>>>(code, width, plane, rows, ws);
-  rowdict_index_kernel<<<1, 1024, 0, s>>>(ws, width, dict_delta, dict_val, pat, plen);
-  count_launch(2);
-  NNB_CUDA(cudaGetLastError());
-  int flags[4];  // count, overflow, collision, size
-  NNB_CUDA(cudaMemcpyAsync(flags, &ws->count, sizeof(flags), cudaMemcpyDeviceToHost, s));
-  NNB_CUDA(cudaStreamSynchronize(s));
-  if (flags[1] || flags[3] > kRowDictMax) return 0;
-  rowdict_encode_kernel<<<rows_grid(rows), 256, 0, s>>>(code, width, plane, rows, ws, rcode, &ws->collision);
-  count_launch();
-  NNB_CUDA(cudaGetLastError());
-  NNB_CUDA(cudaMemcpyAsync(flags, &ws->count, sizeof(flags), cudaMemcpyDeviceToHost, s));
-  NNB_CUDA(cudaStreamSynchronize(s));
-  if (flags[2]) return 0;
-  *npat = flags[3];
-  *ok = true;
+  // As the pair dictionary: patterns first from the first and last kSample rows (a
+  // stencil shows every boundary case there), verified over all rows by the encode
+  // pass; a row outside the sample sends the build round again over all rows.
+  constexpr int64_t kSample = 65536;
+  const bool can_sample = rows > 4 * kSample;
+  for (int full = can_sample ? 0 : 1; full < 2; ++full) {
+    NNB_CUDA(cudaMemsetAsync(ws, 0, sizeof(RowDictWs), s));
+    if (full) {
+      rowdict_insert_kernel<<<rows_grid(rows), 256, 0, s>>>(code, width, plane, rows, ws);
+    } else {
+      rowdict_insert_kernel<<<rows_grid(kSample), 256, 0, s>>>(code, width, plane, kSample, ws);
+      rowdict_insert_kernel<<<rows_grid(kSample), 256, 0, s>>>(code + (rows - kSample), width, plane, kSample, ws);
+      count_launch();
+    }
+    rowdict_index_kernel<<<1, 1024, 0, s>>>(ws, width, dict_delta, dict_val, pat, plen);
+    count_launch(2);
+    NNB_CUDA(cudaGetLastError());
+    int flags[4];  // count, overflow, collision, size
+    NNB_CUDA(cudaMemcpyAsync(flags, &ws->count, sizeof(flags), cudaMemcpyDeviceToHost, s));
+    NNB_CUDA(cudaStreamSynchronize(s));
+    if (flags[1] || flags[3] > kRowDictMax) {
+      if (full) return 0;
+      continue;
+    }
+    rowdict_encode_kernel<<<rows_grid(rows), 256, 0, s>>>(code, width, plane, rows, ws, rcode, &ws->collision);
+    count_launch();
+    NNB_CUDA(cudaGetLastError());
+    NNB_CUDA(cudaMemcpyAsync(flags, &ws->count, sizeof(flags), cudaMemcpyDeviceToHost, s));
+    NNB_CUDA(cudaStreamSynchronize(s));
+    if (flags[2]) continue;  // a row outside the sample (or a hash collision): the full round decides
+    *npat = flags[3];
+    *ok = true;
+    return 0;
+  }
   return 0;
 }
 

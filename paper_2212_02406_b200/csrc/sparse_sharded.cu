@@ -19,6 +19,7 @@
 // device copies — validates partition, remap, halo sizes and the
 // interior/boundary split on a single device.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -73,8 +74,61 @@ struct Slab {
   const double* val = nullptr;
   double* ext[5] = {};                  // T0, T1, Z0, Z1, B (extended)
   int* flags = nullptr;                 // [64]
+  // pair / row dictionaries of the slab (one right-hand side), as sparse.cu's single-GPU solve
+  DevBuf dict_mem, code_mem, rowdict_mem;
+  const uint8_t* code = nullptr;
+  const int32_t* dict_delta = nullptr;
+  const double* dict_val = nullptr;
+  int dict_size = 0, ell_width = 0, band_lo = 0, band_hi = 0;
+  int64_t ell_rows = 0;
+  const uint8_t* rcode = nullptr;
+  const double2* rpat = nullptr;
+  const uint8_t* rlen = nullptr;
+  int npat = 0;
   int64_t ext_len() const { return h_lo + rows + h_hi; }
 };
+
+// The slab's rows in 1-byte codes when the operator allows (sparse.cu build_pair_dict /
+// build_row_dict): the gathers stay r + diag_off + delta into the extended vector.
+int setup_slab_dict(Slab& sl, const int64_t* rp_dev, const int32_t* col_dev, const double* val_dev,
+                    cudaStream_t s) {
+  static const bool dict_on = !(std::getenv("NNB_SPARSE_DICT") && std::strcmp(std::getenv("NNB_SPARSE_DICT"), "0") == 0);
+  static const bool rowdict_on =
+      !(std::getenv("NNB_SPARSE_ROWDICT") && std::strcmp(std::getenv("NNB_SPARSE_ROWDICT"), "0") == 0);
+  if (!dict_on || sl.rows == 0) return 0;
+  NNB_TRY(sl.dict_mem.alloc((sizeof(int32_t) + sizeof(double)) * kPairDictMax, s));
+  double* dv = sl.dict_mem.as<double>();
+  int32_t* dd = reinterpret_cast<int32_t*>(dv + kPairDictMax);
+  bool ok = false;
+  int size = 0, width = 0, lo = 0, hi = 0;
+  int64_t plane = 0;
+  NNB_TRY(build_pair_dict(rp_dev, col_dev, val_dev, sl.rows, sl.row0, sl.nnz, sl.code_mem, &width, &plane, &lo, &hi,
+                          dd, dv, &size, &ok, s));
+  if (!ok) return 0;
+  sl.code = sl.code_mem.as<uint8_t>();
+  sl.dict_delta = dd;
+  sl.dict_val = dv;
+  sl.dict_size = size;
+  sl.ell_width = width;
+  sl.ell_rows = plane;
+  sl.band_lo = lo;
+  sl.band_hi = hi;
+  if (!width || !rowdict_on) return 0;
+  NNB_TRY(sl.rowdict_mem.alloc(sizeof(double2) * kRowDictMax * kEllMaxWidth + kRowDictMax + sl.rows, s));
+  double2* pat = sl.rowdict_mem.as<double2>();
+  uint8_t* plen = reinterpret_cast<uint8_t*>(pat + kRowDictMax * kEllMaxWidth);
+  uint8_t* rcode = plen + kRowDictMax;
+  bool rok = false;
+  int npat = 0;
+  NNB_TRY(build_row_dict(sl.code, width, plane, sl.rows, dd, dv, rcode, pat, plen, &npat, &rok, s));
+  if (rok) {
+    sl.rcode = rcode;
+    sl.rpat = pat;
+    sl.rlen = plen;
+    sl.npat = npat;
+  }
+  return 0;
+}
 
 // Builds the slab's device structures from its CSR rows (global columns).
 int setup_slab(Slab& sl, const int64_t* rp_dev, const int32_t* col_dev, const double* val_dev, int64_t k,
@@ -126,6 +180,15 @@ int setup_slab(Slab& sl, const int64_t* rp_dev, const int32_t* col_dev, const do
     count_launch();
   }
   sl.val = val_dev + base;
+  if (k == 1) NNB_TRY(setup_slab_dict(sl, rp_dev, col_dev, val_dev, s));
+  set_sparse_bytes_per_nnz(sl.code ? 1 : (sl.col16 ? 10 : 12));
+  set_sparse_format(sl.rcode ? "row-dictionary"
+                    : sl.ell_width ? "pair-dictionary-ell"
+                    : sl.code ? "pair-dictionary-csr"
+                    : sl.col16 ? "csr-int16-delta" : "csr-int32");
+  set_sparse_matrix_bytes(sl.rcode ? sl.rows
+                          : sl.ell_width ? (int64_t)sl.ell_width * sl.rows
+                                         : sl.nnz * (sl.code ? 1 : (sl.col16 ? 10 : 12)) + (sl.rows + 1) * 4);
   NNB_CUDA(cudaGetLastError());
   return 0;
 }
@@ -155,7 +218,8 @@ int run_slabs(std::vector<Slab*>& slabs, int64_t k, int s_factors, double theta,
         Slab& sl = *slabs[g];
         SpmvOp<int32_t> op{sl.rp, sl.col, sl.col16, sl.h_lo, sl.val, k, sl.ext[tin], sl.ext[tin] + sl.h_lo * k,
                            out < 0 ? x_own[g] : sl.ext[out] + sl.h_lo * k, sl.ext[zcur] + sl.h_lo * k, theta,
-                           sl.flags + f};
+                           sl.flags + f, sl.code, sl.dict_delta, sl.dict_val, sl.dict_size, sl.ell_width,
+                           sl.ell_rows, sl.band_lo, sl.band_hi, sl.rcode, sl.rpat, sl.rlen, sl.npat};
         spmv_apply(op, mode, sl.lo_end, sl.hi_start, s);  // interior, while the halo is in flight
         NNB_TRY(wait_halo(g));
         spmv_apply(op, mode, 0, sl.lo_end, s);            // boundary rows

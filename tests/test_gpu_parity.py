@@ -457,6 +457,30 @@ def test_sparse_pair_dictionary_sample_miss(ref):
     b = W.rhs(n, seed=5)
     x, _ = nnb.solve_sparse_factorized(nnb.Csr(rp, col, val, n=n), b, 15, nnb.Normalization(0.25, valid=True))
     assert nnb.sparse_last_bytes_per_nnz() == 1
+    assert nnb.sparse_last_format() == "pair-dictionary-csr"  # one width-5 row: ELL would pad by 67 %
+    xr, _, _ = ref.sparse_factorized(rp, col, val, b, 15, 0.25)
+    assert np.array_equal(x, xr.real)
+
+
+def test_sparse_row_dictionary_sample_miss(ref):
+    """Every pair occurs in the sampled rows but one whole row (no diagonal) only in the
+    middle: the pair dictionary is taken from the sample, the row dictionary goes round
+    again over all rows -- bit-identical either way."""
+    n = 400000
+    mid = n // 2
+    rp = np.zeros(n + 1, np.int64)
+    cols, vals = [], []
+    for i in range(n):
+        ents = [(i - 1, -1.0), (i + 1, -1.0)] if i == mid else [(i - 1, -1.0), (i, 4.0), (i + 1, -1.0)]
+        for j, v in ents:
+            if 0 <= j < n:
+                cols.append(j)
+                vals.append(v)
+        rp[i + 1] = len(cols)
+    col, val = np.array(cols, np.int32), np.array(vals)
+    b = W.rhs(n, seed=6)
+    x, _ = nnb.solve_sparse_factorized(nnb.Csr(rp, col, val, n=n), b, 15, nnb.Normalization(0.25, valid=True))
+    assert nnb.sparse_last_format() == "row-dictionary"
     xr, _, _ = ref.sparse_factorized(rp, col, val, b, 15, 0.25)
     assert np.array_equal(x, xr.real)
 

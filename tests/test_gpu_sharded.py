@@ -75,9 +75,10 @@ def test_sparse_sharded_emulated_bitexact(ref, world):
     csr = nnb.Csr(rp, col, val, n=10000)
     norm = nnb.Normalization(theta=0.2, valid=True)
     xs, cnt = nnb.solve_sparse_factorized_sharded_emulated(csr, b, 63, norm, world)
+    assert nnb.sparse_last_format() == "row-dictionary"  # each slab's rows in 1-byte pattern codes
     xr, cr, _ = ref.sparse_factorized(rp, col, val, b, 63, 0.2)
     assert cnt == cr == 63 and np.array_equal(xs, xr.real)
-    b2 = np.random.default_rng(world).standard_normal((10000, 2))
+    b2 = np.random.default_rng(world).standard_normal((10000, 2))  # two right-hand sides: int16 deltas
     xs2, _ = nnb.solve_sparse_factorized_sharded_emulated(csr, b2, 15, norm, world)
     xr2, _, _ = ref.sparse_factorized(rp, col, val, b2, 15, 0.2)
     assert np.array_equal(xs2, xr2.real)
@@ -96,6 +97,7 @@ def test_sparse_sharded_emulated_full_size_matches_single():
     x8, _ = nnb.solve_sparse_factorized_sharded_emulated(csr, b, 63, norm, 8)
     torch.cuda.synchronize()
     assert torch.equal(x1, x8)
+    assert nnb.sparse_last_format() == "row-dictionary"
 
 
 def test_sparse_sharded_nccl_world1(ref):
