@@ -166,6 +166,28 @@ __device__ __forceinline__ void zmma_ss(ZAcc<M3>& acc, const SMat& L, const SMat
   }
 }
 
+// 3M acc += L·R where L·R is Hermitian: tiles (0,0), (0,1), (1,1) only (36 DMMA
+// instead of 48); epilogue_seeded_herm mirrors (0,1) into (1,0).
+__device__ __forceinline__ void zmma_ss_herm(ZAcc<true>& acc, const SMat& L, const SMat& R, int g, int t) {
+#pragma unroll
+  for (int kb = 0; kb < 4; ++kb) {
+    double lr[2], li[2], rr[2], ri[2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int idx = swz(8 * mt + g, 4 * kb + t);
+      lr[mt] = L.re[idx];
+      li[mt] = L.im[idx];
+    }
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int idx = swz(4 * kb + t, 8 * nt + g);
+      rr[nt] = R.re[idx];
+      ri[nt] = R.im[idx];
+    }
+    acc.step_herm(lr, li, rr, ri);
+  }
+}
+
 // acc += L·A with A's B-operand fragments in registers: areg[nt][kb][plane] = A[4kb+t][8nt+g].
 template <bool M3>
 __device__ __forceinline__ void zmma_sr(ZAcc<M3>& acc, const SMat& L, const double (&areg)[2][4][2], int g,
@@ -264,6 +286,69 @@ __device__ __forceinline__ void epilogue_seeded(const ZAcc<true>& acc, const SMa
   __syncwarp();
 }
 
+// epilogue_seeded<false> for a Hermitian result from zmma_ss_herm: tiles (0,0),
+// (0,1), (1,1) stored, (1,0) = conj((0,1))ᵀ.
+__device__ __forceinline__ void epilogue_seeded_herm(const ZAcc<true>& acc, const SMat& out, int g, int t) {
+  __syncwarp();  // every lane finished reading operands that `out` may overwrite
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = mt; nt < 2; ++nt) {
+      const int r = 8 * mt + g, c = 8 * nt + 2 * t;
+      const double* p0 = acc.v[mt][nt][0];
+      const double* p1 = acc.v[mt][nt][1];
+      const double* p2 = acc.v[mt][nt][2];
+      const double2 vr = make_double2(p0[0] - p1[0], p0[1] - p1[1]);
+      const double2 vi = make_double2(p2[0] - (p0[0] + p1[0]), p2[1] - (p0[1] + p1[1]));
+      *reinterpret_cast<double2*>(out.re + swz(r, c)) = vr;
+      *reinterpret_cast<double2*>(out.im + swz(r, c)) = vi;
+      if (mt != nt) {
+        out.re[swz(c, r)] = vr.x;
+        out.im[swz(c, r)] = -vi.x;
+        out.re[swz(c + 1, r)] = vr.y;
+        out.im[swz(c + 1, r)] = -vi.y;
+      }
+    }
+  __syncwarp();
+}
+
+// One Horner step V' = X + P·V (3M, seeded).  For Hermitian A and X every such
+// product is Hermitian — P·V = poly(P)·X and (I − XA)^k X = X (I − AX)^k — so
+// `herm` computes three of its four 8×8 tiles and mirrors the fourth.
+__device__ __forceinline__ void horner_step(ZAcc<true>& acc, const SMat& X, const SMat& Pm, const SMat& v,
+                                            const SMat& out, bool herm, int g, int t) {
+  acc.template seed<false>(&X, 0.0, g, t);
+  if (herm) {
+    zmma_ss_herm(acc, Pm, v, g, t);
+    epilogue_seeded_herm(acc, out, g, t);
+  } else {
+    zmma_ss(acc, Pm, v, g, t);
+    epilogue_seeded<false>(acc, out, g, t);
+  }
+}
+
+// A == Aᴴ exactly (NaN never equal: such systems take the full products), from
+// A's register fragments alone: lane (g, t) holds A[4kb+t][8nt+g]; the
+// transposed element A[8nt+g][4kb+t] sits in lane (4(kb&1)+t, g&3) as its
+// fragment [kb>>1][2nt + (g>>2)], fetched by shuffles (both candidates, then
+// selected).  Called once the fragments are in use anyway, so it adds no wait.
+__device__ __forceinline__ bool is_hermitian(const double (&areg)[2][4][2], int g, int t) {
+  bool ok = true;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {
+      const int src = (4 * (kb & 1) + t) * 4 + (g & 3);
+      const double r0 = __shfl_sync(0xffffffffu, areg[kb >> 1][2 * nt][0], src);
+      const double i0 = __shfl_sync(0xffffffffu, areg[kb >> 1][2 * nt][1], src);
+      const double r1 = __shfl_sync(0xffffffffu, areg[kb >> 1][2 * nt + 1][0], src);
+      const double i1 = __shfl_sync(0xffffffffu, areg[kb >> 1][2 * nt + 1][1], src);
+      const bool hi = (g >> 2) != 0;
+      ok &= (hi ? r1 : r0) == areg[nt][kb][0] && (hi ? i1 : i0) == -areg[nt][kb][1];
+    }
+  return __all_sync(0xffffffffu, ok);
+}
+
 // Σ|I − X·A|² without storing the residual.
 template <bool M3>
 __device__ __forceinline__ double residual_ss(const ZAcc<M3>& acc, int g, int t) {
@@ -304,7 +389,8 @@ __device__ __forceinline__ void load_a_frags(const double2* __restrict__ As, int
 // C2 system).  Returns with X = X1 and P holding I − X0·A.
 template <int P, bool M3>
 __device__ __forceinline__ void first_nest_diag(ZAcc<M3>& acc, const SMat& X, const SMat& Pm, const SMat& V,
-                                                const double (&areg)[2][4][2], int g, int t) {
+                                                const double (&areg)[2][4][2], int g, int t, bool herm_ok,
+                                                bool* herm_out) {
   double2 xr[4], xc[2], pv[2][4];
 #pragma unroll
   for (int kb = 0; kb < 4; ++kb) {
@@ -345,13 +431,15 @@ __device__ __forceinline__ void first_nest_diag(ZAcc<M3>& acc, const SMat& X, co
       d1.im[idx] = vi;
     }
   __syncwarp();
+  // A's fragments have arrived (used above): the Hermitian test costs no wait here;
+  // the caller passes the result on to the later nests
+  const bool herm = herm_ok && (herm_out ? is_hermitian(areg, g, t) : true);
+  if (herm_out) *herm_out = herm;
   const SMat* v = &V;
 #pragma unroll
   for (int j = 2; j <= P; ++j) {  // V = X0 + P·V; the last step lands in X
     if constexpr (M3) {
-      acc.template seed<false>(&X, 0.0, g, t);
-      zmma_ss(acc, Pm, *v, g, t);
-      epilogue_seeded<false>(acc, (j == P) ? X : V, g, t);
+      horner_step(acc, X, Pm, *v, (j == P) ? X : V, herm, g, t);
     } else {
       acc.zero();
       zmma_ss(acc, Pm, *v, g, t);
@@ -367,7 +455,7 @@ __device__ __forceinline__ void first_nest_diag(ZAcc<M3>& acc, const SMat& X, co
 template <int P, bool M3, bool PREFETCH>
 __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
     batched_z16_kernel(const double2* __restrict__ A, int64_t batch, int iters, int ns_order,
-                       double2* __restrict__ Xout, double* __restrict__ eps_last, int ns_mode) {
+                       double2* __restrict__ Xout, double* __restrict__ eps_last, int ns_mode, int herm_ok) {
   __shared__ __align__(16) double smem[kWarpsPerCta][3][2][kMat];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -393,6 +481,7 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
     } else {
       load_a_frags(As, g, t, areg);
     }
+
     // X0 = diag(A)^-1 (Smith's complex reciprocal, as libgcc's __divdc3)
     for (int i = lane; i < kMat; i += 32) {
       X.re[i] = 0.0;
@@ -419,7 +508,9 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
     ZAcc<M3> acc;
     if (!ns_mode) {
       // ---- Nested Neumann: `iters` nests of depth P (nest 0 from the diagonal X0) ----
-      if (iters > 0) first_nest_diag<P, M3>(acc, X, Pm, V, areg, g, t);
+      // Hermitian A (and so X0): the Horner products compute three of four tiles
+      bool herm = false;
+      if (iters > 0) first_nest_diag<P, M3>(acc, X, Pm, V, areg, g, t, M3 && herm_ok, &herm);
       for (int it = 1; it < iters; ++it) {
         const SMat* v = &X;
         if constexpr (M3) {
@@ -428,9 +519,7 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
           epilogue_seeded<true>(acc, Pm, g, t);         // P = I − X·A
 #pragma unroll
           for (int j = 1; j <= P; ++j) {
-            acc.template seed<false>(&X, 0.0, g, t);    // X
-            zmma_ss(acc, Pm, *v, g, t);                 // X + P·V
-            epilogue_seeded<false>(acc, (j == P) ? X : V, g, t);  // the last Horner step lands in X
+            horner_step(acc, X, Pm, *v, (j == P) ? X : V, herm, g, t);  // X + P·V; the last lands in X
             v = &V;
           }
         } else {
@@ -516,7 +605,7 @@ template <int P>
 __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
     mimo_detect_kernel(const double2* __restrict__ H, const double2* __restrict__ Y, int64_t batch, int ant,
                        double sigma2, int iters, double2* __restrict__ xhat, double2* __restrict__ Xout,
-                       double* __restrict__ eps_last) {
+                       double* __restrict__ eps_last, int herm_ok) {
   constexpr bool M3 = true;
   __shared__ __align__(16) double smem[kWarpsPerCta][3][2][kMat];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -586,7 +675,9 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
     }
     __syncwarp();
     // ---- Nested Neumann inversion (seeded 3M products, nest 0 from the diagonal X0) ----
-    if (iters > 0) first_nest_diag<P, true>(acc, X, Pm, V, areg, g, t);
+    // A = HᴴH + σ²I is Hermitian by construction (gram_epilogue mirrors it)
+    const bool herm = herm_ok != 0;
+    if (iters > 0) first_nest_diag<P, true>(acc, X, Pm, V, areg, g, t, herm, nullptr);
     for (int it = 1; it < iters; ++it) {
       acc.template seed<true>(nullptr, 1.0, g, t);
       zmma_sr(acc, X, areg, g, t);
@@ -594,9 +685,7 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
       const SMat* v = &X;
 #pragma unroll
       for (int j = 1; j <= P; ++j) {
-        acc.template seed<false>(&X, 0.0, g, t);
-        zmma_ss(acc, Pm, *v, g, t);
-        epilogue_seeded<false>(acc, (j == P) ? X : V, g, t);  // V = X + P·V
+        horner_step(acc, X, Pm, *v, (j == P) ? X : V, herm, g, t);  // V = X + P·V
         v = &V;
       }
     }
@@ -637,6 +726,12 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
   }
 }
 
+// NNB_BATCHED_HERM=0: full products for Hermitian systems too (A/B measurement)
+int herm_enabled() {
+  static const int on = !(std::getenv("NNB_BATCHED_HERM") && std::strcmp(std::getenv("NNB_BATCHED_HERM"), "0") == 0);
+  return on;
+}
+
 template <int P, bool M3, bool PF>
 int launch_variant(const double2* a, int64_t batch, int iters, int ns_order, double2* x, double* eps,
                    int ns_mode, cudaStream_t s) {
@@ -651,7 +746,7 @@ int launch_variant(const double2* a, int64_t batch, int iters, int ns_order, dou
   }
   const int64_t want = (batch + kWarpsPerCta - 1) / kWarpsPerCta;
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(want, (int64_t)sms * blocks_per_sm));
-  batched_z16_kernel<P, M3, PF><<<grid, kThreads, 0, s>>>(a, batch, iters, ns_order, x, eps, ns_mode);
+  batched_z16_kernel<P, M3, PF><<<grid, kThreads, 0, s>>>(a, batch, iters, ns_order, x, eps, ns_mode, herm_enabled());
   count_launch();
   NNB_CUDA(cudaGetLastError());
   return 0;
@@ -688,7 +783,7 @@ int launch_mimo(const double2* h, const double2* y, int64_t batch, int ant, doub
   }
   const int64_t want = (batch + kWarpsPerCta - 1) / kWarpsPerCta;
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(want, (int64_t)sms * blocks_per_sm));
-  mimo_detect_kernel<P><<<grid, kThreads, 0, s>>>(h, y, batch, ant, sigma2, iters, xhat, X, eps);
+  mimo_detect_kernel<P><<<grid, kThreads, 0, s>>>(h, y, batch, ant, sigma2, iters, xhat, X, eps, herm_enabled());
   count_launch();
   NNB_CUDA(cudaGetLastError());
   return 0;

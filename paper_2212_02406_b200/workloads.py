@@ -42,18 +42,22 @@ def spd_conditioned(n: int, cond: float, seed: int) -> np.ndarray:
 
 def mimo_gram_host(batch: int, seed: int, antennas: int = 128, users: int = 16,
                    sigma2: float = 0.1) -> np.ndarray:
-    """C2 on the host: A = H^H·H + sigma²·I, H antennas×users, H_ij ~ CN(0, 1/antennas)."""
+    """C2 on the host: A = H^H·H + sigma²·I, H antennas×users, H_ij ~ CN(0, 1/antennas).
+    The product is symmetrised so A is stored exactly Hermitian (a GEMM rounds (i, j)
+    and (j, i) independently); the batched kernel's mirrored Horner products need it."""
     rng = np.random.default_rng(seed)
     s = np.sqrt(0.5 / antennas)
     h = (rng.standard_normal((batch, antennas, users)) + 1j * rng.standard_normal((batch, antennas, users))) * s
     a = np.conj(np.transpose(h, (0, 2, 1))) @ h
+    a = 0.5 * (a + np.conj(np.transpose(a, (0, 2, 1))))  # exactly Hermitian, as H^H·H is
     a += sigma2 * np.eye(users)
     return a
 
 
 def mimo_gram_device(batch: int, seed: int, antennas: int = 128, users: int = 16, sigma2: float = 0.1,
                      device: str = "cuda", chunk: int = 32768):
-    """C2 on the GPU (torch Philox), chunked so H never exceeds ~1 GB."""
+    """C2 on the GPU (torch Philox), chunked so H never exceeds ~1 GB; exactly Hermitian
+    like mimo_gram_host."""
     import torch
 
     gen = torch.Generator(device=device)
@@ -66,7 +70,8 @@ def mimo_gram_device(batch: int, seed: int, antennas: int = 128, users: int = 16
         re = torch.randn((b1 - b0, antennas, users), dtype=torch.float64, device=device, generator=gen)
         im = torch.randn((b1 - b0, antennas, users), dtype=torch.float64, device=device, generator=gen)
         h = torch.complex(re, im) * s
-        out[b0:b1] = h.conj().transpose(1, 2) @ h + eye
+        g = h.conj().transpose(1, 2) @ h
+        out[b0:b1] = 0.5 * (g + g.conj().transpose(1, 2)) + eye  # exactly Hermitian, as H^H·H is
     return out
 
 

@@ -285,6 +285,23 @@ def test_batched_vs_reference(ref, p, iters):
     eps_close(eps, er)
 
 
+def test_batched_mixed_hermitian_and_general(ref):
+    """Hermitian systems run their Horner products on three of four 8x8 tiles (the
+    fourth mirrored); any other system -- one element off its conjugate mirror, or a
+    general diagonally dominant matrix -- takes the full products.  Both kinds in one
+    batch (one warp per system) match the reference."""
+    a = W.mimo_gram_host(96, seed=21)
+    rng = np.random.default_rng(5)
+    a[1, 2, 5] += 1e-3  # no longer Hermitian
+    for s in range(3, 96, 4):  # general complex, diagonally dominant
+        m = (rng.standard_normal((16, 16)) + 1j * rng.standard_normal((16, 16))) * 0.02
+        a[s] = m + np.diag(1.0 + 0.1 * rng.random(16))
+    x, eps = nnb.nn_batched(a, p=2, iters=4)
+    xr, er, _ = ref.batched("nn", a, 2, 4, threads=8)
+    assert max(rel_frob(x[s], xr[s]) for s in range(96)) < TOL_X
+    eps_close(eps, er)
+
+
 def test_batched_ns_orders(ref):
     a = W.mimo_gram_host(64, seed=11)
     for order in (0, 1, 2, 26):

@@ -26,7 +26,7 @@ def test_gram_and_spd():
 def test_mimo_gram():
     a = W.mimo_gram_host(8, 1)
     assert a.shape == (8, 16, 16)
-    assert np.allclose(a, np.conj(np.transpose(a, (0, 2, 1))))
+    assert np.array_equal(a, np.conj(np.transpose(a, (0, 2, 1))))  # exactly Hermitian
     assert np.all(np.linalg.eigvalsh(a) >= 0.1 - 1e-12)
     # E[diag] = 1 + sigma^2 for CN(0, 1/128) entries over 128 antennas
     assert abs(np.mean(np.real(np.diagonal(a, axis1=1, axis2=2))) - 1.1) < 0.1
