@@ -338,6 +338,7 @@ __device__ __forceinline__ bool is_hermitian(const double (&areg)[2][4][2], int 
   for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
     for (int kb = 0; kb < 4; ++kb) {
+      if (nt == 1 && kb < 2) continue;  // the tile above the diagonal: its mirror (nt 0, kb 2..3) checked it
       const int src = (4 * (kb & 1) + t) * 4 + (g & 3);
       const double r0 = __shfl_sync(0xffffffffu, areg[kb >> 1][2 * nt][0], src);
       const double i0 = __shfl_sync(0xffffffffu, areg[kb >> 1][2 * nt][1], src);
