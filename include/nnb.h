@@ -223,7 +223,11 @@ int nnb_nn_explicit_z(const double* phi0, const double* w, int64_t n, int64_t ne
 /* ---- batched small complex systems (massive-MIMO Gram inversion) ------- */
 /* batch independent n×n complex128 systems (n == 16), X0 = diag(A)^-1,
  * `iters` nests of depth p in reference order (nn_step per system) and the
- * residual after the last nest in eps_last (nullable, host or device). */
+ * residual after the last nest in eps_last (nullable, host or device).
+ * A system whose A is stored exactly Hermitian (A == A^H bit for bit, as
+ * the massive-MIMO Gram H^H·H + s²·I is) runs its Horner products on three
+ * of four 8×8 tiles: each is Hermitian by push-through.  Results agree with
+ * the full products to rounding; other systems take the full products. */
 int nnb_nn_batched_z(const double* A, int64_t batch, int32_t n, int32_t p, int32_t iters,
                      double* X_out, double* eps_last, void* stream);
 /* Neumann-series baseline of `order` terms from the same X0 (ns_sum). */
