@@ -738,6 +738,40 @@ def test_c4_full_size_nest_cubes_the_residual():
     assert rep.products == 4
 
 
+def test_c4_full_size_sampled_residual_rows():
+    """SURVEY §8(c) C4 items (iii)-(iv) at the headline size (N=32768, p=2), where no CPU
+    oracle runs whole: 64 seeded rows of R = I - A·X (at 64 seeded columns) recomputed on
+    the host in 80-bit extended precision agree with the DMMA GEMM's within the
+    deterministic FP64 bound K·u·(|A||X|); and the eps history falls monotonically, each
+    nest cubing the residual (eps_k+1 <= eps_k up to its first factor)."""
+    import torch
+
+    n = 32768
+    g = torch.Generator(device="cuda").manual_seed(2213)
+    b = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
+    a = torch.addmm(torch.eye(n, dtype=torch.float64, device="cuda"), b, b.T, alpha=1.0 / n)
+    del b
+    torch.cuda.empty_cache()
+    x, rep = nnb.nn_chain(a, None, p=2, max_iters=4)  # X0 = A^T/(|A|_1|A|_inf) built on the device
+    eps = [e for _, e in rep.history]
+    assert len(eps) == 5 and all(e1 < e0 for e0, e1 in zip(eps, eps[1:]))
+    rng = np.random.default_rng(2212)
+    rows = np.sort(rng.choice(n, 64, replace=False))
+    cols = np.sort(rng.choice(n, 64, replace=False))
+    ri = torch.from_numpy(rows).cuda()
+    ar = a.index_select(0, ri).contiguous()
+    r_gpu = -nnb.matmul(ar, x)  # the library's DMMA GEMM: -(A[rows]·X)
+    r_gpu[torch.arange(64, device="cuda"), ri] += 1.0
+    r_gpu = r_gpu[:, torch.from_numpy(cols).cuda()].cpu().numpy()
+    a_ld = ar.cpu().numpy().astype(np.longdouble)
+    x_ld = x[:, torch.from_numpy(cols).cuda()].cpu().numpy().astype(np.longdouble)
+    r_ld = (rows[:, None] == cols[None, :]).astype(np.longdouble) - a_ld @ x_ld
+    bound = n * 2.0 ** -53 * (np.abs(a_ld) @ np.abs(x_ld))
+    diff = np.abs(r_gpu.astype(np.longdouble) - r_ld)
+    assert (diff <= bound).all(), float((diff / bound).max())
+    assert float(np.median(diff / bound)) < 1e-2  # typical errors far inside the worst case
+
+
 # ----------------------------------------------------------------- direct inverse oracle
 @pytest.mark.parametrize("n,seed", [(1, 1), (5, 2), (64, 3), (200, 4)])
 def test_direct_inverse_bitexact(ref, n, seed):
