@@ -538,6 +538,75 @@ __global__ void rowdict_encode_kernel(const uint8_t* __restrict__ code, int widt
   if (bad) atomicOr(collision, 1);
 }
 
+// Pair codes and row keys in one pass over the CSR: each nonzero's (column − row,
+// value) is looked up (and verified) in the pair table, the row's codes packed
+// into its key, and the key looked up in the row table; only the row code is
+// written.  Any miss (a pair or row outside the sampled tables, a longer row)
+// sets *collision and the caller takes the two-pass build.
+__global__ void rowdict_direct_encode_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                             const double* __restrict__ val, int64_t rows, int64_t row0,
+                                             const DictWs* ws, const RowDictWs* rws, int width,
+                                             uint8_t* __restrict__ rcode, int* collision) {
+  bool bad = false, have = false;
+  unsigned long long last = 0;
+  int last_idx = -1;
+  // the last verified pair at each position (compile-time indexed: registers): a
+  // thread's rows, one grid stride apart, mostly repeat them, so the pair table
+  // is probed only when a position's pair changes
+  int32_t cd[kEllMaxWidth];
+  unsigned long long cb[kEllMaxWidth];
+  int ci[kEllMaxWidth];
+#pragma unroll
+  for (int i = 0; i < kEllMaxWidth; ++i) ci[i] = -1;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = rp[r], len = rp[r + 1] - e0;
+    if (len > width) {
+      bad = true;
+      continue;
+    }
+    unsigned long long key = ~0ull;
+#pragma unroll
+    for (int i = 0; i < kEllMaxWidth; ++i) {
+      if (i >= len) break;
+      const int64_t dl = (int64_t)col[e0 + i] - (row0 + r);
+      const int32_t d = static_cast<int32_t>(dl);
+      const unsigned long long b = __double_as_longlong(val[e0 + i]);
+      if (!(ci[i] >= 0 && cd[i] == d && cb[i] == b && dl == d)) {
+        const unsigned long long h = pair_hash(d, b);
+        int slot = static_cast<int>(h & (kDictSlots - 1));
+        int probe = 0;
+        while (ws->hash[slot] != h && ws->hash[slot] != 0 && probe < kDictSlots) {
+          slot = (slot + 1) & (kDictSlots - 1);
+          ++probe;
+        }
+        const bool hit = dl >= INT32_MIN && dl <= INT32_MAX && ws->hash[slot] == h && ws->delta[slot] == d &&
+                         __double_as_longlong(ws->val[slot]) == static_cast<long long>(b);
+        bad |= !hit;
+        cd[i] = d;
+        cb[i] = b;
+        ci[i] = hit ? ws->index[slot] : -1;
+      }
+      const unsigned long long q = ci[i] >= 0 ? static_cast<unsigned long long>(ci[i]) : 0ull;
+      key = (key & ~(0xffull << (8 * i))) | (q << (8 * i));
+    }
+    if (!have || key != last) {
+      const unsigned long long h = key_hash(key);
+      int slot = static_cast<int>(h & (kDictSlots - 1));
+      int probe = 0;
+      while (rws->hash[slot] != h && rws->hash[slot] != 0 && probe < kDictSlots) {
+        slot = (slot + 1) & (kDictSlots - 1);
+        ++probe;
+      }
+      last_idx = (rws->hash[slot] == h && rws->key[slot] == key) ? rws->index[slot] : -1;
+      last = key;
+      have = true;
+    }
+    bad |= last_idx < 0;
+    rcode[r] = static_cast<uint8_t>(last_idx < 0 ? 0 : last_idx);
+  }
+  if (bad) atomicOr(collision, 1);
+}
+
 // Plain Y = W·X for nn::spmv_block (same rounding as the reference's sum).
 __global__ void spmv_plain_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                                   const double* __restrict__ val, int64_t n, int64_t k,
@@ -890,6 +959,70 @@ int build_row_dict(const uint8_t* code, int width, int64_t plane, int64_t rows, 
   return 0;
 }
 
+int build_row_dict_direct(const int64_t* rp, const int32_t* col, const double* val, int64_t rows, int64_t row0,
+                          int32_t* dict_delta, double* dict_val, int* dict_size, int* width, int* band_lo,
+                          int* band_hi, uint8_t* rcode, double2* pat, uint8_t* plen, int* npat, bool* ok,
+                          cudaStream_t s) {
+  *ok = false;
+  constexpr int64_t kSample = 65536;
+  if (rows <= 4 * kSample) return 0;  // small operators: the two-pass build
+  DevBuf wsb, rwsb, sample;
+  NNB_TRY(wsb.alloc(sizeof(DictWs), s));
+  NNB_TRY(rwsb.alloc(sizeof(RowDictWs), s));
+  DictWs* ws = wsb.as<DictWs>();
+  RowDictWs* rws = rwsb.as<RowDictWs>();
+  NNB_CUDA(cudaMemsetAsync(ws, 0, sizeof(DictWs), s));
+  NNB_CUDA(cudaMemsetAsync(rws, 0, sizeof(RowDictWs), s));
+  // pair table from the first and last kSample rows
+  dict_insert_kernel<<<rows_grid(kSample), 256, 0, s>>>(rp, col, val, kSample, row0, ws);
+  dict_insert_kernel<<<rows_grid(kSample), 256, 0, s>>>(rp + (rows - kSample), col, val, kSample,
+                                                        row0 + rows - kSample, ws);
+  dict_index_kernel<<<1, 1024, 0, s>>>(ws, dict_delta, dict_val);
+  count_launch(3);
+  int f[5];  // count, overflow, collision, size, max_len
+  NNB_CUDA(cudaMemcpyAsync(f, &ws->count, sizeof(f), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  const int w = f[4];
+  if (f[1] || f[3] > kPairDictMax - 1 || w < 1 || w > kEllMaxWidth) return 0;
+  // the sampled rows' ELL codes, then the row table from them
+  const int64_t plane = 2 * kSample;
+  NNB_TRY(sample.alloc((size_t)w * plane, s));
+  uint8_t* sc = sample.as<uint8_t>();
+  dict_encode_kernel<<<rows_grid(kSample), 256, 0, s>>>(rp, col, val, kSample, row0, ws, sc, w, plane,
+                                                        &ws->collision);
+  dict_encode_kernel<<<rows_grid(kSample), 256, 0, s>>>(rp + (rows - kSample), col, val, kSample,
+                                                        row0 + rows - kSample, ws, sc + kSample, w, plane,
+                                                        &ws->collision);
+  rowdict_insert_kernel<<<rows_grid(plane), 256, 0, s>>>(sc, w, plane, plane, rws);
+  rowdict_index_kernel<<<1, 1024, 0, s>>>(rws, w, dict_delta, dict_val, pat, plen);
+  count_launch(4);
+  int rf[4];  // count, overflow, collision, size
+  NNB_CUDA(cudaMemcpyAsync(f, &ws->count, sizeof(f), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaMemcpyAsync(rf, &rws->count, sizeof(rf), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  if (f[2] || rf[1] || rf[3] > kRowDictMax) return 0;
+  // every row: pair codes verified, row key looked up, one byte written
+  rowdict_direct_encode_kernel<<<rows_grid(rows), 256, 0, s>>>(rp, col, val, rows, row0, ws, rws, w, rcode,
+                                                               &rws->collision);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  NNB_CUDA(cudaMemcpyAsync(rf, &rws->count, sizeof(rf), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  if (rf[2]) return 0;
+  std::vector<int32_t> dh(f[3]);
+  NNB_CUDA(cudaMemcpy(dh.data(), dict_delta, sizeof(int32_t) * dh.size(), cudaMemcpyDeviceToHost));
+  *band_lo = *band_hi = 0;
+  for (int32_t d : dh) {
+    *band_lo = std::min(*band_lo, d);
+    *band_hi = std::max(*band_hi, d);
+  }
+  *dict_size = f[3];
+  *width = w;
+  *npat = rf[3];
+  *ok = true;
+  return 0;
+}
+
 int spmv_csr(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n, const double* X, int64_t k,
              double* Y, cudaStream_t s) {
   if (n == 0) return 0;
@@ -991,36 +1124,50 @@ int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* 
       bool ok = false;
       int size = 0, width = 0, lo = 0, hi = 0;
       int64_t plane = 0;
-      NNB_TRY(build_pair_dict(row_ptr, col, val, n, 0, nnz, code_buf, &width, &plane, &lo, &hi, dd, dv, &size, &ok,
-                              s));
-      if (ok) dict = PairDict{code_buf.as<uint8_t>(), dd, dv, size, width, plane, lo, hi};
-      // ELL codes with few distinct rows (stencils): one pattern code per row
       static const bool rowdict_on = [] {  // NNB_SPARSE_ROWDICT=0: keep the ELL pair codes (A/B measurement)
         const char* e = std::getenv("NNB_SPARSE_ROWDICT");
         return !(e && std::strcmp(e, "0") == 0);
       }();
-      if (ok && width && k == 1 && rowdict_on) {
-        NNB_TRY(rowdict_buf.alloc(sizeof(double2) * kRowDictMax * kEllMaxWidth + kRowDictMax + n, s));
-        double2* pat = rowdict_buf.as<double2>();
-        uint8_t* plen = reinterpret_cast<uint8_t*>(pat + kRowDictMax * kEllMaxWidth);
-        uint8_t* rcode = plen + kRowDictMax;
-        bool rok = false;
-        int npat = 0;
-        NNB_TRY(build_row_dict(dict.code, width, plane, n, dd, dv, rcode, pat, plen, &npat, &rok, s));
-        if (rok) {
-          dict.rcode = rcode;
-          dict.rpat = pat;
-          dict.rlen = plen;
-          dict.npat = npat;
+      static const bool direct_on = [] {  // NNB_SPARSE_DIRECT=0: the two-pass row-dictionary build (A/B)
+        const char* e = std::getenv("NNB_SPARSE_DIRECT");
+        return !(e && std::strcmp(e, "0") == 0);
+      }();
+      const bool want_rows = k == 1 && rowdict_on && n < INT32_MAX / 2;
+      if (want_rows) NNB_TRY(rowdict_buf.alloc(sizeof(double2) * kRowDictMax * kEllMaxWidth + kRowDictMax + n, s));
+      double2* pat = want_rows ? rowdict_buf.as<double2>() : nullptr;
+      uint8_t* plen = want_rows ? reinterpret_cast<uint8_t*>(pat + kRowDictMax * kEllMaxWidth) : nullptr;
+      uint8_t* rcode = want_rows ? plen + kRowDictMax : nullptr;
+      bool rok = false;
+      int npat = 0;
+      // stencil-like operators: pair and row tables from sampled rows, then one pass
+      // over the CSR writing only the row codes (no ELL pair codes are materialised)
+      if (want_rows && direct_on)
+        NNB_TRY(build_row_dict_direct(row_ptr, col, val, n, 0, dd, dv, &size, &width, &lo, &hi, rcode, pat, plen,
+                                      &npat, &rok, s));
+      if (rok) {
+        dict = PairDict{nullptr, dd, dv, size, width, 0, lo, hi, rcode, pat, plen, npat};
+      } else {
+        NNB_TRY(build_pair_dict(row_ptr, col, val, n, 0, nnz, code_buf, &width, &plane, &lo, &hi, dd, dv, &size,
+                                &ok, s));
+        if (ok) dict = PairDict{code_buf.as<uint8_t>(), dd, dv, size, width, plane, lo, hi};
+        // ELL codes with few distinct rows (stencils): one pattern code per row
+        if (ok && width && want_rows) {
+          NNB_TRY(build_row_dict(dict.code, width, plane, n, dd, dv, rcode, pat, plen, &npat, &rok, s));
+          if (rok) {
+            dict.rcode = rcode;
+            dict.rpat = pat;
+            dict.rlen = plen;
+            dict.npat = npat;
+          }
         }
       }
     }
     // int32 offsets, and int16 column deltas when the operator's band allows (the ELL
     // dictionary needs neither)
     bool fits = false;
-    if (!(dict.code && dict.ell_width)) NNB_TRY(compact_csr(row_ptr, col, n, 0, rp32, col16, &fits, s));
+    if (!(dict.code && dict.ell_width) && !dict.rcode) NNB_TRY(compact_csr(row_ptr, col, n, 0, rp32, col16, &fits, s));
     fits = fits && !force32;
-    set_sparse_bytes_per_nnz(dict.code ? 1 : (fits ? 10 : 12));
+    set_sparse_bytes_per_nnz(dict.code || dict.rcode ? 1 : (fits ? 10 : 12));
     set_sparse_format(dict.rcode ? "row-dictionary"
                       : dict.ell_width ? "pair-dictionary-ell"
                       : dict.code ? "pair-dictionary-csr"
