@@ -27,6 +27,8 @@ import threading
 import time
 from pathlib import Path
 
+_JSON_OUT = sys.stdout  # main() points this at a private duplicate of the original stdout
+
 import numpy as np
 
 ROOT = Path(__file__).resolve().parent
@@ -626,6 +628,13 @@ def cpu_sparse_sample(grid: int):
 
 # ------------------------------------------------------------------ main
 def main():
+    # stdout carries exactly the one JSON line: native libraries (NCCL prints its version
+    # line at communicator init) write to fd 1, so fd 1 becomes stderr for the run and
+    # the JSON goes to a private duplicate of the original stdout
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -675,7 +684,7 @@ def main():
                                                                        max(1, len(vals)), 1),
                     cpu_baseline=cb, e2e={"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                                           "d2h_bytes_per_step": 0})
-        print(json.dumps(line))
+        print(json.dumps(line), file=_JSON_OUT, flush=True)
         return
 
     import torch
@@ -710,7 +719,7 @@ def main():
         if "sparse" in legs:
             line["legs"]["sparse"]["cpu_baseline"] = cpu_sparse_sample(512)
     if rank == 0:
-        print(json.dumps(line))
+        print(json.dumps(line), file=_JSON_OUT, flush=True)
     if world > 1 or args.sharded:
         import torch.distributed as dist
 

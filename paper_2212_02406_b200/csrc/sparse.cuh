@@ -80,6 +80,14 @@ int build_row_dict(const uint8_t* code, int width, int64_t plane, int64_t rows, 
                    const double* dict_val, uint8_t* rcode, double2* pat, uint8_t* plen, int* npat, bool* ok,
                    cudaStream_t s);
 
+// Both tables from the first and last 65536 rows, then one verified pass over the
+// CSR writing only the row codes (operators above 4·65536 rows; *ok = false on any
+// miss, the caller then takes build_pair_dict + build_row_dict).
+int build_row_dict_direct(const int64_t* rp, const int32_t* col, const double* val, int64_t rows, int64_t row0,
+                          int32_t* dict_delta, double* dict_val, int* dict_size, int* width, int* band_lo,
+                          int* band_hi, uint8_t* rcode, double2* pat, uint8_t* plen, int* npat, bool* ok,
+                          cudaStream_t s);
+
 template <typename Idx>
 void spmv_apply(const SpmvOp<Idx>& op, int mode, int64_t r_begin, int64_t r_end, cudaStream_t s);
 

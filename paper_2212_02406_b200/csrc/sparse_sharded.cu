@@ -102,6 +102,28 @@ int setup_slab_dict(Slab& sl, const int64_t* rp_dev, const int32_t* col_dev, con
   bool ok = false;
   int size = 0, width = 0, lo = 0, hi = 0;
   int64_t plane = 0;
+  if (rowdict_on && sl.rows < INT32_MAX / 4) {  // stencil slabs: row codes straight from the CSR
+    NNB_TRY(sl.rowdict_mem.alloc(sizeof(double2) * kRowDictMax * kEllMaxWidth + kRowDictMax + sl.rows, s));
+    double2* pat = sl.rowdict_mem.as<double2>();
+    uint8_t* plen = reinterpret_cast<uint8_t*>(pat + kRowDictMax * kEllMaxWidth);
+    uint8_t* rcode = plen + kRowDictMax;
+    int npat = 0;
+    NNB_TRY(build_row_dict_direct(rp_dev, col_dev, val_dev, sl.rows, sl.row0, dd, dv, &size, &width, &lo, &hi, rcode,
+                                  pat, plen, &npat, &ok, s));
+    if (ok) {
+      sl.dict_delta = dd;
+      sl.dict_val = dv;
+      sl.dict_size = size;
+      sl.ell_width = width;
+      sl.band_lo = lo;
+      sl.band_hi = hi;
+      sl.rcode = rcode;
+      sl.rpat = pat;
+      sl.rlen = plen;
+      sl.npat = npat;
+      return 0;
+    }
+  }
   NNB_TRY(build_pair_dict(rp_dev, col_dev, val_dev, sl.rows, sl.row0, sl.nnz, sl.code_mem, &width, &plane, &lo, &hi,
                           dd, dv, &size, &ok, s));
   if (!ok) return 0;
@@ -114,7 +136,8 @@ int setup_slab_dict(Slab& sl, const int64_t* rp_dev, const int32_t* col_dev, con
   sl.band_lo = lo;
   sl.band_hi = hi;
   if (!width || !rowdict_on) return 0;
-  NNB_TRY(sl.rowdict_mem.alloc(sizeof(double2) * kRowDictMax * kEllMaxWidth + kRowDictMax + sl.rows, s));
+  if (!sl.rowdict_mem.p)
+    NNB_TRY(sl.rowdict_mem.alloc(sizeof(double2) * kRowDictMax * kEllMaxWidth + kRowDictMax + sl.rows, s));
   double2* pat = sl.rowdict_mem.as<double2>();
   uint8_t* plen = reinterpret_cast<uint8_t*>(pat + kRowDictMax * kEllMaxWidth);
   uint8_t* rcode = plen + kRowDictMax;
@@ -181,7 +204,7 @@ int setup_slab(Slab& sl, const int64_t* rp_dev, const int32_t* col_dev, const do
   }
   sl.val = val_dev + base;
   if (k == 1) NNB_TRY(setup_slab_dict(sl, rp_dev, col_dev, val_dev, s));
-  set_sparse_bytes_per_nnz(sl.code ? 1 : (sl.col16 ? 10 : 12));
+  set_sparse_bytes_per_nnz(sl.code || sl.rcode ? 1 : (sl.col16 ? 10 : 12));
   set_sparse_format(sl.rcode ? "row-dictionary"
                     : sl.ell_width ? "pair-dictionary-ell"
                     : sl.code ? "pair-dictionary-csr"
