@@ -53,7 +53,104 @@ static void* mm_rows(void* arg) {
   return NULL;
 }
 
+/* Real-data fast path.  When both operands have all-zero imaginary parts
+ * (every real chain: C1, C3, C4), std::complex's (a*b).re = a.re*b.re - (±0)
+ * is a.re*b.re exactly and every imaginary sum stays +0, so the reference's
+ * element C[i][j] = (((0 + a_i0 b_0j) + a_i1 b_1j) + ...) is reproduced by
+ * any loop nest that keeps each element's products rounded separately and
+ * added in ascending k.  This one holds a 4x16 block of C in vector
+ * registers across the whole k loop (mul and add as separate instructions:
+ * -ffp-contract=off), over a packed 16-column panel of B.  Pinned
+ * bit-for-bit against oracle/_ref like the general loop
+ * (tests/test_oracle_pins.py::test_matmul_real_fast_path). */
+typedef double v8d __attribute__((vector_size(64)));
+typedef struct {
+  const double *ar, *br; /* ar m x k, br k x n (real parts) */
+  double* cr;            /* m x n */
+  int64_t m, k, n, p0, p1; /* panel range [p0, p1) of 16-column panels; p == n/16 is the tail */
+} mmr_job;
+
+#define MMR_BODY                                                                         \
+  const mmr_job* j = (const mmr_job*)arg;                                                \
+  const int64_t m = j->m, k = j->k, n = j->n;                                            \
+  v8d* pan = (v8d*)aligned_alloc(64, sizeof(v8d) * 2 * (size_t)(k > 0 ? k : 1));         \
+  for (int64_t p = j->p0; p < j->p1; ++p) {                                              \
+    const int64_t c0 = p * 16;                                                           \
+    if (c0 + 16 <= n) {                                                                  \
+      for (int64_t kk = 0; kk < k; ++kk) memcpy(&pan[2 * kk], j->br + kk * n + c0, 128); \
+      int64_t i = 0;                                                                     \
+      for (; i + 4 <= m; i += 4) {                                                       \
+        v8d s00 = {0}, s01 = {0}, s10 = {0}, s11 = {0}, s20 = {0}, s21 = {0}, s30 = {0}, s31 = {0}; \
+        const double *a0 = j->ar + i * k, *a1 = a0 + k, *a2 = a1 + k, *a3 = a2 + k;      \
+        for (int64_t kk = 0; kk < k; ++kk) {                                             \
+          const v8d b0 = pan[2 * kk], b1 = pan[2 * kk + 1];                              \
+          v8d t;                                                                         \
+          t = a0[kk] * b0; s00 += t; t = a0[kk] * b1; s01 += t;                         \
+          t = a1[kk] * b0; s10 += t; t = a1[kk] * b1; s11 += t;                         \
+          t = a2[kk] * b0; s20 += t; t = a2[kk] * b1; s21 += t;                         \
+          t = a3[kk] * b0; s30 += t; t = a3[kk] * b1; s31 += t;                         \
+        }                                                                                \
+        memcpy(j->cr + (i + 0) * n + c0, &s00, 64); memcpy(j->cr + (i + 0) * n + c0 + 8, &s01, 64); \
+        memcpy(j->cr + (i + 1) * n + c0, &s10, 64); memcpy(j->cr + (i + 1) * n + c0 + 8, &s11, 64); \
+        memcpy(j->cr + (i + 2) * n + c0, &s20, 64); memcpy(j->cr + (i + 2) * n + c0 + 8, &s21, 64); \
+        memcpy(j->cr + (i + 3) * n + c0, &s30, 64); memcpy(j->cr + (i + 3) * n + c0 + 8, &s31, 64); \
+      }                                                                                  \
+      for (; i < m; ++i) {                                                               \
+        v8d s0 = {0}, s1 = {0};                                                          \
+        const double* a0 = j->ar + i * k;                                                \
+        for (int64_t kk = 0; kk < k; ++kk) {                                             \
+          v8d t = a0[kk] * pan[2 * kk]; s0 += t; t = a0[kk] * pan[2 * kk + 1]; s1 += t;  \
+        }                                                                                \
+        memcpy(j->cr + i * n + c0, &s0, 64); memcpy(j->cr + i * n + c0 + 8, &s1, 64);    \
+      }                                                                                  \
+    } else {                                                                             \
+      for (int64_t i = 0; i < m; ++i)                                                    \
+        for (int64_t col = c0; col < n; ++col) {                                         \
+          double s = 0.0;                                                                \
+          for (int64_t kk = 0; kk < k; ++kk) { const double t = j->ar[i * k + kk] * j->br[kk * n + col]; s += t; } \
+          j->cr[i * n + col] = s;                                                        \
+        }                                                                                \
+    }                                                                                    \
+  }                                                                                      \
+  free(pan);                                                                             \
+  return NULL;
+
+__attribute__((target("avx512f"))) static void* mmr_panels_avx512(void* arg) { MMR_BODY }
+static void* mmr_panels_generic(void* arg) { MMR_BODY }
+
+static int imag_all_zero(const double* p, int64_t count) {
+  for (int64_t i = 0; i < count; ++i)
+    if (p[2 * i + 1] != 0.0) return 0;
+  return 1;
+}
+
+static void matmul_real(const double* a, const double* b, int64_t m, int64_t k, int64_t n, double* c) {
+  double* ar = (double*)malloc(sizeof(double) * (size_t)(m * k + 1));
+  double* br = (double*)malloc(sizeof(double) * (size_t)(k * n + 1));
+  double* cr = (double*)malloc(sizeof(double) * (size_t)(m * n + 1));
+  for (int64_t i = 0; i < m * k; ++i) ar[i] = a[2 * i];
+  for (int64_t i = 0; i < k * n; ++i) br[i] = b[2 * i];
+  void* (*fn)(void*) = __builtin_cpu_supports("avx512f") ? mmr_panels_avx512 : mmr_panels_generic;
+  const int64_t panels = (n + 15) / 16;
+  int workers = g_threads < panels ? g_threads : (int)panels;
+  if (workers < 1) workers = 1;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * workers);
+  mmr_job* jobs = (mmr_job*)malloc(sizeof(mmr_job) * workers);
+  for (int w = 0; w < workers; ++w) {
+    jobs[w] = (mmr_job){ar, br, cr, m, k, n, panels * w / workers, panels * (w + 1) / workers};
+    if (workers > 1) pthread_create(&th[w], NULL, fn, &jobs[w]);
+  }
+  if (workers > 1) for (int w = 0; w < workers; ++w) pthread_join(th[w], NULL);
+  else fn(&jobs[0]);
+  for (int64_t i = 0; i < m * n; ++i) { c[2 * i] = cr[i]; c[2 * i + 1] = 0.0; }
+  free(th); free(jobs); free(ar); free(br); free(cr);
+}
+
 int nno_matmul_z(const double* a, const double* b, int64_t m, int64_t k, int64_t n, double* c) {
+  if (m * n >= 4096 && imag_all_zero(a, m * k) && imag_all_zero(b, k * n)) {
+    matmul_real(a, b, m, k, n, c);
+    return all_finite(c, 2 * m * n) ? 0 : 2;
+  }
   int workers = g_threads;
   if (workers <= 1 || m < 64) {
     mm_job j = {(const cplx*)a, (const cplx*)b, (cplx*)c, k, n, 0, m};

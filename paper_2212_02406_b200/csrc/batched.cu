@@ -24,6 +24,7 @@
 //   P = I − X·A;  V = X + P·X;  V = X + P·V (p−1 more);  X = V,
 // and the Neumann-series baseline follows ns_sum (proj/src/solver.cpp:77-91):
 //   P = I − X0·A;  T = I + P;  T = T·P + I (order−1 times);  X = T·X0.
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 
@@ -261,8 +262,10 @@ __device__ __forceinline__ void gram_epilogue(const ZAcc<true>& acc, double sigm
 }
 
 // 3M with seeded accumulators: out = s·acc (s = −1 when NEG), stored to shared `out`.
+// Returns this lane's Σ|out|² (dead code unless the caller uses it).
 template <bool NEG>
-__device__ __forceinline__ void epilogue_seeded(const ZAcc<true>& acc, const SMat& out, int g, int t) {
+__device__ __forceinline__ double epilogue_seeded(const ZAcc<true>& acc, const SMat& out, int g, int t) {
+  double ss = 0.0;
   __syncwarp();  // every lane finished reading operands that `out` may overwrite
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
@@ -282,8 +285,10 @@ __device__ __forceinline__ void epilogue_seeded(const ZAcc<true>& acc, const SMa
       }
       *reinterpret_cast<double2*>(out.re + idx) = vr;
       *reinterpret_cast<double2*>(out.im + idx) = vi;
+      ss += vr.x * vr.x + vr.y * vr.y + vi.x * vi.x + vi.y * vi.y;
     }
   __syncwarp();
+  return ss;
 }
 
 // epilogue_seeded<false> for a Hermitian result from zmma_ss_herm: tiles (0,0),
@@ -512,12 +517,21 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
       // Hermitian A (and so X0): the Horner products compute three of four tiles
       bool herm = false;
       if (iters > 0) first_nest_diag<P, M3>(acc, X, Pm, V, areg, g, t, M3 && herm_ok, &herm);
+      double eps_prev = INFINITY;
       for (int it = 1; it < iters; ++it) {
         const SMat* v = &X;
         if constexpr (M3) {
           acc.template seed<true>(nullptr, 1.0, g, t);  // −I
           zmma_sr(acc, X, areg, g, t);                  // −I + X·A
-          epilogue_seeded<true>(acc, Pm, g, t);         // P = I − X·A
+          const double pss = epilogue_seeded<true>(acc, Pm, g, t);  // P = I − X·A
+          if (herm) {
+            // Mirrored Horner products leave a κ·u residual floor (the dense chain's
+            // NNB_ORDER_SYMMETRIC measured it): as there, full products from the first
+            // nest whose ε = ‖P‖_F/√n is below 1e-4 or no longer falling (sticky)
+            const double eps = sqrt(warp_sum(pss)) * 0.25;
+            herm = eps >= 1e-4 && eps < eps_prev;
+            eps_prev = eps;
+          }
 #pragma unroll
           for (int j = 1; j <= P; ++j) {
             horner_step(acc, X, Pm, *v, (j == P) ? X : V, herm, g, t);  // X + P·V; the last lands in X
@@ -677,12 +691,18 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
     __syncwarp();
     // ---- Nested Neumann inversion (seeded 3M products, nest 0 from the diagonal X0) ----
     // A = HᴴH + σ²I is Hermitian by construction (gram_epilogue mirrors it)
-    const bool herm = herm_ok != 0;
+    bool herm = herm_ok != 0;
     if (iters > 0) first_nest_diag<P, true>(acc, X, Pm, V, areg, g, t, herm, nullptr);
+    double eps_prev = INFINITY;
     for (int it = 1; it < iters; ++it) {
       acc.template seed<true>(nullptr, 1.0, g, t);
       zmma_sr(acc, X, areg, g, t);
-      epilogue_seeded<true>(acc, Pm, g, t);  // P = I − X·A
+      const double pss = epilogue_seeded<true>(acc, Pm, g, t);  // P = I − X·A
+      if (herm) {  // the batched kernel's cutover: full products once ε < 1e-4 or not falling
+        const double eps = sqrt(warp_sum(pss)) * 0.25;
+        herm = eps >= 1e-4 && eps < eps_prev;
+        eps_prev = eps;
+      }
       const SMat* v = &X;
 #pragma unroll
       for (int j = 1; j <= P; ++j) {
@@ -729,7 +749,7 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
 
 // NNB_BATCHED_HERM=0: full products for Hermitian systems too (A/B measurement)
 int herm_enabled() {
-  static const int on = !(std::getenv("NNB_BATCHED_HERM") && std::strcmp(std::getenv("NNB_BATCHED_HERM"), "0") == 0);
+  static const int on = !(debug_env("NNB_BATCHED_HERM") && std::strcmp(debug_env("NNB_BATCHED_HERM"), "0") == 0);
   return on;
 }
 
@@ -760,7 +780,7 @@ int launch_variant(const double2* a, int64_t batch, int iters, int ns_order, dou
 template <int P>
 int launch_p(const double2* a, int64_t batch, int iters, int ns_order, double2* x, double* eps, int ns_mode,
              cudaStream_t s) {
-  static const char* env = std::getenv("NNB_BATCHED_VARIANT");
+  static const char* env = debug_env("NNB_BATCHED_VARIANT");
   const bool m4 = env && env[0] == '4';
   const bool nopf = !env || std::strstr(env, "nopf");
   if (m4) {

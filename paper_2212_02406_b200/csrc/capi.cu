@@ -165,7 +165,7 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
                      const ChainCfg& c, double* X_out, double* eps_hist, nnb_chain_result* result,
                      cudaStream_t s) {
   static const int chunks = [] {
-    const char* e = std::getenv("NNB_STREAM_CHUNKS");
+    const char* e = debug_env("NNB_STREAM_CHUNKS");
     return std::min(64, std::max(1, e ? std::atoi(e) : 8));
   }();
   const bool host_a = !is_device_ptr(A), host_out = X_out && !is_device_ptr(X_out);
@@ -223,6 +223,9 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
   const int st = chain_real(a.d, n, a.ld, x.d, c, eps_hist, &o, s, &io);
   fill_result(result, o);
   if (st != 0 && st != NNB_ERR_DIVERGENCE && st != NNB_ERR_DOMAIN) return st;
+  // with zero products (max_iters = 0, no final residual) nothing on s has waited
+  // for X0's copy yet; the store must not read x ahead of it
+  NNB_CUDA(cudaStreamWaitEvent(s, in_done, 0));
   if (X_out && !io.out_streamed) NNB_TRY(x.store(X_out, n, s));
   NNB_TRY(sync(s));
   NNB_CUDA(cudaStreamSynchronize(lane.cs));

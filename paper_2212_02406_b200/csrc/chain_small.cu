@@ -375,12 +375,7 @@ size_t smem_bytes(int n) {
 template <int TM>
 int launch(const SmallMaps& maps, SmallArgs& a, cudaStream_t s) {
   const size_t smem = smem_bytes<TM>(a.n);
-  static size_t attr = 0;  // per instantiation
-  if (smem > attr) {
-    NNB_CUDA(cudaFuncSetAttribute(small_chain_kernel<TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    attr = smem;
-  }
+  NNB_TRY(ensure_smem<small_chain_kernel<TM>>(static_cast<int>(smem)));
   int per_sm = 0, dev = 0, sms = 0;
   NNB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_chain_kernel<TM>, kThreads, smem));
   NNB_CUDA(cudaGetDevice(&dev));
@@ -398,7 +393,7 @@ int launch(const SmallMaps& maps, SmallArgs& a, cudaStream_t s) {
 }  // namespace
 
 int small_chain_max_n() {
-  static const int v = std::getenv("NNB_SMALL_CHAIN_MAX") ? std::atoi(std::getenv("NNB_SMALL_CHAIN_MAX")) : 384;
+  static const int v = debug_env("NNB_SMALL_CHAIN_MAX") ? std::atoi(debug_env("NNB_SMALL_CHAIN_MAX")) : 384;
   return v;
 }
 
@@ -409,7 +404,7 @@ bool small_chain_eligible(int64_t n, int64_t ld, const ChainCfg& cfg) {
 }
 
 static int small_tm(int64_t n) {
-  static const char* force = std::getenv("NNB_SMALL_TM");
+  static const char* force = debug_env("NNB_SMALL_TM");
   const bool fits32 = smem_bytes<32>(static_cast<int>(n)) <= 227 * 1024;
   if (force) return std::atoi(force) == 32 && fits32 ? 32 : 16;
   const int64_t t32 = ((n + 31) / 32) * ((n + 15) / 16);

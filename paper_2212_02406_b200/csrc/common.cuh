@@ -9,7 +9,22 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 namespace nnb {
+
+// A/B measurement knobs (NNB_GEMM_CFG, NNB_SPARSE_*, NNB_SMALL_CHAIN_MAX, ...).
+// The product path reads no environment variable unless NNB_DEBUG=1 is set, so
+// a stray variable cannot change the benchmarked path; with NNB_DEBUG=1 the
+// named variable overrides the built-in choice.  (NNB_ARITHMETIC is not a
+// knob: it is the documented switch of nnb_set_arithmetic.)
+inline const char* debug_env(const char* name) {
+  static const bool on = [] {
+    const char* e = std::getenv("NNB_DEBUG");
+    return e && e[0] == '1';
+  }();
+  return on ? std::getenv(name) : nullptr;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

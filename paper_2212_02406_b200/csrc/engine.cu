@@ -187,19 +187,19 @@ using NanoCfg = GemmCfg<16, 16, 16, 2, 2, 4>;  // smaller still: config 0 (N=256
 
 // The 16×16 tiles when even 32×32 ones leave most SMs idle.
 static bool use_nano(int64_t M, int64_t N) {
-  static const char* force = std::getenv("NNB_GEMM_CFG");
+  static const char* force = debug_env("NNB_GEMM_CFG");
   if (force) return force[0] == 'n';
   return ((M + 31) / 32) * ((N + 31) / 32) < 148;
 }
 
 static bool use_tiny(int64_t M, int64_t N) {
-  static const char* force = std::getenv("NNB_GEMM_CFG");
+  static const char* force = debug_env("NNB_GEMM_CFG");
   if (force) return force[0] == 't';
   return ((M + 63) / 64) * ((N + 63) / 64) < 148;
 }
 
 static bool use_big(int64_t M, int64_t N) {
-  static const char* force = std::getenv("NNB_GEMM_CFG");  // debug override: "big" / "small"
+  static const char* force = debug_env("NNB_GEMM_CFG");  // debug override: "big" / "small"
   if (force && force[0] == 'b') return true;
   if (force && force[0] == 's') return false;
   const int64_t big_tiles = ((M + 127) / 128) * ((N + 127) / 128);
@@ -207,7 +207,7 @@ static bool use_big(int64_t M, int64_t N) {
 }
 
 static int smem_pad() {
-  static const int pad = std::getenv("NNB_GEMM_SMEM_PAD") ? std::atoi(std::getenv("NNB_GEMM_SMEM_PAD")) : 0;
+  static const int pad = debug_env("NNB_GEMM_SMEM_PAD") ? std::atoi(debug_env("NNB_GEMM_SMEM_PAD")) : 0;
   return pad;
 }
 
@@ -224,12 +224,7 @@ static int launch_cfg(const GemmOp& op, cudaStream_t s) {
   else
     NNB_TRY(make_tmap(&tb, op.B, op.K, op.N, op.ldb, Cfg::kBK, Cfg::kBN, false));
   const int smem = Cfg::kSmemBytes + smem_pad();
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    NNB_CUDA(cudaFuncSetAttribute(gemm_f64_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  smem));
-    attr_set = true;
-  }
+  NNB_TRY(ensure_smem<gemm_f64_kernel<Cfg>>(smem));
   const int64_t tm = (op.M + Cfg::kBM - 1) / Cfg::kBM;
   const int64_t tiles = op.ep.sym ? tm * (tm + 1) / 2 : tm * ((op.N + Cfg::kBN - 1) / Cfg::kBN);
   gemm_f64_kernel<Cfg><<<static_cast<unsigned>(tiles), Cfg::kThreads, smem, s>>>(

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <string>
 
@@ -28,6 +29,23 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
   } while (0)
 
 int fail(int code, const std::string& msg);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-device setting:
+// remember, per kernel and device, the largest size already set (thread-safe),
+// so a second GPU driven from the same process gets its own call.
+template <auto Kernel>
+int ensure_smem(int bytes) {
+  static std::atomic<int> done[64] = {};
+  int dev = 0;
+  NNB_CUDA(cudaGetDevice(&dev));
+  std::atomic<int>& d = done[dev & 63];
+  int cur = d.load(std::memory_order_acquire);
+  if (cur >= bytes) return 0;
+  NNB_CUDA(cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  while (cur < bytes && !d.compare_exchange_weak(cur, bytes, std::memory_order_acq_rel)) {
+  }
+  return 0;
+}
 void count_launch(uint64_t n = 1);
 uint64_t launches();
 

@@ -207,8 +207,7 @@ int householder_q_dev(T* a, int64_t n, T* q, T* vmat, double* betas, cudaStream_
   constexpr int64_t kMaxStaged = 220 * 1024 / sizeof(double);  // the column fits one SM's shared memory
   const bool staged = !CPLX && n <= kMaxStaged;
   if (staged && n * (int64_t)sizeof(double) > 48 * 1024)
-    NNB_CUDA(cudaFuncSetAttribute(reflector_d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(n * sizeof(double))));
+    NNB_TRY(ensure_smem<reflector_d_kernel>((int)(n * sizeof(double))));
   for (int64_t k = 0; k + 1 < n; ++k) {
     T* v = vmat + k * n;
     if constexpr (CPLX) {

@@ -362,8 +362,12 @@ __global__ void dict_index_kernel(DictWs* ws, int32_t* __restrict__ dict_delta, 
     const int slot = threadIdx.x * per + i;
     if (ws->hash[slot] == 0) continue;
     ws->index[slot] = idx;
-    dict_delta[idx] = ws->delta[slot];
-    dict_val[idx] = ws->val[slot];
+    // on overflow up to kDictSlots slots can be occupied; the dictionary arrays
+    // hold kPairDictMax entries (the overflowed build is discarded by the host)
+    if (idx < kPairDictMax) {
+      dict_delta[idx] = ws->delta[slot];
+      dict_val[idx] = ws->val[slot];
+    }
     ++idx;
   }
 }
@@ -679,7 +683,7 @@ void launch_rows_v(const SpmvOp<Idx>& op, const C* col, int64_t r_begin, int64_t
 
 template <typename Idx, typename C, int MODE>
 void launch_rows(const SpmvOp<Idx>& op, const C* col, int64_t r_begin, int64_t r_end, cudaStream_t s) {
-  static const bool k1_off = std::getenv("NNB_SPMV_K1") && std::strcmp(std::getenv("NNB_SPMV_K1"), "0") == 0;
+  static const bool k1_off = debug_env("NNB_SPMV_K1") && std::strcmp(debug_env("NNB_SPMV_K1"), "0") == 0;
   if (!k1_off && k1_ok(op, r_end)) launch_rows_v<Idx, C, MODE, true>(op, col, r_begin, r_end, s);
   else launch_rows_v<Idx, C, MODE, false>(op, col, r_begin, r_end, s);
 }
@@ -741,11 +745,12 @@ void launch_rowdict_v(const SpmvOp<int32_t>& op, int64_t r_begin, int64_t r_end,
   const int smem = op.npat * op.ell_width * (int)sizeof(double2) + op.npat * (int)sizeof(int);
   static unsigned resident = 0;
   static int resident_smem = -1;
+  ensure_smem<spmv_rowdict_kernel<MODE, WMAX>>(smem);  // per device
   if (resident_smem != smem) {
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(spmv_rowdict_kernel<MODE, WMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, spmv_rowdict_kernel<MODE, WMAX>, NNB_SPMV_THREADS, smem);
     resident = static_cast<unsigned>(sms * std::max(1, per));
     resident_smem = smem;
@@ -855,7 +860,7 @@ int build_pair_dict(const int64_t* rp, const int32_t* col, const double* val, in
   DevBuf wsb;
   NNB_TRY(wsb.alloc(sizeof(DictWs), s));
   DictWs* ws = wsb.as<DictWs>();
-  static const bool ell_on = !(std::getenv("NNB_DICT_ELL") && std::strcmp(std::getenv("NNB_DICT_ELL"), "0") == 0);
+  static const bool ell_on = !(debug_env("NNB_DICT_ELL") && std::strcmp(debug_env("NNB_DICT_ELL"), "0") == 0);
   // First try a dictionary (and ELL width) from the first and last kSample rows only:
   // structured operators show every pair there (a stencil's boundary rows recur every
   // grid row).  The encode pass verifies every nonzero against it; a missing pair or a
@@ -1100,7 +1105,7 @@ int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* 
                          (narrow ? sizeof(int32_t) * (n + 1) + sizeof(int16_t) * nnz + 32 : 0),
                      s));
   static const bool dict_on = [] {  // NNB_SPARSE_DICT=0: keep the column format (A/B measurement)
-    const char* e = std::getenv("NNB_SPARSE_DICT");
+    const char* e = debug_env("NNB_SPARSE_DICT");
     return !(e && std::strcmp(e, "0") == 0);
   }();
   double* z[2] = {work.as<double>(), work.as<double>() + vec};
@@ -1111,7 +1116,7 @@ int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* 
     int32_t* rp32 = flags + 64;
     int16_t* col16 = reinterpret_cast<int16_t*>(rp32 + n + 2);
     static const bool force32 = [] {  // NNB_SPARSE_COL=32: int32 columns (A/B measurement)
-      const char* e = std::getenv("NNB_SPARSE_COL");
+      const char* e = debug_env("NNB_SPARSE_COL");
       return e && std::strcmp(e, "32") == 0;
     }();
     // operators with <= 255 distinct (column − row, value) pairs: 1 byte per nonzero
@@ -1125,11 +1130,11 @@ int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* 
       int size = 0, width = 0, lo = 0, hi = 0;
       int64_t plane = 0;
       static const bool rowdict_on = [] {  // NNB_SPARSE_ROWDICT=0: keep the ELL pair codes (A/B measurement)
-        const char* e = std::getenv("NNB_SPARSE_ROWDICT");
+        const char* e = debug_env("NNB_SPARSE_ROWDICT");
         return !(e && std::strcmp(e, "0") == 0);
       }();
       static const bool direct_on = [] {  // NNB_SPARSE_DIRECT=0: the two-pass row-dictionary build (A/B)
-        const char* e = std::getenv("NNB_SPARSE_DIRECT");
+        const char* e = debug_env("NNB_SPARSE_DIRECT");
         return !(e && std::strcmp(e, "0") == 0);
       }();
       const bool want_rows = k == 1 && rowdict_on && n < INT32_MAX / 2;

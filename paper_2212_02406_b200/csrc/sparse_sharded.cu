@@ -92,9 +92,9 @@ struct Slab {
 // build_row_dict): the gathers stay r + diag_off + delta into the extended vector.
 int setup_slab_dict(Slab& sl, const int64_t* rp_dev, const int32_t* col_dev, const double* val_dev,
                     cudaStream_t s) {
-  static const bool dict_on = !(std::getenv("NNB_SPARSE_DICT") && std::strcmp(std::getenv("NNB_SPARSE_DICT"), "0") == 0);
+  static const bool dict_on = !(debug_env("NNB_SPARSE_DICT") && std::strcmp(debug_env("NNB_SPARSE_DICT"), "0") == 0);
   static const bool rowdict_on =
-      !(std::getenv("NNB_SPARSE_ROWDICT") && std::strcmp(std::getenv("NNB_SPARSE_ROWDICT"), "0") == 0);
+      !(debug_env("NNB_SPARSE_ROWDICT") && std::strcmp(debug_env("NNB_SPARSE_ROWDICT"), "0") == 0);
   if (!dict_on || sl.rows == 0) return 0;
   NNB_TRY(sl.dict_mem.alloc((sizeof(int32_t) + sizeof(double)) * kPairDictMax, s));
   double* dv = sl.dict_mem.as<double>();

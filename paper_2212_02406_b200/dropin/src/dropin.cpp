@@ -668,8 +668,11 @@ std::pair<DenseMatrix, ConvergenceReport> nn_invert(const DenseMatrix& w, const 
   if (config.record_history)
     for (std::size_t k = 0; k <= nests; ++k) report.history.emplace_back(k, hist[k]);
   report.stopped_reason = res.stopped == 0 ? StopReason::Tolerance : StopReason::MaxNests;
-  const double n3 = static_cast<double>(nests * (config.depth_L + 1));
-  const std::int64_t n2 = static_cast<std::int64_t>(nests * (config.depth_L + 1));
+  // nn_step with depth_L = 0 returns phi untouched: no products, no elementwise ops
+  // (proj/src/solver.cpp:97)
+  const std::size_t per_nest = config.depth_L > 0 ? config.depth_L + 1 : 0;
+  const double n3 = static_cast<double>(nests * per_nest);
+  const std::int64_t n2 = static_cast<std::int64_t>(nests * per_nest);
   if (counter) {
     add_products(counter, n3);
     counter->add_n2(n2);

@@ -316,6 +316,17 @@ static void device_tests() {
         CHECK(cnt.n3_multiplies() == static_cast<double>(nests * (depth + 1)));
         CHECK(r.history.size() == nests + 1);
       }
+    {  // depth_L = 0: nn_step is the identity (proj/src/solver.cpp:97), so no products are tallied
+      SolverConfig c0;
+      c0.depth_L = 0;
+      c0.max_nests = 3;
+      c0.tol = 1e-15;
+      OpCounter cnt;
+      const auto [x0, r0] = nn_invert(w16, nm, c0, &cnt);
+      CHECK(r0.n3_multiplies == 0.0 && r0.n2_ops == 0);
+      CHECK(cnt.n3_multiplies() == 0.0);
+      CHECK(r0.history.size() == 4);
+    }
     // deeper nests converge in fewer iterations; history strictly decreasing above 1e-12
     SolverConfig c;
     c.tol = 1e-10;

@@ -302,6 +302,25 @@ def test_batched_mixed_hermitian_and_general(ref):
     eps_close(eps, er)
 
 
+def test_batched_ill_conditioned_hermitian_reaches_reference_floor(ref):
+    """kappa = 1e4 Hermitian systems (one small eigenvalue; Jacobi still contracts):
+    mirrored Horner products would stall at a kappa*u residual floor, so the kernel
+    switches to full products once eps < 1e-4 (or stops falling), like the dense
+    NNB_ORDER_SYMMETRIC chain.  14 nests of p=2 must reach the reference's floor."""
+    rng = np.random.default_rng(44)
+    a = np.empty((40, 16, 16), np.complex128)
+    for s in range(40):
+        q, _ = np.linalg.qr(rng.standard_normal((16, 16)) + 1j * rng.standard_normal((16, 16)))
+        lam = np.ones(16)
+        lam[0] = 10.0 ** -(3 + (s % 3))  # kappa 1e3 .. 1e5
+        m = (q * lam) @ q.conj().T
+        a[s] = 0.5 * (m + m.conj().T)  # exactly Hermitian
+    x, eps = nnb.nn_batched(a, p=2, iters=14)
+    xr, er, _ = ref.batched("nn", a, 2, 14, threads=8)
+    assert np.all(eps <= 4.0 * er + 1e-14), np.c_[eps, er]
+    assert max(rel_frob(x[s], xr[s]) for s in range(40)) < TOL_X
+
+
 def test_batched_ns_orders(ref):
     a = W.mimo_gram_host(64, seed=11)
     for order in (0, 1, 2, 26):

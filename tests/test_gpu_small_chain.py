@@ -51,7 +51,7 @@ print(json.dumps(out))
 def _run(tmp, small_max):
     sub = os.path.join(tmp, str(small_max))
     os.makedirs(sub, exist_ok=True)
-    env = dict(os.environ, NNB_SMALL_CHAIN_MAX=str(small_max))
+    env = dict(os.environ, NNB_DEBUG="1", NNB_SMALL_CHAIN_MAX=str(small_max))
     code = CHILD % dict(root=ROOT, cases=CASES, tmp=sub)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]

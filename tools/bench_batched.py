@@ -1,4 +1,4 @@
-"""A/B timing of the batched 16x16 complex kernel variants (NNB_BATCHED_VARIANT set by the caller)."""
+"""A/B timing of the batched 16x16 complex kernel variants (NNB_DEBUG=1 NNB_BATCHED_VARIANT=... set by the caller)."""
 import os, sys
 sys.path.insert(0, ".")
 import torch

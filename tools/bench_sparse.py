@@ -1,5 +1,5 @@
 """A/B timing of the factorized sparse solve (C5, 4096^2 Laplacian, gamma=63) through the one-shot API.
-NNB_SPARSE_COL=32 forces int32 columns (A/B against the default int16 deltas)."""
+NNB_DEBUG=1 NNB_SPARSE_COL=32 forces int32 columns (A/B against the default int16 deltas)."""
 import os, sys, hashlib
 sys.path.insert(0, ".")
 import torch
