@@ -315,8 +315,10 @@ def run_dense_symmetric(nnb, torch, a, n, p, args):
 
 
 def cpu_dense_sample(n_sample: int, p: int):
-    """Reference nn_step + residual_epsilon (one nest, p+2 products incl. the residual it
-    spends) on an N=n_sample matrix, all host threads (NN_WORKERS=nproc)."""
+    """One reference product (nn::matmul, the routine every NN nest is made of:
+    proj/src/kernels.cpp:137-162) on an N=n_sample slice of the config's matrices,
+    all host threads (NN_WORKERS=nproc).  The rate is the reference's per-product
+    FP64 rate; the N=32768 nest (p+1 products of 2N^3 flop) is extrapolated from it."""
     from oracle import Reference
 
     from paper_2212_02406_b200 import workloads as W
@@ -327,11 +329,14 @@ def cpu_dense_sample(n_sample: int, p: int):
     a = W.gram_shifted(n_sample, seed=1, shift=1.0)
     x0 = W.x0_transpose_norm(a)
     ref.matmul(a[:64], a[:, :64])  # warm the worker pool
-    _, _, _, secs = ref.chain(a, x0, p, 1)  # residual + (p+1) products + final residual
-    flops = (p + 3) * 2.0 * n_sample ** 3
+    t0 = time.perf_counter()
+    ref.matmul(a, x0)
+    secs = time.perf_counter() - t0
+    flops = 2.0 * n_sample ** 3
     return {"value": round(flops / secs / 1e12, 6), "unit": "TFLOP/s", "cores": cores, "kind": "reference",
-            "sample": f"reference §8(c) loop, 1 nest p={p} + 2 residuals on N={n_sample} "
-                      f"({p + 3} complex<double> products, {secs:.2f} s)"}
+            "n_sample": n_sample, "extrapolated": True,
+            "sample": f"one reference nn::matmul (complex<double>, real data) at N={n_sample}: {secs:.2f} s; "
+                      f"the N=32768 nest (p={p}: {p + 1} products) is extrapolated at this per-product rate"}
 
 
 # ------------------------------------------------------------------ configs 0 and 2 (small / mid dense)
@@ -565,8 +570,11 @@ def run_sparse(args, world, rank):
         r0, rows = nnb.partition_rows(n, world, rank)
         csr = nnb.Csr(dev(rp[r0:r0 + rows + 1].copy()), dev(col), dev(val), n=rows, nnz=col.size)
         b = dev(b_full[r0:r0 + rows].copy())
-        plan = nnb.SparseShardedPlan(comm, csr, n, k=1, stream_like=b)  # slab setup once, outside the timing
-        solve = lambda: plan.solve(b, 63, norm)
+        # one-shot sharded solve: the slab's format pass runs inside every step, as the
+        # single-GPU solve's does, so every N times the same per-solve work
+        solve = lambda: nnb.solve_sparse_factorized_sharded(comm, csr, n, b, 63, norm)
+        plan = nnb.SparseShardedPlan(comm, csr, n, k=1, stream_like=b)  # planned solve, reported beside it
+        plan_solve = lambda: plan.solve(b, 63, norm)
     else:
         csr = nnb.Csr(dev(rp), dev(col), dev(val), n=n, nnz=col.size)
         b = dev(b_full)
@@ -582,7 +590,17 @@ def run_sparse(args, world, rank):
     e1.record()
     torch.cuda.synchronize()
     ms = max_over_ranks(world, e0.elapsed_time(e1)) / steps
+    planned_ms = None
     if sharded:
+        for _ in range(2):
+            plan_solve()
+        barrier(world)
+        e0.record()
+        for _ in range(steps):
+            plan_solve()
+        e1.record()
+        torch.cuda.synchronize()
+        planned_ms = max_over_ranks(world, e0.elapsed_time(e1)) / steps
         plan.close()
         comm.close()
     # the format the device consumed (csrc/sparse.cu): 1 = pair dictionary, 10 = f64 + int16 delta, 12
@@ -600,14 +618,14 @@ def run_sparse(args, world, rank):
     return {"metric": "sparse factorized solve, 4096^2 5-pt Laplacian+I, gamma=63 (GB/s of SURVEY 8(d) algorithmic "
                       "bytes: 12 B per nonzero)", "value": round(gbs, 1),
             "unit": "GB/s", "ms_per_step": round(ms, 3), "format": fname, "format_bytes_per_nnz": fb,
+            "planned_ms_per_step": None if planned_ms is None else round(planned_ms, 3),
             "parallelism": f"row slabs x{world}, NCCL halo exchange" if sharded else "single GPU",
             "roofline": {"bound": "hbm", "achieved": round(moved_gbs, 1), "peak": HBM_PEAK * world, "unit": "GB/s",
                          "frac": round(moved_gbs / (HBM_PEAK * world), 4),
                          "traffic": ncu_traffic("sparse_application") if grid == 4096 and not sharded else None,
                          "traffic_unit": "bytes per application (63 per solve)",
                          "per_launch": f"{mat:.0f} operator bytes + 2N*8 per application (x63, whole solve timed "
-                                       + ("excl. the slab plan's one-time format pass" if sharded else
-                                          "incl. the per-solve format pass") + f"): {fmt}; t in + t out"}}
+                                       + "incl. the per-solve format pass" + f"): {fmt}; t in + t out"}}
 
 
 def cpu_sparse_sample(grid: int):
@@ -626,12 +644,41 @@ def cpu_sparse_sample(grid: int):
             "sample": f"reference solve_sparse_factorized gamma=63 on a {grid}^2 grid ({secs:.2f} s)"}
 
 
+# ------------------------------------------------------------------ launcher
+def relaunch_under_torchrun(argv, gpus: int) -> int:
+    """`bench.py --gpus N` without a torchrun environment: start N ranks (one per GPU)
+    through torch.distributed.run on 127.0.0.1 and return its exit status.  Refuses
+    loudly when the node has fewer than N GPUs instead of running fewer ranks."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < gpus:
+        print(f"bench.py: --gpus {gpus} requested but this node has {have} CUDA device(s); "
+              "refusing to run fewer ranks than requested", file=sys.stderr, flush=True)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *argv]
+    return subprocess.run(cmd).returncode
+
+
 # ------------------------------------------------------------------ main
 def main():
     # stdout carries exactly the one JSON line: native libraries (NCCL prints its version
     # line at communicator init) write to fd 1, so fd 1 becomes stderr for the run and
     # the JSON goes to a private duplicate of the original stdout
     global _JSON_OUT
+    pre = argparse.ArgumentParser(add_help=False)
+    pre.add_argument("--gpus", type=int, default=1)
+    pre.add_argument("--impl", default="ours")
+    pre.add_argument("--sharded", action="store_true")
+    known, _ = pre.parse_known_args()
+    if "WORLD_SIZE" not in os.environ and known.impl == "ours" and (known.gpus > 1 or known.sharded):
+        sys.exit(relaunch_under_torchrun(sys.argv[1:], known.gpus))
     sys.stdout.flush()
     _JSON_OUT = os.fdopen(os.dup(1), "w")
     os.dup2(2, 1)
@@ -655,6 +702,10 @@ def main():
     legs = set(args.legs.split(","))
     world, rank, local = dist_setup(args.sharded) if args.impl == "ours" else (int(os.environ.get("WORLD_SIZE", "1")),
                                                                    int(os.environ.get("RANK", "0")), 0)
+    if args.impl == "ours" and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch with --nproc-per-node {args.gpus}",
+              file=sys.stderr, flush=True)
+        sys.exit(2)
     cores, model = cpu_info()
     config = {"workload": f"BASELINE config 3: dense NN inversion N={args.n}, p={args.p}, one nest per step "
                           f"(A=B·B^T/N+I, X0=A^T/(|A|_1|A|_inf))",
@@ -663,7 +714,7 @@ def main():
               "parallelism": f"row-sharded x{world} (NCCL ring all-gather overlapped with K-split GEMMs)"
                              if world > 1 else "single GPU",
               "host_cpu": f"{cores} x {model}"}
-    base = {"metric": "NN inversion FP64 TFLOP/s", "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+    base = {"metric": "NN inversion FP64 TFLOP/s", "unit": "TFLOP/s", "n_gpus": world if args.impl == "ours" else args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded)", "config": config}
     if world > 1:
@@ -676,10 +727,12 @@ def main():
         t0 = time.perf_counter()
         vals = []
         for _ in range(args.warmup + args.steps):
-            vals.append(cpu_dense_sample(512, args.p))
+            vals.append(cpu_dense_sample(1024, args.p))
         v = statistics.median(x["value"] for x in vals[args.warmup:]) if args.steps else vals[-1]["value"]
         cb = dict(vals[-1])
         cb["value"] = v
+        # the trend the extrapolation rests on: the same product once at N=2048
+        cb["n2048_once"] = cpu_dense_sample(2048, args.p)["value"]
         line = dict(base, impl="reference", value=v, ms_per_step=round((time.perf_counter() - t0) * 1e3 /
                                                                        max(1, len(vals)), 1),
                     cpu_baseline=cb, e2e={"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
@@ -713,7 +766,7 @@ def main():
     if "c3" in legs and world == 1:
         line["legs"]["c3"] = run_c3(args)
     if rank == 0 and args.cpu:
-        line["cpu_baseline"] = cpu_dense_sample(512, args.p)
+        line["cpu_baseline"] = cpu_dense_sample(1024, args.p)
         if "mimo" in legs:
             line["legs"]["mimo"]["cpu_baseline"] = cpu_mimo_sample(16384)
         if "sparse" in legs:

@@ -14,6 +14,7 @@
 // ±, "+D", "+γI" and reduction terms.
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <vector>
 
 #include "engine.cuh"
@@ -314,11 +315,42 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
   const bool sym_mode = !exact && !c.cplx && cfg.order == 2;
   c.sym = false;
   int k = 0, products = 0, stopped = 1, recorded = 0;
+  // Fixed-count mode stops at a divergent nest like the reference (solver.cpp:151-157)
+  // without a host round trip per nest: each nest's non-finite flags go to pinned host
+  // memory behind an event, and nest k is enqueued only once nest k−2 has completed and
+  // was finite, so one nest stays queued and the device never idles on the check.
+  const bool watch = !tol_mode && !small && cfg.max_iters >= 3 && n >= 1024;
+  constexpr int kLag = 2;
+  int* nf_watch = nullptr;
+  std::vector<cudaEvent_t> nest_done;
+  if (watch) {
+    NNB_CUDA(cudaHostAlloc(&nf_watch, sizeof(int) * nf_count, cudaHostAllocDefault));
+    nest_done.assign(slots, nullptr);
+  }
+  auto watch_cleanup = [&]() {
+    for (cudaEvent_t e : nest_done)
+      if (e) cudaEventDestroy(e);
+    if (nf_watch) cudaFreeHost(nf_watch);
+  };
+  struct Guard {
+    std::function<void()> f;
+    ~Guard() { f(); }
+  } guard{watch_cleanup};
+  bool diverged_early = false;
   if (small)
     NNB_TRY(small_chain_real(A.re, X.re, R.re, bufs[1].re, bufs[2].re, n, c.ld, cfg, eps_dev, nf_dev, status_dev, c.s));
   for (; !small; ++k) {
     const bool last = (k >= cfg.max_iters);
     if (last && !cfg.final_residual) break;
+    if (watch && k >= kLag && nest_done[k - kLag]) {
+      NNB_CUDA(cudaEventSynchronize(nest_done[k - kLag]));
+      bool bad = false;
+      for (int j = 0; j <= p; ++j) bad |= nf_watch[(k - kLag) * (p + 1) + j] != 0;
+      if (bad) {  // reported below from the device flags, at the first non-finite nest
+        diverged_early = true;
+        break;
+      }
+    }
     const Plane& Xk = bufs[xi];
     const Plane& lhs = order == 0 ? A : Xk;
     const Plane& rhs = order == 0 ? Xk : A;
@@ -384,7 +416,14 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
       xi = vi;
       c.sym = false;
     }
+    if (watch) {
+      NNB_CUDA(cudaMemcpyAsync(nf_watch + k * (p + 1), nf_dev + k * (p + 1), sizeof(int) * (p + 1),
+                               cudaMemcpyDeviceToHost, c.s));
+      NNB_CUDA(cudaEventCreateWithFlags(&nest_done[k], cudaEventDisableTiming));
+      NNB_CUDA(cudaEventRecord(nest_done[k], c.s));
+    }
   }
+  (void)diverged_early;
   NNB_CUDA(cudaEventRecord(e1, c.s));
   // copy the final iterate into the caller's X buffer if it lives elsewhere
   if (bufs[xi].re != caller_x.re && !(io && io->out_streamed)) {

@@ -280,9 +280,33 @@ int run_sharded(Shard& sh, const double* A_local, int64_t lda_rows_stride, bool 
   std::vector<double> eps_h(slots, 0.0);
   std::vector<int> nf_h(nf_count, 0);
   int k = 0, products = 0, stopped = 1, recorded = 0;
+  // Fixed-count mode stops at a divergent nest (proj/src/solver.cpp:151-157) as the
+  // single-GPU chain does: the rank-combined non-finite flags of nest k (identical on
+  // every rank, so every rank takes the same decision) go to pinned memory behind an
+  // event; nest k is enqueued once nest k−2 completed finite.
+  const bool watch = cfg.tol <= 0.0 && cfg.max_iters >= 3;
+  constexpr int kLag = 2;
+  int* nf_watch = nullptr;
+  std::vector<cudaEvent_t> nest_done(slots, nullptr);
+  if (watch) NNB_CUDA(cudaHostAlloc(&nf_watch, sizeof(int) * nf_count, cudaHostAllocDefault));
+  struct WatchGuard {
+    std::vector<cudaEvent_t>& ev;
+    int* pinned;
+    ~WatchGuard() {
+      for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
+      if (pinned) cudaFreeHost(pinned);
+    }
+  } watch_guard{nest_done, nf_watch};
   for (;; ++k) {
     const bool last = k >= cfg.max_iters;
     if (last && !cfg.final_residual) break;
+    if (watch && k >= kLag && nest_done[k - kLag]) {
+      NNB_CUDA(cudaEventSynchronize(nest_done[k - kLag]));
+      bool bad = false;
+      for (int j = 0; j <= p; ++j) bad |= nf_watch[(k - kLag) * (p + 1) + j] != 0;
+      if (bad) break;  // reported below from the device flags
+    }
     // ---- R_g = I_g − A_g·X (ring all-gather of X overlapped) ----
     NNB_TRY(ring_allgather(sh, XF[cur]));
     for (int g : sh.local) {
@@ -338,6 +362,12 @@ int run_sharded(Shard& sh, const double* A_local, int64_t lda_rows_stride, bool 
                                              scale);
     count_launch();
     cur = nxt;
+    if (watch) {
+      NNB_CUDA(cudaMemcpyAsync(nf_watch + k * (p + 1), nf_dev + k * (p + 1), sizeof(int) * (p + 1),
+                               cudaMemcpyDeviceToHost, sh.s));
+      NNB_CUDA(cudaEventCreateWithFlags(&nest_done[k], cudaEventDisableTiming));
+      NNB_CUDA(cudaEventRecord(nest_done[k], sh.s));
+    }
   }
   NNB_CUDA(cudaEventRecord(e1, sh.s));
   NNB_CUDA(cudaMemcpyAsync(eps_h.data(), eps_dev, sizeof(double) * slots, cudaMemcpyDeviceToHost,
@@ -410,7 +440,16 @@ int nnb_comm_init(const void* id, int32_t world, int32_t rank, nnb_comm_t* comm_
     delete c;
     return fail(NNB_ERR_NCCL, std::string("ncclCommInitRank: ") + api.errorString(r));
   }
-  cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking);
+  // The ring's send/recv kernels must not queue behind a 1-CTA-per-SM GEMM grid:
+  // the block scheduler dispatches pending CTAs of the highest-priority stream first
+  // as SMs free up, so the communication stream gets the greatest priority.
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  if (cudaStreamCreateWithPriority(&c->cs, cudaStreamNonBlocking, greatest) != cudaSuccess) {
+    api.commDestroy(c->comm);
+    delete c;
+    return fail(NNB_ERR_CUDA, "comm: communication stream");
+  }
   *comm_out = c;
   return 0;
 }

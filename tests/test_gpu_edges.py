@@ -112,3 +112,24 @@ def test_sparse_rows_without_entries(ref):
 def test_spectral_and_transpose_degenerate():
     assert nnb.conjugate_transpose(np.zeros((0, 5))).shape == (5, 0)
     assert np.array_equal(nnb.random_spd(1, 10.0, 4), np.array([[1.0]]))
+
+
+def test_fixed_count_chain_stops_at_the_divergent_nest(port):
+    """Fixed-count mode: a chain that blows up at nest f raises DivergenceError(f) -- the
+    reference's index (proj/src/solver.cpp:151-157, through the bit-exact port) -- and
+    stops enqueueing nests two behind the failure instead of running all 40."""
+    from oracle import OracleError
+
+    a = W.gram_shifted(1024, seed=4, shift=1.0)
+    x0 = 3.0 * np.eye(1024)  # ||I - A X0|| > 1: eps squares every Newton nest until overflow
+    with pytest.raises(OracleError) as er:
+        port.chain(a, x0, 1, 40)
+    f = er.value.index
+    assert f is not None and 1 <= f < 20
+    l0 = nnb.kernel_launches()
+    with pytest.raises(nnb.DivergenceError) as ed:
+        nnb.nn_chain(a, x0, p=1, max_iters=40)
+    assert ed.value.nest_index == f
+    launched = nnb.kernel_launches() - l0
+    # (p+1) product launches per nest (+ the residual's), at most kLag = 2 nests past f
+    assert launched <= 4 * (f + 3) + 16, launched

@@ -25,6 +25,19 @@ def test_port_matmul_bitexact(port, ref):
         assert np.array_equal(port.matmul(a, b), ref.matmul(a, b)[0])
 
 
+def test_port_matmul_real_fast_path_bitexact(port, ref):
+    """Real operands take the port's blocked 4x16-register path (ascending k per element,
+    mul and add rounded separately); it must equal the reference's complex loop bit for
+    bit -- ragged shapes, panel tails, signed zeros and denormal-scale entries included."""
+    rng = np.random.default_rng(3)
+    for (m, k, n) in [(64, 64, 64), (97, 130, 77), (300, 17, 333), (256, 256, 256), (5, 900, 1000)]:
+        a, b = rng.standard_normal((m, k)), rng.standard_normal((k, n))
+        a[0, :3] = [-0.0, 1e-310, -1e-300]
+        b[:2, 0] = [0.0, -0.0]
+        pa, ra = port.matmul(a, b), ref.matmul(a, b)[0]
+        assert np.array_equal(pa.view(np.uint64), ra.view(np.uint64)), (m, k, n)
+
+
 def test_port_residual_and_steps_bitexact(port, ref):
     g = golden("steps_spd8.npz")
     wt, z = g["wt"], g["z"]
