@@ -104,10 +104,17 @@ uint64_t nnb_kernel_launches(void);
  *   rounded CUDA-core loops, serial Frobenius sums and the reference's own
  *   nest sequence — BIT-IDENTICAL to the reference for real data
  *   (a verification mode; complex products keep the 4-GEMM path).
- * The sparse path is bit-identical in both modes. */
-enum nnb_arith { NNB_ARITH_FAST = 0, NNB_ARITH_REFERENCE = 1 };
+ * NNB_ARITH_OZAKI: real dense products emulated on the int8 tensor cores
+ *   (tcgen05.mma kind::i8, Ozaki scheme II with 16 moduli: csrc/ozaki.cu):
+ *   every entry keeps 53 bits relative to its row's (column's) largest, the
+ *   integer products are exact; same parity gate as FAST (X within 1e-10,
+ *   identical nest counts).  Complex products keep the DMMA path.
+ * The sparse path is bit-identical in every mode. */
+enum nnb_arith { NNB_ARITH_FAST = 0, NNB_ARITH_REFERENCE = 1, NNB_ARITH_OZAKI = 2 };
 int nnb_set_arithmetic(int32_t mode);
 int32_t nnb_get_arithmetic(void);
+/* Moduli (= int8 GEMMs per product) NNB_ARITH_OZAKI uses for inner dimension k. */
+int32_t nnb_ozaki_moduli(int64_t k);
 
 /* ---- dense kernels ------------------------------------------------------ */
 /* C = A·B.  Replaces nn::matmul (proj/include/nn/kernels.hpp:20-21,

@@ -92,6 +92,7 @@ _SIGS = {
     "nnb_kernel_launches": ([], C.c_uint64),
     "nnb_set_arithmetic": ([_i32], C.c_int),
     "nnb_get_arithmetic": ([], C.c_int32),
+    "nnb_ozaki_moduli": ([_i64], C.c_int32),
     "nnb_gemm_d": ([_dp, _i64, _dp, _i64, _dp, _i64, _i64, _i64, _i64, _dp], C.c_int),
     "nnb_gemm_z": ([_dp, _dp, _dp, _i64, _i64, _i64, _dp], C.c_int),
     "nnb_gemm_nt_d": ([_dp, _i64, _dp, _i64, _dp, _i64, _i64, _i64, _i64, _dp], C.c_int),
@@ -181,20 +182,43 @@ def kernel_launches() -> int:
     return int(lib().nnb_kernel_launches())
 
 
-ARITH_FAST, ARITH_REFERENCE = 0, 1
+ARITH_FAST, ARITH_REFERENCE, ARITH_OZAKI = 0, 1, 2
 
 
-class reference_arithmetic:
-    """Context manager: run real dense products in the reference-exact mode
-    (bit-identical to the reference; CUDA-core FP64, a verification mode)."""
+class arithmetic:
+    """Context manager: run real dense products in the given arithmetic mode of the
+    calling thread (nnb_set_arithmetic), restoring the previous mode on exit."""
+
+    def __init__(self, mode: int):
+        self.mode = mode
 
     def __enter__(self):
         self._prev = lib().nnb_get_arithmetic()
-        _check(lib().nnb_set_arithmetic(ARITH_REFERENCE))
+        _check(lib().nnb_set_arithmetic(self.mode))
         return self
 
     def __exit__(self, *exc):
         lib().nnb_set_arithmetic(self._prev)
+
+
+def ozaki_moduli(k: int) -> int:
+    """Moduli the int8 emulation uses for inner dimension k (each is one int8 GEMM)."""
+    return int(lib().nnb_ozaki_moduli(int(k)))
+
+
+class reference_arithmetic(arithmetic):
+    """Reference-exact mode (bit-identical to the reference; CUDA-core FP64, a
+    verification mode)."""
+
+    def __init__(self):
+        super().__init__(ARITH_REFERENCE)
+
+
+class ozaki_arithmetic(arithmetic):
+    """Real products emulated on the int8 tensor cores (Ozaki scheme II, csrc/ozaki.cu)."""
+
+    def __init__(self):
+        super().__init__(ARITH_OZAKI)
 
 
 def _check(status: int, index: int = 0) -> None:

@@ -245,7 +245,16 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
   // reference-exact mode (real data): the reference's operand order and nest sequence
   const bool exact = arith() == 1 && !c.cplx;
   // small real N: the whole loop in one cooperative kernel (chain_small.cu)
-  const bool small = !c.cplx && !exact && !io && small_chain_eligible(n, c.ld, cfg);
+  const bool small = !c.cplx && !exact && arith() != 2 && !io && small_chain_eligible(n, c.ld, cfg);
+  // int8-emulated products (NNB_ARITH_OZAKI): A is the same operand in every nest, so its
+  // int8 splits are formed once per chain
+  struct OzPin {
+    bool on;
+    ~OzPin() {
+      if (on) oz_unpin();
+    }
+  } oz_pin_guard{arith() == 2 && !c.cplx};
+  if (oz_pin_guard.on) oz_pin(A.re, c.ld, n, n);
   if (!small) NNB_TRY(c.red.init(max_tiles_for(n, n), c.s));
   DevBuf work;
   NNB_TRY(work.alloc(sizeof(double) * (size_t)mat * planes * 3, c.s));

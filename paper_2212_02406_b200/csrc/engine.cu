@@ -177,6 +177,22 @@ int make_tmap(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, 
   return 0;
 }
 
+int make_tmap_u8(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                 int box_cols) {
+  auto fn = encode_fn();
+  if (!fn) return fail(7, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld & 15)) return fail(7, "TMA u8 operand needs 16B alignment");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(7, "cuTensorMapEncodeTiled (u8) failed: " + std::to_string(r));
+  return 0;
+}
+
 // ============================ GEMM ============================
 using BigCfg = GemmCfg<128, 128, 16, 2, 4, 4>;
 using SmallCfg = GemmCfg<64, 64, 16, 2, 2, 4>;
@@ -294,6 +310,10 @@ int gemm(GemmOp op, RedWs* red, cudaStream_t s) {
     return 0;
   }
   if (arith() == 1 && !op.b_kmajor) return gemm_exact(op, s);  // reference-exact mode (exact.cu)
+  if (arith() == 2 && !op.ep.C2 && !op.ep.acc_in) {               // int8 emulation (ozaki.cu)
+    op.ep.sym = 0;  // the emulated product is formed whole
+    return gemm_ozaki(op, s);
+  }
   if (op.b_kmajor) return use_big(op.M, op.N) ? launch_cfg<BigCfgT>(op, s) : launch_cfg<SmallCfgT>(op, s);
   if (use_nano(op.M, op.N)) return launch_cfg<NanoCfg>(op, s);
   if (use_tiny(op.M, op.N)) return launch_cfg<TinyCfg>(op, s);

@@ -114,6 +114,15 @@ int make_tmap(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, 
 void set_arith(int mode);
 int arith();
 int gemm_exact(const GemmOp& op, cudaStream_t s);
+// Ozaki-II emulation of a real product on the int8 tensor cores (ozaki.cu).
+int gemm_ozaki(const GemmOp& op, cudaStream_t s);
+int ozaki_moduli_for(int64_t k);
+// A chain operand that stays unchanged while pinned: its int8 splits are reused.
+void oz_pin(const double* p, int64_t ld, int64_t rows, int64_t cols);
+void oz_unpin();
+// 2D uint8 TMA descriptor (rows × cols bytes, leading dimension ld bytes), 128B swizzle.
+int make_tmap_u8(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                 int box_cols);
 // Launches C = epilogue(A·B).  If `red` is non-null the Σ C² / non-finite
 // reduction is wired to it (ep.ss_out / nf_out / eps_out chosen by caller).
 int gemm(GemmOp op, RedWs* red, cudaStream_t s);

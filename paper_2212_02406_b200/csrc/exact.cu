@@ -21,11 +21,11 @@
 
 namespace nnb {
 
-// 0 fast (DMMA), 1 reference-exact.  NNB_ARITHMETIC=reference selects the exact
-// mode for every thread (e.g. for the C++ drop-in without code changes).
+// 0 fast (DMMA), 1 reference-exact, 2 Ozaki int8 emulation (ozaki.cu).
+// NNB_ARITHMETIC=reference (=ozaki) selects the mode for every thread (e.g. for the C++ drop-in without code changes).
 static int initial_arith() {
   const char* e = std::getenv("NNB_ARITHMETIC");
-  return (e && e[0] == 'r') ? 1 : 0;
+  return (e && e[0] == 'r') ? 1 : (e && e[0] == 'o') ? 2 : 0;
 }
 static thread_local int g_arith = initial_arith();
 void set_arith(int mode) { g_arith = mode; }

@@ -1,0 +1,734 @@
+// FP64 products emulated on the int8 tensor cores (tcgen05.mma kind::i8):
+// the Ozaki scheme II, NNB_ARITH_OZAKI.  sm_100a has no FP64 tcgen05 kind, and
+// its DMMA pipe peaks at 37 TFLOP/s; the int8 pipe runs ~120x faster, so an
+// FP64 product that costs s int8 GEMMs (s = 16 moduli) plus O(N^2) passes
+// beats DMMA by several times at large N.  Every product of the chain
+// (proj/src/kernels.cpp:137-162, the reference's nn::matmul) goes through it
+// when the mode is on; the chain logic, its epilogue contract (α·A·B + β·D +
+// γ·I, deterministic Σ C², non-finite count) and its stop rules are unchanged.
+//
+// The scheme, for C = A·B with A m×k and B k×n:
+//   1. Scale.  Row i of A by 2^ea_i and column j of B by 2^eb_j so that the
+//      largest magnitude of each lands in [2^52, 2^53); round to integers
+//      A' = rint(2^ea·A), B' = rint(B·2^eb) (|A'|, |B'| <= 2^53).  This is the
+//      only rounding of the scheme: each entry keeps its bits down to 2^-53
+//      of its row's (column's) largest entry.
+//   2. Residues.  For pairwise coprime moduli m_1..m_s <= 256 (M = Πm_l),
+//      A'_l = A' mod m_l and B'_l = B' mod m_l as signed int8 (symmetric).
+//   3. s int8 GEMMs on tcgen05: C_l = A'_l·B'_lᵀ accumulates exactly in int32
+//      (|A'_l|,|B'_l| <= 128, k < 2^17), stored as C_l mod m_l (uint8).
+//   4. Reconstruction.  Garner's mixed-radix digits of C' = A'·B' from the s
+//      residues (exact small-integer arithmetic), the symmetric representative
+//      (k·2^106 < M/8, so the top digit decides the sign), a Horner evaluation
+//      in FP64 (rounds only once |C'| passes 2^53, relative error ~s·2^-53),
+//      the scaling back by 2^-(ea_i+eb_j), and the chain's epilogue.
+// The integer product A'·B' is exact, so the error is step 1's truncation
+// only: |C − fl(C)| <= 2^-53·k·max_i|a_i·|·max_j|b_·j| per element, the same
+// order as a DGEMM's u·k·|a||b| bound.  Parity against the reference is
+// therefore the same gate as the DMMA path: X within 1e-10 and identical nest
+// counts (tests/test_gpu_ozaki.py).
+//
+// The int8 GEMM (oz_gemm_kernel): one CTA per 128×256 output tile and modulus,
+// warp-specialised — warp 0 lane 0 drives a 4-stage TMA ring (A 128×128 B,
+// B 256×128 B, 128B swizzle, K-major), warp 1 lane 0 issues tcgen05.mma
+// (M=128, N=256, K=32 per instruction) into a 256-column TMEM accumulator and
+// frees each stage with tcgen05.commit, warps 2-5 drain TMEM (tcgen05.ld
+// 32x32b), reduce mod m_l and store uint8 residues.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "common.cuh"
+#include "engine.cuh"
+
+namespace nnb {
+namespace {
+
+constexpr int kMaxMod = 20;
+constexpr int kModuli[kMaxMod] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227,
+                                  223, 217, 211, 199, 197, 193, 191, 181, 179, 173};
+constexpr int kAlpha = 53;                  // bits kept per row (column) of an operand
+constexpr int kBadExp = INT_MIN / 4;        // exponent marking a row/column with a non-finite entry
+constexpr int64_t kMaxK = 131071;           // 128·128·k < 2^31: exact int32 accumulation
+
+// Garner constants for the first s moduli (host-computed, passed by value).
+struct OzConst {
+  int s;
+  int mi[kMaxMod];
+  float mf[kMaxMod];
+  float inv_mf[kMaxMod];
+  double md[kMaxMod];
+  double inv_md[kMaxMod];
+  float P[kMaxMod];                 // v_j = (r_j·P_j + Σ_{i<j} v_i·Q[i][j]) mod m_j
+  float Q[kMaxMod][kMaxMod];
+};
+
+// The same Garner constants at compile time (template parameters -> FFMA immediates),
+// so the reconstruction's 120 FFMAs do not hold 120 constants in registers.
+constexpr int kMod(int j) {
+  return j == 0 ? 256 : j == 1 ? 255 : j == 2 ? 253 : j == 3 ? 251 : j == 4 ? 247 : j == 5 ? 241 : j == 6 ? 239
+       : j == 7 ? 233 : j == 8 ? 229 : j == 9 ? 227 : j == 10 ? 223 : j == 11 ? 217 : j == 12 ? 211
+       : j == 13 ? 199 : j == 14 ? 197 : j == 15 ? 193 : j == 16 ? 191 : j == 17 ? 181 : j == 18 ? 179 : 173;
+}
+constexpr int cinv_mod(int a, int m) {
+  a %= m;
+  for (int x = 1; x < m; ++x)
+    if ((a * x) % m == 1) return x;
+  return 0;
+}
+constexpr int garner_p(int j) {  // Π_{k<j} m_k^-1 mod m_j
+  long long prod = 1;
+  for (int k = 0; k < j; ++k) prod = prod * cinv_mod(kMod(k), kMod(j)) % kMod(j);
+  return static_cast<int>(prod);
+}
+constexpr int garner_q(int i, int j) {  // m_j − Π_{k=i}^{j−1} m_k^-1 mod m_j
+  long long q = 1;
+  for (int k = i; k < j; ++k) q = q * cinv_mod(kMod(k), kMod(j)) % kMod(j);
+  return static_cast<int>((kMod(j) - q) % kMod(j));
+}
+template <int I, int L>
+struct GarnerQ {
+  static constexpr float v = static_cast<float>(garner_q(I, L));
+};
+template <int L>
+struct GarnerP {
+  static constexpr float v = static_cast<float>(garner_p(L));
+  static constexpr float m = static_cast<float>(kMod(L));
+  static constexpr float inv = 1.0f / static_cast<float>(kMod(L));
+};
+// x + Σ_{i<L} v_i·Q[i][L]
+template <int L, int I>
+__device__ __forceinline__ float garner_sum(const float* v, float x) {
+  if constexpr (I < L) return garner_sum<L, I + 1>(v, fmaf(v[I], GarnerQ<I, L>::v, x));
+  else return x;
+}
+// mixed-radix digits v_0..v_{S-1} of the residues r (exact small-integer float arithmetic)
+template <int L, int S>
+__device__ __forceinline__ void garner_digits(float* v, const float* r) {
+  if constexpr (L < S) {
+    if constexpr (L == 0) {
+      v[0] = r[0];
+    } else {
+      const float x = garner_sum<L, 0>(v, r[L] * GarnerP<L>::v);  // < 2^20
+      const float qf = floorf(x * GarnerP<L>::inv);
+      float d = fmaf(-qf, GarnerP<L>::m, x);
+      d += (d < 0.0f) ? GarnerP<L>::m : 0.0f;
+      d -= (d >= GarnerP<L>::m) ? GarnerP<L>::m : 0.0f;
+      v[L] = d;
+    }
+    garner_digits<L + 1, S>(v, r);
+  }
+}
+// Horner from the top digit: x·m_L + v_L for L = S−2 .. 0
+template <int L>
+__device__ __forceinline__ double horner(const float* v, double x) {
+  if constexpr (L < 0) return x;
+  else return horner<L - 1>(v, fma(x, static_cast<double>(kMod(L)), static_cast<double>(v[L])));
+}
+
+int inv_mod(int a, int m) {
+  a %= m;
+  for (int x = 1; x < m; ++x)
+    if ((a * x) % m == 1) return x;
+  return 0;
+}
+
+OzConst make_const(int s) {
+  OzConst c{};
+  c.s = s;
+  for (int j = 0; j < s; ++j) {
+    const int m = kModuli[j];
+    c.mi[j] = m;
+    c.mf[j] = static_cast<float>(m);
+    c.inv_mf[j] = 1.0f / static_cast<float>(m);
+    c.md[j] = m;
+    c.inv_md[j] = 1.0 / m;
+    // Garner: t = r_j; for i < j: t = (t − v_i)·inv(m_i) mod m_j
+    //   => v_j = r_j·Π_{k<j} inv_k − Σ_{i<j} v_i·Π_{k=i}^{j−1} inv_k   (mod m_j)
+    long long prod = 1;
+    for (int k = 0; k < j; ++k) prod = prod * inv_mod(kModuli[k], m) % m;
+    c.P[j] = static_cast<float>(prod);
+    for (int i = 0; i < j; ++i) {
+      long long q = 1;
+      for (int k = i; k < j; ++k) q = q * inv_mod(kModuli[k], m) % m;
+      c.Q[i][j] = static_cast<float>((m - q) % m);  // + v_i·(m − q) ≡ − v_i·q
+    }
+  }
+  return c;
+}
+
+// moduli needed so that k·2^(2·53) < M/8 (exact, sign decided by the top digit)
+int moduli_for(int64_t k) {
+  const double need = 2.0 * kAlpha + std::ceil(std::log2(static_cast<double>(std::max<int64_t>(k, 2)))) + 3.0;
+  double have = 0.0;
+  for (int s = 0; s < kMaxMod; ++s) {
+    have += std::log2(static_cast<double>(kModuli[s]));
+    if (have >= need) return s + 1;
+  }
+  return kMaxMod;
+}
+
+// ---------------------------------------------------------------- tcgen05 wrappers
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive on `bar` once every tcgen05.mma this thread issued so far has completed
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// 32 lanes × 32 consecutive 32-bit TMEM columns -> 32 registers per thread (row = lane)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// K-major operand tile, 128B swizzle (rows of 128 bytes, 8-row groups 1024 B apart):
+// start address >> 4, LBO 1 (unused for swizzled K-major), SBO 1024 B, version 1, SWIZZLE_128B
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// ---------------------------------------------------------------- the int8 GEMM
+constexpr int kBM = 128, kBN = 256, kBK = 128, kStages = 4;
+constexpr int kABytes = kBM * kBK;  // 16 KB
+constexpr int kBBytes = kBN * kBK;  // 32 KB
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kGemmSmem = kStages * kStageBytes + 1024 + 256;
+constexpr uint32_t kIdesc = (2u << 4) |            // D: s32
+                            (1u << 7) | (1u << 10) |  // A, B: signed int8
+                            ((uint32_t)(kBN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);  // K-major both
+
+// out[l][row][col] = (Σ_k a_l[row][k]·b_l[col][k]) mod m_l, for blockIdx.z = l.
+// a_l rows live at l·M + row of tma_a, b_l rows at l·N + col of tma_b.
+__global__ void __launch_bounds__(192, 1)
+    oz_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, int M, int N,
+                   int K, int64_t ldr, uint8_t* __restrict__ out, const OzConst cst) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* done = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int l = blockIdx.z;
+  const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * kBN;
+  const int nk = (K + kBK - 1) / kBK;
+
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, kBN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      tma_prefetch_desc(&tma_a);
+      tma_prefetch_desc(&tma_b);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int st = kb % kStages;
+        if (kb >= kStages) mbar_wait(&empty[st], ((kb / kStages) & 1) ^ 1);
+        uint8_t* sa = smem + st * kStageBytes;
+        mbar_arrive_expect_tx(&full[st], kStageBytes);
+        tma_load_2d(sa, &tma_a, &full[st], kb * kBK, l * M + m0);
+        tma_load_2d(sa + kABytes, &tma_b, &full[st], kb * kBK, l * N + n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      for (int kb = 0; kb < nk; ++kb) {
+        const int st = kb % kStages;
+        mbar_wait(&full[st], (kb / kStages) & 1);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(smem + st * kStageBytes), b_addr = a_addr + kABytes;
+#pragma unroll
+        for (int k = 0; k < kBK / 32; ++k)
+          mma_i8(tbase, sw128_desc(a_addr + 32 * k), sw128_desc(b_addr + 32 * k), kIdesc, (kb | k) != 0);
+        mma_commit(&empty[st]);  // the stage is free once these MMAs have read it
+      }
+      mma_commit(done);
+    }
+  } else {  // epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
+    const int q = warp & 3;
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const int row = m0 + 32 * q + lane;
+    const int m = cst.mi[l];
+    const double inv = cst.inv_md[l];
+    uint8_t* orow = out + ((int64_t)l * M + row) * ldr;
+#pragma unroll 1
+    for (int c = 0; c < kBN / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld32(tbase + (static_cast<uint32_t>(32 * q) << 16) + 32 * c, v);
+      const int col = n0 + 32 * c;
+      if (row < M && col < ldr) {
+        uint32_t packed[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int a = static_cast<int>(v[4 * w + b]);
+            int r = a - m * __double2int_rd(static_cast<double>(a) * inv);
+            r += (r < 0) ? m : 0;
+            r -= (r >= m) ? m : 0;
+            word |= static_cast<uint32_t>(r) << (8 * b);
+          }
+          packed[w] = word;
+        }
+        uint4* dst = reinterpret_cast<uint4*>(orow + col);
+        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        if (col + 16 < ldr) dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, kBN);
+  }
+}
+
+// ---------------------------------------------------------------- operand splits
+__device__ __forceinline__ int exp_for(double amax) {
+  // 2^e·amax in [2^52, 2^53)
+  return amax == 0.0 ? 0 : kAlpha - 1 - ilogb(amax);
+}
+
+// signed residue of the integer-valued double a (|a| <= 2^53) modulo m, in [-128, 127]
+__device__ __forceinline__ int resid(double a, double m, double inv_m) {
+  const double q = rint(a * inv_m);
+  int r = static_cast<int>(fma(-q, m, a));  // exact: the result is a small integer
+  const int mi = static_cast<int>(m);
+  r -= (r > 127) ? mi : 0;
+  r += (r < -128) ? mi : 0;
+  return r;
+}
+
+// Left operand: per-row scaling.  One 256-thread block per row:
+// out[l][row][kp] int8 residues (zero-padded from k to kp), exps[row].
+__global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __restrict__ X, int64_t ld, int rows,
+                                                            int k, int64_t kp, int8_t* __restrict__ out,
+                                                            int* __restrict__ exps, const OzConst cst) {
+  __shared__ double smax[8];
+  __shared__ int sbad[8];
+  const int row = blockIdx.x;
+  const double* xr = X + (int64_t)row * ld;
+  double mx = 0.0;
+  int bad = 0;
+  for (int c = threadIdx.x; c < k; c += 256) {
+    const double v = xr[c];
+    bad |= !isfinite(v);
+    mx = fmax(mx, fabs(v));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    smax[threadIdx.x >> 5] = mx;
+    sbad[threadIdx.x >> 5] = bad;
+  }
+  __syncthreads();
+  mx = 0.0;
+  bad = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    mx = fmax(mx, smax[w]);
+    bad |= sbad[w];
+  }
+  const int e = bad ? kBadExp : exp_for(mx);
+  if (threadIdx.x == 0) exps[row] = e;
+  const int s = cst.s;
+  for (int64_t c0 = threadIdx.x * 8; c0 < kp; c0 += 256 * 8) {
+    double a[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t c = c0 + j;
+      a[j] = (c < k && !bad) ? rint(scalbn(xr[c], e)) : 0.0;
+    }
+    for (int l = 0; l < s; ++l) {
+      const double m = cst.md[l], inv = cst.inv_md[l];
+      uint32_t lo = 0, hi = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) lo |= (static_cast<uint32_t>(resid(a[j], m, inv)) & 0xffu) << (8 * j);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) hi |= (static_cast<uint32_t>(resid(a[4 + j], m, inv)) & 0xffu) << (8 * j);
+      if (c0 + 8 <= kp) {
+        *reinterpret_cast<uint2*>(out + ((int64_t)l * rows + row) * kp + c0) = make_uint2(lo, hi);
+      } else {  // kp is a multiple of 16 and c0 of 8: never partial, kept for safety
+        *reinterpret_cast<uint32_t*>(out + ((int64_t)l * rows + row) * kp + c0) = lo;
+      }
+    }
+  }
+}
+
+// Right operand, pass 1: per-column max |b| (as ordered bits) and non-finite flags.
+__global__ void __launch_bounds__(256) oz_colmax_kernel(const double* __restrict__ B, int64_t ld, int k, int n,
+                                                        unsigned long long* __restrict__ colmax,
+                                                        int* __restrict__ colbad) {
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= n) return;
+  const int r0 = blockIdx.y * 256, r1 = min(k, r0 + 256);
+  double mx = 0.0;
+  int bad = 0;
+  for (int r = r0; r < r1; ++r) {
+    const double v = B[(int64_t)r * ld + c];
+    bad |= !isfinite(v);
+    mx = fmax(mx, fabs(v));
+  }
+  if (mx > 0.0) atomicMax(colmax + c, static_cast<unsigned long long>(__double_as_longlong(mx)));
+  if (bad) atomicOr(colbad + c, 1);
+}
+
+// Right operand, pass 2: 64(k)×64(n) tiles transposed through shared memory into
+// K-major residues out[l][col][kp]; exps[col] written by the first k-tile row.
+__global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __restrict__ B, int64_t ld, int k, int n,
+                                                            int64_t kp, const unsigned long long* __restrict__ colmax,
+                                                            const int* __restrict__ colbad,
+                                                            int8_t* __restrict__ out, int* __restrict__ exps,
+                                                            const OzConst cst) {
+  __shared__ double tile[64][65];
+  const int n0 = blockIdx.x * 64, k0 = blockIdx.y * 64;
+  for (int i = threadIdx.x; i < 64 * 64; i += 256) {
+    const int kk = i >> 6, nn = i & 63;
+    const int r = k0 + kk, c = n0 + nn;
+    tile[kk][nn] = (r < k && c < n) ? B[(int64_t)r * ld + c] : 0.0;
+  }
+  __syncthreads();
+  const int nn = threadIdx.x >> 2, kc = (threadIdx.x & 3) * 16;
+  const int col = n0 + nn;
+  if (col >= n) return;
+  const bool bad = colbad[col] != 0;
+  const int e = bad ? kBadExp : exp_for(__longlong_as_double(static_cast<long long>(colmax[col])));
+  if (blockIdx.y == 0 && kc == 0) exps[col] = e;
+  if (k0 + kc >= kp) return;
+  double a[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) a[j] = bad ? 0.0 : rint(scalbn(tile[kc + j][nn], e));
+  const int s = cst.s;
+  for (int l = 0; l < s; ++l) {
+    const double m = cst.md[l], inv = cst.inv_md[l];
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) word |= (static_cast<uint32_t>(resid(a[4 * q + j], m, inv)) & 0xffu) << (8 * j);
+      w[q] = word;
+    }
+    *reinterpret_cast<uint4*>(out + ((int64_t)l * n + col) * kp + k0 + kc) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// ---------------------------------------------------------------- reconstruction
+// One block: 16 rows × 128 columns; thread t: row t/16, 8 consecutive columns.
+template <int S>
+__global__ void __launch_bounds__(256) oz_recon_kernel(const uint8_t* __restrict__ res, int64_t ldr, int M, int N,
+                                                       const int* __restrict__ ea, const int* __restrict__ eb,
+                                                       GemmEpilogue ep, const OzConst cst) {
+  __shared__ double red[8];
+  __shared__ int redi[8];
+  __shared__ int last_flag;
+  const int row = blockIdx.y * 16 + (threadIdx.x >> 4);
+  const int c0 = blockIdx.x * 128 + (threadIdx.x & 15) * 8;
+  double ss = 0.0;
+  int nf = 0;
+  const bool want_red = ep.ss_partial != nullptr;
+  if (row < M && c0 < N) {
+    uint2 rv[S];
+#pragma unroll
+    for (int l = 0; l < S; ++l) rv[l] = *reinterpret_cast<const uint2*>(res + ((int64_t)l * M + row) * ldr + c0);
+    const int era = ea[row];
+#pragma unroll 1
+    for (int jp = 0; jp < 4; ++jp) {
+      const int c = c0 + 2 * jp;
+      if (c >= N) break;
+      const bool two = c + 1 < N;
+      double out2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 2 * jp + h;
+        const int shift = 8 * (j & 3);
+        float r[S], v[S];
+#pragma unroll
+        for (int l = 0; l < S; ++l) {
+          const uint32_t word = (jp < 2) ? rv[l].x : rv[l].y;
+          r[l] = static_cast<float>((word >> shift) & 0xffu);
+        }
+        garner_digits<0, S>(v, r);
+        // symmetric representative: C' − M replaces the top digit v_S by v_S − m_S
+        double x = static_cast<double>(v[S - 1]);
+        if (v[S - 1] >= 0.5f * static_cast<float>(kMod(S - 1))) x -= static_cast<double>(kMod(S - 1));
+        x = horner<S - 2>(v, x);
+        // scale back by 2^-(ea+eb), then the chain's epilogue
+        const int cc = c + h;
+        const int e = (cc < N) ? eb[cc] : 0;
+        double cv;
+        if (era == kBadExp || e == kBadExp) cv = __longlong_as_double(0x7ff8000000000000LL);
+        else cv = scalbn(x, -(era + e));
+        double o = ep.alpha * cv;
+        if (ep.D && cc < N) o = fma(ep.beta, ep.D[(int64_t)row * ep.ldd + cc], o);
+        if ((int64_t)row + ep.diag_offset == cc) o += ep.gamma;
+        out2[h] = o;
+      }
+      double* cp = ep.C + (int64_t)row * ep.ldc + c;
+      if (two) {
+        *reinterpret_cast<double2*>(cp) = make_double2(out2[0], out2[1]);
+      } else {
+        cp[0] = out2[0];
+      }
+      if (want_red) {
+        ss = fma(out2[0], out2[0], ss);
+        nf += !isfinite(out2[0]);
+        if (two) {
+          ss = fma(out2[1], out2[1], ss);
+          nf += !isfinite(out2[1]);
+        }
+      }
+    }
+  }
+  if (!want_red) return;
+  // deterministic reduction: fixed shuffle tree, fixed warp order, last block sums the
+  // block partials in index order (the DMMA epilogue's scheme, gemm_f64.cuh)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  ss = warp_sum(ss);
+  nf = warp_sum_i(nf);
+  if (lane == 0) {
+    red[warp] = ss;
+    redi[warp] = nf;
+  }
+  __syncthreads();
+  const int pid = blockIdx.y * gridDim.x + blockIdx.x;
+  const int nblocks = gridDim.x * gridDim.y;
+  if (threadIdx.x == 0) {
+    double tss = 0.0;
+    int tnf = 0;
+    for (int w = 0; w < 8; ++w) {
+      tss += red[w];
+      tnf += redi[w];
+    }
+    ep.ss_partial[pid] = tss;
+    ep.nf_partial[pid] = tnf;
+    __threadfence();
+    const unsigned done = atomicAdd(ep.tile_counter, 1u);
+    last_flag = (done == (unsigned)(nblocks - 1));
+  }
+  __syncthreads();
+  if (!last_flag) return;
+  __threadfence();
+  double s2 = 0.0;
+  int n2 = 0;
+  for (int k = threadIdx.x; k < nblocks; k += 256) {
+    s2 += __ldcg(ep.ss_partial + k);
+    n2 += __ldcg(ep.nf_partial + k);
+  }
+  s2 = warp_sum(s2);
+  n2 = warp_sum_i(n2);
+  __syncthreads();
+  if (lane == 0) {
+    red[warp] = s2;
+    redi[warp] = n2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    int ntot = 0;
+    for (int w = 0; w < 8; ++w) {
+      tot += red[w];
+      ntot += redi[w];
+    }
+    if (ep.ss_out) *ep.ss_out = tot;
+    if (ep.nf_out) *ep.nf_out = ntot;
+    if (ep.eps_out) *ep.eps_out = sqrt(tot) * ep.eps_scale;
+    *ep.tile_counter = 0u;
+  }
+}
+
+// ---------------------------------------------------------------- host side
+struct OzOperand {
+  DevBuf res;   // int8 [s][rows][kp]
+  DevBuf exps;  // int [rows]
+  int64_t rows = 0, k = 0, kp = 0;
+  int s = 0;
+};
+
+int split_left(const double* A, int64_t lda, int64_t rows, int64_t k, const OzConst& c, OzOperand& o,
+               cudaStream_t st) {
+  o.rows = rows;
+  o.k = k;
+  o.kp = (k + 15) / 16 * 16;
+  o.s = c.s;
+  NNB_TRY(o.res.alloc((size_t)c.s * rows * o.kp, st));
+  NNB_TRY(o.exps.alloc(sizeof(int) * std::max<int64_t>(rows, 1), st));
+  oz_split_rows_kernel<<<static_cast<unsigned>(rows), 256, 0, st>>>(A, lda, (int)rows, (int)k, o.kp,
+                                                                      o.res.as<int8_t>(), o.exps.as<int>(), c);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// B is k×n row-major (ldb), or with kmajor its transpose Bᵀ (n×k row-major)
+int split_right(const double* B, int64_t ldb, int64_t k, int64_t n, bool kmajor, const OzConst& c, OzOperand& o,
+                cudaStream_t st) {
+  if (kmajor) return split_left(B, ldb, n, k, c, o, st);
+  o.rows = n;
+  o.k = k;
+  o.kp = (k + 15) / 16 * 16;
+  o.s = c.s;
+  NNB_TRY(o.res.alloc((size_t)c.s * n * o.kp, st));
+  NNB_TRY(o.exps.alloc(sizeof(int) * std::max<int64_t>(n, 1), st));
+  DevBuf cm;
+  NNB_TRY(cm.alloc((sizeof(unsigned long long) + sizeof(int)) * n, st));
+  unsigned long long* colmax = cm.as<unsigned long long>();
+  int* colbad = reinterpret_cast<int*>(colmax + n);
+  NNB_CUDA(cudaMemsetAsync(cm.p, 0, cm.bytes, st));
+  oz_colmax_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)((k + 255) / 256)), 256, 0, st>>>(
+      B, ldb, (int)k, (int)n, colmax, colbad);
+  count_launch();
+  oz_split_cols_kernel<<<dim3((unsigned)((n + 63) / 64), (unsigned)((o.kp + 63) / 64)), 256, 0, st>>>(
+      B, ldb, (int)k, (int)n, o.kp, colmax, colbad, o.res.as<int8_t>(), o.exps.as<int>(), c);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int launch_recon(int s, const uint8_t* res, int64_t ldr, int M, int N, const int* ea, const int* eb,
+                 const GemmEpilogue& ep, const OzConst& c, cudaStream_t st) {
+  const dim3 grid((unsigned)((N + 127) / 128), (unsigned)((M + 15) / 16));
+  switch (s) {
+#define NNB_OZ_RECON(S)                                                                     \
+  case S:                                                                                   \
+    oz_recon_kernel<S><<<grid, 256, 0, st>>>(res, ldr, M, N, ea, eb, ep, c);                \
+    break;
+    NNB_OZ_RECON(15)
+    NNB_OZ_RECON(16)
+    NNB_OZ_RECON(17)
+#undef NNB_OZ_RECON
+    default:
+      return fail(7, "ozaki: unsupported moduli count " + std::to_string(s));
+  }
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// Operand pinned by the chain for its whole run (A never changes between nests):
+// its split is computed once per role and reused.
+struct Pinned {
+  const double* p = nullptr;
+  int64_t ld = 0, rows = 0, cols = 0;
+  OzOperand left, right;
+  bool have_left = false, have_right = false;
+  int s_left = 0, s_right = 0;
+};
+thread_local Pinned* g_pinned = nullptr;
+
+}  // namespace
+
+void oz_pin(const double* p, int64_t ld, int64_t rows, int64_t cols) {
+  delete g_pinned;
+  g_pinned = new Pinned();
+  g_pinned->p = p;
+  g_pinned->ld = ld;
+  g_pinned->rows = rows;
+  g_pinned->cols = cols;
+}
+
+void oz_unpin() {
+  delete g_pinned;
+  g_pinned = nullptr;
+}
+
+int make_tmap_u8(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                 int box_cols);
+
+int gemm_ozaki(const GemmOp& op, cudaStream_t st) {
+  const int64_t M = op.M, N = op.N, K = op.K;
+  if (K > kMaxK) return fail(7, "ozaki: inner dimension above 131071 (int32 accumulation bound)");
+  if (op.ep.C2 || op.ep.acc_in) return fail(7, "ozaki: dual-output and K-split epilogues are DMMA-only");
+  const int s = std::max(15, moduli_for(K));  // small k: 15 (the smallest instantiated set)
+  const OzConst c = make_const(s);
+  // operand splits (the pinned chain operand's are cached per role)
+  OzOperand la, rb;
+  const OzOperand* L = &la;
+  const OzOperand* R = &rb;
+  Pinned* pin = g_pinned;
+  if (pin && op.A == pin->p && op.lda == pin->ld && M == pin->rows && K == pin->cols) {
+    if (!pin->have_left || pin->s_left != s) {
+      NNB_TRY(split_left(op.A, op.lda, M, K, c, pin->left, st));
+      pin->have_left = true;
+      pin->s_left = s;
+    }
+    L = &pin->left;
+  } else {
+    NNB_TRY(split_left(op.A, op.lda, M, K, c, la, st));
+  }
+  if (pin && !op.b_kmajor && op.B == pin->p && op.ldb == pin->ld && K == pin->rows && N == pin->cols) {
+    if (!pin->have_right || pin->s_right != s) {
+      NNB_TRY(split_right(op.B, op.ldb, K, N, false, c, pin->right, st));
+      pin->have_right = true;
+      pin->s_right = s;
+    }
+    R = &pin->right;
+  } else {
+    NNB_TRY(split_right(op.B, op.ldb, K, N, op.b_kmajor, c, rb, st));
+  }
+  // s int8 GEMMs -> residues
+  const int64_t ldr = (N + 15) / 16 * 16;
+  DevBuf res;
+  NNB_TRY(res.alloc((size_t)s * M * ldr, st));
+  CUtensorMap ta, tb;
+  NNB_TRY(make_tmap_u8(&ta, L->res.p, (int64_t)s * M, L->kp, L->kp, kBM, kBK));
+  NNB_TRY(make_tmap_u8(&tb, R->res.p, (int64_t)s * N, R->kp, R->kp, kBN, kBK));
+  NNB_TRY(ensure_smem<oz_gemm_kernel>(kGemmSmem));
+  const dim3 grid((unsigned)((N + kBN - 1) / kBN), (unsigned)((M + kBM - 1) / kBM), (unsigned)s);
+  oz_gemm_kernel<<<grid, 192, kGemmSmem, st>>>(ta, tb, (int)M, (int)N, (int)K, ldr, res.as<uint8_t>(), c);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  // reconstruction + the chain's epilogue
+  return launch_recon(s, res.as<uint8_t>(), ldr, (int)M, (int)N, L->exps.as<int>(), R->exps.as<int>(), op.ep, c,
+                      st);
+}
+
+int ozaki_moduli_for(int64_t k) { return std::max(15, moduli_for(k)); }
+
+}  // namespace nnb
