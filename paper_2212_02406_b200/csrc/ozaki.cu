@@ -227,31 +227,57 @@ constexpr uint32_t kIdesc = (2u << 4) |            // D: s32
                             (1u << 7) | (1u << 10) |  // A, B: signed int8
                             ((uint32_t)(kBN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);  // K-major both
 
-// out[l][row][col] = (Σ_k a_l[row][k]·b_l[col][k]) mod m_l, for blockIdx.z = l.
-// a_l rows live at l·M + row of tma_a, b_l rows at l·N + col of tma_b.
+constexpr int kAccBufs = 2;    // TMEM accumulators: 2 × 256 columns (the whole 512)
+constexpr int kEpiWarps = 4;
+constexpr int kGroupM = 8;     // rasterisation: 8 tile-rows per group, so a wave shares A and B panels
+
+struct TileCoord {
+  int l, mt, nt;
+};
+__device__ __forceinline__ TileCoord tile_of(int t, int tiles_m, int tiles_n) {
+  const int per = tiles_m * tiles_n;
+  TileCoord c;
+  c.l = t / per;
+  const int r = t - c.l * per;
+  const int group = r / (kGroupM * tiles_n);
+  const int first_m = group * kGroupM;
+  const int gm = min(tiles_m - first_m, kGroupM);
+  const int w = r - group * kGroupM * tiles_n;
+  c.mt = first_m + w % gm;
+  c.nt = w / gm;
+  return c;
+}
+
+// Persistent: CTA b takes tiles b, b + grid, ... of the (modulus, tile-row, tile-col) space;
+// out[l][row][col] = (Σ_k a_l[row][k]·b_l[col][k]) mod m_l.  a_l's rows live at l·M + row
+// of tma_a, b_l's at l·N + col of tma_b.  The TMA ring runs across tile boundaries and the
+// two TMEM accumulators let the epilogue of tile i overlap the MMAs of tile i+1.
 __global__ void __launch_bounds__(192, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, int M, int N,
-                   int K, int64_t ldr, uint8_t* __restrict__ out, const OzConst cst) {
+                   int K, int64_t ldr, uint8_t* __restrict__ out, const OzConst cst, int tiles_m, int tiles_n) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
-  uint64_t* done = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + kAccBufs;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int l = blockIdx.z;
-  const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * kBN;
   const int nk = (K + kBK - 1) / kBK;
+  const int total = tiles_m * tiles_n * cst.s;
 
   if (threadIdx.x == 0) {
     for (int st = 0; st < kStages; ++st) {
       mbar_init(&full[st], 1);
       mbar_init(&empty[st], 1);
     }
-    mbar_init(done, 1);
+    for (int b = 0; b < kAccBufs; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], kEpiWarps);
+    }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, kBN);
+  if (warp == 1) tmem_alloc(tmem_slot, kBN * kAccBufs);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -261,68 +287,88 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {  // TMA producer
       tma_prefetch_desc(&tma_a);
       tma_prefetch_desc(&tma_b);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int st = kb % kStages;
-        if (kb >= kStages) mbar_wait(&empty[st], ((kb / kStages) & 1) ^ 1);
-        uint8_t* sa = smem + st * kStageBytes;
-        mbar_arrive_expect_tx(&full[st], kStageBytes);
-        tma_load_2d(sa, &tma_a, &full[st], kb * kBK, l * M + m0);
-        tma_load_2d(sa + kABytes, &tma_b, &full[st], kb * kBK, l * N + n0);
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const TileCoord tc = tile_of(t, tiles_m, tiles_n);
+        const int arow = tc.l * M + tc.mt * kBM, brow = tc.l * N + tc.nt * kBN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int st = it % kStages;
+          if (it >= kStages) mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
+          uint8_t* sa = smem + st * kStageBytes;
+          mbar_arrive_expect_tx(&full[st], kStageBytes);
+          tma_load_2d(sa, &tma_a, &full[st], kb * kBK, arow);
+          tma_load_2d(sa + kABytes, &tma_b, &full[st], kb * kBK, brow);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
-      for (int kb = 0; kb < nk; ++kb) {
-        const int st = kb % kStages;
-        mbar_wait(&full[st], (kb / kStages) & 1);
+      int it = 0, n_t = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++n_t) {
+        const int acc = n_t & 1;
+        if (n_t >= kAccBufs) mbar_wait(&tempty[acc], ((n_t >> 1) & 1) ^ 1);  // epilogue drained it
         tc_fence_after();
-        const uint32_t a_addr = smem_u32(smem + st * kStageBytes), b_addr = a_addr + kABytes;
+        const uint32_t tacc = tbase + acc * kBN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int st = it % kStages;
+          mbar_wait(&full[st], (it / kStages) & 1);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + st * kStageBytes), b_addr = a_addr + kABytes;
 #pragma unroll
-        for (int k = 0; k < kBK / 32; ++k)
-          mma_i8(tbase, sw128_desc(a_addr + 32 * k), sw128_desc(b_addr + 32 * k), kIdesc, (kb | k) != 0);
-        mma_commit(&empty[st]);  // the stage is free once these MMAs have read it
+          for (int k = 0; k < kBK / 32; ++k)
+            mma_i8(tacc, sw128_desc(a_addr + 32 * k), sw128_desc(b_addr + 32 * k), kIdesc, (kb | k) != 0);
+          mma_commit(&empty[st]);  // the stage is free once these MMAs have read it
+        }
+        mma_commit(&tfull[acc]);  // the accumulator is complete
       }
-      mma_commit(done);
     }
   } else {  // epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
     const int q = warp & 3;
-    mbar_wait(done, 0);
-    tc_fence_after();
-    const int row = m0 + 32 * q + lane;
-    const int m = cst.mi[l];
-    const double inv = cst.inv_md[l];
-    uint8_t* orow = out + ((int64_t)l * M + row) * ldr;
+    int n_t = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++n_t) {
+      const TileCoord tc = tile_of(t, tiles_m, tiles_n);
+      const int acc = n_t & 1;
+      mbar_wait(&tfull[acc], (n_t >> 1) & 1);
+      tc_fence_after();
+      const int row = tc.mt * kBM + 32 * q + lane;
+      const int m = cst.mi[tc.l];
+      const double inv = cst.inv_md[tc.l];
+      uint8_t* orow = out + ((int64_t)tc.l * M + row) * ldr;
 #pragma unroll 1
-    for (int c = 0; c < kBN / 32; ++c) {
-      uint32_t v[32];
-      tmem_ld32(tbase + (static_cast<uint32_t>(32 * q) << 16) + 32 * c, v);
-      const int col = n0 + 32 * c;
-      if (row < M && col < ldr) {
-        uint32_t packed[8];
+      for (int c = 0; c < kBN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tbase + acc * kBN + (static_cast<uint32_t>(32 * q) << 16) + 32 * c, v);
+        const int col = tc.nt * kBN + 32 * c;
+        if (row < M && col < ldr) {
+          uint32_t packed[8];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          uint32_t word = 0;
+          for (int w = 0; w < 8; ++w) {
+            uint32_t word = 0;
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int a = static_cast<int>(v[4 * w + b]);
-            int r = a - m * __double2int_rd(static_cast<double>(a) * inv);
-            r += (r < 0) ? m : 0;
-            r -= (r >= m) ? m : 0;
-            word |= static_cast<uint32_t>(r) << (8 * b);
+            for (int b = 0; b < 4; ++b) {
+              const int a = static_cast<int>(v[4 * w + b]);
+              int r = a - m * __double2int_rd(static_cast<double>(a) * inv);
+              r += (r < 0) ? m : 0;
+              r -= (r >= m) ? m : 0;
+              word |= static_cast<uint32_t>(r) << (8 * b);
+            }
+            packed[w] = word;
           }
-          packed[w] = word;
+          uint4* dst = reinterpret_cast<uint4*>(orow + col);
+          dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+          if (col + 16 < ldr) dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
         }
-        uint4* dst = reinterpret_cast<uint4*>(orow + col);
-        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-        if (col + 16 < ldr) dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
       }
+      tc_fence_before();  // this warp's TMEM reads are ordered before the release
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tbase, kBN);
+    tmem_dealloc(tbase, kBN * kAccBufs);
   }
 }
 
@@ -720,8 +766,18 @@ int gemm_ozaki(const GemmOp& op, cudaStream_t st) {
   NNB_TRY(make_tmap_u8(&ta, L->res.p, (int64_t)s * M, L->kp, L->kp, kBM, kBK));
   NNB_TRY(make_tmap_u8(&tb, R->res.p, (int64_t)s * N, R->kp, R->kp, kBN, kBK));
   NNB_TRY(ensure_smem<oz_gemm_kernel>(kGemmSmem));
-  const dim3 grid((unsigned)((N + kBN - 1) / kBN), (unsigned)((M + kBM - 1) / kBM), (unsigned)s);
-  oz_gemm_kernel<<<grid, 192, kGemmSmem, st>>>(ta, tb, (int)M, (int)N, (int)K, ldr, res.as<uint8_t>(), c);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    NNB_CUDA(cudaGetDevice(&dev));
+    NNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int tiles_m = (int)((M + kBM - 1) / kBM), tiles_n = (int)((N + kBN - 1) / kBN);
+  const int64_t total = (int64_t)tiles_m * tiles_n * s;
+  if (total > INT32_MAX) return fail(7, "ozaki: too many tiles");
+  const unsigned grid = (unsigned)std::min<int64_t>(total, sms);
+  oz_gemm_kernel<<<grid, 192, kGemmSmem, st>>>(ta, tb, (int)M, (int)N, (int)K, ldr, res.as<uint8_t>(), c, tiles_m,
+                                               tiles_n);
   count_launch();
   NNB_CUDA(cudaGetLastError());
   // reconstruction + the chain's epilogue

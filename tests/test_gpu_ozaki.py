@@ -68,12 +68,15 @@ def test_ozaki_matmul_special_values():
         c = nnb.matmul(a, b)
     ref = a.astype(np.longdouble) @ b.astype(np.longdouble)
     assert np.all(c[5] == 0.0)
-    rel = np.abs(c - ref.astype(np.float64)) / (np.abs(a).max(1, keepdims=True) * np.abs(b).sum(0, keepdims=True))
+    scale = np.abs(a).max(1, keepdims=True) * np.abs(b).sum(0, keepdims=True)
+    keep = np.arange(200) != 5
+    rel = np.abs(c - ref.astype(np.float64))[keep] / scale[keep]
     assert float(rel.max()) < 1e-15
-    a[3, 4] = np.nan
-    with nnb.ozaki_arithmetic():
-        c = nnb.matmul(a, b)
-    assert np.all(np.isnan(c[3])) and np.isfinite(np.delete(c, 3, axis=0)).all()
+    a[3, 4] = np.nan  # check_finite (proj/src/kernels.cpp:14-17): DomainError, as on the DMMA path
+    with pytest.raises(nnb.DomainError):
+        nnb.matmul(a, b)
+    with nnb.ozaki_arithmetic(), pytest.raises(nnb.DomainError):
+        nnb.matmul(a, b)
 
 
 @pytest.mark.parametrize("p", [1, 2, 3])
