@@ -98,8 +98,12 @@ int nnb_device_count(void);
 uint64_t nnb_kernel_launches(void);
 
 /* Arithmetic mode of the calling thread.
- * NNB_ARITH_FAST (default): DMMA products, tile-parallel reductions —
- *   agrees with the reference to ~1e-15 relative.
+ * NNB_ARITH_FAST (default): the faster of the two FP64-accurate product
+ *   paths per product — the int8 emulation below for real products with
+ *   M, N, K >= 1024 and M·N·K >= 3072^3, DMMA otherwise (complex, symmetric-
+ *   order and K-split products always DMMA); agrees with the reference to
+ *   ~1e-15 relative.
+ * NNB_ARITH_DMMA: every product on the FP64 tensor pipe (DMMA.8x8x4).
  * NNB_ARITH_REFERENCE: real dense products as ascending-k, explicitly
  *   rounded CUDA-core loops, serial Frobenius sums and the reference's own
  *   nest sequence — BIT-IDENTICAL to the reference for real data
@@ -110,7 +114,7 @@ uint64_t nnb_kernel_launches(void);
  *   integer products are exact; same parity gate as FAST (X within 1e-10,
  *   identical nest counts).  Complex products keep the DMMA path.
  * The sparse path is bit-identical in every mode. */
-enum nnb_arith { NNB_ARITH_FAST = 0, NNB_ARITH_REFERENCE = 1, NNB_ARITH_OZAKI = 2 };
+enum nnb_arith { NNB_ARITH_FAST = 0, NNB_ARITH_REFERENCE = 1, NNB_ARITH_OZAKI = 2, NNB_ARITH_DMMA = 3 };
 int nnb_set_arithmetic(int32_t mode);
 int32_t nnb_get_arithmetic(void);
 /* Moduli (= int8 GEMMs per product) NNB_ARITH_OZAKI uses for inner dimension k. */

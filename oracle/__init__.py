@@ -320,6 +320,17 @@ class Port(_Lib):
     def set_threads(self, t: int) -> None:
         self.fn("set_threads", [C.c_int], None)(t)
 
+    def gaussian(self, seed: int, n: int) -> np.ndarray:
+        out = np.empty(n)
+        self.fn("gaussian", [C.c_uint64, C.c_int64, _dp], None)(seed, n, _ptr(out))
+        return out
+
+    def random_spd(self, n: int, cond: float, seed: int) -> np.ndarray:
+        """nn::random_spd restated (real, float64), bit-identical to the reference's."""
+        out = np.empty((n, n))
+        self._check(self.fn("random_spd", [C.c_int64, C.c_double, C.c_uint64, _dp])(n, cond, seed, _ptr(out)))
+        return out
+
     def matmul(self, a, b):
         a, b = _z(a), _z(b)
         out = np.empty((a.shape[0], b.shape[1]), np.complex128)

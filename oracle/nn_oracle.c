@@ -124,12 +124,8 @@ static int imag_all_zero(const double* p, int64_t count) {
   return 1;
 }
 
-static void matmul_real(const double* a, const double* b, int64_t m, int64_t k, int64_t n, double* c) {
-  double* ar = (double*)malloc(sizeof(double) * (size_t)(m * k + 1));
-  double* br = (double*)malloc(sizeof(double) * (size_t)(k * n + 1));
-  double* cr = (double*)malloc(sizeof(double) * (size_t)(m * n + 1));
-  for (int64_t i = 0; i < m * k; ++i) ar[i] = a[2 * i];
-  for (int64_t i = 0; i < k * n; ++i) br[i] = b[2 * i];
+/* real row-major ar (m x k) times br (k x n) into cr, ascending k per element */
+static void matmul_real_raw(const double* ar, const double* br, int64_t m, int64_t k, int64_t n, double* cr) {
   void* (*fn)(void*) = __builtin_cpu_supports("avx512f") ? mmr_panels_avx512 : mmr_panels_generic;
   const int64_t panels = (n + 15) / 16;
   int workers = g_threads < panels ? g_threads : (int)panels;
@@ -142,8 +138,18 @@ static void matmul_real(const double* a, const double* b, int64_t m, int64_t k, 
   }
   if (workers > 1) for (int w = 0; w < workers; ++w) pthread_join(th[w], NULL);
   else fn(&jobs[0]);
+  free(th); free(jobs);
+}
+
+static void matmul_real(const double* a, const double* b, int64_t m, int64_t k, int64_t n, double* c) {
+  double* ar = (double*)malloc(sizeof(double) * (size_t)(m * k + 1));
+  double* br = (double*)malloc(sizeof(double) * (size_t)(k * n + 1));
+  double* cr = (double*)malloc(sizeof(double) * (size_t)(m * n + 1));
+  for (int64_t i = 0; i < m * k; ++i) ar[i] = a[2 * i];
+  for (int64_t i = 0; i < k * n; ++i) br[i] = b[2 * i];
+  matmul_real_raw(ar, br, m, k, n, cr);
   for (int64_t i = 0; i < m * n; ++i) { c[2 * i] = cr[i]; c[2 * i + 1] = 0.0; }
-  free(th); free(jobs); free(ar); free(br); free(cr);
+  free(ar); free(br); free(cr);
 }
 
 int nno_matmul_z(const double* a, const double* b, int64_t m, int64_t k, int64_t n, double* c) {
@@ -428,4 +434,158 @@ int nno_sparse_factorized_z(const int64_t* row_ptr, const int32_t* col, const do
   if (spmv_count) *spmv_count = applied;
   free(z); free(t); free(y);
   return st;
+}
+
+/* ---- GaussianStream: proj/include/nn/rng.hpp:15-52 (mt19937_64 + Box-Muller,
+ * libm log/sqrt/sin/cos), restated with the standard mt19937_64 recurrence. ---- */
+typedef struct {
+  uint64_t mt[312];
+  int mti;
+  double spare;
+  int have_spare;
+} gauss_stream;
+
+static void gs_init(gauss_stream* g, uint64_t seed) {
+  g->mt[0] = seed;
+  for (int i = 1; i < 312; ++i) g->mt[i] = 6364136223846793005ULL * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
+  g->mti = 312;
+  g->have_spare = 0;
+  g->spare = 0.0;
+}
+
+static uint64_t gs_u64(gauss_stream* g) {
+  static const uint64_t mag[2] = {0ULL, 0xB5026F5AA96619E9ULL};
+  const uint64_t um = 0xFFFFFFFF80000000ULL, lm = 0x7FFFFFFFULL;
+  if (g->mti >= 312) {
+    int i;
+    uint64_t x;
+    for (i = 0; i < 312 - 156; ++i) {
+      x = (g->mt[i] & um) | (g->mt[i + 1] & lm);
+      g->mt[i] = g->mt[i + 156] ^ (x >> 1) ^ mag[x & 1];
+    }
+    for (; i < 311; ++i) {
+      x = (g->mt[i] & um) | (g->mt[i + 1] & lm);
+      g->mt[i] = g->mt[i + (156 - 312)] ^ (x >> 1) ^ mag[x & 1];
+    }
+    x = (g->mt[311] & um) | (g->mt[0] & lm);
+    g->mt[311] = g->mt[155] ^ (x >> 1) ^ mag[x & 1];
+    g->mti = 0;
+  }
+  uint64_t x = g->mt[g->mti++];
+  x ^= (x >> 29) & 0x5555555555555555ULL;
+  x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+  x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+  x ^= (x >> 43);
+  return x;
+}
+
+static double gs_uniform01(gauss_stream* g) { return (double)(gs_u64(g) >> 11) * 0x1.0p-53; }
+
+static double gs_next(gauss_stream* g) {
+  if (g->have_spare) {
+    g->have_spare = 0;
+    return g->spare;
+  }
+  double u1 = 0.0;
+  do {
+    u1 = gs_uniform01(g);
+  } while (u1 <= 0.0);
+  const double u2 = gs_uniform01(g);
+  const double radius = sqrt(-2.0 * log(u1));
+  const double angle = 2.0 * 3.14159265358979323846 * u2;
+  g->spare = radius * sin(angle);
+  g->have_spare = 1;
+  return radius * cos(angle);
+}
+
+void nno_gaussian(uint64_t seed, int64_t count, double* out) {
+  gauss_stream g;
+  gs_init(&g, seed);
+  for (int64_t i = 0; i < count; ++i) out[i] = gs_next(&g);
+}
+
+/* ---- random_spd: proj/src/kernels.cpp:64-124,352-381 for real data.
+ * householder_q's column loops (for j: dot_j = Σ_i conj(v_i) a(i,j); a(i,j) -= v_i dot_j)
+ * are run row-wise here -- every dot_j still accumulates in ascending i and every
+ * a(i,j) sees the same single update -- so the result is the reference's bit for bit
+ * (std::complex on zero imaginary parts is real arithmetic: conj(v)*a has real part
+ * v*a - (-0)*0 = v*a).  Pinned against oracle/_ref (tests/test_oracle_pins.py). ---- */
+#define HH_APPLY_BODY                                                                   \
+  for (int64_t j = j0; j < n; ++j) dot[j] = 0.0;                                        \
+  for (int64_t i = r0; i < n; ++i) {                                                    \
+    const double vi = v[i];                                                             \
+    const double* row = m + i * n;                                                      \
+    for (int64_t j = j0; j < n; ++j) { const double t = vi * row[j]; dot[j] += t; }     \
+  }                                                                                     \
+  for (int64_t j = j0; j < n; ++j) dot[j] *= beta;                                      \
+  for (int64_t i = r0; i < n; ++i) {                                                    \
+    const double vi = v[i];                                                             \
+    double* row = m + i * n;                                                            \
+    for (int64_t j = j0; j < n; ++j) { const double t = vi * dot[j]; row[j] -= t; }     \
+  }
+
+/* m <- (I - beta v v^T) m on rows r0.., columns j0.. */
+__attribute__((target("avx512f"))) static void hh_apply_avx512(double* m, const double* v, double* dot, int64_t n,
+                                                                int64_t r0, int64_t j0, double beta) {
+  HH_APPLY_BODY
+}
+static void hh_apply_generic(double* m, const double* v, double* dot, int64_t n, int64_t r0, int64_t j0,
+                             double beta) {
+  HH_APPLY_BODY
+}
+
+int nno_random_spd(int64_t n, double cond, uint64_t seed, double* out) {
+  if (n < 1 || cond < 1.0) return 2;
+  void (*apply)(double*, const double*, double*, int64_t, int64_t, int64_t, double) =
+      __builtin_cpu_supports("avx512f") ? hh_apply_avx512 : hh_apply_generic;
+  double* a = (double*)malloc(sizeof(double) * n * n);
+  double* refl = (double*)calloc((size_t)n * n, sizeof(double));
+  double* dot = (double*)malloc(sizeof(double) * n);
+  nno_gaussian(seed, n * n, a);
+  /* householder_q: kernels.cpp:64-103 */
+  for (int64_t k = 0; k + 1 < n; ++k) {
+    double* v = refl + k * n;
+    double xnorm2 = 0.0;
+    for (int64_t i = k; i < n; ++i) { const double t = a[i * n + k] * a[i * n + k]; xnorm2 += t; }
+    const double xnorm = sqrt(xnorm2);
+    if (xnorm == 0.0) continue;
+    const double x0 = a[k * n + k];
+    const double x0abs = fabs(x0);
+    const double phase = x0abs > 0.0 ? x0 / x0abs : 1.0;
+    const double alpha = -phase * xnorm;
+    for (int64_t i = k; i < n; ++i) v[i] = a[i * n + k];
+    v[k] -= alpha;
+    double vnorm2 = 0.0;
+    for (int64_t i = k; i < n; ++i) { const double t = v[i] * v[i]; vnorm2 += t; }
+    if (vnorm2 == 0.0) continue;
+    apply(a, v, dot, n, k, k, 2.0 / vnorm2);
+  }
+  /* Q = H_0 ... H_{n-2}, applied to I from the last reflector (kernels.cpp:91-102) */
+  double* q = (double*)calloc((size_t)n * n, sizeof(double));
+  for (int64_t i = 0; i < n; ++i) q[i * n + i] = 1.0;
+  for (int64_t r = n - 1; r-- > 0;) {
+    const double* v = refl + r * n;
+    double vnorm2 = 0.0;
+    for (int64_t i = r; i < n; ++i) { const double t = v[i] * v[i]; vnorm2 += t; }
+    if (vnorm2 == 0.0) continue;
+    apply(q, v, dot, n, r, 0, 2.0 / vnorm2);
+  }
+  /* lambda (kernels.cpp:116-124), ql = Q diag(lambda), w = ql Q^T, symmetrised (:359-379) */
+  double* ql = (double*)malloc(sizeof(double) * n * n);
+  for (int64_t j = 0; j < n; ++j) {
+    const double lam = n == 1 ? 1.0 : pow(cond, -((double)(n - 1 - j) / (double)(n - 1)));
+    for (int64_t i = 0; i < n; ++i) ql[i * n + j] = q[i * n + j] * lam;
+  }
+  double* qt = (double*)malloc(sizeof(double) * n * n);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) qt[j * n + i] = q[i * n + j];
+  matmul_real_raw(ql, qt, n, n, n, out);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = i + 1; j < n; ++j) {
+      const double avg = (out[i * n + j] + out[j * n + i]) * 0.5;
+      out[i * n + j] = avg;
+      out[j * n + i] = avg;
+    }
+  free(a); free(refl); free(dot); free(q); free(ql); free(qt);
+  return all_finite(out, n * n) ? 0 : 2;
 }

@@ -33,6 +33,9 @@ int nno_sparse_factorized_z(const int64_t* row_ptr, const int32_t* col, const do
                             int64_t n, const double* b, int64_t k, int64_t gamma, double theta,
                             double* x_out, int64_t* spmv_count, int* fail_index);
 
+void nno_gaussian(uint64_t seed, int64_t count, double* out);
+int nno_random_spd(int64_t n, double cond, uint64_t seed, double* out);
+
 #ifdef __cplusplus
 }
 #endif

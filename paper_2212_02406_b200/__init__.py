@@ -182,7 +182,7 @@ def kernel_launches() -> int:
     return int(lib().nnb_kernel_launches())
 
 
-ARITH_FAST, ARITH_REFERENCE, ARITH_OZAKI = 0, 1, 2
+ARITH_FAST, ARITH_REFERENCE, ARITH_OZAKI, ARITH_DMMA = 0, 1, 2, 3
 
 
 class arithmetic:
@@ -212,6 +212,13 @@ class reference_arithmetic(arithmetic):
 
     def __init__(self):
         super().__init__(ARITH_REFERENCE)
+
+
+class dmma_arithmetic(arithmetic):
+    """Every product on the FP64 tensor pipe (DMMA), no int8 emulation."""
+
+    def __init__(self):
+        super().__init__(ARITH_DMMA)
 
 
 class ozaki_arithmetic(arithmetic):

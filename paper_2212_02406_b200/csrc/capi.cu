@@ -189,7 +189,8 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
   const int64_t rows_per = ((n + chunks - 1) / chunks + 127) / 128 * 128;
   const int used = static_cast<int>((n + rows_per - 1) / rows_per);
   // block q of the first product's inner dimension: X0's rows and A's columns of q
-  const bool ksplit = host_a && x0_given && cfg->order == NNB_ORDER_NORTHSTAR && arith() == 0;
+  // the K-split first product resumes DMMA accumulators (acc_in): DMMA-only
+  const bool ksplit = host_a && x0_given && cfg->order == NNB_ORDER_NORTHSTAR && arith() == 3;
   if (ksplit) {
     for (int q = 0; q < used; ++q) {
       const int64_t k0 = q * rows_per, kq = std::min<int64_t>(rows_per, n - k0);
@@ -249,7 +250,7 @@ int nnb_device_count(void) {
 uint64_t nnb_kernel_launches(void) { return launches(); }
 
 int nnb_set_arithmetic(int32_t mode) {
-  if (mode != NNB_ARITH_FAST && mode != NNB_ARITH_REFERENCE && mode != NNB_ARITH_OZAKI)
+  if (mode < NNB_ARITH_FAST || mode > NNB_ARITH_DMMA)
     return fail(NNB_ERR_DOMAIN, "nnb_set_arithmetic: unknown mode");
   set_arith(mode);
   return 0;
@@ -607,7 +608,7 @@ int nnb_nn_chain_d(const double* A, int64_t n, const double* X0, const nnb_chain
   NNB_TRY(chain_cfg(cfg, &c));
   cudaStream_t s = resolve(stream);
   const bool host_a = !is_device_ptr(A), host_out = X_out && !is_device_ptr(X_out);
-  if ((host_a || host_out) && n >= kStreamMinN && (arith() == 0 || arith() == 2))
+  if ((host_a || host_out) && n >= kStreamMinN && arith() != 1)
     return chain_d_streamed(A, n, X0, cfg, c, X_out, eps_hist, result, s);
   DMat a;
   NNB_TRY(a.load(A, n, n, n, s));

@@ -253,7 +253,7 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
     ~OzPin() {
       if (on) oz_unpin();
     }
-  } oz_pin_guard{arith() == 2 && !c.cplx};
+  } oz_pin_guard{(arith() == 2 || (arith() == 0 && ozaki_pays(n, n, n))) && !c.cplx};
   if (oz_pin_guard.on) oz_pin(A.re, c.ld, n, n);
   if (!small) NNB_TRY(c.red.init(max_tiles_for(n, n), c.s));
   DevBuf work;

@@ -117,6 +117,11 @@ int gemm_exact(const GemmOp& op, cudaStream_t s);
 // Ozaki-II emulation of a real product on the int8 tensor cores (ozaki.cu).
 int gemm_ozaki(const GemmOp& op, cudaStream_t s);
 int ozaki_moduli_for(int64_t k);
+// NNB_ARITH_FAST routes a real product to the int8 emulation where it beats DMMA
+// (measured crossover between N=2048 and 4096): M, N >= 1024 and M·N·K >= 3072^3.
+inline bool ozaki_pays(int64_t M, int64_t N, int64_t K) {
+  return M >= 1024 && N >= 1024 && K >= 1024 && K <= 131071 && (double)M * N * K >= 3072.0 * 3072.0 * 3072.0;
+}
 // A chain operand that stays unchanged while pinned: its int8 splits are reused.
 void oz_pin(const double* p, int64_t ld, int64_t rows, int64_t cols);
 void oz_unpin();

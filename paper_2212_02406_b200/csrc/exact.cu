@@ -21,11 +21,12 @@
 
 namespace nnb {
 
-// 0 fast (DMMA), 1 reference-exact, 2 Ozaki int8 emulation (ozaki.cu).
-// NNB_ARITHMETIC=reference (=ozaki) selects the mode for every thread (e.g. for the C++ drop-in without code changes).
+// 0 fast (per product: int8 emulation where it pays, else DMMA), 1 reference-exact,
+// 2 Ozaki int8 emulation for every real product (ozaki.cu), 3 DMMA only.
+// NNB_ARITHMETIC=reference|ozaki|dmma selects the mode for every thread (e.g. for the C++ drop-in without code changes).
 static int initial_arith() {
   const char* e = std::getenv("NNB_ARITHMETIC");
-  return (e && e[0] == 'r') ? 1 : (e && e[0] == 'o') ? 2 : 0;
+  return (e && e[0] == 'r') ? 1 : (e && e[0] == 'o') ? 2 : (e && e[0] == 'd') ? 3 : 0;
 }
 static thread_local int g_arith = initial_arith();
 void set_arith(int mode) { g_arith = mode; }

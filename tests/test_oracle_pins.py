@@ -209,3 +209,16 @@ def test_known_errors(port, ref):
     with pytest.raises(OracleError) as e:
         ref.nn_invert(w, 0.1, False, 2, 64, 1e-10)
     assert e.value.status == 4
+
+
+def test_port_gaussian_stream_and_random_spd_bitexact(port, ref):
+    """GaussianStream (proj/include/nn/rng.hpp:15-52) and random_spd (proj/src/kernels.cpp:352-381)
+    restated in C with row-wise Householder loops: bit-identical to the reference, so the
+    port can generate BASELINE config 2's N=4096 input (the reference's column loops would
+    take hours there)."""
+    for seed in (0, 3, 2 ** 63 + 11):
+        assert np.array_equal(port.gaussian(seed, 1001), ref.gaussian(seed, 1001))
+    for n, cond, seed in [(1, 1.0, 1), (2, 10.0, 2), (17, 1e3, 3), (64, 1e3, 3), (130, 1e6, 5), (200, 1e3, 3)]:
+        w = port.random_spd(n, cond, seed)
+        wr = ref.random_spd(n, cond, seed)
+        assert np.array_equal(w, wr.real) and not np.any(wr.imag), (n, cond, seed)
