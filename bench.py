@@ -40,10 +40,20 @@ try:
 except Exception:
     pass
 HBM_PEAK = PEAKS.get("hbm_gbs", 6650.0)
-# FP64 tensor (DMMA) peak measured on this pool by tools/microbench/fp64_peak.cu
-# (profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json carries no FP64 entry.
-FP64_PEAK_TFLOPS = 37.2
+# Peaks MEASURED_PEAKS.json does not carry, measured on this pool and committed:
+# profiles/r02_int8_peak.json (tools/microbench/int8_peak.py: cuBLAS int8 GEMM burst and
+# sustained under the power cap; its fp64 entry is the DMMA.8x8x4 microbenchmark of
+# tools/microbench/fp64_peak.cu, profiles/r01_fp64_peak.txt).
+try:
+    EXTRA_PEAKS = json.loads((ROOT / "profiles" / "r02_int8_peak.json").read_text())
+except Exception:
+    EXTRA_PEAKS = {}
+FP64_PEAK_TFLOPS = EXTRA_PEAKS.get("fp64_dmma_tflops", 37.2)
 FP64_PEAK_SOURCE = "measured DMMA.8x8x4 microbenchmark, profiles/r01_fp64_peak.txt"
+INT8_PEAK_TOPS = EXTRA_PEAKS.get("int8_tops_sustained", 2.0 * PEAKS.get("bf16_tflops_sustained", 1388.0))
+INT8_PEAK_SOURCE = ("measured cuBLAS int8 GEMM (torch._int_mm 8192^3) sustained under the power cap, "
+                    "profiles/r02_int8_peak.json" if "int8_tops_sustained" in EXTRA_PEAKS else
+                    "fallback: 2 x MEASURED_PEAKS bf16_tflops_sustained")
 # DRAM traffic per launch of each dominant kernel from the committed ncu --set full captures
 try:
     NCU_TRAFFIC = json.loads((ROOT / "profiles" / "r01_ncu_traffic.json").read_text())
@@ -227,6 +237,8 @@ def run_dense(args, world, rank):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     lib_ms = []
     eps = []
+    nnb.ozaki_stats(reset=True)
+    nnb.ozaki_profile(True)  # CUDA events around each emulation kernel (the live roofline)
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
         torch.cuda.synchronize()
         e0.record()
@@ -236,29 +248,67 @@ def run_dense(args, world, rank):
             eps.append(rep.history[0][1])
         e1.record()
         torch.cuda.synchronize()
+    nnb.ozaki_profile(False)
+    oz = nnb.ozaki_stats(reset=True)
     launches = nnb.kernel_launches() - l0
     ms = max_over_ranks(world, e0.elapsed_time(e1))
     barrier(world)
     ms_step = ms / args.steps
     value = flops_step * args.steps / (ms * 1e-3) / 1e12  # whole job: one N^3 nest per step
-    # dominant kernel: the fused DMMA GEMM — the library's device time of a nest is its
-    # (p+1) GEMM launches (per rank: its row share of each product)
     dev_ms = statistics.mean(lib_ms)
-    achieved = flops_step / world / (dev_ms * 1e-3) / 1e12
     rows_here = nnb.partition_rows(n, world, rank)[1] if world > 1 else n
+    g = oz["gemm"]
+    if g["launches"]:
+        # dominant kernel: the int8 GEMM of the FP64 emulation (csrc/ozaki.cu), timed live with
+        # CUDA events on its stream; work = s moduli x 2*M*N*K int8 ops per launch
+        achieved = g["work"] / (g["ms"] * 1e-3) / 1e12
+        per_launch = g["work"] / g["launches"]
+        moduli = nnb.ozaki_moduli(n)
+        roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": INT8_PEAK_TOPS, "unit": "TFLOP/s",
+                "frac": round(achieved / INT8_PEAK_TOPS, 4),
+                "traffic": ncu_traffic("oz_gemm_n32768") if n == 32768 and world == 1 else None,
+                "kernel": "oz_gemm_kernel (tcgen05.mma kind::i8 M128 N256 K32, TMEM accumulators x2, 4-stage TMA "
+                          "ring, persistent, grouped raster)",
+                "unit_note": "int8 tensor ops/s (TOP/s); the FP64-equivalent rate is `value`",
+                "per_launch": f"{moduli} moduli x 2*rows*N^2 = {per_launch:.4g} int8 ops (rows={rows_here}, N={n}); "
+                              f"{g['launches']} launches, {g['ms'] / g['launches']:.2f} ms mean",
+                "share_of_step": round(g["ms"] / (ms / world if world == 1 else dev_ms * args.steps), 4),
+                "peak_source": INT8_PEAK_SOURCE,
+                "other_kernels": {k: {"ms_per_launch": round(v["ms"] / v["launches"], 3),
+                                      "gbs": round(v["work"] / (v["ms"] * 1e-3) / 1e9, 1),
+                                      "frac_hbm": round(v["work"] / (v["ms"] * 1e-3) / 1e9 / HBM_PEAK, 3)}
+                                  for k, v in oz.items() if k != "gemm" and v["launches"]},
+                "fp64_equivalent": {"achieved": round(flops_step / world / (dev_ms * 1e-3) / 1e12, 3),
+                                    "dmma_peak": FP64_PEAK_TFLOPS,
+                                    "ratio_to_dmma_peak": round(flops_step / world / (dev_ms * 1e-3) / 1e12
+                                                                / FP64_PEAK_TFLOPS, 3)}}
+    else:
+        # DMMA path: the fused FP64 GEMM — the library's device time of a nest is its
+        # (p+1) GEMM launches (per rank: its row share of each product)
+        achieved = flops_step / world / (dev_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
+                "traffic": ncu_traffic("dense_gemm_n32768") if n == 32768 and world == 1 else None,
+                "kernel": "gemm_f64_kernel<128x128x16, 2x4 warps, 4 stages> (DMMA.8x8x4 + TMA)",
+                "per_launch": f"2*rows*N^2 = {2.0 * rows_here * n * n:.4g} flop (rows={rows_here}, N={n}), "
+                              f"{p + 1} launches per nest" + (f" x {world} K-split partials" if world > 1 else ""),
+                "peak_source": FP64_PEAK_SOURCE}
     out = dict(value=value, ms_per_step=ms_step, launches=launches, clocks=clk.summary(),
-               eps_first=eps[0], eps_last=eps[-1],
-               roofline={"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS,
-                         "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
-                         "traffic": ncu_traffic("dense_gemm_n32768") if n == 32768 and world == 1 else None,
-                         "traffic_note": "bytes/launch from profiles/r01_ncu_traffic.json (N=32768). Algorithmic "
-                                         "3*8*N^2 = 25.8 GB; the excess is L2-capacity re-reads of K=32768 operand "
-                                         "strips at 7% DRAM utilisation - even with no L2 reuse a 128x128 tile "
-                                         "needs 2*N^3/16 B = 4.4 TB (2.3 TB/s), so the kernel stays DMMA-bound",
-                         "kernel": "gemm_f64_kernel<128x128x16, 2x4 warps, 4 stages> (DMMA.8x8x4 + TMA)",
-                         "per_launch": f"2*rows*N^2 = {2.0 * rows_here * n * n:.4g} flop (rows={rows_here}, N={n}), "
-                                       f"{p + 1} launches per nest" + (f" x {world} K-split partials" if world > 1 else ""),
-                         "peak_source": FP64_PEAK_SOURCE})
+               eps_first=eps[0], eps_last=eps[-1], roofline=roof)
+    # the same nest with every product on the FP64 tensor pipe (DMMA), for comparison
+    if not sharded and args.dmma:
+        with nnb.dmma_arithmetic():
+            nnb.nn_chain(a, x, p=p, max_iters=1, final_residual=False)  # warm
+            torch.cuda.synchronize()
+            xd, rd = nnb.nn_chain(a, x, p=p, max_iters=1, final_residual=False)
+            torch.cuda.synchronize()
+        out["dmma"] = {"arithmetic": "NNB_ARITH_DMMA (every product on DMMA.8x8x4)",
+                       "ms_per_nest": round(rd.device_ms, 2),
+                       "tflops": round(flops_step / (rd.device_ms * 1e-3) / 1e12, 3),
+                       "frac_of_dmma_peak": round(flops_step / (rd.device_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
+                       "eps_before_nest": rd.history[0][1],
+                       "x_rel_frob_vs_headline_nest": float(torch.linalg.norm(xd - step(x)[0]) / torch.linalg.norm(xd))}
+        del xd
     # NNB_ORDER_SYMMETRIC on the same nest (A == A^T, X a polynomial in A): upper
     # tile triangles, mirrored — time per nest, reported beside the headline
     if not sharded and args.symmetric:
@@ -696,6 +746,8 @@ def main():
     ap.add_argument("--no-symmetric", dest="symmetric", action="store_false",
                     help="skip the NNB_ORDER_SYMMETRIC timing beside the headline nest")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    ap.add_argument("--no-dmma", dest="dmma", action="store_false",
+                    help="skip the DMMA-only timing of the headline nest")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU (sharded) dense/sparse paths even at one rank (code-path check)")
     args = ap.parse_args()
@@ -716,7 +768,11 @@ def main():
               "host_cpu": f"{cores} x {model}"}
     base = {"metric": "NN inversion FP64 TFLOP/s", "unit": "TFLOP/s", "n_gpus": world if args.impl == "ours" else args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (seeded)", "config": config}
+            "dtype": "f64", "data": "synthetic (seeded)", "config": config,
+            "arithmetic": "NNB_ARITH_FAST: each real N^3 product (N >= 3072) runs as an FP64-accurate emulation on "
+                          "the int8 tensor cores (Ozaki scheme II: 53-bit row/column-scaled integers, 16 moduli, "
+                          "exact int32 accumulation, Garner reconstruction; csrc/ozaki.cu) - same parity gate as "
+                          "DMMA (X within 1e-10, identical nest counts); smaller/complex products on DMMA"}
     if world > 1:
         base["scaling"] = "strong"  # the N=32768 matrix is fixed; ranks split its rows
 

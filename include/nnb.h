@@ -117,8 +117,19 @@ uint64_t nnb_kernel_launches(void);
 enum nnb_arith { NNB_ARITH_FAST = 0, NNB_ARITH_REFERENCE = 1, NNB_ARITH_OZAKI = 2, NNB_ARITH_DMMA = 3 };
 int nnb_set_arithmetic(int32_t mode);
 int32_t nnb_get_arithmetic(void);
+/* The next real nnb_nn_chain_d of the calling thread (with final_residual = 1) copies
+ * its final residual R = I − A·X — the product eps_last is computed from — into the
+ * device buffer R_out (n×n, leading dimension ldr).  A test hook for sampling the
+ * chain's own R at sizes no CPU oracle reaches (SURVEY §8(c) C4 item iii). */
+int nnb_chain_capture_residual(double* R_out, int64_t ldr);
 /* Moduli (= int8 GEMMs per product) NNB_ARITH_OZAKI uses for inner dimension k. */
 int32_t nnb_ozaki_moduli(int64_t k);
+/* Live timing of the emulation's kernels (for roofline reporting): while on, every
+ * int8 GEMM / operand split / reconstruction launch is bracketed by CUDA events on its
+ * stream.  nnb_ozaki_stats fills ms[3], work[3] (int8 ops; algorithmic bytes; bytes)
+ * and launches[3] for the three classes, synchronising the recorded events. */
+void nnb_ozaki_profile(int32_t on);
+void nnb_ozaki_stats(double* ms, double* work, int64_t* launches, int32_t reset);
 
 /* ---- dense kernels ------------------------------------------------------ */
 /* C = A·B.  Replaces nn::matmul (proj/include/nn/kernels.hpp:20-21,

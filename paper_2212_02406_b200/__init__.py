@@ -93,6 +93,9 @@ _SIGS = {
     "nnb_set_arithmetic": ([_i32], C.c_int),
     "nnb_get_arithmetic": ([], C.c_int32),
     "nnb_ozaki_moduli": ([_i64], C.c_int32),
+    "nnb_chain_capture_residual": ([C.c_void_p, _i64], C.c_int),
+    "nnb_ozaki_profile": ([_i32], None),
+    "nnb_ozaki_stats": ([C.c_void_p, C.c_void_p, C.c_void_p, _i32], None),
     "nnb_gemm_d": ([_dp, _i64, _dp, _i64, _dp, _i64, _i64, _i64, _i64, _dp], C.c_int),
     "nnb_gemm_z": ([_dp, _dp, _dp, _i64, _i64, _i64, _dp], C.c_int),
     "nnb_gemm_nt_d": ([_dp, _i64, _dp, _i64, _dp, _i64, _i64, _i64, _i64, _dp], C.c_int),
@@ -204,6 +207,20 @@ class arithmetic:
 def ozaki_moduli(k: int) -> int:
     """Moduli the int8 emulation uses for inner dimension k (each is one int8 GEMM)."""
     return int(lib().nnb_ozaki_moduli(int(k)))
+
+
+def ozaki_profile(on: bool) -> None:
+    lib().nnb_ozaki_profile(1 if on else 0)
+
+
+def ozaki_stats(reset: bool = True) -> dict:
+    """Summed device time (CUDA events), work and launch count of the emulation's kernels
+    recorded while ozaki_profile(True): classes gemm (int8 ops), split and recon (bytes)."""
+    ms, work = (C.c_double * 3)(), (C.c_double * 3)()
+    n = (C.c_int64 * 3)()
+    lib().nnb_ozaki_stats(C.addressof(ms), C.addressof(work), C.addressof(n), 1 if reset else 0)
+    return {name: {"ms": ms[i], "work": work[i], "launches": n[i]}
+            for i, name in enumerate(("gemm", "split", "recon"))}
 
 
 class reference_arithmetic(arithmetic):
@@ -523,12 +540,16 @@ class ChainReport:
 
 
 def nn_chain(a, x0=None, *, p: int, max_iters: int, tol: float = 0.0, order: int = ORDER_NORTHSTAR,
-             x0_kind: Optional[int] = None, x0_scale: float = 1.0, final_residual: bool = True, out=None):
+             x0_kind: Optional[int] = None, x0_scale: float = 1.0, final_residual: bool = True, out=None,
+             residual_out=None):
     """Nested Neumann chain from X0; returns (X, ChainReport).
 
     eps is recorded before every nest and after the last one; stops when
-    eps < tol (tol > 0) or after max_iters nests.
+    eps < tol (tol > 0) or after max_iters nests.  residual_out (a device n×n float64
+    tensor, real chains) receives the chain's own final residual R = I − A·X.
     """
+    if residual_out is not None:
+        _check(lib().nnb_chain_capture_residual(_ptr(residual_out), residual_out.shape[1]))
     n = a.shape[0]
     if a.shape != (n, n):
         raise ShapeError("nn chain: matrix must be square")

@@ -257,6 +257,15 @@ int nnb_set_arithmetic(int32_t mode) {
 }
 int32_t nnb_get_arithmetic(void) { return arith(); }
 int32_t nnb_ozaki_moduli(int64_t k) { return ozaki_moduli_for(k); }
+int nnb_chain_capture_residual(double* R_out, int64_t ldr) {
+  if (R_out && !is_device_ptr(R_out)) return fail(NNB_ERR_DOMAIN, "residual capture needs a device buffer");
+  set_chain_capture(R_out, ldr);
+  return 0;
+}
+void nnb_ozaki_profile(int32_t on) { ozaki_profile(on); }
+void nnb_ozaki_stats(double* ms, double* work, int64_t* launches, int32_t reset) {
+  ozaki_stats(ms, work, launches, reset);
+}
 
 // ---------------------------------------------------------------- dense kernels
 int nnb_gemm_d(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,

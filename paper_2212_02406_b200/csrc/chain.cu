@@ -233,8 +233,16 @@ int product_ksplit(Ctx& c, const Plane& A, const Plane& B, double alpha, double 
   return 0;
 }
 
+// nnb_chain_capture_residual: the next real chain of this thread copies its final
+// residual R = I − A·X (the last residual product, the one eps_last is taken from) here.
+thread_local double* g_capture_r = nullptr;
+thread_local int64_t g_capture_ld = 0;
+
 int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_hist,
               ChainOut* out, ChainIo* io = nullptr) {
+  double* capture = c.cplx ? nullptr : g_capture_r;
+  const int64_t capture_ld = g_capture_ld;
+  g_capture_r = nullptr;
   const int64_t n = c.n, mat = n * c.ld;
   const int planes = c.cplx ? 2 : 1;
   const int p = cfg.p;
@@ -245,7 +253,7 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
   // reference-exact mode (real data): the reference's operand order and nest sequence
   const bool exact = arith() == 1 && !c.cplx;
   // small real N: the whole loop in one cooperative kernel (chain_small.cu)
-  const bool small = !c.cplx && !exact && arith() != 2 && !io && small_chain_eligible(n, c.ld, cfg);
+  const bool small = !c.cplx && !exact && arith() != 2 && !io && !capture && small_chain_eligible(n, c.ld, cfg);
   // int8-emulated products (NNB_ARITH_OZAKI): A is the same operand in every nest, so its
   // int8 splits are formed once per chain
   struct OzPin {
@@ -434,6 +442,7 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
   }
   (void)diverged_early;
   NNB_CUDA(cudaEventRecord(e1, c.s));
+  if (capture && cfg.final_residual) NNB_TRY(copy2d(R.re, c.ld, capture, capture_ld, n, n, c.s));
   // copy the final iterate into the caller's X buffer if it lives elsewhere
   if (bufs[xi].re != caller_x.re && !(io && io->out_streamed)) {
     NNB_TRY(copy2d(bufs[xi].re, c.ld, caller_x.re, c.ld, n, n, c.s));
@@ -800,6 +809,11 @@ int chain_complex(const double* Ar, const double* Ai, int64_t n, int64_t ldn, do
   c.s = s;
   Plane a{const_cast<double*>(Ar), const_cast<double*>(Ai)}, x{Xr, Xi};
   return run_chain(c, a, x, cfg, eps_hist, out);
+}
+
+void set_chain_capture(double* r, int64_t ld) {
+  g_capture_r = r;
+  g_capture_ld = ld;
 }
 
 }  // namespace nnb

@@ -117,6 +117,8 @@ int gemm_exact(const GemmOp& op, cudaStream_t s);
 // Ozaki-II emulation of a real product on the int8 tensor cores (ozaki.cu).
 int gemm_ozaki(const GemmOp& op, cudaStream_t s);
 int ozaki_moduli_for(int64_t k);
+void ozaki_profile(int on);
+void ozaki_stats(double* ms, double* work, int64_t* launches, int reset);
 // NNB_ARITH_FAST routes a real product to the int8 emulation where it beats DMMA
 // (measured crossover between N=2048 and 4096): M, N >= 1024 and M·N·K >= 3072^3.
 inline bool ozaki_pays(int64_t M, int64_t N, int64_t K) {
@@ -125,6 +127,8 @@ inline bool ozaki_pays(int64_t M, int64_t N, int64_t K) {
 // A chain operand that stays unchanged while pinned: its int8 splits are reused.
 void oz_pin(const double* p, int64_t ld, int64_t rows, int64_t cols);
 void oz_unpin();
+// the next real chain of the calling thread copies its final residual I − A·X to r (device, ld)
+void set_chain_capture(double* r, int64_t ld);
 // 2D uint8 TMA descriptor (rows × cols bytes, leading dimension ld bytes), 128B swizzle.
 int make_tmap_u8(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                  int box_cols);

@@ -42,6 +42,8 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "engine.cuh"
@@ -124,11 +126,26 @@ __device__ __forceinline__ void garner_digits(float* v, const float* r) {
     garner_digits<L + 1, S>(v, r);
   }
 }
-// Horner from the top digit: x·m_L + v_L for L = S−2 .. 0
-template <int L>
-__device__ __forceinline__ double horner(const float* v, double x) {
-  if constexpr (L < 0) return x;
-  else return horner<L - 1>(v, fma(x, static_cast<double>(kMod(L)), static_cast<double>(v[L])));
+// Horner from the top digit: x·m_L + v_L for L = S−2 .. 0.  The top digits' partial
+// values stay below 2^53 (exact); from step L <= S−7 on, each step is compensated
+// (TwoProduct by FMA, FastTwoSum: |x·m| >= m > v whenever x != 0; CompHorner of
+// Graillat, Langlois and Louvet), so C' is rounded about once, not once per step.
+template <int L, int S>
+__device__ __forceinline__ double horner(const float* v, double x, double c) {
+  if constexpr (L < 0) {
+    return x + c;
+  } else {
+    const double m = static_cast<double>(kMod(L)), d = static_cast<double>(v[L]);
+    if constexpr (L > S - 7) {
+      return horner<L - 1, S>(v, fma(x, m, d), c);
+    } else {
+      const double p = x * m;
+      const double pe = fma(x, m, -p);
+      const double sum = p + d;
+      const double se = d - (sum - p);
+      return horner<L - 1, S>(v, sum, fma(c, m, pe + se));
+    }
+  }
 }
 
 int inv_mod(int a, int m) {
@@ -544,7 +561,7 @@ __global__ void __launch_bounds__(256) oz_recon_kernel(const uint8_t* __restrict
         // symmetric representative: C' − M replaces the top digit v_S by v_S − m_S
         double x = static_cast<double>(v[S - 1]);
         if (v[S - 1] >= 0.5f * static_cast<float>(kMod(S - 1))) x -= static_cast<double>(kMod(S - 1));
-        x = horner<S - 2>(v, x);
+        x = horner<S - 2, S>(v, x, 0.0);
         // scale back by 2^-(ea+eb), then the chain's epilogue
         const int cc = c + h;
         const int e = (cc < N) ? eb[cc] : 0;
@@ -629,6 +646,48 @@ __global__ void __launch_bounds__(256) oz_recon_kernel(const uint8_t* __restrict
   }
 }
 
+// Live per-kernel timing for bench.py's roofline (nnb_ozaki_profile / nnb_ozaki_stats):
+// while enabled, each int8 GEMM, split and reconstruction launch is bracketed by CUDA
+// events on its own stream; the sums are read (and the events drained) on request.
+struct OzStats {
+  std::mutex mu;
+  bool on = false;
+  struct Rec {
+    int cls;
+    cudaEvent_t a, b;
+    double work;
+  };
+  std::vector<Rec> pending;
+  double ms[3] = {0, 0, 0}, work[3] = {0, 0, 0};
+  int64_t n[3] = {0, 0, 0};
+};
+OzStats& stats() {
+  static OzStats s;
+  return s;
+}
+struct Timed {
+  int cls;
+  double work;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  Timed(int c, double w, cudaStream_t s) : cls(c), work(w), st(s) {
+    OzStats& S = stats();
+    std::lock_guard<std::mutex> g(S.mu);
+    if (!S.on) return;
+    cudaEventCreate(&a);
+    cudaEventRecord(a, st);
+  }
+  ~Timed() {
+    if (!a) return;
+    cudaEvent_t b;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, st);
+    OzStats& S = stats();
+    std::lock_guard<std::mutex> g(S.mu);
+    S.pending.push_back({cls, a, b, work});
+  }
+};
+
 // ---------------------------------------------------------------- host side
 struct OzOperand {
   DevBuf res;   // int8 [s][rows][kp]
@@ -645,6 +704,7 @@ int split_left(const double* A, int64_t lda, int64_t rows, int64_t k, const OzCo
   o.s = c.s;
   NNB_TRY(o.res.alloc((size_t)c.s * rows * o.kp, st));
   NNB_TRY(o.exps.alloc(sizeof(int) * std::max<int64_t>(rows, 1), st));
+  Timed tm(1, (double)rows * k * (8.0 + c.s), st);  // algorithmic bytes: 8 B in, s B out per entry
   oz_split_rows_kernel<<<static_cast<unsigned>(rows), 256, 0, st>>>(A, lda, (int)rows, (int)k, o.kp,
                                                                       o.res.as<int8_t>(), o.exps.as<int>(), c);
   count_launch();
@@ -667,6 +727,7 @@ int split_right(const double* B, int64_t ldb, int64_t k, int64_t n, bool kmajor,
   unsigned long long* colmax = cm.as<unsigned long long>();
   int* colbad = reinterpret_cast<int*>(colmax + n);
   NNB_CUDA(cudaMemsetAsync(cm.p, 0, cm.bytes, st));
+  Timed tm(1, (double)n * k * (8.0 + 8.0 + c.s), st);  // column max pass + the split pass
   oz_colmax_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)((k + 255) / 256)), 256, 0, st>>>(
       B, ldb, (int)k, (int)n, colmax, colbad);
   count_launch();
@@ -680,6 +741,7 @@ int split_right(const double* B, int64_t ldb, int64_t k, int64_t n, bool kmajor,
 int launch_recon(int s, const uint8_t* res, int64_t ldr, int M, int N, const int* ea, const int* eb,
                  const GemmEpilogue& ep, const OzConst& c, cudaStream_t st) {
   const dim3 grid((unsigned)((N + 127) / 128), (unsigned)((M + 15) / 16));
+  Timed tm(2, (double)M * N * (s + (ep.D ? 16.0 : 8.0)), st);  // s residue bytes (+ D) in, 8 B out
   switch (s) {
 #define NNB_OZ_RECON(S)                                                                     \
   case S:                                                                                   \
@@ -776,15 +838,50 @@ int gemm_ozaki(const GemmOp& op, cudaStream_t st) {
   const int64_t total = (int64_t)tiles_m * tiles_n * s;
   if (total > INT32_MAX) return fail(7, "ozaki: too many tiles");
   const unsigned grid = (unsigned)std::min<int64_t>(total, sms);
+  {
+  Timed tm(0, 2.0 * s * (double)M * N * K, st);  // int8 tensor ops
   oz_gemm_kernel<<<grid, 192, kGemmSmem, st>>>(ta, tb, (int)M, (int)N, (int)K, ldr, res.as<uint8_t>(), c, tiles_m,
                                                tiles_n);
   count_launch();
   NNB_CUDA(cudaGetLastError());
+  }
   // reconstruction + the chain's epilogue
   return launch_recon(s, res.as<uint8_t>(), ldr, (int)M, (int)N, L->exps.as<int>(), R->exps.as<int>(), op.ep, c,
                       st);
 }
 
 int ozaki_moduli_for(int64_t k) { return std::max(15, moduli_for(k)); }
+
+void ozaki_profile(int on) {
+  OzStats& S = stats();
+  std::lock_guard<std::mutex> g(S.mu);
+  S.on = on != 0;
+}
+
+// class 0: int8 GEMMs (work = int8 ops), 1: operand splits, 2: reconstructions (work = bytes)
+void ozaki_stats(double* ms, double* work, int64_t* launches, int reset) {
+  OzStats& S = stats();
+  std::lock_guard<std::mutex> g(S.mu);
+  for (auto& r : S.pending) {
+    cudaEventSynchronize(r.b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    S.ms[r.cls] += t;
+    S.work[r.cls] += r.work;
+    S.n[r.cls] += 1;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  S.pending.clear();
+  for (int c = 0; c < 3; ++c) {
+    if (ms) ms[c] = S.ms[c];
+    if (work) work[c] = S.work[c];
+    if (launches) launches[c] = S.n[c];
+    if (reset) {
+      S.ms[c] = S.work[c] = 0.0;
+      S.n[c] = 0;
+    }
+  }
+}
 
 }  // namespace nnb

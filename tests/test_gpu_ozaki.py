@@ -53,8 +53,8 @@ def test_ozaki_matmul_within_truncation_bound(m, k, n):
     assert rel_frob(c, ref) < 1e-14, rel_frob(c, ref)
     if exact is not None:
         err = np.abs(c.astype(np.longdouble) - exact).astype(np.float64)
-        # + the FP64 Horner's rounding once |C'| passes 2^53 (at most ~9 of its 15 steps)
-        lim = bound(a, b) + 2.0 ** -49 * np.abs(exact).astype(np.float64) + 1e-300
+        # + the (compensated) FP64 Horner's final rounding
+        lim = bound(a, b) + 2.0 ** -52 * np.abs(exact).astype(np.float64) + 1e-300
         assert np.all(err <= lim), float(np.max(err / lim))
 
 

@@ -145,3 +145,25 @@ def test_sparse_plan_reuse_nccl_world1(ref):
     finally:
         plan.close()
         comm.close()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_c4_emulated_sharded_matches_single_gpu_n8192(world):
+    """SURVEY §8(c) C4 item (ii) at N=8192: the row-sharded schedule (ring all-gathers,
+    K-split partial products, rank-ordered eps) over 2/4/8 virtual ranks gives the
+    single-GPU X to 1e-12 relative, and the same eps history."""
+    import torch
+
+    n = 8192
+    g = torch.Generator(device="cuda").manual_seed(8192)
+    b = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
+    a = torch.addmm(torch.eye(n, dtype=torch.float64, device="cuda"), b, b.T, alpha=1.0 / n)
+    del b
+    x1, r1 = nnb.nn_chain(a, None, p=2, max_iters=3)
+    xs, rs = nnb.nn_chain_sharded_emulated(a, world, None, p=2, max_iters=3)
+    assert rs.iters == r1.iters == 3 and rs.products == r1.products
+    rel = (torch.linalg.norm(torch.as_tensor(xs, device="cuda") - x1) / torch.linalg.norm(x1)).item()
+    assert rel < 1e-12, rel
+    e1 = np.array([e for _, e in r1.history])
+    es = np.array([e for _, e in rs.history])
+    assert np.allclose(es, e1, rtol=1e-10, atol=1e-15)

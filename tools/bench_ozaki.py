@@ -28,11 +28,13 @@ for n in [int(v) for v in sys.argv[1:]] or [4096, 8192, 16384]:
     a = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
     b = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
     reps = max(1, int(2e12 / n ** 3))
-    t_d = timed(lambda: nnb.matmul(a, b), reps)
+    with nnb.dmma_arithmetic():
+        t_d = timed(lambda: nnb.matmul(a, b), reps)
+        c_d = nnb.matmul(a, b)
     with nnb.ozaki_arithmetic():
         t_o = timed(lambda: nnb.matmul(a, b), reps)
         c_o = nnb.matmul(a, b)
-    c_d = nnb.matmul(a, b)
+
     rel = (torch.linalg.norm(c_o - c_d) / torch.linalg.norm(c_d)).item()
     f = 2.0 * n ** 3
     print(f"N={n}: DMMA {t_d:.3f} ms ({f / t_d / 1e9:.1f} TF/s)  OZAKI {t_o:.3f} ms ({f / t_o / 1e9:.1f} TF/s, "
