@@ -812,6 +812,8 @@ def main():
             line["e2e"] = d["e2e"]
         if "symmetric" in d:
             line["legs"]["dense_symmetric"] = d["symmetric"]
+        if "dmma" in d:
+            line["legs"]["dense_dmma"] = d["dmma"]
         config["eps_first_last"] = [d["eps_first"], d["eps_last"]]
     if "mimo" in legs:
         line["legs"]["mimo"] = run_mimo(args, world, rank)

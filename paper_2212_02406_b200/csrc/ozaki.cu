@@ -246,20 +246,21 @@ constexpr uint32_t kIdesc = (2u << 4) |            // D: s32
 
 constexpr int kAccBufs = 2;    // TMEM accumulators: 2 × 256 columns (the whole 512)
 constexpr int kEpiWarps = 4;
-constexpr int kGroupM = 8;     // rasterisation: 8 tile-rows per group, so a wave shares A and B panels
+constexpr int kGroupM = 16;    // rasterisation: 16 tile-rows per group (measured best of 4..32: DRAM 72 vs 106 GB at N=16384 for 8)
 
 struct TileCoord {
   int l, mt, nt;
 };
-__device__ __forceinline__ TileCoord tile_of(int t, int tiles_m, int tiles_n) {
+__device__ __forceinline__ TileCoord tile_of(int t, int tiles_m, int tiles_n, int group_m = kGroupM) {
+  // group_m tile-rows per group; each group is walked column by column
   const int per = tiles_m * tiles_n;
   TileCoord c;
   c.l = t / per;
   const int r = t - c.l * per;
-  const int group = r / (kGroupM * tiles_n);
-  const int first_m = group * kGroupM;
-  const int gm = min(tiles_m - first_m, kGroupM);
-  const int w = r - group * kGroupM * tiles_n;
+  const int group = r / (group_m * tiles_n);
+  const int first_m = group * group_m;
+  const int gm = min(tiles_m - first_m, group_m);
+  const int w = r - group * group_m * tiles_n;
   c.mt = first_m + w % gm;
   c.nt = w / gm;
   return c;
@@ -271,7 +272,8 @@ __device__ __forceinline__ TileCoord tile_of(int t, int tiles_m, int tiles_n) {
 // two TMEM accumulators let the epilogue of tile i overlap the MMAs of tile i+1.
 __global__ void __launch_bounds__(192, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, int M, int N,
-                   int K, int64_t ldr, uint8_t* __restrict__ out, const OzConst cst, int tiles_m, int tiles_n) {
+                   int K, int64_t ldr, uint8_t* __restrict__ out, const OzConst cst, int tiles_m, int tiles_n,
+                   int group_m) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -306,7 +308,7 @@ __global__ void __launch_bounds__(192, 1)
       tma_prefetch_desc(&tma_b);
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const TileCoord tc = tile_of(t, tiles_m, tiles_n);
+        const TileCoord tc = tile_of(t, tiles_m, tiles_n, group_m);
         const int arow = tc.l * M + tc.mt * kBM, brow = tc.l * N + tc.nt * kBN;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int st = it % kStages;
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;
     int n_t = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++n_t) {
-      const TileCoord tc = tile_of(t, tiles_m, tiles_n);
+      const TileCoord tc = tile_of(t, tiles_m, tiles_n, group_m);
       const int acc = n_t & 1;
       mbar_wait(&tfull[acc], (n_t >> 1) & 1);
       tc_fence_after();
@@ -837,13 +839,14 @@ int gemm_ozaki(const GemmOp& op, cudaStream_t st) {
   const int tiles_m = (int)((M + kBM - 1) / kBM), tiles_n = (int)((N + kBN - 1) / kBN);
   const int64_t total = (int64_t)tiles_m * tiles_n * s;
   if (total > INT32_MAX) return fail(7, "ozaki: too many tiles");
-  const unsigned grid = (unsigned)std::min<int64_t>(total, sms);
   {
-  Timed tm(0, 2.0 * s * (double)M * N * K, st);  // int8 tensor ops
-  oz_gemm_kernel<<<grid, 192, kGemmSmem, st>>>(ta, tb, (int)M, (int)N, (int)K, ldr, res.as<uint8_t>(), c, tiles_m,
-                                               tiles_n);
-  count_launch();
-  NNB_CUDA(cudaGetLastError());
+    Timed tm(0, 2.0 * s * (double)M * N * K, st);  // int8 tensor ops
+    const unsigned grid = (unsigned)std::min<int64_t>(total, sms);
+    static const int gm = debug_env("NNB_OZ_GROUP") ? std::atoi(debug_env("NNB_OZ_GROUP")) : kGroupM;
+    oz_gemm_kernel<<<grid, 192, kGemmSmem, st>>>(ta, tb, (int)M, (int)N, (int)K, ldr, res.as<uint8_t>(), c,
+                                                 tiles_m, tiles_n, gm);
+    count_launch();
+    NNB_CUDA(cudaGetLastError());
   }
   // reconstruction + the chain's epilogue
   return launch_recon(s, res.as<uint8_t>(), ldr, (int)M, (int)N, L->exps.as<int>(), R->exps.as<int>(), op.ep, c,
