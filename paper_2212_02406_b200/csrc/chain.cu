@@ -148,11 +148,13 @@ int product(Ctx& c, const Plane& A, const Plane& B, double alpha, const Plane* D
 int product_chunked(Ctx& c, const Plane& A, const Plane& B, double alpha, const Plane* D, double beta,
                     double gamma, const Plane& C, double* eps_out, int* nf_out, ChainIo& io, bool wait_in,
                     bool stream_out, double* chunk_ss, int* chunk_nf) {
+  // every chunk multiplies by the same B: under the int8 emulation its split is formed once
+  OzPinScope pin_b(!c.cplx && (arith() == 2 || arith() == 0), B.re, c.ld, c.n, c.n);
   int m = 0;
   for (int q = 0; q < io.chunks; ++q) {
     const int64_t r0 = q * io.chunk_rows, rows = std::min<int64_t>(io.chunk_rows, c.n - r0);
     if (rows <= 0) break;
-    if (wait_in) NNB_CUDA(cudaStreamWaitEvent(c.s, io.a_ready[q], 0));
+    if (wait_in) NNB_CUDA(cudaStreamWaitEvent(c.s, io.a_rows_ready ? io.a_rows_ready[q] : io.a_ready[q], 0));
     GemmOp op;
     op.M = rows;
     op.N = op.K = c.n;
@@ -256,13 +258,8 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
   const bool small = !c.cplx && !exact && arith() != 2 && !io && !capture && small_chain_eligible(n, c.ld, cfg);
   // int8-emulated products (NNB_ARITH_OZAKI): A is the same operand in every nest, so its
   // int8 splits are formed once per chain
-  struct OzPin {
-    bool on;
-    ~OzPin() {
-      if (on) oz_unpin();
-    }
-  } oz_pin_guard{(arith() == 2 || (arith() == 0 && ozaki_pays(n, n, n))) && !c.cplx};
-  if (oz_pin_guard.on) oz_pin(A.re, c.ld, n, n);
+  const bool oz = (arith() == 2 || (arith() == 0 && ozaki_pays(n, n, n))) && !c.cplx;
+  OzPinScope oz_pin_a(oz, A.re, c.ld, n, n);
   if (!small) NNB_TRY(c.red.init(max_tiles_for(n, n), c.s));
   DevBuf work;
   NNB_TRY(work.alloc(sizeof(double) * (size_t)mat * planes * 3, c.s));
@@ -373,7 +370,11 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
     const Plane& rhs = order == 0 ? Xk : A;
     if (k == 0 && io && io->a_ready && order == 0)  // R_0 = I − A·X_0 as A's columns and X_0's rows arrive
       NNB_TRY(product_ksplit(c, lhs, rhs, -1.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1), *io));
-    else
+    else if (k == 0 && io && io->a_rows_ready && order == 0) {  // X_0 whole, A's row chunks as they arrive
+      NNB_CUDA(cudaStreamWaitEvent(c.s, io->x_ready, 0));
+      NNB_TRY(product_chunked(c, lhs, rhs, -1.0, nullptr, 0.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1), *io, true,
+                              false, chunk_ss, chunk_nf));
+    } else
       NNB_TRY(product(c, lhs, rhs, -1.0, nullptr, 0.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1)));
     ++products;
     recorded = k + 1;

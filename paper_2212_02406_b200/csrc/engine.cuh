@@ -125,8 +125,19 @@ inline bool ozaki_pays(int64_t M, int64_t N, int64_t K) {
   return M >= 1024 && N >= 1024 && K >= 1024 && K <= 131071 && (double)M * N * K >= 3072.0 * 3072.0 * 3072.0;
 }
 // A chain operand that stays unchanged while pinned: its int8 splits are reused.
-void oz_pin(const double* p, int64_t ld, int64_t rows, int64_t cols);
-void oz_unpin();
+// returns false (and changes nothing) when p is already pinned
+bool oz_pin(const double* p, int64_t ld, int64_t rows, int64_t cols);
+void oz_unpin(const double* p);
+// RAII pin for a scope in which p's contents do not change (no-op when off)
+struct OzPinScope {
+  const double* p = nullptr;
+  OzPinScope(bool on, const double* ptr, int64_t ld, int64_t rows, int64_t cols) {
+    if (on && oz_pin(ptr, ld, rows, cols)) p = ptr;
+  }
+  ~OzPinScope() {
+    if (p) oz_unpin(p);
+  }
+};
 // the next real chain of the calling thread copies its final residual I − A·X to r (device, ld)
 void set_chain_capture(double* r, int64_t ld);
 // 2D uint8 TMA descriptor (rows × cols bytes, leading dimension ld bytes), 128B swizzle.
@@ -215,6 +226,10 @@ struct ChainIo {
   cudaEvent_t* out_done = nullptr; // [chunks] scratch
   cudaEvent_t copy_done = nullptr; // scratch
   bool out_streamed = false;       // run_chain delivered the final X to host_out (X itself is then stale)
+  // int8-emulation streaming: X0 is whole on the device once x_ready fires and A arrives by
+  // row chunks (a_rows_ready[q]); the first product R = I − A·X0 then runs chunk by chunk
+  cudaEvent_t x_ready = nullptr;
+  cudaEvent_t* a_rows_ready = nullptr;
 };
 // Real chain on device buffers with ld == ldn (ldn even, >= n).  X holds X0
 // on entry and the final iterate on exit.  eps_hist host (nullable).

@@ -770,22 +770,29 @@ struct Pinned {
   bool have_left = false, have_right = false;
   int s_left = 0, s_right = 0;
 };
-thread_local Pinned* g_pinned = nullptr;
+thread_local std::vector<Pinned*> g_pins;  // at most a few: the chain's A, a chunked product's B
 
 }  // namespace
 
-void oz_pin(const double* p, int64_t ld, int64_t rows, int64_t cols) {
-  delete g_pinned;
-  g_pinned = new Pinned();
-  g_pinned->p = p;
-  g_pinned->ld = ld;
-  g_pinned->rows = rows;
-  g_pinned->cols = cols;
+bool oz_pin(const double* p, int64_t ld, int64_t rows, int64_t cols) {
+  for (Pinned* q : g_pins)
+    if (q->p == p) return false;  // already pinned by an enclosing scope: keep its splits
+  Pinned* q = new Pinned();
+  q->p = p;
+  q->ld = ld;
+  q->rows = rows;
+  q->cols = cols;
+  g_pins.push_back(q);
+  return true;
 }
 
-void oz_unpin() {
-  delete g_pinned;
-  g_pinned = nullptr;
+void oz_unpin(const double* p) {
+  for (size_t i = 0; i < g_pins.size(); ++i)
+    if (g_pins[i]->p == p) {
+      delete g_pins[i];
+      g_pins.erase(g_pins.begin() + i);
+      return;
+    }
 }
 
 int make_tmap_u8(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
@@ -801,8 +808,13 @@ int gemm_ozaki(const GemmOp& op, cudaStream_t st) {
   OzOperand la, rb;
   const OzOperand* L = &la;
   const OzOperand* R = &rb;
-  Pinned* pin = g_pinned;
-  if (pin && op.A == pin->p && op.lda == pin->ld && M == pin->rows && K == pin->cols) {
+  auto find = [](const double* p) -> Pinned* {
+    for (Pinned* q : g_pins)
+      if (q->p == p) return q;
+    return nullptr;
+  };
+  Pinned* pin = find(op.A);
+  if (pin && op.lda == pin->ld && M == pin->rows && K == pin->cols) {
     if (!pin->have_left || pin->s_left != s) {
       NNB_TRY(split_left(op.A, op.lda, M, K, c, pin->left, st));
       pin->have_left = true;
@@ -812,7 +824,8 @@ int gemm_ozaki(const GemmOp& op, cudaStream_t st) {
   } else {
     NNB_TRY(split_left(op.A, op.lda, M, K, c, la, st));
   }
-  if (pin && !op.b_kmajor && op.B == pin->p && op.ldb == pin->ld && K == pin->rows && N == pin->cols) {
+  pin = find(op.B);
+  if (pin && !op.b_kmajor && op.ldb == pin->ld && K == pin->rows && N == pin->cols) {
     if (!pin->have_right || pin->s_right != s) {
       NNB_TRY(split_right(op.B, op.ldb, K, N, false, c, pin->right, st));
       pin->have_right = true;
