@@ -116,38 +116,18 @@ __device__ __forceinline__ void garner_digits(float* v, const float* r) {
     if constexpr (L == 0) {
       v[0] = r[0];
     } else {
-      const float x = garner_sum<L, 0>(v, r[L] * GarnerP<L>::v);  // < 2^20
-      const float qf = floorf(x * GarnerP<L>::inv);
-      float d = fmaf(-qf, GarnerP<L>::m, x);
-      d += (d < 0.0f) ? GarnerP<L>::m : 0.0f;
-      d -= (d >= GarnerP<L>::m) ? GarnerP<L>::m : 0.0f;
-      v[L] = d;
+      // balanced digit: any representative of the residue class works in Garner's
+      // recurrence (later digits are formed from the digits actually used), so the
+      // nearest-integer quotient needs no fix-up; |v| <= 1.5·m keeps every partial
+      // sum below 2^21 (exact in FP32) and the final Σ v_l·W_l within ±0.76·M, which
+      // with |C'| < M/8 makes it C' itself — no sign pass either
+      const float x = garner_sum<L, 0>(v, r[L] * GarnerP<L>::v);
+      const float qf = fmaf(x, GarnerP<L>::inv, 12582912.0f) - 12582912.0f;  // rint by the 1.5·2^23 shifter
+      v[L] = fmaf(-qf, GarnerP<L>::m, x);                                    // exact
     }
     garner_digits<L + 1, S>(v, r);
   }
 }
-// Horner from the top digit: x·m_L + v_L for L = S−2 .. 0.  The top digits' partial
-// values stay below 2^53 (exact); from step L <= S−7 on, each step is compensated
-// (TwoProduct by FMA, FastTwoSum: |x·m| >= m > v whenever x != 0; CompHorner of
-// Graillat, Langlois and Louvet), so C' is rounded about once, not once per step.
-template <int L, int S>
-__device__ __forceinline__ double horner(const float* v, double x, double c) {
-  if constexpr (L < 0) {
-    return x + c;
-  } else {
-    const double m = static_cast<double>(kMod(L)), d = static_cast<double>(v[L]);
-    if constexpr (L > S - 7) {
-      return horner<L - 1, S>(v, fma(x, m, d), c);
-    } else {
-      const double p = x * m;
-      const double pe = fma(x, m, -p);
-      const double sum = p + d;
-      const double se = d - (sum - p);
-      return horner<L - 1, S>(v, sum, fma(c, m, pe + se));
-    }
-  }
-}
-
 int inv_mod(int a, int m) {
   a %= m;
   for (int x = 1; x < m; ++x)
@@ -398,13 +378,55 @@ __device__ __forceinline__ int exp_for(double amax) {
 }
 
 // signed residue of the integer-valued double a (|a| <= 2^53) modulo m, in [-128, 127]
+// Exact integer value of a group of digits lo..hi (Horner; the group's weight
+// Π m_lo..m_hi stays below 2^53, so every step is exact).
+template <int L, int LO>
+__device__ __forceinline__ double group(const float* v, double x) {
+  if constexpr (L < LO) return x;
+  else return group<L - 1, LO>(v, fma(x, static_cast<double>(kMod(L)), static_cast<double>(v[L])));
+}
+constexpr double weight(int lo, int hi) {  // Π_{lo<=l<=hi} m_l
+  double w = 1.0;
+  for (int l = lo; l <= hi; ++l) w *= kMod(l);
+  return w;
+}
+// C' = ((G2·W'+ G1)·W + G0) from three exact digit groups (digits 0-5, 6-11, 12..S-1,
+// the top one signed); W = Π m_0..5 and W' = Π m_6..11 are exact doubles (< 2^48).
+// The two multiply-adds are error-free (TwoProduct by FMA, TwoSum), so C' is rounded
+// once at the end: relative error ~2^-53, 24 FP64 operations instead of a 15-step
+// compensated Horner.
+template <int S>
+__device__ __forceinline__ double value_of(const float* v, float top) {
+  static_assert(S >= 13 && S <= 18, "three groups of at most 6 digits");
+  constexpr double W = weight(0, 5), W2 = weight(6, 11);
+  const double g0 = group<5, 0>(v, 0.0);
+  const double g1 = group<11, 6>(v, 0.0);
+  const double g2 = group<S - 2, 12>(v, static_cast<double>(top));  // top digit already signed
+  // inner = g2·W2 + g1 as a double-double (hi, lo)
+  const double p = g2 * W2;
+  const double pe = fma(g2, W2, -p);
+  const double s1 = p + g1;
+  const double bb = s1 - p;
+  const double se = (p - (s1 - bb)) + (g1 - bb);
+  const double lo = pe + se;
+  // C' = (s1 + lo)·W + g0
+  const double q = s1 * W;
+  const double qe = fma(s1, W, -q);
+  return q + (fma(lo, W, qe) + g0);
+}
+
+// Round-to-nearest by the 1.5·2^52 shifter (exact for |x| < 2^51): one DFMA and one DADD
+// instead of FRND.F64; and the low word of (r + 1.5·2^52) is r in two's complement, so
+// the residue leaves the FP64 pipe without an F2I conversion.
+constexpr double kShift52 = 6755399441055744.0;
 __device__ __forceinline__ int resid(double a, double m, double inv_m) {
-  const double q = rint(a * inv_m);
-  int r = static_cast<int>(fma(-q, m, a));  // exact: the result is a small integer
+  const double q = fma(a, inv_m, kShift52) - kShift52;  // |a·inv_m| < 2^46: rint(a/m) up to one
+  const double r = fma(-q, m, a);                          // exact: a small integer
+  int ri = __double2loint(r + kShift52);
   const int mi = static_cast<int>(m);
-  r -= (r > 127) ? mi : 0;
-  r += (r < -128) ? mi : 0;
-  return r;
+  ri -= (ri > 127) ? mi : 0;   // q one off near a half-integer: bring r into int8 range
+  ri += (ri < -128) ? mi : 0;
+  return ri;
 }
 
 // Left operand: per-row scaling.  One 256-thread block per row:
@@ -557,13 +579,11 @@ __global__ void __launch_bounds__(256) oz_recon_kernel(const uint8_t* __restrict
 #pragma unroll
         for (int l = 0; l < S; ++l) {
           const uint32_t word = (jp < 2) ? rv[l].x : rv[l].y;
-          r[l] = static_cast<float>((word >> shift) & 0xffu);
+          // byte b -> float exactly: the bits 0x4B0000bb are 2^23 + b
+          r[l] = __uint_as_float(__byte_perm(word, 0x4B00u, 0x5440u + (shift >> 3))) - 8388608.0f;
         }
         garner_digits<0, S>(v, r);
-        // symmetric representative: C' − M replaces the top digit v_S by v_S − m_S
-        double x = static_cast<double>(v[S - 1]);
-        if (v[S - 1] >= 0.5f * static_cast<float>(kMod(S - 1))) x -= static_cast<double>(kMod(S - 1));
-        x = horner<S - 2, S>(v, x, 0.0);
+        const double x = value_of<S>(v, v[S - 1]);
         // scale back by 2^-(ea+eb), then the chain's epilogue
         const int cc = c + h;
         const int e = (cc < N) ? eb[cc] : 0;
