@@ -764,7 +764,8 @@ def nn_chain_sharded_emulated(a, world: int, x0=None, *, p: int, max_iters: int,
 
 # ------------------------------------------------------------ batched (C2)
 def nn_batched(a, p: int = 2, iters: int = 4, want_eps: bool = True, out=None):
-    """Batched 16×16 complex NN inversion with Jacobi X0; returns (X, eps_last)."""
+    """Batched n×n complex NN inversion with Jacobi X0 (n = 16: batched_z16_kernel; n = 8, 24, 32:
+    batched_generic.cu); returns (X, eps_last)."""
     a = _prep(a, True)
     b, n = a.shape[0], a.shape[1]
     out = _empty_like(a) if out is None else out
@@ -783,7 +784,8 @@ def nn_batched(a, p: int = 2, iters: int = 4, want_eps: bool = True, out=None):
 def mimo_detect(h, y, sigma2: float = 0.1, p: int = 2, iters: int = 4, want_x: bool = False,
                 want_eps: bool = False):
     """Fused MIMO detection: A = HᴴH + σ²I, X = NN⁻¹(A), x̂ = X·Hᴴy per system.
-    h: (batch, antennas, 16) complex, y: (batch, antennas) complex. Returns (x̂, X or None, eps or None)."""
+    h: (batch, antennas, users) complex with users in {8, 16, 24, 32}, y: (batch, antennas) complex.
+    Returns (x̂, X or None, eps or None)."""
     h = _prep(h, True)
     y = _prep(y, True)
     b, ant, users = h.shape

@@ -261,11 +261,17 @@ __device__ __forceinline__ void gram_epilogue(const ZAcc<true>& acc, double sigm
   __syncwarp();
 }
 
+// Largest |x| of a few doubles, to within a factor 2, by integer ops on their high words
+// (sign cleared; IEEE order = integer order) — kept off the FP64 pipe, which DMMA uses.
+__device__ __forceinline__ uint32_t mag_hi(double x) {
+  return static_cast<uint32_t>(__double2hiint(x)) & 0x7fffffffu;
+}
+
 // 3M with seeded accumulators: out = s·acc (s = −1 when NEG), stored to shared `out`.
-// Returns this lane's Σ|out|² (dead code unless the caller uses it).
+// Returns the high word of this lane's largest |out| entry (dead code unless used).
 template <bool NEG>
-__device__ __forceinline__ double epilogue_seeded(const ZAcc<true>& acc, const SMat& out, int g, int t) {
-  double ss = 0.0;
+__device__ __forceinline__ uint32_t epilogue_seeded(const ZAcc<true>& acc, const SMat& out, int g, int t) {
+  uint32_t mx = 0;
   __syncwarp();  // every lane finished reading operands that `out` may overwrite
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
@@ -285,10 +291,10 @@ __device__ __forceinline__ double epilogue_seeded(const ZAcc<true>& acc, const S
       }
       *reinterpret_cast<double2*>(out.re + idx) = vr;
       *reinterpret_cast<double2*>(out.im + idx) = vi;
-      ss += vr.x * vr.x + vr.y * vr.y + vi.x * vi.x + vi.y * vi.y;
+      mx = max(max(max(mx, mag_hi(vr.x)), max(mag_hi(vr.y), mag_hi(vi.x))), mag_hi(vi.y));
     }
   __syncwarp();
-  return ss;
+  return mx;
 }
 
 // epilogue_seeded<false> for a Hermitian result from zmma_ss_herm: tiles (0,0),
@@ -454,6 +460,54 @@ __device__ __forceinline__ void first_nest_diag(ZAcc<M3>& acc, const SMat& X, co
   }
 }
 
+// Mirrored (Hermitian) Horner products leave a κ·u residual floor — the dense chain's
+// NNB_ORDER_SYMMETRIC measured it.  Keep them while ε = ‖I − X·A‖_F/√n, formed for
+// free from the nest's P, falls at the nest's order: the first nest whose ε stops
+// falling, or lands 1e3× above ε_prev^(p+1) once ε_prev < 1e-2, is at that floor, and
+// from there on every product is full (sticky).  The last nest is also full when the
+// system is ill-conditioned and the nest would land where the floor decides it
+// (ε^(p+1) < 1e-13): κ is estimated from the nest k at which ε first fell below 1e-2
+// — (1 − 1/κ)^((p+1)^k) ≈ 1e-2 gives κ ≈ (p+1)^k / 4.6 — and "ill-conditioned" is
+// κ > 100, where the mirrored floor (~κ·u) would exceed the parity gate's 1e-12.  One
+// full nest restores Newton's self-correction (a κ = 1e5 batch: ε 6.8e-8 with a
+// mirrored last nest against the reference's 4.7e-12).  Config 1 (κ <= 4, ε < 1e-2
+// after one or two nests) keeps the 25 % cheaper products throughout: 2.40 ms against
+// 2.61 with a full last nest.
+struct MirrorState {
+  float eps_prev = INFINITY;
+  int k_drop = -1;  // first nest with ε < 1e-2
+};
+// Called one nest late (its warp reduction then costs no latency): eps is the size of
+// nest `it`'s P — max |P_ij| from the high words (an integer warp max, no FP64 work:
+// the FP64 pipe is the one DMMA issues on), which tracks ‖P‖_F/√n within a small
+// factor, ample for these thresholds — and the decision is for nest it + 1, which
+// would land near ε^((p+1)^2).
+template <int P>
+__device__ __forceinline__ bool keep_mirrored(float eps, MirrorState& st, int it, bool last) {
+  float expect = st.eps_prev, next = eps;
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    expect *= st.eps_prev;  // ε_prev^(p+1)
+    next *= eps;            // ε^(p+1)
+  }
+  float next2 = next;
+#pragma unroll
+  for (int j = 0; j < P; ++j) next2 *= next;  // ε^((p+1)^2), 0 when it underflows
+  if (st.k_drop < 0 && eps < 1e-2f) st.k_drop = it;
+  float kappa = 1.0f;
+  for (int k = 0; k < (st.k_drop < 0 ? it + 1 : st.k_drop); ++k) kappa *= (P + 1);
+  const bool ill = kappa > 460.0f;  // κ ≈ (p+1)^k / 4.6 > 100
+  const bool ok = eps < st.eps_prev && !(st.eps_prev < 1e-2f && eps > 1e3f * expect) &&
+                  !(last && ill && next2 < 1e-13f);
+  st.eps_prev = eps;
+  return ok;
+}
+// ε proxy of a P from every lane's high-word maximum
+__device__ __forceinline__ float p_size(uint32_t mx) {
+  const uint32_t w = __reduce_max_sync(0xffffffffu, mx);
+  return static_cast<float>(__hiloint2double(static_cast<int>(w), 0));
+}
+
 // NNB_BATCHED_MINB (compile-time) caps registers so that MINB CTAs fit per SM.
 #ifndef NNB_BATCHED_MINB
 #define NNB_BATCHED_MINB 4
@@ -517,21 +571,18 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
       // Hermitian A (and so X0): the Horner products compute three of four tiles
       bool herm = false;
       if (iters > 0) first_nest_diag<P, M3>(acc, X, Pm, V, areg, g, t, M3 && herm_ok, &herm);
-      double eps_prev = INFINITY;
+      MirrorState mst;
+      float eps_pending = INFINITY;
       for (int it = 1; it < iters; ++it) {
         const SMat* v = &X;
         if constexpr (M3) {
           acc.template seed<true>(nullptr, 1.0, g, t);  // −I
           zmma_sr(acc, X, areg, g, t);                  // −I + X·A
-          const double pss = epilogue_seeded<true>(acc, Pm, g, t);  // P = I − X·A
-          if (herm) {
-            // Mirrored Horner products leave a κ·u residual floor (the dense chain's
-            // NNB_ORDER_SYMMETRIC measured it): as there, full products from the first
-            // nest whose ε = ‖P‖_F/√n is below 1e-4 or no longer falling (sticky)
-            const double eps = sqrt(warp_sum(pss)) * 0.25;
-            herm = eps >= 1e-4 && eps < eps_prev;
-            eps_prev = eps;
-          }
+          const uint32_t pss = epilogue_seeded<true>(acc, Pm, g, t);  // P = I − X·A
+          // decide this nest from the previous nest's ε (its reduction is long done), then
+          // start this nest's reduction — nothing waits on it until the next nest
+          if (herm && it >= 2) herm = keep_mirrored<P>(eps_pending, mst, it - 1, it == iters - 1);
+          eps_pending = p_size(pss);
 #pragma unroll
           for (int j = 1; j <= P; ++j) {
             horner_step(acc, X, Pm, *v, (j == P) ? X : V, herm, g, t);  // X + P·V; the last lands in X
@@ -693,16 +744,14 @@ __global__ void __launch_bounds__(kThreads, NNB_BATCHED_MINB)
     // A = HᴴH + σ²I is Hermitian by construction (gram_epilogue mirrors it)
     bool herm = herm_ok != 0;
     if (iters > 0) first_nest_diag<P, true>(acc, X, Pm, V, areg, g, t, herm, nullptr);
-    double eps_prev = INFINITY;
+    MirrorState mst;
+    float eps_pending = INFINITY;
     for (int it = 1; it < iters; ++it) {
       acc.template seed<true>(nullptr, 1.0, g, t);
       zmma_sr(acc, X, areg, g, t);
-      const double pss = epilogue_seeded<true>(acc, Pm, g, t);  // P = I − X·A
-      if (herm) {  // the batched kernel's cutover: full products once ε < 1e-4 or not falling
-        const double eps = sqrt(warp_sum(pss)) * 0.25;
-        herm = eps >= 1e-4 && eps < eps_prev;
-        eps_prev = eps;
-      }
+      const uint32_t pss = epilogue_seeded<true>(acc, Pm, g, t);  // P = I − X·A
+      if (herm && it >= 2) herm = keep_mirrored<P>(eps_pending, mst, it - 1, it == iters - 1);
+      eps_pending = p_size(pss);
       const SMat* v = &X;
 #pragma unroll
       for (int j = 1; j <= P; ++j) {

@@ -949,9 +949,22 @@ static int batched_pipelined(const double* A, int64_t batch, int p, int iters, i
 static int batched(const double* A, int64_t batch, int32_t n, int p, int iters, int ns_order,
                    double* X_out, double* eps_last, void* stream) {
   NNB_TRY(require_device());
-  if (n != 16) return fail(NNB_ERR_SHAPE, "batched: only 16x16 systems are supported");
+  if (n != 8 && n != 16 && n != 24 && n != 32)
+    return fail(NNB_ERR_SHAPE, "batched: n must be 8, 16, 24 or 32 (users of a massive-MIMO uplink)");
   if (batch < 0) return fail(NNB_ERR_SHAPE, "batched: negative batch");
   cudaStream_t s = resolve(stream);
+  if (n != 16) {  // batched_generic.cu
+    const size_t cnt = (size_t)batch * 2 * n * n;
+    In a;
+    NNB_TRY(a.stage(A, cnt, s));
+    Out x, e;
+    NNB_TRY(x.prepare(X_out, cnt, s));
+    if (eps_last) NNB_TRY(e.prepare(eps_last, (size_t)batch, s));
+    NNB_TRY(batched_nn_gen(a.d, batch, n, p, iters, ns_order, x.d, eps_last ? e.d : nullptr, s));
+    NNB_TRY(x.finish(s));
+    if (eps_last) NNB_TRY(e.finish(s));
+    return 0;
+  }
   const size_t cnt = (size_t)batch * 2 * 256;
   const bool host_in = !is_device_ptr(A), host_out = !is_device_ptr(X_out) ||
                                                      (eps_last && !is_device_ptr(eps_last));
@@ -979,7 +992,8 @@ int nnb_mimo_detect_z(const double* H, const double* y, int64_t batch, int32_t a
                       double sigma2, int32_t p, int32_t iters, double* xhat_out, double* X_out, double* eps_last,
                       void* stream) {
   NNB_TRY(require_device());
-  if (users != 16) return fail(NNB_ERR_SHAPE, "mimo detect: only 16 users (16x16 Gram systems) are supported");
+  if (users != 8 && users != 16 && users != 24 && users != 32)
+    return fail(NNB_ERR_SHAPE, "mimo detect: users must be 8, 16, 24 or 32");
   if (antennas < 4 || antennas % 4) return fail(NNB_ERR_SHAPE, "mimo detect: antennas must be a positive multiple of 4");
   if (p < 1 || p > 4 || iters < 0) return fail(NNB_ERR_DOMAIN, "mimo detect: depth p in 1..4, iters >= 0");
   if (batch < 0) return fail(NNB_ERR_SHAPE, "mimo detect: negative batch");
@@ -989,10 +1003,14 @@ int nnb_mimo_detect_z(const double* H, const double* y, int64_t batch, int32_t a
   NNB_TRY(yy.stage(y, (size_t)batch * antennas * 2, s));
   Out xh, x, e;
   NNB_TRY(xh.prepare(xhat_out, (size_t)batch * users * 2, s));
-  if (X_out) NNB_TRY(x.prepare(X_out, (size_t)batch * 512, s));
+  if (X_out) NNB_TRY(x.prepare(X_out, (size_t)batch * 2 * users * users, s));
   if (eps_last) NNB_TRY(e.prepare(eps_last, (size_t)batch, s));
-  NNB_TRY(mimo_detect_z16(h.d, yy.d, batch, antennas, sigma2, p, iters, xh.d, X_out ? x.d : nullptr,
-                          eps_last ? e.d : nullptr, s));
+  if (users == 16)
+    NNB_TRY(mimo_detect_z16(h.d, yy.d, batch, antennas, sigma2, p, iters, xh.d, X_out ? x.d : nullptr,
+                            eps_last ? e.d : nullptr, s));
+  else
+    NNB_TRY(mimo_detect_gen(h.d, yy.d, batch, antennas, users, sigma2, p, iters, xh.d, X_out ? x.d : nullptr,
+                            eps_last ? e.d : nullptr, s));
   NNB_TRY(xh.finish(s));
   if (X_out) NNB_TRY(x.finish(s));
   if (eps_last) NNB_TRY(e.finish(s));

@@ -278,6 +278,11 @@ int axpby_z(double ar, double ai, const double* A, double br, double bi, const d
 // ---- batched / sparse (separate translation units) -------------------------------
 int batched_nn_z16(const double* A, int64_t batch, int p, int iters, int ns_order, double* X,
                    double* eps_last, cudaStream_t s);
+// n = 8, 24, 32 (batched_generic.cu): one warp per system, iterates in shared memory
+int batched_nn_gen(const double* A, int64_t batch, int n, int p, int iters, int ns_order, double* X, double* eps,
+                   cudaStream_t s);
+int mimo_detect_gen(const double* H, const double* y, int64_t batch, int antennas, int users, double sigma2, int p,
+                    int iters, double* xhat, double* X, double* eps, cudaStream_t s);
 int mimo_detect_z16(const double* H, const double* y, int64_t batch, int antennas, double sigma2, int p,
                     int iters, double* xhat, double* X, double* eps_last, cudaStream_t s);
 int spmv_csr(const int64_t* row_ptr, const int32_t* col, const double* val, int64_t n,

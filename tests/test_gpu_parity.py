@@ -837,3 +837,41 @@ def test_chain_odd_sizes_vs_reference(ref, n, p):
         assert rel_frob(x, xr.real) < TOL_X
     z = (np.random.default_rng(n).standard_normal((n, n)) + 1j * np.random.default_rng(n + 1).standard_normal((n, n)))
     assert rel_frob(nnb.matmul(z, z.T.copy()), ref.matmul(z, z.T.copy())[0]) < 1e-14  # 3M complex at an odd size
+
+
+# ----------------------------------------------------------------- batched, other user counts
+@pytest.mark.parametrize("n", [8, 24, 32])
+@pytest.mark.parametrize("p,iters", [(1, 6), (2, 4), (3, 3)])
+def test_batched_other_sizes_vs_reference(ref, n, p, iters):
+    """n = 8, 24, 32 users (batched_generic.cu): the reference's per-system nn_step loop
+    (proj/src/solver.cpp:93-103) from Jacobi X0, X within 1e-10, eps after the last nest."""
+    a = W.mimo_gram_host(37, seed=n + p, users=n)  # ragged batch
+    x, eps = nnb.nn_batched(a, p=p, iters=iters)
+    xr, er, _ = ref.batched("nn", a, p, iters, threads=8)
+    assert max(rel_frob(x[s], xr[s]) for s in range(a.shape[0])) < TOL_X
+    eps_close(eps, er)
+
+
+@pytest.mark.parametrize("n", [8, 32])
+def test_batched_other_sizes_ns_orders(ref, n):
+    a = W.mimo_gram_host(20, seed=5, users=n)
+    for order in (0, 1, 2, 9):
+        xs = nnb.ns_batched(a, order)
+        xr, _, _ = ref.batched("ns", a, 1, order, threads=8)
+        assert max(rel_frob(xs[s], xr[s]) for s in range(20)) < TOL_X
+
+
+@pytest.mark.parametrize("users", [8, 32])
+def test_mimo_detect_other_user_counts(port, users):
+    """Fused detection for 8 and 32 users: the Gram, the NN inverse and x̂ = X·Hᴴy
+    against the oracle's inverse of the same Gram (formed in extended precision)."""
+    h, y, sym = W.mimo_uplink_host(24, seed=users, users=users)
+    xh, x, eps = nnb.mimo_detect(h, y, want_x=True, want_eps=True)
+    g = np.conj(np.transpose(h, (0, 2, 1))) @ h + 0.1 * np.eye(users)
+    xr, er = port.batched("nn", g, 2, 4, threads=8)
+    assert max(rel_frob(x[s], xr[s]) for s in range(24)) < 1e-9  # Gram rounding differs (DMMA vs numpy)
+    z = np.einsum("bau,ba->bu", np.conj(h), y)
+    xhat_ref = np.einsum("buv,bv->bu", xr, z)
+    assert max(rel_frob(xh[s], xhat_ref[s]) for s in range(24)) < 1e-9
+    if users == 8:  # 8 users over 128 antennas: 4 nests converge, QPSK symbols recovered at 10 dB
+        assert np.mean((np.sign(xh.real) == np.sign(sym.real)) & (np.sign(xh.imag) == np.sign(sym.imag))) > 0.95

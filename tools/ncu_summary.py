@@ -23,6 +23,16 @@ KEYS = [
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", ""),
     ("lts__t_bytes.sum", "L2 traffic"),
     ("sm__cycles_elapsed.avg", ""), ("smsp__cycles_active.avg", ""),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe (tcgen05) active, elapsed"),
+    ("sm__pipe_tensor_subpipe_imma_cycles_active_realtime.avg", "int8 (IMMA) subpipe cycles"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit rate"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem reads by the tensor core"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots active"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe"),
+    ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "ALU pipe"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("gpc__cycles_elapsed.avg.per_second", "SM clock"),
 ]
 
 
