@@ -1172,6 +1172,36 @@ int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* 
     bool fits = false;
     if (!(dict.code && dict.ell_width) && !dict.rcode) NNB_TRY(compact_csr(row_ptr, col, n, 0, rp32, col16, &fits, s));
     fits = fits && !force32;
+    // 5-point stencils: temporal blocking, up to 8 applications per pass through HBM
+    static const bool tb_on = [] {  // NNB_SPARSE_TB=0: one launch per application (A/B measurement)
+      const char* e = debug_env("NNB_SPARSE_TB");
+      return !(e && std::strcmp(e, "0") == 0);
+    }();
+    if (dict.rcode && tb_on && k == 1 && s_factors <= 62) {
+      DevBuf table;
+      int W = 0, H = 0;
+      bool sok = false;
+      NNB_TRY(stencil_plan(n, dict.rcode, dict.rpat, dict.rlen, dict.npat, dict.ell_width, table, &W, &H, &sok, s));
+      if (sok) {
+        int64_t moved = 0;
+        NNB_TRY(stencil_factors(dict.rcode, table, dict.npat, W, H, B, s_factors, theta, X, z, tb, flags, &moved, s));
+        set_sparse_bytes_per_nnz(1);
+        set_sparse_format("row-dictionary-stencil-tb");
+        // per application, averaged over the solve (the bench multiplies by the applications)
+        const int64_t apps = (int64_t(1) << s_factors) - 1;
+        set_sparse_matrix_bytes(moved / std::max<int64_t>(1, apps) - 2 * n * 8);
+        NNB_CUDA(cudaGetLastError());
+        int hf[64];
+        NNB_CUDA(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, s));
+        NNB_CUDA(cudaStreamSynchronize(s));
+        for (int f = 0; f < s_factors && f < 64; ++f)
+          if (hf[f]) {
+            if (fail_factor) *fail_factor = f;
+            return fail(3, "solve_sparse_factorized: non-finite block at factor " + std::to_string(f));
+          }
+        return 0;
+      }
+    }
     set_sparse_bytes_per_nnz(dict.code || dict.rcode ? 1 : (fits ? 10 : 12));
     set_sparse_format(dict.rcode ? "row-dictionary"
                       : dict.ell_width ? "pair-dictionary-ell"

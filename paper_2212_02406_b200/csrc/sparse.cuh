@@ -93,6 +93,18 @@ void spmv_apply(const SpmvOp<Idx>& op, int mode, int64_t r_begin, int64_t r_end,
 
 int narrow_offsets(const int64_t* in, int32_t* out, int64_t count, int64_t base, cudaStream_t s);
 
+// Temporal blocking for 5-point-stencil operators (sparse_stencil.cu): from the row
+// dictionary, *ok when every pattern is a CSR-ordered subset of {−W, −1, 0, +1, +W}
+// for one W with n = W·H and no pattern reaches across the grid's edges; `table`
+// then holds the device pattern table.
+int stencil_plan(int64_t n, const uint8_t* rcode, const double2* pat, const uint8_t* plen, int npat, int width,
+                 DevBuf& table, int* W, int* H, bool* ok, cudaStream_t s);
+// The whole factorized solve (one RHS) in passes of up to 8 applications per launch;
+// bit-identical to run_factors.  *bytes_moved: HBM bytes the passes stream.
+int stencil_factors(const uint8_t* rcode, const DevBuf& table, int npat, int W, int H, const double* B,
+                    int s_factors, double theta, double* X, double* z[2], double* tb[2], int* flags,
+                    int64_t* bytes_moved, cudaStream_t s);
+
 // rp32[r] = rp[r] − rp[0] and col16[e] = col[e] − (row0 + r) for `rows` rows
 // (col indexed by rp).  Returns 0 and sets *fits = false when some delta does
 // not fit in int16 (col16 is then garbage; use int32 columns).

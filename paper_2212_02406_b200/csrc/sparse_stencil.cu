@@ -1,0 +1,318 @@
+// Temporal blocking of the factorized sparse solve for 5-point-stencil operators
+// (BASELINE config 4: the 4096² Dirichlet Laplacian + I).
+//
+// solve_sparse_factorized (proj/src/factorized.cpp:101-140) runs, per factor f,
+// 2^f applications t ← t − θ·W·t — 63 for γ = 63.  One launch per application
+// streams t in and out of HBM each time (68 µs at 4096², sparse.cu K8).  When the
+// row dictionary shows a 5-point stencil — every row pattern's deltas are a subset
+// of {−W, −1, 0, +1, +W} in that (CSR) order, rows at x = 0 / W−1 have no −1 / +1
+// entry, n = W·H — a block instead loads a 2-D tile of t with an S-cell halo into
+// shared memory and runs S applications there (the valid region shrinks by one cell
+// per step), writing only the tile's interior: HBM traffic falls ≈S-fold.
+//
+// Exactness: each row is still computed as the reference does — y summed from 0 in
+// CSR order with one rounded multiply and one rounded add per entry, then
+// fused_axpy_sub / add / scale exactly as sparse.cu's finish<> — from bitwise the
+// same inputs, so x is bit-identical to the reference and to the one-launch kernels
+// (tests: array_equal, and the 4096² SHA-256 golden).
+//
+// Layout: a 1008-thread block owns a TX × TY = 128 × 64 output tile; its region is
+// (TX + 2S) × (TY + 2S) = 144 × 80 cells, two double buffers (ping-pong between
+// steps) and one code byte per cell: 196 KB of shared memory, filled by cp.async
+// (the whole region in flight at once).  Thread (cx, seg) sweeps column cx over a
+// 12-row segment with the column's y−1 / y / y+1 values in
+// registers (a sliding window), so a cell costs three shared loads (own row below,
+// left, right) and one store; a row's pattern (mask + 5 values) is reloaded only
+// when its code changes along the sweep.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "engine.cuh"
+#include "sparse.cuh"
+
+namespace nnb {
+namespace {
+
+constexpr int kTX = 128, kTY = 64, kS = 8;
+constexpr int kRX = kTX + 2 * kS, kRY = kTY + 2 * kS;  // 144 × 80
+constexpr int kSeg = 7, kSegRows = (kRY + kSeg - 1) / kSeg;  // 7 segments of <= 12 rows
+constexpr int kThreads = kRX * kSeg;                         // 1008 (31.5 warps)
+constexpr int kSmem = 2 * kRX * kRY * 8 + kRX * kRY + kRowDictMax * 48;
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+struct StPat {
+  double v[5];  // values of the N (−W), W (−1), C (0), E (+1), S (+W) entries present
+  int mask;     // bit i: direction i present
+  int pad;
+};
+
+// One thread's column segment of one step.  UNI: the whole tile is one full 5-point
+// pattern (no per-cell code lookups); else each cell's pattern from its code.
+template <int MODE, bool UNI>
+__device__ __forceinline__ bool sweep(const double* __restrict__ src, double* __restrict__ dst,
+                                      const uint8_t* __restrict__ code, const StPat* __restrict__ spat, int uc,
+                                      int cx, int ya, int yb, int y0, int gx, int W, double theta, bool last,
+                                      double* __restrict__ out) {
+  bool bad = false;
+  const double* col = src + cx;
+  double tN = col[(ya - 1) * kRX], tC = col[ya * kRX];
+  int pc = UNI ? uc : -1;
+  int mask = 31;
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
+  if (UNI) {
+    v0 = spat[uc].v[0];
+    v1 = spat[uc].v[1];
+    v2 = spat[uc].v[2];
+    v3 = spat[uc].v[3];
+    v4 = spat[uc].v[4];
+  }
+  for (int y = ya; y < yb; ++y) {
+    const double tS = col[(y + 1) * kRX];
+    const double tW = col[y * kRX - 1], tE = col[y * kRX + 1];
+    double acc;  // CSR order: −W, −1, 0, +1, +W, from 0
+    if (UNI) {
+      acc = __dadd_rn(0.0, __dmul_rn(v0, tN));
+      acc = __dadd_rn(acc, __dmul_rn(v1, tW));
+      acc = __dadd_rn(acc, __dmul_rn(v2, tC));
+      acc = __dadd_rn(acc, __dmul_rn(v3, tE));
+      acc = __dadd_rn(acc, __dmul_rn(v4, tS));
+    } else {
+      const int c = code[y * kRX + cx];
+      if (c != pc) {
+        const StPat& P = spat[c];
+        v0 = P.v[0];
+        v1 = P.v[1];
+        v2 = P.v[2];
+        v3 = P.v[3];
+        v4 = P.v[4];
+        mask = P.mask;
+        pc = c;
+      }
+      acc = 0.0;
+      if (mask & 1) acc = __dadd_rn(acc, __dmul_rn(v0, tN));
+      if (mask & 2) acc = __dadd_rn(acc, __dmul_rn(v1, tW));
+      if (mask & 4) acc = __dadd_rn(acc, __dmul_rn(v2, tC));
+      if (mask & 8) acc = __dadd_rn(acc, __dmul_rn(v3, tE));
+      if (mask & 16) acc = __dadd_rn(acc, __dmul_rn(v4, tS));
+    }
+    const double t = __dsub_rn(tC, __dmul_rn(theta, acc));  // fused_axpy_sub, factorized.cpp:21-30
+    if (last) {
+      // a non-finite value persists in its cell (t keeps its own term) and every cell is
+      // some block's interior, so the pass's outputs see it: checking them flags the
+      // same factor the reference's per-application check would
+      const int64_t r = (int64_t)(y0 + y) * W + gx;
+      double o = t;
+      if (MODE == kFactorEnd) o = __dadd_rn(dst[y * kRX + cx], t);                    // factorized.cpp:136
+      else if (MODE == kFinal) o = __dmul_rn(__dadd_rn(dst[y * kRX + cx], t), theta);  // factorized.cpp:139
+      bad |= !isfinite(acc) || !isfinite(t) || !isfinite(o);
+      out[r] = o;
+    } else {
+      dst[y * kRX + cx] = t;
+    }
+    tN = tC;
+    tC = tS;
+  }
+  return bad;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    stencil_tb_kernel(const double* __restrict__ tin, const uint8_t* __restrict__ rcode,
+                      const double* __restrict__ zold, double* __restrict__ out, const StPat* __restrict__ pats,
+                      int npat, int W, int H, int steps, double theta, int* __restrict__ flag) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  double* buf0 = reinterpret_cast<double*>(sm);
+  double* buf1 = buf0 + kRX * kRY;
+  StPat* spat = reinterpret_cast<StPat*>(buf1 + kRX * kRY);
+  uint8_t* code = reinterpret_cast<uint8_t*>(spat + kRowDictMax);
+  const int x0 = blockIdx.x * kTX - kS, y0 = blockIdx.y * kTY - kS;
+  for (int i = threadIdx.x; i < npat; i += kThreads) spat[i] = pats[i];
+  // the region through cp.async (all of it in flight at once; cells off the grid zero-filled)
+#pragma unroll
+  for (int j = 0; j < (kRX * kRY + kThreads - 1) / kThreads; ++j) {
+    const int i = threadIdx.x + j * kThreads;
+    if (i >= kRX * kRY) break;
+    const int gx = x0 + i % kRX, gy = y0 + i / kRX;
+    const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
+    cp_async8(buf0 + i, in ? tin + (int64_t)gy * W + gx : tin, in);
+  }
+  for (int i = threadIdx.x; i < kRX * kRY / 4; i += kThreads) {  // codes in 4-byte groups (W % 4 == 0)
+    const int gx = x0 + (4 * i) % kRX, gy = y0 + (4 * i) / kRX;
+    const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
+    cp_async4(code + 4 * i, in ? rcode + (int64_t)gy * W + gx : rcode, in);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  // a tile whose whole region is one full 5-point pattern (all but the grid's edge
+  // tiles) skips the per-cell code lookups
+  int uc = code[0];
+  bool uniform = spat[uc].mask == 31 && x0 >= 0 && y0 >= 0 && x0 + kRX <= W && y0 + kRY <= H;
+  for (int i = threadIdx.x; i < kRX * kRY && uniform; i += kThreads) uniform = code[i] == uc;
+  uniform = __syncthreads_and(uniform);
+  const int cx = threadIdx.x % kRX, seg = threadIdx.x / kRX;
+  const int gx = x0 + cx;
+  const bool col_in = gx >= 0 && gx < W;
+  bool bad = false;
+  for (int s = 1; s <= steps; ++s) {
+    const double* src = (s & 1) ? buf0 : buf1;
+    double* dst = (s & 1) ? buf1 : buf0;
+    const int m = steps - s;  // cells still needed beyond the interior after this step
+    const int xlo = kS - m, xhi = kS + kTX + m, ylo = kS - m, yhi = kS + kTY + m;
+    const bool last = s == steps;
+    if (last && MODE != kInner) {  // Z of the interior into the free buffer, one wait per pass
+      for (int i = threadIdx.x; i < kTX * kTY; i += kThreads) {
+        const int rx = kS + i % kTX, ry = kS + i / kTX;
+        const int gxx = x0 + rx, gyy = y0 + ry;
+        const bool in = gxx < W && gyy < H;
+        cp_async8(dst + ry * kRX + rx, in ? zold + (int64_t)gyy * W + gxx : zold, in);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+    }
+    if (cx >= xlo && cx < xhi && col_in) {
+      // this thread's rows of the step, clipped to the grid (rows off it are never read)
+      const int ya = max(max(seg * kSegRows, ylo), -y0);
+      const int yb = min(min(min(seg * kSegRows + kSegRows, kRY), yhi), H - y0);
+      if (ya < yb) {
+        if (uniform) bad |= sweep<MODE, true>(src, dst, code, spat, uc, cx, ya, yb, y0, gx, W, theta, last, out);
+        else bad |= sweep<MODE, false>(src, dst, code, spat, uc, cx, ya, yb, y0, gx, W, theta, last, out);
+      }
+    }
+    if (!last) __syncthreads();
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// rows on the grid's edges whose pattern reaches across it (x wrap or out of range)
+__global__ void stencil_edge_check(const uint8_t* __restrict__ rcode, const StPat* __restrict__ pats, int W, int H,
+                                   int* __restrict__ bad) {
+  const int64_t per = 2LL * W + 2LL * H;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < per; i += (int64_t)gridDim.x * blockDim.x) {
+    int x, y, forbid;
+    if (i < W) { x = (int)i; y = 0; forbid = 1; }                        // top row: no −W
+    else if (i < 2LL * W) { x = (int)(i - W); y = H - 1; forbid = 16; }  // bottom row: no +W
+    else if (i < 2LL * W + H) { x = 0; y = (int)(i - 2LL * W); forbid = 2; }  // left column: no −1
+    else { x = W - 1; y = (int)(i - 2LL * W - H); forbid = 8; }          // right column: no +1
+    const int m = pats[rcode[(int64_t)y * W + x]].mask;
+    if (m & forbid) atomicOr(bad, 1);
+  }
+}
+
+}  // namespace
+
+int stencil_plan(int64_t n, const uint8_t* rcode, const double2* pat, const uint8_t* plen, int npat, int width,
+                 DevBuf& table, int* W_out, int* H_out, bool* ok, cudaStream_t s) {
+  *ok = false;
+  if (npat < 1 || npat > kRowDictMax || width < 1 || width > kEllMaxWidth || n < 4) return 0;
+  std::vector<double2> hp((size_t)npat * width);
+  std::vector<uint8_t> hl(npat);
+  NNB_CUDA(cudaMemcpyAsync(hp.data(), pat, sizeof(double2) * hp.size(), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaMemcpyAsync(hl.data(), plen, npat, cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  int64_t w = 0;
+  for (int p = 0; p < npat; ++p)
+    for (int i = 0; i < hl[p]; ++i) {
+      int64_t d;
+      std::memcpy(&d, &hp[(size_t)p * width + i].y, 8);
+      if (d != 0 && d != 1 && d != -1) {
+        if (w && std::llabs(d) != w) return 0;
+        w = std::llabs(d);
+      }
+    }
+  if (w < 4 || w % 4 != 0 || n % w != 0 || w > INT32_MAX || n / w > INT32_MAX) return 0;
+  std::vector<StPat> tab(npat);
+  for (int p = 0; p < npat; ++p) {
+    StPat sp{};
+    int last_dir = -1;
+    for (int i = 0; i < hl[p]; ++i) {
+      int64_t d;
+      std::memcpy(&d, &hp[(size_t)p * width + i].y, 8);
+      const int dir = d == -w ? 0 : d == -1 ? 1 : d == 0 ? 2 : d == 1 ? 3 : 4;
+      if (dir <= last_dir) return 0;  // repeated or out-of-order entries: not the CSR order assumed
+      last_dir = dir;
+      sp.v[dir] = hp[(size_t)p * width + i].x;
+      sp.mask |= 1 << dir;
+    }
+    tab[p] = sp;
+  }
+  NNB_TRY(table.alloc(sizeof(StPat) * npat + sizeof(int), s));
+  NNB_CUDA(cudaMemcpyAsync(table.p, tab.data(), sizeof(StPat) * npat, cudaMemcpyHostToDevice, s));
+  int* bad = reinterpret_cast<int*>(table.as<StPat>() + npat);
+  NNB_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  const int W = (int)w, H = (int)(n / w);
+  stencil_edge_check<<<148, 256, 0, s>>>(rcode, table.as<StPat>(), W, H, bad);
+  count_launch();
+  int hbad = 1;
+  NNB_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  if (hbad) return 0;
+  *W_out = W;
+  *H_out = H;
+  *ok = true;
+  return 0;
+}
+
+int stencil_factors(const uint8_t* rcode, const DevBuf& table, int npat, int W, int H, const double* B,
+                    int s_factors, double theta, double* X, double* z[2], double* tb[2], int* flags,
+                    int64_t* bytes_moved, cudaStream_t s) {
+  NNB_TRY(ensure_smem<stencil_tb_kernel<kInner>>(kSmem));
+  NNB_TRY(ensure_smem<stencil_tb_kernel<kFactorEnd>>(kSmem));
+  NNB_TRY(ensure_smem<stencil_tb_kernel<kFinal>>(kSmem));
+  const dim3 grid((unsigned)((W + kTX - 1) / kTX), (unsigned)((H + kTY - 1) / kTY));
+  const StPat* pats = table.as<StPat>();
+  const double n = (double)W * H;
+  const double halo = (double)kRX * kRY / ((double)kTX * kTY);  // region cells read per output cell
+  double moved = 0.0;
+  const double* zcur = B;
+  int zi = 0;
+  for (int f = 0; f < s_factors; ++f) {
+    int64_t left = int64_t(1) << f;
+    const double* tin = zcur;
+    int ti = 0;
+    while (left > 0) {
+      const int steps = (int)std::min<int64_t>(kS, left);
+      left -= steps;
+      const int mode = left > 0 ? kInner : (f == s_factors - 1 ? kFinal : kFactorEnd);
+      double* out = mode == kInner ? tb[ti] : (mode == kFinal ? X : z[zi]);
+      switch (mode) {
+        case kInner:
+          stencil_tb_kernel<kInner><<<grid, kThreads, kSmem, s>>>(tin, rcode, zcur, out, pats, npat, W, H, steps,
+                                                                  theta, flags + f);
+          break;
+        case kFactorEnd:
+          stencil_tb_kernel<kFactorEnd><<<grid, kThreads, kSmem, s>>>(tin, rcode, zcur, out, pats, npat, W, H,
+                                                                      steps, theta, flags + f);
+          break;
+        default:
+          stencil_tb_kernel<kFinal><<<grid, kThreads, kSmem, s>>>(tin, rcode, zcur, out, pats, npat, W, H, steps,
+                                                                  theta, flags + f);
+      }
+      count_launch();
+      NNB_CUDA(cudaGetLastError());
+      moved += n * (halo * (8.0 + 1.0) + 8.0 + (mode == kInner ? 0.0 : 8.0));
+      if (mode == kInner) {
+        tin = tb[ti];
+        ti ^= 1;
+      } else if (mode == kFactorEnd) {
+        zcur = z[zi];
+        zi ^= 1;
+      }
+    }
+  }
+  if (bytes_moved) *bytes_moved = (int64_t)moved;
+  return 0;
+}
+
+}  // namespace nnb
