@@ -263,7 +263,7 @@ def run_dense(args, world, rank):
         # CUDA events on its stream; work = s moduli x 2*M*N*K int8 ops per launch
         achieved = g["work"] / (g["ms"] * 1e-3) / 1e12
         per_launch = g["work"] / g["launches"]
-        moduli = nnb.ozaki_moduli(n)
+        moduli = round(per_launch / (2.0 * rows_here * n * n))  # moduli the products actually used
         roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": INT8_PEAK_TOPS, "unit": "TFLOP/s",
                 "frac": round(achieved / INT8_PEAK_TOPS, 4),
                 "traffic": ncu_traffic("oz_gemm_n32768") if n == 32768 and world == 1 else None,
@@ -678,6 +678,31 @@ def run_sparse(args, world, rank):
            "csr-int16-delta": "f64 values + int16 column deltas, int32 row offsets",
            "csr-int32": "f64 values + int32 columns, row offsets"}.get(fname, fname)
     mat = sum_over_ranks(world, float(nnb.sparse_last_matrix_bytes())) if sharded else nnb.sparse_last_matrix_bytes()
+    general = None
+    if not sharded:
+        # the same operator shape with per-entry random weights (no value dictionary applies):
+        # the general-CSR rate (int16 column deltas + f64 values), beside the stencil formats
+        rng = np.random.default_rng(11)
+        val_g = val.copy()
+        off = val_g != 5.0
+        val_g[off] = -rng.uniform(0.5, 1.0, int(off.sum()))
+        csr_g = nnb.Csr(dev(rp), dev(col), dev(val_g), n=n, nnz=col.size)
+        for _ in range(2):
+            nnb.solve_sparse_factorized(csr_g, b, 63, norm)
+        e0.record()
+        for _ in range(3):
+            nnb.solve_sparse_factorized(csr_g, b, 63, norm)
+        e1.record()
+        torch.cuda.synchronize()
+        ms_g = e0.elapsed_time(e1) / 3
+        fb_g = nnb.sparse_last_bytes_per_nnz()
+        mat_g = nnb.sparse_last_matrix_bytes()
+        general = {"ms_per_step": round(ms_g, 3), "format": nnb.sparse_last_format(),
+                   "gbs_algorithmic": round(63 * sparse_bytes(n, col.size, 12) / (ms_g * 1e-3) / 1e9, 1),
+                   "frac_hbm_consumed_format": round(63 * (mat_g + 2 * n * 8) / (ms_g * 1e-3) / 1e9 / HBM_PEAK, 4),
+                   "bytes_per_nnz": fb_g,
+                   "note": "same 4096^2 5-point pattern, off-diagonal values random in [-1, -0.5]: no dictionary"}
+        del csr_g
     alg = 63 * sparse_bytes(n, col.size, 12)  # SURVEY §8(d) algorithmic bytes per solve: the work unit
     moved = 63 * (mat + 2 * n * 8)  # bytes of the consumed format (operator + t in + t out): the roofline
     gbs, moved_gbs = alg / (ms * 1e-3) / 1e9, moved / (ms * 1e-3) / 1e9
@@ -685,6 +710,7 @@ def run_sparse(args, world, rank):
                       "bytes: 12 B per nonzero)", "value": round(gbs, 1),
             "unit": "GB/s", "ms_per_step": round(ms, 3), "format": fname, "format_bytes_per_nnz": fb,
             "planned_ms_per_step": None if planned_ms is None else round(planned_ms, 3),
+            "general_csr": general,
             "parallelism": f"row slabs x{world}, NCCL halo exchange" if sharded else "single GPU",
             "roofline": {"bound": "hbm", "achieved": round(moved_gbs, 1), "peak": HBM_PEAK * world, "unit": "GB/s",
                          "frac": round(moved_gbs / (HBM_PEAK * world), 4),

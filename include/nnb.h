@@ -122,7 +122,8 @@ int32_t nnb_get_arithmetic(void);
  * device buffer R_out (n×n, leading dimension ldr).  A test hook for sampling the
  * chain's own R at sizes no CPU oracle reaches (SURVEY §8(c) C4 item iii). */
 int nnb_chain_capture_residual(double* R_out, int64_t ldr);
-/* Moduli (= int8 GEMMs per product) NNB_ARITH_OZAKI uses for inner dimension k. */
+/* Most moduli (= int8 GEMMs per product) NNB_ARITH_OZAKI uses for inner dimension k; a
+ * product uses fewer when its operands' L1/max ratios bound the integer product lower. */
 int32_t nnb_ozaki_moduli(int64_t k);
 /* Live timing of the emulation's kernels (for roofline reporting): while on, every
  * int8 GEMM / operand split / reconstruction launch is bracketed by CUDA events on its

@@ -429,41 +429,57 @@ __device__ __forceinline__ int resid(double a, double m, double inv_m) {
   return ri;
 }
 
-// Left operand: per-row scaling.  One 256-thread block per row:
-// out[l][row][kp] int8 residues (zero-padded from k to kp), exps[row].
-__global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __restrict__ X, int64_t ld, int rows,
-                                                            int k, int64_t kp, int8_t* __restrict__ out,
-                                                            int* __restrict__ exps, const OzConst cst) {
-  __shared__ double smax[8];
+// Left operand, pass 1: one 256-thread block per row: the row's exponent (exps[row])
+// and its L1/max ratio, folded into *ratio (float bits, atomic max): Σ_k |a'_ik| <=
+// ratio·2^53 bounds the integer product (the moduli count follows from it).
+__global__ void __launch_bounds__(256) oz_rowstat_kernel(const double* __restrict__ X, int64_t ld, int rows, int k,
+                                                         int* __restrict__ exps, unsigned* __restrict__ ratio) {
+  __shared__ double smax[8], ssum[8];
   __shared__ int sbad[8];
   const int row = blockIdx.x;
   const double* xr = X + (int64_t)row * ld;
-  double mx = 0.0;
+  double mx = 0.0, sum = 0.0;
   int bad = 0;
   for (int c = threadIdx.x; c < k; c += 256) {
     const double v = xr[c];
     bad |= !isfinite(v);
     mx = fmax(mx, fabs(v));
+    sum += fabs(v);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
     bad |= __shfl_xor_sync(0xffffffffu, bad, o);
   }
   if ((threadIdx.x & 31) == 0) {
     smax[threadIdx.x >> 5] = mx;
+    ssum[threadIdx.x >> 5] = sum;
     sbad[threadIdx.x >> 5] = bad;
   }
   __syncthreads();
-  mx = 0.0;
-  bad = 0;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    mx = fmax(mx, smax[w]);
-    bad |= sbad[w];
+  if (threadIdx.x == 0) {
+    mx = 0.0;
+    sum = 0.0;
+    bad = 0;
+    for (int w = 0; w < 8; ++w) {
+      mx = fmax(mx, smax[w]);
+      sum += ssum[w];
+      bad |= sbad[w];
+    }
+    exps[row] = bad ? kBadExp : exp_for(mx);
+    if (!bad && mx > 0.0) atomicMax(ratio, __float_as_uint(static_cast<float>(sum / mx) * 1.0001f));
   }
-  const int e = bad ? kBadExp : exp_for(mx);
-  if (threadIdx.x == 0) exps[row] = e;
+}
+
+// Left operand, pass 2: out[l][row][kp] int8 residues for s moduli (zero-padded from k).
+__global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __restrict__ X, int64_t ld, int rows,
+                                                            int k, int64_t kp, int8_t* __restrict__ out,
+                                                            const int* __restrict__ exps, const OzConst cst) {
+  const int row = blockIdx.x;
+  const double* xr = X + (int64_t)row * ld;
+  const int e = exps[row];
+  const bool bad = e == kBadExp;
   const int s = cst.s;
   for (int64_t c0 = threadIdx.x * 8; c0 < kp; c0 += 256 * 8) {
     double a[8];
@@ -479,11 +495,7 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
       for (int j = 0; j < 4; ++j) lo |= (static_cast<uint32_t>(resid(a[j], m, inv)) & 0xffu) << (8 * j);
 #pragma unroll
       for (int j = 0; j < 4; ++j) hi |= (static_cast<uint32_t>(resid(a[4 + j], m, inv)) & 0xffu) << (8 * j);
-      if (c0 + 8 <= kp) {
-        *reinterpret_cast<uint2*>(out + ((int64_t)l * rows + row) * kp + c0) = make_uint2(lo, hi);
-      } else {  // kp is a multiple of 16 and c0 of 8: never partial, kept for safety
-        *reinterpret_cast<uint32_t*>(out + ((int64_t)l * rows + row) * kp + c0) = lo;
-      }
+      *reinterpret_cast<uint2*>(out + ((int64_t)l * rows + row) * kp + c0) = make_uint2(lo, hi);
     }
   }
 }
@@ -491,28 +503,46 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
 // Right operand, pass 1: per-column max |b| (as ordered bits) and non-finite flags.
 __global__ void __launch_bounds__(256) oz_colmax_kernel(const double* __restrict__ B, int64_t ld, int k, int n,
                                                         unsigned long long* __restrict__ colmax,
-                                                        int* __restrict__ colbad) {
+                                                        double* __restrict__ colsum, int* __restrict__ colbad) {
   const int c = blockIdx.x * 256 + threadIdx.x;
   if (c >= n) return;
   const int r0 = blockIdx.y * 256, r1 = min(k, r0 + 256);
-  double mx = 0.0;
+  double mx = 0.0, sum = 0.0;
   int bad = 0;
   for (int r = r0; r < r1; ++r) {
     const double v = B[(int64_t)r * ld + c];
     bad |= !isfinite(v);
     mx = fmax(mx, fabs(v));
+    sum += fabs(v);
   }
   if (mx > 0.0) atomicMax(colmax + c, static_cast<unsigned long long>(__double_as_longlong(mx)));
+  if (sum > 0.0) atomicAdd(colsum + c, sum);  // a bound only: its summation order does not matter
   if (bad) atomicOr(colbad + c, 1);
+}
+
+// Right operand, pass 1b: column exponents and the L1/max ratio bound (as rows above)
+__global__ void __launch_bounds__(256) oz_colratio_kernel(const unsigned long long* __restrict__ colmax,
+                                                          const double* __restrict__ colsum,
+                                                          const int* __restrict__ colbad, int n,
+                                                          int* __restrict__ exps, unsigned* __restrict__ ratio) {
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  float r = 0.0f;
+  if (c < n) {
+    const double mx = __longlong_as_double(static_cast<long long>(colmax[c]));
+    const bool bad = colbad[c] != 0;
+    exps[c] = bad ? kBadExp : exp_for(mx);
+    if (!bad && mx > 0.0) r = static_cast<float>(colsum[c] / mx) * 1.0001f;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r = fmaxf(r, __shfl_xor_sync(0xffffffffu, r, o));
+  if ((threadIdx.x & 31) == 0 && r > 0.0f) atomicMax(ratio, __float_as_uint(r));
 }
 
 // Right operand, pass 2: 64(k)×64(n) tiles transposed through shared memory into
 // K-major residues out[l][col][kp]; exps[col] written by the first k-tile row.
 __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __restrict__ B, int64_t ld, int k, int n,
-                                                            int64_t kp, const unsigned long long* __restrict__ colmax,
-                                                            const int* __restrict__ colbad,
-                                                            int8_t* __restrict__ out, int* __restrict__ exps,
-                                                            const OzConst cst) {
+                                                            int64_t kp, int8_t* __restrict__ out,
+                                                            const int* __restrict__ exps, const OzConst cst) {
   __shared__ double tile[64][65];
   const int n0 = blockIdx.x * 64, k0 = blockIdx.y * 64;
   for (int i = threadIdx.x; i < 64 * 64; i += 256) {
@@ -524,9 +554,8 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
   const int nn = threadIdx.x >> 2, kc = (threadIdx.x & 3) * 16;
   const int col = n0 + nn;
   if (col >= n) return;
-  const bool bad = colbad[col] != 0;
-  const int e = bad ? kBadExp : exp_for(__longlong_as_double(static_cast<long long>(colmax[col])));
-  if (blockIdx.y == 0 && kc == 0) exps[col] = e;
+  const int e = exps[col];
+  const bool bad = e == kBadExp;
   if (k0 + kc >= kp) return;
   double a[16];
 #pragma unroll
@@ -718,46 +747,65 @@ struct OzOperand {
   int s = 0;
 };
 
-int split_left(const double* A, int64_t lda, int64_t rows, int64_t k, const OzConst& c, OzOperand& o,
-               cudaStream_t st) {
+// Pass 1 of an operand: exponents and the L1/max ratio (into *ratio on the device).
+// `left`: per-row scaling of a rows×k row-major operand; else per-column scaling of a
+// k×n row-major right operand (n = rows of its K-major residues).
+int operand_stats(const double* X, int64_t ld, int64_t rows, int64_t k, bool left, OzOperand& o, unsigned* ratio,
+                  cudaStream_t st) {
   o.rows = rows;
   o.k = k;
   o.kp = (k + 15) / 16 * 16;
-  o.s = c.s;
-  NNB_TRY(o.res.alloc((size_t)c.s * rows * o.kp, st));
+  o.s = 0;
   NNB_TRY(o.exps.alloc(sizeof(int) * std::max<int64_t>(rows, 1), st));
-  Timed tm(1, (double)rows * k * (8.0 + c.s), st);  // algorithmic bytes: 8 B in, s B out per entry
-  oz_split_rows_kernel<<<static_cast<unsigned>(rows), 256, 0, st>>>(A, lda, (int)rows, (int)k, o.kp,
-                                                                      o.res.as<int8_t>(), o.exps.as<int>(), c);
+  Timed tm(1, (double)rows * k * 8.0, st);  // one read of the operand
+  if (left) {
+    oz_rowstat_kernel<<<static_cast<unsigned>(rows), 256, 0, st>>>(X, ld, (int)rows, (int)k, o.exps.as<int>(),
+                                                                    ratio);
+    count_launch();
+  } else {
+    const int64_t n = rows;
+    DevBuf cm;
+    NNB_TRY(cm.alloc((sizeof(unsigned long long) + sizeof(double) + sizeof(int)) * n, st));
+    unsigned long long* colmax = cm.as<unsigned long long>();
+    double* colsum = reinterpret_cast<double*>(colmax + n);
+    int* colbad = reinterpret_cast<int*>(colsum + n);
+    NNB_CUDA(cudaMemsetAsync(cm.p, 0, cm.bytes, st));
+    oz_colmax_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)((k + 255) / 256)), 256, 0, st>>>(
+        X, ld, (int)k, (int)n, colmax, colsum, colbad);
+    oz_colratio_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(colmax, colsum, colbad, (int)n,
+                                                                   o.exps.as<int>(), ratio);
+    count_launch(2);
+  }
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// Pass 2: residues for c.s moduli (the operand's exponents from pass 1).
+int operand_residues(const double* X, int64_t ld, bool left, const OzConst& c, OzOperand& o, cudaStream_t st) {
+  NNB_TRY(o.res.alloc((size_t)c.s * o.rows * o.kp, st));
+  o.s = c.s;
+  Timed tm(1, (double)o.rows * o.k * (8.0 + c.s), st);  // 8 B in, s B out per entry
+  if (left) {
+    oz_split_rows_kernel<<<static_cast<unsigned>(o.rows), 256, 0, st>>>(X, ld, (int)o.rows, (int)o.k, o.kp,
+                                                                          o.res.as<int8_t>(), o.exps.as<int>(), c);
+  } else {
+    oz_split_cols_kernel<<<dim3((unsigned)((o.rows + 63) / 64), (unsigned)((o.kp + 63) / 64)), 256, 0, st>>>(
+        X, ld, (int)o.k, (int)o.rows, o.kp, o.res.as<int8_t>(), o.exps.as<int>(), c);
+  }
   count_launch();
   NNB_CUDA(cudaGetLastError());
   return 0;
 }
 
-// B is k×n row-major (ldb), or with kmajor its transpose Bᵀ (n×k row-major)
-int split_right(const double* B, int64_t ldb, int64_t k, int64_t n, bool kmajor, const OzConst& c, OzOperand& o,
-                cudaStream_t st) {
-  if (kmajor) return split_left(B, ldb, n, k, c, o, st);
-  o.rows = n;
-  o.k = k;
-  o.kp = (k + 15) / 16 * 16;
-  o.s = c.s;
-  NNB_TRY(o.res.alloc((size_t)c.s * n * o.kp, st));
-  NNB_TRY(o.exps.alloc(sizeof(int) * std::max<int64_t>(n, 1), st));
-  DevBuf cm;
-  NNB_TRY(cm.alloc((sizeof(unsigned long long) + sizeof(int)) * n, st));
-  unsigned long long* colmax = cm.as<unsigned long long>();
-  int* colbad = reinterpret_cast<int*>(colmax + n);
-  NNB_CUDA(cudaMemsetAsync(cm.p, 0, cm.bytes, st));
-  Timed tm(1, (double)n * k * (8.0 + 8.0 + c.s), st);  // column max pass + the split pass
-  oz_colmax_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)((k + 255) / 256)), 256, 0, st>>>(
-      B, ldb, (int)k, (int)n, colmax, colbad);
-  count_launch();
-  oz_split_cols_kernel<<<dim3((unsigned)((n + 63) / 64), (unsigned)((o.kp + 63) / 64)), 256, 0, st>>>(
-      B, ldb, (int)k, (int)n, o.kp, colmax, colbad, o.res.as<int8_t>(), o.exps.as<int>(), c);
-  count_launch();
-  NNB_CUDA(cudaGetLastError());
-  return 0;
+// moduli for |C'| <= ratio·2^106 < M/8 (the balanced Garner value is then C' itself)
+int moduli_for_ratio(double ratio) {
+  const double need = 2.0 * kAlpha + std::log2(std::max(ratio, 1.0)) + 3.0;
+  double have = 0.0;
+  for (int s = 0; s < kMaxMod; ++s) {
+    have += std::log2(static_cast<double>(kModuli[s]));
+    if (have >= need) return s + 1;
+  }
+  return kMaxMod;
 }
 
 int launch_recon(int s, const uint8_t* res, int64_t ldr, int M, int N, const int* ea, const int* eb,
@@ -787,8 +835,8 @@ struct Pinned {
   const double* p = nullptr;
   int64_t ld = 0, rows = 0, cols = 0;
   OzOperand left, right;
-  bool have_left = false, have_right = false;
-  int s_left = 0, s_right = 0;
+  bool have_left = false, have_right = false;  // exponents and ratio formed
+  float ratio_left = 0.0f, ratio_right = 0.0f;
 };
 thread_local std::vector<Pinned*> g_pins;  // at most a few: the chain's A, a chunked product's B
 
@@ -822,39 +870,62 @@ int gemm_ozaki(const GemmOp& op, cudaStream_t st) {
   const int64_t M = op.M, N = op.N, K = op.K;
   if (K > kMaxK) return fail(7, "ozaki: inner dimension above 131071 (int32 accumulation bound)");
   if (op.ep.C2 || op.ep.acc_in) return fail(7, "ozaki: dual-output and K-split epilogues are DMMA-only");
-  const int s = std::max(15, moduli_for(K));  // small k: 15 (the smallest instantiated set)
-  const OzConst c = make_const(s);
-  // operand splits (the pinned chain operand's are cached per role)
-  OzOperand la, rb;
-  const OzOperand* L = &la;
-  const OzOperand* R = &rb;
+  // Pass 1 of both operands: exponents, and the L1/max ratios that bound the integer
+  // product (|C'| <= min(rA, rB)·2^106) — the moduli count follows from them, so a
+  // product of the configs' matrices (ratios ~70) needs 15 moduli instead of the
+  // worst case's 16.  One small host read per product.
   auto find = [](const double* p) -> Pinned* {
     for (Pinned* q : g_pins)
       if (q->p == p) return q;
     return nullptr;
   };
-  Pinned* pin = find(op.A);
-  if (pin && op.lda == pin->ld && M == pin->rows && K == pin->cols) {
-    if (!pin->have_left || pin->s_left != s) {
-      NNB_TRY(split_left(op.A, op.lda, M, K, c, pin->left, st));
-      pin->have_left = true;
-      pin->s_left = s;
-    }
-    L = &pin->left;
+  static thread_local unsigned* ratio_host = nullptr;
+  if (!ratio_host) NNB_CUDA(cudaHostAlloc(&ratio_host, sizeof(unsigned) * 2, cudaHostAllocDefault));
+  DevBuf ratio_dev;
+  NNB_TRY(ratio_dev.alloc(sizeof(unsigned) * 2, st));
+  unsigned* rd = ratio_dev.as<unsigned>();
+  NNB_CUDA(cudaMemsetAsync(rd, 0, sizeof(unsigned) * 2, st));
+  OzOperand la, rb;
+  OzOperand* L = &la;
+  OzOperand* R = &rb;
+  Pinned* pa = find(op.A);
+  if (!(pa && op.lda == pa->ld && M == pa->rows && K == pa->cols)) pa = nullptr;
+  Pinned* pb = find(op.B);
+  if (!(pb && !op.b_kmajor && op.ldb == pb->ld && K == pb->rows && N == pb->cols)) pb = nullptr;
+  if (pa) {
+    L = &pa->left;
+    if (!pa->have_left) NNB_TRY(operand_stats(op.A, op.lda, M, K, true, *L, rd, st));
   } else {
-    NNB_TRY(split_left(op.A, op.lda, M, K, c, la, st));
+    NNB_TRY(operand_stats(op.A, op.lda, M, K, true, la, rd, st));
   }
-  pin = find(op.B);
-  if (pin && !op.b_kmajor && op.ldb == pin->ld && K == pin->rows && N == pin->cols) {
-    if (!pin->have_right || pin->s_right != s) {
-      NNB_TRY(split_right(op.B, op.ldb, K, N, false, c, pin->right, st));
-      pin->have_right = true;
-      pin->s_right = s;
-    }
-    R = &pin->right;
+  const bool right_as_rows = op.b_kmajor;  // Bᵀ given: its rows are B's columns
+  if (pb) {
+    R = &pb->right;
+    if (!pb->have_right) NNB_TRY(operand_stats(op.B, op.ldb, N, K, false, *R, rd + 1, st));
   } else {
-    NNB_TRY(split_right(op.B, op.ldb, K, N, op.b_kmajor, c, rb, st));
+    NNB_TRY(operand_stats(op.B, op.ldb, N, K, right_as_rows, rb, rd + 1, st));
   }
+  NNB_CUDA(cudaMemcpyAsync(ratio_host, rd, sizeof(unsigned) * 2, cudaMemcpyDeviceToHost, st));
+  NNB_CUDA(cudaStreamSynchronize(st));
+  float ra = pa && pa->have_left ? pa->ratio_left : __builtin_bit_cast(float, ratio_host[0]);
+  float rbv = pb && pb->have_right ? pb->ratio_right : __builtin_bit_cast(float, ratio_host[1]);
+  if (pa && !pa->have_left) {
+    pa->have_left = true;
+    pa->ratio_left = ra;
+  }
+  if (pb && !pb->have_right) {
+    pb->have_right = true;
+    pb->ratio_right = rbv;
+  }
+  // an operand with no finite nonzero row/column reads 0: its product is exact zeros
+  const double ratio = std::min(std::max((double)ra, 1.0), std::max((double)rbv, 1.0));
+  const int s = std::max(15, std::min(kMaxMod, moduli_for_ratio(std::min(ratio, (double)K))));
+  if (s > 17) return fail(7, "ozaki: more than 17 moduli needed");
+  const OzConst c = make_const(s);
+  // Pass 2: residues (a pinned operand keeps the planes it has when they suffice; the
+  // moduli are a fixed sequence, so a prefix of its planes is the residues for s)
+  if (L->s < s) NNB_TRY(operand_residues(op.A, op.lda, true, c, *L, st));
+  if (R->s < s) NNB_TRY(operand_residues(op.B, op.ldb, right_as_rows, c, *R, st));
   // s int8 GEMMs -> residues
   const int64_t ldr = (N + 15) / 16 * 16;
   DevBuf res;
