@@ -432,43 +432,53 @@ __device__ __forceinline__ int resid(double a, double m, double inv_m) {
 // Left operand, pass 1: one 256-thread block per row: the row's exponent (exps[row])
 // and its L1/max ratio, folded into *ratio (float bits, atomic max): Σ_k |a'_ik| <=
 // ratio·2^53 bounds the integer product (the moduli count follows from it).
+// ratio[0]: max L1/max, ratio[2]: max L2/max (float bits, atomic max); the caller
+// interleaves two operands' slots (ratio + 0 / + 1)
 __global__ void __launch_bounds__(256) oz_rowstat_kernel(const double* __restrict__ X, int64_t ld, int rows, int k,
                                                          int* __restrict__ exps, unsigned* __restrict__ ratio) {
-  __shared__ double smax[8], ssum[8];
+  __shared__ double smax[8], ssum[8], ssq[8];
   __shared__ int sbad[8];
   const int row = blockIdx.x;
   const double* xr = X + (int64_t)row * ld;
-  double mx = 0.0, sum = 0.0;
+  double mx = 0.0, sum = 0.0, sq = 0.0;
   int bad = 0;
   for (int c = threadIdx.x; c < k; c += 256) {
     const double v = xr[c];
     bad |= !isfinite(v);
     mx = fmax(mx, fabs(v));
     sum += fabs(v);
+    sq = fma(v, v, sq);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    sq += __shfl_xor_sync(0xffffffffu, sq, o);
     bad |= __shfl_xor_sync(0xffffffffu, bad, o);
   }
   if ((threadIdx.x & 31) == 0) {
     smax[threadIdx.x >> 5] = mx;
     ssum[threadIdx.x >> 5] = sum;
+    ssq[threadIdx.x >> 5] = sq;
     sbad[threadIdx.x >> 5] = bad;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     mx = 0.0;
     sum = 0.0;
+    sq = 0.0;
     bad = 0;
     for (int w = 0; w < 8; ++w) {
       mx = fmax(mx, smax[w]);
       sum += ssum[w];
+      sq += ssq[w];
       bad |= sbad[w];
     }
     exps[row] = bad ? kBadExp : exp_for(mx);
-    if (!bad && mx > 0.0) atomicMax(ratio, __float_as_uint(static_cast<float>(sum / mx) * 1.0001f));
+    if (!bad && mx > 0.0) {
+      atomicMax(ratio, __float_as_uint(static_cast<float>(sum / mx) * 1.0001f));
+      atomicMax(ratio + 2, __float_as_uint(static_cast<float>(sqrt(sq) / mx) * 1.0001f));
+    }
   }
 }
 
@@ -503,39 +513,54 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
 // Right operand, pass 1: per-column max |b| (as ordered bits) and non-finite flags.
 __global__ void __launch_bounds__(256) oz_colmax_kernel(const double* __restrict__ B, int64_t ld, int k, int n,
                                                         unsigned long long* __restrict__ colmax,
-                                                        double* __restrict__ colsum, int* __restrict__ colbad) {
+                                                        double* __restrict__ colsum, double* __restrict__ colsq,
+                                                        int* __restrict__ colbad) {
   const int c = blockIdx.x * 256 + threadIdx.x;
   if (c >= n) return;
   const int r0 = blockIdx.y * 256, r1 = min(k, r0 + 256);
-  double mx = 0.0, sum = 0.0;
+  double mx = 0.0, sum = 0.0, sq = 0.0;
   int bad = 0;
   for (int r = r0; r < r1; ++r) {
     const double v = B[(int64_t)r * ld + c];
     bad |= !isfinite(v);
     mx = fmax(mx, fabs(v));
     sum += fabs(v);
+    sq = fma(v, v, sq);
   }
   if (mx > 0.0) atomicMax(colmax + c, static_cast<unsigned long long>(__double_as_longlong(mx)));
-  if (sum > 0.0) atomicAdd(colsum + c, sum);  // a bound only: its summation order does not matter
+  if (sum > 0.0) {  // bounds only: their summation order does not matter
+    atomicAdd(colsum + c, sum);
+    atomicAdd(colsq + c, sq);
+  }
   if (bad) atomicOr(colbad + c, 1);
 }
 
 // Right operand, pass 1b: column exponents and the L1/max ratio bound (as rows above)
 __global__ void __launch_bounds__(256) oz_colratio_kernel(const unsigned long long* __restrict__ colmax,
                                                           const double* __restrict__ colsum,
+                                                          const double* __restrict__ colsq,
                                                           const int* __restrict__ colbad, int n,
                                                           int* __restrict__ exps, unsigned* __restrict__ ratio) {
   const int c = blockIdx.x * 256 + threadIdx.x;
-  float r = 0.0f;
+  float r = 0.0f, r2 = 0.0f;
   if (c < n) {
     const double mx = __longlong_as_double(static_cast<long long>(colmax[c]));
     const bool bad = colbad[c] != 0;
     exps[c] = bad ? kBadExp : exp_for(mx);
-    if (!bad && mx > 0.0) r = static_cast<float>(colsum[c] / mx) * 1.0001f;
+    if (!bad && mx > 0.0) {
+      r = static_cast<float>(colsum[c] / mx) * 1.0001f;
+      r2 = static_cast<float>(sqrt(colsq[c]) / mx) * 1.0001f;
+    }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) r = fmaxf(r, __shfl_xor_sync(0xffffffffu, r, o));
-  if ((threadIdx.x & 31) == 0 && r > 0.0f) atomicMax(ratio, __float_as_uint(r));
+  for (int o = 16; o > 0; o >>= 1) {
+    r = fmaxf(r, __shfl_xor_sync(0xffffffffu, r, o));
+    r2 = fmaxf(r2, __shfl_xor_sync(0xffffffffu, r2, o));
+  }
+  if ((threadIdx.x & 31) == 0 && r > 0.0f) {
+    atomicMax(ratio, __float_as_uint(r));
+    atomicMax(ratio + 2, __float_as_uint(r2));
+  }
 }
 
 // Right operand, pass 2: 64(k)×64(n) tiles transposed through shared memory into
@@ -765,14 +790,15 @@ int operand_stats(const double* X, int64_t ld, int64_t rows, int64_t k, bool lef
   } else {
     const int64_t n = rows;
     DevBuf cm;
-    NNB_TRY(cm.alloc((sizeof(unsigned long long) + sizeof(double) + sizeof(int)) * n, st));
+    NNB_TRY(cm.alloc((sizeof(unsigned long long) + 2 * sizeof(double) + sizeof(int)) * n, st));
     unsigned long long* colmax = cm.as<unsigned long long>();
     double* colsum = reinterpret_cast<double*>(colmax + n);
-    int* colbad = reinterpret_cast<int*>(colsum + n);
+    double* colsq = colsum + n;
+    int* colbad = reinterpret_cast<int*>(colsq + n);
     NNB_CUDA(cudaMemsetAsync(cm.p, 0, cm.bytes, st));
     oz_colmax_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)((k + 255) / 256)), 256, 0, st>>>(
-        X, ld, (int)k, (int)n, colmax, colsum, colbad);
-    oz_colratio_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(colmax, colsum, colbad, (int)n,
+        X, ld, (int)k, (int)n, colmax, colsum, colsq, colbad);
+    oz_colratio_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(colmax, colsum, colsq, colbad, (int)n,
                                                                    o.exps.as<int>(), ratio);
     count_launch(2);
   }
@@ -817,6 +843,7 @@ int launch_recon(int s, const uint8_t* res, int64_t ldr, int M, int N, const int
   case S:                                                                                   \
     oz_recon_kernel<S><<<grid, 256, 0, st>>>(res, ldr, M, N, ea, eb, ep, c);                \
     break;
+    NNB_OZ_RECON(14)
     NNB_OZ_RECON(15)
     NNB_OZ_RECON(16)
     NNB_OZ_RECON(17)
@@ -835,8 +862,8 @@ struct Pinned {
   const double* p = nullptr;
   int64_t ld = 0, rows = 0, cols = 0;
   OzOperand left, right;
-  bool have_left = false, have_right = false;  // exponents and ratio formed
-  float ratio_left = 0.0f, ratio_right = 0.0f;
+  bool have_left = false, have_right = false;  // exponents and ratios formed
+  float ratio_left = 0.0f, ratio_right = 0.0f, ratio_left2 = 0.0f, ratio_right2 = 0.0f;
 };
 thread_local std::vector<Pinned*> g_pins;  // at most a few: the chain's A, a chunked product's B
 
@@ -880,11 +907,11 @@ int gemm_ozaki(const GemmOp& op, cudaStream_t st) {
     return nullptr;
   };
   static thread_local unsigned* ratio_host = nullptr;
-  if (!ratio_host) NNB_CUDA(cudaHostAlloc(&ratio_host, sizeof(unsigned) * 2, cudaHostAllocDefault));
-  DevBuf ratio_dev;
-  NNB_TRY(ratio_dev.alloc(sizeof(unsigned) * 2, st));
+  if (!ratio_host) NNB_CUDA(cudaHostAlloc(&ratio_host, sizeof(unsigned) * 4, cudaHostAllocDefault));
+  DevBuf ratio_dev;  // [L1 A, L1 B, L2 A, L2 B] ratios to the row/column max
+  NNB_TRY(ratio_dev.alloc(sizeof(unsigned) * 4, st));
   unsigned* rd = ratio_dev.as<unsigned>();
-  NNB_CUDA(cudaMemsetAsync(rd, 0, sizeof(unsigned) * 2, st));
+  NNB_CUDA(cudaMemsetAsync(rd, 0, sizeof(unsigned) * 4, st));
   OzOperand la, rb;
   OzOperand* L = &la;
   OzOperand* R = &rb;
@@ -905,21 +932,33 @@ int gemm_ozaki(const GemmOp& op, cudaStream_t st) {
   } else {
     NNB_TRY(operand_stats(op.B, op.ldb, N, K, right_as_rows, rb, rd + 1, st));
   }
-  NNB_CUDA(cudaMemcpyAsync(ratio_host, rd, sizeof(unsigned) * 2, cudaMemcpyDeviceToHost, st));
+  NNB_CUDA(cudaMemcpyAsync(ratio_host, rd, sizeof(unsigned) * 4, cudaMemcpyDeviceToHost, st));
   NNB_CUDA(cudaStreamSynchronize(st));
-  float ra = pa && pa->have_left ? pa->ratio_left : __builtin_bit_cast(float, ratio_host[0]);
-  float rbv = pb && pb->have_right ? pb->ratio_right : __builtin_bit_cast(float, ratio_host[1]);
-  if (pa && !pa->have_left) {
-    pa->have_left = true;
-    pa->ratio_left = ra;
+  const auto f = [](unsigned u) { return std::max((double)__builtin_bit_cast(float, u), 1.0); };
+  double a1 = f(ratio_host[0]), b1 = f(ratio_host[1]), a2 = f(ratio_host[2]), b2 = f(ratio_host[3]);
+  if (pa) {
+    if (!pa->have_left) {
+      pa->have_left = true;
+      pa->ratio_left = (float)a1;
+      pa->ratio_left2 = (float)a2;
+    }
+    a1 = pa->ratio_left;
+    a2 = pa->ratio_left2;
   }
-  if (pb && !pb->have_right) {
-    pb->have_right = true;
-    pb->ratio_right = rbv;
+  if (pb) {
+    if (!pb->have_right) {
+      pb->have_right = true;
+      pb->ratio_right = (float)b1;
+      pb->ratio_right2 = (float)b2;
+    }
+    b1 = pb->ratio_right;
+    b2 = pb->ratio_right2;
   }
-  // an operand with no finite nonzero row/column reads 0: its product is exact zeros
-  const double ratio = std::min(std::max((double)ra, 1.0), std::max((double)rbv, 1.0));
-  const int s = std::max(15, std::min(kMaxMod, moduli_for_ratio(std::min(ratio, (double)K))));
+  // |C'_ij| <= Σ|a'||b'| <= min(‖a'_i‖₁·max|b'|, max|a'|·‖b'_j‖₁, ‖a'_i‖₂‖b'_j‖₂)
+  // (Cauchy-Schwarz) = 2^106·min(L1 ratios, product of L2 ratios); an operand with no
+  // finite nonzero row/column reads 0 and its product is exact zeros
+  const double ratio = std::min(std::min(a1, b1), a2 * b2);
+  const int s = std::max(14, std::min(kMaxMod, moduli_for_ratio(std::min(ratio, (double)K))));
   if (s > 17) return fail(7, "ozaki: more than 17 moduli needed");
   const OzConst c = make_const(s);
   // Pass 2: residues (a pinned operand keeps the planes it has when they suffice; the
