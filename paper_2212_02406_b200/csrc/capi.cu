@@ -179,11 +179,11 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
   NNB_TRY(x.own.alloc(sizeof(double) * n * a.ld, s));
   x.d = x.own.as<double>();
   CopyLane lane;  // declared after the buffers: its destructor drains the copies before they are freed
-  NNB_TRY(lane.init(2 * chunks + 4));
+  NNB_TRY(lane.init(3 * chunks + 3));
   cudaEvent_t* a_ready = lane.ev.data();
   cudaEvent_t* out_done = a_ready + chunks;
   cudaEvent_t alloc_ev = out_done[chunks], copy_done = out_done[chunks + 1], in_done = out_done[chunks + 2];
-  cudaEvent_t x_ready = out_done[chunks + 3];
+  cudaEvent_t* x_cols = out_done + chunks + 3;  // [chunks]
   // the copy stream may touch the stream-ordered allocations only once they exist
   NNB_CUDA(cudaEventRecord(alloc_ev, s));
   NNB_CUDA(cudaStreamWaitEvent(lane.cs, alloc_ev, 0));
@@ -192,18 +192,25 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
   // block q of the first product's inner dimension: X0's rows and A's columns of q
   // the K-split first product resumes DMMA accumulators (acc_in): DMMA-only
   const bool ksplit = host_a && x0_given && cfg->order == NNB_ORDER_NORTHSTAR && arith() == 3;
-  // int8 emulation: X0 whole first, then A by row chunks; the first product R = I − A·X0
-  // runs chunk by chunk behind them (a row chunk needs only its own rows of A)
-  const bool rows_stream = host_a && x0_given && cfg->order == NNB_ORDER_NORTHSTAR && !ksplit && arith() != 1;
+  // int8 emulation: A by row chunks and X0 by column chunks, ordered so block (0, 0) can
+  // start after two chunks; the first product R = I − A·X0 runs block by block behind them
+  const bool rows_stream = host_a && x0_given && cfg->order == NNB_ORDER_NORTHSTAR && !ksplit && arith() != 1 &&
+                           (arith() == 2 || ozaki_pays(n, n, n));
   if (rows_stream) {
-    NNB_CUDA(cudaMemcpy2DAsync(x.d, x.ld * 8, X0, n * 8, n * 8, n, cudaMemcpyDefault, lane.cs));
-    NNB_CUDA(cudaEventRecord(x_ready, lane.cs));
-    for (int q = 0; q < used; ++q) {
+    auto copy_a = [&](int q) -> int {
       const int64_t r0 = q * rows_per, rq = std::min<int64_t>(rows_per, n - r0);
       NNB_CUDA(cudaMemcpy2DAsync(a.d + r0 * a.ld, a.ld * 8, A + r0 * n, n * 8, n * 8, rq, cudaMemcpyHostToDevice,
                                  lane.cs));
       NNB_CUDA(cudaEventRecord(a_ready[q], lane.cs));
+      return 0;
+    };
+    NNB_TRY(copy_a(0));
+    for (int q = 0; q < used; ++q) {
+      const int64_t c0 = q * rows_per, cq = std::min<int64_t>(rows_per, n - c0);
+      NNB_CUDA(cudaMemcpy2DAsync(x.d + c0, x.ld * 8, X0 + c0, n * 8, cq * 8, n, cudaMemcpyDefault, lane.cs));
+      NNB_CUDA(cudaEventRecord(x_cols[q], lane.cs));
     }
+    for (int q = 1; q < used; ++q) NNB_TRY(copy_a(q));
   } else if (ksplit) {
     for (int q = 0; q < used; ++q) {
       const int64_t k0 = q * rows_per, kq = std::min<int64_t>(rows_per, n - k0);
@@ -230,7 +237,7 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
     io.a_ready = a_ready;  // the first product consumes A and X0 block by block
   } else if (rows_stream) {
     io.a_rows_ready = a_ready;
-    io.x_ready = x_ready;
+    io.x_cols_ready = x_cols;
   } else {
     NNB_CUDA(cudaStreamWaitEvent(s, in_done, 0));
     if (!x0_given) NNB_TRY(x0_build(a.d, a.ld, n, cfg->x0_kind, cfg->x0_scale, x.d, x.ld, s));

@@ -148,8 +148,27 @@ int product(Ctx& c, const Plane& A, const Plane& B, double alpha, const Plane* D
 int product_chunked(Ctx& c, const Plane& A, const Plane& B, double alpha, const Plane* D, double beta,
                     double gamma, const Plane& C, double* eps_out, int* nf_out, ChainIo& io, bool wait_in,
                     bool stream_out, double* chunk_ss, int* chunk_nf) {
-  // every chunk multiplies by the same B: under the int8 emulation its split is formed once
-  OzPinScope pin_b(!c.cplx && (arith() == 2 || arith() == 0), B.re, c.ld, c.n, c.n);
+  // every chunk multiplies by the same B: under the int8 emulation its split is formed once,
+  // and every chunk uses the whole product's moduli count, so each element rounds as in
+  // the one-launch product (host-buffer X bit-identical to the device-buffer run)
+  const bool oz = !c.cplx && (arith() == 2 || (arith() == 0 && ozaki_pays(c.n, c.n, c.n)));
+  OzPinScope pin_b(oz, B.re, c.ld, c.n, c.n);
+  struct Force {
+    bool on;
+    ~Force() {
+      if (on) ozaki_force_moduli(0);
+    }
+  } force{oz};
+  if (oz) {
+    GemmOp whole;
+    whole.M = whole.N = whole.K = c.n;
+    whole.lda = whole.ldb = c.ld;
+    whole.A = A.re;
+    whole.B = B.re;
+    int s_whole = 0;
+    NNB_TRY(ozaki_plan_moduli(whole, c.s, &s_whole));
+    ozaki_force_moduli(s_whole);
+  }
   int m = 0;
   for (int q = 0; q < io.chunks; ++q) {
     const int64_t r0 = q * io.chunk_rows, rows = std::min<int64_t>(io.chunk_rows, c.n - r0);
@@ -193,6 +212,57 @@ int product_chunked(Ctx& c, const Plane& A, const Plane& B, double alpha, const 
     count_launch();
     NNB_CUDA(cudaGetLastError());
   }
+  return 0;
+}
+
+// R = alpha·(A·B) + gamma·I in io.chunks × io.chunks blocks (int8 emulation, host
+// buffers): block (i, j) needs A's row chunk i and B's column chunk j only, and runs
+// as soon as both have landed (io.a_rows_ready[i], io.x_cols_ready[j]), so the copy of
+// the inputs overlaps the product instead of preceding it.  Row and column scaling
+// are per row of A and per column of B, so every block is the whole product's
+// element-for-element result; each operand chunk is split once (pins).  eps from the
+// blocks' Σ R², combined in block order.
+int product_2d(Ctx& c, const Plane& A, const Plane& B, double alpha, double gamma, const Plane& C, double* eps_out,
+               int* nf_out, ChainIo& io, double* chunk_ss, int* chunk_nf) {
+  const int q = io.chunks;
+  std::vector<OzPinScope> cols;
+  cols.reserve(q);
+  for (int j = 0; j < q; ++j) {
+    const int64_t c0 = j * io.chunk_rows, cn = std::min<int64_t>(io.chunk_rows, c.n - c0);
+    if (cn > 0) cols.emplace_back(true, B.re + c0, c.ld, c.n, cn);
+  }
+  int m = 0;
+  for (int i = 0; i < q; ++i) {
+    const int64_t r0 = i * io.chunk_rows, rn = std::min<int64_t>(io.chunk_rows, c.n - r0);
+    if (rn <= 0) break;
+    NNB_CUDA(cudaStreamWaitEvent(c.s, io.a_rows_ready[i], 0));
+    OzPinScope pin_row(true, A.re + r0 * c.ld, c.ld, rn, c.n);
+    for (int j = 0; j < q; ++j) {
+      const int64_t c0 = j * io.chunk_rows, cn = std::min<int64_t>(io.chunk_rows, c.n - c0);
+      if (cn <= 0) break;
+      if (i == 0) NNB_CUDA(cudaStreamWaitEvent(c.s, io.x_cols_ready[j], 0));
+      GemmOp op;
+      op.M = rn;
+      op.N = cn;
+      op.K = c.n;
+      op.lda = op.ldb = c.ld;
+      op.A = A.re + r0 * c.ld;
+      op.B = B.re + c0;
+      op.ep.alpha = alpha;
+      op.ep.gamma = gamma;
+      op.ep.diag_offset = r0 - c0;
+      op.ep.C = C.re + r0 * c.ld + c0;
+      op.ep.ldc = c.ld;
+      op.ep.ss_out = chunk_ss + m;
+      op.ep.nf_out = chunk_nf + m;
+      NNB_TRY(gemm(op, &c.red, c.s));
+      ++m;
+    }
+  }
+  combine_chunks_kernel<<<1, 32, 0, c.s>>>(chunk_ss, chunk_nf, m, eps_out, nf_out,
+                                           1.0 / std::sqrt(static_cast<double>(c.n)));
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
   return 0;
 }
 
@@ -370,11 +440,9 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
     const Plane& rhs = order == 0 ? Xk : A;
     if (k == 0 && io && io->a_ready && order == 0)  // R_0 = I − A·X_0 as A's columns and X_0's rows arrive
       NNB_TRY(product_ksplit(c, lhs, rhs, -1.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1), *io));
-    else if (k == 0 && io && io->a_rows_ready && order == 0) {  // X_0 whole, A's row chunks as they arrive
-      NNB_CUDA(cudaStreamWaitEvent(c.s, io->x_ready, 0));
-      NNB_TRY(product_chunked(c, lhs, rhs, -1.0, nullptr, 0.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1), *io, true,
-                              false, chunk_ss, chunk_nf));
-    } else
+    else if (k == 0 && io && io->a_rows_ready && io->x_cols_ready && order == 0)  // blocks as A and X_0 arrive
+      NNB_TRY(product_2d(c, lhs, rhs, -1.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1), *io, chunk_ss, chunk_nf));
+    else
       NNB_TRY(product(c, lhs, rhs, -1.0, nullptr, 0.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1)));
     ++products;
     recorded = k + 1;
@@ -410,6 +478,9 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
         sym_on = eps_h[k] >= kSymSwitch && (k == 0 || eps_h[k] < eps_h[k - 1]);
       }
       c.sym = sym_mode && sym_on;
+      // R is the same operand of all p Horner products: under the int8 emulation its
+      // split (right operand; left operand in the reference order) is formed once
+      OzPinScope oz_pin_r(oz && p > 1, R.re, c.ld, n, n);
       Plane v = Xk;
       int vi = xi;
       int dst_i = (xi + 1) % 3;

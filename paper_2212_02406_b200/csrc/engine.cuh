@@ -117,6 +117,10 @@ int gemm_exact(const GemmOp& op, cudaStream_t s);
 // Ozaki-II emulation of a real product on the int8 tensor cores (ozaki.cu).
 int gemm_ozaki(const GemmOp& op, cudaStream_t s);
 int ozaki_moduli_for(int64_t k);
+// moduli the whole product op needs (stats passes only), and a thread-local floor that
+// a chunked product's pieces then use (0 = off)
+int ozaki_plan_moduli(const GemmOp& op, cudaStream_t st, int* s_out);
+void ozaki_force_moduli(int s);
 void ozaki_profile(int on);
 void ozaki_stats(double* ms, double* work, int64_t* launches, int reset);
 // NNB_ARITH_FAST routes a real product to the int8 emulation where it beats DMMA
@@ -226,10 +230,10 @@ struct ChainIo {
   cudaEvent_t* out_done = nullptr; // [chunks] scratch
   cudaEvent_t copy_done = nullptr; // scratch
   bool out_streamed = false;       // run_chain delivered the final X to host_out (X itself is then stale)
-  // int8-emulation streaming: X0 is whole on the device once x_ready fires and A arrives by
-  // row chunks (a_rows_ready[q]); the first product R = I − A·X0 then runs chunk by chunk
-  cudaEvent_t x_ready = nullptr;
-  cudaEvent_t* a_rows_ready = nullptr;
+  // int8-emulation streaming: A arrives by row chunks and X0 by column chunks, and the first
+  // product R = I − A·X0 runs by blocks as their chunks land (chain.cu product_2d)
+  cudaEvent_t* a_rows_ready = nullptr;  // [chunks] A's row chunk i landed
+  cudaEvent_t* x_cols_ready = nullptr;  // [chunks] X0's column chunk j landed
 };
 // Real chain on device buffers with ld == ldn (ldn even, >= n).  X holds X0
 // on entry and the final iterate on exit.  eps_hist host (nullable).

@@ -528,10 +528,10 @@ __global__ void __launch_bounds__(256) oz_colmax_kernel(const double* __restrict
     sq = fma(v, v, sq);
   }
   if (mx > 0.0) atomicMax(colmax + c, static_cast<unsigned long long>(__double_as_longlong(mx)));
-  if (sum > 0.0) {  // bounds only: their summation order does not matter
-    atomicAdd(colsum + c, sum);
-    atomicAdd(colsq + c, sq);
-  }
+  // per-256-row partial sums, added in row-block order by oz_colratio_kernel: the bound,
+  // and so the moduli count, is the same on every run (no floating-point atomics)
+  colsum[(int64_t)blockIdx.y * n + c] = sum;
+  colsq[(int64_t)blockIdx.y * n + c] = sq;
   if (bad) atomicOr(colbad + c, 1);
 }
 
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(256) oz_colmax_kernel(const double* __restrict
 __global__ void __launch_bounds__(256) oz_colratio_kernel(const unsigned long long* __restrict__ colmax,
                                                           const double* __restrict__ colsum,
                                                           const double* __restrict__ colsq,
-                                                          const int* __restrict__ colbad, int n,
+                                                          const int* __restrict__ colbad, int n, int kblocks,
                                                           int* __restrict__ exps, unsigned* __restrict__ ratio) {
   const int c = blockIdx.x * 256 + threadIdx.x;
   float r = 0.0f, r2 = 0.0f;
@@ -548,8 +548,13 @@ __global__ void __launch_bounds__(256) oz_colratio_kernel(const unsigned long lo
     const bool bad = colbad[c] != 0;
     exps[c] = bad ? kBadExp : exp_for(mx);
     if (!bad && mx > 0.0) {
-      r = static_cast<float>(colsum[c] / mx) * 1.0001f;
-      r2 = static_cast<float>(sqrt(colsq[c]) / mx) * 1.0001f;
+      double sum = 0.0, sq = 0.0;
+      for (int b = 0; b < kblocks; ++b) {
+        sum += colsum[(int64_t)b * n + c];
+        sq += colsq[(int64_t)b * n + c];
+      }
+      r = static_cast<float>(sum / mx) * 1.0001f;
+      r2 = static_cast<float>(sqrt(sq) / mx) * 1.0001f;
     }
   }
 #pragma unroll
@@ -790,15 +795,16 @@ int operand_stats(const double* X, int64_t ld, int64_t rows, int64_t k, bool lef
   } else {
     const int64_t n = rows;
     DevBuf cm;
-    NNB_TRY(cm.alloc((sizeof(unsigned long long) + 2 * sizeof(double) + sizeof(int)) * n, st));
+    const int64_t kb = (k + 255) / 256;
+    NNB_TRY(cm.alloc((sizeof(unsigned long long) + sizeof(int)) * n + 8 + 2 * sizeof(double) * kb * n, st));
     unsigned long long* colmax = cm.as<unsigned long long>();
-    double* colsum = reinterpret_cast<double*>(colmax + n);
-    double* colsq = colsum + n;
-    int* colbad = reinterpret_cast<int*>(colsq + n);
-    NNB_CUDA(cudaMemsetAsync(cm.p, 0, cm.bytes, st));
-    oz_colmax_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)((k + 255) / 256)), 256, 0, st>>>(
-        X, ld, (int)k, (int)n, colmax, colsum, colsq, colbad);
-    oz_colratio_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(colmax, colsum, colsq, colbad, (int)n,
+    int* colbad = reinterpret_cast<int*>(colmax + n);
+    double* colsum = reinterpret_cast<double*>(colbad + n + (n & 1));  // [kb][n] partials
+    double* colsq = colsum + kb * n;
+    NNB_CUDA(cudaMemsetAsync(cm.p, 0, (sizeof(unsigned long long) + sizeof(int)) * n, st));
+    oz_colmax_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)kb), 256, 0, st>>>(X, ld, (int)k, (int)n, colmax,
+                                                                                    colsum, colsq, colbad);
+    oz_colratio_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(colmax, colsum, colsq, colbad, (int)n, (int)kb,
                                                                    o.exps.as<int>(), ratio);
     count_launch(2);
   }
@@ -893,7 +899,19 @@ void oz_unpin(const double* p) {
 int make_tmap_u8(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                  int box_cols);
 
-int gemm_ozaki(const GemmOp& op, cudaStream_t st) {
+thread_local int g_forced_s = 0;  // ozaki_force_moduli: a chunked product uses its whole product's count
+
+int gemm_ozaki_impl(const GemmOp& op, cudaStream_t st, bool plan_only, int* s_out);
+
+int gemm_ozaki(const GemmOp& op, cudaStream_t st) { return gemm_ozaki_impl(op, st, false, nullptr); }
+
+// The moduli count the whole product `op` needs (its stats passes only; the operands'
+// pins keep them), so that chunks of it can be formed with the same count — every
+// element then rounds exactly as in the whole product.
+int ozaki_plan_moduli(const GemmOp& op, cudaStream_t st, int* s_out) { return gemm_ozaki_impl(op, st, true, s_out); }
+void ozaki_force_moduli(int s) { g_forced_s = s; }
+
+int gemm_ozaki_impl(const GemmOp& op, cudaStream_t st, bool plan_only, int* s_out) {
   const int64_t M = op.M, N = op.N, K = op.K;
   if (K > kMaxK) return fail(7, "ozaki: inner dimension above 131071 (int32 accumulation bound)");
   if (op.ep.C2 || op.ep.acc_in) return fail(7, "ozaki: dual-output and K-split epilogues are DMMA-only");
@@ -958,7 +976,14 @@ int gemm_ozaki(const GemmOp& op, cudaStream_t st) {
   // (Cauchy-Schwarz) = 2^106·min(L1 ratios, product of L2 ratios); an operand with no
   // finite nonzero row/column reads 0 and its product is exact zeros
   const double ratio = std::min(std::min(a1, b1), a2 * b2);
-  const int s = std::max(14, std::min(kMaxMod, moduli_for_ratio(std::min(ratio, (double)K))));
+  const int s_need = std::max(14, std::min(kMaxMod, moduli_for_ratio(std::min(ratio, (double)K))));
+  if (plan_only) {
+    *s_out = s_need;
+    return 0;
+  }
+  // a forced count comes from the whole product of which this is a chunk: never fewer
+  // than this chunk needs (a chunk's rows and columns are a subset of the whole's)
+  const int s = std::max(s_need, g_forced_s);
   if (s > 17) return fail(7, "ozaki: more than 17 moduli needed");
   const OzConst c = make_const(s);
   // Pass 2: residues (a pinned operand keeps the planes it has when they suffice; the

@@ -271,6 +271,7 @@ __global__ void __launch_bounds__(NNB_SPMV_THREADS, NNB_SPMV_MINB)
 
 // ---- pair dictionary build: hash insert, index assignment, verified encode ----
 constexpr int kDictSlots = 4096;  // open addressing, power of two
+constexpr int kMaxProbe = 64;     // longer probe runs only happen past the dictionary's capacity
 
 __device__ __forceinline__ unsigned long long pair_hash(int32_t d, unsigned long long bits) {
   unsigned long long h = bits ^ (static_cast<unsigned long long>(static_cast<uint32_t>(d)) * 0x9E3779B97F4A7C15ull);
@@ -314,7 +315,15 @@ __global__ void dict_insert_kernel(const int64_t* __restrict__ rp, const int32_t
       if (last_h && d == last_d && b == last_b) continue;
       const unsigned long long h = pair_hash(d, b);
       int slot = static_cast<int>(h & (kDictSlots - 1));
-      for (int probe = 0; probe < kDictSlots; ++probe) {
+      for (int probe = 0;; ++probe) {
+        // a dictionary of <= 255 pairs fills under 7 % of the table, so a long probe run
+        // means the operator has too many pairs: racing inserts past the 256th can fill the
+        // whole table, and probing it to the end per nonzero cost 68 ms per solve on a
+        // random-valued 4096² operator
+        if (probe >= kMaxProbe || *(volatile int*)&ws->overflow) {
+          atomicOr(&ws->overflow, 1);
+          return;
+        }
         unsigned long long cur = *(volatile unsigned long long*)&ws->hash[slot];
         if (cur == 0) {
           cur = atomicCAS(&ws->hash[slot], 0ull, h);
@@ -454,7 +463,11 @@ __global__ void rowdict_insert_kernel(const uint8_t* __restrict__ code, int widt
     if (*(volatile int*)&ws->overflow) return;
     const unsigned long long h = key_hash(k);
     int slot = static_cast<int>(h & (kDictSlots - 1));
-    for (int probe = 0; probe < kDictSlots; ++probe) {
+    for (int probe = 0;; ++probe) {
+      if (probe >= kMaxProbe || *(volatile int*)&ws->overflow) {  // too many rows (see dict_insert_kernel)
+        atomicOr(&ws->overflow, 1);
+        return;
+      }
       unsigned long long cur = *(volatile unsigned long long*)&ws->hash[slot];
       if (cur == 0) {
         cur = atomicCAS(&ws->hash[slot], 0ull, h);
