@@ -100,9 +100,8 @@ uint64_t nnb_kernel_launches(void);
 /* Arithmetic mode of the calling thread.
  * NNB_ARITH_FAST (default): the faster of the two FP64-accurate product
  *   paths per product — the int8 emulation below for real products with
- *   M, N, K >= 1024 and M·N·K >= 3072^3, DMMA otherwise (complex, symmetric-
- *   order and K-split products always DMMA); agrees with the reference to
- *   ~1e-15 relative.
+ *   M, N, K >= 1024 and M·N·K >= 3072^3, DMMA otherwise (complex and K-split
+ *   products always DMMA); agrees with the reference to ~1e-15 relative.
  * NNB_ARITH_DMMA: every product on the FP64 tensor pipe (DMMA.8x8x4).
  * NNB_ARITH_REFERENCE: real dense products as ascending-k, explicitly
  *   rounded CUDA-core loops, serial Frobenius sums and the reference's own

@@ -192,8 +192,8 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
   // block q of the first product's inner dimension: X0's rows and A's columns of q
   // the K-split first product resumes DMMA accumulators (acc_in): DMMA-only
   const bool ksplit = host_a && x0_given && cfg->order == NNB_ORDER_NORTHSTAR && arith() == 3;
-  // int8 emulation: A by row chunks and X0 by column chunks, ordered so block (0, 0) can
-  // start after two chunks; the first product R = I − A·X0 runs block by block behind them
+  // int8 emulation: A by row chunks and X0 by column chunks, interleaved, so block (0, 0)
+  // starts after two chunks; the first product R = I − A·X0 runs block by block behind them
   const bool rows_stream = host_a && x0_given && cfg->order == NNB_ORDER_NORTHSTAR && !ksplit && arith() != 1 &&
                            (arith() == 2 || ozaki_pays(n, n, n));
   if (rows_stream) {
@@ -204,13 +204,12 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
       NNB_CUDA(cudaEventRecord(a_ready[q], lane.cs));
       return 0;
     };
-    NNB_TRY(copy_a(0));
-    for (int q = 0; q < used; ++q) {
+    for (int q = 0; q < used; ++q) {  // A_0, X_0, A_1, X_1, ... (chain.cu product_2d's order)
+      NNB_TRY(copy_a(q));
       const int64_t c0 = q * rows_per, cq = std::min<int64_t>(rows_per, n - c0);
       NNB_CUDA(cudaMemcpy2DAsync(x.d + c0, x.ld * 8, X0 + c0, n * 8, cq * 8, n, cudaMemcpyDefault, lane.cs));
       NNB_CUDA(cudaEventRecord(x_cols[q], lane.cs));
     }
-    for (int q = 1; q < used; ++q) NNB_TRY(copy_a(q));
   } else if (ksplit) {
     for (int q = 0; q < used; ++q) {
       const int64_t k0 = q * rows_per, kq = std::min<int64_t>(rows_per, n - k0);

@@ -225,41 +225,49 @@ int product_chunked(Ctx& c, const Plane& A, const Plane& B, double alpha, const 
 int product_2d(Ctx& c, const Plane& A, const Plane& B, double alpha, double gamma, const Plane& C, double* eps_out,
                int* nf_out, ChainIo& io, double* chunk_ss, int* chunk_nf) {
   const int q = io.chunks;
-  std::vector<OzPinScope> cols;
-  cols.reserve(q);
-  for (int j = 0; j < q; ++j) {
-    const int64_t c0 = j * io.chunk_rows, cn = std::min<int64_t>(io.chunk_rows, c.n - c0);
-    if (cn > 0) cols.emplace_back(true, B.re + c0, c.ld, c.n, cn);
+  // every chunk of both operands stays pinned for the product (each is split once)
+  std::vector<OzPinScope> pins;
+  pins.reserve(2 * q);
+  for (int t = 0; t < q; ++t) {
+    const int64_t o = t * io.chunk_rows, w = std::min<int64_t>(io.chunk_rows, c.n - o);
+    if (w <= 0) break;
+    pins.emplace_back(true, A.re + o * c.ld, c.ld, w, c.n);
+    pins.emplace_back(true, B.re + o, c.ld, c.n, w);
   }
+  // the copies arrive as A_0, X_0, A_1, X_1, ...: after step t the blocks (t, 0..t) and
+  // (0..t−1, t) become computable, so the work available grows with t² while the copy
+  // time grows with t
   int m = 0;
-  for (int i = 0; i < q; ++i) {
+  auto block = [&](int i, int j) -> int {
     const int64_t r0 = i * io.chunk_rows, rn = std::min<int64_t>(io.chunk_rows, c.n - r0);
-    if (rn <= 0) break;
-    NNB_CUDA(cudaStreamWaitEvent(c.s, io.a_rows_ready[i], 0));
-    OzPinScope pin_row(true, A.re + r0 * c.ld, c.ld, rn, c.n);
-    for (int j = 0; j < q; ++j) {
-      const int64_t c0 = j * io.chunk_rows, cn = std::min<int64_t>(io.chunk_rows, c.n - c0);
-      if (cn <= 0) break;
-      if (i == 0) NNB_CUDA(cudaStreamWaitEvent(c.s, io.x_cols_ready[j], 0));
-      GemmOp op;
-      op.M = rn;
-      op.N = cn;
-      op.K = c.n;
-      op.lda = op.ldb = c.ld;
-      op.A = A.re + r0 * c.ld;
-      op.B = B.re + c0;
-      op.ep.alpha = alpha;
-      op.ep.gamma = gamma;
-      op.ep.diag_offset = r0 - c0;
-      op.ep.C = C.re + r0 * c.ld + c0;
-      op.ep.ldc = c.ld;
-      op.ep.ss_out = chunk_ss + m;
-      op.ep.nf_out = chunk_nf + m;
-      NNB_TRY(gemm(op, &c.red, c.s));
-      ++m;
-    }
+    const int64_t c0 = j * io.chunk_rows, cn = std::min<int64_t>(io.chunk_rows, c.n - c0);
+    GemmOp op;
+    op.M = rn;
+    op.N = cn;
+    op.K = c.n;
+    op.lda = op.ldb = c.ld;
+    op.A = A.re + r0 * c.ld;
+    op.B = B.re + c0;
+    op.ep.alpha = alpha;
+    op.ep.gamma = gamma;
+    op.ep.diag_offset = r0 - c0;
+    op.ep.C = C.re + r0 * c.ld + c0;
+    op.ep.ldc = c.ld;
+    op.ep.ss_out = chunk_ss + (i * q + j);  // block order: the combine below is deterministic
+    op.ep.nf_out = chunk_nf + (i * q + j);
+    NNB_TRY(gemm(op, &c.red, c.s));
+    ++m;
+    return 0;
+  };
+  int used = 0;
+  while (used < q && used * io.chunk_rows < c.n) ++used;
+  for (int t = 0; t < used; ++t) {
+    NNB_CUDA(cudaStreamWaitEvent(c.s, io.a_rows_ready[t], 0));
+    NNB_CUDA(cudaStreamWaitEvent(c.s, io.x_cols_ready[t], 0));
+    for (int j = 0; j <= t; ++j) NNB_TRY(block(t, j));
+    for (int i = 0; i < t; ++i) NNB_TRY(block(i, t));
   }
-  combine_chunks_kernel<<<1, 32, 0, c.s>>>(chunk_ss, chunk_nf, m, eps_out, nf_out,
+  combine_chunks_kernel<<<1, 32, 0, c.s>>>(chunk_ss, chunk_nf, used * used, eps_out, nf_out,
                                            1.0 / std::sqrt(static_cast<double>(c.n)));
   count_launch();
   NNB_CUDA(cudaGetLastError());
