@@ -128,6 +128,52 @@ __device__ __forceinline__ void garner_digits(float* v, const float* r) {
     garner_digits<L + 1, S>(v, r);
   }
 }
+// The same recurrence for two elements at once in packed FP32 (FFMA2/FADD2/FMUL2 on
+// sm_100a; the Garner constants become broadcast immediates): half the instructions of
+// the FP32 pipe work of the reconstruction, which is issue-bound.
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(unsigned long long r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long bc2(float c) { return pk2(c, c); }
+template <int L, int I>
+__device__ __forceinline__ unsigned long long garner_sum2(const unsigned long long* v, unsigned long long x) {
+  if constexpr (I < L) return garner_sum2<L, I + 1>(v, fma2(v[I], bc2(GarnerQ<I, L>::v), x));
+  else return x;
+}
+template <int L, int S>
+__device__ __forceinline__ void garner_digits2(unsigned long long* v, const unsigned long long* r) {
+  if constexpr (L < S) {
+    if constexpr (L == 0) {
+      v[0] = r[0];
+    } else {
+      const unsigned long long x = garner_sum2<L, 0>(v, mul2(r[L], bc2(GarnerP<L>::v)));
+      const unsigned long long qf = add2(fma2(x, bc2(GarnerP<L>::inv), bc2(12582912.0f)), bc2(-12582912.0f));
+      v[L] = fma2(qf, bc2(-GarnerP<L>::m), x);
+    }
+    garner_digits2<L + 1, S>(v, r);
+  }
+}
+
 int inv_mod(int a, int m) {
   a %= m;
   for (int x = 1; x < m; ++x)
@@ -630,18 +676,27 @@ __global__ void __launch_bounds__(256) oz_recon_kernel(const uint8_t* __restrict
       if (c >= N) break;
       const bool two = c + 1 < N;
       double out2[2];
+      // Garner digits of both elements of the pair in packed FP32
+      unsigned long long r2[S], v2[S];
+#pragma unroll
+      for (int l = 0; l < S; ++l) {
+        const uint32_t word = (jp < 2) ? rv[l].x : rv[l].y;
+        const int sel = (2 * jp) & 3;
+        // byte b -> float exactly: the bits 0x4B0000bb are 2^23 + b
+        r2[l] = add2(pk2(__uint_as_float(__byte_perm(word, 0x4B00u, 0x5440u + sel)),
+                         __uint_as_float(__byte_perm(word, 0x4B00u, 0x5440u + sel + 1))),
+                     bc2(-8388608.0f));
+      }
+      garner_digits2<0, S>(v2, r2);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int j = 2 * jp + h;
-        const int shift = 8 * (j & 3);
-        float r[S], v[S];
+        float v[S];
 #pragma unroll
         for (int l = 0; l < S; ++l) {
-          const uint32_t word = (jp < 2) ? rv[l].x : rv[l].y;
-          // byte b -> float exactly: the bits 0x4B0000bb are 2^23 + b
-          r[l] = __uint_as_float(__byte_perm(word, 0x4B00u, 0x5440u + (shift >> 3))) - 8388608.0f;
+          float a, b;
+          upk2(v2[l], a, b);
+          v[l] = h ? b : a;
         }
-        garner_digits<0, S>(v, r);
         const double x = value_of<S>(v, v[S - 1]);
         // scale back by 2^-(ea+eb), then the chain's epilogue
         const int cc = c + h;
