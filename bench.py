@@ -56,7 +56,7 @@ INT8_PEAK_SOURCE = ("measured cuBLAS int8 GEMM (torch._int_mm 8192^3) sustained 
                     "fallback: 2 x MEASURED_PEAKS bf16_tflops_sustained")
 # DRAM traffic per launch of each dominant kernel from the committed ncu --set full captures
 try:
-    NCU_TRAFFIC = json.loads((ROOT / "profiles" / "r01_ncu_traffic.json").read_text())
+    NCU_TRAFFIC = json.loads((ROOT / "profiles" / "r02_ncu_traffic.json").read_text())
 except Exception:
     NCU_TRAFFIC = {}
 

@@ -7,6 +7,7 @@
 // point computes anything on the host.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <random>
 #include <vector>
@@ -16,6 +17,20 @@
 #include "sparse.cuh"
 
 using namespace nnb;
+
+void nnb::trace_dump() {
+  if (!trace_on()) return;
+  int* n;
+  TraceMark* m = trace_marks(&n);
+  cudaDeviceSynchronize();
+  for (int i = 0; i < *n; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, m[0].ev, m[i].ev);
+    std::fprintf(stderr, "trace %9.2f ms  host %9.2f ms  %s\n", ms, m[i].host_ms - m[0].host_ms, m[i].label);
+  }
+  for (int i = 0; i < *n; ++i) cudaEventDestroy(m[i].ev);
+  *n = 0;
+}
 
 namespace {
 
@@ -171,6 +186,8 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
   const bool host_a = !is_device_ptr(A), host_out = X_out && !is_device_ptr(X_out);
   const bool x0_given = cfg->x0_kind == NNB_X0_GIVEN;
   if (x0_given && !X0) return fail(NNB_ERR_DOMAIN, "nn chain: X0 required for NNB_X0_GIVEN");
+  if (trace_on()) trace_reset();
+  trace_mark(s, "start");
   DMat a, x;
   if (host_a) NNB_TRY(a.alloc(n, n, s));
   else NNB_TRY(a.load(A, n, n, n, s));
@@ -202,6 +219,7 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
       NNB_CUDA(cudaMemcpy2DAsync(a.d + r0 * a.ld, a.ld * 8, A + r0 * n, n * 8, n * 8, rq, cudaMemcpyHostToDevice,
                                  lane.cs));
       NNB_CUDA(cudaEventRecord(a_ready[q], lane.cs));
+      trace_mark(lane.cs, "h2d A rows ", q);
       return 0;
     };
     for (int q = 0; q < used; ++q) {  // A_0, X_0, A_1, X_1, ... (chain.cu product_2d's order)
@@ -209,6 +227,7 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
       const int64_t c0 = q * rows_per, cq = std::min<int64_t>(rows_per, n - c0);
       NNB_CUDA(cudaMemcpy2DAsync(x.d + c0, x.ld * 8, X0 + c0, n * 8, cq * 8, n, cudaMemcpyDefault, lane.cs));
       NNB_CUDA(cudaEventRecord(x_cols[q], lane.cs));
+      trace_mark(lane.cs, "h2d X0 cols ", q);
     }
   } else if (ksplit) {
     for (int q = 0; q < used; ++q) {
@@ -244,6 +263,7 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
   }
   ChainOut o;
   const int st = chain_real(a.d, n, a.ld, x.d, c, eps_hist, &o, s, &io);
+  trace_mark(s, "chain done");
   fill_result(result, o);
   if (st != 0 && st != NNB_ERR_DIVERGENCE && st != NNB_ERR_DOMAIN) return st;
   // with zero products (max_iters = 0, no final residual) nothing on s has waited
@@ -252,6 +272,8 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
   if (X_out && !io.out_streamed) NNB_TRY(x.store(X_out, n, s));
   NNB_TRY(sync(s));
   NNB_CUDA(cudaStreamSynchronize(lane.cs));
+  trace_mark(s, "end");
+  trace_dump();
   return st;
 }
 

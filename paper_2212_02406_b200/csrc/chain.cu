@@ -199,6 +199,7 @@ int product_chunked(Ctx& c, const Plane& A, const Plane& B, double alpha, const 
       NNB_CUDA(cudaMemcpy2DAsync(io.host_out + r0 * c.n, c.n * sizeof(double), C.re + r0 * c.ld,
                                  c.ld * sizeof(double), c.n * sizeof(double), rows, cudaMemcpyDeviceToHost,
                                  io.copy));
+      trace_mark(io.copy, "d2h X rows ", q);
     }
     ++m;
   }
@@ -266,6 +267,7 @@ int product_2d(Ctx& c, const Plane& A, const Plane& B, double alpha, double gamm
     NNB_CUDA(cudaStreamWaitEvent(c.s, io.x_cols_ready[t], 0));
     for (int j = 0; j <= t; ++j) NNB_TRY(block(t, j));
     for (int i = 0; i < t; ++i) NNB_TRY(block(i, t));
+    trace_mark(c.s, "L-block done ", t);
   }
   combine_chunks_kernel<<<1, 32, 0, c.s>>>(chunk_ss, chunk_nf, used * used, eps_out, nf_out,
                                            1.0 / std::sqrt(static_cast<double>(c.n)));
@@ -329,6 +331,7 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
   const int slots = cfg.max_iters + 1;
 
   constexpr int kMaxChunks = 64;
+  constexpr int kChunkSlots = kMaxChunks * kMaxChunks;  // product_2d: one slot per block
   if (io && (io->chunks < 1 || io->chunks > kMaxChunks || c.cplx)) io = nullptr;
   // reference-exact mode (real data): the reference's operand order and nest sequence
   const bool exact = arith() == 1 && !c.cplx;
@@ -345,14 +348,14 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
   const size_t nf_count = (size_t)slots * (p + 1);
   // device scalars, one block (one D2H copy): ε per nest | complex Σ² | chunk Σ² | non-finite
   // counts | complex counts | chunk counts | small-kernel status
-  NNB_TRY(scal.alloc(sizeof(double) * (slots + 8 + kMaxChunks) + sizeof(int) * (nf_count + 8 + kMaxChunks + 8), c.s));
+  NNB_TRY(scal.alloc(sizeof(double) * (slots + 8 + kChunkSlots) + sizeof(int) * (nf_count + 8 + kChunkSlots + 8), c.s));
   double* eps_dev = scal.as<double>();
   c.ss2 = eps_dev + slots;
   double* chunk_ss = c.ss2 + 8;
-  int* nf_dev = reinterpret_cast<int*>(chunk_ss + kMaxChunks);
+  int* nf_dev = reinterpret_cast<int*>(chunk_ss + kChunkSlots);
   c.nf2 = nf_dev + nf_count;
   int* chunk_nf = c.nf2 + 8;
-  int* status_dev = chunk_nf + kMaxChunks;
+  int* status_dev = chunk_nf + kChunkSlots;
   NNB_CUDA(cudaMemsetAsync(scal.p, 0, scal.bytes, c.s));
   std::vector<double> eps_h(slots, 0.0);
   std::vector<int> nf_h(nf_count, 0);
@@ -364,9 +367,9 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
     NNB_CUDA(cudaMemcpyAsync(h, scal.p, scal.bytes, cudaMemcpyDeviceToHost, c.s));
     NNB_CUDA(cudaStreamSynchronize(c.s));
     std::memcpy(eps_h.data(), h, sizeof(double) * slots);
-    const uint8_t* hi = h + sizeof(double) * (slots + 8 + kMaxChunks);
+    const uint8_t* hi = h + sizeof(double) * (slots + 8 + kChunkSlots);
     std::memcpy(nf_h.data(), hi, sizeof(int) * nf_count);
-    std::memcpy(status_h, hi + sizeof(int) * (nf_count + 8 + kMaxChunks), sizeof(status_h));
+    std::memcpy(status_h, hi + sizeof(int) * (nf_count + 8 + kChunkSlots), sizeof(status_h));
     return 0;
   };
 
@@ -452,6 +455,7 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
       NNB_TRY(product_2d(c, lhs, rhs, -1.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1), *io, chunk_ss, chunk_nf));
     else
       NNB_TRY(product(c, lhs, rhs, -1.0, nullptr, 0.0, 1.0, R, eps_dev + k, nf_dev + k * (p + 1)));
+    trace_mark(c.s, "residual done ", k);
     ++products;
     recorded = k + 1;
     if (tol_mode) {
@@ -504,6 +508,7 @@ int run_chain(Ctx& c, const Plane& A, Plane X, const ChainCfg& cfg, double* eps_
         } else {
           NNB_TRY(product(c, l, r, 1.0, &Xk, 1.0, 0.0, dst, nullptr, nf_dev + k * (p + 1) + j));
         }
+        trace_mark(c.s, "horner done ", j);
         ++products;
         v = dst;
         vi = dst_i;
@@ -876,7 +881,13 @@ int chain_real(const double* A, int64_t n, int64_t ldn, double* X, const ChainCf
   c.cplx = false;
   c.s = s;
   Plane a{const_cast<double*>(A), nullptr}, x{X, nullptr};
-  return run_chain(c, a, x, cfg, eps_hist, out, io);
+  if (!io && trace_on()) {  // device-resident nest: its own timeline
+    trace_reset();
+    trace_mark(s, "start");
+  }
+  const int st = run_chain(c, a, x, cfg, eps_hist, out, io);
+  if (!io) trace_dump();
+  return st;
 }
 
 int chain_complex(const double* Ar, const double* Ai, int64_t n, int64_t ldn, double* Xr,

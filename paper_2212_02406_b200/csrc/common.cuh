@@ -10,6 +10,7 @@
 #include <stdint.h>
 
 #include <cstdlib>
+#include <ctime>
 
 namespace nnb {
 
@@ -25,6 +26,55 @@ inline const char* debug_env(const char* name) {
   }();
   return on ? std::getenv(name) : nullptr;
 }
+
+// NNB_DEBUG=1 NNB_TRACE=1: timing events at labelled points on any stream; trace_dump()
+// synchronizes and prints each point's time since the first one to stderr (the e2e
+// copy/compute timeline: tools/e2e_timeline.py)
+struct TraceMark {
+  char label[24];
+  cudaEvent_t ev;
+  double host_ms;  // host clock at the mark (a device time below it = the GPU waited for the host)
+};
+inline double trace_host_ms() {
+  timespec t;
+  clock_gettime(CLOCK_MONOTONIC, &t);
+  return t.tv_sec * 1e3 + t.tv_nsec * 1e-6;
+}
+inline TraceMark* trace_marks(int** count) {
+  static TraceMark marks[512];
+  static int n = 0;
+  *count = &n;
+  return marks;
+}
+inline bool trace_on() {
+  static const bool on = debug_env("NNB_TRACE") != nullptr;
+  return on;
+}
+inline void trace_mark(cudaStream_t s, const char* label, int idx = -1) {
+  if (!trace_on()) return;
+  int* n;
+  TraceMark* m = trace_marks(&n);
+  if (*n >= 512) return;
+  TraceMark& t = m[*n];
+  if (cudaEventCreate(&t.ev) != cudaSuccess) return;
+  int i = 0;
+  for (; label[i] && i < 16; ++i) t.label[i] = label[i];
+  if (idx >= 0) {
+    t.label[i++] = static_cast<char>('0' + idx / 10 % 10);
+    t.label[i++] = static_cast<char>('0' + idx % 10);
+  }
+  t.label[i] = 0;
+  t.host_ms = trace_host_ms();
+  cudaEventRecord(t.ev, s);
+  ++*n;
+}
+inline void trace_reset() {
+  int* n;
+  TraceMark* m = trace_marks(&n);
+  for (int i = 0; i < *n; ++i) cudaEventDestroy(m[i].ev);
+  *n = 0;
+}
+void trace_dump();  // capi.cu
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

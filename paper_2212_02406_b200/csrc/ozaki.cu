@@ -885,6 +885,11 @@ int operand_residues(const double* X, int64_t ld, bool left, const OzConst& c, O
 }
 
 // moduli for |C'| <= ratio·2^106 < M/8 (the balanced Garner value is then C' itself)
+__global__ void oz_ratio_out_kernel(const unsigned* __restrict__ rd, unsigned* out) {
+  if (threadIdx.x < 4) out[threadIdx.x] = rd[threadIdx.x];
+  __threadfence_system();
+}
+
 int moduli_for_ratio(double ratio) {
   const double need = 2.0 * kAlpha + std::log2(std::max(ratio, 1.0)) + 3.0;
   double have = 0.0;
@@ -979,8 +984,15 @@ int gemm_ozaki_impl(const GemmOp& op, cudaStream_t st, bool plan_only, int* s_ou
       if (q->p == p) return q;
     return nullptr;
   };
+  // the ratios come back through mapped host memory written by a one-warp kernel, not
+  // a copy: a device-to-host copy would queue behind any large copy on the same engine
+  // (the host-buffer nest streams X out during its last product)
   static thread_local unsigned* ratio_host = nullptr;
-  if (!ratio_host) NNB_CUDA(cudaHostAlloc(&ratio_host, sizeof(unsigned) * 4, cudaHostAllocDefault));
+  static thread_local unsigned* ratio_mapped = nullptr;
+  if (!ratio_host) {
+    NNB_CUDA(cudaHostAlloc(&ratio_host, sizeof(unsigned) * 4, cudaHostAllocMapped));
+    NNB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ratio_mapped), ratio_host, 0));
+  }
   DevBuf ratio_dev;  // [L1 A, L1 B, L2 A, L2 B] ratios to the row/column max
   NNB_TRY(ratio_dev.alloc(sizeof(unsigned) * 4, st));
   unsigned* rd = ratio_dev.as<unsigned>();
@@ -1005,25 +1017,39 @@ int gemm_ozaki_impl(const GemmOp& op, cudaStream_t st, bool plan_only, int* s_ou
   } else {
     NNB_TRY(operand_stats(op.B, op.ldb, N, K, right_as_rows, rb, rd + 1, st));
   }
-  NNB_CUDA(cudaMemcpyAsync(ratio_host, rd, sizeof(unsigned) * 4, cudaMemcpyDeviceToHost, st));
-  NNB_CUDA(cudaStreamSynchronize(st));
-  const auto f = [](unsigned u) { return std::max((double)__builtin_bit_cast(float, u), 1.0); };
-  double a1 = f(ratio_host[0]), b1 = f(ratio_host[1]), a2 = f(ratio_host[2]), b2 = f(ratio_host[3]);
-  if (pa) {
-    if (!pa->have_left) {
+  // A chunk of a planned product (ozaki_force_moduli) uses the whole product's count,
+  // which bounds its own (its rows and columns are a subset): no host read at all.
+  // Two pinned operands whose ratios are known need none either.
+  const bool forced = g_forced_s > 0 && !plan_only;
+  const bool known = pa && pa->have_left && pb && pb->have_right;
+  double a1 = 1.0, b1 = 1.0, a2 = 1.0, b2 = 1.0;
+  if (!forced && !known) {
+    oz_ratio_out_kernel<<<1, 32, 0, st>>>(rd, ratio_mapped);
+    count_launch();
+    NNB_CUDA(cudaGetLastError());
+    NNB_CUDA(cudaStreamSynchronize(st));
+    trace_mark(st, "oz stats");
+    const auto f = [](unsigned u) { return std::max((double)__builtin_bit_cast(float, u), 1.0); };
+    a1 = f(ratio_host[0]);
+    b1 = f(ratio_host[1]);
+    a2 = f(ratio_host[2]);
+    b2 = f(ratio_host[3]);
+    if (pa && !pa->have_left) {
       pa->have_left = true;
       pa->ratio_left = (float)a1;
       pa->ratio_left2 = (float)a2;
     }
-    a1 = pa->ratio_left;
-    a2 = pa->ratio_left2;
-  }
-  if (pb) {
-    if (!pb->have_right) {
+    if (pb && !pb->have_right) {
       pb->have_right = true;
       pb->ratio_right = (float)b1;
       pb->ratio_right2 = (float)b2;
     }
+  }
+  if (pa && pa->have_left) {
+    a1 = pa->ratio_left;
+    a2 = pa->ratio_left2;
+  }
+  if (pb && pb->have_right) {
     b1 = pb->ratio_right;
     b2 = pb->ratio_right2;
   }
@@ -1031,7 +1057,7 @@ int gemm_ozaki_impl(const GemmOp& op, cudaStream_t st, bool plan_only, int* s_ou
   // (Cauchy-Schwarz) = 2^106·min(L1 ratios, product of L2 ratios); an operand with no
   // finite nonzero row/column reads 0 and its product is exact zeros
   const double ratio = std::min(std::min(a1, b1), a2 * b2);
-  const int s_need = std::max(14, std::min(kMaxMod, moduli_for_ratio(std::min(ratio, (double)K))));
+  const int s_need = forced ? 0 : std::max(14, std::min(kMaxMod, moduli_for_ratio(std::min(ratio, (double)K))));
   if (plan_only) {
     *s_out = s_need;
     return 0;
@@ -1045,6 +1071,7 @@ int gemm_ozaki_impl(const GemmOp& op, cudaStream_t st, bool plan_only, int* s_ou
   // moduli are a fixed sequence, so a prefix of its planes is the residues for s)
   if (L->s < s) NNB_TRY(operand_residues(op.A, op.lda, true, c, *L, st));
   if (R->s < s) NNB_TRY(operand_residues(op.B, op.ldb, right_as_rows, c, *R, st));
+  trace_mark(st, "oz split");
   // s int8 GEMMs -> residues
   const int64_t ldr = (N + 15) / 16 * 16;
   DevBuf res;
@@ -1071,9 +1098,12 @@ int gemm_ozaki_impl(const GemmOp& op, cudaStream_t st, bool plan_only, int* s_ou
     count_launch();
     NNB_CUDA(cudaGetLastError());
   }
+  trace_mark(st, "oz gemm");
   // reconstruction + the chain's epilogue
-  return launch_recon(s, res.as<uint8_t>(), ldr, (int)M, (int)N, L->exps.as<int>(), R->exps.as<int>(), op.ep, c,
-                      st);
+  NNB_TRY(launch_recon(s, res.as<uint8_t>(), ldr, (int)M, (int)N, L->exps.as<int>(), R->exps.as<int>(), op.ep, c,
+                       st));
+  trace_mark(st, "oz recon");
+  return 0;
 }
 
 int ozaki_moduli_for(int64_t k) { return std::max(15, moduli_for(k)); }

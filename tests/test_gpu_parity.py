@@ -542,6 +542,50 @@ def test_sparse_laplacian_uses_pair_dictionary(ref):
     assert np.array_equal(x, xr.real)
 
 
+def laplacian_rect(width: int, height: int, shift: float = 1.0):
+    """Dirichlet 5-point Laplacian on a width x height mesh (row-major, row stride width)."""
+    n = width * height
+    r = np.arange(n, dtype=np.int64)
+    i, j = r // width, r % width
+    cols = np.stack([r - width, r - 1, r, r + 1, r + width], axis=1)
+    valid = np.stack([i > 0, j > 0, np.ones(n, bool), j < width - 1, i < height - 1], axis=1)
+    vals = np.broadcast_to(np.array([-1.0, -1.0, 4.0 + shift, -1.0, -1.0]), (n, 5))
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum(valid.sum(axis=1), out=rp[1:])
+    return rp, cols[valid].astype(np.int32), np.ascontiguousarray(vals[valid])
+
+
+@pytest.mark.parametrize("width,height,gamma", [
+    (36, 50, 63),     # narrow tiles, ragged last tile row
+    (132, 70, 31),    # 128-wide tile plus a 4-column straggler; 4 passes of 8
+    (256, 130, 15),   # 4 factors: 1 + 2 + 4 + 8 applications, one pass each
+    (64, 1, 7),       # single mesh row: no up/down neighbours at all
+    (4, 300, 3),      # minimum stencil width
+])
+def test_sparse_stencil_rectangular_meshes(ref, width, height, gamma):
+    """The temporally blocked stencil path (sparse_stencil.cu) on non-square meshes with
+    ragged tiles and pass lengths that are not multiples of 8: bit-identical to the reference."""
+    rp, col, val = laplacian_rect(width, height)
+    n = width * height
+    b = W.rhs(n, seed=width + height)
+    x, cnt = nnb.solve_sparse_factorized(nnb.Csr(rp, col, val, n=n), b, gamma, nnb.Normalization(0.2, valid=True))
+    if height > 1:
+        assert nnb.sparse_last_format() == "row-dictionary-stencil-tb"
+    xr, cr, _ = ref.sparse_factorized(rp, col, val, b, gamma, 0.2)
+    assert cnt == cr and np.array_equal(x, xr.real)
+
+
+def test_sparse_stencil_width_not_multiple_of_4(ref):
+    """Row stride 30: the stencil plan declines (W % 4 != 0) and the row-dictionary kernel
+    runs instead -- same bits."""
+    rp, col, val = laplacian_rect(30, 40)
+    b = W.rhs(1200, seed=5)
+    x, _ = nnb.solve_sparse_factorized(nnb.Csr(rp, col, val, n=1200), b, 63, nnb.Normalization(0.2, valid=True))
+    assert nnb.sparse_last_format() != "row-dictionary-stencil-tb"
+    xr, _, _ = ref.sparse_factorized(rp, col, val, b, 63, 0.2)
+    assert np.array_equal(x, xr.real)
+
+
 def laplacian_7pt(m: int):
     """3-D 7-point Dirichlet Laplacian + I on an m^3 grid (diagonal 7): width 7 rows."""
     n = m ** 3
