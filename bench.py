@@ -309,6 +309,12 @@ def run_dense(args, world, rank):
                        "eps_before_nest": rd.history[0][1],
                        "x_rel_frob_vs_headline_nest": float(torch.linalg.norm(xd - step(x)[0]) / torch.linalg.norm(xd))}
         del xd
+    # the 8-rank sharded schedule emulated on this GPU (virtual ranks run one after another):
+    # its device time against the single-GPU nest is the per-rank compute efficiency the
+    # schedule allows at G=8 (residue splits of the own block, G K-block int8 GEMMs per
+    # product, reconstructions of the own rows) before any communication
+    if not sharded and args.emulated and n >= 8192:
+        out["sharded_emulated"] = run_dense_emulated(nnb, torch, a, x, n, p, 8, ms_step, flops_step)
     # NNB_ORDER_SYMMETRIC on the same nest (A == A^T, X a polynomial in A): upper
     # tile triangles, mirrored — time per nest, reported beside the headline
     if not sharded and args.symmetric:
@@ -342,6 +348,28 @@ def run_dense(args, world, rank):
     if sharded:
         comm.close()
     return out
+
+
+def run_dense_emulated(nnb, torch, a, x, n, p, world, ms_single, flops_step):
+    nnb.ozaki_stats(reset=True)
+    nnb.ozaki_profile(True)
+    xe, re_ = nnb.nn_chain_sharded_emulated(a, world, x, p=p, max_iters=1, final_residual=False)
+    torch.cuda.synchronize()
+    nnb.ozaki_profile(False)
+    oz = nnb.ozaki_stats(reset=True)
+    xs, _ = nnb.nn_chain(a, x, p=p, max_iters=1, final_residual=False)
+    torch.cuda.synchronize()
+    same = bool(torch.equal(torch.as_tensor(xe, device="cuda"), xs))
+    del xe, xs
+    torch.cuda.empty_cache()
+    return {"world": world, "ms_per_nest_all_ranks": round(re_.device_ms, 2),
+            "ms_per_rank_mean": round(re_.device_ms / world, 2),
+            "single_gpu_ms_per_nest": round(ms_single, 2),
+            "compute_efficiency": round(ms_single / re_.device_ms, 4),
+            "x_bit_identical_to_single_gpu": same,
+            "kernels_ms": {k: round(v["ms"], 1) for k, v in oz.items()},
+            "note": f"the {world}-rank row-sharded nest (int8-emulated products, residue-block ring) run as {world} "
+                    "virtual ranks one after another on this GPU; communication not included (one GPU)"}
 
 
 def run_dense_symmetric(nnb, torch, a, n, p, args):
@@ -788,6 +816,8 @@ def main():
     ap.add_argument("--no-symmetric", dest="symmetric", action="store_false",
                     help="skip the NNB_ORDER_SYMMETRIC timing beside the headline nest")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    ap.add_argument("--no-emulated", dest="emulated", action="store_false",
+                    help="skip the 8-rank sharded schedule emulated on one GPU")
     ap.add_argument("--no-dmma", dest="dmma", action="store_false",
                     help="skip the DMMA-only timing of the headline nest")
     ap.add_argument("--sharded", action="store_true",
@@ -805,8 +835,9 @@ def main():
                           f"(A=B·B^T/N+I, X0=A^T/(|A|_1|A|_inf))",
               "n": args.n, "depth_p": args.p, "products_per_step": args.p + 1,
               "l2": "inputs (8*N^2 bytes per matrix) exceed the 126 MB L2; no flush",
-              "parallelism": f"row-sharded x{world} (NCCL ring all-gather overlapped with K-split GEMMs)"
-                             if world > 1 else "single GPU",
+              "parallelism": f"row-sharded x{world} (int8-emulated products: column statistics all-gathered, "
+                             "residue blocks moved by an NCCL ring overlapped with the K-block int8 GEMMs)"
+                             if world > 1 or args.sharded else "single GPU",
               "host_cpu": f"{cores} x {model}"}
     base = {"metric": "NN inversion FP64 TFLOP/s", "unit": "TFLOP/s", "n_gpus": world if args.impl == "ours" else args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -856,6 +887,8 @@ def main():
             line["legs"]["dense_symmetric"] = d["symmetric"]
         if "dmma" in d:
             line["legs"]["dense_dmma"] = d["dmma"]
+        if "sharded_emulated" in d:
+            line["legs"]["dense_sharded_emulated"] = d["sharded_emulated"]
         config["eps_first_last"] = [d["eps_first"], d["eps_last"]]
     if "mimo" in legs:
         line["legs"]["mimo"] = run_mimo(args, world, rank)

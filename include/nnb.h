@@ -317,7 +317,7 @@ int nnb_spectral_norm_shifted_csr(const int64_t* row_ptr, const int32_t* col, co
  * Not in the reference (single-process). */
 typedef struct nnb_comm* nnb_comm_t;
 #define NNB_UNIQUE_ID_BYTES 128
-/* Partition used by the sharded entry points: blocks of whole 8-row units,
+/* Partition used by the sharded entry points: blocks of whole 16-row units,
  * balanced, rank order.  Pure host arithmetic (no device needed). */
 void nnb_partition_rows(int64_t n, int32_t world, int32_t rank, int64_t* row0, int64_t* rows);
 int nnb_comm_unique_id(void* id_out /* NNB_UNIQUE_ID_BYTES */);

@@ -678,7 +678,7 @@ def random_conditioned_complex(n: int, cond: float, seed: int) -> np.ndarray:
 
 # ------------------------------------------------------------ multi-GPU (C4)
 def partition_rows(n: int, world: int, rank: int) -> tuple[int, int]:
-    """(row0, rows) of `rank`'s block in the sharded chain (8-row units, balanced)."""
+    """(row0, rows) of `rank`'s block in the sharded chain (16-row units, balanced)."""
     r0, rs = C.c_int64(), C.c_int64()
     lib().nnb_partition_rows(n, world, rank, C.byref(r0), C.byref(rs))
     return r0.value, rs.value

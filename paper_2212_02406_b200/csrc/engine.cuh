@@ -142,6 +142,28 @@ struct OzPinScope {
     if (p) oz_unpin(p);
   }
 };
+// ---- int8 emulation of a row-sharded product (ozaki.cu; sharded.cu drives it) ----------
+// C_g = epilogue(L_g·F) with F = [F_0; …; F_{G−1}] row-block sharded.  F's column exponents
+// come from every rank's column statistics (gathered, combined in rank order), each rank
+// splits its own block into K-major residues, the residue blocks are all-gathered, and the
+// G block products accumulate mod m_l (oz_gemm_block, `accumulate`) before one
+// reconstruction — every element then equals the single-GPU emulated product's.
+// ratio slots (float bits, as the single-GPU path): [L1 left, L1 right, L2 left, L2 right].
+int oz_col_partials(const double* F, int64_t ld, int64_t rows, int64_t n, double* out /*[3][n]*/, cudaStream_t s);
+int oz_col_combine(const double* gathered /*[world][stride]*/, int world, int64_t stride, int64_t n, int* exps,
+                   unsigned* ratio /*right slots: ratio + 1*/, cudaStream_t s);
+int oz_row_stats(const double* L, int64_t ld, int64_t rows, int64_t k, int* exps, unsigned* ratio, cudaStream_t s);
+int oz_read_ratios(const unsigned* ratio_dev, double out[4], cudaStream_t s);  // synchronises s
+int oz_moduli(double a1, double a2, double b1, double b2, int64_t K);
+int oz_split_left(const double* L, int64_t ld, int64_t rows, int64_t k, const int* exps, int s, int8_t* out,
+                  int64_t kp, cudaStream_t st);
+int oz_split_right(const double* F, int64_t ld, int64_t k_rows, int64_t n, const int* exps, int s, int8_t* out,
+                   int64_t kp, cudaStream_t st);
+int oz_gemm_block(const int8_t* a_res, int64_t M, int64_t a_kp, int64_t a_k0, const int8_t* b_res, int64_t N,
+                  int64_t b_kp, int s, uint8_t* out, int64_t ldr, bool accumulate, cudaStream_t st,
+                  int reserve_sms = 0);  // persistent grid of SMs − reserve_sms CTAs
+int oz_reconstruct(int s, const uint8_t* res, int64_t ldr, int64_t M, int64_t N, const int* ea, const int* eb,
+                   GemmEpilogue ep, struct RedWs* red, cudaStream_t st);
 // the next real chain of the calling thread copies its final residual I − A·X to r (device, ld)
 void set_chain_capture(double* r, int64_t ld);
 // 2D uint8 TMA descriptor (rows × cols bytes, leading dimension ld bytes), 128B swizzle.

@@ -62,6 +62,8 @@ constexpr int64_t kMaxK = 131071;           // 128·128·k < 2^31: exact int32 a
 struct OzConst {
   int s;
   int mi[kMaxMod];
+  unsigned magic[kMaxMod];   // floor(2^32 / m): the epilogue's integer reduction mod m
+  unsigned offset[kMaxMod];  // m·ceil(2^31 / m): a + offset >= 0 for every int32 accumulator a
   float mf[kMaxMod];
   float inv_mf[kMaxMod];
   double md[kMaxMod];
@@ -187,6 +189,8 @@ OzConst make_const(int s) {
   for (int j = 0; j < s; ++j) {
     const int m = kModuli[j];
     c.mi[j] = m;
+    c.magic[j] = static_cast<unsigned>((1ull << 32) / static_cast<unsigned long long>(m));
+    c.offset[j] = static_cast<unsigned>(static_cast<unsigned long long>(m) * (((1ull << 31) + m - 1) / m));
     c.mf[j] = static_cast<float>(m);
     c.inv_mf[j] = 1.0f / static_cast<float>(m);
     c.md[j] = m;
@@ -299,7 +303,7 @@ __device__ __forceinline__ TileCoord tile_of(int t, int tiles_m, int tiles_n, in
 __global__ void __launch_bounds__(192, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, int M, int N,
                    int K, int64_t ldr, uint8_t* __restrict__ out, const OzConst cst, int tiles_m, int tiles_n,
-                   int group_m) {
+                   int group_m, int a_k0, int accumulate) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -341,7 +345,7 @@ __global__ void __launch_bounds__(192, 1)
           if (it >= kStages) mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
           uint8_t* sa = smem + st * kStageBytes;
           mbar_arrive_expect_tx(&full[st], kStageBytes);
-          tma_load_2d(sa, &tma_a, &full[st], kb * kBK, arow);
+          tma_load_2d(sa, &tma_a, &full[st], a_k0 + kb * kBK, arow);
           tma_load_2d(sa + kABytes, &tma_b, &full[st], kb * kBK, brow);
         }
       }
@@ -376,8 +380,8 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&tfull[acc], (n_t >> 1) & 1);
       tc_fence_after();
       const int row = tc.mt * kBM + 32 * q + lane;
-      const int m = cst.mi[tc.l];
-      const double inv = cst.inv_md[tc.l];
+      const unsigned m = static_cast<unsigned>(cst.mi[tc.l]);
+      const unsigned magic = cst.magic[tc.l], off = cst.offset[tc.l];
       uint8_t* orow = out + ((int64_t)tc.l * M + row) * ldr;
 #pragma unroll 1
       for (int c = 0; c < kBN / 32; ++c) {
@@ -386,20 +390,34 @@ __global__ void __launch_bounds__(192, 1)
         const int col = tc.nt * kBN + 32 * c;
         if (row < M && col < ldr) {
           uint32_t packed[8];
+          uint4* dst = reinterpret_cast<uint4*>(orow + col);
+          uint32_t prev[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          if (accumulate) {  // K-split in residue space: this block's product is added mod m_l
+            const uint4 p0 = dst[0];
+            prev[0] = p0.x, prev[1] = p0.y, prev[2] = p0.z, prev[3] = p0.w;
+            if (col + 16 < ldr) {
+              const uint4 p1 = dst[1];
+              prev[4] = p1.x, prev[5] = p1.y, prev[6] = p1.z, prev[7] = p1.w;
+            }
+          }
+          // a mod m in integer arithmetic (the FP64 form made this epilogue FP64-pipe bound
+          // once K blocks got short): |a| < 2^14·K < 2^31 − 2^14, so u = a + offset is in
+          // [0, 2^32) and u ≡ a (mod m); q = umulhi(u, floor(2^32/m)) is floor(u/m) or one
+          // less, so u − q·m is in [0, 2m) and one unsigned min brings it into [0, m)
 #pragma unroll
           for (int w = 0; w < 8; ++w) {
             uint32_t word = 0;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-              const int a = static_cast<int>(v[4 * w + b]);
-              int r = a - m * __double2int_rd(static_cast<double>(a) * inv);
-              r += (r < 0) ? m : 0;
-              r -= (r >= m) ? m : 0;
-              word |= static_cast<uint32_t>(r) << (8 * b);
+              const unsigned u = v[4 * w + b] + off;
+              unsigned r = u - __umulhi(u, magic) * m;
+              r = min(r, r - m);
+              r += (prev[w] >> (8 * b)) & 0xffu;  // K-split: add the earlier blocks' residue
+              r = min(r, r - m);
+              word |= r << (8 * b);
             }
             packed[w] = word;
           }
-          uint4* dst = reinterpret_cast<uint4*>(orow + col);
           dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
           if (col + 16 < ldr) dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
         }
@@ -599,6 +617,79 @@ __global__ void __launch_bounds__(256) oz_colratio_kernel(const unsigned long lo
         sum += colsum[(int64_t)b * n + c];
         sq += colsq[(int64_t)b * n + c];
       }
+      r = static_cast<float>(sum / mx) * 1.0001f;
+      r2 = static_cast<float>(sqrt(sq) / mx) * 1.0001f;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r = fmaxf(r, __shfl_xor_sync(0xffffffffu, r, o));
+    r2 = fmaxf(r2, __shfl_xor_sync(0xffffffffu, r2, o));
+  }
+  if ((threadIdx.x & 31) == 0 && r > 0.0f) {
+    atomicMax(ratio, __float_as_uint(r));
+    atomicMax(ratio + 2, __float_as_uint(r2));
+  }
+}
+
+// Row-sharded right operand (sharded.cu): per-column statistics of one rank's row block,
+// combined over the ranks in rank order.  part[y][3][n] per 256-row block y: max|x| (+inf
+// when the block holds a non-finite entry), Σ|x|, Σx².
+__global__ void __launch_bounds__(256) oz_colpart_kernel(const double* __restrict__ B, int64_t ld, int k, int n,
+                                                         double* __restrict__ part) {
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= n) return;
+  const int r0 = blockIdx.y * 256, r1 = min(k, r0 + 256);
+  double mx = 0.0, sum = 0.0, sq = 0.0;
+  int bad = 0;
+  for (int r = r0; r < r1; ++r) {
+    const double v = B[(int64_t)r * ld + c];
+    bad |= !isfinite(v);
+    mx = fmax(mx, fabs(v));
+    sum += fabs(v);
+    sq = fma(v, v, sq);
+  }
+  double* o = part + (int64_t)blockIdx.y * 3 * n + c;
+  o[0] = bad ? INFINITY : mx;
+  o[n] = sum;
+  o[2 * (int64_t)n] = sq;
+}
+// out[3][n] = the rank's column statistics: the 256-row block partials in block order
+// (for one rank: the same sums oz_colratio_kernel forms for the whole operand)
+__global__ void __launch_bounds__(256) oz_colpart_sum_kernel(const double* __restrict__ part, int kblocks, int n,
+                                                             double* __restrict__ out) {
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= n) return;
+  double mx = 0.0, sum = 0.0, sq = 0.0;
+  for (int y = 0; y < kblocks; ++y) {
+    const double* o = part + (int64_t)y * 3 * n + c;
+    mx = fmax(mx, o[0]);
+    sum += o[n];
+    sq += o[2 * (int64_t)n];
+  }
+  out[c] = mx;
+  out[n + c] = sum;
+  out[2 * (int64_t)n + c] = sq;
+}
+// gathered[g][3][n] (g in rank order) -> global column exponents and the L1/L2 ratio bounds
+// (ratio[0], ratio[2], as oz_colratio_kernel); identical on every rank
+__global__ void __launch_bounds__(256) oz_colcombine_kernel(const double* __restrict__ gathered, int world, int n,
+                                                            int64_t stride, int* __restrict__ exps,
+                                                            unsigned* __restrict__ ratio) {
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  float r = 0.0f, r2 = 0.0f;
+  if (c < n) {
+    double mx = 0.0, sum = 0.0, sq = 0.0;
+    bool bad = false;
+    for (int g = 0; g < world; ++g) {
+      const double* o = gathered + (int64_t)g * stride;
+      bad |= isinf(o[c]);
+      mx = fmax(mx, o[c]);
+      sum += o[n + c];
+      sq += o[2 * (int64_t)n + c];
+    }
+    exps[c] = bad ? kBadExp : exp_for(mx);
+    if (!bad && mx > 0.0) {
       r = static_cast<float>(sum / mx) * 1.0001f;
       r2 = static_cast<float>(sqrt(sq) / mx) * 1.0001f;
     }
@@ -959,6 +1050,38 @@ void oz_unpin(const double* p) {
 int make_tmap_u8(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                  int box_cols);
 
+// s int8 GEMMs out[l] = (a_l[:, a_k0 : a_k0+K] · b_lᵀ) mod m_l (+ out[l] mod m_l when
+// `accumulate`): a_l = a_res[l·M .. l·M+M) (row stride a_kp), b_l = b_res[l·N .. l·N+N)
+// (row stride b_kp, zero beyond b_kp).  a_k0 > 0 multiplies a column block of the left
+// operand's residues with a row block of the right operand's (the sharded K split);
+// the left operand's columns past the block meet the right block's zeros.
+int launch_oz_gemm(const int8_t* a_res, int64_t M, int64_t a_kp, int64_t a_k0, const int8_t* b_res, int64_t N,
+                   int64_t b_kp, int64_t K, const OzConst& c, uint8_t* out, int64_t ldr, bool accumulate,
+                   cudaStream_t st, int reserve_sms = 0) {
+  const int s = c.s;
+  CUtensorMap ta, tb;
+  NNB_TRY(make_tmap_u8(&ta, a_res, (int64_t)s * M, a_kp, a_kp, kBM, kBK));
+  NNB_TRY(make_tmap_u8(&tb, b_res, (int64_t)s * N, b_kp, b_kp, kBN, kBK));
+  NNB_TRY(ensure_smem<oz_gemm_kernel>(kGemmSmem));
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    NNB_CUDA(cudaGetDevice(&dev));
+    NNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int tiles_m = (int)((M + kBM - 1) / kBM), tiles_n = (int)((N + kBN - 1) / kBN);
+  const int64_t total = (int64_t)tiles_m * tiles_n * s;
+  if (total > INT32_MAX) return fail(7, "ozaki: too many tiles");
+  Timed tm(0, 2.0 * s * (double)M * N * K, st);  // int8 tensor ops
+  const unsigned grid = (unsigned)std::min<int64_t>(total, std::max(1, sms - reserve_sms));
+  static const int gm = debug_env("NNB_OZ_GROUP") ? std::atoi(debug_env("NNB_OZ_GROUP")) : kGroupM;
+  oz_gemm_kernel<<<grid, 192, kGemmSmem, st>>>(ta, tb, (int)M, (int)N, (int)K, ldr, out, c, tiles_m, tiles_n, gm,
+                                               (int)a_k0, accumulate ? 1 : 0);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
 thread_local int g_forced_s = 0;  // ozaki_force_moduli: a chunked product uses its whole product's count
 
 int gemm_ozaki_impl(const GemmOp& op, cudaStream_t st, bool plan_only, int* s_out);
@@ -1076,28 +1199,8 @@ int gemm_ozaki_impl(const GemmOp& op, cudaStream_t st, bool plan_only, int* s_ou
   const int64_t ldr = (N + 15) / 16 * 16;
   DevBuf res;
   NNB_TRY(res.alloc((size_t)s * M * ldr, st));
-  CUtensorMap ta, tb;
-  NNB_TRY(make_tmap_u8(&ta, L->res.p, (int64_t)s * M, L->kp, L->kp, kBM, kBK));
-  NNB_TRY(make_tmap_u8(&tb, R->res.p, (int64_t)s * N, R->kp, R->kp, kBN, kBK));
-  NNB_TRY(ensure_smem<oz_gemm_kernel>(kGemmSmem));
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    NNB_CUDA(cudaGetDevice(&dev));
-    NNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
-  const int tiles_m = (int)((M + kBM - 1) / kBM), tiles_n = (int)((N + kBN - 1) / kBN);
-  const int64_t total = (int64_t)tiles_m * tiles_n * s;
-  if (total > INT32_MAX) return fail(7, "ozaki: too many tiles");
-  {
-    Timed tm(0, 2.0 * s * (double)M * N * K, st);  // int8 tensor ops
-    const unsigned grid = (unsigned)std::min<int64_t>(total, sms);
-    static const int gm = debug_env("NNB_OZ_GROUP") ? std::atoi(debug_env("NNB_OZ_GROUP")) : kGroupM;
-    oz_gemm_kernel<<<grid, 192, kGemmSmem, st>>>(ta, tb, (int)M, (int)N, (int)K, ldr, res.as<uint8_t>(), c,
-                                                 tiles_m, tiles_n, gm);
-    count_launch();
-    NNB_CUDA(cudaGetLastError());
-  }
+  NNB_TRY(launch_oz_gemm(L->res.as<int8_t>(), M, L->kp, 0, R->res.as<int8_t>(), N, R->kp, K, c, res.as<uint8_t>(),
+                         ldr, false, st));
   trace_mark(st, "oz gemm");
   // reconstruction + the chain's epilogue
   NNB_TRY(launch_recon(s, res.as<uint8_t>(), ldr, (int)M, (int)N, L->exps.as<int>(), R->exps.as<int>(), op.ep, c,
@@ -1138,6 +1241,115 @@ void ozaki_stats(double* ms, double* work, int64_t* launches, int reset) {
       S.n[c] = 0;
     }
   }
+}
+
+// ---------------------------------------------------------------- row-sharded products
+// (sharded.cu drives them; see engine.cuh)
+int oz_col_partials(const double* F, int64_t ld, int64_t rows, int64_t n, double* out, cudaStream_t st) {
+  if (n <= 0) return 0;
+  const int64_t kb = std::max<int64_t>((rows + 255) / 256, 1);
+  DevBuf part;
+  NNB_TRY(part.alloc(sizeof(double) * 3 * kb * n, st));
+  Timed tm(1, (double)rows * n * 8.0, st);
+  if (rows > 0) {
+    oz_colpart_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)kb), 256, 0, st>>>(F, ld, (int)rows, (int)n,
+                                                                                    part.as<double>());
+    oz_colpart_sum_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part.as<double>(), (int)kb, (int)n, out);
+    count_launch(2);
+  } else {
+    NNB_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 3 * n, st));
+  }
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int oz_col_combine(const double* gathered, int world, int64_t stride, int64_t n, int* exps, unsigned* ratio,
+                   cudaStream_t st) {
+  if (n <= 0) return 0;
+  oz_colcombine_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(gathered, world, (int)n, stride, exps, ratio);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int oz_row_stats(const double* L, int64_t ld, int64_t rows, int64_t k, int* exps, unsigned* ratio, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  Timed tm(1, (double)rows * k * 8.0, st);
+  oz_rowstat_kernel<<<static_cast<unsigned>(rows), 256, 0, st>>>(L, ld, (int)rows, (int)k, exps, ratio);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int oz_read_ratios(const unsigned* rd, double out[4], cudaStream_t st) {
+  static thread_local unsigned* host = nullptr;
+  static thread_local unsigned* mapped = nullptr;
+  if (!host) {
+    NNB_CUDA(cudaHostAlloc(&host, sizeof(unsigned) * 4, cudaHostAllocMapped));
+    NNB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mapped), host, 0));
+  }
+  oz_ratio_out_kernel<<<1, 32, 0, st>>>(rd, mapped);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  NNB_CUDA(cudaStreamSynchronize(st));
+  for (int i = 0; i < 4; ++i) out[i] = std::max((double)__builtin_bit_cast(float, host[i]), 1.0);
+  return 0;
+}
+
+int oz_moduli(double a1, double a2, double b1, double b2, int64_t K) {
+  const double ratio = std::min(std::min(a1, b1), a2 * b2);
+  return std::max(14, std::min(kMaxMod, moduli_for_ratio(std::min(ratio, (double)K))));
+}
+
+int oz_split_left(const double* L, int64_t ld, int64_t rows, int64_t k, const int* exps, int s, int8_t* out,
+                  int64_t kp, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  if (s > 17) return fail(7, "ozaki: more than 17 moduli needed");
+  const OzConst c = make_const(s);
+  Timed tm(1, (double)rows * k * (8.0 + s), st);
+  oz_split_rows_kernel<<<static_cast<unsigned>(rows), 256, 0, st>>>(L, ld, (int)rows, (int)k, kp, out, exps, c);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int oz_split_right(const double* F, int64_t ld, int64_t k_rows, int64_t n, const int* exps, int s, int8_t* out,
+                   int64_t kp, cudaStream_t st) {
+  if (n <= 0 || kp <= 0) return 0;
+  if (s > 17) return fail(7, "ozaki: more than 17 moduli needed");
+  const OzConst c = make_const(s);
+  Timed tm(1, (double)k_rows * n * (8.0 + s), st);
+  oz_split_cols_kernel<<<dim3((unsigned)((n + 63) / 64), (unsigned)((kp + 63) / 64)), 256, 0, st>>>(
+      F, ld, (int)k_rows, (int)n, kp, out, exps, c);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int oz_gemm_block(const int8_t* a_res, int64_t M, int64_t a_kp, int64_t a_k0, const int8_t* b_res, int64_t N,
+                  int64_t b_kp, int s, uint8_t* out, int64_t ldr, bool accumulate, cudaStream_t st,
+                  int reserve_sms) {
+  if (M <= 0 || N <= 0) return 0;
+  if (s > 17) return fail(7, "ozaki: more than 17 moduli needed");
+  // a TMA box must start on a 16-byte boundary of the row (the sharded partition's 16-row
+  // units guarantee it for the block origins)
+  if (a_k0 % 16 || b_kp % 16 || a_kp % 16) return fail(7, "ozaki: block origin or stride not a multiple of 16 bytes");
+  return launch_oz_gemm(a_res, M, a_kp, a_k0, b_res, N, b_kp, b_kp, make_const(s), out, ldr, accumulate, st,
+                        reserve_sms);
+}
+
+int oz_reconstruct(int s, const uint8_t* res, int64_t ldr, int64_t M, int64_t N, const int* ea, const int* eb,
+                   GemmEpilogue ep, RedWs* red, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return 0;
+  if (red) {
+    if (red->capacity < max_tiles_for(M, N)) return fail(7, "ozaki: reduction workspace too small");
+    ep.ss_partial = red->ss_partial;
+    ep.nf_partial = red->nf_partial;
+    ep.tile_counter = red->counter;
+  } else {
+    ep.ss_partial = nullptr;
+  }
+  return launch_recon(s, res, ldr, (int)M, (int)N, ea, eb, ep, make_const(s), st);
 }
 
 }  // namespace nnb

@@ -1,7 +1,7 @@
 // Row-sharded Nested Neumann chain across GPUs (BASELINE config 3:
 // N=32768 on 1/2/4/8 B200s) — SURVEY.md §8(e).
 //
-// Rank g owns the rows J_g = [row0_g, row0_g+rows_g) of A and X (8-row units,
+// Rank g owns the rows J_g = [row0_g, row0_g+rows_g) of A and X (16-row units,
 // balanced).  Per nest, with full-size ping-pong buffers XF[2] and RF:
 //   1. ring all-gather of X (NCCL send/recv on a side stream, G−1 steps);
 //      overlapped with the K-split product
@@ -25,6 +25,8 @@
 
 #include <cmath>
 #include <cstring>
+#include <functional>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -144,15 +146,19 @@ struct Shard {
   RedWs red;
 };
 
+// 16-row units: every block starts at a multiple of 16 rows, so a block's columns of a
+// left operand's int8 residues start on a 16-byte boundary (the TMA box origin the
+// sharded int8 GEMM needs), and FP64 rows stay 16-byte aligned for the DMMA path
 void partition(int64_t n, int world, std::vector<int64_t>& row0, std::vector<int64_t>& rows) {
-  const int64_t units = (n + 7) / 8;
+  constexpr int64_t kUnit = 16;
+  const int64_t units = (n + kUnit - 1) / kUnit;
   row0.assign(world, 0);
   rows.assign(world, 0);
   int64_t u0 = 0;
   for (int g = 0; g < world; ++g) {
     const int64_t u = units / world + (g < units % world ? 1 : 0);
-    row0[g] = std::min<int64_t>(n, u0 * 8);
-    rows[g] = std::min<int64_t>(n, (u0 + u) * 8) - row0[g];
+    row0[g] = std::min<int64_t>(n, u0 * kUnit);
+    rows[g] = std::min<int64_t>(n, (u0 + u) * kUnit) - row0[g];
     u0 += u;
   }
 }
@@ -240,9 +246,232 @@ int ksplit_product(Shard& sh, int g, const double* L, int64_t ldl, const double*
   return 0;
 }
 
+// ---- int8 emulation of the sharded products (NNB_ARITH_FAST at large n, NNB_ARITH_OZAKI) ----
+// The right operand F (X for the residual product, R for the Horner products) is gathered
+// as int8 residues instead of FP64 rows:
+//   1. every rank reduces its rows of F to per-column [max|x|, Σ|x|, Σx²]; the G records are
+//      all-gathered and combined in rank order into F's column exponents and ratio bounds
+//      (identical on every rank);
+//   2. the moduli count s comes from those and the left operands' row ratios (a 16-byte
+//      all-gather), the same count the single-GPU product of the whole matrices takes;
+//   3. each rank splits its own block of F into K-major residues [s][n][kpb_g] (block g at a
+//      fixed offset of one gathered buffer) and a ring all-gather moves the residue blocks;
+//   4. rank g's product runs as G int8 GEMMs over the K blocks (own block first, then ring
+//      order, each waiting only for its block) accumulating mod m_l, then one
+//      reconstruction with the chain's epilogue.
+// Every element equals the single-GPU emulated product's (same exponents, same residues, an
+// exact modular sum, the same Garner reconstruction), so the sharded X matches the
+// single-GPU X; FP64 traffic per nest drops to the G small records.
+__global__ void max_slots_kernel(const unsigned* __restrict__ slots, int world, unsigned* __restrict__ out) {
+  if (threadIdx.x < 4) {
+    unsigned m = 0;
+    for (int g = 0; g < world; ++g) m = max(m, slots[4 * g + threadIdx.x]);  // float bits >= 0: ordered
+    out[threadIdx.x] = m;
+  }
+}
+
+constexpr int kRingSms = 8;  // SMs the int8 GEMM leaves free while the residue ring runs
+
+struct OzSh {
+  int64_t n = 0, kp = 0, kp_total = 0, stride = 0;  // stride: doubles per rank record
+  std::vector<int64_t> kpb, koff;
+  DevBuf stats;  // [G][stride]: 3n column statistics + 2 doubles (= 4 ratio slots)
+  DevBuf ints;   // fexps[n] | aexps[n] | lexps[n] | rd[4] | rdf[4]
+  DevBuf fres;   // gathered residues of F: block j at s·n·koff_j
+  int fcap = 0, fplanes = 0;
+  bool fcombined = false, fknown = false;
+  double fb1 = 1.0, fb2 = 1.0;
+  std::vector<std::unique_ptr<DevBuf>> ares;  // pinned A: residues per local rank
+  std::vector<int> aplanes;
+  bool aknown = false;
+  double aa1 = 1.0, aa2 = 1.0;
+  DevBuf lres, out, slots;   // slots: [G][4] ratio slots
+  int64_t lcap = 0, ocap = 0;
+  const double* fsrc = nullptr;  // the F whose statistics were gathered last
+  int* fexps() const { return ints.as<int>(); }
+  int* aexps() const { return ints.as<int>() + n; }
+  int* lexps() const { return ints.as<int>() + 2 * n; }
+  unsigned* rd() const { return reinterpret_cast<unsigned*>(ints.as<int>() + 3 * n); }
+  unsigned* rdf() const { return rd() + 4; }
+};
+
+// in-place all-gather of equal per-rank records (count doubles each) on the comm stream
+int gather_records(Shard& sh, double* buf, size_t count) {
+  if (!sh.comm || sh.world == 1) return 0;
+  NNB_CUDA(cudaEventRecord(sh.ready, sh.s));
+  NNB_CUDA(cudaStreamWaitEvent(sh.comm->cs, sh.ready, 0));
+  NNB_NCCL(nccl().allGather(buf + count * sh.comm->rank, buf, count, ncclDouble, sh.comm->comm, sh.comm->cs));
+  NNB_CUDA(cudaEventRecord(sh.ev[0], sh.comm->cs));
+  NNB_CUDA(cudaStreamWaitEvent(sh.s, sh.ev[0], 0));
+  return 0;
+}
+
+int oz_init(Shard& sh, OzSh& oz) {
+  const int G = sh.world;
+  oz.n = sh.n;
+  oz.kp = (sh.n + 15) / 16 * 16;
+  oz.kpb.assign(G, 0);
+  oz.koff.assign(G, 0);
+  oz.kp_total = 0;
+  for (int j = 0; j < G; ++j) {
+    oz.kpb[j] = (sh.rows[j] + 15) / 16 * 16;
+    oz.koff[j] = oz.kp_total;
+    oz.kp_total += oz.kpb[j];
+  }
+  oz.stride = 3 * sh.n + 2;
+  NNB_TRY(oz.stats.alloc(sizeof(double) * oz.stride * G, sh.s));
+  NNB_TRY(oz.ints.alloc(sizeof(int) * (3 * sh.n + 8), sh.s));
+  NNB_TRY(oz.slots.alloc(sizeof(unsigned) * 4 * G, sh.s));
+  oz.ares.clear();
+  for (size_t i = 0; i < sh.local.size(); ++i) oz.ares.emplace_back(new DevBuf());
+  oz.aplanes.assign(sh.local.size(), 0);
+  return 0;
+}
+
+// step 1 for a new F (full-size buffer, rank g's rows at row0_g)
+int oz_prepare_right(Shard& sh, OzSh& oz, const double* F) {
+  for (int g : sh.local)
+    NNB_TRY(oz_col_partials(F + sh.row0[g] * sh.ld, sh.ld, sh.rows[g], sh.n, oz.stats.as<double>() + g * oz.stride,
+                            sh.s));
+  NNB_TRY(gather_records(sh, oz.stats.as<double>(), (size_t)oz.stride));
+  oz.fsrc = F;
+  oz.fcombined = false;
+  oz.fknown = false;
+  oz.fplanes = 0;
+  return 0;
+}
+
+// in-place ring all-gather of F's residue blocks (s planes) on the comm stream
+int oz_ring(Shard& sh, OzSh& oz, int s) {
+  if (!sh.comm || sh.world == 1) return 0;
+  auto& api = nccl();
+  const int G = sh.world, me = sh.comm->rank;
+  uint8_t* base = oz.fres.as<uint8_t>();
+  auto blk = [&](int j) { return base + (size_t)s * oz.n * oz.koff[j]; };
+  auto bytes = [&](int j) { return (size_t)s * oz.n * oz.kpb[j]; };
+  NNB_CUDA(cudaEventRecord(sh.ready, sh.s));
+  NNB_CUDA(cudaStreamWaitEvent(sh.comm->cs, sh.ready, 0));
+  for (int q = 1; q < G; ++q) {
+    const int send_blk = ((me - q + 1) % G + G) % G, recv_blk = ((me - q) % G + G) % G;
+    NNB_NCCL(api.groupStart());
+    if (bytes(send_blk)) NNB_NCCL(api.send(blk(send_blk), bytes(send_blk), ncclUint8, (me + 1) % G, sh.comm->comm, sh.comm->cs));
+    if (bytes(recv_blk)) NNB_NCCL(api.recv(blk(recv_blk), bytes(recv_blk), ncclUint8, (me - 1 + G) % G, sh.comm->comm, sh.comm->cs));
+    NNB_NCCL(api.groupEnd());
+    NNB_CUDA(cudaEventRecord(sh.ev[q], sh.comm->cs));
+  }
+  return 0;
+}
+
+// steps 2-4: C_g = ep_of(g)(L_g·F) for every local rank g; after(g) runs on the stream
+// right after rank g's reconstruction.  `pinned`: L is the chain's A (splits kept).
+int oz_product(Shard& sh, OzSh& oz, const std::function<const double*(int)>& left, int64_t ldl, bool pinned,
+               const std::function<GemmEpilogue(int)>& ep_of, const std::function<int(int)>& after) {
+  const int G = sh.world;
+  const int64_t n = sh.n;
+  int* lexps = pinned ? oz.aexps() : oz.lexps();
+  // ---- 2. moduli count: F's column ratios (combined once per F), the left rows' ratios
+  const bool need_left = !(pinned && oz.aknown);
+  double a1 = oz.aa1, a2 = oz.aa2;
+  if (!oz.fcombined || need_left) {
+    unsigned* rd = oz.rd();
+    NNB_CUDA(cudaMemsetAsync(rd, 0, sizeof(unsigned) * 4, sh.s));
+    if (!oz.fcombined) {
+      NNB_TRY(oz_col_combine(oz.stats.as<double>(), G, oz.stride, n, oz.fexps(), rd + 1, sh.s));
+      oz.fcombined = true;
+    }
+    if (need_left)
+      for (int g : sh.local)
+        NNB_TRY(oz_row_stats(left(g), ldl, sh.rows[g], n, lexps + sh.row0[g], rd, sh.s));
+    double r[4];
+    if (sh.comm && G > 1) {  // every rank's 4 slots (16 B), then the slot-wise max
+      unsigned* slots = oz.slots.as<unsigned>();
+      NNB_CUDA(cudaMemcpyAsync(slots + 4 * sh.comm->rank, rd, sizeof(unsigned) * 4, cudaMemcpyDeviceToDevice, sh.s));
+      NNB_TRY(gather_records(sh, oz.slots.as<double>(), 2));
+      max_slots_kernel<<<1, 32, 0, sh.s>>>(slots, G, oz.rdf());
+      count_launch();
+      NNB_TRY(oz_read_ratios(oz.rdf(), r, sh.s));
+    } else {
+      NNB_TRY(oz_read_ratios(rd, r, sh.s));
+    }
+    if (!oz.fknown) {
+      oz.fb1 = r[1];
+      oz.fb2 = r[3];
+      oz.fknown = true;
+    }
+    if (need_left) {
+      a1 = r[0];
+      a2 = r[2];
+      if (pinned) {
+        oz.aa1 = a1;
+        oz.aa2 = a2;
+        oz.aknown = true;
+      }
+    }
+  }
+  const int s = oz_moduli(a1, a2, oz.fb1, oz.fb2, n);
+  // ---- 3. F's residues: own block(s) split, then the ring (again only if s grew)
+  if (oz.fplanes < s) {
+    if (oz.fcap < s) {
+      NNB_TRY(oz.fres.alloc((size_t)s * n * oz.kp_total, sh.s));
+      oz.fcap = s;
+    }
+    for (int g : sh.local)
+      NNB_TRY(oz_split_right(oz.fsrc + sh.row0[g] * sh.ld, sh.ld, sh.rows[g], n, oz.fexps(), s,
+                             oz.fres.as<int8_t>() + (size_t)s * n * oz.koff[g], oz.kpb[g], sh.s));
+    NNB_TRY(oz_ring(sh, oz, s));
+    oz.fplanes = s;
+  }
+  const int fs = oz.fplanes;  // F's planes (a prefix of them serves s)
+  // ---- 4. per local rank: left residues, the G block GEMMs, the reconstruction
+  for (size_t li = 0; li < sh.local.size(); ++li) {
+    const int g = sh.local[li];
+    const int64_t rows = sh.rows[g];
+    if (rows == 0) continue;
+    DevBuf* lbuf = &oz.lres;
+    if (pinned) {
+      lbuf = oz.ares[li].get();
+      if (oz.aplanes[li] < s) {
+        NNB_TRY(lbuf->alloc((size_t)s * rows * oz.kp, sh.s));
+        NNB_TRY(oz_split_left(left(g), ldl, rows, n, lexps + sh.row0[g], s, lbuf->as<int8_t>(), oz.kp, sh.s));
+        oz.aplanes[li] = s;
+      }
+    } else {
+      if (oz.lcap < (int64_t)s * rows) {
+        NNB_TRY(oz.lres.alloc((size_t)s * rows * oz.kp, sh.s));
+        oz.lcap = (int64_t)s * rows;
+      }
+      NNB_TRY(oz_split_left(left(g), ldl, rows, n, lexps + sh.row0[g], s, lbuf->as<int8_t>(), oz.kp, sh.s));
+    }
+    if (oz.ocap < (int64_t)s * rows) {
+      NNB_TRY(oz.out.alloc((size_t)s * rows * oz.kp, sh.s));
+      oz.ocap = (int64_t)s * rows;
+    }
+    // residue arrays are plane-major, so an array split for more planes than s serves s as
+    // its first s planes; only F's block offsets depend on the planes it was split with (fs)
+    bool first = true;
+    for (int q = 0; q < G; ++q) {
+      const int j = ((g - q) % G + G) % G;
+      if (sh.rows[j] == 0) continue;
+      if (sh.comm && q > 0) NNB_CUDA(cudaStreamWaitEvent(sh.s, sh.ev[q], 0));
+      // the int8 GEMM is persistent (one CTA per SM, never yielding): while ring steps are
+      // still to come it leaves kRingSms SMs to NCCL's send/recv CTAs, which could not
+      // otherwise be scheduled before the grid drains (stream priority orders only pending CTAs)
+      const int reserve = (sh.comm && G > 1 && q < G - 1) ? kRingSms : 0;
+      NNB_TRY(oz_gemm_block(lbuf->as<int8_t>(), rows, oz.kp, sh.row0[j],
+                            oz.fres.as<int8_t>() + (size_t)fs * n * oz.koff[j], n, oz.kpb[j], s,
+                            oz.out.as<uint8_t>(), oz.kp, !first, sh.s, reserve));
+      first = false;
+    }
+    NNB_TRY(oz_reconstruct(s, oz.out.as<uint8_t>(), oz.kp, rows, n, lexps + sh.row0[g], oz.fexps(), ep_of(g),
+                           &sh.red, sh.s));
+    NNB_TRY(after(g));
+  }
+  return 0;
+}
+
 int run_sharded(Shard& sh, const double* A_local, int64_t lda_rows_stride, bool a_full,
                 double* XF0, double* XF1, double* RF, double* Vbase, const ChainCfg& cfg,
-                double* eps_hist, ChainOut* out) {
+                double* eps_hist, ChainOut* out, OzSh* oz) {
   const int G = sh.world, p = cfg.p;
   const int64_t ld = sh.ld;
   const int slots = cfg.max_iters + 1;
@@ -308,12 +537,34 @@ int run_sharded(Shard& sh, const double* A_local, int64_t lda_rows_stride, bool 
       if (bad) break;  // reported below from the device flags
     }
     // ---- R_g = I_g − A_g·X (ring all-gather of X overlapped) ----
-    NNB_TRY(ring_allgather(sh, XF[cur]));
-    for (int g : sh.local) {
-      NNB_TRY(ksplit_product(sh, g, a_rows(g), lda_rows_stride, XF[cur], -1.0, nullptr, 0.0, 1.0,
-                             RF + sh.row0[g] * ld, ld, true, ss_tmp, nf_tmp));
-      pack_pair_kernel<<<1, 32, 0, sh.s>>>(ss_tmp, nf_tmp, pairs + 2 * g);
-      count_launch();
+    if (oz) {
+      NNB_TRY(oz_prepare_right(sh, *oz, XF[cur]));
+      NNB_TRY(oz_product(
+          sh, *oz, a_rows, lda_rows_stride, true,
+          [&](int g) {
+            GemmEpilogue ep;
+            ep.C = RF + sh.row0[g] * ld;
+            ep.ldc = ld;
+            ep.alpha = -1.0;
+            ep.gamma = 1.0;
+            ep.diag_offset = sh.row0[g];
+            ep.ss_out = ss_tmp;
+            ep.nf_out = nf_tmp;
+            return ep;
+          },
+          [&](int g) {
+            pack_pair_kernel<<<1, 32, 0, sh.s>>>(ss_tmp, nf_tmp, pairs + 2 * g);
+            count_launch();
+            return 0;
+          }));
+    } else {
+      NNB_TRY(ring_allgather(sh, XF[cur]));
+      for (int g : sh.local) {
+        NNB_TRY(ksplit_product(sh, g, a_rows(g), lda_rows_stride, XF[cur], -1.0, nullptr, 0.0, 1.0,
+                               RF + sh.row0[g] * ld, ld, true, ss_tmp, nf_tmp));
+        pack_pair_kernel<<<1, 32, 0, sh.s>>>(ss_tmp, nf_tmp, pairs + 2 * g);
+        count_launch();
+      }
     }
     // ---- eps: per-rank pairs gathered, summed in rank order ----
     NNB_TRY(gather_pairs(sh, pairs, gathered));
@@ -338,8 +589,32 @@ int run_sharded(Shard& sh, const double* A_local, int64_t lda_rows_stride, bool 
     if (last) break;
     if (p == 0) continue;
     // ---- Horner: V_g = X_g + V_g·R (ring all-gather of R overlapped with the first) ----
-    NNB_TRY(ring_allgather(sh, RF));
     const int nxt = cur ^ 1;
+    if (oz) {
+      NNB_TRY(oz_prepare_right(sh, *oz, RF));
+      for (int j = 1; j <= p; ++j) {
+        // V_g = X_g + V_g·R, the first V_g being X_g; the last lands in XF[nxt]
+        NNB_TRY(oz_product(
+            sh, *oz,
+            [&](int g) -> const double* {
+              return j == 1 ? XF[cur] + sh.row0[g] * ld : vbuf(g, (j - 2) & 1);
+            },
+            ld, false,
+            [&](int g) {
+              GemmEpilogue ep;
+              ep.C = (j == p) ? XF[nxt] + sh.row0[g] * ld : vbuf(g, (j - 1) & 1);
+              ep.ldc = ld;
+              ep.D = XF[cur] + sh.row0[g] * ld;
+              ep.ldd = ld;
+              ep.beta = 1.0;
+              ep.ss_out = ss_tmp + 1;
+              ep.nf_out = nf_tmp + 8 + g;
+              return ep;
+            },
+            [](int) { return 0; }));
+      }
+    } else {
+    NNB_TRY(ring_allgather(sh, RF));
     for (int g : sh.local) {
       const double* xg = XF[cur] + sh.row0[g] * ld;
       const double* v = xg;
@@ -350,6 +625,7 @@ int run_sharded(Shard& sh, const double* A_local, int64_t lda_rows_stride, bool 
                                nf_tmp + 8 + g));
         v = dst;
       }
+    }
     }
     products += p;  // global N^3-equivalent products (each rank did its row share)
     // fold this nest's Horner non-finite flags (all local ranks; gathered over ranks below)
@@ -462,6 +738,12 @@ int nnb_comm_destroy(nnb_comm_t comm) {
   return 0;
 }
 
+// the sharded products take the int8 emulation exactly where the single-GPU chain's
+// products of the whole matrices would (engine.cu gemm())
+static bool use_ozaki(int64_t n) {
+  return n <= 131071 && (arith() == 2 || (arith() == 0 && ozaki_pays(n, n, n)));
+}
+
 static int chain_cfg_sharded(const nnb_chain_config* cfg, ChainCfg* c) {
   if (!cfg) return fail(NNB_ERR_DOMAIN, "sharded chain: config is NULL");
   if (cfg->depth_p < 0 || cfg->max_iters < 0) return fail(NNB_ERR_DOMAIN, "sharded chain: bad depth/budget");
@@ -543,8 +825,14 @@ int nnb_nn_chain_sharded_d(nnb_comm_t comm, const double* A_rows, int64_t n, con
     default:
       return fail(NNB_ERR_DOMAIN, "sharded chain: unknown X0 kind");
   }
+  OzSh ozs;
+  OzSh* oz = nullptr;
+  if (use_ozaki(n)) {
+    NNB_TRY(oz_init(sh, ozs));
+    oz = &ozs;
+  }
   ChainOut o;
-  const int st = run_sharded(sh, Ag, ld, false, XF0, XF1, RF, V, c, eps_hist, &o);
+  const int st = run_sharded(sh, Ag, ld, false, XF0, XF1, RF, V, c, eps_hist, &o, oz);
   fill(result, o);
   for (auto& e : sh.ev) cudaEventDestroy(e);
   cudaEventDestroy(sh.ready);
@@ -590,8 +878,14 @@ int nnb_nn_chain_sharded_emulated_d(const double* A, int64_t n, int32_t world, c
   } else {
     NNB_TRY(x0_build(Af, ld, n, cfg->x0_kind, cfg->x0_scale, XF0, ld, sh.s));
   }
+  OzSh ozs;
+  OzSh* oz = nullptr;
+  if (use_ozaki(n)) {
+    NNB_TRY(oz_init(sh, ozs));
+    oz = &ozs;
+  }
   ChainOut o;
-  const int st = run_sharded(sh, Af, ld, true, XF0, XF1, RF, V, c, eps_hist, &o);
+  const int st = run_sharded(sh, Af, ld, true, XF0, XF1, RF, V, c, eps_hist, &o, oz);
   fill(result, o);
   if (st != 0 && st != NNB_ERR_DIVERGENCE && st != NNB_ERR_DOMAIN) return st;
   NNB_CUDA(cudaMemcpy2DAsync(X_out, n * 8, o.x_index ? XF1 : XF0, ld * 8, n * 8, n,

@@ -12,7 +12,7 @@ from paper_2212_02406_b200 import workloads as W  # noqa: E402
 
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
 def test_emulated_sharded_matches_single_gpu_and_oracle(port, world):
-    n = 1000  # ragged: 125 8-row units over 3 or 8 ranks
+    n = 1000  # ragged: 63 16-row units over 3 or 8 ranks
     a = W.gram_shifted(n, seed=3, shift=1.0)
     x1, r1 = nnb.nn_chain(a, None, p=2, max_iters=8)
     xs, rs = nnb.nn_chain_sharded_emulated(a, world, None, p=2, max_iters=8)
@@ -167,3 +167,66 @@ def test_c4_emulated_sharded_matches_single_gpu_n8192(world):
     e1 = np.array([e for _, e in r1.history])
     es = np.array([e for _, e in rs.history])
     assert np.allclose(es, e1, rtol=1e-10, atol=1e-15)
+
+
+def _np(x):
+    import torch
+
+    return torch.as_tensor(x).cpu().numpy() if not isinstance(x, np.ndarray) else x
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_emulated_sharded_int8_emulation_bit_identical(world):
+    """The sharded int8-emulated products (column statistics gathered and combined in rank
+    order, residue blocks all-gathered, G block GEMMs accumulated mod m_l, one
+    reconstruction) give the single-GPU emulated chain's X bit for bit (N=4096, the FAST
+    mode's int8 path; ragged blocks at world 3)."""
+    import torch
+
+    n = 4096
+    g = torch.Generator(device="cuda").manual_seed(4096)
+    b = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
+    a = torch.addmm(torch.eye(n, dtype=torch.float64, device="cuda"), b, b.T, alpha=1.0 / n)
+    del b
+    x1, r1 = nnb.nn_chain(a, None, p=2, max_iters=3)
+    xs, rs = nnb.nn_chain_sharded_emulated(a, world, None, p=2, max_iters=3)
+    assert rs.iters == r1.iters == 3 and rs.products == r1.products
+    x1, xs = _np(x1), _np(xs)
+    assert np.array_equal(xs, x1), rel_frob(xs, x1)
+    e1 = np.array([e for _, e in r1.history])
+    es = np.array([e for _, e in rs.history])
+    assert np.allclose(es, e1, rtol=1e-12, atol=1e-15)
+
+
+@pytest.mark.parametrize("world", [3, 8])
+def test_emulated_sharded_forced_int8_ragged(port, world):
+    """NNB_ARITH_OZAKI at N=1000 (63 16-row units over 3 or 8 ranks: blocks of 336/328 and
+    128/104 rows, partial 128-row tiles, K blocks that are not multiples of the 128-byte
+    k-tile): bit-identical to the single-GPU emulated chain, and the oracle to 1e-10."""
+    n = 1000
+    a = W.gram_shifted(n, seed=3, shift=1.0)
+    with nnb.ozaki_arithmetic():
+        x1, r1 = nnb.nn_chain(a, None, p=3, max_iters=5)
+        xs, rs = nnb.nn_chain_sharded_emulated(a, world, None, p=3, max_iters=5)
+    assert np.array_equal(_np(xs), _np(x1)), rel_frob(_np(xs), _np(x1))
+    if world == 3:
+        xr, _, _ = port.chain(a, W.x0_transpose_norm(a), 3, 5)
+        assert rel_frob(_np(xs), xr.real) < 1e-10
+
+
+def test_nccl_world1_int8_emulation_matches_single_gpu():
+    import torch
+
+    n = 4096
+    g = torch.Generator(device="cuda").manual_seed(7)
+    b = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
+    a = torch.addmm(torch.eye(n, dtype=torch.float64, device="cuda"), b, b.T, alpha=1.0 / n)
+    del b
+    comm = nnb.Comm(1, 0, nnb.Comm.unique_id())
+    try:
+        xs, rs = nnb.nn_chain_sharded(comm, a, n, None, p=2, max_iters=3)
+    finally:
+        comm.close()
+    x1, r1 = nnb.nn_chain(a, None, p=2, max_iters=3)
+    assert np.array_equal(_np(xs), _np(x1))
+    assert np.allclose([e for _, e in rs.history], [e for _, e in r1.history], rtol=1e-12, atol=1e-15)
