@@ -676,13 +676,14 @@ def run_sparse(args, world, rank):
     for _ in range(args.warmup):
         x, _ = solve()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    steps = max(args.steps, 5)
+    steps = max(args.steps, 100)  # ≈0.35 s of solves: long enough for the clock samples
     barrier(world)
-    e0.record()
-    for _ in range(steps):
-        x, _ = solve()
-    e1.record()
-    torch.cuda.synchronize()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        e0.record()
+        for _ in range(steps):
+            x, _ = solve()
+        e1.record()
+        torch.cuda.synchronize()
     ms = max_over_ranks(world, e0.elapsed_time(e1)) / steps
     planned_ms = None
     if sharded:
@@ -734,6 +735,16 @@ def run_sparse(args, world, rank):
     alg = 63 * sparse_bytes(n, col.size, 12)  # SURVEY §8(d) algorithmic bytes per solve: the work unit
     moved = 63 * (mat + 2 * n * 8)  # bytes of the consumed format (operator + t in + t out): the roofline
     gbs, moved_gbs = alg / (ms * 1e-3) / 1e9, moved / (ms * 1e-3) / 1e9
+    if fname == "row-dictionary-stencil-tb":
+        # temporal blocking: t crosses HBM once per pass of up to 8 applications (plus halos),
+        # so the bytes moved per application are below one read + one write of t
+        per_launch = (f"{moved / 63:.0f} bytes moved per application, averaged over the solve's 10 passes "
+                      "(t in + t out once per pass of up to 8 applications, 1-byte row codes; whole solve timed "
+                      "incl. the per-solve format pass); the 8-step pass is issue-bound "
+                      "(profiles/r02_ncu_stencil_tb.txt), so this fraction is not its limit")
+    else:
+        per_launch = (f"{mat:.0f} operator bytes + 2N*8 per application (x63, whole solve timed "
+                      f"incl. the per-solve format pass): {fmt}; t in + t out")
     return {"metric": "sparse factorized solve, 4096^2 5-pt Laplacian+I, gamma=63 (GB/s of SURVEY 8(d) algorithmic "
                       "bytes: 12 B per nonzero)", "value": round(gbs, 1),
             "unit": "GB/s", "ms_per_step": round(ms, 3), "format": fname, "format_bytes_per_nnz": fb,
@@ -744,8 +755,8 @@ def run_sparse(args, world, rank):
                          "frac": round(moved_gbs / (HBM_PEAK * world), 4),
                          "traffic": ncu_traffic("sparse_application") if grid == 4096 and not sharded else None,
                          "traffic_unit": "bytes per application (63 per solve)",
-                         "per_launch": f"{mat:.0f} operator bytes + 2N*8 per application (x63, whole solve timed "
-                                       + "incl. the per-solve format pass" + f"): {fmt}; t in + t out"}}
+                         "per_launch": per_launch},
+            "clocks": clk.summary()}
 
 
 def cpu_sparse_sample(grid: int):

@@ -441,6 +441,12 @@ __device__ __forceinline__ int exp_for(double amax) {
   return amax == 0.0 ? 0 : kAlpha - 1 - ilogb(amax);
 }
 
+// x·2^e as scalbn(x, e) computes it (one correctly rounded multiply) while 2^e is a normal
+// double — one DMUL instead of scalbn's range-reduction sequence (6 DMULs) — else scalbn
+__device__ __forceinline__ bool pow2_normal(int e) { return e >= -1022 && e <= 1023; }
+__device__ __forceinline__ double pow2(int e) { return __longlong_as_double(static_cast<long long>(1023 + e) << 52); }
+__device__ __forceinline__ double scale2(double x, int e) { return pow2_normal(e) ? x * pow2(e) : scalbn(x, e); }
+
 // signed residue of the integer-valued double a (|a| <= 2^53) modulo m, in [-128, 127]
 // Exact integer value of a group of digits lo..hi (Horner; the group's weight
 // Π m_lo..m_hi stays below 2^53, so every step is exact).
@@ -448,6 +454,20 @@ template <int L, int LO>
 __device__ __forceinline__ double group(const float* v, double x) {
   if constexpr (L < LO) return x;
   else return group<L - 1, LO>(v, fma(x, static_cast<double>(kMod(L)), static_cast<double>(v[L])));
+}
+// The same group value from digit pairs: v_{I−1} + m_{I−1}·v_I is an exact FP32 integer
+// (|v| <= 1.5·m, so |pair| < 2^17), so each pair costs one FFMA, one float→double
+// conversion and one DFMA instead of two of each.
+template <int I, int LO>
+__device__ __forceinline__ double group_pairs(const float* v, double x) {
+  if constexpr (I < LO) {
+    return x;
+  } else if constexpr (I - 1 >= LO) {
+    const float pr = fmaf(v[I], static_cast<float>(kMod(I - 1)), v[I - 1]);
+    return group_pairs<I - 2, LO>(v, fma(x, static_cast<double>(kMod(I - 1)) * kMod(I), static_cast<double>(pr)));
+  } else {
+    return group_pairs<I - 1, LO>(v, fma(x, static_cast<double>(kMod(I)), static_cast<double>(v[I])));
+  }
 }
 constexpr double weight(int lo, int hi) {  // Π_{lo<=l<=hi} m_l
   double w = 1.0;
@@ -463,9 +483,10 @@ template <int S>
 __device__ __forceinline__ double value_of(const float* v, float top) {
   static_assert(S >= 13 && S <= 18, "three groups of at most 6 digits");
   constexpr double W = weight(0, 5), W2 = weight(6, 11);
-  const double g0 = group<5, 0>(v, 0.0);
-  const double g1 = group<11, 6>(v, 0.0);
-  const double g2 = group<S - 2, 12>(v, static_cast<double>(top));  // top digit already signed
+  (void)top;  // the top digit (already signed) is v[S − 1]
+  const double g0 = group_pairs<5, 0>(v, 0.0);
+  const double g1 = group_pairs<11, 6>(v, 0.0);
+  const double g2 = group_pairs<S - 1, 12>(v, 0.0);
   // inner = g2·W2 + g1 as a double-double (hi, lo)
   const double p = g2 * W2;
   const double pe = fma(g2, W2, -p);
@@ -560,7 +581,7 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int64_t c = c0 + j;
-      a[j] = (c < k && !bad) ? rint(scalbn(xr[c], e)) : 0.0;
+      a[j] = (c < k && !bad) ? rint(scale2(xr[c], e)) : 0.0;
     }
     for (int l = 0; l < s; ++l) {
       const double m = cst.md[l], inv = cst.inv_md[l];
@@ -726,7 +747,7 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __rest
   if (k0 + kc >= kp) return;
   double a[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) a[j] = bad ? 0.0 : rint(scalbn(tile[kc + j][nn], e));
+  for (int j = 0; j < 16; ++j) a[j] = bad ? 0.0 : rint(scale2(tile[kc + j][nn], e));
   const int s = cst.s;
   for (int l = 0; l < s; ++l) {
     const double m = cst.md[l], inv = cst.inv_md[l];
@@ -794,7 +815,7 @@ __global__ void __launch_bounds__(256) oz_recon_kernel(const uint8_t* __restrict
         const int e = (cc < N) ? eb[cc] : 0;
         double cv;
         if (era == kBadExp || e == kBadExp) cv = __longlong_as_double(0x7ff8000000000000LL);
-        else cv = scalbn(x, -(era + e));
+        else cv = scale2(x, -(era + e));
         double o = ep.alpha * cv;
         if (ep.D && cc < N) o = fma(ep.beta, ep.D[(int64_t)row * ep.ldd + cc], o);
         if ((int64_t)row + ep.diag_offset == cc) o += ep.gamma;

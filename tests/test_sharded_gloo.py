@@ -8,7 +8,11 @@ for NCCL and numpy for the local DMMA GEMMs:
     then in ring order (K split by the ranks' row blocks),
   * eps from the per-rank Σ‖R_g‖² all-gathered and summed in rank order.
 Checked against the single-process oracle chain and for bit-identical eps on
-every rank (identical stop decisions)."""
+every rank (identical stop decisions).  The int8-emulated products of the same
+file (column statistics gathered and combined in rank order, residue blocks on
+the ring, K-block products accumulated mod m) are restated with integer numpy
+and checked against the whole product's residues; the sparse halo schedule is
+checked bit-exact against the reference."""
 import os
 import socket
 
@@ -209,3 +213,113 @@ def test_sparse_halo_schedule_gloo_world2(port):
     rp, col, val = W.laplacian_5pt(grid)
     xr, _ = port.sparse_factorized(rp, col, val, W.rhs(grid * grid, seed=9), gamma, theta)
     assert np.array_equal(x, xr.real)  # bit-identical across the partition
+
+
+# ---------------------------------------------------------------- int8-emulated products over gloo
+_MODULI = (256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199)
+
+
+def _exp_for(amax):
+    """2^e·amax in [2^52, 2^53) (ozaki.cu exp_for)."""
+    return 0 if amax == 0.0 else 52 - (np.frexp(amax)[1] - 1)
+
+
+def _residues(ints, s):
+    """Signed residues in [-128, 127] of exact integers (int64 array) for the first s moduli."""
+    out = []
+    for m in _MODULI[:s]:
+        r = np.mod(ints, m)
+        r = np.where(r > 127, r - m, r)
+        out.append(r.astype(np.int64))
+    return out
+
+
+def _oz_worker(rank, world, port, n, s, out_q):
+    """csrc/sharded.cu's int8-emulated product C_g = L_g·F with F row-sharded, restated with
+    gloo for NCCL and numpy integers for the int8 GEMMs:
+      * per-column [max|x|, Σ|x|, Σx²] of the rank's rows, all-gathered, combined in rank order;
+      * the rank's block of F scaled by the global column exponents and split into residues;
+      * a ring all-gather of the residue blocks (same step order as oz_ring);
+      * G K-block products accumulated mod m, own block first then ring order."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2212_02406_b200 as nnb
+
+    parts = [nnb.partition_rows(n, world, g) for g in range(world)]
+    row0 = [r0 for r0, _ in parts]
+    rows = [r for _, r in parts]
+    rng = np.random.default_rng(11)
+    L = rng.standard_normal((n, n)) * np.exp(rng.uniform(-3, 3, (n, 1)))
+    F = rng.standard_normal((n, n)) * np.exp(rng.uniform(-3, 3, (1, n)))
+    me = rank
+    fg = F[row0[me]:row0[me] + rows[me]]
+    # 1. column statistics of the own rows, gathered and combined in rank order
+    rec = torch.from_numpy(np.concatenate([np.abs(fg).max(axis=0, initial=0.0), np.abs(fg).sum(axis=0),
+                                           (fg * fg).sum(axis=0)]))
+    recs = [torch.zeros(3 * n, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(recs, rec)
+    colmax = np.zeros(n)
+    for g in range(world):
+        colmax = np.maximum(colmax, recs[g][:n].numpy())
+    eb = np.array([_exp_for(v) for v in colmax])
+    # 2. own block scaled and split
+    fb = np.rint(np.ldexp(fg, eb[None, :])).astype(np.int64)
+    blocks = {me: _residues(fb, s)}
+    # 3. ring of residue blocks
+    for q in range(1, world):
+        send_blk, recv_blk = (me - q + 1) % world, (me - q) % world
+        sbuf = torch.from_numpy(np.stack(blocks[send_blk]).astype(np.int8))
+        rbuf = torch.empty((s, rows[recv_blk], n), dtype=torch.int8)
+        reqs = [dist.isend(sbuf, (me + 1) % world), dist.irecv(rbuf, (me - 1) % world)]
+        for r in reqs:
+            r.wait()
+        blocks[recv_blk] = [rbuf[l].numpy().astype(np.int64) for l in range(s)]
+    # 4. the rank's rows of L, its row exponents and residues; K-block products mod m
+    lg = L[row0[me]:row0[me] + rows[me]]
+    ea = np.array([_exp_for(v) for v in np.abs(lg).max(axis=1, initial=0.0)])
+    la = _residues(np.rint(np.ldexp(lg, ea[:, None])).astype(np.int64), s)
+    acc = [None] * s
+    for q in range(world):
+        j = (me - q) % world
+        for l, m in enumerate(_MODULI[:s]):
+            part = np.mod(la[l][:, row0[j]:row0[j] + rows[j]] @ blocks[j][l], m)
+            acc[l] = part if acc[l] is None else np.mod(acc[l] + part, m)
+    out_q.put((rank, row0[me], eb, ea, np.stack(acc)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_int8_emulated_product_schedule_gloo(world):
+    """The sharded residue schedule reproduces the whole product's residues exactly: the
+    global column exponents and, per modulus, (A'·B') mod m of the unsharded scaled operands."""
+    n, s = 72, 4  # 72 rows: 16-row units give ragged blocks (48/24 at world 2, 32/32/8 at world 3)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    portn = _free_port()
+    procs = [ctx.Process(target=_oz_worker, args=(r, world, portn, n, s, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted((q.get(timeout=120) for _ in range(world)), key=lambda r: r[0])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    rng = np.random.default_rng(11)
+    L = rng.standard_normal((n, n)) * np.exp(rng.uniform(-3, 3, (n, 1)))
+    F = rng.standard_normal((n, n)) * np.exp(rng.uniform(-3, 3, (1, n)))
+    eb = np.array([_exp_for(v) for v in np.abs(F).max(axis=0)])
+    ea = np.array([_exp_for(v) for v in np.abs(L).max(axis=1)])
+    A = np.rint(np.ldexp(L, ea[:, None])).astype(np.int64)
+    B = np.rint(np.ldexp(F, eb[None, :])).astype(np.int64)
+    la, fb = _residues(A, s), _residues(B, s)
+    for rank, r0, eb_r, ea_r, acc in res:
+        assert np.array_equal(eb_r, eb)  # every rank: the global column exponents
+        rows = acc.shape[1]
+        assert np.array_equal(ea_r, ea[r0:r0 + rows])
+        for l, m in enumerate(_MODULI[:s]):
+            whole = np.mod(la[l][r0:r0 + rows] @ fb[l], m)
+            assert np.array_equal(acc[l], whole)
+    # and the residues are those of the exact integer product A'·B' (CRT-consistent)
+    prod = A[:8].astype(object) @ B.astype(object)
+    for l, m in enumerate(_MODULI[:s]):
+        assert np.array_equal(np.mod(prod, m).astype(np.int64), res[0][4][l][:8])
