@@ -153,7 +153,7 @@ void fill_result(nnb_chain_result* r, const ChainOut& o) {
 // an event per chunk, so the first residual product starts once X0 and A's
 // first chunk have landed rather than after all 2·8·n² bytes.  The final X
 // leaves per chunk of the last Horner product (ChainIo).  NNB_STREAM_CHUNKS
-// sets the chunk count (default 8, 1..64).
+// sets the chunk count (default 16, 1..64: 8 and 32 measured 5-10 % slower e2e at N=32768).
 constexpr int64_t kStreamMinN = 8192;
 
 struct CopyLane {
@@ -181,7 +181,7 @@ int chain_d_streamed(const double* A, int64_t n, const double* X0, const nnb_cha
                      cudaStream_t s) {
   static const int chunks = [] {
     const char* e = debug_env("NNB_STREAM_CHUNKS");
-    return std::min(64, std::max(1, e ? std::atoi(e) : 8));
+    return std::min(64, std::max(1, e ? std::atoi(e) : 16));
   }();
   const bool host_a = !is_device_ptr(A), host_out = X_out && !is_device_ptr(X_out);
   const bool x0_given = cfg->x0_kind == NNB_X0_GIVEN;

@@ -142,6 +142,20 @@ int product(Ctx& c, const Plane& A, const Plane& B, double alpha, const Plane* D
   return 0;
 }
 
+// The pieces of a product that the int8 emulation forms whole run on the emulation too,
+// whatever their own shape (ozaki_pays would send a 512-row chunk to DMMA): every element
+// then comes from the same arithmetic as in the one-launch product.
+struct ArithScope {
+  int prev;
+  bool on;
+  ArithScope(bool enable, int mode) : prev(arith()), on(enable) {
+    if (on) set_arith(mode);
+  }
+  ~ArithScope() {
+    if (on) set_arith(prev);
+  }
+};
+
 // A real product in io.chunks row chunks (see ChainIo): chunk q first waits for
 // io.a_ready[q] (wait_in), and its rows are copied to io.host_out once written
 // (stream_out).  Σ C² is reduced per chunk and combined in chunk order.
@@ -159,6 +173,7 @@ int product_chunked(Ctx& c, const Plane& A, const Plane& B, double alpha, const 
       if (on) ozaki_force_moduli(0);
     }
   } force{oz};
+  ArithScope emul(oz, 2);
   if (oz) {
     GemmOp whole;
     whole.M = whole.N = whole.K = c.n;
@@ -226,6 +241,7 @@ int product_chunked(Ctx& c, const Plane& A, const Plane& B, double alpha, const 
 int product_2d(Ctx& c, const Plane& A, const Plane& B, double alpha, double gamma, const Plane& C, double* eps_out,
                int* nf_out, ChainIo& io, double* chunk_ss, int* chunk_nf) {
   const int q = io.chunks;
+  ArithScope emul(true, 2);  // the whole product is an emulated one (capi.cu rows_stream)
   // every chunk of both operands stays pinned for the product (each is split once)
   std::vector<OzPinScope> pins;
   pins.reserve(2 * q);
