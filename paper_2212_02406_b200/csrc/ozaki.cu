@@ -38,6 +38,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstdint>
@@ -57,6 +58,7 @@ constexpr int kModuli[kMaxMod] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 2
 constexpr int kAlpha = 53;                  // bits kept per row (column) of an operand
 constexpr int kBadExp = INT_MIN / 4;        // exponent marking a row/column with a non-finite entry
 constexpr int64_t kMaxK = 131071;           // 128·128·k < 2^31: exact int32 accumulation
+constexpr int kColRows = 64;                // rows per block of the column-statistics passes
 
 // Garner constants for the first s moduli (host-computed, passed by value).
 struct OzConst {
@@ -296,10 +298,43 @@ __device__ __forceinline__ TileCoord tile_of(int t, int tiles_m, int tiles_n, in
   return c;
 }
 
+// cluster helpers (kC = 2: B multicast across a CTA pair)
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// the box lands at the same shared-memory offset in every CTA of `mask`; each CTA's mbarrier
+// at `bar`'s offset receives complete_tx for the bytes delivered to it
+__device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                               int32_t c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+// arrive on `bar` in every CTA of `mask` once this thread's MMAs so far have completed
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 // Persistent: CTA b takes tiles b, b + grid, ... of the (modulus, tile-row, tile-col) space;
 // out[l][row][col] = (Σ_k a_l[row][k]·b_l[col][k]) mod m_l.  a_l's rows live at l·M + row
 // of tma_a, b_l's at l·N + col of tma_b.  The TMA ring runs across tile boundaries and the
 // two TMEM accumulators let the epilogue of tile i overlap the MMAs of tile i+1.
+// kC = 2: CTA pairs (clusters of 2) take vertically adjacent tiles with the same B tile;
+// each CTA loads half of that B tile and multicasts it to both (tma_b's box is then
+// kBN/2 rows), so B crosses L2→SM once per pair; a stage is refilled only after both
+// CTAs' MMAs released it (empty barriers count kC commits, multicast by each MMA issuer).
+template <int kC>
 __global__ void __launch_bounds__(192, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, int M, int N,
                    int K, int64_t ldr, uint8_t* __restrict__ out, const OzConst cst, int tiles_m, int tiles_n,
@@ -313,12 +348,17 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = (K + kBK - 1) / kBK;
-  const int total = tiles_m * tiles_n * cst.s;
+  const uint32_t crank = kC > 1 ? cluster_ctarank() : 0u;
+  const int unit = static_cast<int>(blockIdx.x) / kC, nunits = static_cast<int>(gridDim.x) / kC;
+  const int tiles_mu = (tiles_m + kC - 1) / kC;  // tile-rows in units of kC
+  const int group_u = max(1, group_m / kC);
+  const int total = tiles_mu * tiles_n * cst.s;
+  constexpr uint16_t kMask = static_cast<uint16_t>((1u << kC) - 1u);
 
   if (threadIdx.x == 0) {
     for (int st = 0; st < kStages; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], 1);
+      mbar_init(&empty[st], kC);
     }
     for (int b = 0; b < kAccBufs; ++b) {
       mbar_init(&tfull[b], 1);
@@ -330,6 +370,7 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if constexpr (kC > 1) cluster_sync_all();  // the peer's barriers exist before any multicast
   const uint32_t tbase = *tmem_slot;
 
   if (warp == 0) {
@@ -337,23 +378,35 @@ __global__ void __launch_bounds__(192, 1)
       tma_prefetch_desc(&tma_a);
       tma_prefetch_desc(&tma_b);
       int it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const TileCoord tc = tile_of(t, tiles_m, tiles_n, group_m);
-        const int arow = tc.l * M + tc.mt * kBM, brow = tc.l * N + tc.nt * kBN;
+      for (int t = unit; t < total; t += nunits) {
+        const TileCoord tc = tile_of(t, tiles_mu, tiles_n, group_u);
+        const int mt = tc.mt * kC + static_cast<int>(crank);
+        const int arow = tc.l * M + mt * kBM, brow = tc.l * N + tc.nt * kBN;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int st = it % kStages;
           if (it >= kStages) mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
           uint8_t* sa = smem + st * kStageBytes;
           mbar_arrive_expect_tx(&full[st], kStageBytes);
           tma_load_2d(sa, &tma_a, &full[st], a_k0 + kb * kBK, arow);
-          tma_load_2d(sa + kABytes, &tma_b, &full[st], kb * kBK, brow);
+          if constexpr (kC == 1) {
+            tma_load_2d(sa + kABytes, &tma_b, &full[st], kb * kBK, brow);
+          } else {
+            tma_load_2d_mc(sa + kABytes + crank * (kBBytes / kC), &tma_b, &full[st], kb * kBK,
+                           brow + static_cast<int>(crank) * (kBN / kC), kMask);
+          }
         }
+      }
+      if constexpr (kC > 1) {
+        // drain: every stage's last release (both CTAs' commits) has arrived before teardown,
+        // so no commit from the peer targets this CTA's barriers after it exits
+        for (int j = 0; j < kStages; ++j, ++it)
+          if (it >= kStages) mbar_wait(&empty[it % kStages], ((it / kStages) & 1) ^ 1);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       int it = 0, n_t = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++n_t) {
+      for (int t = unit; t < total; t += nunits, ++n_t) {
         const int acc = n_t & 1;
         if (n_t >= kAccBufs) mbar_wait(&tempty[acc], ((n_t >> 1) & 1) ^ 1);  // epilogue drained it
         tc_fence_after();
@@ -366,7 +419,8 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int k = 0; k < kBK / 32; ++k)
             mma_i8(tacc, sw128_desc(a_addr + 32 * k), sw128_desc(b_addr + 32 * k), kIdesc, (kb | k) != 0);
-          mma_commit(&empty[st]);  // the stage is free once these MMAs have read it
+          if constexpr (kC == 1) mma_commit(&empty[st]);  // the stage is free once these MMAs have read it
+          else mma_commit_mc(&empty[st], kMask);           // ... in both CTAs (the peer refills it too)
         }
         mma_commit(&tfull[acc]);  // the accumulator is complete
       }
@@ -374,12 +428,13 @@ __global__ void __launch_bounds__(192, 1)
   } else {  // epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
     const int q = warp & 3;
     int n_t = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++n_t) {
-      const TileCoord tc = tile_of(t, tiles_m, tiles_n, group_m);
+    for (int t = unit; t < total; t += nunits, ++n_t) {
+      const TileCoord tc = tile_of(t, tiles_mu, tiles_n, group_u);
+      const int mt = tc.mt * kC + static_cast<int>(crank);
       const int acc = n_t & 1;
       mbar_wait(&tfull[acc], (n_t >> 1) & 1);
       tc_fence_after();
-      const int row = tc.mt * kBM + 32 * q + lane;
+      const int row = mt * kBM + 32 * q + lane;
       const unsigned m = static_cast<unsigned>(cst.mi[tc.l]);
       const unsigned magic = cst.magic[tc.l], off = cst.offset[tc.l];
       uint8_t* orow = out + ((int64_t)tc.l * M + row) * ldr;
@@ -429,6 +484,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kC > 1) cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tbase, kBN * kAccBufs);
@@ -514,6 +570,86 @@ __device__ __forceinline__ int resid(double a, double m, double inv_m) {
   return ri;
 }
 
+// ---- residues in packed FP32, two entries per instruction (FFMA2) ------------------
+// An entry a' (integer-valued, |a'| < 2^53) becomes five 12-bit limbs a' = Σ_i L_i·2^(12i)
+// (L_0..3 in [0, 4096), L_4 = a' >> 48 signed), each an exact float built from its bits.
+// For modulus m: t = Σ_i L_i·(2^(12i) mod m) is an exact FP32 integer (|t| < 2^22.1), and
+// r = t − m·rint(t·(1/m)) is exact; the float quotient can be one off near a half-integer,
+// so |r| <= m/2 + 1, inside [−128, 127] for every modulus below 254 — 256 and 255 fold
+// r = 128 to r − m.  r + 1.5·2^23 carries r's two's-complement byte in its low bits.  The
+// moduli and the limb weights are template constants (immediates), so a residue costs
+// about 4 FFMA2 + 4 more FP32 ops per two entries, against ~17 instructions per entry
+// for the FP64 form above (the splits were issue-bound on those).
+__device__ __forceinline__ float limb_f(uint32_t v) { return __uint_as_float(0x4B000000u | v) - 8388608.0f; }
+__device__ __forceinline__ void limbs_of(double a, float (&L)[5]) {
+  const long long ai = __double2ll_rn(a);
+  const uint32_t lo = static_cast<uint32_t>(ai), hi = static_cast<uint32_t>(static_cast<unsigned long long>(ai) >> 32);
+  L[0] = limb_f(lo & 0xFFFu);
+  L[1] = limb_f((lo >> 12) & 0xFFFu);
+  L[2] = limb_f(__funnelshift_r(lo, hi, 24) & 0xFFFu);
+  L[3] = limb_f((hi >> 4) & 0xFFFu);
+  L[4] = __uint_as_float(0x4B000000u | static_cast<uint32_t>((static_cast<int>(hi) >> 16) + 0x400000)) - 12582912.0f;
+}
+constexpr int pow2_mod(int e, int m) {
+  long long r = 1;
+  for (int i = 0; i < e; ++i) r = (r * 2) % m;
+  return static_cast<int>(r);
+}
+// packed residues of two entries for modulus L: the bytes sit in bits 0-7 of each half
+template <int L>
+__device__ __forceinline__ unsigned long long resid2(const unsigned long long (&lp)[5]) {
+  constexpr int m = kMod(L);
+  constexpr float c1 = pow2_mod(12, m), c2 = pow2_mod(24, m), c3 = pow2_mod(36, m), c4 = pow2_mod(48, m);
+  unsigned long long t = fma2(lp[1], bc2(c1), lp[0]);
+  t = fma2(lp[2], bc2(c2), t);
+  t = fma2(lp[3], bc2(c3), t);
+  t = fma2(lp[4], bc2(c4), t);
+  const unsigned long long q = add2(fma2(t, bc2(1.0f / m), bc2(12582912.0f)), bc2(-12582912.0f));
+  unsigned long long r = fma2(q, bc2(-static_cast<float>(m)), t);
+  if constexpr (m >= 254) {
+    float r0, r1;
+    upk2(r, r0, r1);
+    r0 = r0 > 127.5f ? r0 - m : r0;
+    r1 = r1 > 127.5f ? r1 - m : r1;
+    r = pk2(r0, r1);
+  }
+  return add2(r, bc2(12582912.0f));
+}
+// 4 bytes (byte 0 of each 32-bit half of two packed pairs)
+__device__ __forceinline__ uint32_t bytes4(unsigned long long p, unsigned long long q) {
+  const uint32_t w0 = __byte_perm(static_cast<uint32_t>(p), static_cast<uint32_t>(p >> 32), 0x0040);
+  const uint32_t w1 = __byte_perm(static_cast<uint32_t>(q), static_cast<uint32_t>(q >> 32), 0x0040);
+  return __byte_perm(w0, w1, 0x5410);
+}
+// residues of P packed pairs (2P consecutive entries) for moduli L..S−1, plane stride `ps`
+template <int L, int S, int P>
+__device__ __forceinline__ void store_residues(const unsigned long long (&lp)[P][5], int8_t* out, int64_t ps) {
+  if constexpr (L < S) {
+    unsigned long long b[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) b[p] = resid2<L>(lp[p]);
+    if constexpr (P == 4) {
+      *reinterpret_cast<uint2*>(out + L * ps) = make_uint2(bytes4(b[0], b[1]), bytes4(b[2], b[3]));
+    } else {
+      static_assert(P == 8, "8 or 16 entries per thread");
+      *reinterpret_cast<uint4*>(out + L * ps) =
+          make_uint4(bytes4(b[0], b[1]), bytes4(b[2], b[3]), bytes4(b[4], b[5]), bytes4(b[6], b[7]));
+    }
+    store_residues<L + 1, S, P>(lp, out, ps);
+  }
+}
+template <int P>
+__device__ __forceinline__ void pack_limbs(const double (&a)[2 * P], unsigned long long (&lp)[P][5]) {
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    float x[5], y[5];
+    limbs_of(a[2 * p], x);
+    limbs_of(a[2 * p + 1], y);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) lp[p][i] = pk2(x[i], y[i]);
+  }
+}
+
 // Left operand, pass 1: one 256-thread block per row: the row's exponent (exps[row])
 // and its L1/max ratio, folded into *ratio (float bits, atomic max): Σ_k |a'_ik| <=
 // ratio·2^53 bounds the integer product (the moduli count follows from it).
@@ -567,15 +703,15 @@ __global__ void __launch_bounds__(256) oz_rowstat_kernel(const double* __restric
   }
 }
 
-// Left operand, pass 2: out[l][row][kp] int8 residues for s moduli (zero-padded from k).
+// Left operand, pass 2: out[l][row][kp] int8 residues for S moduli (zero-padded from k).
+template <int S>
 __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __restrict__ X, int64_t ld, int rows,
                                                             int k, int64_t kp, int8_t* __restrict__ out,
-                                                            const int* __restrict__ exps, const OzConst cst) {
+                                                            const int* __restrict__ exps) {
   const int row = blockIdx.x;
   const double* xr = X + (int64_t)row * ld;
   const int e = exps[row];
   const bool bad = e == kBadExp;
-  const int s = cst.s;
   for (int64_t c0 = threadIdx.x * 8; c0 < kp; c0 += 256 * 8) {
     double a[8];
 #pragma unroll
@@ -583,15 +719,9 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const double* __rest
       const int64_t c = c0 + j;
       a[j] = (c < k && !bad) ? rint(scale2(xr[c], e)) : 0.0;
     }
-    for (int l = 0; l < s; ++l) {
-      const double m = cst.md[l], inv = cst.inv_md[l];
-      uint32_t lo = 0, hi = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) lo |= (static_cast<uint32_t>(resid(a[j], m, inv)) & 0xffu) << (8 * j);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) hi |= (static_cast<uint32_t>(resid(a[4 + j], m, inv)) & 0xffu) << (8 * j);
-      *reinterpret_cast<uint2*>(out + ((int64_t)l * rows + row) * kp + c0) = make_uint2(lo, hi);
-    }
+    unsigned long long lp[4][5];
+    pack_limbs<4>(a, lp);
+    store_residues<0, S, 4>(lp, out + (int64_t)row * kp + c0, (int64_t)rows * kp);
   }
 }
 
@@ -602,7 +732,7 @@ __global__ void __launch_bounds__(256) oz_colmax_kernel(const double* __restrict
                                                         int* __restrict__ colbad) {
   const int c = blockIdx.x * 256 + threadIdx.x;
   if (c >= n) return;
-  const int r0 = blockIdx.y * 256, r1 = min(k, r0 + 256);
+  const int r0 = blockIdx.y * kColRows, r1 = min(k, r0 + kColRows);
   double mx = 0.0, sum = 0.0, sq = 0.0;
   int bad = 0;
   for (int r = r0; r < r1; ++r) {
@@ -613,7 +743,7 @@ __global__ void __launch_bounds__(256) oz_colmax_kernel(const double* __restrict
     sq = fma(v, v, sq);
   }
   if (mx > 0.0) atomicMax(colmax + c, static_cast<unsigned long long>(__double_as_longlong(mx)));
-  // per-256-row partial sums, added in row-block order by oz_colratio_kernel: the bound,
+  // per-kColRows-row partial sums, added in row-block order by oz_colratio_kernel: the bound,
   // and so the moduli count, is the same on every run (no floating-point atomics)
   colsum[(int64_t)blockIdx.y * n + c] = sum;
   colsq[(int64_t)blockIdx.y * n + c] = sq;
@@ -654,13 +784,13 @@ __global__ void __launch_bounds__(256) oz_colratio_kernel(const unsigned long lo
 }
 
 // Row-sharded right operand (sharded.cu): per-column statistics of one rank's row block,
-// combined over the ranks in rank order.  part[y][3][n] per 256-row block y: max|x| (+inf
+// combined over the ranks in rank order.  part[y][3][n] per kColRows-row block y: max|x| (+inf
 // when the block holds a non-finite entry), Σ|x|, Σx².
 __global__ void __launch_bounds__(256) oz_colpart_kernel(const double* __restrict__ B, int64_t ld, int k, int n,
                                                          double* __restrict__ part) {
   const int c = blockIdx.x * 256 + threadIdx.x;
   if (c >= n) return;
-  const int r0 = blockIdx.y * 256, r1 = min(k, r0 + 256);
+  const int r0 = blockIdx.y * kColRows, r1 = min(k, r0 + kColRows);
   double mx = 0.0, sum = 0.0, sq = 0.0;
   int bad = 0;
   for (int r = r0; r < r1; ++r) {
@@ -675,7 +805,7 @@ __global__ void __launch_bounds__(256) oz_colpart_kernel(const double* __restric
   o[n] = sum;
   o[2 * (int64_t)n] = sq;
 }
-// out[3][n] = the rank's column statistics: the 256-row block partials in block order
+// out[3][n] = the rank's column statistics: the kColRows-row block partials in block order
 // (for one rank: the same sums oz_colratio_kernel forms for the whole operand)
 __global__ void __launch_bounds__(256) oz_colpart_sum_kernel(const double* __restrict__ part, int kblocks, int n,
                                                              double* __restrict__ out) {
@@ -727,40 +857,81 @@ __global__ void __launch_bounds__(256) oz_colcombine_kernel(const double* __rest
 }
 
 // Right operand, pass 2: 64(k)×64(n) tiles transposed through shared memory into
-// K-major residues out[l][col][kp]; exps[col] written by the first k-tile row.
+// K-major residues out[l][col][kp].  Thread (column nn, 8-entry k segment 8g): the 8
+// threads of a column write its 64 residue bytes per plane contiguously.  The tile's
+// column index is XOR-swizzled by bit 4 of the row (phys = nn ^ 4·((kk >> 4) & 1)), so a
+// warp's reads (4 columns × 8 segments) fall on 16 distinct double banks — the
+// 2-wavefront minimum (unswizzled, segments 16 rows apart share banks: 4-way conflicts).
+template <int S>
 __global__ void __launch_bounds__(256) oz_split_cols_kernel(const double* __restrict__ B, int64_t ld, int k, int n,
                                                             int64_t kp, int8_t* __restrict__ out,
-                                                            const int* __restrict__ exps, const OzConst cst) {
+                                                            const int* __restrict__ exps) {
   __shared__ double tile[64][65];
   const int n0 = blockIdx.x * 64, k0 = blockIdx.y * 64;
   for (int i = threadIdx.x; i < 64 * 64; i += 256) {
     const int kk = i >> 6, nn = i & 63;
     const int r = k0 + kk, c = n0 + nn;
-    tile[kk][nn] = (r < k && c < n) ? B[(int64_t)r * ld + c] : 0.0;
+    tile[kk][nn ^ (((kk >> 4) & 1) << 2)] = (r < k && c < n) ? B[(int64_t)r * ld + c] : 0.0;
   }
   __syncthreads();
-  const int nn = threadIdx.x >> 2, kc = (threadIdx.x & 3) * 16;
-  const int col = n0 + nn;
-  if (col >= n) return;
-  const int e = exps[col];
-  const bool bad = e == kBadExp;
+  const int kc = (threadIdx.x & 7) * 8;
   if (k0 + kc >= kp) return;
-  double a[16];
+  const int sw = ((kc >> 4) & 1) << 2;
+#pragma unroll 1
+  for (int half = 0; half < 2; ++half) {
+    const int nn = (threadIdx.x >> 3) + 32 * half;
+    const int col = n0 + nn;
+    if (col >= n) break;
+    const int e = exps[col];
+    const bool bad = e == kBadExp;
+    double a[8];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) a[j] = bad ? 0.0 : rint(scale2(tile[kc + j][nn], e));
-  const int s = cst.s;
-  for (int l = 0; l < s; ++l) {
-    const double m = cst.md[l], inv = cst.inv_md[l];
-    uint32_t w[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t word = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) word |= (static_cast<uint32_t>(resid(a[4 * q + j], m, inv)) & 0xffu) << (8 * j);
-      w[q] = word;
-    }
-    *reinterpret_cast<uint4*>(out + ((int64_t)l * n + col) * kp + k0 + kc) = make_uint4(w[0], w[1], w[2], w[3]);
+    for (int j = 0; j < 8; ++j) a[j] = bad ? 0.0 : rint(scale2(tile[kc + j][nn ^ sw], e));
+    unsigned long long lp[4][5];
+    pack_limbs<4>(a, lp);
+    store_residues<0, S, 4>(lp, out + (int64_t)col * kp + k0 + kc, (int64_t)n * kp);
   }
+}
+
+// launchers for the moduli counts the emulation uses (14..17)
+int split_rows_launch(int s, const double* X, int64_t ld, int rows, int k, int64_t kp, int8_t* out, const int* exps,
+                      cudaStream_t st) {
+  switch (s) {
+#define NNB_OZ_SR(S)                                                                          \
+  case S:                                                                                     \
+    oz_split_rows_kernel<S><<<static_cast<unsigned>(rows), 256, 0, st>>>(X, ld, rows, k, kp, out, exps); \
+    break;
+    NNB_OZ_SR(14)
+    NNB_OZ_SR(15)
+    NNB_OZ_SR(16)
+    NNB_OZ_SR(17)
+#undef NNB_OZ_SR
+    default:
+      return fail(7, "ozaki: unsupported moduli count " + std::to_string(s));
+  }
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+int split_cols_launch(int s, const double* B, int64_t ld, int k, int n, int64_t kp, int8_t* out, const int* exps,
+                      cudaStream_t st) {
+  const dim3 grid((unsigned)((n + 63) / 64), (unsigned)((kp + 63) / 64));
+  switch (s) {
+#define NNB_OZ_SC(S)                                                                  \
+  case S:                                                                             \
+    oz_split_cols_kernel<S><<<grid, 256, 0, st>>>(B, ld, k, n, kp, out, exps);       \
+    break;
+    NNB_OZ_SC(14)
+    NNB_OZ_SC(15)
+    NNB_OZ_SC(16)
+    NNB_OZ_SC(17)
+#undef NNB_OZ_SC
+    default:
+      return fail(7, "ozaki: unsupported moduli count " + std::to_string(s));
+  }
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
 }
 
 // ---------------------------------------------------------------- reconstruction
@@ -962,7 +1133,7 @@ int operand_stats(const double* X, int64_t ld, int64_t rows, int64_t k, bool lef
   } else {
     const int64_t n = rows;
     DevBuf cm;
-    const int64_t kb = (k + 255) / 256;
+    const int64_t kb = (k + kColRows - 1) / kColRows;
     NNB_TRY(cm.alloc((sizeof(unsigned long long) + sizeof(int)) * n + 8 + 2 * sizeof(double) * kb * n, st));
     unsigned long long* colmax = cm.as<unsigned long long>();
     int* colbad = reinterpret_cast<int*>(colmax + n);
@@ -984,22 +1155,50 @@ int operand_residues(const double* X, int64_t ld, bool left, const OzConst& c, O
   NNB_TRY(o.res.alloc((size_t)c.s * o.rows * o.kp, st));
   o.s = c.s;
   Timed tm(1, (double)o.rows * o.k * (8.0 + c.s), st);  // 8 B in, s B out per entry
-  if (left) {
-    oz_split_rows_kernel<<<static_cast<unsigned>(o.rows), 256, 0, st>>>(X, ld, (int)o.rows, (int)o.k, o.kp,
-                                                                          o.res.as<int8_t>(), o.exps.as<int>(), c);
-  } else {
-    oz_split_cols_kernel<<<dim3((unsigned)((o.rows + 63) / 64), (unsigned)((o.kp + 63) / 64)), 256, 0, st>>>(
-        X, ld, (int)o.k, (int)o.rows, o.kp, o.res.as<int8_t>(), o.exps.as<int>(), c);
-  }
-  count_launch();
-  NNB_CUDA(cudaGetLastError());
-  return 0;
+  if (left) return split_rows_launch(c.s, X, ld, (int)o.rows, (int)o.k, o.kp, o.res.as<int8_t>(), o.exps.as<int>(), st);
+  return split_cols_launch(c.s, X, ld, (int)o.k, (int)o.rows, o.kp, o.res.as<int8_t>(), o.exps.as<int>(), st);
 }
 
 // moduli for |C'| <= ratio·2^106 < M/8 (the balanced Garner value is then C' itself)
-__global__ void oz_ratio_out_kernel(const unsigned* __restrict__ rd, unsigned* out) {
+__global__ void oz_ratio_out_kernel(const unsigned* __restrict__ rd, unsigned* out, unsigned seq) {
   if (threadIdx.x < 4) out[threadIdx.x] = rd[threadIdx.x];
   __threadfence_system();
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    *reinterpret_cast<volatile unsigned*>(out + 4) = seq;  // published after the ratios
+    __threadfence_system();
+  }
+}
+
+// The 4 ratio slots of `rd` on the host, the moment the stream reaches them: a one-warp
+// kernel writes them and then a sequence number to mapped host memory, and the host polls
+// that word instead of synchronising the stream (cudaStreamSynchronize returned ~0.14 ms
+// after the GPU got there, an idle gap before every product's split at N=4096);
+// cudaStreamQuery every 16384 polls surfaces any error of the stream.
+int read_ratios_mapped(const unsigned* rd, unsigned out[4], cudaStream_t st) {
+  static thread_local unsigned* host = nullptr;
+  static thread_local unsigned* mapped = nullptr;
+  static thread_local unsigned seq = 0;
+  if (!host) {
+    NNB_CUDA(cudaHostAlloc(&host, sizeof(unsigned) * 8, cudaHostAllocMapped));
+    NNB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mapped), host, 0));
+    host[4] = 0;
+  }
+  ++seq;
+  oz_ratio_out_kernel<<<1, 32, 0, st>>>(rd, mapped, seq);
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  volatile unsigned* flag = host + 4;
+  for (int spins = 0; *flag != seq; ++spins) {
+    if ((spins & 16383) == 16383) {
+      const cudaError_t q = cudaStreamQuery(st);
+      if (q == cudaSuccess) break;  // everything enqueued so far (the ratio kernel too) is done
+      if (q != cudaErrorNotReady) NNB_CUDA(q);
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  for (int i = 0; i < 4; ++i) out[i] = reinterpret_cast<volatile unsigned*>(host)[i];
+  return 0;
 }
 
 int moduli_for_ratio(double ratio) {
@@ -1080,10 +1279,13 @@ int launch_oz_gemm(const int8_t* a_res, int64_t M, int64_t a_kp, int64_t a_k0, c
                    int64_t b_kp, int64_t K, const OzConst& c, uint8_t* out, int64_t ldr, bool accumulate,
                    cudaStream_t st, int reserve_sms = 0) {
   const int s = c.s;
+  // NNB_DEBUG=1 NNB_OZ_CLUSTER=2: B multicast across CTA pairs (oz_gemm_kernel<2>)
+  static const int kc = debug_env("NNB_OZ_CLUSTER") && std::atoi(debug_env("NNB_OZ_CLUSTER")) == 2 ? 2 : 1;
   CUtensorMap ta, tb;
   NNB_TRY(make_tmap_u8(&ta, a_res, (int64_t)s * M, a_kp, a_kp, kBM, kBK));
-  NNB_TRY(make_tmap_u8(&tb, b_res, (int64_t)s * N, b_kp, b_kp, kBN, kBK));
-  NNB_TRY(ensure_smem<oz_gemm_kernel>(kGemmSmem));
+  NNB_TRY(make_tmap_u8(&tb, b_res, (int64_t)s * N, b_kp, b_kp, kBN / kc, kBK));
+  NNB_TRY(ensure_smem<oz_gemm_kernel<1>>(kGemmSmem));
+  NNB_TRY(ensure_smem<oz_gemm_kernel<2>>(kGemmSmem));
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -1091,13 +1293,37 @@ int launch_oz_gemm(const int8_t* a_res, int64_t M, int64_t a_kp, int64_t a_k0, c
     NNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   const int tiles_m = (int)((M + kBM - 1) / kBM), tiles_n = (int)((N + kBN - 1) / kBN);
-  const int64_t total = (int64_t)tiles_m * tiles_n * s;
+  const int64_t total = (int64_t)((tiles_m + kc - 1) / kc) * tiles_n * s;
   if (total > INT32_MAX) return fail(7, "ozaki: too many tiles");
   Timed tm(0, 2.0 * s * (double)M * N * K, st);  // int8 tensor ops
-  const unsigned grid = (unsigned)std::min<int64_t>(total, std::max(1, sms - reserve_sms));
   static const int gm = debug_env("NNB_OZ_GROUP") ? std::atoi(debug_env("NNB_OZ_GROUP")) : kGroupM;
-  oz_gemm_kernel<<<grid, 192, kGemmSmem, st>>>(ta, tb, (int)M, (int)N, (int)K, ldr, out, c, tiles_m, tiles_n, gm,
-                                               (int)a_k0, accumulate ? 1 : 0);
+  if (kc == 1) {
+    const unsigned grid = (unsigned)std::min<int64_t>(total, std::max(1, sms - reserve_sms));
+    oz_gemm_kernel<1><<<grid, 192, kGemmSmem, st>>>(ta, tb, (int)M, (int)N, (int)K, ldr, out, c, tiles_m, tiles_n,
+                                                    gm, (int)a_k0, accumulate ? 1 : 0);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = kGemmSmem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    static int max_clusters = 0;
+    if (!max_clusters) {
+      cfg.gridDim = dim3(2 * 74);
+      NNB_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, oz_gemm_kernel<2>, &cfg));
+      if (max_clusters < 1) return fail(7, "ozaki: no co-resident CTA pairs");
+    }
+    const int64_t units = std::min<int64_t>(total, std::max(1, std::min(max_clusters, (sms - reserve_sms) / 2)));
+    cfg.gridDim = dim3((unsigned)(2 * units));
+    NNB_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<2>, ta, tb, (int)M, (int)N, (int)K, ldr, out, c, tiles_m,
+                                tiles_n, gm, (int)a_k0, accumulate ? 1 : 0));
+  }
   count_launch();
   NNB_CUDA(cudaGetLastError());
   return 0;
@@ -1131,12 +1357,6 @@ int gemm_ozaki_impl(const GemmOp& op, cudaStream_t st, bool plan_only, int* s_ou
   // the ratios come back through mapped host memory written by a one-warp kernel, not
   // a copy: a device-to-host copy would queue behind any large copy on the same engine
   // (the host-buffer nest streams X out during its last product)
-  static thread_local unsigned* ratio_host = nullptr;
-  static thread_local unsigned* ratio_mapped = nullptr;
-  if (!ratio_host) {
-    NNB_CUDA(cudaHostAlloc(&ratio_host, sizeof(unsigned) * 4, cudaHostAllocMapped));
-    NNB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ratio_mapped), ratio_host, 0));
-  }
   DevBuf ratio_dev;  // [L1 A, L1 B, L2 A, L2 B] ratios to the row/column max
   NNB_TRY(ratio_dev.alloc(sizeof(unsigned) * 4, st));
   unsigned* rd = ratio_dev.as<unsigned>();
@@ -1168,10 +1388,8 @@ int gemm_ozaki_impl(const GemmOp& op, cudaStream_t st, bool plan_only, int* s_ou
   const bool known = pa && pa->have_left && pb && pb->have_right;
   double a1 = 1.0, b1 = 1.0, a2 = 1.0, b2 = 1.0;
   if (!forced && !known) {
-    oz_ratio_out_kernel<<<1, 32, 0, st>>>(rd, ratio_mapped);
-    count_launch();
-    NNB_CUDA(cudaGetLastError());
-    NNB_CUDA(cudaStreamSynchronize(st));
+    unsigned ratio_host[4];
+    NNB_TRY(read_ratios_mapped(rd, ratio_host, st));
     trace_mark(st, "oz stats");
     const auto f = [](unsigned u) { return std::max((double)__builtin_bit_cast(float, u), 1.0); };
     a1 = f(ratio_host[0]);
@@ -1268,7 +1486,7 @@ void ozaki_stats(double* ms, double* work, int64_t* launches, int reset) {
 // (sharded.cu drives them; see engine.cuh)
 int oz_col_partials(const double* F, int64_t ld, int64_t rows, int64_t n, double* out, cudaStream_t st) {
   if (n <= 0) return 0;
-  const int64_t kb = std::max<int64_t>((rows + 255) / 256, 1);
+  const int64_t kb = std::max<int64_t>((rows + kColRows - 1) / kColRows, 1);
   DevBuf part;
   NNB_TRY(part.alloc(sizeof(double) * 3 * kb * n, st));
   Timed tm(1, (double)rows * n * 8.0, st);
@@ -1303,17 +1521,9 @@ int oz_row_stats(const double* L, int64_t ld, int64_t rows, int64_t k, int* exps
 }
 
 int oz_read_ratios(const unsigned* rd, double out[4], cudaStream_t st) {
-  static thread_local unsigned* host = nullptr;
-  static thread_local unsigned* mapped = nullptr;
-  if (!host) {
-    NNB_CUDA(cudaHostAlloc(&host, sizeof(unsigned) * 4, cudaHostAllocMapped));
-    NNB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mapped), host, 0));
-  }
-  oz_ratio_out_kernel<<<1, 32, 0, st>>>(rd, mapped);
-  count_launch();
-  NNB_CUDA(cudaGetLastError());
-  NNB_CUDA(cudaStreamSynchronize(st));
-  for (int i = 0; i < 4; ++i) out[i] = std::max((double)__builtin_bit_cast(float, host[i]), 1.0);
+  unsigned h[4];
+  NNB_TRY(read_ratios_mapped(rd, h, st));
+  for (int i = 0; i < 4; ++i) out[i] = std::max((double)__builtin_bit_cast(float, h[i]), 1.0);
   return 0;
 }
 
@@ -1328,10 +1538,8 @@ int oz_split_left(const double* L, int64_t ld, int64_t rows, int64_t k, const in
   if (s > 17) return fail(7, "ozaki: more than 17 moduli needed");
   const OzConst c = make_const(s);
   Timed tm(1, (double)rows * k * (8.0 + s), st);
-  oz_split_rows_kernel<<<static_cast<unsigned>(rows), 256, 0, st>>>(L, ld, (int)rows, (int)k, kp, out, exps, c);
-  count_launch();
-  NNB_CUDA(cudaGetLastError());
-  return 0;
+  (void)c;
+  return split_rows_launch(s, L, ld, (int)rows, (int)k, kp, out, exps, st);
 }
 
 int oz_split_right(const double* F, int64_t ld, int64_t k_rows, int64_t n, const int* exps, int s, int8_t* out,
@@ -1340,11 +1548,8 @@ int oz_split_right(const double* F, int64_t ld, int64_t k_rows, int64_t n, const
   if (s > 17) return fail(7, "ozaki: more than 17 moduli needed");
   const OzConst c = make_const(s);
   Timed tm(1, (double)k_rows * n * (8.0 + s), st);
-  oz_split_cols_kernel<<<dim3((unsigned)((n + 63) / 64), (unsigned)((kp + 63) / 64)), 256, 0, st>>>(
-      F, ld, (int)k_rows, (int)n, kp, out, exps, c);
-  count_launch();
-  NNB_CUDA(cudaGetLastError());
-  return 0;
+  (void)c;
+  return split_cols_launch(s, F, ld, (int)k_rows, (int)n, kp, out, exps, st);
 }
 
 int oz_gemm_block(const int8_t* a_res, int64_t M, int64_t a_kp, int64_t a_k0, const int8_t* b_res, int64_t N,
