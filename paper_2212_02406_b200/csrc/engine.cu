@@ -311,9 +311,8 @@ int gemm(GemmOp op, RedWs* red, cudaStream_t s) {
   }
   if (arith() == 1 && !op.b_kmajor) return gemm_exact(op, s);  // reference-exact mode (exact.cu)
   if ((arith() == 2 || (arith() == 0 && ozaki_pays(op.M, op.N, op.K))) && !op.ep.C2 && !op.ep.acc_in) {
-    // int8 emulation (ozaki.cu).  A symmetric-order product is formed whole here: the
-    // whole emulated product (≈4× DMMA's rate) beats DMMA on its upper tile triangle (2×)
-    op.ep.sym = 0;
+    // int8 emulation (ozaki.cu).  A symmetric-order product runs only the int8 GEMM tiles
+    // that meet the upper triangle and the reconstruction mirrors them (ep.sym)
     return gemm_ozaki(op, s);
   }
   if (op.b_kmajor) return use_big(op.M, op.N) ? launch_cfg<BigCfgT>(op, s) : launch_cfg<SmallCfgT>(op, s);

@@ -44,6 +44,7 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -338,7 +339,7 @@ template <int kC>
 __global__ void __launch_bounds__(192, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, int M, int N,
                    int K, int64_t ldr, uint8_t* __restrict__ out, const OzConst cst, int tiles_m, int tiles_n,
-                   int group_m, int a_k0, int accumulate) {
+                   int group_m, int a_k0, int accumulate, const uint32_t* __restrict__ tile_list, int list_len) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -352,7 +353,19 @@ __global__ void __launch_bounds__(192, 1)
   const int unit = static_cast<int>(blockIdx.x) / kC, nunits = static_cast<int>(gridDim.x) / kC;
   const int tiles_mu = (tiles_m + kC - 1) / kC;  // tile-rows in units of kC
   const int group_u = max(1, group_m / kC);
-  const int total = tiles_mu * tiles_n * cst.s;
+  // a tile list (symmetric products: the tiles that meet the upper triangle, in raster
+  // order) replaces the full (tile-row, tile-col) space
+  const int per = tile_list ? list_len : tiles_mu * tiles_n;
+  const int total = per * cst.s;
+  const auto coord = [&](int t) -> TileCoord {
+    if (!tile_list) return tile_of(t, tiles_mu, tiles_n, group_u);
+    TileCoord c;
+    c.l = t / per;
+    const uint32_t code = __ldg(tile_list + (t - c.l * per));
+    c.mt = static_cast<int>(code >> 16);
+    c.nt = static_cast<int>(code & 0xffffu);
+    return c;
+  };
   constexpr uint16_t kMask = static_cast<uint16_t>((1u << kC) - 1u);
 
   if (threadIdx.x == 0) {
@@ -379,7 +392,7 @@ __global__ void __launch_bounds__(192, 1)
       tma_prefetch_desc(&tma_b);
       int it = 0;
       for (int t = unit; t < total; t += nunits) {
-        const TileCoord tc = tile_of(t, tiles_mu, tiles_n, group_u);
+        const TileCoord tc = coord(t);
         const int mt = tc.mt * kC + static_cast<int>(crank);
         const int arow = tc.l * M + mt * kBM, brow = tc.l * N + tc.nt * kBN;
         for (int kb = 0; kb < nk; ++kb, ++it) {
@@ -429,7 +442,7 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;
     int n_t = 0;
     for (int t = unit; t < total; t += nunits, ++n_t) {
-      const TileCoord tc = tile_of(t, tiles_mu, tiles_n, group_u);
+      const TileCoord tc = coord(t);
       const int mt = tc.mt * kC + static_cast<int>(crank);
       const int acc = n_t & 1;
       mbar_wait(&tfull[acc], (n_t >> 1) & 1);
@@ -948,7 +961,11 @@ __global__ void __launch_bounds__(256) oz_recon_kernel(const uint8_t* __restrict
   double ss = 0.0;
   int nf = 0;
   const bool want_red = ep.ss_partial != nullptr;
-  if (row < M && c0 < N) {
+  // symmetric products (ep.sym): only the elements r <= c exist in the residues (the GEMM
+  // ran the upper-triangle tiles); each is stored with its mirror and counted twice in
+  // the Σ C² / non-finite reduction, as the DMMA epilogue does
+  const bool sym = ep.sym != 0;
+  if (row < M && c0 < N && !(sym && c0 + 7 < row)) {
     uint2 rv[S];
 #pragma unroll
     for (int l = 0; l < S; ++l) rv[l] = *reinterpret_cast<const uint2*>(res + ((int64_t)l * M + row) * ldr + c0);
@@ -988,9 +1005,24 @@ __global__ void __launch_bounds__(256) oz_recon_kernel(const uint8_t* __restrict
         if (era == kBadExp || e == kBadExp) cv = __longlong_as_double(0x7ff8000000000000LL);
         else cv = scale2(x, -(era + e));
         double o = ep.alpha * cv;
-        if (ep.D && cc < N) o = fma(ep.beta, ep.D[(int64_t)row * ep.ldd + cc], o);
+        if (ep.D && cc < N && !(sym && row > cc)) o = fma(ep.beta, ep.D[(int64_t)row * ep.ldd + cc], o);
         if ((int64_t)row + ep.diag_offset == cc) o += ep.gamma;
         out2[h] = o;
+      }
+      if (sym) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cc = c + h;
+          if (cc >= N || row > cc) continue;
+          ep.C[(int64_t)row * ep.ldc + cc] = out2[h];
+          if (row < cc) ep.C[(int64_t)cc * ep.ldc + row] = out2[h];
+          if (want_red) {
+            const double w = row < cc ? 2.0 : 1.0;
+            ss = fma(w * out2[h], out2[h], ss);
+            nf += (row < cc ? 2 : 1) * !isfinite(out2[h]);
+          }
+        }
+        continue;
       }
       double* cp = ep.C + (int64_t)row * ep.ldc + c;
       if (two) {
@@ -1275,12 +1307,44 @@ int make_tmap_u8(CUtensorMap* map, const void* base, int64_t rows, int64_t cols,
 // (row stride b_kp, zero beyond b_kp).  a_k0 > 0 multiplies a column block of the left
 // operand's residues with a row block of the right operand's (the sharded K split);
 // the left operand's columns past the block meet the right block's zeros.
+// The tiles (128-row tile-row mt, 256-column tile-col nt) of an n×n product that meet its
+// upper triangle (128·mt <= 256·nt + 255), in the grouped raster order of tile_of, packed
+// mt << 16 | nt — built once per shape and device and kept.
+const uint32_t* upper_tile_list(int tiles_m, int tiles_n, int group_m, int* len, cudaStream_t st) {
+  static std::mutex mu;
+  static std::vector<std::tuple<int, int, int, int, uint32_t*, int>> cache;  // dev, tm, tn, gm, list, len
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  for (auto& e : cache)
+    if (std::get<0>(e) == dev && std::get<1>(e) == tiles_m && std::get<2>(e) == tiles_n && std::get<3>(e) == group_m) {
+      *len = std::get<5>(e);
+      return std::get<4>(e);
+    }
+  std::vector<uint32_t> h;
+  for (int r = 0; r < tiles_m * tiles_n; ++r) {  // tile_of's raster, host side
+    const int group = r / (group_m * tiles_n), first_m = group * group_m;
+    const int gm = std::min(tiles_m - first_m, group_m), w = r - group * group_m * tiles_n;
+    const int mt = first_m + w % gm, nt = w / gm;
+    if (128LL * mt <= 256LL * nt + 255) h.push_back(static_cast<uint32_t>(mt) << 16 | static_cast<uint32_t>(nt));
+  }
+  uint32_t* d = nullptr;
+  if (cudaMalloc(&d, sizeof(uint32_t) * h.size()) != cudaSuccess) return nullptr;
+  if (cudaMemcpyAsync(d, h.data(), sizeof(uint32_t) * h.size(), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return nullptr;
+  cache.emplace_back(dev, tiles_m, tiles_n, group_m, d, static_cast<int>(h.size()));
+  *len = static_cast<int>(h.size());
+  return d;
+}
+
 int launch_oz_gemm(const int8_t* a_res, int64_t M, int64_t a_kp, int64_t a_k0, const int8_t* b_res, int64_t N,
                    int64_t b_kp, int64_t K, const OzConst& c, uint8_t* out, int64_t ldr, bool accumulate,
-                   cudaStream_t st, int reserve_sms = 0) {
+                   cudaStream_t st, int reserve_sms = 0, bool upper = false) {
   const int s = c.s;
   // NNB_DEBUG=1 NNB_OZ_CLUSTER=2: B multicast across CTA pairs (oz_gemm_kernel<2>)
-  static const int kc = debug_env("NNB_OZ_CLUSTER") && std::atoi(debug_env("NNB_OZ_CLUSTER")) == 2 ? 2 : 1;
+  static const int kc_env = debug_env("NNB_OZ_CLUSTER") && std::atoi(debug_env("NNB_OZ_CLUSTER")) == 2 ? 2 : 1;
+  const int kc = upper ? 1 : kc_env;
   CUtensorMap ta, tb;
   NNB_TRY(make_tmap_u8(&ta, a_res, (int64_t)s * M, a_kp, a_kp, kBM, kBK));
   NNB_TRY(make_tmap_u8(&tb, b_res, (int64_t)s * N, b_kp, b_kp, kBN / kc, kBK));
@@ -1293,14 +1357,20 @@ int launch_oz_gemm(const int8_t* a_res, int64_t M, int64_t a_kp, int64_t a_k0, c
     NNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   const int tiles_m = (int)((M + kBM - 1) / kBM), tiles_n = (int)((N + kBN - 1) / kBN);
-  const int64_t total = (int64_t)((tiles_m + kc - 1) / kc) * tiles_n * s;
-  if (total > INT32_MAX) return fail(7, "ozaki: too many tiles");
-  Timed tm(0, 2.0 * s * (double)M * N * K, st);  // int8 tensor ops
   static const int gm = debug_env("NNB_OZ_GROUP") ? std::atoi(debug_env("NNB_OZ_GROUP")) : kGroupM;
+  int list_len = 0;
+  const uint32_t* list = nullptr;
+  if (upper) {
+    list = upper_tile_list(tiles_m, tiles_n, gm, &list_len, st);
+    if (!list) return fail(7, "ozaki: upper-triangle tile list");
+  }
+  const int64_t total = (upper ? (int64_t)list_len : (int64_t)((tiles_m + kc - 1) / kc) * tiles_n) * s;
+  if (total > INT32_MAX) return fail(7, "ozaki: too many tiles");
+  Timed tm(0, 2.0 * s * (double)M * N * K * (upper ? (double)list_len / ((double)tiles_m * tiles_n) : 1.0), st);
   if (kc == 1) {
     const unsigned grid = (unsigned)std::min<int64_t>(total, std::max(1, sms - reserve_sms));
     oz_gemm_kernel<1><<<grid, 192, kGemmSmem, st>>>(ta, tb, (int)M, (int)N, (int)K, ldr, out, c, tiles_m, tiles_n,
-                                                    gm, (int)a_k0, accumulate ? 1 : 0);
+                                                    gm, (int)a_k0, accumulate ? 1 : 0, list, list_len);
   } else {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
@@ -1322,7 +1392,8 @@ int launch_oz_gemm(const int8_t* a_res, int64_t M, int64_t a_kp, int64_t a_k0, c
     const int64_t units = std::min<int64_t>(total, std::max(1, std::min(max_clusters, (sms - reserve_sms) / 2)));
     cfg.gridDim = dim3((unsigned)(2 * units));
     NNB_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<2>, ta, tb, (int)M, (int)N, (int)K, ldr, out, c, tiles_m,
-                                tiles_n, gm, (int)a_k0, accumulate ? 1 : 0));
+                                tiles_n, gm, (int)a_k0, accumulate ? 1 : 0, static_cast<const uint32_t*>(nullptr),
+                                0));
   }
   count_launch();
   NNB_CUDA(cudaGetLastError());
@@ -1439,7 +1510,7 @@ int gemm_ozaki_impl(const GemmOp& op, cudaStream_t st, bool plan_only, int* s_ou
   DevBuf res;
   NNB_TRY(res.alloc((size_t)s * M * ldr, st));
   NNB_TRY(launch_oz_gemm(L->res.as<int8_t>(), M, L->kp, 0, R->res.as<int8_t>(), N, R->kp, K, c, res.as<uint8_t>(),
-                         ldr, false, st));
+                         ldr, false, st, 0, op.ep.sym != 0));
   trace_mark(st, "oz gemm");
   // reconstruction + the chain's epilogue
   NNB_TRY(launch_recon(s, res.as<uint8_t>(), ldr, (int)M, (int)N, L->exps.as<int>(), R->exps.as<int>(), op.ep, c,

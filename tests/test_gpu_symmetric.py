@@ -142,3 +142,35 @@ def test_symmetric_nonfinite_input_diverges():
     a[10, 20] = a[20, 10] = np.nan
     with pytest.raises((nnb.DivergenceError, nnb.DomainError)):
         nnb.nn_chain(a, None, p=1, max_iters=3, order=nnb.ORDER_SYMMETRIC)
+
+
+def test_symmetric_int8_emulation_runs_upper_tiles():
+    """Under the int8 emulation (N >= 3072 in FAST) a symmetric-order Horner product runs
+    only the int8 GEMM tiles that meet the upper triangle and the reconstruction mirrors
+    them: for nests above the eps switch the int8 work is R (full) + p upper-tile products,
+    X stays symmetric bit for bit, and X matches the full-product chain."""
+    import torch
+
+    n, p = 4096, 2
+    a = torch.from_numpy(W.spd_conditioned(n, 1e3, seed=7)).cuda()
+    nnb.ozaki_profile(True)
+    try:
+        nnb.ozaki_stats(reset=True)
+        xs, rs = nnb.nn_chain(a, None, p=p, max_iters=3, order=nnb.ORDER_SYMMETRIC)
+        torch.cuda.synchronize()
+        ws = nnb.ozaki_stats(reset=True)["gemm"]
+        xn, rn = nnb.nn_chain(a, None, p=p, max_iters=3)
+        torch.cuda.synchronize()
+        wn = nnb.ozaki_stats(reset=True)["gemm"]
+    finally:
+        nnb.ozaki_profile(False)
+    assert ws["launches"] == wn["launches"] > 0
+    tm, tn = n // 128, n // 256
+    frac = sum(1 for m in range(tm) for c in range(tn) if 128 * m <= 256 * c + 255) / (tm * tn)
+    # 3 nests (eps stays far above 1e-4) + the final residual: 3 + 1 full products,
+    # 3·p upper-tile ones; equal moduli counts in both chains assumed by the ratio
+    expect = (4 + 3 * p * frac) / (4 + 3 * p)
+    assert abs(ws["work"] / wn["work"] - expect) < 0.02, (ws["work"] / wn["work"], expect)
+    assert torch.equal(xs, xs.T)
+    assert (torch.linalg.norm(xs - xn) / torch.linalg.norm(xn)).item() < 1e-12
+    assert np.allclose([e for _, e in rs.history], [e for _, e in rn.history], rtol=1e-9, atol=1e-15)
