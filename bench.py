@@ -320,7 +320,7 @@ def run_dense(args, world, rank):
                        "tflops": round(flops_step / (rd.device_ms * 1e-3) / 1e12, 3),
                        "frac_of_dmma_peak": round(flops_step / (rd.device_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
                        "eps_before_nest": rd.history[0][1],
-                       "x_rel_frob_vs_headline_nest": float(torch.linalg.norm(xd - step(x)[0]) / torch.linalg.norm(xd))}
+                       "x_rel_frob_vs_headline_nest": float(torch.linalg.norm(xd - chain(x, 1)[0]) / torch.linalg.norm(xd))}
         del xd
     # the 8-rank sharded schedule emulated on this GPU (virtual ranks run one after another):
     # its device time against the single-GPU nest is the per-rank compute efficiency the

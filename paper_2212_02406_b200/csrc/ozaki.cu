@@ -45,6 +45,7 @@
 #include <cstring>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -948,16 +949,18 @@ int split_cols_launch(int s, const double* B, int64_t ld, int k, int n, int64_t 
 }
 
 // ---------------------------------------------------------------- reconstruction
-// One block: 16 rows × 128 columns; thread t: row t/16, 8 consecutive columns.
-template <int S>
-__global__ void __launch_bounds__(256) oz_recon_kernel(const uint8_t* __restrict__ res, int64_t ldr, int M, int N,
-                                                       const int* __restrict__ ea, const int* __restrict__ eb,
-                                                       GemmEpilogue ep, const OzConst cst) {
+// One block: 16 rows × 16·CPT columns; thread t: row t/16, CPT consecutive columns.
+template <int S, int CPT>
+__device__ __forceinline__ void recon_body(const uint8_t* __restrict__ res, int64_t ldr, int M, int N,
+                                           const int* __restrict__ ea, const int* __restrict__ eb,
+                                           const GemmEpilogue& ep) {
+  static_assert(CPT == 8 || CPT == 4, "8 or 4 columns per thread");
+  using RV = typename std::conditional<CPT == 8, uint2, uint32_t>::type;
   __shared__ double red[8];
   __shared__ int redi[8];
   __shared__ int last_flag;
   const int row = blockIdx.y * 16 + (threadIdx.x >> 4);
-  const int c0 = blockIdx.x * 128 + (threadIdx.x & 15) * 8;
+  const int c0 = blockIdx.x * (16 * CPT) + (threadIdx.x & 15) * CPT;
   double ss = 0.0;
   int nf = 0;
   const bool want_red = ep.ss_partial != nullptr;
@@ -965,13 +968,13 @@ __global__ void __launch_bounds__(256) oz_recon_kernel(const uint8_t* __restrict
   // ran the upper-triangle tiles); each is stored with its mirror and counted twice in
   // the Σ C² / non-finite reduction, as the DMMA epilogue does
   const bool sym = ep.sym != 0;
-  if (row < M && c0 < N && !(sym && c0 + 7 < row)) {
-    uint2 rv[S];
+  if (row < M && c0 < N && !(sym && c0 + CPT - 1 < row)) {
+    RV rv[S];
 #pragma unroll
-    for (int l = 0; l < S; ++l) rv[l] = *reinterpret_cast<const uint2*>(res + ((int64_t)l * M + row) * ldr + c0);
+    for (int l = 0; l < S; ++l) rv[l] = *reinterpret_cast<const RV*>(res + ((int64_t)l * M + row) * ldr + c0);
     const int era = ea[row];
 #pragma unroll 1
-    for (int jp = 0; jp < 4; ++jp) {
+    for (int jp = 0; jp < CPT / 2; ++jp) {
       const int c = c0 + 2 * jp;
       if (c >= N) break;
       const bool two = c + 1 < N;
@@ -980,7 +983,9 @@ __global__ void __launch_bounds__(256) oz_recon_kernel(const uint8_t* __restrict
       unsigned long long r2[S], v2[S];
 #pragma unroll
       for (int l = 0; l < S; ++l) {
-        const uint32_t word = (jp < 2) ? rv[l].x : rv[l].y;
+        uint32_t word;
+        if constexpr (CPT == 8) word = (jp < 2) ? rv[l].x : rv[l].y;
+        else word = rv[l];
         const int sel = (2 * jp) & 3;
         // byte b -> float exactly: the bits 0x4B0000bb are 2^23 + b
         r2[l] = add2(pk2(__uint_as_float(__byte_perm(word, 0x4B00u, 0x5440u + sel)),
@@ -1095,6 +1100,15 @@ __global__ void __launch_bounds__(256) oz_recon_kernel(const uint8_t* __restrict
     if (ep.eps_out) *ep.eps_out = sqrt(tot) * ep.eps_scale;
     *ep.tile_counter = 0u;
   }
+}
+
+// 8 columns per thread: 80 registers, 3 blocks per SM.  (4 columns per thread capped at 64
+// registers for 4 blocks per SM measured 10-15 % slower at N=8192.)
+template <int S>
+__global__ void __launch_bounds__(256) oz_recon_kernel(const uint8_t* __restrict__ res, int64_t ldr, int M, int N,
+                                                       const int* __restrict__ ea, const int* __restrict__ eb,
+                                                       GemmEpilogue ep, const OzConst cst) {
+  recon_body<S, 8>(res, ldr, M, N, ea, eb, ep);
 }
 
 // Live per-kernel timing for bench.py's roofline (nnb_ozaki_profile / nnb_ozaki_stats):
