@@ -364,6 +364,10 @@ def run_dense(args, world, rank):
 
 
 def run_dense_emulated(nnb, torch, a, x, n, p, world, ms_single, flops_step):
+    # warm: the schedule's residue buffers (≈35 GB at N=32768) come from the stream-ordered
+    # pool, which grows on the first call
+    nnb.nn_chain_sharded_emulated(a, world, x, p=p, max_iters=1, final_residual=False)
+    torch.cuda.synchronize()
     nnb.ozaki_stats(reset=True)
     nnb.ozaki_profile(True)
     xe, re_ = nnb.nn_chain_sharded_emulated(a, world, x, p=p, max_iters=1, final_residual=False)

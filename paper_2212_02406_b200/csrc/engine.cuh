@@ -159,9 +159,12 @@ int oz_split_left(const double* L, int64_t ld, int64_t rows, int64_t k, const in
                   int64_t kp, cudaStream_t st);
 int oz_split_right(const double* F, int64_t ld, int64_t k_rows, int64_t n, const int* exps, int s, int8_t* out,
                    int64_t kp, cudaStream_t st);
-int oz_gemm_block(const int8_t* a_res, int64_t M, int64_t a_kp, int64_t a_k0, const int8_t* b_res, int64_t N,
-                  int64_t b_kp, int s, uint8_t* out, int64_t ldr, bool accumulate, cudaStream_t st,
-                  int reserve_sms = 0);  // persistent grid of SMs − reserve_sms CTAs
+// s int8 GEMMs over nblk K blocks in one launch: block b multiplies the left residues' columns
+// from a_k0[b] by the right residue array's rows from b_row0[b] (b_kp bytes each, zero-padded);
+// `accumulate` adds to the residues in `out` (mod m); persistent grid of SMs − reserve_sms CTAs
+int oz_gemm_blocks(const int8_t* a_res, int64_t M, int64_t a_kp, const int64_t* a_k0, const int8_t* b_res, int64_t N,
+                   int64_t b_rows, int64_t b_kp, const int64_t* b_row0, int nblk, int s, uint8_t* out, int64_t ldr,
+                   bool accumulate, cudaStream_t st, int reserve_sms = 0);
 int oz_reconstruct(int s, const uint8_t* res, int64_t ldr, int64_t M, int64_t N, const int* ea, const int* eb,
                    GemmEpilogue ep, struct RedWs* red, cudaStream_t st);
 // the next real chain of the calling thread copies its final residual I − A·X to r (device, ld)

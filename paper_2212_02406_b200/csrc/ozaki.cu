@@ -328,6 +328,17 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// The K range of one int8 GEMM launch: `n` blocks of `nk` 128-byte k-tiles each; block b
+// reads the left operand's residues from column a_k0[b] and the right operand's from row
+// b_row0[b] of tma_b (the sharded K split hands several arrived residue blocks to one
+// launch; a single-GPU product is one block at 0, 0).
+constexpr int kMaxKBlocks = 16;
+struct KSpan {
+  int n = 1, nk = 0;
+  int a_k0[kMaxKBlocks] = {};
+  int b_row0[kMaxKBlocks] = {};
+};
+
 // Persistent: CTA b takes tiles b, b + grid, ... of the (modulus, tile-row, tile-col) space;
 // out[l][row][col] = (Σ_k a_l[row][k]·b_l[col][k]) mod m_l.  a_l's rows live at l·M + row
 // of tma_a, b_l's at l·N + col of tma_b.  The TMA ring runs across tile boundaries and the
@@ -339,8 +350,8 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
 template <int kC>
 __global__ void __launch_bounds__(192, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, int M, int N,
-                   int K, int64_t ldr, uint8_t* __restrict__ out, const OzConst cst, int tiles_m, int tiles_n,
-                   int group_m, int a_k0, int accumulate, const uint32_t* __restrict__ tile_list, int list_len) {
+                   int64_t ldr, uint8_t* __restrict__ out, const OzConst cst, int tiles_m, int tiles_n,
+                   int group_m, const KSpan ks, int accumulate, const uint32_t* __restrict__ tile_list, int list_len) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -349,7 +360,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tempty = tfull + kAccBufs;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nk = (K + kBK - 1) / kBK;
+  const int nk = ks.n * ks.nk;  // k-tiles per output tile over all K blocks
   const uint32_t crank = kC > 1 ? cluster_ctarank() : 0u;
   const int unit = static_cast<int>(blockIdx.x) / kC, nunits = static_cast<int>(gridDim.x) / kC;
   const int tiles_mu = (tiles_m + kC - 1) / kC;  // tile-rows in units of kC
@@ -401,12 +412,13 @@ __global__ void __launch_bounds__(192, 1)
           if (it >= kStages) mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
           uint8_t* sa = smem + st * kStageBytes;
           mbar_arrive_expect_tx(&full[st], kStageBytes);
-          tma_load_2d(sa, &tma_a, &full[st], a_k0 + kb * kBK, arow);
+          const int blk = kb / ks.nk, kt = kb - blk * ks.nk;
+          tma_load_2d(sa, &tma_a, &full[st], ks.a_k0[blk] + kt * kBK, arow);
           if constexpr (kC == 1) {
-            tma_load_2d(sa + kABytes, &tma_b, &full[st], kb * kBK, brow);
+            tma_load_2d(sa + kABytes, &tma_b, &full[st], kt * kBK, ks.b_row0[blk] + brow);
           } else {
-            tma_load_2d_mc(sa + kABytes + crank * (kBBytes / kC), &tma_b, &full[st], kb * kBK,
-                           brow + static_cast<int>(crank) * (kBN / kC), kMask);
+            tma_load_2d_mc(sa + kABytes + crank * (kBBytes / kC), &tma_b, &full[st], kt * kBK,
+                           ks.b_row0[blk] + brow + static_cast<int>(crank) * (kBN / kC), kMask);
           }
         }
       }
@@ -1352,16 +1364,20 @@ const uint32_t* upper_tile_list(int tiles_m, int tiles_n, int group_m, int* len,
   return d;
 }
 
-int launch_oz_gemm(const int8_t* a_res, int64_t M, int64_t a_kp, int64_t a_k0, const int8_t* b_res, int64_t N,
-                   int64_t b_kp, int64_t K, const OzConst& c, uint8_t* out, int64_t ldr, bool accumulate,
+// b_rows: rows of the right operand's residue array (s·N for one block; the sharded
+// gather holds G blocks of fs·N rows)
+int launch_oz_gemm(const int8_t* a_res, int64_t M, int64_t a_kp, const int8_t* b_res, int64_t N, int64_t b_rows,
+                   int64_t b_kp, const KSpan& ks, const OzConst& c, uint8_t* out, int64_t ldr, bool accumulate,
                    cudaStream_t st, int reserve_sms = 0, bool upper = false) {
+  if (ks.n < 1 || ks.n > kMaxKBlocks) return fail(7, "ozaki: K block count out of range");
+  const int64_t K = (int64_t)ks.n * ks.nk * kBK;  // work accounting: the padded K of the launch
   const int s = c.s;
   // NNB_DEBUG=1 NNB_OZ_CLUSTER=2: B multicast across CTA pairs (oz_gemm_kernel<2>)
   static const int kc_env = debug_env("NNB_OZ_CLUSTER") && std::atoi(debug_env("NNB_OZ_CLUSTER")) == 2 ? 2 : 1;
   const int kc = upper ? 1 : kc_env;
   CUtensorMap ta, tb;
   NNB_TRY(make_tmap_u8(&ta, a_res, (int64_t)s * M, a_kp, a_kp, kBM, kBK));
-  NNB_TRY(make_tmap_u8(&tb, b_res, (int64_t)s * N, b_kp, b_kp, kBN / kc, kBK));
+  NNB_TRY(make_tmap_u8(&tb, b_res, b_rows, b_kp, b_kp, kBN / kc, kBK));
   NNB_TRY(ensure_smem<oz_gemm_kernel<1>>(kGemmSmem));
   NNB_TRY(ensure_smem<oz_gemm_kernel<2>>(kGemmSmem));
   static int sms = 0;
@@ -1383,8 +1399,8 @@ int launch_oz_gemm(const int8_t* a_res, int64_t M, int64_t a_kp, int64_t a_k0, c
   Timed tm(0, 2.0 * s * (double)M * N * K * (upper ? (double)list_len / ((double)tiles_m * tiles_n) : 1.0), st);
   if (kc == 1) {
     const unsigned grid = (unsigned)std::min<int64_t>(total, std::max(1, sms - reserve_sms));
-    oz_gemm_kernel<1><<<grid, 192, kGemmSmem, st>>>(ta, tb, (int)M, (int)N, (int)K, ldr, out, c, tiles_m, tiles_n,
-                                                    gm, (int)a_k0, accumulate ? 1 : 0, list, list_len);
+    oz_gemm_kernel<1><<<grid, 192, kGemmSmem, st>>>(ta, tb, (int)M, (int)N, ldr, out, c, tiles_m, tiles_n, gm, ks,
+                                                    accumulate ? 1 : 0, list, list_len);
   } else {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
@@ -1405,9 +1421,8 @@ int launch_oz_gemm(const int8_t* a_res, int64_t M, int64_t a_kp, int64_t a_k0, c
     }
     const int64_t units = std::min<int64_t>(total, std::max(1, std::min(max_clusters, (sms - reserve_sms) / 2)));
     cfg.gridDim = dim3((unsigned)(2 * units));
-    NNB_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<2>, ta, tb, (int)M, (int)N, (int)K, ldr, out, c, tiles_m,
-                                tiles_n, gm, (int)a_k0, accumulate ? 1 : 0, static_cast<const uint32_t*>(nullptr),
-                                0));
+    NNB_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<2>, ta, tb, (int)M, (int)N, ldr, out, c, tiles_m, tiles_n, gm,
+                                ks, accumulate ? 1 : 0, static_cast<const uint32_t*>(nullptr), 0));
   }
   count_launch();
   NNB_CUDA(cudaGetLastError());
@@ -1523,8 +1538,10 @@ int gemm_ozaki_impl(const GemmOp& op, cudaStream_t st, bool plan_only, int* s_ou
   const int64_t ldr = (N + 15) / 16 * 16;
   DevBuf res;
   NNB_TRY(res.alloc((size_t)s * M * ldr, st));
-  NNB_TRY(launch_oz_gemm(L->res.as<int8_t>(), M, L->kp, 0, R->res.as<int8_t>(), N, R->kp, K, c, res.as<uint8_t>(),
-                         ldr, false, st, 0, op.ep.sym != 0));
+  KSpan ks;
+  ks.nk = (int)((K + kBK - 1) / kBK);
+  NNB_TRY(launch_oz_gemm(L->res.as<int8_t>(), M, L->kp, R->res.as<int8_t>(), N, (int64_t)s * N, R->kp, ks, c,
+                         res.as<uint8_t>(), ldr, false, st, 0, op.ep.sym != 0));
   trace_mark(st, "oz gemm");
   // reconstruction + the chain's epilogue
   NNB_TRY(launch_recon(s, res.as<uint8_t>(), ldr, (int)M, (int)N, L->exps.as<int>(), R->exps.as<int>(), op.ep, c,
@@ -1637,15 +1654,24 @@ int oz_split_right(const double* F, int64_t ld, int64_t k_rows, int64_t n, const
   return split_cols_launch(s, F, ld, (int)k_rows, (int)n, kp, out, exps, st);
 }
 
-int oz_gemm_block(const int8_t* a_res, int64_t M, int64_t a_kp, int64_t a_k0, const int8_t* b_res, int64_t N,
-                  int64_t b_kp, int s, uint8_t* out, int64_t ldr, bool accumulate, cudaStream_t st,
-                  int reserve_sms) {
-  if (M <= 0 || N <= 0) return 0;
+int oz_gemm_blocks(const int8_t* a_res, int64_t M, int64_t a_kp, const int64_t* a_k0, const int8_t* b_res, int64_t N,
+                   int64_t b_rows, int64_t b_kp, const int64_t* b_row0, int nblk, int s, uint8_t* out, int64_t ldr,
+                   bool accumulate, cudaStream_t st, int reserve_sms) {
+  if (M <= 0 || N <= 0 || nblk <= 0) return 0;
   if (s > 17) return fail(7, "ozaki: more than 17 moduli needed");
+  if (nblk > kMaxKBlocks) return fail(7, "ozaki: more than 16 K blocks in one launch");
   // a TMA box must start on a 16-byte boundary of the row (the sharded partition's 16-row
   // units guarantee it for the block origins)
-  if (a_k0 % 16 || b_kp % 16 || a_kp % 16) return fail(7, "ozaki: block origin or stride not a multiple of 16 bytes");
-  return launch_oz_gemm(a_res, M, a_kp, a_k0, b_res, N, b_kp, b_kp, make_const(s), out, ldr, accumulate, st,
+  if (b_kp % 16 || a_kp % 16) return fail(7, "ozaki: residue rows not a multiple of 16 bytes");
+  KSpan ks;
+  ks.n = nblk;
+  ks.nk = (int)((b_kp + kBK - 1) / kBK);
+  for (int b = 0; b < nblk; ++b) {
+    if (a_k0[b] % 16) return fail(7, "ozaki: block origin not a multiple of 16 bytes");
+    ks.a_k0[b] = (int)a_k0[b];
+    ks.b_row0[b] = (int)b_row0[b];
+  }
+  return launch_oz_gemm(a_res, M, a_kp, b_res, N, b_rows, b_kp, ks, make_const(s), out, ldr, accumulate, st,
                         reserve_sms);
 }
 

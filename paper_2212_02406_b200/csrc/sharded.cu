@@ -254,7 +254,7 @@ int ksplit_product(Shard& sh, int g, const double* L, int64_t ldl, const double*
 //      (identical on every rank);
 //   2. the moduli count s comes from those and the left operands' row ratios (a 16-byte
 //      all-gather), the same count the single-GPU product of the whole matrices takes;
-//   3. each rank splits its own block of F into K-major residues [s][n][kpb_g] (block g at a
+//   3. each rank splits its own block of F into K-major residues [s][n][kpb] (block g at a
 //      fixed offset of one gathered buffer) and a ring all-gather moves the residue blocks;
 //   4. rank g's product runs as G int8 GEMMs over the K blocks (own block first, then ring
 //      order, each waiting only for its block) accumulating mod m_l, then one
@@ -271,13 +271,13 @@ __global__ void max_slots_kernel(const unsigned* __restrict__ slots, int world, 
 }
 
 constexpr int kRingSms = 8;  // SMs the int8 GEMM leaves free while the residue ring runs
+constexpr int kMaxGroup = 16;  // K blocks per int8 GEMM launch (ozaki.cu kMaxKBlocks)
 
 struct OzSh {
-  int64_t n = 0, kp = 0, kp_total = 0, stride = 0;  // stride: doubles per rank record
-  std::vector<int64_t> kpb, koff;
+  int64_t n = 0, kp = 0, kpb = 0, stride = 0;  // kpb: 16-padded rows of the largest block
   DevBuf stats;  // [G][stride]: 3n column statistics + 2 doubles (= 4 ratio slots)
   DevBuf ints;   // fexps[n] | aexps[n] | lexps[n] | rd[4] | rdf[4]
-  DevBuf fres;   // gathered residues of F: block j at s·n·koff_j
+  DevBuf fres;   // gathered residues of F: block j at j·s·n·kpb (equal strides: one TMA map)
   int fcap = 0, fplanes = 0;
   bool fcombined = false, fknown = false;
   double fb1 = 1.0, fb2 = 1.0;
@@ -310,14 +310,8 @@ int oz_init(Shard& sh, OzSh& oz) {
   const int G = sh.world;
   oz.n = sh.n;
   oz.kp = (sh.n + 15) / 16 * 16;
-  oz.kpb.assign(G, 0);
-  oz.koff.assign(G, 0);
-  oz.kp_total = 0;
-  for (int j = 0; j < G; ++j) {
-    oz.kpb[j] = (sh.rows[j] + 15) / 16 * 16;
-    oz.koff[j] = oz.kp_total;
-    oz.kp_total += oz.kpb[j];
-  }
+  oz.kpb = 16;
+  for (int j = 0; j < G; ++j) oz.kpb = std::max<int64_t>(oz.kpb, (sh.rows[j] + 15) / 16 * 16);
   oz.stride = 3 * sh.n + 2;
   NNB_TRY(oz.stats.alloc(sizeof(double) * oz.stride * G, sh.s));
   NNB_TRY(oz.ints.alloc(sizeof(int) * (3 * sh.n + 8), sh.s));
@@ -347,8 +341,8 @@ int oz_ring(Shard& sh, OzSh& oz, int s) {
   auto& api = nccl();
   const int G = sh.world, me = sh.comm->rank;
   uint8_t* base = oz.fres.as<uint8_t>();
-  auto blk = [&](int j) { return base + (size_t)s * oz.n * oz.koff[j]; };
-  auto bytes = [&](int j) { return (size_t)s * oz.n * oz.kpb[j]; };
+  auto blk = [&](int j) { return base + (size_t)j * s * oz.n * oz.kpb; };
+  auto bytes = [&](int j) { return sh.rows[j] ? (size_t)s * oz.n * oz.kpb : (size_t)0; };
   NNB_CUDA(cudaEventRecord(sh.ready, sh.s));
   NNB_CUDA(cudaStreamWaitEvent(sh.comm->cs, sh.ready, 0));
   for (int q = 1; q < G; ++q) {
@@ -412,12 +406,12 @@ int oz_product(Shard& sh, OzSh& oz, const std::function<const double*(int)>& lef
   // ---- 3. F's residues: own block(s) split, then the ring (again only if s grew)
   if (oz.fplanes < s) {
     if (oz.fcap < s) {
-      NNB_TRY(oz.fres.alloc((size_t)s * n * oz.kp_total, sh.s));
+      NNB_TRY(oz.fres.alloc((size_t)G * s * n * oz.kpb, sh.s));
       oz.fcap = s;
     }
     for (int g : sh.local)
       NNB_TRY(oz_split_right(oz.fsrc + sh.row0[g] * sh.ld, sh.ld, sh.rows[g], n, oz.fexps(), s,
-                             oz.fres.as<int8_t>() + (size_t)s * n * oz.koff[g], oz.kpb[g], sh.s));
+                             oz.fres.as<int8_t>() + (size_t)g * s * n * oz.kpb, oz.kpb, sh.s));
     NNB_TRY(oz_ring(sh, oz, s));
     oz.fplanes = s;
   }
@@ -448,18 +442,36 @@ int oz_product(Shard& sh, OzSh& oz, const std::function<const double*(int)>& lef
     }
     // residue arrays are plane-major, so an array split for more planes than s serves s as
     // its first s planes; only F's block offsets depend on the planes it was split with (fs)
+    // the K blocks in ring order (own block first), grouped 1, 2, then the rest: one launch
+    // per group, each waiting only for its last block's ring step, so the ring (≈2.5 ms a step
+    // at G=8, N=32768) stays ahead of the GEMMs (≈7 ms a block) while 3 launches instead of G
+    // re-read and re-write the residues so far
+    std::vector<std::pair<int, int>> groups;  // [q0, q1) in ring steps
+    for (int q0 = 0, want = 1; q0 < G; want = (want == 1 ? 2 : G)) {
+      const int q1 = std::min(G, q0 + std::min<int>(want, (int)kMaxGroup));
+      groups.emplace_back(q0, q1);
+      q0 = q1;
+    }
     bool first = true;
-    for (int q = 0; q < G; ++q) {
-      const int j = ((g - q) % G + G) % G;
-      if (sh.rows[j] == 0) continue;
-      if (sh.comm && q > 0) NNB_CUDA(cudaStreamWaitEvent(sh.s, sh.ev[q], 0));
+    for (const auto& grp : groups) {
+      int64_t a_k0[kMaxGroup], b_row0[kMaxGroup];
+      int nb = 0;
+      for (int q = grp.first; q < grp.second; ++q) {
+        const int jj = ((g - q) % G + G) % G;
+        if (sh.rows[jj] == 0) continue;
+        a_k0[nb] = sh.row0[jj];
+        b_row0[nb] = (int64_t)jj * fs * n;
+        ++nb;
+      }
+      if (nb == 0) continue;
+      const int q_last = grp.second - 1;
+      if (sh.comm && q_last > 0) NNB_CUDA(cudaStreamWaitEvent(sh.s, sh.ev[q_last], 0));
       // the int8 GEMM is persistent (one CTA per SM, never yielding): while ring steps are
       // still to come it leaves kRingSms SMs to NCCL's send/recv CTAs, which could not
       // otherwise be scheduled before the grid drains (stream priority orders only pending CTAs)
-      const int reserve = (sh.comm && G > 1 && q < G - 1) ? kRingSms : 0;
-      NNB_TRY(oz_gemm_block(lbuf->as<int8_t>(), rows, oz.kp, sh.row0[j],
-                            oz.fres.as<int8_t>() + (size_t)fs * n * oz.koff[j], n, oz.kpb[j], s,
-                            oz.out.as<uint8_t>(), oz.kp, !first, sh.s, reserve));
+      const int reserve = (sh.comm && G > 1 && q_last < G - 1) ? kRingSms : 0;
+      NNB_TRY(oz_gemm_blocks(lbuf->as<int8_t>(), rows, oz.kp, a_k0, oz.fres.as<int8_t>(), n, (int64_t)G * fs * n,
+                             oz.kpb, b_row0, nb, s, oz.out.as<uint8_t>(), oz.kp, !first, sh.s, reserve));
       first = false;
     }
     NNB_TRY(oz_reconstruct(s, oz.out.as<uint8_t>(), oz.kp, rows, n, lexps + sh.row0[g], oz.fexps(), ep_of(g),

@@ -61,8 +61,13 @@ nnb.solve_sparse_factorized_sharded_emulated(nnb.Csr(rp, col, val, n=576), W.rhs
                                              nnb.Normalization(theta=0.2, valid=True), 3)
 # generators
 nnb.random_spd(40, 1e3, 3)
-# int8 emulation (tcgen05 + TMA), small
+# int8 emulation (tcgen05 + TMA), small: a product, a chain in symmetric order (upper-tile
+# GEMM + mirrored reconstruction) and the sharded schedule (residue blocks, K-block GEMMs
+# accumulated mod m, ragged 16-row blocks)
 with nnb.ozaki_arithmetic():
     nnb.matmul(rng.standard_normal((200, 300)), rng.standard_normal((300, 260)))
+    a = W.gram_shifted(400, seed=8, shift=1.0)
+    nnb.nn_chain(a, None, p=2, max_iters=2, order=nnb.ORDER_SYMMETRIC)
+    nnb.nn_chain_sharded_emulated(a, 3, p=2, max_iters=2)
 torch.cuda.synchronize()
 print("sanitize subset ok", nnb.kernel_launches(), "launches")
