@@ -1,6 +1,8 @@
 // Shared pieces of the single-GPU and row-sharded sparse factorized solves.
 #pragma once
 
+#include <vector>
+
 #include <cstdint>
 
 #include <cuda_runtime.h>
@@ -99,6 +101,25 @@ int narrow_offsets(const int64_t* in, int32_t* out, int64_t count, int64_t base,
 // then holds the device pattern table.
 int stencil_plan(int64_t n, const uint8_t* rcode, const double2* pat, const uint8_t* plen, int npat, int width,
                  DevBuf& table, int* W, int* H, bool* ok, cudaStream_t s);
+// a row pattern of the stencil table (device layout): values of the N, W, C, E, S entries
+struct StencilPattern {
+  double v[5];
+  int mask;
+  int pad;
+};
+// the pieces of stencil_plan, for row slabs (sparse_sharded.cu): the host pattern table and W
+// from a row dictionary (*W = 0 when it is not a 5-point stencil), and the edge check of an
+// H-row grid of codes (top / bottom rows checked only where they are the grid's)
+int stencil_patterns(const double2* pat, const uint8_t* plen, int npat, int width, int64_t* W,
+                     std::vector<StencilPattern>& tab, cudaStream_t s);
+int stencil_edges_ok(const uint8_t* rcode, const StencilPattern* table_dev, int W, int H, bool top, bool bottom,
+                     bool* ok, cudaStream_t s);
+// one temporal-blocked pass: `steps` (<= stencil_max_steps()) applications over a W×H grid
+int stencil_pass(const double* tin, const uint8_t* rcode, const double* zold, double* out,
+                 const StencilPattern* table_dev, int npat, int W, int H, int steps, int mode, double theta, int* flag,
+                 cudaStream_t s);
+int stencil_max_steps();
+double stencil_region_ratio();
 // The whole factorized solve (one RHS) in passes of up to 8 applications per launch;
 // bit-identical to run_factors.  *bytes_moved: HBM bytes the passes stream.
 int stencil_factors(const uint8_t* rcode, const DevBuf& table, int npat, int W, int H, const double* B,

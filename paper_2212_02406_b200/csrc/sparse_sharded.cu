@@ -19,6 +19,7 @@
 // device copies — validates partition, remap, halo sizes and the
 // interior/boundary split on a single device.
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -39,21 +40,52 @@ namespace sparse_detail {
   } while (0)
 
 // Per-slab statistics: min/max column, last row referencing below the slab,
-// first row referencing above it.
+// first row referencing above it.  Each thread folds its rows, then a warp reduction and
+// one atomic per warp and statistic (per-row atomics on the same four words serialised:
+// 23 ms of a 4096² slab's setup).
+__device__ __forceinline__ long long warp_min_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ long long warp_max_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
 __global__ void slab_stats_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col, int64_t rows,
                                   int64_t row0, int64_t* __restrict__ stats /* [min_col, max_col, lo_end, hi_start] */) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
-    int64_t mn = INT64_MAX, mx = -1;
-    for (int64_t e = rp[r] - rp[0]; e < rp[r + 1] - rp[0]; ++e) {
-      const int64_t c = col[e];
-      mn = c < mn ? c : mn;
-      mx = c > mx ? c : mx;
+  long long mn_all = LLONG_MAX, mx_all = -1, lo_end = 0, hi_start = LLONG_MAX;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t start = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int64_t r = start; r - threadIdx.x % 32 < rows; r += stride) {  // warp-uniform trip count
+    if (r < rows) {
+      long long mn = LLONG_MAX, mx = -1;
+      for (int64_t e = rp[r] - rp[0]; e < rp[r + 1] - rp[0]; ++e) {
+        const long long c = col[e];
+        mn = c < mn ? c : mn;
+        mx = c > mx ? c : mx;
+      }
+      if (mx >= 0) {  // empty rows contribute nothing
+        mn_all = min(mn_all, mn);
+        mx_all = max(mx_all, mx);
+        if (mn < row0) lo_end = max(lo_end, (long long)(r + 1));
+        if (mx >= row0 + rows) hi_start = min(hi_start, (long long)r);
+      }
     }
-    if (mx < 0) continue;  // empty row
-    atomicMin(reinterpret_cast<unsigned long long*>(stats + 0), static_cast<unsigned long long>(mn));
-    atomicMax(reinterpret_cast<unsigned long long*>(stats + 1), static_cast<unsigned long long>(mx));
-    if (mn < row0) atomicMax(reinterpret_cast<unsigned long long*>(stats + 2), static_cast<unsigned long long>(r + 1));
-    if (mx >= row0 + rows) atomicMin(reinterpret_cast<unsigned long long*>(stats + 3), static_cast<unsigned long long>(r));
+  }
+  mn_all = warp_min_ll(mn_all);
+  mx_all = warp_max_ll(mx_all);
+  lo_end = warp_max_ll(lo_end);
+  hi_start = warp_min_ll(hi_start);
+  if ((threadIdx.x & 31) == 0) {
+    if (mx_all >= 0) {
+      atomicMin(reinterpret_cast<unsigned long long*>(stats + 0), static_cast<unsigned long long>(mn_all));
+      atomicMax(reinterpret_cast<unsigned long long*>(stats + 1), static_cast<unsigned long long>(mx_all));
+    }
+    if (lo_end > 0) atomicMax(reinterpret_cast<unsigned long long*>(stats + 2), static_cast<unsigned long long>(lo_end));
+    if (hi_start != LLONG_MAX)
+      atomicMin(reinterpret_cast<unsigned long long*>(stats + 3), static_cast<unsigned long long>(hi_start));
   }
 }
 
@@ -86,7 +118,144 @@ struct Slab {
   const uint8_t* rlen = nullptr;
   int npat = 0;
   int64_t ext_len() const { return h_lo + rows + h_hi; }
+  // temporal blocking across slabs (5-point stencils, slabs whole grid rows): the slab's
+  // grid rows plus kTbRows halo rows on each inner side, codes in the global pattern table
+  bool tb = false;
+  int tbW = 0;
+  int64_t tb_lo = 0, tb_hi = 0;  // halo cells above / below (0 at the grid's edges)
+  DevBuf tb_mem;
+  uint8_t* tb_code = nullptr;
+  double* tb_ext[6] = {};        // T0, T1, Z0, Z1, B, X over the extended rows
+  int64_t tb_len() const { return tb_lo + rows + tb_hi; }
 };
+
+// what every rank contributes to the temporal-blocking decision (gathered, then decided
+// identically everywhere): its W (0: not a stencil slab), whether its own edge rows are
+// clean, and its row-pattern table
+struct TbRecord {
+  double w = 0, edges_ok = 0, npat = 0, pad = 0;
+  StencilPattern tab[kRowDictMax];
+};
+constexpr int kTbRows = 8;  // halo grid rows = applications per pass (sparse_stencil.cu kS)
+
+// the slab's own-pattern record (W, edge check over its own rows, table)
+int tb_record(const Slab& sl, int64_t n, TbRecord* rec, cudaStream_t s) {
+  *rec = TbRecord{};
+  if (!sl.rcode || sl.rows == 0) return 0;
+  int64_t w = 0;
+  std::vector<StencilPattern> tab;
+  NNB_TRY(stencil_patterns(sl.rpat, sl.rlen, sl.npat, sl.ell_width, &w, tab, s));
+  if (!w || sl.row0 % w || sl.rows % w || n % w || sl.rows / w > INT32_MAX) return 0;
+  DevBuf t;
+  NNB_TRY(t.alloc(sizeof(StencilPattern) * tab.size(), s));
+  NNB_CUDA(cudaMemcpyAsync(t.p, tab.data(), sizeof(StencilPattern) * tab.size(), cudaMemcpyHostToDevice, s));
+  bool ok = false;
+  NNB_TRY(stencil_edges_ok(sl.rcode, t.as<StencilPattern>(), (int)w, (int)(sl.rows / w), sl.row0 == 0,
+                           sl.row0 + sl.rows == n, &ok, s));
+  rec->w = (double)w;
+  rec->edges_ok = ok ? 1.0 : 0.0;
+  rec->npat = (double)tab.size();
+  std::copy(tab.begin(), tab.end(), rec->tab);
+  return 0;
+}
+
+// Decides temporal blocking from every rank's record (identical on every rank): one W, the
+// grid rows whole per slab, every slab at least kTbRows rows (each neighbour's halo comes
+// from one slab), clean edges, and at most kRowDictMax patterns in the union of the tables
+// (in rank order).  map[g][c]: rank g's code c in the union.
+bool tb_decide(const std::vector<TbRecord>& recs, const std::vector<int64_t>& rows, std::vector<StencilPattern>& table,
+               std::vector<std::vector<uint8_t>>& map) {
+  const int G = (int)recs.size();
+  const double w = recs[0].w;
+  if (w <= 0) return false;
+  for (int g = 0; g < G; ++g)
+    if (recs[g].w != w || recs[g].edges_ok != 1.0 || rows[g] < kTbRows * (int64_t)w) return false;
+  table.clear();
+  map.assign(G, std::vector<uint8_t>(kRowDictMax, 0));
+  for (int g = 0; g < G; ++g)
+    for (int c = 0; c < (int)recs[g].npat; ++c) {
+      int found = -1;
+      for (size_t i = 0; i < table.size() && found < 0; ++i)
+        if (std::memcmp(&table[i], &recs[g].tab[c], sizeof(StencilPattern)) == 0) found = (int)i;
+      if (found < 0) {
+        if (table.size() >= (size_t)kRowDictMax) return false;
+        found = (int)table.size();
+        table.push_back(recs[g].tab[c]);
+      }
+      map[g][c] = (uint8_t)found;
+    }
+  return true;
+}
+
+__global__ void remap_codes_kernel(const uint8_t* __restrict__ in, int64_t count, const uint8_t* __restrict__ lut,
+                                   uint8_t* __restrict__ out) {
+  __shared__ uint8_t l[kRowDictMax];
+  for (int i = threadIdx.x; i < kRowDictMax; i += blockDim.x) l[i] = lut[i];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = l[in[i]];
+}
+
+// The slab's extended-grid buffers and its own codes in the union table.
+int tb_setup_slab(Slab& sl, int64_t n, int W, const std::vector<uint8_t>& lut, cudaStream_t s) {
+  sl.tb = true;
+  sl.tbW = W;
+  sl.tb_lo = sl.row0 > 0 ? (int64_t)kTbRows * W : 0;
+  sl.tb_hi = sl.row0 + sl.rows < n ? (int64_t)kTbRows * W : 0;
+  const int64_t len = sl.tb_len();
+  NNB_TRY(sl.tb_mem.alloc(sizeof(double) * 6 * len + len + kRowDictMax + 64, s));
+  double* d = sl.tb_mem.as<double>();
+  for (int i = 0; i < 6; ++i) sl.tb_ext[i] = d + i * len;
+  NNB_CUDA(cudaMemsetAsync(d, 0, sizeof(double) * 6 * len, s));
+  sl.tb_code = reinterpret_cast<uint8_t*>(d + 6 * len);
+  uint8_t* lut_d = sl.tb_code + len;
+  NNB_CUDA(cudaMemsetAsync(sl.tb_code, 0, len, s));
+  NNB_CUDA(cudaMemcpyAsync(lut_d, lut.data(), kRowDictMax, cudaMemcpyHostToDevice, s));
+  remap_codes_kernel<<<std::max<int64_t>(1, std::min<int64_t>(1184, (sl.rows + 255) / 256)), 256, 0, s>>>(
+      sl.rcode, sl.rows, lut_d, sl.tb_code + sl.tb_lo);
+  count_launch();
+  NNB_CUDA(cudaStreamSynchronize(s));  // the LUT is a host vector's copy
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// The temporal-blocked factorized solve over row slabs: per pass (up to kTbRows
+// applications, sparse_stencil.cu) the kTbRows·W halo cells of its input are exchanged
+// once, then each slab runs the pass over its extended grid; the halo rows' values go
+// stale from the outside in, one row per application, never reaching the slab's own rows.
+// Each own row is computed as in the single-GPU pass (bitwise the same inputs), so x stays
+// bit-identical.  `exchange(e)` fills every local slab's halo of tb_ext[e].
+template <class Exchange>
+int run_slabs_tb(std::vector<Slab*>& slabs, const StencilPattern* table, int npat, int s_factors, double theta,
+                 std::vector<double*>& x_own, Exchange exchange, cudaStream_t s) {
+  const int kmax = stencil_max_steps();
+  int zcur = 4, zi = 0;  // Z starts as B (tb_ext[4])
+  for (int f = 0; f < s_factors; ++f) {
+    int64_t left = int64_t(1) << f;
+    int tin = zcur, ti = 0;
+    while (left > 0) {
+      const int steps = (int)std::min<int64_t>(kmax, left);
+      left -= steps;
+      const int mode = left > 0 ? kInner : (f == s_factors - 1 ? kFinal : kFactorEnd);
+      const int out = mode == kInner ? ti : (mode == kFinal ? 5 : 2 + zi);
+      NNB_TRY(exchange(tin));
+      for (Slab* sl : slabs)
+        NNB_TRY(stencil_pass(sl->tb_ext[tin], sl->tb_code, sl->tb_ext[zcur], sl->tb_ext[out], table, npat, sl->tbW,
+                             (int)(sl->tb_len() / sl->tbW), steps, mode, theta, sl->flags + f, s));
+      if (mode == kInner) {
+        tin = ti;
+        ti ^= 1;
+      } else if (mode == kFactorEnd) {
+        zcur = 2 + zi;
+        zi ^= 1;
+      }
+    }
+  }
+  for (size_t g = 0; g < slabs.size(); ++g)
+    NNB_CUDA(cudaMemcpyAsync(x_own[g], slabs[g]->tb_ext[5] + slabs[g]->tb_lo, sizeof(double) * slabs[g]->rows,
+                             cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
 
 // The slab's rows in 1-byte codes when the operator allows (sparse.cu build_pair_dict /
 // build_row_dict): the gathers stay r + diag_off + delta into the extended vector.
@@ -304,6 +473,8 @@ struct nnb_sparse_plan {
   int64_t n = 0, k = 0;
   Slab sl;
   DevBuf csr;
+  DevBuf tb_table;  // the union pattern table when the slabs run temporal-blocked passes
+  int tb_npat = 0;
   cudaEvent_t ready = nullptr, landed = nullptr;
   ~nnb_sparse_plan() {
     if (ready) cudaEventDestroy(ready);
@@ -340,7 +511,12 @@ int nnb_sparse_plan_create(nnb_comm_t comm, const int64_t* row_ptr, const int32_
     val_d = reinterpret_cast<const double*>(b + sizeof(int64_t) * (sl.rows + 1)) - base;
     col_d = reinterpret_cast<const int32_t*>(b + sizeof(int64_t) * (sl.rows + 1) + sizeof(double) * nnz) - base;
   }
+  if (trace_on()) {
+    trace_reset();
+    trace_mark(s, "plan start");
+  }
   NNB_TRY(setup_slab(sl, rp_d, col_d, val_d, k, s));
+  trace_mark(s, "slab setup");
   // halo sizes of every rank (each rank sends its neighbours what they need)
   DevBuf hx;
   NNB_TRY(hx.alloc(sizeof(int64_t) * 2 * (G + 1), s));
@@ -359,6 +535,46 @@ int nnb_sparse_plan_create(nnb_comm_t comm, const int64_t* row_ptr, const int32_
   sl.send_next = me < G - 1 ? halos[2 * (me + 1)] : 0;
   NNB_CUDA(cudaEventCreateWithFlags(&plan->ready, cudaEventDisableTiming));
   NNB_CUDA(cudaEventCreateWithFlags(&plan->landed, cudaEventDisableTiming));
+  if (k == 1) {  // temporal blocking across the slabs: every rank's record, one decision
+    static_assert(sizeof(TbRecord) % sizeof(double) == 0, "record in doubles");
+    const size_t rd = sizeof(TbRecord) / sizeof(double);
+    DevBuf rb;
+    NNB_TRY(rb.alloc(sizeof(TbRecord) * (G + 1), s));
+    TbRecord mine_rec;
+    trace_mark(s, "halo sizes");
+    NNB_TRY(tb_record(sl, n, &mine_rec, s));
+    trace_mark(s, "tb record");
+    NNB_CUDA(cudaMemcpyAsync(rb.as<TbRecord>() + G, &mine_rec, sizeof(TbRecord), cudaMemcpyHostToDevice, s));
+    NNB_NCCL2(nccl_allgather(rb.as<TbRecord>() + G, rb.as<TbRecord>(), rd, comm, s));
+    std::vector<TbRecord> recs(G);
+    NNB_CUDA(cudaMemcpyAsync(recs.data(), rb.p, sizeof(TbRecord) * G, cudaMemcpyDeviceToHost, s));
+    NNB_CUDA(cudaStreamSynchronize(s));
+    std::vector<StencilPattern> table;
+    std::vector<std::vector<uint8_t>> map;
+    if (tb_decide(recs, rs, table, map)) {
+      const int W = (int)recs[0].w;
+      NNB_TRY(tb_setup_slab(sl, n, W, map[me], s));
+      NNB_TRY(plan->tb_table.alloc(sizeof(StencilPattern) * table.size(), s));
+      NNB_CUDA(cudaMemcpyAsync(plan->tb_table.p, table.data(), sizeof(StencilPattern) * table.size(),
+                               cudaMemcpyHostToDevice, s));
+      plan->tb_npat = (int)table.size();
+      // the neighbours' edge codes into the halo rows (kTbRows·W bytes = W doubles each way)
+      const size_t hw = (size_t)kTbRows * W / sizeof(double);
+      NNB_NCCL2(nccl_group(true));
+      if (me > 0) {
+        NNB_NCCL2(nccl_send(sl.tb_code + sl.tb_lo, hw, me - 1, comm, s));
+        NNB_NCCL2(nccl_recv(sl.tb_code, hw, me - 1, comm, s));
+      }
+      if (me < G - 1) {
+        NNB_NCCL2(nccl_send(sl.tb_code + sl.tb_lo + sl.rows - (int64_t)kTbRows * W, hw, me + 1, comm, s));
+        NNB_NCCL2(nccl_recv(sl.tb_code + sl.tb_lo + sl.rows, hw, me + 1, comm, s));
+      }
+      NNB_NCCL2(nccl_group(false));
+      NNB_CUDA(cudaStreamSynchronize(s));
+    }
+    trace_mark(s, "tb setup");
+  }
+  trace_dump();
   *plan_out = plan.release();
   return 0;
 }
@@ -381,11 +597,34 @@ int nnb_sparse_plan_solve(nnb_sparse_plan_t plan, const double* B_rows, int64_t 
   Slab& sl = plan->sl;
   NNB_CUDA(cudaMemsetAsync(sl.flags, 0, sizeof(int) * 64, s));
   // Z = B in the extended layout
-  NNB_CUDA(cudaMemcpyAsync(sl.ext[4] + sl.h_lo * k, B_rows, sizeof(double) * sl.rows * k, cudaMemcpyDefault, s));
+  if (sl.tb)
+    NNB_CUDA(cudaMemcpyAsync(sl.tb_ext[4] + sl.tb_lo, B_rows, sizeof(double) * sl.rows, cudaMemcpyDefault, s));
+  else
+    NNB_CUDA(cudaMemcpyAsync(sl.ext[4] + sl.h_lo * k, B_rows, sizeof(double) * sl.rows * k, cudaMemcpyDefault, s));
   Out x;
   NNB_TRY(x.prepare(X_rows, (size_t)(sl.rows * k), s));
   std::vector<Slab*> slabs{&sl};
   std::vector<double*> xo{x.d};
+  auto exchange_tb = [&](int e) -> int {  // kTbRows·W cells each way, once per pass
+    if (G == 1) return 0;
+    double* ext = sl.tb_ext[e];
+    const size_t hw = (size_t)kTbRows * sl.tbW;
+    NNB_CUDA(cudaEventRecord(plan->ready, s));
+    NNB_CUDA(cudaStreamWaitEvent(comm->cs, plan->ready, 0));
+    NNB_NCCL2(nccl_group(true));
+    if (me > 0) {
+      NNB_NCCL2(nccl_send(ext + sl.tb_lo, hw, me - 1, comm, comm->cs));
+      NNB_NCCL2(nccl_recv(ext, hw, me - 1, comm, comm->cs));
+    }
+    if (me < G - 1) {
+      NNB_NCCL2(nccl_send(ext + sl.tb_lo + sl.rows - hw, hw, me + 1, comm, comm->cs));
+      NNB_NCCL2(nccl_recv(ext + sl.tb_lo + sl.rows, hw, me + 1, comm, comm->cs));
+    }
+    NNB_NCCL2(nccl_group(false));
+    NNB_CUDA(cudaEventRecord(plan->landed, comm->cs));
+    NNB_CUDA(cudaStreamWaitEvent(s, plan->landed, 0));
+    return 0;
+  };
   auto exchange = [&](int e) -> int {
     if (G == 1) return 0;
     double* ext = sl.ext[e];
@@ -409,7 +648,13 @@ int nnb_sparse_plan_solve(nnb_sparse_plan_t plan, const double* B_rows, int64_t 
     if (G > 1) NNB_CUDA(cudaStreamWaitEvent(s, plan->landed, 0));
     return 0;
   };
-  int st = run_slabs(slabs, k, s_factors, theta, xo, exchange, wait, s);
+  int st = sl.tb ? run_slabs_tb(slabs, plan->tb_table.as<StencilPattern>(), plan->tb_npat, s_factors, theta, xo,
+                                exchange_tb, s)
+                 : run_slabs(slabs, k, s_factors, theta, xo, exchange, wait, s);
+  if (sl.tb) {
+    set_sparse_format("row-dictionary-stencil-tb");
+    set_sparse_bytes_per_nnz(1);
+  }
   // divergence flags of every rank (so every rank reports the same factor)
   std::vector<int> all(64, 0);
   if (st == 0 && G > 1) {
@@ -481,8 +726,47 @@ int nnb_sparse_factorized_sharded_emulated_d(const int64_t* row_ptr, const int32
     Slab& sl = store[g];
     if ((g > 0 && sl.h_lo > store[g - 1].rows) || (g < world - 1 && sl.h_hi > store[g + 1].rows))
       return fail(NNB_ERR_DOMAIN, "sharded sparse: operator bandwidth exceeds a neighbour slab (halo wider than one rank)");
-    NNB_CUDA(cudaMemcpyAsync(sl.ext[4] + sl.h_lo * k, B + sl.row0 * k, sizeof(double) * sl.rows * k,
-                             cudaMemcpyDefault, s));
+  }
+  // temporal blocking across the slabs: the same records and decision as the NCCL plan
+  bool tb = false;
+  DevBuf tb_table;
+  int tb_npat = 0;
+  if (k == 1) {
+    std::vector<TbRecord> recs(world);
+    std::vector<int64_t> rows(world);
+    for (int g = 0; g < world; ++g) {
+      NNB_TRY(tb_record(store[g], n, &recs[g], s));
+      rows[g] = store[g].rows;
+    }
+    std::vector<StencilPattern> table;
+    std::vector<std::vector<uint8_t>> map;
+    tb = tb_decide(recs, rows, table, map);
+    if (tb) {
+      const int W = (int)recs[0].w;
+      for (int g = 0; g < world; ++g) NNB_TRY(tb_setup_slab(store[g], n, W, map[g], s));
+      NNB_TRY(tb_table.alloc(sizeof(StencilPattern) * table.size(), s));
+      NNB_CUDA(cudaMemcpyAsync(tb_table.p, table.data(), sizeof(StencilPattern) * table.size(),
+                               cudaMemcpyHostToDevice, s));
+      tb_npat = (int)table.size();
+      const int64_t hw = (int64_t)kTbRows * W;
+      for (int g = 0; g < world; ++g) {  // the neighbours' edge codes into the halo rows
+        Slab& sl = store[g];
+        if (g > 0)
+          NNB_CUDA(cudaMemcpyAsync(sl.tb_code, store[g - 1].tb_code + store[g - 1].tb_lo + store[g - 1].rows - hw, hw,
+                                   cudaMemcpyDeviceToDevice, s));
+        if (g < world - 1)
+          NNB_CUDA(cudaMemcpyAsync(sl.tb_code + sl.tb_lo + sl.rows, store[g + 1].tb_code + store[g + 1].tb_lo, hw,
+                                   cudaMemcpyDeviceToDevice, s));
+      }
+    }
+  }
+  for (int g = 0; g < world; ++g) {
+    Slab& sl = store[g];
+    if (tb)
+      NNB_CUDA(cudaMemcpyAsync(sl.tb_ext[4] + sl.tb_lo, B + sl.row0, sizeof(double) * sl.rows, cudaMemcpyDefault, s));
+    else
+      NNB_CUDA(cudaMemcpyAsync(sl.ext[4] + sl.h_lo * k, B + sl.row0 * k, sizeof(double) * sl.rows * k,
+                               cudaMemcpyDefault, s));
   }
   Out x;
   NNB_TRY(x.prepare(X_out, (size_t)(n * k), s));
@@ -505,7 +789,29 @@ int nnb_sparse_factorized_sharded_emulated_d(const int64_t* row_ptr, const int32
     return 0;
   };
   auto wait = [](size_t) -> int { return 0; };
-  int st = run_slabs(slabs, k, s_factors, theta, xo, exchange, wait, s);
+  auto exchange_tb = [&](int e) -> int {  // device copies of the neighbours' edge rows
+    for (int g = 0; g < world; ++g) {
+      Slab& sl = store[g];
+      const int64_t hw = (int64_t)kTbRows * sl.tbW;
+      if (g > 0) {
+        const Slab& pv = store[g - 1];
+        NNB_CUDA(cudaMemcpyAsync(sl.tb_ext[e], pv.tb_ext[e] + pv.tb_lo + pv.rows - hw, sizeof(double) * hw,
+                                 cudaMemcpyDeviceToDevice, s));
+      }
+      if (g < world - 1) {
+        const Slab& nx = store[g + 1];
+        NNB_CUDA(cudaMemcpyAsync(sl.tb_ext[e] + sl.tb_lo + sl.rows, nx.tb_ext[e] + nx.tb_lo, sizeof(double) * hw,
+                                 cudaMemcpyDeviceToDevice, s));
+      }
+    }
+    return 0;
+  };
+  int st = tb ? run_slabs_tb(slabs, tb_table.as<StencilPattern>(), tb_npat, s_factors, theta, xo, exchange_tb, s)
+              : run_slabs(slabs, k, s_factors, theta, xo, exchange, wait, s);
+  if (tb) {
+    set_sparse_format("row-dictionary-stencil-tb");
+    set_sparse_bytes_per_nnz(1);
+  }
   if (st) return st;
   int ff = -1;
   st = collect_flags(slabs, s_factors, &ff, s);

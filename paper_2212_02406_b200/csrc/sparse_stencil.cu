@@ -196,13 +196,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // rows on the grid's edges whose pattern reaches across it (x wrap or out of range)
+// (a row slab checks its top / bottom rows only where they are the grid's: check_top/bottom)
 __global__ void stencil_edge_check(const uint8_t* __restrict__ rcode, const StPat* __restrict__ pats, int W, int H,
-                                   int* __restrict__ bad) {
+                                   int* __restrict__ bad, int check_top, int check_bottom) {
   const int64_t per = 2LL * W + 2LL * H;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < per; i += (int64_t)gridDim.x * blockDim.x) {
     int x, y, forbid;
-    if (i < W) { x = (int)i; y = 0; forbid = 1; }                        // top row: no −W
-    else if (i < 2LL * W) { x = (int)(i - W); y = H - 1; forbid = 16; }  // bottom row: no +W
+    if (i < W) { x = (int)i; y = 0; forbid = check_top ? 1 : 0; }                        // top row: no −W
+    else if (i < 2LL * W) { x = (int)(i - W); y = H - 1; forbid = check_bottom ? 16 : 0; }  // bottom row: no +W
     else if (i < 2LL * W + H) { x = 0; y = (int)(i - 2LL * W); forbid = 2; }  // left column: no −1
     else { x = W - 1; y = (int)(i - 2LL * W - H); forbid = 8; }          // right column: no +1
     const int m = pats[rcode[(int64_t)y * W + x]].mask;
@@ -212,10 +213,12 @@ __global__ void stencil_edge_check(const uint8_t* __restrict__ rcode, const StPa
 
 }  // namespace
 
-int stencil_plan(int64_t n, const uint8_t* rcode, const double2* pat, const uint8_t* plen, int npat, int width,
-                 DevBuf& table, int* W_out, int* H_out, bool* ok, cudaStream_t s) {
-  *ok = false;
-  if (npat < 1 || npat > kRowDictMax || width < 1 || width > kEllMaxWidth || n < 4) return 0;
+int stencil_patterns(const double2* pat, const uint8_t* plen, int npat, int width, int64_t* W_out,
+                     std::vector<StencilPattern>& tab, cudaStream_t s) {
+  static_assert(sizeof(StencilPattern) == sizeof(StPat), "host and device pattern layouts");
+  *W_out = 0;
+  tab.clear();
+  if (npat < 1 || npat > kRowDictMax || width < 1 || width > kEllMaxWidth) return 0;
   std::vector<double2> hp((size_t)npat * width);
   std::vector<uint8_t> hl(npat);
   NNB_CUDA(cudaMemcpyAsync(hp.data(), pat, sizeof(double2) * hp.size(), cudaMemcpyDeviceToHost, s));
@@ -231,10 +234,10 @@ int stencil_plan(int64_t n, const uint8_t* rcode, const double2* pat, const uint
         w = std::llabs(d);
       }
     }
-  if (w < 4 || w % 4 != 0 || n % w != 0 || w > INT32_MAX || n / w > INT32_MAX) return 0;
-  std::vector<StPat> tab(npat);
+  if (w < 4 || w % 4 != 0 || w > INT32_MAX) return 0;
+  std::vector<StencilPattern> t(npat);
   for (int p = 0; p < npat; ++p) {
-    StPat sp{};
+    StencilPattern sp{};
     int last_dir = -1;
     for (int i = 0; i < hl[p]; ++i) {
       int64_t d;
@@ -245,35 +248,82 @@ int stencil_plan(int64_t n, const uint8_t* rcode, const double2* pat, const uint
       sp.v[dir] = hp[(size_t)p * width + i].x;
       sp.mask |= 1 << dir;
     }
-    tab[p] = sp;
+    t[p] = sp;
   }
-  NNB_TRY(table.alloc(sizeof(StPat) * npat + sizeof(int), s));
-  NNB_CUDA(cudaMemcpyAsync(table.p, tab.data(), sizeof(StPat) * npat, cudaMemcpyHostToDevice, s));
-  int* bad = reinterpret_cast<int*>(table.as<StPat>() + npat);
-  NNB_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
-  const int W = (int)w, H = (int)(n / w);
-  stencil_edge_check<<<148, 256, 0, s>>>(rcode, table.as<StPat>(), W, H, bad);
+  tab.swap(t);
+  *W_out = w;
+  return 0;
+}
+
+int stencil_edges_ok(const uint8_t* rcode, const StencilPattern* table_dev, int W, int H, bool top, bool bottom,
+                     bool* ok, cudaStream_t s) {
+  DevBuf b;
+  NNB_TRY(b.alloc(sizeof(int), s));
+  NNB_CUDA(cudaMemsetAsync(b.p, 0, sizeof(int), s));
+  stencil_edge_check<<<148, 256, 0, s>>>(rcode, reinterpret_cast<const StPat*>(table_dev), W, H, b.as<int>(),
+                                         top ? 1 : 0, bottom ? 1 : 0);
   count_launch();
   int hbad = 1;
-  NNB_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaMemcpyAsync(&hbad, b.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   NNB_CUDA(cudaStreamSynchronize(s));
-  if (hbad) return 0;
+  *ok = hbad == 0;
+  return 0;
+}
+
+int stencil_plan(int64_t n, const uint8_t* rcode, const double2* pat, const uint8_t* plen, int npat, int width,
+                 DevBuf& table, int* W_out, int* H_out, bool* ok, cudaStream_t s) {
+  *ok = false;
+  if (n < 4) return 0;
+  int64_t w = 0;
+  std::vector<StencilPattern> tab;
+  NNB_TRY(stencil_patterns(pat, plen, npat, width, &w, tab, s));
+  if (!w || n % w != 0 || n / w > INT32_MAX) return 0;
+  NNB_TRY(table.alloc(sizeof(StPat) * npat, s));
+  NNB_CUDA(cudaMemcpyAsync(table.p, tab.data(), sizeof(StPat) * npat, cudaMemcpyHostToDevice, s));
+  const int W = (int)w, H = (int)(n / w);
+  bool eok = false;
+  NNB_TRY(stencil_edges_ok(rcode, table.as<StencilPattern>(), W, H, true, true, &eok, s));
+  if (!eok) return 0;
   *W_out = W;
   *H_out = H;
   *ok = true;
   return 0;
 }
 
-int stencil_factors(const uint8_t* rcode, const DevBuf& table, int npat, int W, int H, const double* B,
-                    int s_factors, double theta, double* X, double* z[2], double* tb[2], int* flags,
-                    int64_t* bytes_moved, cudaStream_t s) {
+int stencil_pass(const double* tin, const uint8_t* rcode, const double* zold, double* out,
+                 const StencilPattern* table_dev, int npat, int W, int H, int steps, int mode, double theta, int* flag,
+                 cudaStream_t s) {
   NNB_TRY(ensure_smem<stencil_tb_kernel<kInner>>(kSmem));
   NNB_TRY(ensure_smem<stencil_tb_kernel<kFactorEnd>>(kSmem));
   NNB_TRY(ensure_smem<stencil_tb_kernel<kFinal>>(kSmem));
   const dim3 grid((unsigned)((W + kTX - 1) / kTX), (unsigned)((H + kTY - 1) / kTY));
-  const StPat* pats = table.as<StPat>();
+  const StPat* pats = reinterpret_cast<const StPat*>(table_dev);
+  switch (mode) {
+    case kInner:
+      stencil_tb_kernel<kInner><<<grid, kThreads, kSmem, s>>>(tin, rcode, zold, out, pats, npat, W, H, steps, theta,
+                                                              flag);
+      break;
+    case kFactorEnd:
+      stencil_tb_kernel<kFactorEnd><<<grid, kThreads, kSmem, s>>>(tin, rcode, zold, out, pats, npat, W, H, steps,
+                                                                  theta, flag);
+      break;
+    default:
+      stencil_tb_kernel<kFinal><<<grid, kThreads, kSmem, s>>>(tin, rcode, zold, out, pats, npat, W, H, steps, theta,
+                                                              flag);
+  }
+  count_launch();
+  NNB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int stencil_max_steps() { return kS; }
+double stencil_region_ratio() { return (double)kRX * kRY / ((double)kTX * kTY); }
+
+int stencil_factors(const uint8_t* rcode, const DevBuf& table, int npat, int W, int H, const double* B,
+                    int s_factors, double theta, double* X, double* z[2], double* tb[2], int* flags,
+                    int64_t* bytes_moved, cudaStream_t s) {
   const double n = (double)W * H;
-  const double halo = (double)kRX * kRY / ((double)kTX * kTY);  // region cells read per output cell
+  const double halo = stencil_region_ratio();  // region cells read per output cell
   double moved = 0.0;
   const double* zcur = B;
   int zi = 0;
@@ -286,21 +336,8 @@ int stencil_factors(const uint8_t* rcode, const DevBuf& table, int npat, int W, 
       left -= steps;
       const int mode = left > 0 ? kInner : (f == s_factors - 1 ? kFinal : kFactorEnd);
       double* out = mode == kInner ? tb[ti] : (mode == kFinal ? X : z[zi]);
-      switch (mode) {
-        case kInner:
-          stencil_tb_kernel<kInner><<<grid, kThreads, kSmem, s>>>(tin, rcode, zcur, out, pats, npat, W, H, steps,
-                                                                  theta, flags + f);
-          break;
-        case kFactorEnd:
-          stencil_tb_kernel<kFactorEnd><<<grid, kThreads, kSmem, s>>>(tin, rcode, zcur, out, pats, npat, W, H,
-                                                                      steps, theta, flags + f);
-          break;
-        default:
-          stencil_tb_kernel<kFinal><<<grid, kThreads, kSmem, s>>>(tin, rcode, zcur, out, pats, npat, W, H, steps,
-                                                                  theta, flags + f);
-      }
-      count_launch();
-      NNB_CUDA(cudaGetLastError());
+      NNB_TRY(stencil_pass(tin, rcode, zcur, out, table.as<StencilPattern>(), npat, W, H, steps, mode, theta,
+                           flags + f, s));
       moved += n * (halo * (8.0 + 1.0) + 8.0 + (mode == kInner ? 0.0 : 8.0));
       if (mode == kInner) {
         tin = tb[ti];

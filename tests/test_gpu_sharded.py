@@ -75,13 +75,30 @@ def test_sparse_sharded_emulated_bitexact(ref, world):
     csr = nnb.Csr(rp, col, val, n=10000)
     norm = nnb.Normalization(theta=0.2, valid=True)
     xs, cnt = nnb.solve_sparse_factorized_sharded_emulated(csr, b, 63, norm, world)
-    assert nnb.sparse_last_format() == "row-dictionary"  # each slab's rows in 1-byte pattern codes
+    # each slab's rows in 1-byte pattern codes; one slab (whole grid rows) runs temporal-blocked
+    # passes, the other partitions (16-row units, not whole 100-cell grid rows) one launch per
+    # application
+    assert nnb.sparse_last_format() == ("row-dictionary-stencil-tb" if world == 1 else "row-dictionary")
     xr, cr, _ = ref.sparse_factorized(rp, col, val, b, 63, 0.2)
     assert cnt == cr == 63 and np.array_equal(xs, xr.real)
     b2 = np.random.default_rng(world).standard_normal((10000, 2))  # two right-hand sides: int16 deltas
     xs2, _ = nnb.solve_sparse_factorized_sharded_emulated(csr, b2, 15, norm, world)
     xr2, _, _ = ref.sparse_factorized(rp, col, val, b2, 15, 0.2)
     assert np.array_equal(xs2, xr2.real)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_sparse_sharded_temporal_blocking_bitexact(ref, world):
+    """Slabs of whole grid rows (64×64 grid: 32, 16 or 8 grid rows per slab) run the
+    temporal-blocked passes with an 8-row halo exchanged once per pass; x bit-identical to the
+    reference.  World 3 (slabs not whole grid rows) keeps one launch per application."""
+    rp, col, val = W.laplacian_5pt(64)
+    b = W.rhs(4096, seed=20 + world)
+    xs, cnt = nnb.solve_sparse_factorized_sharded_emulated(nnb.Csr(rp, col, val, n=4096), b, 63,
+                                                           nnb.Normalization(theta=0.2, valid=True), world)
+    assert nnb.sparse_last_format() == ("row-dictionary" if world == 3 else "row-dictionary-stencil-tb")
+    xr, cr, _ = ref.sparse_factorized(rp, col, val, b, 63, 0.2)
+    assert cnt == cr == 63 and np.array_equal(xs, xr.real)
 
 
 def test_sparse_sharded_emulated_full_size_matches_single():
@@ -97,7 +114,7 @@ def test_sparse_sharded_emulated_full_size_matches_single():
     x8, _ = nnb.solve_sparse_factorized_sharded_emulated(csr, b, 63, norm, 8)
     torch.cuda.synchronize()
     assert torch.equal(x1, x8)
-    assert nnb.sparse_last_format() == "row-dictionary"
+    assert nnb.sparse_last_format() == "row-dictionary-stencil-tb"  # 8 slabs of 512 grid rows
 
 
 def test_sparse_sharded_nccl_world1(ref):
