@@ -224,11 +224,12 @@ int tb_setup_slab(Slab& sl, int64_t n, int W, const std::vector<uint8_t>& lut, c
 // once, then each slab runs the pass over its extended grid; the halo rows' values go
 // stale from the outside in, one row per application, never reaching the slab's own rows.
 // Each own row is computed as in the single-GPU pass (bitwise the same inputs), so x stays
-// bit-identical.  `exchange(e)` fills every local slab's halo of tb_ext[e].
-template <class Exchange>
+// bit-identical.  The tile rows whose region stays clear of the halo rows run while the
+// exchange is in flight (`exchange(e)` starts it, `wait_halo()` orders the rest after it).
+template <class Exchange, class WaitHalo>
 int run_slabs_tb(std::vector<Slab*>& slabs, const StencilPattern* table, int npat, int s_factors, double theta,
-                 std::vector<double*>& x_own, Exchange exchange, cudaStream_t s) {
-  const int kmax = stencil_max_steps();
+                 std::vector<double*>& x_own, Exchange exchange, WaitHalo wait_halo, cudaStream_t s) {
+  const int kmax = stencil_max_steps(), ty = stencil_tile_rows();
   int zcur = 4, zi = 0;  // Z starts as B (tb_ext[4])
   for (int f = 0; f < s_factors; ++f) {
     int64_t left = int64_t(1) << f;
@@ -239,9 +240,34 @@ int run_slabs_tb(std::vector<Slab*>& slabs, const StencilPattern* table, int npa
       const int mode = left > 0 ? kInner : (f == s_factors - 1 ? kFinal : kFactorEnd);
       const int out = mode == kInner ? ti : (mode == kFinal ? 5 : 2 + zi);
       NNB_TRY(exchange(tin));
-      for (Slab* sl : slabs)
-        NNB_TRY(stencil_pass(sl->tb_ext[tin], sl->tb_code, sl->tb_ext[zcur], sl->tb_ext[out], table, npat, sl->tbW,
-                             (int)(sl->tb_len() / sl->tbW), steps, mode, theta, sl->flags + f, s));
+      struct Range {
+        int a, b;
+      };
+      std::vector<Range> rest;
+      for (Slab* sl : slabs) {
+        const int W = sl->tbW, H = (int)(sl->tb_len() / W);
+        const int hlo = (int)(sl->tb_lo / W), hhi = (int)(sl->tb_hi / W), tiles = (H + ty - 1) / ty;
+        // tile row t reads region rows [t·ty − kmax, t·ty + ty + kmax)
+        int t0 = 0, t1 = tiles;
+        if (hlo > 0) t0 = (hlo + kmax + ty - 1) / ty;
+        if (hhi > 0) {
+          const int num = H - hhi - ty - kmax;  // the last interior tile row t has t·ty <= num
+          t1 = num < 0 ? 0 : num / ty + 1;
+        }
+        if (t0 > t1) t0 = t1 = 0;
+        NNB_TRY(stencil_pass(sl->tb_ext[tin], sl->tb_code, sl->tb_ext[zcur], sl->tb_ext[out], table, npat, W, H,
+                             steps, mode, theta, sl->flags + f, s, t0, t1));
+        rest.push_back({t0, t1});
+      }
+      NNB_TRY(wait_halo());
+      for (size_t g = 0; g < slabs.size(); ++g) {
+        Slab* sl = slabs[g];
+        const int W = sl->tbW, H = (int)(sl->tb_len() / W);
+        NNB_TRY(stencil_pass(sl->tb_ext[tin], sl->tb_code, sl->tb_ext[zcur], sl->tb_ext[out], table, npat, W, H,
+                             steps, mode, theta, sl->flags + f, s, 0, rest[g].a));
+        NNB_TRY(stencil_pass(sl->tb_ext[tin], sl->tb_code, sl->tb_ext[zcur], sl->tb_ext[out], table, npat, W, H,
+                             steps, mode, theta, sl->flags + f, s, rest[g].b, -1));
+      }
       if (mode == kInner) {
         tin = ti;
         ti ^= 1;
@@ -622,7 +648,10 @@ int nnb_sparse_plan_solve(nnb_sparse_plan_t plan, const double* B_rows, int64_t 
     }
     NNB_NCCL2(nccl_group(false));
     NNB_CUDA(cudaEventRecord(plan->landed, comm->cs));
-    NNB_CUDA(cudaStreamWaitEvent(s, plan->landed, 0));
+    return 0;
+  };
+  auto wait_tb = [&]() -> int {
+    if (G > 1) NNB_CUDA(cudaStreamWaitEvent(s, plan->landed, 0));
     return 0;
   };
   auto exchange = [&](int e) -> int {
@@ -649,7 +678,7 @@ int nnb_sparse_plan_solve(nnb_sparse_plan_t plan, const double* B_rows, int64_t 
     return 0;
   };
   int st = sl.tb ? run_slabs_tb(slabs, plan->tb_table.as<StencilPattern>(), plan->tb_npat, s_factors, theta, xo,
-                                exchange_tb, s)
+                                exchange_tb, wait_tb, s)
                  : run_slabs(slabs, k, s_factors, theta, xo, exchange, wait, s);
   if (sl.tb) {
     set_sparse_format("row-dictionary-stencil-tb");
@@ -806,7 +835,9 @@ int nnb_sparse_factorized_sharded_emulated_d(const int64_t* row_ptr, const int32
     }
     return 0;
   };
-  int st = tb ? run_slabs_tb(slabs, tb_table.as<StencilPattern>(), tb_npat, s_factors, theta, xo, exchange_tb, s)
+  auto wait_tb = []() -> int { return 0; };
+  int st = tb ? run_slabs_tb(slabs, tb_table.as<StencilPattern>(), tb_npat, s_factors, theta, xo, exchange_tb, wait_tb,
+                             s)
               : run_slabs(slabs, k, s_factors, theta, xo, exchange, wait, s);
   if (tb) {
     set_sparse_format("row-dictionary-stencil-tb");
