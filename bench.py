@@ -342,6 +342,7 @@ def run_dense(args, world, rank):
         x_h.copy_(x)
         del a, x
         torch.cuda.empty_cache()
+        nnb.release_cached_memory()  # the legs above left the library's pool holding ≈100 GB
         a_np, x_np, xo_np = a_h.numpy(), x_h.numpy(), xo_h.numpy()
         if sharded:
             call = lambda: nnb.nn_chain_sharded(comm, a_np, n, x_np, p=p, max_iters=1, final_residual=False, out=xo_np)
@@ -367,7 +368,9 @@ def run_dense_emulated(nnb, torch, a, x, n, p, world, ms_single, k):
     """The `world`-rank sharded schedule as virtual ranks on this GPU, K nests in one call
     (as the headline's K-nest call), against the headline's per-nest time."""
     # warm: the schedule's residue buffers (≈35 GB at N=32768) come from the stream-ordered
-    # pool, which grows on the first call
+    # pool, which grows on the first call (after the other legs' buffers went back)
+    torch.cuda.empty_cache()
+    nnb.release_cached_memory()
     nnb.nn_chain_sharded_emulated(a, world, x, p=p, max_iters=1, final_residual=False)
     torch.cuda.synchronize()
     nnb.ozaki_stats(reset=True)

@@ -96,6 +96,9 @@ const char* nnb_last_error(void);
 int nnb_device_count(void);
 /* Launch count of this library's kernels since load (for bench gpu_launches). */
 uint64_t nnb_kernel_launches(void);
+/* Returns the library's cached work buffers (the current device's stream-ordered pool,
+ * kept across calls) to the driver, after a device synchronisation. */
+int nnb_release_cached_memory(void);
 
 /* Arithmetic mode of the calling thread.
  * NNB_ARITH_FAST (default): the faster of the two FP64-accurate product

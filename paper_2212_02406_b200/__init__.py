@@ -90,6 +90,7 @@ _SIGS = {
     "nnb_last_error": ([], C.c_char_p),
     "nnb_device_count": ([], C.c_int),
     "nnb_kernel_launches": ([], C.c_uint64),
+    "nnb_release_cached_memory": ([], C.c_int),
     "nnb_set_arithmetic": ([_i32], C.c_int),
     "nnb_get_arithmetic": ([], C.c_int32),
     "nnb_ozaki_moduli": ([_i64], C.c_int32),
@@ -179,6 +180,11 @@ def lib() -> C.CDLL:
 
 def exported_symbols() -> list[str]:
     return list(_SIGS)
+
+
+def release_cached_memory() -> None:
+    """Return libnnb's cached work buffers (its stream-ordered pool) to the driver."""
+    _check(lib().nnb_release_cached_memory())
 
 
 def kernel_launches() -> int:

@@ -293,6 +293,17 @@ int nnb_device_count(void) {
 }
 uint64_t nnb_kernel_launches(void) { return launches(); }
 
+int nnb_release_cached_memory(void) {
+  NNB_TRY(require_device());
+  int dev = 0;
+  NNB_CUDA(cudaGetDevice(&dev));
+  NNB_CUDA(cudaDeviceSynchronize());
+  cudaMemPool_t pool;
+  NNB_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  NNB_CUDA(cudaMemPoolTrimTo(pool, 0));
+  return 0;
+}
+
 int nnb_set_arithmetic(int32_t mode) {
   if (mode < NNB_ARITH_FAST || mode > NNB_ARITH_DMMA)
     return fail(NNB_ERR_DOMAIN, "nnb_set_arithmetic: unknown mode");
