@@ -379,16 +379,19 @@ def run_dense_emulated(nnb, torch, a, x, n, p, world, ms_single, k):
     torch.cuda.synchronize()
     nnb.ozaki_profile(False)
     oz = nnb.ozaki_stats(reset=True)
-    xs, _ = nnb.nn_chain(a, x, p=p, max_iters=k, final_residual=False)
+    # the single-GPU reference timed right after (same clocks: the power-capped int8 GEMM
+    # slows as the GPU warms over the legs, so the headline's own time is not the reference)
+    xs, rs_ = nnb.nn_chain(a, x, p=p, max_iters=k, final_residual=False)
     torch.cuda.synchronize()
     same = bool(torch.equal(torch.as_tensor(xe, device="cuda"), xs))
     del xe, xs
     torch.cuda.empty_cache()
     ms = re_.device_ms / k
+    ms_adj = rs_.device_ms / k
     return {"world": world, "nests": k, "ms_per_nest_all_ranks": round(ms, 2),
             "ms_per_rank_mean": round(ms / world, 2),
-            "single_gpu_ms_per_nest": round(ms_single, 2),
-            "compute_efficiency": round(ms_single / ms, 4),
+            "single_gpu_ms_per_nest": round(ms_adj, 2), "headline_ms_per_nest": round(ms_single, 2),
+            "compute_efficiency": round(ms_adj / ms, 4),
             "x_bit_identical_to_single_gpu": same,
             "kernels_ms_per_nest": {c: round(v["ms"] / k, 1) for c, v in oz.items()},
             "note": f"the {world}-rank row-sharded nest (int8-emulated products, residue-block ring) run as {world} "
@@ -773,11 +776,17 @@ def run_sparse(args, world, rank):
         e1.record()
         torch.cuda.synchronize()
         ms_e = e0.elapsed_time(e1) / 5
+        ms_sched = nnb.sparse_last_solve_ms()  # the last solve without its 8 slab setups
         emulated = {"world": 8, "ms_per_solve_all_ranks": round(ms_e, 3), "single_gpu_ms": round(ms, 3),
-                    "compute_efficiency": round(ms / ms_e, 4), "format": nnb.sparse_last_format(),
+                    "compute_efficiency": round(ms / ms_e, 4),
+                    "schedule_ms_all_ranks": round(ms_sched, 3),
+                    "schedule_efficiency": round(ms / ms_sched, 4) if ms_sched > 0 else None,
+                    "format": nnb.sparse_last_format(),
                     "x_bit_identical_to_single_gpu": bool(torch.equal(xe, x)),
                     "note": "row slabs of 512 grid rows, temporal-blocked passes with an 8-row halo exchanged once "
-                            "per pass (device copies here), one-shot solve incl. the slab setup"}
+                            "per pass (device copies here); compute_efficiency: one-shot solves incl. the 8 slab "
+                            "setups (run in parallel on 8 GPUs, one after another here); schedule_efficiency: the "
+                            "factor schedule alone (the single-GPU time includes its format pass)"}
     alg = 63 * sparse_bytes(n, col.size, 12)  # SURVEY §8(d) algorithmic bytes per solve: the work unit
     moved = 63 * (mat + 2 * n * 8)  # bytes of the consumed format (operator + t in + t out): the roofline
     gbs, moved_gbs = alg / (ms * 1e-3) / 1e9, moved / (ms * 1e-3) / 1e9

@@ -296,6 +296,9 @@ int64_t nnb_sparse_last_matrix_bytes(void);
  * "pair-dictionary-csr", "csr-int16-delta", "csr-int32", "csr-int64-offsets";
  * "" before any solve. */
 const char* nnb_sparse_last_format(void);
+/* Device time (ms, CUDA events) of the calling thread's last row-slab solve without its
+ * slab setup (the factor schedule and its halo exchanges); 0 before any. */
+double nnb_sparse_last_solve_ms(void);
 
 /* ---- contraction measurement (theta_trace's spectral estimate) ---------- */
 /* Power iteration on M^H M from the unit probe v0 (complex128, length n):

@@ -131,6 +131,7 @@ _SIGS = {
     "nnb_sparse_last_bytes_per_nnz": ([], C.c_int),
     "nnb_sparse_last_matrix_bytes": ([], C.c_int64),
     "nnb_sparse_last_format": ([], C.c_char_p),
+    "nnb_sparse_last_solve_ms": ([], C.c_double),
     "nnb_gaussian_stream": ([C.c_uint64, _i64, _dp], C.c_int),
     "nnb_householder_q_d": ([_dp, _i64, _dp, _dp], C.c_int),
     "nnb_householder_q_z": ([_dp, _i64, _dp, _dp], C.c_int),
@@ -865,6 +866,11 @@ def sparse_last_matrix_bytes() -> int:
 def sparse_last_format() -> str:
     """Name of the operator format the calling thread's last sparse solve consumed."""
     return lib().nnb_sparse_last_format().decode()
+
+
+def sparse_last_solve_ms() -> float:
+    """Device ms of the calling thread's last row-slab solve without its slab setup."""
+    return float(lib().nnb_sparse_last_solve_ms())
 
 
 def solve_sparse_factorized_sharded(comm: Comm, csr_rows: Csr, n: int, b_rows, gamma: int, norm: Normalization):

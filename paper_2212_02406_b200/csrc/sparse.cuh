@@ -115,10 +115,11 @@ int stencil_patterns(const double2* pat, const uint8_t* plen, int npat, int widt
 int stencil_edges_ok(const uint8_t* rcode, const StencilPattern* table_dev, int W, int H, bool top, bool bottom,
                      bool* ok, cudaStream_t s);
 // one temporal-blocked pass: `steps` (<= stencil_max_steps()) applications over a W×H grid
-// (tile rows [ty0, ty1) of the grid only; ty1 < 0: to the last)
+// Output tile rows [ty0, ty1) only (ty1 < 0: to the last) of the out_rows rows from row
+// y_off (out_rows < 0: all H); the grid's other rows are inputs only (a slab's halo rows).
 int stencil_pass(const double* tin, const uint8_t* rcode, const double* zold, double* out,
                  const StencilPattern* table_dev, int npat, int W, int H, int steps, int mode, double theta, int* flag,
-                 cudaStream_t s, int ty0 = 0, int ty1 = -1);
+                 cudaStream_t s, int ty0 = 0, int ty1 = -1, int y_off = 0, int out_rows = -1);
 int stencil_tile_rows();
 int stencil_max_steps();
 double stencil_region_ratio();

@@ -33,6 +33,30 @@
 namespace nnb {
 namespace sparse_detail {
 
+thread_local double g_last_solve_ms = 0.0;  // nnb_sparse_last_solve_ms
+
+// CUDA-event bracket of a solve's schedule on stream s
+struct SolveTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  explicit SolveTimer(cudaStream_t st) : s(st) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+  }
+  void stop() {
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    g_last_solve_ms = ms;
+  }
+  ~SolveTimer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
 #define NNB_NCCL2(x)                                                                             \
   do {                                                                                           \
     ncclResult_t _r = (x);                                                                       \
@@ -224,12 +248,16 @@ int tb_setup_slab(Slab& sl, int64_t n, int W, const std::vector<uint8_t>& lut, c
 // once, then each slab runs the pass over its extended grid; the halo rows' values go
 // stale from the outside in, one row per application, never reaching the slab's own rows.
 // Each own row is computed as in the single-GPU pass (bitwise the same inputs), so x stays
-// bit-identical.  The tile rows whose region stays clear of the halo rows run while the
-// exchange is in flight (`exchange(e)` starts it, `wait_halo()` orders the rest after it).
-template <class Exchange, class WaitHalo>
+// bit-identical.  With a real exchange (`bs` = the communication stream) the tile rows
+// whose region stays clear of the halo rows run on s while the exchange is in flight, and
+// the edge tile rows run on bs right behind the exchange — at its higher priority, filling
+// the interior launch's last wave — before s joins it (`join()`).  Without one (bs null:
+// the emulation's device copies) each slab's pass is one launch.
+template <class Exchange, class Join>
 int run_slabs_tb(std::vector<Slab*>& slabs, const StencilPattern* table, int npat, int s_factors, double theta,
-                 std::vector<double*>& x_own, Exchange exchange, WaitHalo wait_halo, cudaStream_t s) {
+                 std::vector<double*>& x_own, Exchange exchange, Join join, cudaStream_t s, cudaStream_t bs) {
   const int kmax = stencil_max_steps(), ty = stencil_tile_rows();
+  (void)kmax;
   int zcur = 4, zi = 0;  // Z starts as B (tb_ext[4])
   for (int f = 0; f < s_factors; ++f) {
     int64_t left = int64_t(1) << f;
@@ -240,34 +268,33 @@ int run_slabs_tb(std::vector<Slab*>& slabs, const StencilPattern* table, int npa
       const int mode = left > 0 ? kInner : (f == s_factors - 1 ? kFinal : kFactorEnd);
       const int out = mode == kInner ? ti : (mode == kFinal ? 5 : 2 + zi);
       NNB_TRY(exchange(tin));
-      struct Range {
-        int a, b;
-      };
-      std::vector<Range> rest;
       for (Slab* sl : slabs) {
+        // output tiles cover the slab's own rows only (from its first own row); the halo rows
+        // are inputs, refreshed by the next exchange
         const int W = sl->tbW, H = (int)(sl->tb_len() / W);
-        const int hlo = (int)(sl->tb_lo / W), hhi = (int)(sl->tb_hi / W), tiles = (H + ty - 1) / ty;
-        // tile row t reads region rows [t·ty − kmax, t·ty + ty + kmax)
+        const int hlo = (int)(sl->tb_lo / W), hhi = (int)(sl->tb_hi / W), R = (int)(sl->rows / W);
+        if (!bs) {
+          NNB_TRY(stencil_pass(sl->tb_ext[tin], sl->tb_code, sl->tb_ext[zcur], sl->tb_ext[out], table, npat, W, H,
+                               steps, mode, theta, sl->flags + f, s, 0, -1, hlo, R));
+          continue;
+        }
+        // own tile row t reads region rows [hlo + t·ty − kmax, hlo + t·ty + ty + kmax)
+        const int tiles = (R + ty - 1) / ty;
         int t0 = 0, t1 = tiles;
-        if (hlo > 0) t0 = (hlo + kmax + ty - 1) / ty;
+        if (hlo > 0) t0 = (kmax + ty - 1) / ty;
         if (hhi > 0) {
-          const int num = H - hhi - ty - kmax;  // the last interior tile row t has t·ty <= num
-          t1 = num < 0 ? 0 : num / ty + 1;
+          const int num = R - ty - kmax;  // the last interior tile row t has t·ty <= num
+          t1 = num < 0 ? 0 : std::min(tiles, num / ty + 1);
         }
         if (t0 > t1) t0 = t1 = 0;
         NNB_TRY(stencil_pass(sl->tb_ext[tin], sl->tb_code, sl->tb_ext[zcur], sl->tb_ext[out], table, npat, W, H,
-                             steps, mode, theta, sl->flags + f, s, t0, t1));
-        rest.push_back({t0, t1});
-      }
-      NNB_TRY(wait_halo());
-      for (size_t g = 0; g < slabs.size(); ++g) {
-        Slab* sl = slabs[g];
-        const int W = sl->tbW, H = (int)(sl->tb_len() / W);
+                             steps, mode, theta, sl->flags + f, s, t0, t1, hlo, R));
         NNB_TRY(stencil_pass(sl->tb_ext[tin], sl->tb_code, sl->tb_ext[zcur], sl->tb_ext[out], table, npat, W, H,
-                             steps, mode, theta, sl->flags + f, s, 0, rest[g].a));
+                             steps, mode, theta, sl->flags + f, bs, 0, t0, hlo, R));
         NNB_TRY(stencil_pass(sl->tb_ext[tin], sl->tb_code, sl->tb_ext[zcur], sl->tb_ext[out], table, npat, W, H,
-                             steps, mode, theta, sl->flags + f, s, rest[g].b, -1));
+                             steps, mode, theta, sl->flags + f, bs, t1, -1, hlo, R));
       }
+      NNB_TRY(join());
       if (mode == kInner) {
         tin = ti;
         ti ^= 1;
@@ -605,6 +632,8 @@ int nnb_sparse_plan_create(nnb_comm_t comm, const int64_t* row_ptr, const int32_
   return 0;
 }
 
+double nnb_sparse_last_solve_ms(void) { return g_last_solve_ms; }
+
 int nnb_sparse_plan_destroy(nnb_sparse_plan_t plan) {
   delete plan;
   return 0;
@@ -647,11 +676,13 @@ int nnb_sparse_plan_solve(nnb_sparse_plan_t plan, const double* B_rows, int64_t 
       NNB_NCCL2(nccl_recv(ext + sl.tb_lo + sl.rows, hw, me + 1, comm, comm->cs));
     }
     NNB_NCCL2(nccl_group(false));
-    NNB_CUDA(cudaEventRecord(plan->landed, comm->cs));
     return 0;
   };
-  auto wait_tb = [&]() -> int {
-    if (G > 1) NNB_CUDA(cudaStreamWaitEvent(s, plan->landed, 0));
+  auto join_tb = [&]() -> int {  // s waits for the edge tile rows launched behind the exchange
+    if (G > 1) {
+      NNB_CUDA(cudaEventRecord(plan->landed, comm->cs));
+      NNB_CUDA(cudaStreamWaitEvent(s, plan->landed, 0));
+    }
     return 0;
   };
   auto exchange = [&](int e) -> int {
@@ -677,9 +708,11 @@ int nnb_sparse_plan_solve(nnb_sparse_plan_t plan, const double* B_rows, int64_t 
     if (G > 1) NNB_CUDA(cudaStreamWaitEvent(s, plan->landed, 0));
     return 0;
   };
+  SolveTimer timer(s);
   int st = sl.tb ? run_slabs_tb(slabs, plan->tb_table.as<StencilPattern>(), plan->tb_npat, s_factors, theta, xo,
-                                exchange_tb, wait_tb, s)
+                                exchange_tb, join_tb, s, G > 1 ? comm->cs : nullptr)
                  : run_slabs(slabs, k, s_factors, theta, xo, exchange, wait, s);
+  if (st == 0) timer.stop();
   if (sl.tb) {
     set_sparse_format("row-dictionary-stencil-tb");
     set_sparse_bytes_per_nnz(1);
@@ -835,10 +868,12 @@ int nnb_sparse_factorized_sharded_emulated_d(const int64_t* row_ptr, const int32
     }
     return 0;
   };
-  auto wait_tb = []() -> int { return 0; };
-  int st = tb ? run_slabs_tb(slabs, tb_table.as<StencilPattern>(), tb_npat, s_factors, theta, xo, exchange_tb, wait_tb,
-                             s)
+  auto join_tb = []() -> int { return 0; };
+  SolveTimer timer(s);
+  int st = tb ? run_slabs_tb(slabs, tb_table.as<StencilPattern>(), tb_npat, s_factors, theta, xo, exchange_tb, join_tb,
+                             s, nullptr)
               : run_slabs(slabs, k, s_factors, theta, xo, exchange, wait, s);
+  if (st == 0) timer.stop();
   if (tb) {
     set_sparse_format("row-dictionary-stencil-tb");
     set_sparse_bytes_per_nnz(1);

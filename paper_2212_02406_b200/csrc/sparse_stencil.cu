@@ -131,13 +131,14 @@ template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     stencil_tb_kernel(const double* __restrict__ tin, const uint8_t* __restrict__ rcode,
                       const double* __restrict__ zold, double* __restrict__ out, const StPat* __restrict__ pats,
-                      int npat, int W, int H, int steps, double theta, int* __restrict__ flag, int ty0) {
+                      int npat, int W, int H, int steps, double theta, int* __restrict__ flag, int ty0,
+                      int y_off) {
   extern __shared__ __align__(16) uint8_t sm[];
   double* buf0 = reinterpret_cast<double*>(sm);
   double* buf1 = buf0 + kRX * kRY;
   StPat* spat = reinterpret_cast<StPat*>(buf1 + kRX * kRY);
   uint8_t* code = reinterpret_cast<uint8_t*>(spat + kRowDictMax);
-  const int x0 = blockIdx.x * kTX - kS, y0 = (blockIdx.y + ty0) * kTY - kS;
+  const int x0 = blockIdx.x * kTX - kS, y0 = (blockIdx.y + ty0) * kTY + y_off - kS;
   for (int i = threadIdx.x; i < npat; i += kThreads) spat[i] = pats[i];
   // the region through cp.async (all of it in flight at once; cells off the grid zero-filled)
 #pragma unroll
@@ -294,11 +295,11 @@ int stencil_tile_rows() { return kTY; }
 
 int stencil_pass(const double* tin, const uint8_t* rcode, const double* zold, double* out,
                  const StencilPattern* table_dev, int npat, int W, int H, int steps, int mode, double theta, int* flag,
-                 cudaStream_t s, int ty0, int ty1) {
+                 cudaStream_t s, int ty0, int ty1, int y_off, int out_rows) {
   NNB_TRY(ensure_smem<stencil_tb_kernel<kInner>>(kSmem));
   NNB_TRY(ensure_smem<stencil_tb_kernel<kFactorEnd>>(kSmem));
   NNB_TRY(ensure_smem<stencil_tb_kernel<kFinal>>(kSmem));
-  const int tiles_y = (H + kTY - 1) / kTY;
+  const int tiles_y = ((out_rows < 0 ? H : out_rows) + kTY - 1) / kTY;
   if (ty1 < 0 || ty1 > tiles_y) ty1 = tiles_y;
   if (ty0 >= ty1) return 0;
   const dim3 grid((unsigned)((W + kTX - 1) / kTX), (unsigned)(ty1 - ty0));
@@ -306,15 +307,15 @@ int stencil_pass(const double* tin, const uint8_t* rcode, const double* zold, do
   switch (mode) {
     case kInner:
       stencil_tb_kernel<kInner><<<grid, kThreads, kSmem, s>>>(tin, rcode, zold, out, pats, npat, W, H, steps, theta,
-                                                              flag, ty0);
+                                                              flag, ty0, y_off);
       break;
     case kFactorEnd:
       stencil_tb_kernel<kFactorEnd><<<grid, kThreads, kSmem, s>>>(tin, rcode, zold, out, pats, npat, W, H, steps,
-                                                                  theta, flag, ty0);
+                                                                  theta, flag, ty0, y_off);
       break;
     default:
       stencil_tb_kernel<kFinal><<<grid, kThreads, kSmem, s>>>(tin, rcode, zold, out, pats, npat, W, H, steps, theta,
-                                                              flag, ty0);
+                                                              flag, ty0, y_off);
   }
   count_launch();
   NNB_CUDA(cudaGetLastError());
