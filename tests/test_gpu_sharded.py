@@ -247,3 +247,40 @@ def test_nccl_world1_int8_emulation_matches_single_gpu():
     x1, r1 = nnb.nn_chain(a, None, p=2, max_iters=3)
     assert np.array_equal(_np(xs), _np(x1))
     assert np.allclose([e for _, e in rs.history], [e for _, e in r1.history], rtol=1e-12, atol=1e-15)
+
+
+def test_emulated_sharded_int8_divergence_and_tolerance(ref):
+    """The int8-emulated sharded schedule keeps the chain's contracts: a non-finite start is
+    reported like the single-GPU chain's (same error class), and the tolerance stop comes at
+    the reference's nest (NNB_ARITH_OZAKI at N=256, 4 virtual ranks)."""
+    a = W.spd_conditioned(256, 1e3, seed=9)
+    x0 = W.x0_transpose_norm(a)
+    with nnb.ozaki_arithmetic():
+        xs, rs = nnb.nn_chain_sharded_emulated(a, 4, x0, p=2, max_iters=60, tol=1e-12)
+        bad = x0.copy()
+        bad[3, 5] = np.nan
+        errs = []
+        for fn in (lambda: nnb.nn_chain(a, bad, p=2, max_iters=4),
+                   lambda: nnb.nn_chain_sharded_emulated(a, 4, bad, p=2, max_iters=4)):
+            with pytest.raises(nnb.Error) as e:
+                fn()
+            errs.append(type(e.value))
+    xr, hr, ir, _ = ref.chain(a, x0, 2, 60, tol=1e-12)
+    assert rs.iters == ir and rs.stopped_reason == "tolerance"
+    assert rel_frob(_np(xs), xr.real) < 1e-10
+    assert errs[0] is errs[1]
+
+
+def test_sparse_sharded_temporal_blocking_nonfinite(ref):
+    """A non-finite right-hand side entry in one slab: the temporal-blocked slab schedule
+    reports the same factor as the single-GPU solve."""
+    rp, col, val = W.laplacian_5pt(64)
+    b = W.rhs(4096, seed=31)
+    b[2000] = np.inf
+    norm = nnb.Normalization(theta=0.2, valid=True)
+    with pytest.raises(nnb.DivergenceError) as e1:
+        nnb.solve_sparse_factorized(nnb.Csr(rp, col, val, n=4096), b, 63, norm)
+    with pytest.raises(nnb.DivergenceError) as e4:
+        nnb.solve_sparse_factorized_sharded_emulated(nnb.Csr(rp, col, val, n=4096), b, 63, norm, 4)
+    assert nnb.sparse_last_format() == "row-dictionary-stencil-tb"
+    assert e1.value.nest_index == e4.value.nest_index
