@@ -328,6 +328,126 @@ int gemm(GemmOp op, RedWs* red, cudaStream_t s) {
 //   Cr −= α·Ai·Bi,                Ci −= α·Ai·Bi      (one GEMM, dual epilogue + Σ|C|²)
 // = α(ArBr − AiBi) + β·Dr + γI  and  α(SA·SB − ArBr − AiBi) + β·Di: three DMMA
 // GEMMs instead of four; the last epilogue reduces |Cr|² + |Ci|² (eps, non-finite).
+// Complex 3M on the int8 emulation: the emulated products take plain epilogues, so the
+// dual-output updates of the DMMA form become one elementwise pass per real product:
+//   Cr = α·T + β·Dr + γ·I and Ci −= α·T   (T = Ar·Br, `first`)
+//   Cr −= α·T and Ci −= α·T               (T = Ai·Bi), with the deterministic Σ(Cr² + Ci²) /
+// non-finite count per block (partials summed in block order by zdual_finish_kernel).
+__global__ void zdual_update_kernel(const double* __restrict__ T, int64_t ldt, double* __restrict__ Cr,
+                                    double* __restrict__ Ci, int64_t ldc, const double* __restrict__ Dr, int64_t ldd,
+                                    double alpha, double beta, double gamma, int64_t diag_offset, int64_t M, int64_t N,
+                                    int first, double* __restrict__ ss_part, int* __restrict__ nf_part) {
+  __shared__ double red[8];
+  __shared__ int redi[8];
+  double ss = 0.0;
+  int nf = 0;
+  const int64_t total = M * N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / N, c = e % N;
+    const double t = alpha * T[r * ldt + c];
+    double cr;
+    if (first) {
+      cr = t;
+      if (Dr) cr = fma(beta, Dr[r * ldd + c], cr);
+      if (r + diag_offset == c) cr += gamma;
+    } else {
+      cr = Cr[r * ldc + c] - t;
+    }
+    const double ci = Ci[r * ldc + c] - t;
+    Cr[r * ldc + c] = cr;
+    Ci[r * ldc + c] = ci;
+    if (ss_part) {
+      ss = fma(cr, cr, ss);
+      ss = fma(ci, ci, ss);
+      nf += !isfinite(cr) + !isfinite(ci);
+    }
+  }
+  if (!ss_part) return;
+  ss = warp_sum(ss);
+  nf = warp_sum_i(nf);
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = ss;
+    redi[threadIdx.x >> 5] = nf;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    int f = 0;
+    for (int w = 0; w < 8; ++w) {
+      t += red[w];
+      f += redi[w];
+    }
+    ss_part[blockIdx.x] = t;
+    nf_part[blockIdx.x] = f;
+  }
+}
+__global__ void zdual_finish_kernel(const double* __restrict__ ss_part, const int* __restrict__ nf_part, int blocks,
+                                    double* ss_out, int* nf_out, double* eps_out, double eps_scale) {
+  if (threadIdx.x) return;
+  double t = 0.0;
+  int f = 0;
+  for (int b = 0; b < blocks; ++b) {
+    t += ss_part[b];
+    f += nf_part[b];
+  }
+  if (ss_out) *ss_out = t;
+  if (nf_out) *nf_out = f;
+  if (eps_out) *eps_out = sqrt(t) * eps_scale;
+}
+
+static int zgemm3m_emulated(const ZGemm& z, RedWs* red, const double* sa, int64_t lsa, const double* sb, int64_t lsb,
+                            cudaStream_t s) {
+  const int64_t M = z.M, N = z.N, K = z.K;
+  // Ci = α·(Ar+Ai)(Br+Bi) + β·Di
+  GemmOp g1;
+  g1.A = sa;
+  g1.lda = lsa;
+  g1.B = sb;
+  g1.ldb = lsb;
+  g1.M = M;
+  g1.N = N;
+  g1.K = K;
+  g1.ep.alpha = z.alpha;
+  g1.ep.D = z.Di;
+  g1.ep.ldd = z.ldd;
+  g1.ep.beta = z.beta;
+  g1.ep.C = z.Ci;
+  g1.ep.ldc = z.ldc;
+  NNB_TRY(gemm(g1, nullptr, s));
+  const int64_t ldt = (N + 7) / 8 * 8;
+  DevBuf tb;
+  NNB_TRY(tb.alloc(sizeof(double) * M * ldt, s));
+  const bool want = z.nf_out != nullptr && red != nullptr;
+  const int kBlocks = want ? std::max(1, std::min(1184, red->capacity)) : 1184;  // ≤ 8 per SM
+  for (int pass = 0; pass < 2; ++pass) {
+    GemmOp g;
+    g.A = pass ? z.Ai : z.Ar;
+    g.lda = z.lda;
+    g.B = pass ? z.Bi : z.Br;
+    g.ldb = z.ldb;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.ep.C = tb.as<double>();
+    g.ep.ldc = ldt;
+    NNB_TRY(gemm(g, nullptr, s));
+    const bool red_here = pass == 1 && want;
+    zdual_update_kernel<<<kBlocks, 256, 0, s>>>(tb.as<double>(), ldt, z.Cr, z.Ci, z.ldc, z.Dr, z.ldd, z.alpha, z.beta,
+                                                z.gamma, z.diag_offset, M, N, pass == 0 ? 1 : 0,
+                                                red_here ? red->ss_partial : nullptr,
+                                                red_here ? red->nf_partial : nullptr);
+    count_launch();
+    NNB_CUDA(cudaGetLastError());
+  }
+  if (want) {
+    zdual_finish_kernel<<<1, 32, 0, s>>>(red->ss_partial, red->nf_partial, kBlocks, z.ss_out, z.nf_out, z.eps_out,
+                                         z.eps_scale);
+    count_launch();
+    NNB_CUDA(cudaGetLastError());
+  }
+  return 0;
+}
+
 int zgemm3m(const ZGemm& z, RedWs* red, cudaStream_t s) {
   const int64_t M = z.M, N = z.N, K = z.K;
   if (M <= 0 || N <= 0) return 0;
@@ -338,6 +458,8 @@ int zgemm3m(const ZGemm& z, RedWs* red, cudaStream_t s) {
   double* sb = sa + M * lsa;
   NNB_TRY(axpby(1.0, z.Ar, z.lda, 1.0, z.Ai, z.lda, 0.0, 0, sa, lsa, M, K, s));
   NNB_TRY(axpby(1.0, z.Br, z.ldb, 1.0, z.Bi, z.ldb, 0.0, 0, sb, lsb, K, N, s));
+  // the three real products on the int8 emulation where it pays (as gemm() decides for one)
+  if (arith() == 2 || (arith() == 0 && ozaki_pays(M, N, K))) return zgemm3m_emulated(z, red, sa, lsa, sb, lsb, s);
   GemmOp g1;
   g1.A = sa;
   g1.lda = lsa;

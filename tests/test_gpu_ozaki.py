@@ -113,3 +113,24 @@ def test_ozaki_chain_divergence_index(port):
     with nnb.ozaki_arithmetic(), pytest.raises(nnb.DivergenceError) as ed:
         nnb.nn_chain(a, x0, p=1, max_iters=40)
     assert ed.value.nest_index == er.value.index
+
+
+def test_complex_products_on_the_int8_emulation(port):
+    """Complex products under the emulation: 3M over three emulated real products, the
+    dual-output DMMA epilogue replaced by elementwise updates (ozaki_arithmetic at small
+    sizes; FAST routes complex N >= 3072 products the same way)."""
+    rng = np.random.default_rng(12)
+    a = rng.standard_normal((300, 260)) + 1j * rng.standard_normal((300, 260))
+    b = rng.standard_normal((260, 280)) + 1j * rng.standard_normal((260, 280))
+    with nnb.ozaki_arithmetic():
+        c = nnb.matmul(a, b)
+    assert rel_frob(c, port.matmul(a, b)) < 1e-13
+    # a complex Hermitian-positive chain: the emulated chain against the oracle's
+    h = rng.standard_normal((400, 200)) + 1j * rng.standard_normal((400, 200))
+    az = np.conj(h.T) @ h / 400 + 0.5 * np.eye(200)
+    x0 = np.conj(az.T) / (np.abs(az).sum(axis=0).max() * np.abs(az).sum(axis=1).max())
+    with nnb.ozaki_arithmetic():
+        xz, rz = nnb.nn_chain(az, x0, p=2, max_iters=6)
+    xr, hr, _ = port.chain(az, x0, 2, 6)
+    assert rel_frob(xz, xr) < 1e-10
+    assert np.allclose([e for _, e in rz.history], hr, rtol=1e-6, atol=1e-13)
