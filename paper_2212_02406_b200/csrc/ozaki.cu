@@ -319,6 +319,28 @@ __device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const CUtensorMap
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
       : "memory");
 }
+// TMA load with an L2 eviction-priority hint (createpolicy): the int8 GEMM's A panels are
+// re-read by every tile of a raster group (evict_last), its B panels pass once per group
+// (evict_first)
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                                 int32_t c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
 // arrive on `bar` in every CTA of `mask` once this thread's MMAs so far have completed
 __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
   asm volatile(
@@ -351,7 +373,8 @@ template <int kC>
 __global__ void __launch_bounds__(192, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, int M, int N,
                    int64_t ldr, uint8_t* __restrict__ out, const OzConst cst, int tiles_m, int tiles_n,
-                   int group_m, const KSpan ks, int accumulate, const uint32_t* __restrict__ tile_list, int list_len) {
+                   int group_m, const KSpan ks, int accumulate, const uint32_t* __restrict__ tile_list, int list_len,
+                   int hints) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -402,6 +425,7 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {  // TMA producer
       tma_prefetch_desc(&tma_a);
       tma_prefetch_desc(&tma_b);
+      const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
       int it = 0;
       for (int t = unit; t < total; t += nunits) {
         const TileCoord tc = coord(t);
@@ -413,9 +437,11 @@ __global__ void __launch_bounds__(192, 1)
           uint8_t* sa = smem + st * kStageBytes;
           mbar_arrive_expect_tx(&full[st], kStageBytes);
           const int blk = kb / ks.nk, kt = kb - blk * ks.nk;
-          tma_load_2d(sa, &tma_a, &full[st], ks.a_k0[blk] + kt * kBK, arow);
+          if (hints & 1) tma_load_2d_hint(sa, &tma_a, &full[st], ks.a_k0[blk] + kt * kBK, arow, pol_a);
+          else tma_load_2d(sa, &tma_a, &full[st], ks.a_k0[blk] + kt * kBK, arow);
           if constexpr (kC == 1) {
-            tma_load_2d(sa + kABytes, &tma_b, &full[st], kt * kBK, ks.b_row0[blk] + brow);
+            if (hints & 2) tma_load_2d_hint(sa + kABytes, &tma_b, &full[st], kt * kBK, ks.b_row0[blk] + brow, pol_b);
+            else tma_load_2d(sa + kABytes, &tma_b, &full[st], kt * kBK, ks.b_row0[blk] + brow);
           } else {
             tma_load_2d_mc(sa + kABytes + crank * (kBBytes / kC), &tma_b, &full[st], kt * kBK,
                            ks.b_row0[blk] + brow + static_cast<int>(crank) * (kBN / kC), kMask);
@@ -1388,6 +1414,10 @@ int launch_oz_gemm(const int8_t* a_res, int64_t M, int64_t a_kp, const int8_t* b
   }
   const int tiles_m = (int)((M + kBM - 1) / kBM), tiles_n = (int)((N + kBN - 1) / kBN);
   static const int gm = debug_env("NNB_OZ_GROUP") ? std::atoi(debug_env("NNB_OZ_GROUP")) : kGroupM;
+  // NNB_DEBUG=1 NNB_OZ_HINTS=bits: L2 eviction hints on the operand loads (1: A evict_last,
+  // 2: B evict_first; both together measured 1.7x slower at N=32768: B panels serve a whole
+  // raster group and evict_first lost them)
+  static const int hints = debug_env("NNB_OZ_HINTS") ? std::atoi(debug_env("NNB_OZ_HINTS")) : 0;
   int list_len = 0;
   const uint32_t* list = nullptr;
   if (upper) {
@@ -1400,7 +1430,7 @@ int launch_oz_gemm(const int8_t* a_res, int64_t M, int64_t a_kp, const int8_t* b
   if (kc == 1) {
     const unsigned grid = (unsigned)std::min<int64_t>(total, std::max(1, sms - reserve_sms));
     oz_gemm_kernel<1><<<grid, 192, kGemmSmem, st>>>(ta, tb, (int)M, (int)N, ldr, out, c, tiles_m, tiles_n, gm, ks,
-                                                    accumulate ? 1 : 0, list, list_len);
+                                                    accumulate ? 1 : 0, list, list_len, hints);
   } else {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
@@ -1422,7 +1452,7 @@ int launch_oz_gemm(const int8_t* a_res, int64_t M, int64_t a_kp, const int8_t* b
     const int64_t units = std::min<int64_t>(total, std::max(1, std::min(max_clusters, (sms - reserve_sms) / 2)));
     cfg.gridDim = dim3((unsigned)(2 * units));
     NNB_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<2>, ta, tb, (int)M, (int)N, ldr, out, c, tiles_m, tiles_n, gm,
-                                ks, accumulate ? 1 : 0, static_cast<const uint32_t*>(nullptr), 0));
+                                ks, accumulate ? 1 : 0, static_cast<const uint32_t*>(nullptr), 0, 0));
   }
   count_launch();
   NNB_CUDA(cudaGetLastError());

@@ -9,7 +9,7 @@ sys.path.insert(0, ".")
 import paper_2212_02406_b200 as nnb  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
-worlds = [int(w) for w in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1, 2, 4, 8]
+worlds = [int(w) for w in sys.argv[2].split(",") if w] if len(sys.argv) > 2 else [1, 2, 4, 8]
 g = torch.Generator(device="cuda").manual_seed(1)
 b = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
 a = nnb.matmul_nt(b, b)
