@@ -291,8 +291,10 @@ int nnb_sparse_last_bytes_per_nnz(void);
  * (row dictionary: n bytes), the pair codes (slot-major ELL: width*n bytes, no row
  * offsets) or values and columns, plus row offsets. */
 int64_t nnb_sparse_last_matrix_bytes(void);
-/* That format by name: "row-dictionary" (<= 256 distinct whole rows over the ELL
- * pair codes, e.g. stencils: one uint8 code per row), "pair-dictionary-ell",
+/* That format by name: "row-dictionary-stencil-tb" (5-point stencils: row codes over
+ * temporal-blocked passes of up to 8 applications, on one GPU or across row slabs of
+ * whole grid rows), "row-dictionary" (<= 256 distinct whole rows over the ELL pair
+ * codes, e.g. stencils: one uint8 code per row), "pair-dictionary-ell",
  * "pair-dictionary-csr", "csr-int16-delta", "csr-int32", "csr-int64-offsets";
  * "" before any solve. */
 const char* nnb_sparse_last_format(void);
@@ -332,7 +334,11 @@ int nnb_comm_init(const void* id, int32_t world, int32_t rank, nnb_comm_t* comm_
 int nnb_comm_destroy(nnb_comm_t comm);
 /* A_rows / X0_rows / X_rows_out: this rank's rows_g × n block (row-major).
  * X0 kinds: GIVEN, SCALED_IDENTITY, JACOBI, and TRANSPOSE_NORM (which
- * gathers A to form the transposed block). */
+ * gathers A to form the transposed block).  Where the int8 emulation applies
+ * (NNB_ARITH_FAST at n >= 3072, NNB_ARITH_OZAKI) the ranks exchange column
+ * statistics and int8 residue blocks instead of FP64 rows, and X equals the
+ * single-GPU chain's bit for bit; otherwise an FP64 ring feeds K-split DMMA
+ * products.  Replaces the nn_invert loop (proj/src/solver.cpp:138-159) across GPUs. */
 int nnb_nn_chain_sharded_d(nnb_comm_t comm, const double* A_rows, int64_t n,
                            const double* X0_rows, const nnb_chain_config* cfg, double* X_rows_out,
                            double* eps_hist, nnb_chain_result* result, void* stream);
