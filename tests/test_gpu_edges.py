@@ -133,3 +133,20 @@ def test_fixed_count_chain_stops_at_the_divergent_nest(port):
     launched = nnb.kernel_launches() - l0
     # (p+1) product launches per nest (+ the residual's), at most kLag = 2 nests past f
     assert launched <= 4 * (f + 3) + 16, launched
+
+
+def test_release_cached_memory_and_solve_timer():
+    """nnb_release_cached_memory trims the library's pool between calls without
+    disturbing later work; nnb_sparse_last_solve_ms reports a slab solve's schedule."""
+    import paper_2212_02406_b200 as nnb
+    from paper_2212_02406_b200 import workloads as W
+
+    a = W.gram_shifted(300, seed=2, shift=1.0)
+    x1, _ = nnb.nn_chain(a, None, p=2, max_iters=3)
+    nnb.release_cached_memory()
+    x2, _ = nnb.nn_chain(a, None, p=2, max_iters=3)
+    assert np.array_equal(x1, x2)
+    rp, col, val = W.laplacian_5pt(64)
+    nnb.solve_sparse_factorized_sharded_emulated(nnb.Csr(rp, col, val, n=4096), W.rhs(4096, seed=1), 15,
+                                                 nnb.Normalization(theta=0.2, valid=True), 2)
+    assert nnb.sparse_last_solve_ms() > 0.0
