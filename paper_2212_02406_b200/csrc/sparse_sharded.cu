@@ -382,6 +382,7 @@ int setup_slab(Slab& sl, const int64_t* rp_dev, const int32_t* col_dev, const do
   int64_t base = 0;
   NNB_CUDA(cudaMemcpyAsync(&base, rp_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   NNB_CUDA(cudaStreamSynchronize(s));
+  trace_mark(s, "  slab: nnz");
   sl.nnz -= base;
   if (sl.nnz >= INT32_MAX) return fail(NNB_ERR_SHAPE, "sharded sparse: a slab exceeds 2^31 nonzeros");
   DevBuf st;
@@ -395,6 +396,7 @@ int setup_slab(Slab& sl, const int64_t* rp_dev, const int32_t* col_dev, const do
   int64_t h[4];
   NNB_CUDA(cudaMemcpyAsync(h, st.p, sizeof(h), cudaMemcpyDeviceToHost, s));
   NNB_CUDA(cudaStreamSynchronize(s));
+  trace_mark(s, "  slab: stats");
   const bool any = h[0] != INT64_MAX;  // at least one nonzero in the slab
   sl.h_lo = (any && h[0] < sl.row0) ? sl.row0 - h[0] : 0;
   sl.h_hi = (any && h[1] >= sl.row0 + sl.rows) ? h[1] - (sl.row0 + sl.rows - 1) : 0;
@@ -416,16 +418,23 @@ int setup_slab(Slab& sl, const int64_t* rp_dev, const int32_t* col_dev, const do
   NNB_CUDA(cudaMemsetAsync(sl.flags, 0, sizeof(int) * 64, s));
   NNB_CUDA(cudaMemsetAsync(d, 0, sizeof(double) * 5 * ext, s));
   bool fits = false;
-  NNB_TRY(compact_csr(rp_dev, col_dev, sl.rows, sl.row0, sl.rp, c16, &fits, s));
-  if (fits) {
-    sl.col16 = c16;
-  } else if (sl.nnz) {
-    remap_cols_kernel<<<std::max<int64_t>(1, std::min<int64_t>(4736, (sl.nnz + 255) / 256)), 256, 0, s>>>(
-        col_dev + base, sl.nnz, sl.h_lo - sl.row0, sl.col);
-    count_launch();
-  }
+  trace_mark(s, "  slab: buffers");
   sl.val = val_dev + base;
   if (k == 1) NNB_TRY(setup_slab_dict(sl, rp_dev, col_dev, val_dev, s));
+  trace_mark(s, "  slab: dictionary");
+  // int32 offsets and int16 / remapped columns only for the formats that read them: a slab
+  // in row codes (spmv_apply's row-dictionary branch, 32-bit index math) never does
+  if (!(sl.rcode && sl.rows + sl.h_lo < INT32_MAX / 2)) {
+    NNB_TRY(compact_csr(rp_dev, col_dev, sl.rows, sl.row0, sl.rp, c16, &fits, s));
+    if (fits) {
+      sl.col16 = c16;
+    } else if (sl.nnz) {
+      remap_cols_kernel<<<std::max<int64_t>(1, std::min<int64_t>(4736, (sl.nnz + 255) / 256)), 256, 0, s>>>(
+          col_dev + base, sl.nnz, sl.h_lo - sl.row0, sl.col);
+      count_launch();
+    }
+    trace_mark(s, "  slab: compact");
+  }
   set_sparse_bytes_per_nnz(sl.code || sl.rcode ? 1 : (sl.col16 ? 10 : 12));
   set_sparse_format(sl.rcode ? "row-dictionary"
                     : sl.ell_width ? "pair-dictionary-ell"

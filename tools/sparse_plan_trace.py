@@ -9,8 +9,9 @@ sys.path.insert(0, ".")
 import paper_2212_02406_b200 as nnb  # noqa: E402
 from paper_2212_02406_b200 import workloads as W  # noqa: E402
 
-rp, col, val = W.laplacian_5pt(4096)
-n = 4096 * 4096
+g = int(sys.argv[1]) if len(sys.argv) > 1 else 4096  # 1448: a 4096^2 / 8 slab's rows
+rp, col, val = W.laplacian_5pt(g)
+n = g * g
 dev = lambda a: torch.from_numpy(a).cuda()
 csr = nnb.Csr(dev(rp), dev(col), dev(val), n=n, nnz=col.size)
 b = dev(W.rhs(n, seed=7))
