@@ -11,8 +11,9 @@ Checked against the single-process oracle chain and for bit-identical eps on
 every rank (identical stop decisions).  The int8-emulated products of the same
 file (column statistics gathered and combined in rank order, residue blocks on
 the ring, K-block products accumulated mod m) are restated with integer numpy
-and checked against the whole product's residues; the sparse halo schedule is
-checked bit-exact against the reference."""
+and checked against the whole product's residues; the sparse halo schedules (a
+halo per application, and the temporal-blocked slabs with an 8-row halo per pass)
+are checked bit-exact against the reference."""
 import os
 import socket
 
@@ -323,3 +324,91 @@ def test_int8_emulated_product_schedule_gloo(world):
     prod = A[:8].astype(object) @ B.astype(object)
     for l, m in enumerate(_MODULI[:s]):
         assert np.array_equal(np.mod(prod, m).astype(np.int64), res[0][4][l][:8])
+
+
+# ---------------------------------------------------------------- temporal-blocked slabs over gloo
+def _tb_worker(rank, world, port, grid, gamma, theta, out_q):
+    """sparse_sharded.cu's temporal-blocked slab schedule (run_slabs_tb) restated with gloo and
+    scalar IEEE arithmetic in the reference's order: per pass of up to 8 applications the 8
+    halo grid rows of its input are exchanged once, the pass runs over the slab's extended
+    rows (cells past them read as zero, so the halo goes stale one row per application and
+    never reaches the own rows), and only the own rows are kept."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2212_02406_b200 as nnb
+
+    W_, n = grid, grid * grid
+    rp, col, val = W.laplacian_5pt(grid)
+    b = W.rhs(n, seed=13)
+    r0, rows = nnb.partition_rows(n, world, rank)
+    assert r0 % W_ == 0 and rows % W_ == 0 and rows >= 8 * W_
+    hw = 8 * W_
+    lo = hw if rank > 0 else 0
+    hi = hw if rank < world - 1 else 0
+    e0 = r0 - lo  # global index of the extended region's first cell
+
+    def exchange(ext):
+        reqs, bufs = [], []
+        if rank > 0:
+            reqs.append(dist.isend(torch.tensor(ext[lo:lo + hw], dtype=torch.float64), rank - 1))
+            bb = torch.empty(hw, dtype=torch.float64)
+            reqs.append(dist.irecv(bb, rank - 1))
+            bufs.append((0, bb))
+        if rank < world - 1:
+            reqs.append(dist.isend(torch.tensor(ext[lo + rows - hw:lo + rows], dtype=torch.float64), rank + 1))
+            bb = torch.empty(hw, dtype=torch.float64)
+            reqs.append(dist.irecv(bb, rank + 1))
+            bufs.append((lo + rows, bb))
+        for r in reqs:
+            r.wait()
+        for off, bb in bufs:
+            ext[off:off + hw] = bb.tolist()
+
+    def step(ext):
+        out = list(ext)
+        for i in range(len(ext)):
+            g = e0 + i
+            y = 0.0
+            for e in range(rp[g], rp[g + 1]):
+                j = int(col[e]) - e0
+                y = y + float(val[e]) * (ext[j] if 0 <= j < len(ext) else 0.0)
+            out[i] = ext[i] - theta * y
+        return out
+
+    ext_len = lo + rows + hi
+    z = [0.0] * ext_len
+    z[lo:lo + rows] = [float(v) for v in b[r0:r0 + rows]]
+    s_f = 0
+    while (1 << s_f) - 1 < gamma:
+        s_f += 1
+    for f in range(s_f):
+        left, t = 1 << f, list(z)
+        while left > 0:
+            steps = min(8, left)
+            left -= steps
+            exchange(t)
+            for _ in range(steps):
+                t = step(t)
+        z = [zi + ti for zi, ti in zip(z, t)]
+    x = [zi * theta for zi in z[lo:lo + rows]]
+    out_q.put((rank, r0, x))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sparse_temporal_blocked_slabs_gloo_world2(port):
+    world, grid, gamma, theta = 2, 32, 15, 0.2  # 2 slabs of 16 grid rows, 8-row halos
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    portn = _free_port()
+    procs = [ctx.Process(target=_tb_worker, args=(r, world, portn, grid, gamma, theta, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted((q.get(timeout=300) for _ in range(world)), key=lambda r: r[0])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    x = np.concatenate([np.array(r[2]) for r in res])
+    rp, col, val = W.laplacian_5pt(grid)
+    xr, _ = port.sparse_factorized(rp, col, val, W.rhs(grid * grid, seed=13), gamma, theta)
+    assert np.array_equal(x, xr.real)  # bit-identical: the halo never reaches the own rows
