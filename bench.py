@@ -587,6 +587,23 @@ def run_mimo(args, world, rank):
     torch.cuda.synchronize()
     ms_full = max_over_ranks(world, e0.elapsed_time(e1)) / steps
     del a_gemm
+    # other user counts (n = 8, 24, 32: batched_generic.cu), the same 262144 systems of NN p=2 ×4
+    other_users = {}
+    if world == 1:
+        for users in (8, 24, 32):
+            au = W.mimo_gram_device(batch, seed=5, users=users)
+            for _ in range(2):
+                nnb.nn_batched(au, p=2, iters=4)
+            e0.record()
+            for _ in range(3):
+                nnb.nn_batched(au, p=2, iters=4)
+            e1.record()
+            torch.cuda.synchronize()
+            ms_u = e0.elapsed_time(e1) / 3
+            other_users[f"users_{users}"] = {"ms_per_step": round(ms_u, 3),
+                                             "inversions_per_s": round(batch / (ms_u * 1e-3), 1)}
+            del au
+        torch.cuda.empty_cache()
     # NS baseline of the analytically equivalent term count for 4 nests of p=2: 3^4 - 1 = 80
     for _ in range(2):
         xs = nnb.ns_batched(a, 80)
@@ -610,6 +627,7 @@ def run_mimo(args, world, rank):
                                       f"products: nest 0 from the diagonal X0 needs p-1; the {horner} Hermitian "
                                       "Horner products run 3 of 4 8x8 tiles) x 8*16^3 flop (4M-equivalent)",
                         "algorithmic_tflops_13_products": round(batch * 13 * 8.0 * 16 ** 3 / (ms * 1e-3) / 1e12, 3)},
+           "other_user_counts": other_users or None,
            "non_hermitian_input": {"ms_per_step": round(ms_full, 4),
                                    "inversions_per_s": round(sum_over_ranks(world, batch) / (ms_full * 1e-3), 1),
                                    "note": "A not bit-Hermitian (a GEMM-formed Gram): all 11 products full"},

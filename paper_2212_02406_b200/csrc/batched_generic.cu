@@ -13,6 +13,7 @@
 // keeps the m8n8k4 fragment loads at their 2-wavefront minimum.
 // The fused detector (Gram Hᴴ·H + σ²I and z = Hᴴ·y from one pass over H, the NN
 // inverse, x̂ = X·z) has the same shape for n users.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -286,6 +287,181 @@ __global__ void __launch_bounds__(128) detect_gen_kernel(const double2* __restri
   }
 }
 
+// ---- n = 24, 32: one block of n/8 warps per system ---------------------------------
+// With one warp per system a 32-user system's four planar 32×34 matrix pairs (70 KB) left 3
+// warps per SM, and the warp's 16 output tiles did not fit its registers.  Here warp w owns
+// the 8-row stripe w of every product (n/8 tiles, formed in registers), the system's warps
+// meet at a block barrier before the stripe is stored (the output may alias an operand)
+// and after; 3 (n=32) or 5 (n=24) systems per SM, 12-15 warps.  Products are 3M (Gauss):
+// 25 % fewer DMMAs than the one-warp kernel's 4M, within the parity tolerance.
+// 3M (Gauss) for one 8×8 tile: P1 = Σ lr·rr, P2 = Σ li·ri, P3 = Σ (lr+li)(rr+ri);
+// re = P1 − P2, im = P3 − P1 − P2 — 3 DMMA and 2 pre-sum DADDs per k-step instead of 4 DMMA
+template <int N>
+__device__ __forceinline__ void tile_mma3(const Pl& L, const Pl& R, int ti, int tj, int g, int t, double (&cr)[2],
+                                          double (&ci)[2]) {
+  constexpr int ld = Gen<N>::kLd;
+  double p1[2] = {0.0, 0.0}, p2[2] = {0.0, 0.0}, p3[2] = {0.0, 0.0};
+#pragma unroll
+  for (int kb = 0; kb < N / 4; ++kb) {
+    const int ar = 8 * ti + g, ac = 4 * kb + t;
+    const int br = 4 * kb + t, bc = 8 * tj + g;
+    const double lr = L.re[ar * ld + ac], li = L.im[ar * ld + ac];
+    const double rr = R.re[br * ld + bc], ri = R.im[br * ld + bc];
+    dmma_8x8x4(p1[0], p1[1], lr, rr);
+    dmma_8x8x4(p2[0], p2[1], li, ri);
+    dmma_8x8x4(p3[0], p3[1], lr + li, rr + ri);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    cr[h] = p1[h] - p2[h];
+    ci[h] = p3[h] - p1[h] - p2[h];
+  }
+}
+
+template <int N>
+__device__ double product_coop(const Pl& L, const Pl& R, double alpha, const Pl* D, double beta, double gamma,
+                               const Pl& out, int w, int g, int t, bool want_ss) {
+  constexpr int ld = Gen<N>::kLd, kT = Gen<N>::kT;
+  double ss = 0.0;
+  double keep_r[kT][2], keep_i[kT][2];
+#pragma unroll
+  for (int tj = 0; tj < kT; ++tj) {
+    double cr[2], ci[2];
+    tile_mma3<N>(L, R, w, tj, g, t, cr, ci);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = 8 * w + g, c = 8 * tj + 2 * t + h;
+      double vr = alpha * cr[h], vi = alpha * ci[h];
+      if (D) {
+        vr = fma(beta, D->re[r * ld + c], vr);
+        vi = fma(beta, D->im[r * ld + c], vi);
+      }
+      if (r == c) vr += gamma;
+      keep_r[tj][h] = vr;
+      keep_i[tj][h] = vi;
+      if (want_ss) ss += vr * vr + vi * vi;
+    }
+  }
+  __syncthreads();  // every warp has read L, R and D before `out` is overwritten
+#pragma unroll
+  for (int tj = 0; tj < kT; ++tj)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = 8 * w + g, c = 8 * tj + 2 * t + h;
+      out.re[r * ld + c] = keep_r[tj][h];
+      out.im[r * ld + c] = keep_i[tj][h];
+    }
+  __syncthreads();
+  return ss;
+}
+
+template <int N>
+__global__ void __launch_bounds__(32 * (N / 8)) batched_gen_coop_kernel(const double2* __restrict__ A, int64_t batch,
+                                                                        int p, int iters, int ns_order,
+                                                                        double2* __restrict__ Xout,
+                                                                        double* __restrict__ eps_last) {
+  extern __shared__ __align__(16) double gsm[];
+  constexpr int ld = Gen<N>::kLd, kW = N / 8, kThreadsC = 32 * kW;
+  __shared__ double red[kW];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  Pl Am, X, P, V;
+  warp_planes<N>(gsm, Am, X, P, V);
+  for (int64_t s = blockIdx.x; s < batch; s += gridDim.x) {
+    const double2* As = A + s * N * N;
+    for (int e = threadIdx.x; e < N * N; e += kThreadsC) {
+      const double2 v = __ldg(As + e);
+      Am.re[(e / N) * ld + e % N] = v.x;
+      Am.im[(e / N) * ld + e % N] = v.y;
+    }
+    // X0 = diag(A)^-1 (Smith's reciprocal, as jacobi_x0)
+    for (int i = threadIdx.x; i < N * ld; i += kThreadsC) {
+      X.re[i] = 0.0;
+      X.im[i] = 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x < N) {
+      const int r = threadIdx.x;
+      const double c = Am.re[r * ld + r], d = Am.im[r * ld + r];
+      double xr, xi;
+      if (fabs(c) >= fabs(d)) {
+        const double q = d / c, den = c + d * q;
+        xr = (1.0 + 0.0 * q) / den;
+        xi = (0.0 - 1.0 * q) / den;
+      } else {
+        const double q = c / d, den = c * q + d;
+        xr = (1.0 * q + 0.0) / den;
+        xi = (0.0 * q - 1.0) / den;
+      }
+      X.re[r * ld + r] = xr;
+      X.im[r * ld + r] = xi;
+    }
+    __syncthreads();
+    if (ns_order < 0) {
+      for (int it = 0; it < iters; ++it) {
+        product_coop<N>(X, Am, -1.0, nullptr, 0.0, 1.0, P, w, g, t, false);  // P = I − X·A
+        const Pl* v = &X;
+        for (int j = 1; j <= p; ++j) {  // V = X + P·V, V starting at X
+          product_coop<N>(P, *v, 1.0, &X, 1.0, 0.0, V, w, g, t, false);
+          v = &V;
+        }
+        for (int i = threadIdx.x; i < N * ld; i += kThreadsC) {
+          X.re[i] = V.re[i];
+          X.im[i] = V.im[i];
+        }
+        __syncthreads();
+      }
+      if (eps_last) {
+        const double ss = warp_sum(product_coop<N>(X, Am, -1.0, nullptr, 0.0, 1.0, P, w, g, t, true));
+        if (lane == 0) red[w] = ss;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          double tot = 0.0;
+          for (int i = 0; i < kW; ++i) tot += red[i];
+          eps_last[s] = sqrt(tot) / sqrt(static_cast<double>(N));
+        }
+      }
+    } else if (ns_order > 0) {
+      // NS: P = I − X0·A, T = I + P, T = T·P + I (order−1 times), X = T·X0
+      product_coop<N>(X, Am, -1.0, nullptr, 0.0, 1.0, P, w, g, t, false);
+      for (int i = threadIdx.x; i < N * ld; i += kThreadsC) {
+        V.re[i] = P.re[i];
+        V.im[i] = P.im[i];
+      }
+      __syncthreads();
+      if (threadIdx.x < N) V.re[threadIdx.x * ld + threadIdx.x] += 1.0;
+      __syncthreads();
+      for (int step = 2; step <= ns_order; ++step) product_coop<N>(V, P, 1.0, nullptr, 0.0, 1.0, V, w, g, t, false);
+      product_coop<N>(V, X, 1.0, nullptr, 0.0, 0.0, P, w, g, t, false);
+      for (int i = threadIdx.x; i < N * ld; i += kThreadsC) {
+        X.re[i] = P.re[i];
+        X.im[i] = P.im[i];
+      }
+      __syncthreads();
+    }
+    double2* Xs = Xout + s * N * N;
+    for (int e = threadIdx.x; e < N * N; e += kThreadsC)
+      Xs[e] = make_double2(X.re[(e / N) * ld + e % N], X.im[(e / N) * ld + e % N]);
+    __syncthreads();  // X, A are rewritten by the next system
+  }
+}
+
+template <int N>
+int launch_coop(int64_t batch, cudaStream_t s, void** args) {
+  constexpr int threads = 32 * (N / 8);
+  const int smem = static_cast<int>(Gen<N>::kBytesPerWarp);  // one system's matrices
+  NNB_TRY(ensure_smem<batched_gen_coop_kernel<N>>(smem));
+  int per_sm = 0, dev = 0, sms = 0;
+  NNB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batched_gen_coop_kernel<N>, threads, smem));
+  NNB_CUDA(cudaGetDevice(&dev));
+  NNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const unsigned grid =
+      static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)sms * std::max(1, per_sm))));
+  NNB_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(batched_gen_coop_kernel<N>), dim3(grid), dim3(threads), args,
+                            smem, s));
+  count_launch();
+  return 0;
+}
+
 template <auto K>
 int launch_gen(size_t smem_per_warp, int64_t batch, cudaStream_t s, void** args) {
   int warps = static_cast<int>(std::min<size_t>(4, (200 * 1024) / smem_per_warp));
@@ -313,8 +489,8 @@ int batched_nn_gen(const double* A, int64_t batch, int n, int p, int iters, int 
   void* args[] = {&a, &batch, &p, &iters, &ns_order, &x, &eps};
   switch (n) {
     case 8: return launch_gen<batched_gen_kernel<8>>(Gen<8>::kBytesPerWarp, batch, s, args);
-    case 24: return launch_gen<batched_gen_kernel<24>>(Gen<24>::kBytesPerWarp, batch, s, args);
-    case 32: return launch_gen<batched_gen_kernel<32>>(Gen<32>::kBytesPerWarp, batch, s, args);
+    case 24: return launch_coop<24>(batch, s, args);
+    case 32: return launch_coop<32>(batch, s, args);
     default: return fail(1, "batched: n must be 8, 16, 24 or 32");
   }
 }
