@@ -355,6 +355,81 @@ __device__ double product_coop(const Pl& L, const Pl& R, double alpha, const Pl*
   return ss;
 }
 
+// Jacobi X0 and the NN (ns_order < 0) or NS (ns_order > 0) iteration on the system in Am,
+// by the block's n/8 warps; returns eps = ‖I − X·A‖_F/√n after the last nest (NN, want_eps)
+template <int N>
+__device__ double solve_coop(const Pl& Am, const Pl& X, const Pl& P, const Pl& V, int p, int iters, int ns_order,
+                             int w, int g, int t, bool want_eps, double* red) {
+  constexpr int ld = Gen<N>::kLd, kW = N / 8, kThreadsC = 32 * kW;
+  const int lane = threadIdx.x & 31;
+  // X0 = diag(A)^-1 (Smith's reciprocal, as jacobi_x0)
+  for (int i = threadIdx.x; i < N * ld; i += kThreadsC) {
+    X.re[i] = 0.0;
+    X.im[i] = 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x < N) {
+    const int r = threadIdx.x;
+    const double c = Am.re[r * ld + r], d = Am.im[r * ld + r];
+    double xr, xi;
+    if (fabs(c) >= fabs(d)) {
+      const double q = d / c, den = c + d * q;
+      xr = (1.0 + 0.0 * q) / den;
+      xi = (0.0 - 1.0 * q) / den;
+    } else {
+      const double q = c / d, den = c * q + d;
+      xr = (1.0 * q + 0.0) / den;
+      xi = (0.0 * q - 1.0) / den;
+    }
+    X.re[r * ld + r] = xr;
+    X.im[r * ld + r] = xi;
+  }
+  __syncthreads();
+  double eps = 0.0;
+  if (ns_order < 0) {
+    for (int it = 0; it < iters; ++it) {
+      product_coop<N>(X, Am, -1.0, nullptr, 0.0, 1.0, P, w, g, t, false);  // P = I − X·A
+      const Pl* v = &X;
+      for (int j = 1; j <= p; ++j) {  // V = X + P·V, V starting at X
+        product_coop<N>(P, *v, 1.0, &X, 1.0, 0.0, V, w, g, t, false);
+        v = &V;
+      }
+      for (int i = threadIdx.x; i < N * ld; i += kThreadsC) {
+        X.re[i] = V.re[i];
+        X.im[i] = V.im[i];
+      }
+      __syncthreads();
+    }
+    if (want_eps) {
+      const double ss = warp_sum(product_coop<N>(X, Am, -1.0, nullptr, 0.0, 1.0, P, w, g, t, true));
+      if (lane == 0) red[w] = ss;
+      __syncthreads();
+      double tot = 0.0;
+      for (int i = 0; i < kW; ++i) tot += red[i];
+      eps = sqrt(tot) / sqrt(static_cast<double>(N));
+      __syncthreads();  // red is reused by the next system
+    }
+  } else if (ns_order > 0) {
+    // NS: P = I − X0·A, T = I + P, T = T·P + I (order−1 times), X = T·X0
+    product_coop<N>(X, Am, -1.0, nullptr, 0.0, 1.0, P, w, g, t, false);
+    for (int i = threadIdx.x; i < N * ld; i += kThreadsC) {
+      V.re[i] = P.re[i];
+      V.im[i] = P.im[i];
+    }
+    __syncthreads();
+    if (threadIdx.x < N) V.re[threadIdx.x * ld + threadIdx.x] += 1.0;
+    __syncthreads();
+    for (int step = 2; step <= ns_order; ++step) product_coop<N>(V, P, 1.0, nullptr, 0.0, 1.0, V, w, g, t, false);
+    product_coop<N>(V, X, 1.0, nullptr, 0.0, 0.0, P, w, g, t, false);
+    for (int i = threadIdx.x; i < N * ld; i += kThreadsC) {
+      X.re[i] = P.re[i];
+      X.im[i] = P.im[i];
+    }
+    __syncthreads();
+  }
+  return eps;
+}
+
 template <int N>
 __global__ void __launch_bounds__(32 * (N / 8)) batched_gen_coop_kernel(const double2* __restrict__ A, int64_t batch,
                                                                         int p, int iters, int ns_order,
@@ -373,71 +448,9 @@ __global__ void __launch_bounds__(32 * (N / 8)) batched_gen_coop_kernel(const do
       Am.re[(e / N) * ld + e % N] = v.x;
       Am.im[(e / N) * ld + e % N] = v.y;
     }
-    // X0 = diag(A)^-1 (Smith's reciprocal, as jacobi_x0)
-    for (int i = threadIdx.x; i < N * ld; i += kThreadsC) {
-      X.re[i] = 0.0;
-      X.im[i] = 0.0;
-    }
-    __syncthreads();
-    if (threadIdx.x < N) {
-      const int r = threadIdx.x;
-      const double c = Am.re[r * ld + r], d = Am.im[r * ld + r];
-      double xr, xi;
-      if (fabs(c) >= fabs(d)) {
-        const double q = d / c, den = c + d * q;
-        xr = (1.0 + 0.0 * q) / den;
-        xi = (0.0 - 1.0 * q) / den;
-      } else {
-        const double q = c / d, den = c * q + d;
-        xr = (1.0 * q + 0.0) / den;
-        xi = (0.0 * q - 1.0) / den;
-      }
-      X.re[r * ld + r] = xr;
-      X.im[r * ld + r] = xi;
-    }
-    __syncthreads();
-    if (ns_order < 0) {
-      for (int it = 0; it < iters; ++it) {
-        product_coop<N>(X, Am, -1.0, nullptr, 0.0, 1.0, P, w, g, t, false);  // P = I − X·A
-        const Pl* v = &X;
-        for (int j = 1; j <= p; ++j) {  // V = X + P·V, V starting at X
-          product_coop<N>(P, *v, 1.0, &X, 1.0, 0.0, V, w, g, t, false);
-          v = &V;
-        }
-        for (int i = threadIdx.x; i < N * ld; i += kThreadsC) {
-          X.re[i] = V.re[i];
-          X.im[i] = V.im[i];
-        }
-        __syncthreads();
-      }
-      if (eps_last) {
-        const double ss = warp_sum(product_coop<N>(X, Am, -1.0, nullptr, 0.0, 1.0, P, w, g, t, true));
-        if (lane == 0) red[w] = ss;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          double tot = 0.0;
-          for (int i = 0; i < kW; ++i) tot += red[i];
-          eps_last[s] = sqrt(tot) / sqrt(static_cast<double>(N));
-        }
-      }
-    } else if (ns_order > 0) {
-      // NS: P = I − X0·A, T = I + P, T = T·P + I (order−1 times), X = T·X0
-      product_coop<N>(X, Am, -1.0, nullptr, 0.0, 1.0, P, w, g, t, false);
-      for (int i = threadIdx.x; i < N * ld; i += kThreadsC) {
-        V.re[i] = P.re[i];
-        V.im[i] = P.im[i];
-      }
-      __syncthreads();
-      if (threadIdx.x < N) V.re[threadIdx.x * ld + threadIdx.x] += 1.0;
-      __syncthreads();
-      for (int step = 2; step <= ns_order; ++step) product_coop<N>(V, P, 1.0, nullptr, 0.0, 1.0, V, w, g, t, false);
-      product_coop<N>(V, X, 1.0, nullptr, 0.0, 0.0, P, w, g, t, false);
-      for (int i = threadIdx.x; i < N * ld; i += kThreadsC) {
-        X.re[i] = P.re[i];
-        X.im[i] = P.im[i];
-      }
-      __syncthreads();
-    }
+    // (solve_coop's first barrier orders these stores before any read)
+    const double eps = solve_coop<N>(Am, X, P, V, p, iters, ns_order, w, g, t, eps_last != nullptr, red);
+    if (eps_last && threadIdx.x == 0 && ns_order < 0) eps_last[s] = eps;
     double2* Xs = Xout + s * N * N;
     for (int e = threadIdx.x; e < N * N; e += kThreadsC)
       Xs[e] = make_double2(X.re[(e / N) * ld + e % N], X.im[(e / N) * ld + e % N]);
@@ -445,19 +458,87 @@ __global__ void __launch_bounds__(32 * (N / 8)) batched_gen_coop_kernel(const do
   }
 }
 
+// Fused detector for n = 24, 32 users, one block of n/8 warps per uplink: warp w forms the
+// 8-row stripe w of A = Hᴴ·H + σ²I (4M DMMA over the antennas), threads < n form z = Hᴴ·y,
+// then the NN inverse (solve_coop) and x̂ = X·z.
 template <int N>
+__global__ void __launch_bounds__(32 * (N / 8)) detect_gen_coop_kernel(const double2* __restrict__ H,
+                                                                       const double2* __restrict__ Y, int64_t batch,
+                                                                       int ant, double sigma2, int p, int iters,
+                                                                       double2* __restrict__ xhat,
+                                                                       double2* __restrict__ Xout,
+                                                                       double* __restrict__ eps_last) {
+  extern __shared__ __align__(16) double gsm[];
+  constexpr int ld = Gen<N>::kLd, kW = N / 8, kThreadsC = 32 * kW;
+  __shared__ double red[kW];
+  __shared__ double zs[2][N];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  Pl Am, X, P, V;
+  warp_planes<N>(gsm, Am, X, P, V);
+  for (int64_t s = blockIdx.x; s < batch; s += gridDim.x) {
+    const double2* Hs = H + s * (int64_t)ant * N;
+    const double2* Ys = Y + s * (int64_t)ant;
+#pragma unroll 1
+    for (int tj = 0; tj < Gen<N>::kT; ++tj) {
+      double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+      for (int kb = 0; kb < ant / 4; ++kb) {
+        const int a = 4 * kb + t;
+        const double2 hl = __ldg(Hs + (int64_t)a * N + 8 * w + g);  // conj → (x, −y)
+        const double2 hr = __ldg(Hs + (int64_t)a * N + 8 * tj + g);
+        dmma_8x8x4(cr[0], cr[1], hl.x, hr.x);
+        dmma_8x8x4(cr[0], cr[1], hl.y, hr.y);  // −(−y)·y
+        dmma_8x8x4(ci[0], ci[1], hl.x, hr.y);
+        dmma_8x8x4(ci[0], ci[1], -hl.y, hr.x);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = 8 * w + g, c = 8 * tj + 2 * t + h;
+        Am.re[r * ld + c] = cr[h] + (r == c ? sigma2 : 0.0);
+        Am.im[r * ld + c] = ci[h];
+      }
+    }
+    if (threadIdx.x < N) {
+      double zr = 0.0, zi = 0.0;
+      for (int a = 0; a < ant; ++a) {
+        const double2 h = __ldg(Hs + (int64_t)a * N + threadIdx.x), y = __ldg(Ys + a);
+        zr = fma(h.x, y.x, fma(h.y, y.y, zr));
+        zi = fma(h.x, y.y, fma(-h.y, y.x, zi));
+      }
+      zs[0][threadIdx.x] = zr;
+      zs[1][threadIdx.x] = zi;
+    }
+    const double eps = solve_coop<N>(Am, X, P, V, p, iters, -1, w, g, t, eps_last != nullptr, red);
+    if (eps_last && threadIdx.x == 0) eps_last[s] = eps;
+    if (threadIdx.x < N) {  // x̂ = X·z, row threadIdx.x
+      double xr = 0.0, xi = 0.0;
+      for (int j = 0; j < N; ++j) {
+        const double a = X.re[threadIdx.x * ld + j], b = X.im[threadIdx.x * ld + j];
+        xr = fma(a, zs[0][j], fma(-b, zs[1][j], xr));
+        xi = fma(a, zs[1][j], fma(b, zs[0][j], xi));
+      }
+      xhat[s * N + threadIdx.x] = make_double2(xr, xi);
+    }
+    if (Xout) {
+      double2* Xs = Xout + s * N * N;
+      for (int e = threadIdx.x; e < N * N; e += kThreadsC)
+        Xs[e] = make_double2(X.re[(e / N) * ld + e % N], X.im[(e / N) * ld + e % N]);
+    }
+    __syncthreads();  // A, X, z are rewritten by the next uplink
+  }
+}
+
+template <int N, auto K>
 int launch_coop(int64_t batch, cudaStream_t s, void** args) {
   constexpr int threads = 32 * (N / 8);
   const int smem = static_cast<int>(Gen<N>::kBytesPerWarp);  // one system's matrices
-  NNB_TRY(ensure_smem<batched_gen_coop_kernel<N>>(smem));
+  NNB_TRY(ensure_smem<K>(smem));
   int per_sm = 0, dev = 0, sms = 0;
-  NNB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batched_gen_coop_kernel<N>, threads, smem));
+  NNB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K, threads, smem));
   NNB_CUDA(cudaGetDevice(&dev));
   NNB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const unsigned grid =
       static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)sms * std::max(1, per_sm))));
-  NNB_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(batched_gen_coop_kernel<N>), dim3(grid), dim3(threads), args,
-                            smem, s));
+  NNB_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(K), dim3(grid), dim3(threads), args, smem, s));
   count_launch();
   return 0;
 }
@@ -489,8 +570,8 @@ int batched_nn_gen(const double* A, int64_t batch, int n, int p, int iters, int 
   void* args[] = {&a, &batch, &p, &iters, &ns_order, &x, &eps};
   switch (n) {
     case 8: return launch_gen<batched_gen_kernel<8>>(Gen<8>::kBytesPerWarp, batch, s, args);
-    case 24: return launch_coop<24>(batch, s, args);
-    case 32: return launch_coop<32>(batch, s, args);
+    case 24: return launch_coop<24, batched_gen_coop_kernel<24>>(batch, s, args);
+    case 32: return launch_coop<32, batched_gen_coop_kernel<32>>(batch, s, args);
     default: return fail(1, "batched: n must be 8, 16, 24 or 32");
   }
 }
@@ -505,8 +586,8 @@ int mimo_detect_gen(const double* H, const double* y, int64_t batch, int antenna
   void* args[] = {&h, &yy, &batch, &antennas, &sigma2, &p, &iters, &xh, &x, &eps};
   switch (users) {
     case 8: return launch_gen<detect_gen_kernel<8>>(Gen<8>::kBytesPerWarp, batch, s, args);
-    case 24: return launch_gen<detect_gen_kernel<24>>(Gen<24>::kBytesPerWarp, batch, s, args);
-    case 32: return launch_gen<detect_gen_kernel<32>>(Gen<32>::kBytesPerWarp, batch, s, args);
+    case 24: return launch_coop<24, detect_gen_coop_kernel<24>>(batch, s, args);
+    case 32: return launch_coop<32, detect_gen_coop_kernel<32>>(batch, s, args);
     default: return fail(1, "mimo detect: users must be 8, 16, 24 or 32");
   }
 }
