@@ -56,6 +56,30 @@ __device__ __forceinline__ void tile_mma(const Pl& L, const Pl& R, int ti, int t
   }
 }
 
+// 3M (Gauss) for one 8×8 tile: P1 = Σ lr·rr, P2 = Σ li·ri, P3 = Σ (lr+li)(rr+ri);
+// re = P1 − P2, im = P3 − P1 − P2 — 3 DMMA and 2 pre-sum DADDs per k-step instead of 4 DMMA
+template <int N>
+__device__ __forceinline__ void tile_mma3(const Pl& L, const Pl& R, int ti, int tj, int g, int t, double (&cr)[2],
+                                          double (&ci)[2]) {
+  constexpr int ld = Gen<N>::kLd;
+  double p1[2] = {0.0, 0.0}, p2[2] = {0.0, 0.0}, p3[2] = {0.0, 0.0};
+#pragma unroll
+  for (int kb = 0; kb < N / 4; ++kb) {
+    const int ar = 8 * ti + g, ac = 4 * kb + t;
+    const int br = 4 * kb + t, bc = 8 * tj + g;
+    const double lr = L.re[ar * ld + ac], li = L.im[ar * ld + ac];
+    const double rr = R.re[br * ld + bc], ri = R.im[br * ld + bc];
+    dmma_8x8x4(p1[0], p1[1], lr, rr);
+    dmma_8x8x4(p2[0], p2[1], li, ri);
+    dmma_8x8x4(p3[0], p3[1], lr + li, rr + ri);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    cr[h] = p1[h] - p2[h];
+    ci[h] = p3[h] - p1[h] - p2[h];
+  }
+}
+
 // out = alpha·(L·R) + beta·D + gamma·I over all tiles (out may alias any operand: every
 // tile is formed in registers before the first store);
 // returns this lane's Σ |out|² when want_ss
@@ -70,7 +94,7 @@ __device__ double product(const Pl& L, const Pl& R, double alpha, const Pl* D, d
 #pragma unroll
     for (int tj = 0; tj < Gen<N>::kT; ++tj) {
       double cr[2], ci[2];
-      tile_mma<N>(L, R, ti, tj, g, t, cr, ci);
+      tile_mma3<N>(L, R, ti, tj, g, t, cr, ci);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int r = 8 * ti + g, c = 8 * tj + 2 * t + h;
@@ -294,30 +318,6 @@ __global__ void __launch_bounds__(128) detect_gen_kernel(const double2* __restri
 // meet at a block barrier before the stripe is stored (the output may alias an operand)
 // and after; 3 (n=32) or 5 (n=24) systems per SM, 12-15 warps.  Products are 3M (Gauss):
 // 25 % fewer DMMAs than the one-warp kernel's 4M, within the parity tolerance.
-// 3M (Gauss) for one 8×8 tile: P1 = Σ lr·rr, P2 = Σ li·ri, P3 = Σ (lr+li)(rr+ri);
-// re = P1 − P2, im = P3 − P1 − P2 — 3 DMMA and 2 pre-sum DADDs per k-step instead of 4 DMMA
-template <int N>
-__device__ __forceinline__ void tile_mma3(const Pl& L, const Pl& R, int ti, int tj, int g, int t, double (&cr)[2],
-                                          double (&ci)[2]) {
-  constexpr int ld = Gen<N>::kLd;
-  double p1[2] = {0.0, 0.0}, p2[2] = {0.0, 0.0}, p3[2] = {0.0, 0.0};
-#pragma unroll
-  for (int kb = 0; kb < N / 4; ++kb) {
-    const int ar = 8 * ti + g, ac = 4 * kb + t;
-    const int br = 4 * kb + t, bc = 8 * tj + g;
-    const double lr = L.re[ar * ld + ac], li = L.im[ar * ld + ac];
-    const double rr = R.re[br * ld + bc], ri = R.im[br * ld + bc];
-    dmma_8x8x4(p1[0], p1[1], lr, rr);
-    dmma_8x8x4(p2[0], p2[1], li, ri);
-    dmma_8x8x4(p3[0], p3[1], lr + li, rr + ri);
-  }
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    cr[h] = p1[h] - p2[h];
-    ci[h] = p3[h] - p1[h] - p2[h];
-  }
-}
-
 template <int N>
 __device__ double product_coop(const Pl& L, const Pl& R, double alpha, const Pl* D, double beta, double gamma,
                                const Pl& out, int w, int g, int t, bool want_ss) {
