@@ -16,10 +16,10 @@
 // same inputs, so x is bit-identical to the reference and to the one-launch kernels
 // (tests: array_equal, and the 4096² SHA-256 golden).
 //
-// Layout: a 1008-thread block owns a TX × TY = 128 × 64 output tile; its region is
-// (TX + 2S) × (TY + 2S) = 144 × 80 cells, two double buffers (ping-pong between
-// steps) and one code byte per cell: 196 KB of shared memory, filled by cp.async
-// (the whole region in flight at once).  Thread (cx, seg) sweeps column cx over a
+// Layout: a 512-thread block owns a TX × TY = 112 × 32 output tile; its region is
+// (TX + 2S) × (TY + 2S) = 128 × 48 cells, two double buffers (ping-pong between
+// steps) and one code byte per cell: 104 KB of shared memory with the patterns, filled
+// by cp.async (the whole region in flight at once), two blocks per SM.  Thread (cx, seg) sweeps column cx over a
 // 12-row segment with the column's y−1 / y / y+1 values in
 // registers (a sliding window), so a cell costs three shared loads (own row below,
 // left, right) and one store; a row's pattern (mask + 5 values) is reloaded only
@@ -36,11 +36,21 @@
 namespace nnb {
 namespace {
 
-constexpr int kTX = 128, kTY = 64, kS = 8;
-constexpr int kRX = kTX + 2 * kS, kRY = kTY + 2 * kS;  // 144 × 80
-constexpr int kSeg = 7, kSegRows = (kRY + kSeg - 1) / kSeg;  // 7 segments of <= 12 rows
-constexpr int kThreads = kRX * kSeg;                         // 1008 (31.5 warps)
-constexpr int kSmem = 2 * kRX * kRY * 8 + kRX * kRY + kRowDictMax * 48;
+// 112 × 32 output tiles, 8-cell halo: a 128 × 48 region, 4 column segments of 12 rows (512
+// threads); with the pattern table sized to the patterns in use a block needs 104 KB, so
+// two blocks share an SM and one's region loads and barriers overlap the other's steps
+// (128 × 64 tiles at one 1008-thread block per SM: 3.30 ms per C5 solve; 3.19 with the
+// table trimmed, 3.14 at two blocks per SM — though 1.71 region cells are computed per
+// output cell against 1.41)
+constexpr int kTX = 112, kTY = 32, kS = 8;
+constexpr int kRX = kTX + 2 * kS, kRY = kTY + 2 * kS;  // 128 × 48
+constexpr int kSeg = 4, kSegRows = (kRY + kSeg - 1) / kSeg;  // 4 segments of 12 rows
+constexpr int kThreads = kRX * kSeg;                         // 512
+constexpr int kMinBlocks = 2;
+// two region buffers, the region's codes, then the patterns in use (npat)
+constexpr int kSmemBase = 2 * kRX * kRY * 8 + (kRX * kRY + 15) / 16 * 16;
+inline int tb_smem(int npat) { return kSmemBase + npat * 48; }
+constexpr int kSmem = kSmemBase + kRowDictMax * 48;
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 8 : 0)
@@ -128,7 +138,7 @@ __device__ __forceinline__ bool sweep(const double* __restrict__ src, double* __
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
     stencil_tb_kernel(const double* __restrict__ tin, const uint8_t* __restrict__ rcode,
                       const double* __restrict__ zold, double* __restrict__ out, const StPat* __restrict__ pats,
                       int npat, int W, int H, int steps, double theta, int* __restrict__ flag, int ty0,
@@ -136,8 +146,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(16) uint8_t sm[];
   double* buf0 = reinterpret_cast<double*>(sm);
   double* buf1 = buf0 + kRX * kRY;
-  StPat* spat = reinterpret_cast<StPat*>(buf1 + kRX * kRY);
-  uint8_t* code = reinterpret_cast<uint8_t*>(spat + kRowDictMax);
+  uint8_t* code = reinterpret_cast<uint8_t*>(buf1 + kRX * kRY);
+  StPat* spat = reinterpret_cast<StPat*>(code + (kRX * kRY + 15) / 16 * 16);
   const int x0 = blockIdx.x * kTX - kS, y0 = (blockIdx.y + ty0) * kTY + y_off - kS;
   for (int i = threadIdx.x; i < npat; i += kThreads) spat[i] = pats[i];
   // the region through cp.async (all of it in flight at once; cells off the grid zero-filled)
@@ -306,15 +316,15 @@ int stencil_pass(const double* tin, const uint8_t* rcode, const double* zold, do
   const StPat* pats = reinterpret_cast<const StPat*>(table_dev);
   switch (mode) {
     case kInner:
-      stencil_tb_kernel<kInner><<<grid, kThreads, kSmem, s>>>(tin, rcode, zold, out, pats, npat, W, H, steps, theta,
+      stencil_tb_kernel<kInner><<<grid, kThreads, tb_smem(npat), s>>>(tin, rcode, zold, out, pats, npat, W, H, steps, theta,
                                                               flag, ty0, y_off);
       break;
     case kFactorEnd:
-      stencil_tb_kernel<kFactorEnd><<<grid, kThreads, kSmem, s>>>(tin, rcode, zold, out, pats, npat, W, H, steps,
+      stencil_tb_kernel<kFactorEnd><<<grid, kThreads, tb_smem(npat), s>>>(tin, rcode, zold, out, pats, npat, W, H, steps,
                                                                   theta, flag, ty0, y_off);
       break;
     default:
-      stencil_tb_kernel<kFinal><<<grid, kThreads, kSmem, s>>>(tin, rcode, zold, out, pats, npat, W, H, steps, theta,
+      stencil_tb_kernel<kFinal><<<grid, kThreads, tb_smem(npat), s>>>(tin, rcode, zold, out, pats, npat, W, H, steps, theta,
                                                               flag, ty0, y_off);
   }
   count_launch();
