@@ -809,11 +809,11 @@ def run_sparse(args, world, rank):
     moved = 63 * (mat + 2 * n * 8)  # bytes of the consumed format (operator + t in + t out): the roofline
     gbs, moved_gbs = alg / (ms * 1e-3) / 1e9, moved / (ms * 1e-3) / 1e9
     if fname == "row-dictionary-stencil-tb":
-        # temporal blocking: t crosses HBM once per pass of up to 8 applications (plus halos),
+        # temporal blocking: t crosses HBM once per pass of up to 4 applications (plus halos),
         # so the bytes moved per application are below one read + one write of t
-        per_launch = (f"{moved / 63:.0f} bytes moved per application, averaged over the solve's 10 passes "
-                      "(t in + t out once per pass of up to 8 applications, 1-byte row codes; whole solve timed "
-                      "incl. the per-solve format pass); the 8-step pass is issue-bound "
+        per_launch = (f"{moved / 63:.0f} bytes moved per application, averaged over the solve's 17 passes "
+                      "(t in + t out once per pass of up to 4 applications, 1-byte row codes; whole solve timed "
+                      "incl. the per-solve format pass); the pass is issue-bound "
                       "(profiles/r02_ncu_stencil_tb.txt), so this fraction is not its limit")
     else:
         per_launch = (f"{mat:.0f} operator bytes + 2N*8 per application (x63, whole solve timed "

@@ -114,16 +114,19 @@ int stencil_patterns(const double2* pat, const uint8_t* plen, int npat, int widt
                      std::vector<StencilPattern>& tab, cudaStream_t s);
 int stencil_edges_ok(const uint8_t* rcode, const StencilPattern* table_dev, int W, int H, bool top, bool bottom,
                      bool* ok, cudaStream_t s);
-// one temporal-blocked pass: `steps` (<= stencil_max_steps()) applications over a W×H grid
-// Output tile rows [ty0, ty1) only (ty1 < 0: to the last) of the out_rows rows from row
-// y_off (out_rows < 0: all H); the grid's other rows are inputs only (a slab's halo rows).
+// Pass depths (most applications per launch): the whole-grid solve's, and the row slabs'
+// (fewer passes, so fewer halo exchanges; a slab's halo is kStencilDepthSlab grid rows)
+constexpr int kStencilDepthSolo = 4, kStencilDepthSlab = 8;
+// one temporal-blocked pass: `steps` (<= depth) applications over a W×H grid, in the tile
+// shape of that depth.  Output tile rows [ty0, ty1) only (ty1 < 0: to the last) of the
+// out_rows rows from row y_off (out_rows < 0: all H); the grid's other rows are inputs only
+// (a slab's halo rows).
 int stencil_pass(const double* tin, const uint8_t* rcode, const double* zold, double* out,
                  const StencilPattern* table_dev, int npat, int W, int H, int steps, int mode, double theta, int* flag,
-                 cudaStream_t s, int ty0 = 0, int ty1 = -1, int y_off = 0, int out_rows = -1);
-int stencil_tile_rows();
-int stencil_max_steps();
-double stencil_region_ratio();
-// The whole factorized solve (one RHS) in passes of up to 8 applications per launch;
+                 int depth, cudaStream_t s, int ty0 = 0, int ty1 = -1, int y_off = 0, int out_rows = -1);
+int stencil_tile_rows(int depth);
+double stencil_region_ratio(int depth);
+// The whole factorized solve (one RHS) in passes of up to 4 applications per launch;
 // bit-identical to run_factors.  *bytes_moved: HBM bytes the passes stream.
 int stencil_factors(const uint8_t* rcode, const DevBuf& table, int npat, int W, int H, const double* B,
                     int s_factors, double theta, double* X, double* z[2], double* tb[2], int* flags,

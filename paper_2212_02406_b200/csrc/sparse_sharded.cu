@@ -143,7 +143,7 @@ struct Slab {
   int npat = 0;
   int64_t ext_len() const { return h_lo + rows + h_hi; }
   // temporal blocking across slabs (5-point stencils, slabs whole grid rows): the slab's
-  // grid rows plus kTbRows halo rows on each inner side, codes in the global pattern table
+  // grid rows plus tb_rows() halo rows on each inner side, codes in the global pattern table
   bool tb = false;
   int tbW = 0;
   int64_t tb_lo = 0, tb_hi = 0;  // halo cells above / below (0 at the grid's edges)
@@ -160,7 +160,8 @@ struct TbRecord {
   double w = 0, edges_ok = 0, npat = 0, pad = 0;
   StencilPattern tab[kRowDictMax];
 };
-constexpr int kTbRows = 8;  // halo grid rows = applications per pass (sparse_stencil.cu kS)
+// halo grid rows = the most applications a slab pass runs
+constexpr int tb_rows() { return kStencilDepthSlab; }
 
 // the slab's own-pattern record (W, edge check over its own rows, table)
 int tb_record(const Slab& sl, int64_t n, TbRecord* rec, cudaStream_t s) {
@@ -184,7 +185,7 @@ int tb_record(const Slab& sl, int64_t n, TbRecord* rec, cudaStream_t s) {
 }
 
 // Decides temporal blocking from every rank's record (identical on every rank): one W, the
-// grid rows whole per slab, every slab at least kTbRows rows (each neighbour's halo comes
+// grid rows whole per slab, every slab at least tb_rows() rows (each neighbour's halo comes
 // from one slab), clean edges, and at most kRowDictMax patterns in the union of the tables
 // (in rank order).  map[g][c]: rank g's code c in the union.
 bool tb_decide(const std::vector<TbRecord>& recs, const std::vector<int64_t>& rows, std::vector<StencilPattern>& table,
@@ -193,7 +194,7 @@ bool tb_decide(const std::vector<TbRecord>& recs, const std::vector<int64_t>& ro
   const double w = recs[0].w;
   if (w <= 0) return false;
   for (int g = 0; g < G; ++g)
-    if (recs[g].w != w || recs[g].edges_ok != 1.0 || rows[g] < kTbRows * (int64_t)w) return false;
+    if (recs[g].w != w || recs[g].edges_ok != 1.0 || rows[g] < tb_rows() * (int64_t)w) return false;
   table.clear();
   map.assign(G, std::vector<uint8_t>(kRowDictMax, 0));
   for (int g = 0; g < G; ++g)
@@ -224,8 +225,8 @@ __global__ void remap_codes_kernel(const uint8_t* __restrict__ in, int64_t count
 int tb_setup_slab(Slab& sl, int64_t n, int W, const std::vector<uint8_t>& lut, cudaStream_t s) {
   sl.tb = true;
   sl.tbW = W;
-  sl.tb_lo = sl.row0 > 0 ? (int64_t)kTbRows * W : 0;
-  sl.tb_hi = sl.row0 + sl.rows < n ? (int64_t)kTbRows * W : 0;
+  sl.tb_lo = sl.row0 > 0 ? (int64_t)tb_rows() * W : 0;
+  sl.tb_hi = sl.row0 + sl.rows < n ? (int64_t)tb_rows() * W : 0;
   const int64_t len = sl.tb_len();
   NNB_TRY(sl.tb_mem.alloc(sizeof(double) * 6 * len + len + kRowDictMax + 64, s));
   double* d = sl.tb_mem.as<double>();
@@ -243,8 +244,8 @@ int tb_setup_slab(Slab& sl, int64_t n, int W, const std::vector<uint8_t>& lut, c
   return 0;
 }
 
-// The temporal-blocked factorized solve over row slabs: per pass (up to kTbRows
-// applications, sparse_stencil.cu) the kTbRows·W halo cells of its input are exchanged
+// The temporal-blocked factorized solve over row slabs: per pass (up to tb_rows()
+// applications, sparse_stencil.cu) the tb_rows()·W halo cells of its input are exchanged
 // once, then each slab runs the pass over its extended grid; the halo rows' values go
 // stale from the outside in, one row per application, never reaching the slab's own rows.
 // Each own row is computed as in the single-GPU pass (bitwise the same inputs), so x stays
@@ -256,8 +257,7 @@ int tb_setup_slab(Slab& sl, int64_t n, int W, const std::vector<uint8_t>& lut, c
 template <class Exchange, class Join>
 int run_slabs_tb(std::vector<Slab*>& slabs, const StencilPattern* table, int npat, int s_factors, double theta,
                  std::vector<double*>& x_own, Exchange exchange, Join join, cudaStream_t s, cudaStream_t bs) {
-  const int kmax = stencil_max_steps(), ty = stencil_tile_rows();
-  (void)kmax;
+  const int kmax = kStencilDepthSlab, ty = stencil_tile_rows(kStencilDepthSlab);
   int zcur = 4, zi = 0;  // Z starts as B (tb_ext[4])
   for (int f = 0; f < s_factors; ++f) {
     int64_t left = int64_t(1) << f;
@@ -275,7 +275,7 @@ int run_slabs_tb(std::vector<Slab*>& slabs, const StencilPattern* table, int npa
         const int hlo = (int)(sl->tb_lo / W), hhi = (int)(sl->tb_hi / W), R = (int)(sl->rows / W);
         if (!bs) {
           NNB_TRY(stencil_pass(sl->tb_ext[tin], sl->tb_code, sl->tb_ext[zcur], sl->tb_ext[out], table, npat, W, H,
-                               steps, mode, theta, sl->flags + f, s, 0, -1, hlo, R));
+                               steps, mode, theta, sl->flags + f, kmax, s, 0, -1, hlo, R));
           continue;
         }
         // own tile row t reads region rows [hlo + t·ty − kmax, hlo + t·ty + ty + kmax)
@@ -288,11 +288,11 @@ int run_slabs_tb(std::vector<Slab*>& slabs, const StencilPattern* table, int npa
         }
         if (t0 > t1) t0 = t1 = 0;
         NNB_TRY(stencil_pass(sl->tb_ext[tin], sl->tb_code, sl->tb_ext[zcur], sl->tb_ext[out], table, npat, W, H,
-                             steps, mode, theta, sl->flags + f, s, t0, t1, hlo, R));
+                             steps, mode, theta, sl->flags + f, kmax, s, t0, t1, hlo, R));
         NNB_TRY(stencil_pass(sl->tb_ext[tin], sl->tb_code, sl->tb_ext[zcur], sl->tb_ext[out], table, npat, W, H,
-                             steps, mode, theta, sl->flags + f, bs, 0, t0, hlo, R));
+                             steps, mode, theta, sl->flags + f, kmax, bs, 0, t0, hlo, R));
         NNB_TRY(stencil_pass(sl->tb_ext[tin], sl->tb_code, sl->tb_ext[zcur], sl->tb_ext[out], table, npat, W, H,
-                             steps, mode, theta, sl->flags + f, bs, t1, -1, hlo, R));
+                             steps, mode, theta, sl->flags + f, kmax, bs, t1, -1, hlo, R));
       }
       NNB_TRY(join());
       if (mode == kInner) {
@@ -620,15 +620,15 @@ int nnb_sparse_plan_create(nnb_comm_t comm, const int64_t* row_ptr, const int32_
       NNB_CUDA(cudaMemcpyAsync(plan->tb_table.p, table.data(), sizeof(StencilPattern) * table.size(),
                                cudaMemcpyHostToDevice, s));
       plan->tb_npat = (int)table.size();
-      // the neighbours' edge codes into the halo rows (kTbRows·W bytes = W doubles each way)
-      const size_t hw = (size_t)kTbRows * W / sizeof(double);
+      // the neighbours' edge codes into the halo rows (tb_rows()·W bytes each way)
+      const size_t hw = (size_t)tb_rows() * W / sizeof(double);
       NNB_NCCL2(nccl_group(true));
       if (me > 0) {
         NNB_NCCL2(nccl_send(sl.tb_code + sl.tb_lo, hw, me - 1, comm, s));
         NNB_NCCL2(nccl_recv(sl.tb_code, hw, me - 1, comm, s));
       }
       if (me < G - 1) {
-        NNB_NCCL2(nccl_send(sl.tb_code + sl.tb_lo + sl.rows - (int64_t)kTbRows * W, hw, me + 1, comm, s));
+        NNB_NCCL2(nccl_send(sl.tb_code + sl.tb_lo + sl.rows - (int64_t)tb_rows() * W, hw, me + 1, comm, s));
         NNB_NCCL2(nccl_recv(sl.tb_code + sl.tb_lo + sl.rows, hw, me + 1, comm, s));
       }
       NNB_NCCL2(nccl_group(false));
@@ -669,10 +669,10 @@ int nnb_sparse_plan_solve(nnb_sparse_plan_t plan, const double* B_rows, int64_t 
   NNB_TRY(x.prepare(X_rows, (size_t)(sl.rows * k), s));
   std::vector<Slab*> slabs{&sl};
   std::vector<double*> xo{x.d};
-  auto exchange_tb = [&](int e) -> int {  // kTbRows·W cells each way, once per pass
+  auto exchange_tb = [&](int e) -> int {  // tb_rows()·W cells each way, once per pass
     if (G == 1) return 0;
     double* ext = sl.tb_ext[e];
-    const size_t hw = (size_t)kTbRows * sl.tbW;
+    const size_t hw = (size_t)tb_rows() * sl.tbW;
     NNB_CUDA(cudaEventRecord(plan->ready, s));
     NNB_CUDA(cudaStreamWaitEvent(comm->cs, plan->ready, 0));
     NNB_NCCL2(nccl_group(true));
@@ -819,7 +819,7 @@ int nnb_sparse_factorized_sharded_emulated_d(const int64_t* row_ptr, const int32
       NNB_CUDA(cudaMemcpyAsync(tb_table.p, table.data(), sizeof(StencilPattern) * table.size(),
                                cudaMemcpyHostToDevice, s));
       tb_npat = (int)table.size();
-      const int64_t hw = (int64_t)kTbRows * W;
+      const int64_t hw = (int64_t)tb_rows() * W;
       for (int g = 0; g < world; ++g) {  // the neighbours' edge codes into the halo rows
         Slab& sl = store[g];
         if (g > 0)
@@ -863,7 +863,7 @@ int nnb_sparse_factorized_sharded_emulated_d(const int64_t* row_ptr, const int32
   auto exchange_tb = [&](int e) -> int {  // device copies of the neighbours' edge rows
     for (int g = 0; g < world; ++g) {
       Slab& sl = store[g];
-      const int64_t hw = (int64_t)kTbRows * sl.tbW;
+      const int64_t hw = (int64_t)tb_rows() * sl.tbW;
       if (g > 0) {
         const Slab& pv = store[g - 1];
         NNB_CUDA(cudaMemcpyAsync(sl.tb_ext[e], pv.tb_ext[e] + pv.tb_lo + pv.rows - hw, sizeof(double) * hw,

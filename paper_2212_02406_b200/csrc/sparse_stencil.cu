@@ -16,10 +16,10 @@
 // same inputs, so x is bit-identical to the reference and to the one-launch kernels
 // (tests: array_equal, and the 4096² SHA-256 golden).
 //
-// Layout: a 512-thread block owns a TX × TY = 112 × 32 output tile; its region is
-// (TX + 2S) × (TY + 2S) = 128 × 48 cells, two double buffers (ping-pong between
-// steps) and one code byte per cell: 104 KB of shared memory with the patterns, filled
-// by cp.async (the whole region in flight at once), two blocks per SM.  Thread (cx, seg) sweeps column cx over a
+// Layout: a block owns a TX × TY output tile (112 × 40 at S = 4, 112 × 32 at S = 8); its
+// region is (TX + 2S) × (TY + 2S) = 120 × 48 / 128 × 48 cells, two double buffers
+// (ping-pong between steps) and one code byte per cell: ≤ 104 KB of shared memory with the
+// patterns, filled by cp.async (the whole region in flight at once), two blocks per SM.  Thread (cx, seg) sweeps column cx over a
 // 12-row segment with the column's y−1 / y / y+1 values in
 // registers (a sliding window), so a cell costs three shared loads (own row below,
 // left, right) and one store; a row's pattern (mask + 5 values) is reloaded only
@@ -29,6 +29,7 @@
 #include <cstring>
 #include <vector>
 
+#include "../../include/nnb.h"
 #include "common.cuh"
 #include "engine.cuh"
 #include "sparse.cuh"
@@ -36,21 +37,30 @@
 namespace nnb {
 namespace {
 
-// 112 × 32 output tiles, 8-cell halo: a 128 × 48 region, 4 column segments of 12 rows (512
-// threads); with the pattern table sized to the patterns in use a block needs 104 KB, so
-// two blocks share an SM and one's region loads and barriers overlap the other's steps
-// (128 × 64 tiles at one 1008-thread block per SM: 3.30 ms per C5 solve; 3.19 with the
-// table trimmed, 3.14 at two blocks per SM — though 1.71 region cells are computed per
-// output cell against 1.41)
-constexpr int kTX = 112, kTY = 32, kS = 8;
-constexpr int kRX = kTX + 2 * kS, kRY = kTY + 2 * kS;  // 128 × 48
-constexpr int kSeg = 4, kSegRows = (kRY + kSeg - 1) / kSeg;  // 4 segments of 12 rows
-constexpr int kThreads = kRX * kSeg;                         // 512
-constexpr int kMinBlocks = 2;
-// two region buffers, the region's codes, then the patterns in use (npat)
-constexpr int kSmemBase = 2 * kRX * kRY * 8 + (kRX * kRY + 15) / 16 * 16;
-inline int tb_smem(int npat) { return kSmemBase + npat * 48; }
-constexpr int kSmem = kSmemBase + kRowDictMax * 48;
+// Two tile shapes, chosen by the pass depth S (applications per launch): the whole-grid
+// solve runs 112 × 40 tiles with a 4-cell halo (a 120 × 48 region, 1.29 region cells per
+// output cell: 3.06 ms per C5 solve against 3.15 at 112 × 32 / S = 8, 1.71 cells), the row
+// slabs 112 × 32 with an 8-cell halo (128 × 48): half the passes, so half the halo
+// exchanges and launches per solve, which the slabs' schedule pays for more than the
+// region's extra cells.  Both: 4 column segments of 12 rows, 480 / 512 threads; with the
+// pattern table sized to the patterns in use a block needs ≤ 104 KB, so two blocks share an
+// SM and one's region loads and barriers overlap the other's steps (128 × 64 tiles at one
+// 1008-thread block per SM: 3.30 ms).
+constexpr int kTX = 112, kSeg = 4, kMinBlocks = 2;
+template <int S>
+struct Tile {
+  static constexpr int TY = S == 4 ? 40 : 32;
+  static constexpr int RX = kTX + 2 * S, RY = TY + 2 * S;
+  static constexpr int SegRows = (RY + kSeg - 1) / kSeg;
+  static constexpr int Threads = RX * kSeg;
+  // two region buffers, the region's codes, then the patterns in use (npat)
+  static constexpr int SmemBase = 2 * RX * RY * 8 + (RX * RY + 15) / 16 * 16;
+  static constexpr int Smem = SmemBase + kRowDictMax * 48;
+  static int smem(int npat) { return SmemBase + npat * 48; }
+};
+static_assert(Tile<kStencilDepthSolo>::RX % 4 == 0 && Tile<kStencilDepthSlab>::RX % 4 == 0 &&
+                  kStencilDepthSolo % 4 == 0 && kStencilDepthSlab % 4 == 0,
+              "codes load in 4-byte groups: region x0 and width multiples of 4");
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 8 : 0)
@@ -70,11 +80,12 @@ struct StPat {
 
 // One thread's column segment of one step.  UNI: the whole tile is one full 5-point
 // pattern (no per-cell code lookups); else each cell's pattern from its code.
-template <int MODE, bool UNI>
+template <int S, int MODE, bool UNI>
 __device__ __forceinline__ bool sweep(const double* __restrict__ src, double* __restrict__ dst,
                                       const uint8_t* __restrict__ code, const StPat* __restrict__ spat, int uc,
                                       int cx, int ya, int yb, int y0, int gx, int W, double theta, bool last,
                                       double* __restrict__ out) {
+  constexpr int kRX = Tile<S>::RX;
   bool bad = false;
   const double* col = src + cx;
   double tN = col[(ya - 1) * kRX], tC = col[ya * kRX];
@@ -137,12 +148,14 @@ __device__ __forceinline__ bool sweep(const double* __restrict__ src, double* __
   return bad;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+template <int S, int MODE>
+__global__ void __launch_bounds__(Tile<S>::Threads, kMinBlocks)
     stencil_tb_kernel(const double* __restrict__ tin, const uint8_t* __restrict__ rcode,
                       const double* __restrict__ zold, double* __restrict__ out, const StPat* __restrict__ pats,
                       int npat, int W, int H, int steps, double theta, int* __restrict__ flag, int ty0,
                       int y_off) {
+  constexpr int kS = S, kTY = Tile<S>::TY, kRX = Tile<S>::RX, kRY = Tile<S>::RY;
+  constexpr int kSegRows = Tile<S>::SegRows, kThreads = Tile<S>::Threads;
   extern __shared__ __align__(16) uint8_t sm[];
   double* buf0 = reinterpret_cast<double*>(sm);
   double* buf1 = buf0 + kRX * kRY;
@@ -197,8 +210,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       const int ya = max(max(seg * kSegRows, ylo), -y0);
       const int yb = min(min(min(seg * kSegRows + kSegRows, kRY), yhi), H - y0);
       if (ya < yb) {
-        if (uniform) bad |= sweep<MODE, true>(src, dst, code, spat, uc, cx, ya, yb, y0, gx, W, theta, last, out);
-        else bad |= sweep<MODE, false>(src, dst, code, spat, uc, cx, ya, yb, y0, gx, W, theta, last, out);
+        if (uniform) bad |= sweep<S, MODE, true>(src, dst, code, spat, uc, cx, ya, yb, y0, gx, W, theta, last, out);
+        else bad |= sweep<S, MODE, false>(src, dst, code, spat, uc, cx, ya, yb, y0, gx, W, theta, last, out);
       }
     }
     if (!last) __syncthreads();
@@ -301,45 +314,67 @@ int stencil_plan(int64_t n, const uint8_t* rcode, const double2* pat, const uint
   return 0;
 }
 
-int stencil_tile_rows() { return kTY; }
+int stencil_tile_rows(int depth) { return depth == kStencilDepthSlab ? Tile<kStencilDepthSlab>::TY : Tile<kStencilDepthSolo>::TY; }
 
-int stencil_pass(const double* tin, const uint8_t* rcode, const double* zold, double* out,
-                 const StencilPattern* table_dev, int npat, int W, int H, int steps, int mode, double theta, int* flag,
-                 cudaStream_t s, int ty0, int ty1, int y_off, int out_rows) {
-  NNB_TRY(ensure_smem<stencil_tb_kernel<kInner>>(kSmem));
-  NNB_TRY(ensure_smem<stencil_tb_kernel<kFactorEnd>>(kSmem));
-  NNB_TRY(ensure_smem<stencil_tb_kernel<kFinal>>(kSmem));
-  const int tiles_y = ((out_rows < 0 ? H : out_rows) + kTY - 1) / kTY;
+namespace {
+template <int S>
+int pass_launch(const double* tin, const uint8_t* rcode, const double* zold, double* out, const StPat* pats, int npat,
+                int W, int H, int steps, int mode, double theta, int* flag, cudaStream_t s, int ty0, int ty1,
+                int y_off, int out_rows) {
+  using T = Tile<S>;
+  NNB_TRY((ensure_smem<stencil_tb_kernel<S, kInner>>(T::Smem)));
+  NNB_TRY((ensure_smem<stencil_tb_kernel<S, kFactorEnd>>(T::Smem)));
+  NNB_TRY((ensure_smem<stencil_tb_kernel<S, kFinal>>(T::Smem)));
+  const int tiles_y = ((out_rows < 0 ? H : out_rows) + T::TY - 1) / T::TY;
   if (ty1 < 0 || ty1 > tiles_y) ty1 = tiles_y;
   if (ty0 >= ty1) return 0;
   const dim3 grid((unsigned)((W + kTX - 1) / kTX), (unsigned)(ty1 - ty0));
-  const StPat* pats = reinterpret_cast<const StPat*>(table_dev);
+  const int sm = T::smem(npat);
   switch (mode) {
     case kInner:
-      stencil_tb_kernel<kInner><<<grid, kThreads, tb_smem(npat), s>>>(tin, rcode, zold, out, pats, npat, W, H, steps, theta,
-                                                              flag, ty0, y_off);
+      stencil_tb_kernel<S, kInner><<<grid, T::Threads, sm, s>>>(tin, rcode, zold, out, pats, npat, W, H, steps, theta,
+                                                                flag, ty0, y_off);
       break;
     case kFactorEnd:
-      stencil_tb_kernel<kFactorEnd><<<grid, kThreads, tb_smem(npat), s>>>(tin, rcode, zold, out, pats, npat, W, H, steps,
-                                                                  theta, flag, ty0, y_off);
+      stencil_tb_kernel<S, kFactorEnd><<<grid, T::Threads, sm, s>>>(tin, rcode, zold, out, pats, npat, W, H, steps,
+                                                                    theta, flag, ty0, y_off);
       break;
     default:
-      stencil_tb_kernel<kFinal><<<grid, kThreads, tb_smem(npat), s>>>(tin, rcode, zold, out, pats, npat, W, H, steps, theta,
-                                                              flag, ty0, y_off);
+      stencil_tb_kernel<S, kFinal><<<grid, T::Threads, sm, s>>>(tin, rcode, zold, out, pats, npat, W, H, steps, theta,
+                                                                flag, ty0, y_off);
   }
   count_launch();
   NNB_CUDA(cudaGetLastError());
   return 0;
 }
+}  // namespace
 
-int stencil_max_steps() { return kS; }
-double stencil_region_ratio() { return (double)kRX * kRY / ((double)kTX * kTY); }
+int stencil_pass(const double* tin, const uint8_t* rcode, const double* zold, double* out,
+                 const StencilPattern* table_dev, int npat, int W, int H, int steps, int mode, double theta, int* flag,
+                 int depth, cudaStream_t s, int ty0, int ty1, int y_off, int out_rows) {
+  const StPat* pats = reinterpret_cast<const StPat*>(table_dev);
+  if (depth == kStencilDepthSlab) {
+    if (steps < 1 || steps > kStencilDepthSlab) return fail(NNB_ERR_DOMAIN, "stencil pass: steps outside 1..8");
+    return pass_launch<kStencilDepthSlab>(tin, rcode, zold, out, pats, npat, W, H, steps, mode, theta, flag, s, ty0,
+                                          ty1, y_off, out_rows);
+  }
+  if (depth != kStencilDepthSolo || steps < 1 || steps > kStencilDepthSolo)
+    return fail(NNB_ERR_DOMAIN, "stencil pass: depth not 4 / 8 or steps beyond it");
+  return pass_launch<kStencilDepthSolo>(tin, rcode, zold, out, pats, npat, W, H, steps, mode, theta, flag, s, ty0,
+                                        ty1, y_off, out_rows);
+}
+
+double stencil_region_ratio(int depth) {
+  const int S = depth == kStencilDepthSlab ? kStencilDepthSlab : kStencilDepthSolo;
+  const int TY = stencil_tile_rows(depth);
+  return (double)(kTX + 2 * S) * (TY + 2 * S) / ((double)kTX * TY);
+}
 
 int stencil_factors(const uint8_t* rcode, const DevBuf& table, int npat, int W, int H, const double* B,
                     int s_factors, double theta, double* X, double* z[2], double* tb[2], int* flags,
                     int64_t* bytes_moved, cudaStream_t s) {
   const double n = (double)W * H;
-  const double halo = stencil_region_ratio();  // region cells read per output cell
+  const double halo = stencil_region_ratio(kStencilDepthSolo);  // region cells read per output cell
   double moved = 0.0;
   const double* zcur = B;
   int zi = 0;
@@ -348,12 +383,12 @@ int stencil_factors(const uint8_t* rcode, const DevBuf& table, int npat, int W, 
     const double* tin = zcur;
     int ti = 0;
     while (left > 0) {
-      const int steps = (int)std::min<int64_t>(kS, left);
+      const int steps = (int)std::min<int64_t>(kStencilDepthSolo, left);
       left -= steps;
       const int mode = left > 0 ? kInner : (f == s_factors - 1 ? kFinal : kFactorEnd);
       double* out = mode == kInner ? tb[ti] : (mode == kFinal ? X : z[zi]);
       NNB_TRY(stencil_pass(tin, rcode, zcur, out, table.as<StencilPattern>(), npat, W, H, steps, mode, theta,
-                           flags + f, s));
+                           flags + f, kStencilDepthSolo, s));
       moved += n * (halo * (8.0 + 1.0) + 8.0 + (mode == kInner ? 0.0 : 8.0));
       if (mode == kInner) {
         tin = tb[ti];

@@ -90,7 +90,7 @@ def test_sparse_sharded_emulated_bitexact(ref, world):
 @pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_sparse_sharded_temporal_blocking_bitexact(ref, world):
     """Slabs of whole grid rows (64×64 grid: 32, 16 or 8 grid rows per slab) run the
-    temporal-blocked passes with an 8-row halo exchanged once per pass; x bit-identical to the
+    temporal-blocked passes with a halo of the pass depth exchanged once per pass; x bit-identical to the
     reference.  World 3 (slabs not whole grid rows) keeps one launch per application."""
     rp, col, val = W.laplacian_5pt(64)
     b = W.rhs(4096, seed=20 + world)

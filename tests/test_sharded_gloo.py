@@ -12,7 +12,7 @@ every rank (identical stop decisions).  The int8-emulated products of the same
 file (column statistics gathered and combined in rank order, residue blocks on
 the ring, K-block products accumulated mod m) are restated with integer numpy
 and checked against the whole product's residues; the sparse halo schedules (a
-halo per application, and the temporal-blocked slabs with an 8-row halo per pass)
+halo per application, and the temporal-blocked slabs with one halo exchange per pass)
 are checked bit-exact against the reference."""
 import os
 import socket
@@ -329,8 +329,8 @@ def test_int8_emulated_product_schedule_gloo(world):
 # ---------------------------------------------------------------- temporal-blocked slabs over gloo
 def _tb_worker(rank, world, port, grid, gamma, theta, out_q):
     """sparse_sharded.cu's temporal-blocked slab schedule (run_slabs_tb) restated with gloo and
-    scalar IEEE arithmetic in the reference's order: per pass of up to 8 applications the 8
-    halo grid rows of its input are exchanged once, the pass runs over the slab's extended
+    scalar IEEE arithmetic in the reference's order: per pass of up to D applications (D = 8,
+    sparse.cuh kStencilDepthSlab) the D halo grid rows of its input are exchanged once, the pass runs over the slab's extended
     rows (cells past them read as zero, so the halo goes stale one row per application and
     never reaches the own rows), and only the own rows are kept."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -341,8 +341,9 @@ def _tb_worker(rank, world, port, grid, gamma, theta, out_q):
     rp, col, val = W.laplacian_5pt(grid)
     b = W.rhs(n, seed=13)
     r0, rows = nnb.partition_rows(n, world, rank)
-    assert r0 % W_ == 0 and rows % W_ == 0 and rows >= 8 * W_
-    hw = 8 * W_
+    D = 8  # applications per pass = halo grid rows
+    assert r0 % W_ == 0 and rows % W_ == 0 and rows >= D * W_
+    hw = D * W_
     lo = hw if rank > 0 else 0
     hi = hw if rank < world - 1 else 0
     e0 = r0 - lo  # global index of the extended region's first cell
@@ -384,7 +385,7 @@ def _tb_worker(rank, world, port, grid, gamma, theta, out_q):
     for f in range(s_f):
         left, t = 1 << f, list(z)
         while left > 0:
-            steps = min(8, left)
+            steps = min(D, left)
             left -= steps
             exchange(t)
             for _ in range(steps):
