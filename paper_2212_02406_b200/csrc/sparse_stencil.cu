@@ -26,6 +26,7 @@
 // when its code changes along the sweep.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -88,6 +89,7 @@ __device__ __forceinline__ bool sweep(const double* __restrict__ src, double* __
   constexpr int kRX = Tile<S>::RX;
   bool bad = false;
   const double* col = src + cx;
+  int64_t r = (int64_t)(y0 + ya) * W + gx;  // the cell's global index (last step's output)
   double tN = col[(ya - 1) * kRX], tC = col[ya * kRX];
   int pc = UNI ? uc : -1;
   int mask = 31;
@@ -133,7 +135,6 @@ __device__ __forceinline__ bool sweep(const double* __restrict__ src, double* __
       // a non-finite value persists in its cell (t keeps its own term) and every cell is
       // some block's interior, so the pass's outputs see it: checking them flags the
       // same factor the reference's per-application check would
-      const int64_t r = (int64_t)(y0 + y) * W + gx;
       double o = t;
       if (MODE == kFactorEnd) o = __dadd_rn(dst[y * kRX + cx], t);                    // factorized.cpp:136
       else if (MODE == kFinal) o = __dmul_rn(__dadd_rn(dst[y * kRX + cx], t), theta);  // factorized.cpp:139
@@ -144,6 +145,7 @@ __device__ __forceinline__ bool sweep(const double* __restrict__ src, double* __
     }
     tN = tC;
     tC = tS;
+    r += W;
   }
   return bad;
 }
@@ -156,6 +158,8 @@ __global__ void __launch_bounds__(Tile<S>::Threads, kMinBlocks)
                       int y_off) {
   constexpr int kS = S, kTY = Tile<S>::TY, kRX = Tile<S>::RX, kRY = Tile<S>::RY;
   constexpr int kSegRows = Tile<S>::SegRows, kThreads = Tile<S>::Threads;
+  static_assert(kRY % kSeg == 0 && kThreads % (kRX / 4) == 0 && kRY % (kThreads / (kRX / 4)) == 0,
+                "region rows split evenly over the load passes");
   extern __shared__ __align__(16) uint8_t sm[];
   double* buf0 = reinterpret_cast<double*>(sm);
   double* buf1 = buf0 + kRX * kRY;
@@ -163,29 +167,47 @@ __global__ void __launch_bounds__(Tile<S>::Threads, kMinBlocks)
   StPat* spat = reinterpret_cast<StPat*>(code + (kRX * kRY + 15) / 16 * 16);
   const int x0 = blockIdx.x * kTX - kS, y0 = (blockIdx.y + ty0) * kTY + y_off - kS;
   for (int i = threadIdx.x; i < npat; i += kThreads) spat[i] = pats[i];
-  // the region through cp.async (all of it in flight at once; cells off the grid zero-filled)
+  const int cx = threadIdx.x % kRX, seg = threadIdx.x / kRX;
+  // the region through cp.async (all of it in flight at once; cells off the grid
+  // zero-filled): thread (cx, seg) loads column cx of rows seg, seg + kSeg, …, its
+  // address stepped by kSeg grid rows
+  {
+    const int gx = x0 + cx;
+    const bool xin = gx >= 0 && gx < W;
+    int64_t off = (int64_t)(y0 + seg) * W + gx;
+    const int64_t step = (int64_t)kSeg * W;
 #pragma unroll
-  for (int j = 0; j < (kRX * kRY + kThreads - 1) / kThreads; ++j) {
-    const int i = threadIdx.x + j * kThreads;
-    if (i >= kRX * kRY) break;
-    const int gx = x0 + i % kRX, gy = y0 + i / kRX;
-    const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
-    cp_async8(buf0 + i, in ? tin + (int64_t)gy * W + gx : tin, in);
+    for (int j = 0; j < kRY / kSeg; ++j) {
+      const int gy = y0 + seg + j * kSeg;
+      const bool in = xin && gy >= 0 && gy < H;
+      cp_async8(buf0 + (seg + j * kSeg) * kRX + cx, in ? tin + off : tin, in);
+      off += step;
+    }
   }
-  for (int i = threadIdx.x; i < kRX * kRY / 4; i += kThreads) {  // codes in 4-byte groups (W % 4 == 0)
-    const int gx = x0 + (4 * i) % kRX, gy = y0 + (4 * i) / kRX;
-    const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
-    cp_async4(code + 4 * i, in ? rcode + (int64_t)gy * W + gx : rcode, in);
+  {  // codes in 4-byte groups (W % 4 == 0, x0 % 4 == 0): group g of rows r, r + kCodeRowStep, …
+    constexpr int kGroups = kRX / 4, kCodeRowStep = kThreads / kGroups;
+    const int g = threadIdx.x % kGroups, r = threadIdx.x / kGroups;
+    const int gx = x0 + 4 * g;
+    const bool xin = gx >= 0 && gx < W;
+    int64_t off = (int64_t)(y0 + r) * W + gx;
+#pragma unroll
+    for (int j = 0; j < kRY / kCodeRowStep; ++j) {
+      const int gy = y0 + r + j * kCodeRowStep;
+      const bool in = xin && gy >= 0 && gy < H;
+      cp_async4(code + (r + j * kCodeRowStep) * kRX + 4 * g, in ? rcode + off : rcode, in);
+      off += (int64_t)kCodeRowStep * W;
+    }
   }
   cp_async_wait_all();
   __syncthreads();
   // a tile whose whole region is one full 5-point pattern (all but the grid's edge
   // tiles) skips the per-cell code lookups
-  int uc = code[0];
+  const int uc = code[0];
   bool uniform = spat[uc].mask == 31 && x0 >= 0 && y0 >= 0 && x0 + kRX <= W && y0 + kRY <= H;
-  for (int i = threadIdx.x; i < kRX * kRY && uniform; i += kThreads) uniform = code[i] == uc;
+  const uint32_t uc4 = 0x01010101u * (uint32_t)uc;
+  for (int i = threadIdx.x; i < kRX * kRY / 4 && uniform; i += kThreads)
+    uniform = reinterpret_cast<const uint32_t*>(code)[i] == uc4;
   uniform = __syncthreads_and(uniform);
-  const int cx = threadIdx.x % kRX, seg = threadIdx.x / kRX;
   const int gx = x0 + cx;
   const bool col_in = gx >= 0 && gx < W;
   bool bad = false;
@@ -196,11 +218,17 @@ __global__ void __launch_bounds__(Tile<S>::Threads, kMinBlocks)
     const int xlo = kS - m, xhi = kS + kTX + m, ylo = kS - m, yhi = kS + kTY + m;
     const bool last = s == steps;
     if (last && MODE != kInner) {  // Z of the interior into the free buffer, one wait per pass
-      for (int i = threadIdx.x; i < kTX * kTY; i += kThreads) {
-        const int rx = kS + i % kTX, ry = kS + i / kTX;
-        const int gxx = x0 + rx, gyy = y0 + ry;
-        const bool in = gxx < W && gyy < H;
-        cp_async8(dst + ry * kRX + rx, in ? zold + (int64_t)gyy * W + gxx : zold, in);
+      static_assert(kTY % kSeg == 0, "interior rows split evenly over the segments");
+      if (cx >= kS && cx < kS + kTX) {  // column cx of interior rows kS + seg, kS + seg + kSeg, …
+        const bool xin = gx < W;
+        int64_t off = (int64_t)(y0 + kS + seg) * W + gx;
+#pragma unroll
+        for (int j = 0; j < kTY / kSeg; ++j) {
+          const int ry = kS + seg + j * kSeg;
+          const bool in = xin && y0 + ry < H;
+          cp_async8(dst + ry * kRX + cx, in ? zold + off : zold, in);
+          off += (int64_t)kSeg * W;
+        }
       }
       cp_async_wait_all();
       __syncthreads();
@@ -373,8 +401,10 @@ double stencil_region_ratio(int depth) {
 int stencil_factors(const uint8_t* rcode, const DevBuf& table, int npat, int W, int H, const double* B,
                     int s_factors, double theta, double* X, double* z[2], double* tb[2], int* flags,
                     int64_t* bytes_moved, cudaStream_t s) {
+  int depth = kStencilDepthSolo;
+  if (const char* e = debug_env("NNB_STENCIL_DEPTH")) depth = std::atoi(e) == 8 ? 8 : 4;  // A/B only
   const double n = (double)W * H;
-  const double halo = stencil_region_ratio(kStencilDepthSolo);  // region cells read per output cell
+  const double halo = stencil_region_ratio(depth);  // region cells read per output cell
   double moved = 0.0;
   const double* zcur = B;
   int zi = 0;
@@ -383,12 +413,12 @@ int stencil_factors(const uint8_t* rcode, const DevBuf& table, int npat, int W, 
     const double* tin = zcur;
     int ti = 0;
     while (left > 0) {
-      const int steps = (int)std::min<int64_t>(kStencilDepthSolo, left);
+      const int steps = (int)std::min<int64_t>(depth, left);
       left -= steps;
       const int mode = left > 0 ? kInner : (f == s_factors - 1 ? kFinal : kFactorEnd);
       double* out = mode == kInner ? tb[ti] : (mode == kFinal ? X : z[zi]);
       NNB_TRY(stencil_pass(tin, rcode, zcur, out, table.as<StencilPattern>(), npat, W, H, steps, mode, theta,
-                           flags + f, kStencilDepthSolo, s));
+                           flags + f, depth, s));
       moved += n * (halo * (8.0 + 1.0) + 8.0 + (mode == kInner ? 0.0 : 8.0));
       if (mode == kInner) {
         tin = tb[ti];
