@@ -560,67 +560,159 @@ __global__ void rowdict_encode_kernel(const uint8_t* __restrict__ code, int widt
 // into its key, and the key looked up in the row table; only the row code is
 // written.  Any miss (a pair or row outside the sampled tables, a longer row)
 // sets *collision and the caller takes the two-pass build.
-__global__ void rowdict_direct_encode_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                                             const double* __restrict__ val, int64_t rows, int64_t row0,
-                                             const DictWs* ws, const RowDictWs* rws, int width,
-                                             uint8_t* __restrict__ rcode, int* collision) {
+//
+// A warp takes 32 consecutive rows: their nonzeros are one contiguous range, loaded
+// coalesced (lane j of load i: element 32·i + j) into the warp's shared buffer, then
+// each lane encodes its row from there.  The next chunk's row offsets are loaded
+// before this chunk's nonzeros are used, so one memory latency per chunk, not two
+// (one thread per row with rp → col/val dependent loads ran at 0.67 of HBM).
+constexpr int kEncWarps = 8;
+template <bool kNarrow>
+__global__ void __launch_bounds__(kEncWarps * 32)
+    rowdict_direct_encode_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                 const double* __restrict__ val, int64_t rows, int64_t row0, const DictWs* ws,
+                                 const RowDictWs* rws, int width, uint8_t* __restrict__ rcode, int* collision) {
+  __shared__ int32_t s_col[kEncWarps][2][32 * kEllMaxWidth];
+  __shared__ unsigned long long s_val[kEncWarps][2][32 * kEllMaxWidth];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   bool bad = false, have = false;
   unsigned long long last = 0;
-  int last_idx = -1;
+  int last_idx = -1, last_len = -1;
   // the last verified pair at each position (compile-time indexed: registers): a
-  // thread's rows, one grid stride apart, mostly repeat them, so the pair table
-  // is probed only when a position's pair changes
+  // lane's rows, one chunk stride apart, mostly repeat them, so the pair table is
+  // probed only when a position's pair changes
   int32_t cd[kEllMaxWidth];
   unsigned long long cb[kEllMaxWidth];
   int ci[kEllMaxWidth];
 #pragma unroll
   for (int i = 0; i < kEllMaxWidth; ++i) ci[i] = -1;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e0 = rp[r], len = rp[r + 1] - e0;
-    if (len > width) {
-      bad = true;
-      continue;
+  const int64_t chunks = (rows + 31) / 32, stride = (int64_t)gridDim.x * kEncWarps;
+  auto load_rp = [&](int64_t cc, int64_t& l, int64_t& h) {
+    l = h = 0;
+    const int64_t r = cc * 32 + lane;
+    if (cc < chunks && r < rows) {
+      l = rp[r];
+      h = rp[r + 1];
     }
-    unsigned long long key = ~0ull;
+  };
+  // chunk cc's nonzeros straight into buffer b (cp.async: no registers), one commit group
+  auto issue = [&](int64_t cc, int64_t l, int64_t h, int b, int64_t& base, int64_t& cnt) {
+    base = cnt = 0;
+    if (cc < chunks) {
+      const int nr = (int)(rows - cc * 32 < 32 ? rows - cc * 32 : 32);
+      base = __shfl_sync(0xffffffffu, l, 0);
+      cnt = __shfl_sync(0xffffffffu, h, nr - 1) - base;
+      if (cnt <= 32 * width) {  // else some row is longer than width: bad
+        const int n32 = (int)cnt;
 #pragma unroll
-    for (int i = 0; i < kEllMaxWidth; ++i) {
-      if (i >= len) break;
-      const int64_t dl = (int64_t)col[e0 + i] - (row0 + r);
-      const int32_t d = static_cast<int32_t>(dl);
-      const unsigned long long b = __double_as_longlong(val[e0 + i]);
-      if (!(ci[i] >= 0 && cd[i] == d && cb[i] == b && dl == d)) {
-        const unsigned long long h = pair_hash(d, b);
-        int slot = static_cast<int>(h & (kDictSlots - 1));
-        int probe = 0;
-        while (ws->hash[slot] != h && ws->hash[slot] != 0 && probe < kDictSlots) {
-          slot = (slot + 1) & (kDictSlots - 1);
-          ++probe;
+        for (int i = 0; i < kEllMaxWidth; ++i) {
+          const int k = 32 * i + lane;
+          if (k < n32) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&s_col[warp][b][k])),
+                         "l"(col + base + k)
+                         : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(&s_val[warp][b][k])),
+                         "l"(val + base + k)
+                         : "memory");
+          }
         }
-        const bool hit = dl >= INT32_MIN && dl <= INT32_MAX && ws->hash[slot] == h && ws->delta[slot] == d &&
-                         __double_as_longlong(ws->val[slot]) == static_cast<long long>(b);
-        bad |= !hit;
-        cd[i] = d;
-        cb[i] = b;
-        ci[i] = hit ? ws->index[slot] : -1;
       }
-      const unsigned long long q = ci[i] >= 0 ? static_cast<unsigned long long>(ci[i]) : 0ull;
-      key = (key & ~(0xffull << (8 * i))) | (q << (8 * i));
     }
-    if (!have || key != last) {
-      const unsigned long long h = key_hash(key);
-      int slot = static_cast<int>(h & (kDictSlots - 1));
-      int probe = 0;
-      while (rws->hash[slot] != h && rws->hash[slot] != 0 && probe < kDictSlots) {
-        slot = (slot + 1) & (kDictSlots - 1);
-        ++probe;
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  // two chunks in flight per warp: chunk c + stride's nonzeros and chunk c + 2·stride's
+  // offsets load while chunk c is encoded
+  int64_t c = blockIdx.x * (int64_t)kEncWarps + warp;
+  int64_t lo, hi, base, cnt, lo1, hi1;
+  load_rp(c, lo, hi);
+  issue(c, lo, hi, 0, base, cnt);
+  load_rp(c + stride, lo1, hi1);
+  for (int b = 0; c < chunks; c += stride, b ^= 1) {
+    int64_t base1, cnt1, lo2, hi2;
+    issue(c + stride, lo1, hi1, b ^ 1, base1, cnt1);
+    load_rp(c + 2 * stride, lo2, hi2);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    const int64_t r = c * 32 + lane;
+    const bool fits = cnt <= 32 * width;
+    const int32_t* wc = s_col[warp][b];
+    const unsigned long long* wv = s_val[warp][b];
+    if (r < rows) {
+      const int64_t len = hi - lo;
+      if (!fits || len > width) {
+        bad = true;
+      } else {
+        const int off = (int)(lo - base);
+        // fast path: the same length and (delta, value) at every position as this lane's
+        // last row — the same key, so the same code (32-bit deltas when every row index
+        // fits: kNarrow)
+        bool same = have && len == last_len;
+        if (same) {
+#pragma unroll
+          for (int i = 0; i < kEllMaxWidth; ++i) {
+            if (i < len) {
+              if (kNarrow) {
+                same &= wc[off + i] - (int32_t)(row0 + r) == cd[i] && wv[off + i] == cb[i];
+              } else {
+                const int64_t dl = (int64_t)wc[off + i] - (row0 + r);
+                same &= dl == cd[i] && wv[off + i] == cb[i];
+              }
+            }
+          }
+        }
+        if (!same) {
+          last_len = (int)len;
+          unsigned long long key = ~0ull;
+#pragma unroll
+          for (int i = 0; i < kEllMaxWidth; ++i) {
+            if (i >= len) break;
+            const int64_t dl = (int64_t)wc[off + i] - (row0 + r);
+            const int32_t d = static_cast<int32_t>(dl);
+            const unsigned long long b = wv[off + i];
+            if (!(ci[i] >= 0 && cd[i] == d && cb[i] == b && dl == d)) {
+              const unsigned long long h = pair_hash(d, b);
+              int slot = static_cast<int>(h & (kDictSlots - 1));
+              int probe = 0;
+              while (ws->hash[slot] != h && ws->hash[slot] != 0 && probe < kDictSlots) {
+                slot = (slot + 1) & (kDictSlots - 1);
+                ++probe;
+              }
+              const bool hit = dl >= INT32_MIN && dl <= INT32_MAX && ws->hash[slot] == h && ws->delta[slot] == d &&
+                               __double_as_longlong(ws->val[slot]) == static_cast<long long>(b);
+              bad |= !hit;
+              cd[i] = d;
+              cb[i] = b;
+              ci[i] = hit ? ws->index[slot] : -1;
+            }
+            const unsigned long long q = ci[i] >= 0 ? static_cast<unsigned long long>(ci[i]) : 0ull;
+            key = (key & ~(0xffull << (8 * i))) | (q << (8 * i));
+          }
+          if (!have || key != last) {
+            const unsigned long long h = key_hash(key);
+            int slot = static_cast<int>(h & (kDictSlots - 1));
+            int probe = 0;
+            while (rws->hash[slot] != h && rws->hash[slot] != 0 && probe < kDictSlots) {
+              slot = (slot + 1) & (kDictSlots - 1);
+              ++probe;
+            }
+            last_idx = (rws->hash[slot] == h && rws->key[slot] == key) ? rws->index[slot] : -1;
+            last = key;
+            have = true;
+          }
+        }
+        bad |= last_idx < 0;
+        rcode[r] = static_cast<uint8_t>(last_idx < 0 ? 0 : last_idx);
       }
-      last_idx = (rws->hash[slot] == h && rws->key[slot] == key) ? rws->index[slot] : -1;
-      last = key;
-      have = true;
     }
-    bad |= last_idx < 0;
-    rcode[r] = static_cast<uint8_t>(last_idx < 0 ? 0 : last_idx);
+    __syncwarp();
+    lo = lo1;
+    hi = hi1;
+    base = base1;
+    cnt = cnt1;
+    lo1 = lo2;
+    hi1 = hi2;
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   if (bad) atomicOr(collision, 1);
 }
 
@@ -1020,8 +1112,16 @@ int build_row_dict_direct(const int64_t* rp, const int32_t* col, const double* v
   NNB_CUDA(cudaStreamSynchronize(s));
   if (f[2] || rf[1] || rf[3] > kRowDictMax) return 0;
   // every row: pair codes verified, row key looked up, one byte written
-  rowdict_direct_encode_kernel<<<rows_grid(rows), 256, 0, s>>>(rp, col, val, rows, row0, ws, rws, w, rcode,
-                                                               &rws->collision);
+  {
+    const unsigned grid =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>(148 * 8, ((rows + 31) / 32 + kEncWarps - 1) / kEncWarps));
+    if (row0 + rows < INT32_MAX)
+      rowdict_direct_encode_kernel<true><<<grid, kEncWarps * 32, 0, s>>>(rp, col, val, rows, row0, ws, rws, w, rcode,
+                                                                         &rws->collision);
+    else
+      rowdict_direct_encode_kernel<false><<<grid, kEncWarps * 32, 0, s>>>(rp, col, val, rows, row0, ws, rws, w, rcode,
+                                                                          &rws->collision);
+  }
   count_launch();
   NNB_CUDA(cudaGetLastError());
   NNB_CUDA(cudaMemcpyAsync(rf, &rws->count, sizeof(rf), cudaMemcpyDeviceToHost, s));
