@@ -31,6 +31,7 @@
 #include <cstring>
 #include <vector>
 
+#include "../../include/nnb.h"
 #include "engine.cuh"
 #include "sparse.cuh"
 
@@ -1072,7 +1073,7 @@ int build_row_dict(const uint8_t* code, int width, int64_t plane, int64_t rows, 
 int build_row_dict_direct(const int64_t* rp, const int32_t* col, const double* val, int64_t rows, int64_t row0,
                           int32_t* dict_delta, double* dict_val, int* dict_size, int* width, int* band_lo,
                           int* band_hi, uint8_t* rcode, double2* pat, uint8_t* plen, int* npat, bool* ok,
-                          cudaStream_t s) {
+                          cudaStream_t s, std::vector<double2>* pat_host, std::vector<uint8_t>* plen_host) {
   *ok = false;
   constexpr int64_t kSample = 65536;
   if (rows <= 4 * kSample) return 0;  // small operators: the two-pass build
@@ -1106,12 +1107,9 @@ int build_row_dict_direct(const int64_t* rp, const int32_t* col, const double* v
   rowdict_insert_kernel<<<rows_grid(plane), 256, 0, s>>>(sc, w, plane, plane, rws);
   rowdict_index_kernel<<<1, 1024, 0, s>>>(rws, w, dict_delta, dict_val, pat, plen);
   count_launch(4);
-  int rf[4];  // count, overflow, collision, size
-  NNB_CUDA(cudaMemcpyAsync(f, &ws->count, sizeof(f), cudaMemcpyDeviceToHost, s));
-  NNB_CUDA(cudaMemcpyAsync(rf, &rws->count, sizeof(rf), cudaMemcpyDeviceToHost, s));
-  NNB_CUDA(cudaStreamSynchronize(s));
-  if (f[2] || rf[1] || rf[3] > kRowDictMax) return 0;
-  // every row: pair codes verified, row key looked up, one byte written
+  // every row: pair codes verified, row key looked up, one byte written.  No wait for the
+  // sample's verdicts first: a sample collision or an overflowed row table only makes
+  // this pass miss (it writes nothing but rcode), and all of them are read below.
   {
     const unsigned grid =
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(148 * 8, ((rows + 31) / 32 + kEncWarps - 1) / kEncWarps));
@@ -1124,15 +1122,36 @@ int build_row_dict_direct(const int64_t* rp, const int32_t* col, const double* v
   }
   count_launch();
   NNB_CUDA(cudaGetLastError());
-  NNB_CUDA(cudaMemcpyAsync(rf, &rws->count, sizeof(rf), cudaMemcpyDeviceToHost, s));
+  // one round trip: the pair table's and row table's counters, the pair deltas (band)
+  // and, if asked for, the row patterns
+  const bool want_pat = pat_host && plen_host;
+  const size_t off_dd = 64, off_pat = off_dd + sizeof(int32_t) * kPairDictMax;
+  const size_t off_len = off_pat + sizeof(double2) * kRowDictMax * w;
+  const size_t bytes = want_pat ? off_len + kRowDictMax : off_pat;
+  uint8_t* h = static_cast<uint8_t*>(pinned_stage(bytes));
+  if (!h) return fail(NNB_ERR_OOM, "sparse: pinned staging buffer");
+  NNB_CUDA(cudaMemcpyAsync(h, &ws->count, sizeof(int) * 5, cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaMemcpyAsync(h + 32, &rws->count, sizeof(int) * 4, cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaMemcpyAsync(h + off_dd, dict_delta, sizeof(int32_t) * kPairDictMax, cudaMemcpyDeviceToHost, s));
+  if (want_pat) {
+    NNB_CUDA(cudaMemcpyAsync(h + off_pat, pat, sizeof(double2) * kRowDictMax * w, cudaMemcpyDeviceToHost, s));
+    NNB_CUDA(cudaMemcpyAsync(h + off_len, plen, kRowDictMax, cudaMemcpyDeviceToHost, s));
+  }
   NNB_CUDA(cudaStreamSynchronize(s));
-  if (rf[2]) return 0;
-  std::vector<int32_t> dh(f[3]);
-  NNB_CUDA(cudaMemcpy(dh.data(), dict_delta, sizeof(int32_t) * dh.size(), cudaMemcpyDeviceToHost));
+  int rf[4];  // count, overflow, collision, size
+  std::memcpy(f, h, sizeof(int) * 5);
+  std::memcpy(rf, h + 32, sizeof(rf));
+  if (f[1] || f[2] || f[3] > kPairDictMax - 1 || rf[1] || rf[2] || rf[3] > kRowDictMax) return 0;
+  const int32_t* dh = reinterpret_cast<const int32_t*>(h + off_dd);
   *band_lo = *band_hi = 0;
-  for (int32_t d : dh) {
-    *band_lo = std::min(*band_lo, d);
-    *band_hi = std::max(*band_hi, d);
+  for (int i = 0; i < f[3]; ++i) {
+    *band_lo = std::min(*band_lo, dh[i]);
+    *band_hi = std::max(*band_hi, dh[i]);
+  }
+  if (want_pat) {
+    const double2* hp = reinterpret_cast<const double2*>(h + off_pat);
+    pat_host->assign(hp, hp + (size_t)rf[3] * w);
+    plen_host->assign(h + off_len, h + off_len + rf[3]);
   }
   *dict_size = f[3];
   *width = w;
@@ -1235,6 +1254,8 @@ int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* 
     // operators with <= 255 distinct (column − row, value) pairs: 1 byte per nonzero
     DevBuf dict_buf, code_buf, rowdict_buf;
     PairDict dict;
+    std::vector<double2> pat_host;  // the direct build's row patterns (empty otherwise)
+    std::vector<uint8_t> plen_host;
     if (dict_on && !force32) {
       NNB_TRY(dict_buf.alloc((sizeof(int32_t) + sizeof(double)) * kPairDictMax, s));
       double* dv = dict_buf.as<double>();
@@ -1261,7 +1282,7 @@ int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* 
       // over the CSR writing only the row codes (no ELL pair codes are materialised)
       if (want_rows && direct_on)
         NNB_TRY(build_row_dict_direct(row_ptr, col, val, n, 0, dd, dv, &size, &width, &lo, &hi, rcode, pat, plen,
-                                      &npat, &rok, s));
+                                      &npat, &rok, s, &pat_host, &plen_host));
       if (rok) {
         dict = PairDict{nullptr, dd, dv, size, width, 0, lo, hi, rcode, pat, plen, npat};
       } else {
@@ -1294,25 +1315,35 @@ int sparse_factorized(const int64_t* row_ptr, const int32_t* col, const double* 
       DevBuf table;
       int W = 0, H = 0;
       bool sok = false;
-      NNB_TRY(stencil_plan(n, dict.rcode, dict.rpat, dict.rlen, dict.npat, dict.ell_width, table, &W, &H, &sok, s));
+      // with the direct build's host patterns: no round trip before the passes, the edge
+      // check's verdict (flags[63]) read with the factors' flags after them
+      const bool host_pat = (int)plen_host.size() == dict.npat && dict.npat > 0;
+      NNB_TRY(stencil_plan(n, dict.rcode, dict.rpat, dict.rlen, dict.npat, dict.ell_width, table, &W, &H, &sok, s,
+                           host_pat ? pat_host.data() : nullptr, host_pat ? plen_host.data() : nullptr,
+                           host_pat ? flags + 63 : nullptr));
       if (sok) {
         int64_t moved = 0;
         NNB_TRY(stencil_factors(dict.rcode, table, dict.npat, W, H, B, s_factors, theta, X, z, tb, flags, &moved, s));
-        set_sparse_bytes_per_nnz(1);
-        set_sparse_format("row-dictionary-stencil-tb");
-        // per application, averaged over the solve (the bench multiplies by the applications)
-        const int64_t apps = (int64_t(1) << s_factors) - 1;
-        set_sparse_matrix_bytes(moved / std::max<int64_t>(1, apps) - 2 * n * 8);
         NNB_CUDA(cudaGetLastError());
         int hf[64];
         NNB_CUDA(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, s));
         NNB_CUDA(cudaStreamSynchronize(s));
-        for (int f = 0; f < s_factors && f < 64; ++f)
-          if (hf[f]) {
-            if (fail_factor) *fail_factor = f;
-            return fail(3, "solve_sparse_factorized: non-finite block at factor " + std::to_string(f));
-          }
-        return 0;
+        if (!hf[63]) {
+          set_sparse_bytes_per_nnz(1);
+          set_sparse_format("row-dictionary-stencil-tb");
+          // per application, averaged over the solve (the bench multiplies by the applications)
+          const int64_t apps = (int64_t(1) << s_factors) - 1;
+          set_sparse_matrix_bytes(moved / std::max<int64_t>(1, apps) - 2 * n * 8);
+          for (int f = 0; f < s_factors && f < 64; ++f)
+            if (hf[f]) {
+              if (fail_factor) *fail_factor = f;
+              return fail(3, "solve_sparse_factorized: non-finite block at factor " + std::to_string(f));
+            }
+          return 0;
+        }
+        // a pattern reaches across the grid's edges: not a stencil after all; the passes'
+        // results are discarded and the solve runs one launch per application from B
+        NNB_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 64, s));
       }
     }
     set_sparse_bytes_per_nnz(dict.code || dict.rcode ? 1 : (fits ? 10 : 12));

@@ -84,11 +84,14 @@ int build_row_dict(const uint8_t* code, int width, int64_t plane, int64_t rows, 
 
 // Both tables from the first and last 65536 rows, then one verified pass over the
 // CSR writing only the row codes (operators above 4·65536 rows; *ok = false on any
-// miss, the caller then takes build_pair_dict + build_row_dict).
+// miss, the caller then takes build_pair_dict + build_row_dict).  Two host round
+// trips: the sample's width, then every verdict (and, when pat_host / plen_host are
+// given, host copies of the row patterns) in one pinned copy.
 int build_row_dict_direct(const int64_t* rp, const int32_t* col, const double* val, int64_t rows, int64_t row0,
                           int32_t* dict_delta, double* dict_val, int* dict_size, int* width, int* band_lo,
                           int* band_hi, uint8_t* rcode, double2* pat, uint8_t* plen, int* npat, bool* ok,
-                          cudaStream_t s);
+                          cudaStream_t s, std::vector<double2>* pat_host = nullptr,
+                          std::vector<uint8_t>* plen_host = nullptr);
 
 template <typename Idx>
 void spmv_apply(const SpmvOp<Idx>& op, int mode, int64_t r_begin, int64_t r_end, cudaStream_t s);
@@ -99,8 +102,12 @@ int narrow_offsets(const int64_t* in, int32_t* out, int64_t count, int64_t base,
 // dictionary, *ok when every pattern is a CSR-ordered subset of {−W, −1, 0, +1, +W}
 // for one W with n = W·H and no pattern reaches across the grid's edges; `table`
 // then holds the device pattern table.
+// With host copies of the patterns (pat_host / plen_host) the table is built on the device
+// without a round trip; with edge_bad_dev the edge check only sets that device flag (no
+// wait) and *ok covers the patterns alone — the caller discards the passes if it is set.
 int stencil_plan(int64_t n, const uint8_t* rcode, const double2* pat, const uint8_t* plen, int npat, int width,
-                 DevBuf& table, int* W, int* H, bool* ok, cudaStream_t s);
+                 DevBuf& table, int* W, int* H, bool* ok, cudaStream_t s, const double2* pat_host = nullptr,
+                 const uint8_t* plen_host = nullptr, int* edge_bad_dev = nullptr);
 // a row pattern of the stencil table (device layout): values of the N, W, C, E, S entries
 struct StencilPattern {
   double v[5];
@@ -112,6 +119,8 @@ struct StencilPattern {
 // H-row grid of codes (top / bottom rows checked only where they are the grid's)
 int stencil_patterns(const double2* pat, const uint8_t* plen, int npat, int width, int64_t* W,
                      std::vector<StencilPattern>& tab, cudaStream_t s);
+int stencil_patterns_host(const double2* pat, const uint8_t* plen, int npat, int width, int64_t* W,
+                          std::vector<StencilPattern>& tab);
 int stencil_edges_ok(const uint8_t* rcode, const StencilPattern* table_dev, int W, int H, bool top, bool bottom,
                      bool* ok, cudaStream_t s);
 // Pass depths (most applications per launch): the whole-grid solve's, and the row slabs'

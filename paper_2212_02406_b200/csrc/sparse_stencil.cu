@@ -265,17 +265,12 @@ __global__ void stencil_edge_check(const uint8_t* __restrict__ rcode, const StPa
 
 }  // namespace
 
-int stencil_patterns(const double2* pat, const uint8_t* plen, int npat, int width, int64_t* W_out,
-                     std::vector<StencilPattern>& tab, cudaStream_t s) {
+int stencil_patterns_host(const double2* hp, const uint8_t* hl, int npat, int width, int64_t* W_out,
+                          std::vector<StencilPattern>& tab) {
   static_assert(sizeof(StencilPattern) == sizeof(StPat), "host and device pattern layouts");
   *W_out = 0;
   tab.clear();
   if (npat < 1 || npat > kRowDictMax || width < 1 || width > kEllMaxWidth) return 0;
-  std::vector<double2> hp((size_t)npat * width);
-  std::vector<uint8_t> hl(npat);
-  NNB_CUDA(cudaMemcpyAsync(hp.data(), pat, sizeof(double2) * hp.size(), cudaMemcpyDeviceToHost, s));
-  NNB_CUDA(cudaMemcpyAsync(hl.data(), plen, npat, cudaMemcpyDeviceToHost, s));
-  NNB_CUDA(cudaStreamSynchronize(s));
   int64_t w = 0;
   for (int p = 0; p < npat; ++p)
     for (int i = 0; i < hl[p]; ++i) {
@@ -307,6 +302,19 @@ int stencil_patterns(const double2* pat, const uint8_t* plen, int npat, int widt
   return 0;
 }
 
+int stencil_patterns(const double2* pat, const uint8_t* plen, int npat, int width, int64_t* W_out,
+                     std::vector<StencilPattern>& tab, cudaStream_t s) {
+  *W_out = 0;
+  tab.clear();
+  if (npat < 1 || npat > kRowDictMax || width < 1 || width > kEllMaxWidth) return 0;
+  std::vector<double2> hp((size_t)npat * width);
+  std::vector<uint8_t> hl(npat);
+  NNB_CUDA(cudaMemcpyAsync(hp.data(), pat, sizeof(double2) * hp.size(), cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaMemcpyAsync(hl.data(), plen, npat, cudaMemcpyDeviceToHost, s));
+  NNB_CUDA(cudaStreamSynchronize(s));
+  return stencil_patterns_host(hp.data(), hl.data(), npat, width, W_out, tab);
+}
+
 int stencil_edges_ok(const uint8_t* rcode, const StencilPattern* table_dev, int W, int H, bool top, bool bottom,
                      bool* ok, cudaStream_t s) {
   DevBuf b;
@@ -322,20 +330,50 @@ int stencil_edges_ok(const uint8_t* rcode, const StencilPattern* table_dev, int 
   return 0;
 }
 
+namespace {
+// the device pattern table from the row dictionary's patterns (the host checked them)
+__global__ void stencil_table_kernel(const double2* __restrict__ pat, const uint8_t* __restrict__ plen, int npat,
+                                     int width, long long W, StPat* __restrict__ tab) {
+  for (int p = threadIdx.x; p < npat; p += blockDim.x) {
+    StPat sp{};
+    for (int i = 0; i < plen[p]; ++i) {
+      const long long d = __double_as_longlong(pat[(size_t)p * width + i].y);
+      const int dir = d == -W ? 0 : d == -1 ? 1 : d == 0 ? 2 : d == 1 ? 3 : 4;
+      sp.v[dir] = pat[(size_t)p * width + i].x;
+      sp.mask |= 1 << dir;
+    }
+    tab[p] = sp;
+  }
+}
+}  // namespace
+
 int stencil_plan(int64_t n, const uint8_t* rcode, const double2* pat, const uint8_t* plen, int npat, int width,
-                 DevBuf& table, int* W_out, int* H_out, bool* ok, cudaStream_t s) {
+                 DevBuf& table, int* W_out, int* H_out, bool* ok, cudaStream_t s, const double2* pat_host,
+                 const uint8_t* plen_host, int* edge_bad_dev) {
   *ok = false;
   if (n < 4) return 0;
   int64_t w = 0;
   std::vector<StencilPattern> tab;
-  NNB_TRY(stencil_patterns(pat, plen, npat, width, &w, tab, s));
+  if (pat_host && plen_host) NNB_TRY(stencil_patterns_host(pat_host, plen_host, npat, width, &w, tab));
+  else NNB_TRY(stencil_patterns(pat, plen, npat, width, &w, tab, s));
   if (!w || n % w != 0 || n / w > INT32_MAX) return 0;
   NNB_TRY(table.alloc(sizeof(StPat) * npat, s));
-  NNB_CUDA(cudaMemcpyAsync(table.p, tab.data(), sizeof(StPat) * npat, cudaMemcpyHostToDevice, s));
   const int W = (int)w, H = (int)(n / w);
-  bool eok = false;
-  NNB_TRY(stencil_edges_ok(rcode, table.as<StencilPattern>(), W, H, true, true, &eok, s));
-  if (!eok) return 0;
+  if (pat_host && plen_host) {  // built on the device: no host round trip
+    stencil_table_kernel<<<1, 256, 0, s>>>(pat, plen, npat, width, w, table.as<StPat>());
+    count_launch();
+  } else {
+    NNB_CUDA(cudaMemcpyAsync(table.p, tab.data(), sizeof(StPat) * npat, cudaMemcpyHostToDevice, s));
+  }
+  if (edge_bad_dev) {  // the caller reads the edge verdict with its own results
+    stencil_edge_check<<<148, 256, 0, s>>>(rcode, table.as<StPat>(), W, H, edge_bad_dev, 1, 1);
+    count_launch();
+    NNB_CUDA(cudaGetLastError());
+  } else {
+    bool eok = false;
+    NNB_TRY(stencil_edges_ok(rcode, table.as<StencilPattern>(), W, H, true, true, &eok, s));
+    if (!eok) return 0;
+  }
   *W_out = W;
   *H_out = H;
   *ok = true;

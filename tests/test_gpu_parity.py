@@ -575,6 +575,29 @@ def test_sparse_stencil_rectangular_meshes(ref, width, height, gamma):
     assert cnt == cr and np.array_equal(x, xr.real)
 
 
+def test_sparse_stencil_edges_reach_across_fallback(ref):
+    """A 520 x 520 mesh (above the sampled direct build's 4 x 65536 rows) whose -1 / +1
+    neighbours run on across the mesh rows (a 1-D chain plus the +-W couplings): every
+    pattern is a CSR-ordered 5-point subset, so the stencil plan is taken with the edge
+    check deferred to the end of the passes; it fails there, the passes are discarded
+    and the one-launch-per-application solve from B gives the reference's bits."""
+    width = height = 520
+    n = width * height
+    r = np.arange(n, dtype=np.int64)
+    i = r // width
+    cols = np.stack([r - width, r - 1, r, r + 1, r + width], axis=1)
+    valid = np.stack([i > 0, r > 0, np.ones(n, bool), r < n - 1, i < height - 1], axis=1)
+    vals = np.broadcast_to(np.array([-1.0, -1.0, 5.0, -1.0, -1.0]), (n, 5))
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum(valid.sum(axis=1), out=rp[1:])
+    col, val = cols[valid].astype(np.int32), np.ascontiguousarray(vals[valid])
+    b = W.rhs(n, seed=52)
+    x, cnt = nnb.solve_sparse_factorized(nnb.Csr(rp, col, val, n=n), b, 15, nnb.Normalization(0.2, valid=True))
+    assert nnb.sparse_last_format() == "row-dictionary"
+    xr, cr, _ = ref.sparse_factorized(rp, col, val, b, 15, 0.2)
+    assert cnt == cr and np.array_equal(x, xr.real)
+
+
 def test_sparse_stencil_width_not_multiple_of_4(ref):
     """Row stride 30: the stencil plan declines (W % 4 != 0) and the row-dictionary kernel
     runs instead -- same bits."""
