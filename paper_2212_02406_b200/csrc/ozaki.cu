@@ -17,11 +17,10 @@
 //      A'_l = A' mod m_l and B'_l = B' mod m_l as signed int8 (symmetric).
 //   3. s int8 GEMMs on tcgen05: C_l = A'_l·B'_lᵀ accumulates exactly in int32
 //      (|A'_l|,|B'_l| <= 128, k < 2^17), stored as C_l mod m_l (uint8).
-//   4. Reconstruction.  Garner's mixed-radix digits of C' = A'·B' from the s
-//      residues (exact small-integer arithmetic), the symmetric representative
-//      (k·2^106 < M/8, so the top digit decides the sign), a Horner evaluation
-//      in FP64 (rounds only once |C'| passes 2^53, relative error ~s·2^-53),
-//      the scaling back by 2^-(ea_i+eb_j), and the chain's epilogue.
+//   4. Reconstruction.  The CRT sum C' = Σ_l r_l·W_l − q·M over the s residues in
+//      FP64 with the weights split so the large terms cancel exactly (k·2^106 < M/8,
+//      so the nearest multiple of M is the one to remove), rounded once; the scaling
+//      back by 2^-(ea_i+eb_j), and the chain's epilogue.
 // The integer product A'·B' is exact, so the error is step 1's truncation
 // only: |C − fl(C)| <= 2^-53·k·max_i|a_i·|·max_j|b_·j| per element, the same
 // order as a DGEMM's u·k·|a||b| bound.  Parity against the reference is
@@ -62,81 +61,29 @@ constexpr int kBadExp = INT_MIN / 4;        // exponent marking a row/column wit
 constexpr int64_t kMaxK = 131071;           // 128·128·k < 2^31: exact int32 accumulation
 constexpr int kColRows = 64;                // rows per block of the column-statistics passes
 
-// Garner constants for the first s moduli (host-computed, passed by value).
+// Moduli constants for the first s moduli (host-computed, passed by value).
 struct OzConst {
   int s;
   int mi[kMaxMod];
   unsigned magic[kMaxMod];   // floor(2^32 / m): the epilogue's integer reduction mod m
   unsigned offset[kMaxMod];  // m·ceil(2^31 / m): a + offset >= 0 for every int32 accumulator a
-  float mf[kMaxMod];
-  float inv_mf[kMaxMod];
-  double md[kMaxMod];
-  double inv_md[kMaxMod];
-  float P[kMaxMod];                 // v_j = (r_j·P_j + Σ_{i<j} v_i·Q[i][j]) mod m_j
-  float Q[kMaxMod][kMaxMod];
+  // CRT weights of the residue pairs (moduli p_i = m_2i·m_2i+1; the last alone for odd s):
+  // W_i = (M/p_i)·((M/p_i)^-1 mod p_i) < M split at 2^e (e = bits(M) − 34) into
+  // pwhi = floor(W_i / 2^e)·2^e (exact, < 2^34 units of 2^e) and pwlo = W_i mod 2^e
+  // (rounded); the same split of M, and 1/M for the quotient
+  double pwhi[kMaxMod / 2 + 1];
+  double pwlo[kMaxMod / 2 + 1];
+  double pmhi, pmlo, inv_m;
 };
 
-// The same Garner constants at compile time (template parameters -> FFMA immediates),
-// so the reconstruction's 120 FFMAs do not hold 120 constants in registers.
+// The moduli at compile time (template parameters -> immediates in the split kernels).
 constexpr int kMod(int j) {
   return j == 0 ? 256 : j == 1 ? 255 : j == 2 ? 253 : j == 3 ? 251 : j == 4 ? 247 : j == 5 ? 241 : j == 6 ? 239
        : j == 7 ? 233 : j == 8 ? 229 : j == 9 ? 227 : j == 10 ? 223 : j == 11 ? 217 : j == 12 ? 211
        : j == 13 ? 199 : j == 14 ? 197 : j == 15 ? 193 : j == 16 ? 191 : j == 17 ? 181 : j == 18 ? 179 : 173;
 }
-constexpr int cinv_mod(int a, int m) {
-  a %= m;
-  for (int x = 1; x < m; ++x)
-    if ((a * x) % m == 1) return x;
-  return 0;
-}
-constexpr int garner_p(int j) {  // Π_{k<j} m_k^-1 mod m_j
-  long long prod = 1;
-  for (int k = 0; k < j; ++k) prod = prod * cinv_mod(kMod(k), kMod(j)) % kMod(j);
-  return static_cast<int>(prod);
-}
-constexpr int garner_q(int i, int j) {  // m_j − Π_{k=i}^{j−1} m_k^-1 mod m_j
-  long long q = 1;
-  for (int k = i; k < j; ++k) q = q * cinv_mod(kMod(k), kMod(j)) % kMod(j);
-  return static_cast<int>((kMod(j) - q) % kMod(j));
-}
-template <int I, int L>
-struct GarnerQ {
-  static constexpr float v = static_cast<float>(garner_q(I, L));
-};
-template <int L>
-struct GarnerP {
-  static constexpr float v = static_cast<float>(garner_p(L));
-  static constexpr float m = static_cast<float>(kMod(L));
-  static constexpr float inv = 1.0f / static_cast<float>(kMod(L));
-};
-// x + Σ_{i<L} v_i·Q[i][L]
-template <int L, int I>
-__device__ __forceinline__ float garner_sum(const float* v, float x) {
-  if constexpr (I < L) return garner_sum<L, I + 1>(v, fmaf(v[I], GarnerQ<I, L>::v, x));
-  else return x;
-}
-// mixed-radix digits v_0..v_{S-1} of the residues r (exact small-integer float arithmetic)
-template <int L, int S>
-__device__ __forceinline__ void garner_digits(float* v, const float* r) {
-  if constexpr (L < S) {
-    if constexpr (L == 0) {
-      v[0] = r[0];
-    } else {
-      // balanced digit: any representative of the residue class works in Garner's
-      // recurrence (later digits are formed from the digits actually used), so the
-      // nearest-integer quotient needs no fix-up; |v| <= 1.5·m keeps every partial
-      // sum below 2^21 (exact in FP32) and the final Σ v_l·W_l within ±0.76·M, which
-      // with |C'| < M/8 makes it C' itself — no sign pass either
-      const float x = garner_sum<L, 0>(v, r[L] * GarnerP<L>::v);
-      const float qf = fmaf(x, GarnerP<L>::inv, 12582912.0f) - 12582912.0f;  // rint by the 1.5·2^23 shifter
-      v[L] = fmaf(-qf, GarnerP<L>::m, x);                                    // exact
-    }
-    garner_digits<L + 1, S>(v, r);
-  }
-}
-// The same recurrence for two elements at once in packed FP32 (FFMA2/FADD2/FMUL2 on
-// sm_100a; the Garner constants become broadcast immediates): half the instructions of
-// the FP32 pipe work of the reconstruction, which is issue-bound.
+// Packed FP32 (FFMA2/FADD2/FMUL2 on sm_100a; constants become broadcast immediates):
+// two entries per instruction in the residue splits, which are issue-bound.
 __device__ __forceinline__ unsigned long long pk2(float a, float b) {
   unsigned long long r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
@@ -161,25 +108,6 @@ __device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigne
   return d;
 }
 __device__ __forceinline__ unsigned long long bc2(float c) { return pk2(c, c); }
-template <int L, int I>
-__device__ __forceinline__ unsigned long long garner_sum2(const unsigned long long* v, unsigned long long x) {
-  if constexpr (I < L) return garner_sum2<L, I + 1>(v, fma2(v[I], bc2(GarnerQ<I, L>::v), x));
-  else return x;
-}
-template <int L, int S>
-__device__ __forceinline__ void garner_digits2(unsigned long long* v, const unsigned long long* r) {
-  if constexpr (L < S) {
-    if constexpr (L == 0) {
-      v[0] = r[0];
-    } else {
-      const unsigned long long x = garner_sum2<L, 0>(v, mul2(r[L], bc2(GarnerP<L>::v)));
-      const unsigned long long qf = add2(fma2(x, bc2(GarnerP<L>::inv), bc2(12582912.0f)), bc2(-12582912.0f));
-      v[L] = fma2(qf, bc2(-GarnerP<L>::m), x);
-    }
-    garner_digits2<L + 1, S>(v, r);
-  }
-}
-
 int inv_mod(int a, int m) {
   a %= m;
   for (int x = 1; x < m; ++x)
@@ -187,29 +115,88 @@ int inv_mod(int a, int m) {
   return 0;
 }
 
+// Little-endian base-2^32 integers, just wide enough for M = Π m_l (< 2^173) and the
+// CRT weights (host only).
+struct BigU {
+  uint32_t w[6] = {0, 0, 0, 0, 0, 0};
+};
+BigU big_mul(const BigU& a, uint32_t m) {
+  BigU r;
+  uint64_t c = 0;
+  for (int i = 0; i < 6; ++i) {
+    const uint64_t t = static_cast<uint64_t>(a.w[i]) * m + c;
+    r.w[i] = static_cast<uint32_t>(t);
+    c = t >> 32;
+  }
+  return r;
+}
+BigU big_div(const BigU& a, uint32_t m) {  // exact quotient (m divides a)
+  BigU r;
+  uint64_t rem = 0;
+  for (int i = 5; i >= 0; --i) {
+    const uint64_t t = (rem << 32) | a.w[i];
+    r.w[i] = static_cast<uint32_t>(t / m);
+    rem = t % m;
+  }
+  return r;
+}
+int big_bits(const BigU& a) {
+  for (int i = 5; i >= 0; --i)
+    if (a.w[i]) return 32 * i + 32 - __builtin_clz(a.w[i]);
+  return 0;
+}
+bool big_bit(const BigU& a, int i) { return i >= 0 && i < 192 && ((a.w[i >> 5] >> (i & 31)) & 1u); }
+// Σ_{lo <= i < hi} bit_i·2^i as a double (exact when hi − lo <= 53, else rounded once per
+// 53-bit window from the top)
+double big_range(const BigU& a, int lo, int hi) {
+  double v = 0.0;
+  for (int top = hi; top > lo; top -= 53) {
+    const int b0 = std::max(lo, top - 53);
+    uint64_t u = 0;
+    for (int i = top - 1; i >= b0; --i) u = (u << 1) | (big_bit(a, i) ? 1u : 0u);
+    v += std::ldexp(static_cast<double>(u), b0);
+  }
+  return v;
+}
+
 OzConst make_const(int s) {
   OzConst c{};
   c.s = s;
+  BigU M;
+  M.w[0] = 1;
   for (int j = 0; j < s; ++j) {
     const int m = kModuli[j];
     c.mi[j] = m;
     c.magic[j] = static_cast<unsigned>((1ull << 32) / static_cast<unsigned long long>(m));
     c.offset[j] = static_cast<unsigned>(static_cast<unsigned long long>(m) * (((1ull << 31) + m - 1) / m));
-    c.mf[j] = static_cast<float>(m);
-    c.inv_mf[j] = 1.0f / static_cast<float>(m);
-    c.md[j] = m;
-    c.inv_md[j] = 1.0 / m;
-    // Garner: t = r_j; for i < j: t = (t − v_i)·inv(m_i) mod m_j
-    //   => v_j = r_j·Π_{k<j} inv_k − Σ_{i<j} v_i·Π_{k=i}^{j−1} inv_k   (mod m_j)
-    long long prod = 1;
-    for (int k = 0; k < j; ++k) prod = prod * inv_mod(kModuli[k], m) % m;
-    c.P[j] = static_cast<float>(prod);
-    for (int i = 0; i < j; ++i) {
-      long long q = 1;
-      for (int k = i; k < j; ++k) q = q * inv_mod(kModuli[k], m) % m;
-      c.Q[i][j] = static_cast<float>((m - q) % m);  // + v_i·(m − q) ≡ − v_i·q
-    }
+    M = big_mul(M, static_cast<uint32_t>(m));
   }
+  // e: Σ_i u_i·pwhi_i (|u_i| < 2^15.1, <= 10 terms, pwhi < 2^34 units) and q·pmhi (q < 2^18.5)
+  // stay below 2^53 units of 2^e, so both are exact in FP64
+  const int B = big_bits(M);
+  c.inv_m = 1.0 / big_range(M, 0, B);
+  const int e2 = B - 34;  // e
+  for (int i = 0; 2 * i < s; ++i) {
+    const int64_t mod = 2 * i + 1 < s ? static_cast<int64_t>(kModuli[2 * i]) * kModuli[2 * i + 1] : kModuli[2 * i];
+    const BigU Mj = big_div(M, static_cast<uint32_t>(mod));
+    int64_t mj_mod = 0;
+    for (int k = 5; k >= 0; --k) mj_mod = static_cast<int64_t>(((static_cast<uint64_t>(mj_mod) << 32) | Mj.w[k]) % mod);
+    int64_t inv = 0;  // (M/mod)^-1 mod mod by extended Euclid
+    {
+      int64_t r0 = mod, r1 = mj_mod, t0 = 0, t1 = 1;
+      while (r1) {
+        const int64_t qq = r0 / r1;
+        std::tie(r0, r1) = std::make_tuple(r1, r0 - qq * r1);
+        std::tie(t0, t1) = std::make_tuple(t1, t0 - qq * t1);
+      }
+      inv = (t0 % mod + mod) % mod;
+    }
+    const BigU W = big_mul(Mj, static_cast<uint32_t>(inv));  // < M
+    c.pwhi[i] = big_range(W, e2, B);
+    c.pwlo[i] = big_range(W, 0, e2);
+  }
+  c.pmhi = big_range(M, e2, B);
+  c.pmlo = big_range(M, 0, e2);
   return c;
 }
 
@@ -554,59 +541,6 @@ __device__ __forceinline__ int exp_for(double amax) {
 __device__ __forceinline__ bool pow2_normal(int e) { return e >= -1022 && e <= 1023; }
 __device__ __forceinline__ double pow2(int e) { return __longlong_as_double(static_cast<long long>(1023 + e) << 52); }
 __device__ __forceinline__ double scale2(double x, int e) { return pow2_normal(e) ? x * pow2(e) : scalbn(x, e); }
-
-// signed residue of the integer-valued double a (|a| <= 2^53) modulo m, in [-128, 127]
-// Exact integer value of a group of digits lo..hi (Horner; the group's weight
-// Π m_lo..m_hi stays below 2^53, so every step is exact).
-template <int L, int LO>
-__device__ __forceinline__ double group(const float* v, double x) {
-  if constexpr (L < LO) return x;
-  else return group<L - 1, LO>(v, fma(x, static_cast<double>(kMod(L)), static_cast<double>(v[L])));
-}
-// The same group value from digit pairs: v_{I−1} + m_{I−1}·v_I is an exact FP32 integer
-// (|v| <= 1.5·m, so |pair| < 2^17), so each pair costs one FFMA, one float→double
-// conversion and one DFMA instead of two of each.
-template <int I, int LO>
-__device__ __forceinline__ double group_pairs(const float* v, double x) {
-  if constexpr (I < LO) {
-    return x;
-  } else if constexpr (I - 1 >= LO) {
-    const float pr = fmaf(v[I], static_cast<float>(kMod(I - 1)), v[I - 1]);
-    return group_pairs<I - 2, LO>(v, fma(x, static_cast<double>(kMod(I - 1)) * kMod(I), static_cast<double>(pr)));
-  } else {
-    return group_pairs<I - 1, LO>(v, fma(x, static_cast<double>(kMod(I)), static_cast<double>(v[I])));
-  }
-}
-constexpr double weight(int lo, int hi) {  // Π_{lo<=l<=hi} m_l
-  double w = 1.0;
-  for (int l = lo; l <= hi; ++l) w *= kMod(l);
-  return w;
-}
-// C' = ((G2·W'+ G1)·W + G0) from three exact digit groups (digits 0-5, 6-11, 12..S-1,
-// the top one signed); W = Π m_0..5 and W' = Π m_6..11 are exact doubles (< 2^48).
-// The two multiply-adds are error-free (TwoProduct by FMA, TwoSum), so C' is rounded
-// once at the end: relative error ~2^-53, 24 FP64 operations instead of a 15-step
-// compensated Horner.
-template <int S>
-__device__ __forceinline__ double value_of(const float* v, float top) {
-  static_assert(S >= 13 && S <= 18, "three groups of at most 6 digits");
-  constexpr double W = weight(0, 5), W2 = weight(6, 11);
-  (void)top;  // the top digit (already signed) is v[S − 1]
-  const double g0 = group_pairs<5, 0>(v, 0.0);
-  const double g1 = group_pairs<11, 6>(v, 0.0);
-  const double g2 = group_pairs<S - 1, 12>(v, 0.0);
-  // inner = g2·W2 + g1 as a double-double (hi, lo)
-  const double p = g2 * W2;
-  const double pe = fma(g2, W2, -p);
-  const double s1 = p + g1;
-  const double bb = s1 - p;
-  const double se = (p - (s1 - bb)) + (g1 - bb);
-  const double lo = pe + se;
-  // C' = (s1 + lo)·W + g0
-  const double q = s1 * W;
-  const double qe = fma(s1, W, -q);
-  return q + (fma(lo, W, qe) + g0);
-}
 
 // Round-to-nearest by the 1.5·2^52 shifter (exact for |x| < 2^51): one DFMA and one DADD
 // instead of FRND.F64; and the low word of (r + 1.5·2^52) is r in two's complement, so
@@ -987,11 +921,69 @@ int split_cols_launch(int s, const double* B, int64_t ld, int k, int n, int64_t 
 }
 
 // ---------------------------------------------------------------- reconstruction
+// C' from its residues by the CRT sum.  Residue pairs first: u ≡ r_a (mod a), u ≡ r_b
+// (mod b) as u = r_a + a·v, v = (r_b − r_a)·a^-1 mod b (balanced: |u| <= 255 + 256·129 < 2^15.1), in packed
+// FP32 for the thread's two elements at once (the bytes enter as 1.5·2^23 + r, bits
+// 0x4B4000rr, and u leaves the same way, one DADD from a double).  Then, over the P =
+// ceil(s/2) pair moduli, C' ≡ Σ_i u_i·W_i (mod M) with W_i = (M/p_i)·((M/p_i)^-1 mod p_i)
+// < M, and |C'| < M/8 (the moduli count) makes C' = Σ u_i·W_i − q·M for q = rint(Σ/M).
+// Each weight is split at 2^e (e = bits(M) − 34): the high parts' sum and q·mhi stay
+// below 2^53 units of 2^e, so both and their difference are exact; the low parts' sum
+// (< 2^(e+19)) carries ~10 roundings of 2^(e−34), i.e. below M·2^-66 — under the scheme's
+// truncation error (>= M·2^-56) by far; the result is rounded once (the final add).
+// 3 FP64 ops per pair against Garner's O(s^2) small-integer recurrence (round 2's first
+// form): the reconstruction was issue-bound on that.
+constexpr int cinv(int a, int m) {
+  for (int x = 1; x < m; ++x)
+    if ((a % m) * x % m == 1) return x;
+  return 0;
+}
+template <int S, int I>
+__device__ __forceinline__ void crt_pairs(const uint32_t (&w)[S], int b, const OzConst& c, double& sh0, double& sl0,
+                                          double& sh1, double& sl1) {
+  if constexpr (2 * I < S) {
+    constexpr float kOff = 12582912.0f;  // 1.5·2^23
+    const unsigned long long fa = pk2(__uint_as_float(__byte_perm(w[2 * I], 0x4B40u, 0x5460u + b)),
+                                      __uint_as_float(__byte_perm(w[2 * I], 0x4B40u, 0x5460u + b + 1)));
+    unsigned long long u = fa;
+    if constexpr (2 * I + 1 < S) {
+      constexpr int ma = kMod(2 * I), mb = kMod(2 * I + 1);
+      const unsigned long long fb = pk2(__uint_as_float(__byte_perm(w[2 * I + 1], 0x4B40u, 0x5460u + b)),
+                                        __uint_as_float(__byte_perm(w[2 * I + 1], 0x4B40u, 0x5460u + b + 1)));
+      const unsigned long long t = mul2(add2(fb, mul2(fa, bc2(-1.0f))), bc2(static_cast<float>(cinv(ma, mb))));
+      const unsigned long long q = add2(fma2(t, bc2(1.0f / mb), bc2(kOff)), bc2(-kOff));
+      const unsigned long long v = fma2(q, bc2(-static_cast<float>(mb)), t);
+      u = fma2(v, bc2(static_cast<float>(ma)), fa);
+    }
+    float u0, u1;
+    upk2(u, u0, u1);
+    constexpr double kBias = 4503599627370496.0 + 1262485504.0;  // 2^52 + 0x4B400000
+    const double d0 = __hiloint2double(0x43300000, static_cast<int>(__float_as_uint(u0))) - kBias;
+    const double d1 = __hiloint2double(0x43300000, static_cast<int>(__float_as_uint(u1))) - kBias;
+    sh0 = fma(d0, c.pwhi[I], sh0);
+    sl0 = fma(d0, c.pwlo[I], sl0);
+    sh1 = fma(d1, c.pwhi[I], sh1);
+    sl1 = fma(d1, c.pwlo[I], sl1);
+    crt_pairs<S, I + 1>(w, b, c, sh0, sl0, sh1, sl1);
+  }
+}
+// C' of the elements in bytes b and b+1 of the residue words w
+template <int S>
+__device__ __forceinline__ void crt_value_pair(const uint32_t (&w)[S], int b, const OzConst& c, double& x0,
+                                               double& x1) {
+  double sh0 = 0.0, sl0 = 0.0, sh1 = 0.0, sl1 = 0.0;
+  crt_pairs<S, 0>(w, b, c, sh0, sl0, sh1, sl1);
+  const double q0 = fma(sh0 + sl0, c.inv_m, kShift52) - kShift52;  // |Σ/M| < 2^19: rint by the shifter
+  const double q1 = fma(sh1 + sl1, c.inv_m, kShift52) - kShift52;
+  x0 = fma(-q0, c.pmhi, sh0) + fma(-q0, c.pmlo, sl0);
+  x1 = fma(-q1, c.pmhi, sh1) + fma(-q1, c.pmlo, sl1);
+}
+
 // One block: 16 rows × 16·CPT columns; thread t: row t/16, CPT consecutive columns.
 template <int S, int CPT>
 __device__ __forceinline__ void recon_body(const uint8_t* __restrict__ res, int64_t ldr, int M, int N,
                                            const int* __restrict__ ea, const int* __restrict__ eb,
-                                           const GemmEpilogue& ep) {
+                                           const GemmEpilogue& ep, const OzConst& cst) {
   static_assert(CPT == 8 || CPT == 4, "8 or 4 columns per thread");
   using RV = typename std::conditional<CPT == 8, uint2, uint32_t>::type;
   __shared__ double red[8];
@@ -1011,36 +1003,32 @@ __device__ __forceinline__ void recon_body(const uint8_t* __restrict__ res, int6
 #pragma unroll
     for (int l = 0; l < S; ++l) rv[l] = *reinterpret_cast<const RV*>(res + ((int64_t)l * M + row) * ldr + c0);
     const int era = ea[row];
-#pragma unroll 1
+    // β·D of the thread's columns, loaded with the residues (more loads in flight)
+    double dv[CPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      const int cc = c0 + j;
+      dv[j] = (ep.D && cc < N && !(sym && row > cc)) ? ep.D[(int64_t)row * ep.ldd + cc] : 0.0;
+    }
+#pragma unroll
     for (int jp = 0; jp < CPT / 2; ++jp) {
       const int c = c0 + 2 * jp;
       if (c >= N) break;
       const bool two = c + 1 < N;
       double out2[2];
-      // Garner digits of both elements of the pair in packed FP32
-      unsigned long long r2[S], v2[S];
-#pragma unroll
-      for (int l = 0; l < S; ++l) {
-        uint32_t word;
-        if constexpr (CPT == 8) word = (jp < 2) ? rv[l].x : rv[l].y;
-        else word = rv[l];
-        const int sel = (2 * jp) & 3;
-        // byte b -> float exactly: the bits 0x4B0000bb are 2^23 + b
-        r2[l] = add2(pk2(__uint_as_float(__byte_perm(word, 0x4B00u, 0x5440u + sel)),
-                         __uint_as_float(__byte_perm(word, 0x4B00u, 0x5440u + sel + 1))),
-                     bc2(-8388608.0f));
-      }
-      garner_digits2<0, S>(v2, r2);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float v[S];
+      double xp[2];
+      {
+        uint32_t w[S];
 #pragma unroll
         for (int l = 0; l < S; ++l) {
-          float a, b;
-          upk2(v2[l], a, b);
-          v[l] = h ? b : a;
+          if constexpr (CPT == 8) w[l] = (jp < 2) ? rv[l].x : rv[l].y;
+          else w[l] = rv[l];
         }
-        const double x = value_of<S>(v, v[S - 1]);
+        crt_value_pair<S>(w, (2 * jp) & 3, cst, xp[0], xp[1]);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double x = xp[h];
         // scale back by 2^-(ea+eb), then the chain's epilogue
         const int cc = c + h;
         const int e = (cc < N) ? eb[cc] : 0;
@@ -1048,7 +1036,7 @@ __device__ __forceinline__ void recon_body(const uint8_t* __restrict__ res, int6
         if (era == kBadExp || e == kBadExp) cv = __longlong_as_double(0x7ff8000000000000LL);
         else cv = scale2(x, -(era + e));
         double o = ep.alpha * cv;
-        if (ep.D && cc < N && !(sym && row > cc)) o = fma(ep.beta, ep.D[(int64_t)row * ep.ldd + cc], o);
+        if (ep.D && cc < N && !(sym && row > cc)) o = fma(ep.beta, dv[2 * jp + h], o);
         if ((int64_t)row + ep.diag_offset == cc) o += ep.gamma;
         out2[h] = o;
       }
@@ -1140,13 +1128,14 @@ __device__ __forceinline__ void recon_body(const uint8_t* __restrict__ res, int6
   }
 }
 
-// 8 columns per thread: 80 registers, 3 blocks per SM.  (4 columns per thread capped at 64
-// registers for 4 blocks per SM measured 10-15 % slower at N=8192.)
+// 8 columns per thread, 3 blocks per SM (85 registers; the CRT weights are kernel-parameter
+// constants).  A/B at N=32768 under the power cap (tools/recon_ab.sh): 2 blocks per SM with
+// D read in the column loop 16.0 ms, 3 blocks 15.7, D hoisted 14.0, both 13.1.
 template <int S>
-__global__ void __launch_bounds__(256) oz_recon_kernel(const uint8_t* __restrict__ res, int64_t ldr, int M, int N,
+__global__ void __launch_bounds__(256, 3) oz_recon_kernel(const uint8_t* __restrict__ res, int64_t ldr, int M, int N,
                                                        const int* __restrict__ ea, const int* __restrict__ eb,
                                                        GemmEpilogue ep, const OzConst cst) {
-  recon_body<S, 8>(res, ldr, M, N, ea, eb, ep);
+  recon_body<S, 8>(res, ldr, M, N, ea, eb, ep, cst);
 }
 
 // Live per-kernel timing for bench.py's roofline (nnb_ozaki_profile / nnb_ozaki_stats):
