@@ -929,7 +929,7 @@ def main():
             "dtype": "f64", "data": "synthetic (seeded)", "config": config,
             "arithmetic": "NNB_ARITH_FAST: each real N^3 product (N >= 3072) runs as an FP64-accurate emulation on "
                           "the int8 tensor cores (Ozaki scheme II: 53-bit row/column-scaled integers, 16 moduli, "
-                          "exact int32 accumulation, Garner reconstruction; csrc/ozaki.cu) - same parity gate as "
+                          "exact int32 accumulation, CRT-sum reconstruction; csrc/ozaki.cu) - same parity gate as "
                           "DMMA (X within 1e-10, identical nest counts); smaller/complex products on DMMA"}
     if world > 1:
         base["scaling"] = "strong"  # the N=32768 matrix is fixed; ranks split its rows

@@ -260,7 +260,7 @@ int ksplit_product(Shard& sh, int g, const double* L, int64_t ldl, const double*
 //      order, each waiting only for its block) accumulating mod m_l, then one
 //      reconstruction with the chain's epilogue.
 // Every element equals the single-GPU emulated product's (same exponents, same residues, an
-// exact modular sum, the same Garner reconstruction), so the sharded X matches the
+// exact modular sum, the same CRT reconstruction), so the sharded X matches the
 // single-GPU X; FP64 traffic per nest drops to the G small records.
 __global__ void max_slots_kernel(const unsigned* __restrict__ slots, int world, unsigned* __restrict__ out) {
   if (threadIdx.x < 4) {
